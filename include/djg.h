@@ -1,0 +1,152 @@
+/*
+ * djg.h — C-ABI of the B200 DJ-TLED explicit-dynamics engine (libdjg.so).
+ *
+ * What it replaces. The reference is a header-only C++ library with no FFI;
+ * its de-facto operator interface for the hot path is the duck-typed Engine
+ * concept consumed by advance_step / run_simulation:
+ *
+ *   AssembleStats Engine::assemble(const std::vector<Real>& u,
+ *                                  std::vector<Real>& f, int threads,
+ *                                  InversionPolicy policy)
+ *        /root/reference/proj/include/djtled/solver.hpp:269-272 (DjEngine)
+ *   StepOutcome advance_step(SimState&, Engine&, const UpdateCoeffs&,
+ *                            const DofConstraints&, Real dt, int threads,
+ *                            InversionPolicy, std::vector<Real>& u_next)
+ *        solver.hpp:98-153
+ *   RunResult run_simulation(Engine&, node_mass, DofConstraints, RunParams,
+ *                            hook, const SimState* initial)
+ *        solver.hpp:205-258
+ *
+ * Plugging the GPU in at `assemble` would move 2x3N Reals over PCIe per
+ * step, so this ABI sits one level up: the whole step and the run loop, with
+ * the state resident in HBM. Each entry point names the reference call it
+ * replaces. Ownership: the caller owns every host array; djg_create deep
+ * copies them. A handle is not thread-safe (like DjEngine, whose elem_f_ is
+ * mutable, solver.hpp:283); calls are synchronous unless suffixed _async.
+ * No exception crosses the ABI: functions return djg_status codes and
+ * djg_last_error() holds the message.
+ */
+#ifndef DJG_H
+#define DJG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "djg_types.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/*
+ * Canonical per-element hot-field record (Reals, this order), the subset of
+ * ElementConstants<Real> (precompute.hpp:170-201) the step reads:
+ *   [0..8]   J0, row-major, J[i][j] = dx_j/dxi_i       (element.hpp:380)
+ *   [9]      det_J0          [10] V0
+ *   [11..16] m1[6]           [17..22] I1m (xx,yy,zz,xy,xz,yz)
+ *   TI, OT:  m4[6], I4m[6]
+ *   OT:      m6[6], I6m[6]
+ *   MR:      M2 (21, packed upper Sym6, core.hpp:282-305), I2m[6] (6 x 6)
+ *   H8:      k_hg, hg_gamma[4][8]
+ */
+#define DJG_CONST_BASE 23
+int32_t djg_const_count(int32_t kind, int32_t model);
+
+typedef struct djg_engine djg_engine;
+
+/* Engine construction inputs: everything DjEngine + UpdateCoeffs +
+ * DofConstraints hold after precompute (solver.hpp:18-33,64-87,264-267). */
+typedef struct djg_desc {
+    int32_t precision;          /* sizeof(Real): 4 or 8 */
+    int32_t kind;               /* djg_element_kind */
+    int64_t num_nodes;
+    int64_t num_elements;
+    const int32_t* conn;        /* npe*E, Mesh::conn (mesh.hpp:24) */
+    const void* consts;         /* E*nconst Reals, canonical record above */
+    int32_t nconst;             /* must equal djg_const_count(kind, material.model) */
+    int32_t inversion_policy;   /* djg_inversion_policy */
+    const int64_t* csr_offsets; /* N+1, NodeElementAdjacency (mesh.hpp:299-320); */
+    const int64_t* csr_elem;    /*   NULL -> rebuilt from conn by the same   */
+    const int32_t* csr_local;   /*   ascending-element counting sort          */
+    const uint8_t* dof_kind;    /* 3N  DofConstraints::kind */
+    const void* dof_target;     /* 3N Real */
+    const void* dof_t_total;    /* 3N Real */
+    const void* c1;             /* N Real  UpdateCoeffs::c1 */
+    const uint8_t* massless;    /* N       UpdateCoeffs::massless */
+    double c2, c3;              /* UpdateCoeffs::c2/c3 (Real values) */
+    double dt;                  /* Real value */
+    djg_material_params material;
+    int32_t device;             /* CUDA ordinal */
+    uint32_t flags;             /* DJG_FLAG_* */
+} djg_desc;
+
+/* Flags */
+#define DJG_FLAG_NO_GRAPH 1u    /* launch kernels one by one instead of CUDA graphs */
+
+/* DjEngine ctor + UpdateCoeffs::build + DofConstraints::build
+ * (solver.hpp:264-267, 70-86, 18-33). Validates shapes, uploads, builds the
+ * CSR-ordered force-slot layout on the device. */
+int djg_create(const djg_desc* desc, djg_engine** out);
+void djg_destroy(djg_engine* eng);
+
+/* SimState assignment (solver.hpp:41-57; run_simulation's `initial`,
+ * solver.hpp:209,214). u_curr/u_prev: 3N Reals (NULL -> zeros). Clears any
+ * halted inversion/divergence condition. */
+int djg_set_state(djg_engine* eng, const void* u_curr, const void* u_prev, int64_t step);
+/* SimState::r_ext (solver.hpp:44). NULL -> identically zero (the default). */
+int djg_set_external(djg_engine* eng, const void* r_ext);
+/* SimState readback: u_curr/u_prev 3N Reals each (either may be NULL). */
+int djg_get_state(djg_engine* eng, void* u_curr, void* u_prev, int64_t* step);
+
+/* nsteps x advance_step (solver.hpp:98-153) with the loop semantics of
+ * run_simulation (solver.hpp:225-239): stops at the first failing step and
+ * leaves the state at the last good step. Returns DJG_OK,
+ * DJG_E_INVERSION (report->first_inverted = min inverted element id) or
+ * DJG_E_DIVERGENCE (report->fail_step = state.step + 1). */
+int djg_step(djg_engine* eng, int64_t nsteps, djg_report* report);
+
+/* Asynchronous variant for timing: enqueue nsteps on the engine stream and
+ * return. djg_sync waits and fills the report. */
+int djg_step_async(djg_engine* eng, int64_t nsteps);
+int djg_sync(djg_engine* eng, djg_report* report);
+/* The engine's cudaStream_t (for CUDA events / external streams). */
+void* djg_stream(djg_engine* eng);
+
+/* Engine::assemble (solver.hpp:269-272 -> assemble_internal,
+ * djtled_force.hpp:163-209): internal forces f (3N Reals) at displacement u
+ * (3N Reals; NULL -> the current state). Under Abort with an inverted element
+ * f is not written, as in the reference. */
+int djg_assemble(djg_engine* eng, const void* u, void* f_int, djg_assemble_stats* stats);
+
+/* Per-kernel timing of nsteps steps: device milliseconds spent in the
+ * element-force kernel and in the gather+update kernel (CUDA events on the
+ * engine stream). Advances the state like djg_step. */
+int djg_profile_steps(djg_engine* eng, int64_t nsteps, float* ms_element, float* ms_node,
+                      float* ms_total);
+
+/* Layout facts for roofline accounting and tests. */
+typedef struct djg_engine_info {
+    int64_t num_nodes, num_elements;
+    int64_t num_slots;          /* npe*E */
+    int64_t slot_capacity;      /* force-slot buffer entries (sliced layout incl. padding) */
+    int64_t device_bytes;       /* device memory held by the engine */
+    int32_t npe, nconst, const_planes, precision;
+    int32_t kernels_per_step;
+    int32_t sm_count;
+} djg_engine_info;
+int djg_get_info(djg_engine* eng, djg_engine_info* info);
+
+/* Debug/test: copy the engine's force-slot position table (npe*E int32, the
+ * position of (element, local) in the sliced slot buffer) to the host. */
+int djg_get_slot_map(djg_engine* eng, int32_t* slot_pos);
+
+const char* djg_last_error(djg_engine* eng);
+const char* djg_status_string(int32_t status);
+/* Last error of a failed djg_create (no handle). */
+const char* djg_create_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DJG_H */

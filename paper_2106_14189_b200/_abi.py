@@ -1,0 +1,192 @@
+"""ctypes mirror of include/djg_types.h, include/djg.h and include/djg_host.h.
+
+The structs here are byte-for-byte the C structs; tests/test_abi.py checks
+the field offsets against the compiled library. `load_library()` loads the
+in-tree libdjg.so and raises if it is missing -- there is no fallback path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+import numpy as np
+
+PKG_DIR = Path(__file__).resolve().parent
+LIB_PATH = PKG_DIR / "_build" / "libdjg.so"
+
+DJG_T4, DJG_H8 = 0, 1
+DJG_NH, DJG_TI, DJG_OT, DJG_MR = 0, 1, 2, 3
+DJG_ABORT, DJG_SKIP_AND_REPORT = 0, 1
+DJG_FREE, DJG_FIXED, DJG_PRESCRIBED = 0, 1, 2
+DJG_OK, DJG_E_INTERNAL, DJG_E_CONFIG, DJG_E_CUDA, DJG_E_INVERSION, DJG_E_DIVERGENCE = 0, 1, 2, 3, 4, 5
+DJG_FLAG_NO_GRAPH = 1
+
+KIND_NAMES = {"T4": DJG_T4, "H8": DJG_H8}
+MODEL_NAMES = {"NH": DJG_NH, "TI": DJG_TI, "OT": DJG_OT, "MR": DJG_MR}
+
+
+def npe_of(kind: int) -> int:
+    return 4 if kind == DJG_T4 else 8
+
+
+def const_count(kind: int, model: int) -> int:
+    """Reals in the canonical hot-field record (include/djg.h)."""
+    n = 23
+    if model in (DJG_TI, DJG_OT):
+        n += 12
+    if model == DJG_OT:
+        n += 12
+    if model == DJG_MR:
+        n += 57
+    if kind == DJG_H8:
+        n += 33
+    return n
+
+
+class djg_material_params(C.Structure):
+    _fields_ = [
+        ("model", C.c_int32), ("_pad", C.c_int32),
+        ("mu", C.c_double), ("kappa", C.c_double), ("rho", C.c_double),
+        ("eta_a", C.c_double), ("eta_b", C.c_double), ("c10", C.c_double), ("c01", C.c_double),
+        ("fibre_a", C.c_double * 3), ("fibre_b", C.c_double * 3),
+    ]
+
+
+class djg_scenario_spec(C.Structure):
+    _fields_ = [
+        ("precision", C.c_int32), ("kind", C.c_int32),
+        ("divisions", C.c_int32 * 3), ("_pad0", C.c_int32),
+        ("extent", C.c_double * 3),
+        ("num_nodes", C.c_int64), ("num_elements", C.c_int64),
+        ("nodes", C.POINTER(C.c_double)), ("conn", C.POINTER(C.c_int32)),
+        ("material", djg_material_params),
+        ("c_hg", C.c_double),
+        ("bc_mode", C.c_int32), ("fix_all_axes", C.c_int32),
+        ("target", C.c_double), ("ramp_steps", C.c_int64),
+        ("n_fixed", C.c_int64), ("fixed_node", C.POINTER(C.c_int32)), ("fixed_axis", C.POINTER(C.c_int32)),
+        ("n_prescribed", C.c_int64), ("presc_node", C.POINTER(C.c_int32)), ("presc_axis", C.POINTER(C.c_int32)),
+        ("presc_target", C.POINTER(C.c_double)), ("presc_t_total", C.POINTER(C.c_double)),
+        ("dt", C.c_double), ("safety", C.c_double),
+        ("alpha_mode", C.c_int32), ("policy", C.c_int32), ("alpha", C.c_double),
+    ]
+
+
+class djg_image_ptrs(C.Structure):
+    _fields_ = [
+        ("nodes", C.c_void_p), ("conn", C.c_void_p), ("csr_offsets", C.c_void_p), ("csr_elem", C.c_void_p),
+        ("csr_local", C.c_void_p), ("consts", C.c_void_p), ("mass", C.c_void_p), ("c1", C.c_void_p),
+        ("massless", C.c_void_p), ("dof_kind", C.c_void_p), ("dof_target", C.c_void_p), ("dof_t_total", C.c_void_p),
+    ]
+
+
+class djg_image_scalars(C.Structure):
+    _fields_ = [
+        ("num_nodes", C.c_int64), ("num_elements", C.c_int64), ("npe", C.c_int32), ("nconst", C.c_int32),
+        ("dt", C.c_double), ("critical_dt", C.c_double), ("alpha", C.c_double), ("c2", C.c_double),
+        ("c3", C.c_double), ("ramp_t_total", C.c_double), ("wave_speed", C.c_double),
+    ]
+
+
+class djg_report(C.Structure):
+    _fields_ = [
+        ("steps_done", C.c_int64), ("step", C.c_int64), ("first_inverted", C.c_int64),
+        ("inverted_count", C.c_int64), ("inverted_steps", C.c_int64), ("fail_step", C.c_int64),
+        ("diverged", C.c_int32), ("status", C.c_int32),
+    ]
+
+    def as_dict(self) -> dict:
+        return {name: getattr(self, name) for name, _ in self._fields_}
+
+
+class djg_assemble_stats(C.Structure):
+    _fields_ = [("first_inverted", C.c_int64), ("inverted_count", C.c_int64)]
+
+
+class djg_desc(C.Structure):
+    _fields_ = [
+        ("precision", C.c_int32), ("kind", C.c_int32), ("num_nodes", C.c_int64), ("num_elements", C.c_int64),
+        ("conn", C.c_void_p), ("consts", C.c_void_p), ("nconst", C.c_int32), ("inversion_policy", C.c_int32),
+        ("csr_offsets", C.c_void_p), ("csr_elem", C.c_void_p), ("csr_local", C.c_void_p),
+        ("dof_kind", C.c_void_p), ("dof_target", C.c_void_p), ("dof_t_total", C.c_void_p),
+        ("c1", C.c_void_p), ("massless", C.c_void_p),
+        ("c2", C.c_double), ("c3", C.c_double), ("dt", C.c_double),
+        ("material", djg_material_params), ("device", C.c_int32), ("flags", C.c_uint32),
+    ]
+
+
+class djg_engine_info(C.Structure):
+    _fields_ = [
+        ("num_nodes", C.c_int64), ("num_elements", C.c_int64), ("num_slots", C.c_int64),
+        ("slot_capacity", C.c_int64), ("device_bytes", C.c_int64),
+        ("npe", C.c_int32), ("nconst", C.c_int32), ("const_planes", C.c_int32), ("precision", C.c_int32),
+        ("kernels_per_step", C.c_int32), ("sm_count", C.c_int32),
+    ]
+
+
+def ptr(a: np.ndarray | None):
+    """void* of a C-contiguous numpy array (None -> NULL)."""
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"], "array must be C-contiguous"
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def typed_ptr(a: np.ndarray | None, ctype):
+    if a is None:
+        return None
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+_P = C.POINTER
+# (name, restype, argtypes) of every function include/djg.h and include/djg_host.h declare.
+EXPORTS = [
+    ("djg_const_count", C.c_int32, [C.c_int32, C.c_int32]),
+    ("djg_create", C.c_int, [_P(djg_desc), _P(C.c_void_p)]),
+    ("djg_destroy", None, [C.c_void_p]),
+    ("djg_set_state", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
+    ("djg_set_external", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("djg_get_state", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, _P(C.c_int64)]),
+    ("djg_step", C.c_int, [C.c_void_p, C.c_int64, _P(djg_report)]),
+    ("djg_step_async", C.c_int, [C.c_void_p, C.c_int64]),
+    ("djg_sync", C.c_int, [C.c_void_p, _P(djg_report)]),
+    ("djg_stream", C.c_void_p, [C.c_void_p]),
+    ("djg_assemble", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, _P(djg_assemble_stats)]),
+    ("djg_profile_steps", C.c_int, [C.c_void_p, C.c_int64, _P(C.c_float), _P(C.c_float), _P(C.c_float)]),
+    ("djg_get_info", C.c_int, [C.c_void_p, _P(djg_engine_info)]),
+    ("djg_get_slot_map", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("djg_last_error", C.c_char_p, [C.c_void_p]),
+    ("djg_status_string", C.c_char_p, [C.c_int32]),
+    ("djg_create_error", C.c_char_p, []),
+    ("djg_spec_default_box", None, [_P(djg_scenario_spec), C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int64]),
+    ("djg_bench_material", None, [C.c_int32, _P(djg_material_params)]),
+    ("djg_scenario_build", C.c_int, [_P(djg_scenario_spec), C.c_int32, _P(C.c_void_p)]),
+    ("djg_scenario_free", None, [C.c_void_p]),
+    ("djg_scenario_error", C.c_char_p, []),
+    ("djg_scenario_scalars", C.c_int, [C.c_void_p, _P(djg_image_scalars)]),
+    ("djg_scenario_image", C.c_int, [C.c_void_p, _P(djg_image_ptrs)]),
+    ("djg_scenario_desc", C.c_int, [C.c_void_p, C.c_int32, _P(djg_desc)]),
+]
+
+_lib = None
+
+
+def load_library(path: os.PathLike | str | None = None) -> C.CDLL:
+    """Load libdjg.so (the CUDA engine + host builder). Raises if absent."""
+    global _lib
+    if _lib is not None and path is None:
+        return _lib
+    p = Path(path) if path else LIB_PATH
+    if not p.exists():
+        raise RuntimeError(
+            f"libdjg.so not found at {p}: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+            " (there is no CPU fallback)")
+    lib = C.CDLL(str(p))
+    for name, res, args in EXPORTS:
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    if path is None:
+        _lib = lib
+    return lib

@@ -1,0 +1,708 @@
+// libdjg: the B200 DJ-TLED engine behind the C-ABI of include/djg.h.
+//
+// One engine = one problem resident in HBM:
+//   conn/slot   int4 planes [npe/4][E]     connectivity and force-slot positions
+//   consts      Plane planes [nplanes][E]  hot constants (float4 / double2)
+//   u[3]        Node[N]                    triple-buffered displacement (xyz+pad)
+//   ef          Node[capacity]             element-node forces in sliced CSR order
+//   row_len, slice_base, c1, code, target, t_total, r_ext   node data
+//   ctrl        Ctrl                       step counter + failure flags
+// A step is k_element then k_node on one stream; multi-step calls replay a
+// CUDA graph of G steps. Buffer roles rotate with ctrl.step % 3 on the device,
+// so one graph serves every phase and a failed step leaves the state as the
+// reference's advance_step does (solver.hpp:106-110, 143-147).
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#include "djg.h"
+#include "kernels.cuh"
+
+namespace djg {
+namespace {
+
+thread_local std::string g_create_error;
+
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct DescError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+#define CK(call)                                                                                   \
+    do {                                                                                           \
+        const cudaError_t _e = (call);                                                             \
+        if (_e != cudaSuccess)                                                                     \
+            throw CudaError(std::string(#call) + ": " + cudaGetErrorString(_e) + " (" __FILE__ ":" + \
+                            std::to_string(__LINE__) + ")");                                       \
+    } while (0)
+
+inline int npe_of(int kind) { return kind == DJG_T4 ? 4 : 8; }
+
+inline int const_count(int kind, int model) {
+    int n = 23;
+    if (model == DJG_TI || model == DJG_OT) n += 12;
+    if (model == DJG_OT) n += 12;
+    if (model == DJG_MR) n += 57;
+    if (kind == DJG_H8) n += 33;
+    return n;
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void alloc(size_t b) {
+        bytes = b;
+        if (b) CK(cudaMalloc(&p, b));
+    }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+    template <class T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+class EngineBase {
+public:
+    virtual ~EngineBase() = default;
+    virtual void set_state(const void* u, const void* up, int64_t step) = 0;
+    virtual void set_external(const void* r) = 0;
+    virtual void get_state(void* u, void* up, int64_t* step) = 0;
+    virtual int step(int64_t n, djg_report* rep) = 0;
+    virtual void step_async(int64_t n) = 0;
+    virtual int sync(djg_report* rep) = 0;
+    virtual int assemble(const void* u, void* f, djg_assemble_stats* st) = 0;
+    virtual int profile(int64_t n, float* ms_e, float* ms_n, float* ms_t) = 0;
+    virtual void info(djg_engine_info* out) = 0;
+    virtual void slot_map(int32_t* out) = 0;
+    virtual cudaStream_t stream() const = 0;
+};
+
+template <class Real>
+class Engine final : public EngineBase {
+    using T = RT<Real>;
+    using Node = typename T::Node;
+    using Plane = typename T::Plane;
+
+public:
+    explicit Engine(const djg_desc& d) {
+        kind_ = d.kind;
+        model_ = d.material.model;
+        npe_ = npe_of(kind_);
+        N_ = d.num_nodes;
+        E_ = d.num_elements;
+        policy_ = d.inversion_policy;
+        flags_ = d.flags;
+        nconst_ = const_count(kind_, model_);
+        nplanes_ = (nconst_ + T::kPlane - 1) / T::kPlane;
+        if (d.nconst != nconst_) throw DescError("nconst does not match djg_const_count(kind, model)");
+        if (N_ < 1 || E_ < 1) throw DescError("mesh must have nodes and elements");
+        if (!d.conn || !d.consts || !d.dof_kind || !d.c1 || !d.massless)
+            throw DescError("descriptor is missing a required array");
+        if (E_ * npe_ > INT32_MAX || N_ > INT32_MAX) throw DescError("mesh too large for 32-bit slot indexing");
+
+        CK(cudaSetDevice(d.device));
+        CK(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, d.device));
+        CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+
+        const int npe = npe_;
+        const int32_t* conn = d.conn;
+        for (int64_t i = 0; i < E_ * npe; ++i)
+            if (conn[i] < 0 || conn[i] >= N_) throw DescError("connectivity index out of range");
+
+        // Node -> (element, local) adjacency in ascending element order
+        // (NodeElementAdjacency::build, mesh.hpp:299-320).
+        std::vector<int64_t> off_v, elem_v;
+        std::vector<int32_t> loc_v;
+        const int64_t* off = d.csr_offsets;
+        const int64_t* celem = d.csr_elem;
+        const int32_t* cloc = d.csr_local;
+        if (!off || !celem || !cloc) {
+            off_v.assign(size_t(N_) + 1, 0);
+            for (int64_t i = 0; i < E_ * npe; ++i) off_v[size_t(conn[i]) + 1]++;
+            for (int64_t n = 0; n < N_; ++n) off_v[size_t(n) + 1] += off_v[size_t(n)];
+            elem_v.resize(size_t(E_ * npe));
+            loc_v.resize(size_t(E_ * npe));
+            std::vector<int64_t> cur(off_v.begin(), off_v.end() - 1);
+            for (int64_t e = 0; e < E_; ++e)
+                for (int a = 0; a < npe; ++a) {
+                    const int64_t p = cur[size_t(conn[e * npe + a])]++;
+                    elem_v[size_t(p)] = e;
+                    loc_v[size_t(p)] = a;
+                }
+            off = off_v.data();
+            celem = elem_v.data();
+            cloc = loc_v.data();
+        }
+        if (off[0] != 0 || off[N_] != E_ * npe) throw DescError("CSR offsets inconsistent with connectivity");
+
+        // Sliced slot layout: node n's k-th slot at slice_base[n/32] + 32k + n%32.
+        const int64_t S = (N_ + 31) / 32;
+        std::vector<int32_t> row_len(static_cast<size_t>(N_)), slice_base(static_cast<size_t>(S) + 1);
+        int64_t cap = 0;
+        for (int64_t s = 0; s < S; ++s) {
+            slice_base[size_t(s)] = int32_t(cap);
+            int w = 0;
+            for (int64_t n = s * 32; n < std::min<int64_t>(N_, s * 32 + 32); ++n) {
+                const int64_t len = off[n + 1] - off[n];
+                row_len[size_t(n)] = int32_t(len);
+                w = std::max<int>(w, int(len));
+            }
+            cap += int64_t(32) * w;
+            if (cap > INT32_MAX) throw DescError("slot buffer exceeds 32-bit indexing");
+        }
+        slice_base[size_t(S)] = int32_t(cap);
+        capacity_ = std::max<int64_t>(cap, 1);
+        // slot position of (e, a)
+        std::vector<int32_t> slot(size_t(E_ * npe));
+        bool bad = false;
+#pragma omp parallel for schedule(static) reduction(|| : bad)
+        for (int64_t n = 0; n < N_; ++n) {
+            const int64_t base = int64_t(slice_base[size_t(n >> 5)]) + (n & 31);
+            for (int64_t p = off[n]; p < off[n + 1]; ++p) {
+                const int64_t e = celem[p];
+                const int a = cloc[p];
+                if (e < 0 || e >= E_ || a < 0 || a >= npe || conn[e * npe + a] != n) {
+                    bad = true;
+                    continue;
+                }
+                slot[size_t(e * npe + a)] = int32_t(base + 32 * (p - off[n]));
+            }
+        }
+        if (bad) throw DescError("CSR pairs do not match connectivity");
+
+        // Upload connectivity and slots as int4 planes.
+        const int nq = npe / 4;
+        {
+            std::vector<int32_t> planes(size_t(E_ * npe));
+            for (int which = 0; which < 2; ++which) {
+                const int32_t* src = which == 0 ? conn : slot.data();
+#pragma omp parallel for schedule(static)
+                for (int64_t e = 0; e < E_; ++e)
+                    for (int q = 0; q < nq; ++q)
+                        for (int k = 0; k < 4; ++k)
+                            planes[size_t((int64_t(q) * E_ + e) * 4 + k)] = src[e * npe + 4 * q + k];
+                DevBuf& dst = which == 0 ? conn_ : slot_;
+                dst.alloc(planes.size() * sizeof(int32_t));
+                CK(cudaMemcpy(dst.p, planes.data(), dst.bytes, cudaMemcpyHostToDevice));
+            }
+        }
+        // Constants: AoS chunks -> device planes.
+        consts_.alloc(size_t(nplanes_) * size_t(E_) * sizeof(Plane));
+        {
+            const int64_t chunk = std::min<int64_t>(E_, 1 << 20);
+            DevBuf stage;
+            stage.alloc(size_t(chunk) * nconst_ * sizeof(Real));
+            const Real* src = static_cast<const Real*>(d.consts);
+            for (int64_t e0 = 0; e0 < E_; e0 += chunk) {
+                const int64_t ne = std::min(chunk, E_ - e0);
+                CK(cudaMemcpy(stage.p, src + e0 * nconst_, size_t(ne) * nconst_ * sizeof(Real),
+                              cudaMemcpyHostToDevice));
+                const int64_t work = ne * nplanes_;
+                k_transpose_consts<Real><<<unsigned((work + 255) / 256), 256>>>(
+                    stage.as<Real>(), nconst_, e0, ne, E_, nplanes_, consts_.as<Real>());
+                CK(cudaGetLastError());
+            }
+            CK(cudaDeviceSynchronize());
+        }
+        // Node data.
+        for (auto& b : u_) b.alloc(size_t(N_) * sizeof(Node));
+        uscratch_.alloc(size_t(N_) * sizeof(Node));
+        flat_.alloc(size_t(3 * N_) * sizeof(Real));
+        ef_.alloc(size_t(capacity_) * sizeof(Node));
+        CK(cudaMemset(ef_.p, 0, ef_.bytes));
+        rowlen_.alloc(row_len.size() * sizeof(int32_t));
+        CK(cudaMemcpy(rowlen_.p, row_len.data(), rowlen_.bytes, cudaMemcpyHostToDevice));
+        slicebase_.alloc(slice_base.size() * sizeof(int32_t));
+        CK(cudaMemcpy(slicebase_.p, slice_base.data(), slicebase_.bytes, cudaMemcpyHostToDevice));
+        c1_.alloc(size_t(N_) * sizeof(Real));
+        CK(cudaMemcpy(c1_.p, d.c1, c1_.bytes, cudaMemcpyHostToDevice));
+        {
+            std::vector<uint8_t> code(static_cast<size_t>(N_));
+            for (int64_t n = 0; n < N_; ++n) {
+                uint8_t c = 0;
+                for (int i = 0; i < 3; ++i) {
+                    const uint8_t k = d.dof_kind[3 * n + i];
+                    if (k > 2) throw DescError("invalid DOF kind");
+                    c |= uint8_t(k << (2 * i));
+                }
+                if (d.massless[n]) c |= 1u << 6;
+                code[size_t(n)] = c;
+            }
+            code_.alloc(code.size());
+            CK(cudaMemcpy(code_.p, code.data(), code_.bytes, cudaMemcpyHostToDevice));
+        }
+        target_.alloc(size_t(3 * N_) * sizeof(Real));
+        tTotal_.alloc(size_t(3 * N_) * sizeof(Real));
+        if (d.dof_target) CK(cudaMemcpy(target_.p, d.dof_target, target_.bytes, cudaMemcpyHostToDevice));
+        else CK(cudaMemset(target_.p, 0, target_.bytes));
+        if (d.dof_t_total) {
+            CK(cudaMemcpy(tTotal_.p, d.dof_t_total, tTotal_.bytes, cudaMemcpyHostToDevice));
+        } else {
+            std::vector<Real> ones(size_t(3 * N_), Real(1));
+            CK(cudaMemcpy(tTotal_.p, ones.data(), tTotal_.bytes, cudaMemcpyHostToDevice));
+        }
+        ctrl_.alloc(sizeof(Ctrl));
+        CK(cudaMallocHost(reinterpret_cast<void**>(&hctrl_), sizeof(Ctrl)));
+
+        // Kernel arguments.
+        ea_.E = E_;
+        ea_.conn = conn_.as<int4>();
+        ea_.slot = slot_.as<int4>();
+        ea_.c = consts_.as<Plane>();
+        for (int i = 0; i < 3; ++i) ea_.u[i] = u_[i].as<Node>();
+        ea_.u_override = nullptr;
+        ea_.ef = ef_.as<Node>();
+        ea_.ctrl = ctrl_.as<Ctrl>();
+        const Real mu = Real(d.material.mu), c10 = Real(d.material.c10);
+        ea_.mat.dI1 = model_ == DJG_MR ? c10 : mu / 2;
+        ea_.mat.kappa = Real(d.material.kappa);
+        ea_.mat.eta_a = Real(d.material.eta_a);
+        ea_.mat.eta_b = Real(d.material.eta_b);
+        ea_.mat.dI2 = Real(d.material.c01);
+        na_.N = N_;
+        na_.row_len = rowlen_.as<int>();
+        na_.slice_base = slicebase_.as<int>();
+        na_.ef = ef_.as<Node>();
+        for (int i = 0; i < 3; ++i) na_.u[i] = u_[i].as<Node>();
+        na_.r_ext = nullptr;
+        na_.c1 = c1_.as<Real>();
+        na_.code = code_.as<unsigned char>();
+        na_.target = target_.as<Real>();
+        na_.t_total = tTotal_.as<Real>();
+        na_.c2 = Real(d.c2);
+        na_.c3 = Real(d.c3);
+        na_.dt = Real(d.dt);
+        na_.policy = policy_;
+        na_.ctrl = ctrl_.as<Ctrl>();
+        na_.f_out = flat_.as<Real>();
+        set_state(nullptr, nullptr, 0);
+    }
+
+    ~Engine() override {
+        if (graph_big_) cudaGraphExecDestroy(graph_big_);
+        if (graph_one_) cudaGraphExecDestroy(graph_one_);
+        if (hctrl_) cudaFreeHost(hctrl_);
+        if (stream_) cudaStreamDestroy(stream_);
+    }
+
+    cudaStream_t stream() const override { return stream_; }
+
+    void reset_ctrl(int64_t step) {
+        Ctrl c{};
+        c.step = step;
+        c.first_inv = kNone;
+        c.asm_first = kNone;
+        c.halt_first_inv = -1;
+        c.fail_step = -1;
+        *hctrl_ = c;
+        CK(cudaMemcpyAsync(ctrl_.p, hctrl_, sizeof(Ctrl), cudaMemcpyHostToDevice, stream_));
+        CK(cudaStreamSynchronize(stream_));
+    }
+
+    void upload_nodes(const void* flat, Node* dst) {
+        if (flat) {
+            CK(cudaMemcpyAsync(flat_.p, flat, size_t(3 * N_) * sizeof(Real), cudaMemcpyHostToDevice, stream_));
+            k_pack_nodes<Real><<<unsigned((N_ + 255) / 256), 256, 0, stream_>>>(flat_.as<Real>(), N_, dst);
+        } else {
+            k_pack_nodes<Real><<<unsigned((N_ + 255) / 256), 256, 0, stream_>>>(nullptr, N_, dst);
+        }
+        CK(cudaGetLastError());
+    }
+
+    void download_nodes(const Node* src, void* flat) {
+        k_unpack_nodes<Real><<<unsigned((N_ + 255) / 256), 256, 0, stream_>>>(src, N_, flat_.as<Real>());
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(flat, flat_.p, size_t(3 * N_) * sizeof(Real), cudaMemcpyDeviceToHost, stream_));
+    }
+
+    void set_state(const void* u, const void* up, int64_t step) override {
+        if (step < 0) throw DescError("step must be >= 0");
+        const int ph = int(step % 3);
+        upload_nodes(u, u_[ph].as<Node>());
+        upload_nodes(up, u_[(ph + 2) % 3].as<Node>());
+        upload_nodes(nullptr, u_[(ph + 1) % 3].as<Node>());
+        CK(cudaStreamSynchronize(stream_));
+        reset_ctrl(step);
+    }
+
+    void set_external(const void* r) override {
+        if (!r) {
+            na_.r_ext = nullptr;
+        } else {
+            if (!rext_.p) rext_.alloc(size_t(N_) * sizeof(Node));
+            upload_nodes(r, rext_.as<Node>());
+            CK(cudaStreamSynchronize(stream_));
+            na_.r_ext = rext_.as<Node>();
+        }
+        drop_graphs();
+    }
+
+    void read_ctrl() {
+        CK(cudaMemcpyAsync(hctrl_, ctrl_.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+    }
+
+    void get_state(void* u, void* up, int64_t* step) override {
+        read_ctrl();
+        const int ph = int(hctrl_->step % 3);
+        if (u) download_nodes(u_[ph].as<Node>(), u);
+        if (up) download_nodes(u_[(ph + 2) % 3].as<Node>(), up);
+        CK(cudaStreamSynchronize(stream_));
+        if (step) *step = hctrl_->step;
+    }
+
+    void launch_element(cudaStream_t s, const Node* u_override = nullptr) {
+        ElemArgs<Real> a = ea_;
+        a.u_override = u_override;
+        const unsigned grid = unsigned((E_ + 127) / 128);
+#define DJG_K1(K, M) k_element<Real, K, M><<<grid, 128, 0, s>>>(a)
+        if (kind_ == DJG_T4) {
+            switch (model_) {
+                case DJG_NH: DJG_K1(0, 0); break;
+                case DJG_TI: DJG_K1(0, 1); break;
+                case DJG_OT: DJG_K1(0, 2); break;
+                default: DJG_K1(0, 3); break;
+            }
+        } else {
+            switch (model_) {
+                case DJG_NH: DJG_K1(1, 0); break;
+                case DJG_TI: DJG_K1(1, 1); break;
+                case DJG_OT: DJG_K1(1, 2); break;
+                default: DJG_K1(1, 3); break;
+            }
+        }
+#undef DJG_K1
+        CK(cudaGetLastError());
+    }
+
+    void launch_node(cudaStream_t s, bool assemble_mode = false) {
+        const unsigned grid = unsigned((N_ + 255) / 256);
+        if (assemble_mode) k_node<Real, true><<<grid, 256, 0, s>>>(na_);
+        else k_node<Real, false><<<grid, 256, 0, s>>>(na_);
+        CK(cudaGetLastError());
+    }
+
+    void drop_graphs() {
+        if (graph_big_) cudaGraphExecDestroy(graph_big_);
+        if (graph_one_) cudaGraphExecDestroy(graph_one_);
+        graph_big_ = graph_one_ = nullptr;
+    }
+
+    cudaGraphExec_t capture(int steps) {
+        cudaGraph_t g;
+        CK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
+        for (int i = 0; i < steps; ++i) {
+            launch_element(stream_);
+            launch_node(stream_);
+        }
+        CK(cudaStreamEndCapture(stream_, &g));
+        cudaGraphExec_t ex;
+        CK(cudaGraphInstantiate(&ex, g, 0));
+        CK(cudaGraphDestroy(g));
+        return ex;
+    }
+
+    void step_async(int64_t n) override {
+        if (n < 0) throw DescError("nsteps must be >= 0");
+        // Fresh per-call accumulators: totals are read back by sync().
+        read_ctrl();
+        start_step_ = hctrl_->step;
+        start_total_inv_ = hctrl_->total_inv;
+        start_inv_steps_ = hctrl_->inv_steps;
+        if (flags_ & DJG_FLAG_NO_GRAPH) {
+            for (int64_t i = 0; i < n; ++i) {
+                launch_element(stream_);
+                launch_node(stream_);
+            }
+            return;
+        }
+        if (n >= kGraphSteps && !graph_big_) graph_big_ = capture(kGraphSteps);
+        if (n % kGraphSteps && !graph_one_) graph_one_ = capture(1);
+        for (int64_t i = 0; i < n / kGraphSteps; ++i) CK(cudaGraphLaunch(graph_big_, stream_));
+        for (int64_t i = 0; i < n % kGraphSteps; ++i) CK(cudaGraphLaunch(graph_one_, stream_));
+    }
+
+    int sync(djg_report* rep) override {
+        read_ctrl();
+        djg_report r{};
+        r.step = hctrl_->step;
+        r.steps_done = hctrl_->step - start_step_;
+        r.inverted_count = int64_t(hctrl_->total_inv - start_total_inv_);
+        r.inverted_steps = hctrl_->inv_steps - start_inv_steps_;
+        r.first_inverted = -1;
+        r.fail_step = -1;
+        r.status = hctrl_->halted;
+        if (hctrl_->halted == DJG_E_INVERSION) {
+            r.first_inverted = hctrl_->halt_first_inv;
+            r.fail_step = hctrl_->fail_step;
+        } else if (hctrl_->halted == DJG_E_DIVERGENCE) {
+            r.diverged = 1;
+            r.fail_step = hctrl_->fail_step;
+        }
+        if (rep) *rep = r;
+        return r.status;
+    }
+
+    int step(int64_t n, djg_report* rep) override {
+        step_async(n);
+        return sync(rep);
+    }
+
+    int assemble(const void* u, void* f, djg_assemble_stats* st) override {
+        const Node* uo = nullptr;
+        if (u) {
+            upload_nodes(u, uscratch_.as<Node>());
+            uo = uscratch_.as<Node>();
+        } else {
+            read_ctrl();
+            uo = u_[hctrl_->step % 3].as<Node>();
+        }
+        // The element kernel early-outs on a halted engine; assemble must not.
+        read_ctrl();
+        const int halted = hctrl_->halted;
+        if (halted) {
+            hctrl_->halted = 0;
+            CK(cudaMemcpyAsync(ctrl_.p, hctrl_, sizeof(Ctrl), cudaMemcpyHostToDevice, stream_));
+        }
+        launch_element(stream_, uo);
+        launch_node(stream_, true);
+        read_ctrl();
+        if (halted) {
+            hctrl_->halted = halted;
+            CK(cudaMemcpyAsync(ctrl_.p, hctrl_, sizeof(Ctrl), cudaMemcpyHostToDevice, stream_));
+        }
+        const bool abort = hctrl_->asm_first != kNone;
+        if (st) {
+            st->first_inverted = abort ? int64_t(hctrl_->asm_first) : -1;
+            st->inverted_count = int64_t(hctrl_->asm_count);
+        }
+        if (!abort && f) CK(cudaMemcpyAsync(f, flat_.p, size_t(3 * N_) * sizeof(Real), cudaMemcpyDeviceToHost, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        return abort ? DJG_E_INVERSION : DJG_OK;
+    }
+
+    int profile(int64_t n, float* ms_e, float* ms_n, float* ms_t) override {
+        read_ctrl();
+        start_step_ = hctrl_->step;
+        start_total_inv_ = hctrl_->total_inv;
+        start_inv_steps_ = hctrl_->inv_steps;
+        std::vector<cudaEvent_t> ev(size_t(3 * n + 1));
+        for (auto& e : ev) CK(cudaEventCreate(&e));
+        CK(cudaEventRecord(ev[0], stream_));
+        for (int64_t i = 0; i < n; ++i) {
+            launch_element(stream_);
+            CK(cudaEventRecord(ev[size_t(3 * i + 1)], stream_));
+            launch_node(stream_);
+            CK(cudaEventRecord(ev[size_t(3 * i + 2)], stream_));
+            CK(cudaEventRecord(ev[size_t(3 * i + 3)], stream_));
+        }
+        CK(cudaStreamSynchronize(stream_));
+        float te = 0, tn = 0, tt = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            float a = 0, b = 0;
+            CK(cudaEventElapsedTime(&a, ev[size_t(3 * i)], ev[size_t(3 * i + 1)]));
+            CK(cudaEventElapsedTime(&b, ev[size_t(3 * i + 1)], ev[size_t(3 * i + 2)]));
+            te += a;
+            tn += b;
+        }
+        CK(cudaEventElapsedTime(&tt, ev[0], ev[size_t(3 * n)]));
+        for (auto& e : ev) cudaEventDestroy(e);
+        if (ms_e) *ms_e = te;
+        if (ms_n) *ms_n = tn;
+        if (ms_t) *ms_t = tt;
+        return sync(nullptr);
+    }
+
+    void info(djg_engine_info* o) override {
+        std::memset(o, 0, sizeof(*o));
+        o->num_nodes = N_;
+        o->num_elements = E_;
+        o->num_slots = E_ * npe_;
+        o->slot_capacity = capacity_;
+        o->device_bytes = int64_t(conn_.bytes + slot_.bytes + consts_.bytes + 3 * u_[0].bytes + uscratch_.bytes +
+                                  flat_.bytes + ef_.bytes + rowlen_.bytes + slicebase_.bytes + c1_.bytes +
+                                  code_.bytes + target_.bytes + tTotal_.bytes + rext_.bytes + ctrl_.bytes);
+        o->npe = npe_;
+        o->nconst = nconst_;
+        o->const_planes = nplanes_;
+        o->precision = int32_t(sizeof(Real));
+        o->kernels_per_step = 2;
+        o->sm_count = sms_;
+    }
+
+    void slot_map(int32_t* out) override {
+        std::vector<int32_t> planes(size_t(E_ * npe_));
+        CK(cudaMemcpy(planes.data(), slot_.p, slot_.bytes, cudaMemcpyDeviceToHost));
+        const int nq = npe_ / 4;
+        for (int64_t e = 0; e < E_; ++e)
+            for (int q = 0; q < nq; ++q)
+                for (int k = 0; k < 4; ++k) out[e * npe_ + 4 * q + k] = planes[size_t((int64_t(q) * E_ + e) * 4 + k)];
+    }
+
+private:
+    static constexpr int kGraphSteps = 32;
+    int kind_ = 0, model_ = 0, npe_ = 4, nconst_ = 0, nplanes_ = 0, policy_ = 0, sms_ = 0;
+    uint32_t flags_ = 0;
+    int64_t N_ = 0, E_ = 0, capacity_ = 0;
+    cudaStream_t stream_ = nullptr;
+    DevBuf conn_, slot_, consts_, u_[3], uscratch_, flat_, ef_, rowlen_, slicebase_, c1_, code_, target_, tTotal_,
+        rext_, ctrl_;
+    Ctrl* hctrl_ = nullptr;
+    ElemArgs<Real> ea_{};
+    NodeArgs<Real> na_{};
+    cudaGraphExec_t graph_big_ = nullptr, graph_one_ = nullptr;
+    int64_t start_step_ = 0, start_inv_steps_ = 0;
+    unsigned long long start_total_inv_ = 0;
+};
+
+}  // namespace
+}  // namespace djg
+
+struct djg_engine {
+    std::unique_ptr<djg::EngineBase> impl;
+    std::string err;
+};
+
+namespace {
+
+template <class F>
+int guarded(djg_engine* eng, F&& f) {
+    if (!eng || !eng->impl) return DJG_E_CONFIG;
+    try {
+        return f(*eng->impl);
+    } catch (const djg::DescError& e) {
+        eng->err = e.what();
+        return DJG_E_CONFIG;
+    } catch (const djg::CudaError& e) {
+        eng->err = e.what();
+        return DJG_E_CUDA;
+    } catch (const std::exception& e) {
+        eng->err = e.what();
+        return DJG_E_INTERNAL;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t djg_const_count(int32_t kind, int32_t model) { return djg::const_count(kind, model); }
+
+int djg_create(const djg_desc* d, djg_engine** out) {
+    if (!d || !out) {
+        djg::g_create_error = "null argument";
+        return DJG_E_CONFIG;
+    }
+    *out = nullptr;
+    try {
+        if (d->kind != DJG_T4 && d->kind != DJG_H8) throw djg::DescError("unknown element kind");
+        if (d->material.model < DJG_NH || d->material.model > DJG_MR) throw djg::DescError("unknown material model");
+        if (d->inversion_policy != DJG_ABORT && d->inversion_policy != DJG_SKIP_AND_REPORT)
+            throw djg::DescError("unknown inversion policy");
+        auto eng = std::make_unique<djg_engine>();
+        if (d->precision == 4) eng->impl = std::make_unique<djg::Engine<float>>(*d);
+        else if (d->precision == 8) eng->impl = std::make_unique<djg::Engine<double>>(*d);
+        else throw djg::DescError("precision must be 4 or 8");
+        *out = eng.release();
+        return DJG_OK;
+    } catch (const djg::DescError& e) {
+        djg::g_create_error = e.what();
+        return DJG_E_CONFIG;
+    } catch (const djg::CudaError& e) {
+        djg::g_create_error = e.what();
+        return DJG_E_CUDA;
+    } catch (const std::exception& e) {
+        djg::g_create_error = e.what();
+        return DJG_E_INTERNAL;
+    }
+}
+
+void djg_destroy(djg_engine* eng) { delete eng; }
+
+const char* djg_create_error(void) { return djg::g_create_error.c_str(); }
+
+int djg_set_state(djg_engine* eng, const void* u, const void* up, int64_t step) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.set_state(u, up, step);
+        return DJG_OK;
+    });
+}
+
+int djg_set_external(djg_engine* eng, const void* r) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.set_external(r);
+        return DJG_OK;
+    });
+}
+
+int djg_get_state(djg_engine* eng, void* u, void* up, int64_t* step) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.get_state(u, up, step);
+        return DJG_OK;
+    });
+}
+
+int djg_step(djg_engine* eng, int64_t n, djg_report* rep) {
+    return guarded(eng, [&](djg::EngineBase& e) { return e.step(n, rep); });
+}
+
+int djg_step_async(djg_engine* eng, int64_t n) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.step_async(n);
+        return DJG_OK;
+    });
+}
+
+int djg_sync(djg_engine* eng, djg_report* rep) {
+    return guarded(eng, [&](djg::EngineBase& e) { return e.sync(rep); });
+}
+
+void* djg_stream(djg_engine* eng) { return eng && eng->impl ? static_cast<void*>(eng->impl->stream()) : nullptr; }
+
+int djg_assemble(djg_engine* eng, const void* u, void* f, djg_assemble_stats* st) {
+    return guarded(eng, [&](djg::EngineBase& e) { return e.assemble(u, f, st); });
+}
+
+int djg_profile_steps(djg_engine* eng, int64_t n, float* ms_e, float* ms_n, float* ms_t) {
+    return guarded(eng, [&](djg::EngineBase& e) { return e.profile(n, ms_e, ms_n, ms_t); });
+}
+
+int djg_get_info(djg_engine* eng, djg_engine_info* info) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.info(info);
+        return DJG_OK;
+    });
+}
+
+int djg_get_slot_map(djg_engine* eng, int32_t* out) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.slot_map(out);
+        return DJG_OK;
+    });
+}
+
+const char* djg_last_error(djg_engine* eng) { return eng ? eng->err.c_str() : "null engine"; }
+
+const char* djg_status_string(int32_t s) {
+    switch (s) {
+        case DJG_OK: return "ok";
+        case DJG_E_INTERNAL: return "internal error";
+        case DJG_E_CONFIG: return "configuration error";
+        case DJG_E_CUDA: return "CUDA error";
+        case DJG_E_INVERSION: return "element inversion";
+        case DJG_E_DIVERGENCE: return "divergence";
+    }
+    return "unknown status";
+}
+
+}  // extern "C"

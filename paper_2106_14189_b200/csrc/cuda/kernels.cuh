@@ -1,0 +1,530 @@
+// sm_100a kernels of one DJ-TLED explicit step.
+//
+//   k_element  (K1)  one thread per element: 128-bit streaming loads of the
+//                    connectivity, force-slot positions and hot constants
+//                    (structure of 16-byte planes), gather of the element's
+//                    nodal displacements, the direct-Jacobian force of
+//                    Table 3 / Eq. 10 (+ hourglass for H8), one 16-byte store
+//                    per element node into its CSR slot.
+//   k_node     (K2+K3) one thread per node: sums its slots in ascending
+//                    element order (slots live in a sliced layout so lane i
+//                    reads slot k of node i at a coalesced address), then the
+//                    central-difference update with damping and BCs, the
+//                    non-finite detector, and the end-of-step bookkeeping.
+//
+// Arithmetic mirrors the reference expression by expression and the file is
+// compiled with --fmad=false, so results match the CPU reference up to the
+// last-ulp behaviour of cbrt. No float atomics anywhere: the only atomics are
+// the integer inversion/divergence flags (djtled_force.hpp:97-112,
+// solver.hpp:115,137).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace djg {
+
+// ------------------------------------------------------------------ types
+
+struct alignas(32) double4a {
+    double x, y, z, w;
+};
+
+template <class Real>
+struct RT;
+
+template <>
+struct RT<float> {
+    using Node = float4;    // xyz + pad: one 128-bit access per node / slot
+    using Plane = float4;   // 4 Reals per constant plane
+    static constexpr int kPlane = 4;
+    __device__ static inline Node load_node(const Node* p) { return __ldg(p); }
+    __device__ static inline Node load_stream(const Node* p) { return __ldcs(p); }
+    __device__ static inline void store_node(Node* p, float x, float y, float z) { *p = make_float4(x, y, z, 0.f); }
+    __device__ static inline Plane load_plane(const Plane* p) { return __ldcs(p); }
+};
+
+template <>
+struct RT<double> {
+    using Node = double4a;  // xyz + pad, 32 bytes = one sector
+    using Plane = double2;  // 2 Reals per constant plane
+    static constexpr int kPlane = 2;
+    __device__ static inline Node load_node(const Node* p) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+        const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+        return {a.x, a.y, b.x, b.y};
+    }
+    __device__ static inline Node load_stream(const Node* p) {
+        const double2 a = __ldcs(reinterpret_cast<const double2*>(p));
+        const double2 b = __ldcs(reinterpret_cast<const double2*>(p) + 1);
+        return {a.x, a.y, b.x, b.y};
+    }
+    __device__ static inline void store_node(Node* p, double x, double y, double z) {
+        reinterpret_cast<double2*>(p)[0] = make_double2(x, y);
+        reinterpret_cast<double2*>(p)[1] = make_double2(z, 0.0);
+    }
+    __device__ static inline Plane load_plane(const Plane* p) { return __ldcs(p); }
+};
+
+// Record layout per (kind, model): offsets in the canonical record (djg.h).
+template <int KIND, int MODEL>
+struct Layout {
+    static constexpr bool kI4 = MODEL == 1 || MODEL == 2;
+    static constexpr bool kI6 = MODEL == 2;
+    static constexpr bool kI2 = MODEL == 3;
+    static constexpr bool kH8 = KIND == 1;
+    static constexpr int NPE = kH8 ? 8 : 4;
+    static constexpr int m4 = 23, I4m = 29;
+    static constexpr int m6 = kI4 ? 35 : 23, I6m = m6 + 6;
+    static constexpr int M2 = 23, I2m = 44;
+    static constexpr int after_mat = 23 + (kI4 ? 12 : 0) + (kI6 ? 12 : 0) + (kI2 ? 57 : 0);
+    static constexpr int khg = after_mat, gamma = after_mat + 1;
+    static constexpr int count = after_mat + (kH8 ? 33 : 0);
+};
+
+// Device control block: the step counter and the failure flags of
+// advance_step / run_simulation, kept on the device so a multi-step graph
+// needs no host round trip.
+struct Ctrl {
+    long long step;                 // SimState::step
+    unsigned long long first_inv;   // min inverted element this step (~0ull: none)
+    unsigned long long inv_count;   // inverted elements this step
+    unsigned int blocks_done;       // k_node completion counter
+    int diverged;                   // non-finite seen this step
+    int halted;                     // 0, or DJG_E_INVERSION / DJG_E_DIVERGENCE
+    int pad;
+    long long fail_step;            // state.step + 1 of the failing step
+    long long halt_first_inv;       // element reported with an inversion halt
+    unsigned long long total_inv;   // accumulated inverted elements
+    long long inv_steps;            // steps with >= 1 inversion
+    unsigned long long asm_first;   // djg_assemble result
+    unsigned long long asm_count;
+};
+
+constexpr unsigned long long kNone = ~0ull;
+
+template <class Real>
+struct MatParams {
+    Real dI1;     // mu/2 (NH/TI/OT) or c10 (MR): energy_derivatives, material.hpp:266-290
+    Real kappa;   // dJ = kappa (J - 1)
+    Real eta_a;   // dI4 = eta_a (Ib4 - 1)
+    Real eta_b;   // dI6 = eta_b (Ib6 - 1)
+    Real dI2;     // c01
+};
+
+template <class Real>
+struct ElemArgs {
+    long long E;
+    const int4* conn;                    // NPE/4 planes of int4[E]
+    const int4* slot;                    // NPE/4 planes of int4[E]: slot positions
+    const typename RT<Real>::Plane* c;   // nplanes planes of Plane[E]
+    const typename RT<Real>::Node* u[3]; // triple-buffered displacement
+    const typename RT<Real>::Node* u_override;
+    typename RT<Real>::Node* ef;         // sliced force-slot buffer
+    Ctrl* ctrl;
+    MatParams<Real> mat;
+};
+
+template <class Real>
+struct NodeArgs {
+    long long N;
+    const int* row_len;                  // CSR row length per node
+    const int* slice_base;               // first slot position of each 32-node slice
+    const typename RT<Real>::Node* ef;
+    typename RT<Real>::Node* u[3];
+    const typename RT<Real>::Node* r_ext;  // NULL: identically zero
+    const Real* c1;
+    const unsigned char* code;           // 2 bits per DOF kind | massless << 6
+    const Real* target;                  // 3N
+    const Real* t_total;                 // 3N
+    Real c2, c3, dt;
+    int policy;                          // 0 abort, 1 skip and report
+    Ctrl* ctrl;
+    Real* f_out;                         // assemble mode: 3N internal forces
+};
+
+// ------------------------------------------------------------------ K1
+
+template <class Real, int KIND, int MODEL>
+__global__ void __launch_bounds__(128) k_element(const ElemArgs<Real> A) {
+    using L = Layout<KIND, MODEL>;
+    using T = RT<Real>;
+    constexpr int NPE = L::NPE;
+    constexpr int NP = (L::count + T::kPlane - 1) / T::kPlane;
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= A.E) return;
+    if (*(volatile const int*)&A.ctrl->halted) return;
+    const int phase = int(A.ctrl->step % 3);
+    // Select by value: indexing the kernel-parameter array with a runtime
+    // value would copy the whole parameter block to local memory.
+    const typename T::Node* __restrict__ u =
+        A.u_override ? A.u_override : (phase == 0 ? A.u[0] : (phase == 1 ? A.u[1] : A.u[2]));
+
+    // Connectivity (int32 node ids), 128-bit per 4 nodes.
+    int nid[NPE];
+#pragma unroll
+    for (int p = 0; p < NPE / 4; ++p) {
+        const int4 q = __ldcs(A.conn + (long long)p * A.E + e);
+        nid[4 * p + 0] = q.x; nid[4 * p + 1] = q.y; nid[4 * p + 2] = q.z; nid[4 * p + 3] = q.w;
+    }
+    // Hot constants.
+    Real c[NP * T::kPlane];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        const typename T::Plane v = T::load_plane(A.c + (long long)p * A.E + e);
+        if constexpr (T::kPlane == 4) {
+            c[4 * p + 0] = v.x; c[4 * p + 1] = v.y; c[4 * p + 2] = v.z; c[4 * p + 3] = v.w;
+        } else {
+            c[2 * p + 0] = v.x; c[2 * p + 1] = v.y;
+        }
+    }
+    // Gathered displacements of the element's nodes.
+    Real ux[NPE], uy[NPE], uz[NPE];
+#pragma unroll
+    for (int a = 0; a < NPE; ++a) {
+        const typename T::Node v = T::load_node(u + nid[a]);
+        ux[a] = v.x; uy[a] = v.y; uz[a] = v.z;
+    }
+
+    // update_jacobian (kinematics.hpp:31-45): Jt = J0 + D U.
+    Real Jt[3][3];
+    if constexpr (KIND == 0) {
+        // T4: D[i] = (-1, e_i): du = u_{i+1} - u_0 (the reference's sum
+        // 0 - u0 + u_{i+1} + 0 + 0 rounds identically).
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            Jt[i][0] = c[3 * i + 0] + (ux[i + 1] - ux[0]);
+            Jt[i][1] = c[3 * i + 1] + (uy[i + 1] - uy[0]);
+            Jt[i][2] = c[3 * i + 2] + (uz[i + 1] - uz[0]);
+        }
+    } else {
+        // H8: D[i][a] = sign/8; summing the signed terms first and scaling by
+        // the exact power of two 1/8 afterwards gives the same rounding.
+        constexpr int S[8][3] = {{-1, -1, -1}, {+1, -1, -1}, {+1, +1, -1}, {-1, +1, -1},
+                                 {-1, -1, +1}, {+1, -1, +1}, {+1, +1, +1}, {-1, +1, +1}};
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            Real sx = S[0][i] > 0 ? ux[0] : -ux[0];
+            Real sy = S[0][i] > 0 ? uy[0] : -uy[0];
+            Real sz = S[0][i] > 0 ? uz[0] : -uz[0];
+#pragma unroll
+            for (int a = 1; a < 8; ++a) {
+                if (S[a][i] > 0) { sx = sx + ux[a]; sy = sy + uy[a]; sz = sz + uz[a]; }
+                else { sx = sx - ux[a]; sy = sy - uy[a]; sz = sz - uz[a]; }
+            }
+            Jt[i][0] = c[3 * i + 0] + Real(0.125) * sx;
+            Jt[i][1] = c[3 * i + 1] + Real(0.125) * sy;
+            Jt[i][2] = c[3 * i + 2] + Real(0.125) * sz;
+        }
+    }
+
+    // det / inversion test / adjugate inverse (core.hpp:187-212).
+    const Real det = Jt[0][0] * (Jt[1][1] * Jt[2][2] - Jt[1][2] * Jt[2][1]) -
+                     Jt[0][1] * (Jt[1][0] * Jt[2][2] - Jt[1][2] * Jt[2][0]) +
+                     Jt[0][2] * (Jt[1][0] * Jt[2][1] - Jt[1][1] * Jt[2][0]);
+
+    typename T::Node* __restrict__ ef = A.ef;
+    int sl[NPE];
+#pragma unroll
+    for (int p = 0; p < NPE / 4; ++p) {
+        const int4 q = __ldcs(A.slot + (long long)p * A.E + e);
+        sl[4 * p + 0] = q.x; sl[4 * p + 1] = q.y; sl[4 * p + 2] = q.z; sl[4 * p + 3] = q.w;
+    }
+
+    if (!(det > Real(0))) {
+        // record_inversion (djtled_force.hpp:107-112) + zeroed rows (:187-191).
+        atomicAdd(&A.ctrl->inv_count, 1ull);
+        atomicMin(&A.ctrl->first_inv, (unsigned long long)e);
+#pragma unroll
+        for (int a = 0; a < NPE; ++a) T::store_node(ef + sl[a], Real(0), Real(0), Real(0));
+        return;
+    }
+    const Real s_inv = Real(1) / det;
+    Real Ji[3][3];
+    Ji[0][0] = (Jt[1][1] * Jt[2][2] - Jt[1][2] * Jt[2][1]) * s_inv;
+    Ji[0][1] = (Jt[0][2] * Jt[2][1] - Jt[0][1] * Jt[2][2]) * s_inv;
+    Ji[0][2] = (Jt[0][1] * Jt[1][2] - Jt[0][2] * Jt[1][1]) * s_inv;
+    Ji[1][0] = (Jt[1][2] * Jt[2][0] - Jt[1][0] * Jt[2][2]) * s_inv;
+    Ji[1][1] = (Jt[0][0] * Jt[2][2] - Jt[0][2] * Jt[2][0]) * s_inv;
+    Ji[1][2] = (Jt[0][2] * Jt[1][0] - Jt[0][0] * Jt[1][2]) * s_inv;
+    Ji[2][0] = (Jt[1][0] * Jt[2][1] - Jt[1][1] * Jt[2][0]) * s_inv;
+    Ji[2][1] = (Jt[0][1] * Jt[2][0] - Jt[0][0] * Jt[2][1]) * s_inv;
+    Ji[2][2] = (Jt[0][0] * Jt[1][1] - Jt[0][1] * Jt[1][0]) * s_inv;
+
+    // volume_ratio, g_vector, invariants (kinematics.hpp:47-103).
+    const Real J = det / c[9];
+    Real g[6];
+    g[0] = Jt[0][0] * Jt[0][0] + Jt[0][1] * Jt[0][1] + Jt[0][2] * Jt[0][2];
+    g[1] = Jt[1][0] * Jt[1][0] + Jt[1][1] * Jt[1][1] + Jt[1][2] * Jt[1][2];
+    g[2] = Jt[2][0] * Jt[2][0] + Jt[2][1] * Jt[2][1] + Jt[2][2] * Jt[2][2];
+    g[3] = Jt[0][0] * Jt[1][0] + Jt[0][1] * Jt[1][1] + Jt[0][2] * Jt[1][2];
+    g[4] = Jt[0][0] * Jt[2][0] + Jt[0][1] * Jt[2][1] + Jt[0][2] * Jt[2][2];
+    g[5] = Jt[1][0] * Jt[2][0] + Jt[1][1] * Jt[2][1] + Jt[1][2] * Jt[2][2];
+    const Real cb = cbrt(J);
+    const Real j_m23 = Real(1) / (cb * cb);
+    const Real I1 = g[0] * c[11] + g[1] * c[12] + g[2] * c[13] + g[3] * c[14] + g[4] * c[15] + g[5] * c[16];
+    const Real Ib1 = j_m23 * I1;
+
+    // energy_derivatives + the Table 3 bracket (djtled_force.hpp:36-82).
+    const Real dJ = A.mat.kappa * (J - Real(1));
+    Real s[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) s[k] = A.mat.dI1 * c[17 + k];
+    Real dev = A.mat.dI1 * Ib1;
+    if constexpr (L::kI4) {
+        const Real I4 = g[0] * c[L::m4 + 0] + g[1] * c[L::m4 + 1] + g[2] * c[L::m4 + 2] + g[3] * c[L::m4 + 3] +
+                        g[4] * c[L::m4 + 4] + g[5] * c[L::m4 + 5];
+        const Real Ib4 = j_m23 * I4;
+        const Real dI4 = A.mat.eta_a * (Ib4 - Real(1));
+#pragma unroll
+        for (int k = 0; k < 6; ++k) s[k] = s[k] + dI4 * c[L::I4m + k];
+        dev += dI4 * Ib4;
+    }
+    if constexpr (L::kI6) {
+        const Real I6 = g[0] * c[L::m6 + 0] + g[1] * c[L::m6 + 1] + g[2] * c[L::m6 + 2] + g[3] * c[L::m6 + 3] +
+                        g[4] * c[L::m6 + 4] + g[5] * c[L::m6 + 5];
+        const Real Ib6 = j_m23 * I6;
+        const Real dI6 = A.mat.eta_b * (Ib6 - Real(1));
+#pragma unroll
+        for (int k = 0; k < 6; ++k) s[k] = s[k] + dI6 * c[L::I6m + k];
+        dev += dI6 * Ib6;
+    }
+    if constexpr (L::kI2) {
+        // I2 = g^T M2 g (Sym6::quadratic_form, core.hpp:296-304).
+        constexpr int idx[6][6] = {{0, 1, 2, 3, 4, 5},      {1, 6, 7, 8, 9, 10},    {2, 7, 11, 12, 13, 14},
+                                   {3, 8, 12, 15, 16, 17}, {4, 9, 13, 16, 18, 19}, {5, 10, 14, 17, 19, 20}};
+        Real q = Real(0);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+            Real row = c[L::M2 + idx[i][i]] * g[i];
+#pragma unroll
+            for (int j = i + 1; j < 6; ++j) row += Real(2) * c[L::M2 + idx[i][j]] * g[j];
+            q += row * g[i];
+        }
+        const Real j_m43 = j_m23 * j_m23;
+        const Real Ib2 = j_m43 * q;
+        // contract_ghat (djtled_force.hpp:18-24)
+        Real cg[6];
+#pragma unroll
+        for (int k = 0; k < 6; ++k) cg[k] = g[0] * c[L::I2m + k];
+#pragma unroll
+        for (int m = 1; m < 6; ++m)
+#pragma unroll
+            for (int k = 0; k < 6; ++k) cg[k] = cg[k] + g[m] * c[L::I2m + 6 * m + k];
+        const Real w = j_m23 * A.mat.dI2;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) s[k] = s[k] + w * cg[k];
+        dev += Real(2) * A.mat.dI2 * Ib2;
+    }
+    const Real cc = (-Real(2) / Real(3) * dev + J * dJ) * c[10];
+
+    // K = j_m23 (Jt^T S) + c Jt^-1
+    const Real Sm[3][3] = {{s[0], s[3], s[4]}, {s[3], s[1], s[5]}, {s[4], s[5], s[2]}};
+    Real K[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const Real mt = Jt[0][i] * Sm[0][j] + Jt[1][i] * Sm[1][j] + Jt[2][i] * Sm[2][j];
+            K[i][j] = j_m23 * mt + cc * Ji[i][j];
+        }
+
+    if constexpr (KIND == 0) {
+        // T4 rows: f1..f3 = columns of K, f0 = -(f1 + f2 + f3).
+        T::store_node(ef + sl[1], K[0][0], K[1][0], K[2][0]);
+        T::store_node(ef + sl[2], K[0][1], K[1][1], K[2][1]);
+        T::store_node(ef + sl[3], K[0][2], K[1][2], K[2][2]);
+        T::store_node(ef + sl[0], Real(-1) * ((K[0][0] + K[0][1]) + K[0][2]),
+                      Real(-1) * ((K[1][0] + K[1][1]) + K[1][2]), Real(-1) * ((K[2][0] + K[2][1]) + K[2][2]));
+    } else {
+        constexpr int S[8][3] = {{-1, -1, -1}, {+1, -1, -1}, {+1, +1, -1}, {-1, +1, -1},
+                                 {-1, -1, +1}, {+1, -1, +1}, {+1, +1, +1}, {-1, +1, +1}};
+        Real f[8][3];
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                // D0a K[i][0] + D1a K[i][1] + D2a K[i][2] with D = sign/8.
+                Real t = S[a][0] > 0 ? K[i][0] : -K[i][0];
+                t = S[a][1] > 0 ? t + K[i][1] : t - K[i][1];
+                t = S[a][2] > 0 ? t + K[i][2] : t - K[i][2];
+                f[a][i] = Real(0.125) * t;
+            }
+        // hourglass_force (djtled_force.hpp:86-95)
+        const Real khg = c[L::khg];
+        if (khg != Real(0)) {
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                Real q0 = Real(0), q1 = Real(0), q2 = Real(0);
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    const Real gm = c[L::gamma + 8 * m + b];
+                    q0 = q0 + gm * ux[b];
+                    q1 = q1 + gm * uy[b];
+                    q2 = q2 + gm * uz[b];
+                }
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    const Real kg = khg * c[L::gamma + 8 * m + b];
+                    f[b][0] = f[b][0] + kg * q0;
+                    f[b][1] = f[b][1] + kg * q1;
+                    f[b][2] = f[b][2] + kg * q2;
+                }
+            }
+        }
+#pragma unroll
+        for (int a = 0; a < 8; ++a) T::store_node(ef + sl[a], f[a][0], f[a][1], f[a][2]);
+    }
+}
+
+// ------------------------------------------------------------------ K2+K3
+
+// Sums node n's element rows in ascending element order from +0
+// (gather_nodal_forces, djtled_force.hpp:116-134).
+template <class Real>
+__device__ __forceinline__ void gather_row(const NodeArgs<Real>& A, long long n, Real& sx, Real& sy, Real& sz) {
+    using T = RT<Real>;
+    const int len = A.row_len[n];
+    const typename T::Node* p = A.ef + (long long)A.slice_base[n >> 5] + (n & 31);
+    sx = Real(0); sy = Real(0); sz = Real(0);
+    for (int k = 0; k < len; ++k) {
+        const typename T::Node v = T::load_stream(p + 32 * k);
+        sx += v.x; sy += v.y; sz += v.z;
+    }
+}
+
+// Per-DOF central-difference update (advance_step, solver.hpp:112-141).
+template <class Real>
+__device__ __forceinline__ Real dof_update(int kind, bool massless, Real c1, Real r, Real f, Real uc, Real up,
+                                           Real c2, Real c3, Real t_next, const Real* target, const Real* t_total,
+                                           long long dof, bool& nonfinite) {
+    if (kind == 1) return Real(0);
+    if (kind == 2) {
+        const Real s = t_next / t_total[dof];
+        return (s >= Real(1) ? Real(1) : s) * target[dof];
+    }
+    if (massless) return Real(0);
+    const Real v = c1 * (r - f) + c2 * uc + c3 * up;
+    if (!isfinite(v)) nonfinite = true;
+    return v;
+}
+
+template <class Real, bool kAssemble>
+__global__ void __launch_bounds__(256) k_node(const NodeArgs<Real> A) {
+    using T = RT<Real>;
+    Ctrl* ctrl = A.ctrl;
+    if (*(volatile const int*)&ctrl->halted && !kAssemble) return;
+    __shared__ int s_nonfinite;
+    if (threadIdx.x == 0) s_nonfinite = 0;
+    __syncthreads();
+    const long long step = ctrl->step;
+    const bool inverted = ctrl->first_inv != kNone;
+    const bool skip = inverted && A.policy == 0;  // Abort: no gather, no update (djtled_force.hpp:202-208)
+    const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n < A.N && !skip) {
+        Real fx, fy, fz;
+        gather_row(A, n, fx, fy, fz);
+        if constexpr (kAssemble) {
+            A.f_out[3 * n + 0] = fx;
+            A.f_out[3 * n + 1] = fy;
+            A.f_out[3 * n + 2] = fz;
+        } else {
+            const int ph = int(step % 3);
+            const typename T::Node* ucur = ph == 0 ? A.u[0] : (ph == 1 ? A.u[1] : A.u[2]);
+            const typename T::Node* uprv = ph == 0 ? A.u[2] : (ph == 1 ? A.u[0] : A.u[1]);
+            typename T::Node* unxt = ph == 0 ? A.u[1] : (ph == 1 ? A.u[2] : A.u[0]);
+            const typename T::Node uc = T::load_node(ucur + n);
+            const typename T::Node up = T::load_node(uprv + n);
+            typename T::Node r;
+            if (A.r_ext) r = T::load_node(A.r_ext + n);
+            else { r.x = Real(0); r.y = Real(0); r.z = Real(0); }
+            const int code = A.code[n];
+            const bool massless = (code >> 6) & 1;
+            const Real c1 = A.c1[n];
+            const Real t_next = A.dt * Real(step + 1);
+            bool nf = false;
+            const Real vx = dof_update<Real>(code & 3, massless, c1, r.x, fx, uc.x, up.x, A.c2, A.c3, t_next,
+                                             A.target, A.t_total, 3 * n + 0, nf);
+            const Real vy = dof_update<Real>((code >> 2) & 3, massless, c1, r.y, fy, uc.y, up.y, A.c2, A.c3, t_next,
+                                             A.target, A.t_total, 3 * n + 1, nf);
+            const Real vz = dof_update<Real>((code >> 4) & 3, massless, c1, r.z, fz, uc.z, up.z, A.c2, A.c3, t_next,
+                                             A.target, A.t_total, 3 * n + 2, nf);
+            T::store_node(unxt + n, vx, vy, vz);
+            if (nf) s_nonfinite = 1;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    if (s_nonfinite) atomicOr(&ctrl->diverged, 1);
+    __threadfence();
+    const unsigned int done = atomicAdd(&ctrl->blocks_done, 1u);
+    if (done != gridDim.x - 1) return;
+    // Last block: close the step (advance_step's tail, solver.hpp:143-152).
+    __threadfence();
+    const unsigned long long cnt = atomicAdd(&ctrl->inv_count, 0ull);
+    const unsigned long long first = atomicAdd(&ctrl->first_inv, 0ull);
+    if (kAssemble) {
+        ctrl->asm_first = (first != kNone && A.policy == 0) ? first : kNone;
+        ctrl->asm_count = cnt;
+    } else {
+        const int div = atomicOr(&ctrl->diverged, 0);
+        ctrl->total_inv += cnt;
+        if (cnt > 0) ctrl->inv_steps += 1;
+        if (skip) {
+            ctrl->halted = 4;  // DJG_E_INVERSION
+            ctrl->halt_first_inv = (long long)first;
+            ctrl->fail_step = step + 1;
+        } else if (div) {
+            ctrl->halted = 5;  // DJG_E_DIVERGENCE
+            ctrl->fail_step = step + 1;
+        } else {
+            ctrl->step = step + 1;
+        }
+    }
+    ctrl->inv_count = 0;
+    ctrl->first_inv = kNone;
+    ctrl->diverged = 0;
+    __threadfence();
+    ctrl->blocks_done = 0;
+}
+
+// ------------------------------------------------------------------ setup
+
+// AoS record chunk -> plane layout: plane p of element e holds record Reals
+// [kPlane*p, kPlane*p + kPlane).
+template <class Real>
+__global__ void k_transpose_consts(const Real* __restrict__ aos, int nconst, long long e0, long long ne,
+                                   long long E, int nplanes, Real* __restrict__ planes) {
+    constexpr int W = RT<Real>::kPlane;
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= ne * nplanes) return;
+    const long long e = i / nplanes;
+    const int p = int(i % nplanes);
+    Real* dst = planes + ((long long)p * E + e0 + e) * W;
+#pragma unroll
+    for (int k = 0; k < W; ++k) {
+        const int f = p * W + k;
+        dst[k] = f < nconst ? aos[e * nconst + f] : Real(0);
+    }
+}
+
+// Packs flat Real[3N] into padded nodes and back.
+template <class Real>
+__global__ void k_pack_nodes(const Real* __restrict__ flat, long long N, typename RT<Real>::Node* __restrict__ out) {
+    const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    if (flat) RT<Real>::store_node(out + n, flat[3 * n], flat[3 * n + 1], flat[3 * n + 2]);
+    else RT<Real>::store_node(out + n, Real(0), Real(0), Real(0));
+}
+
+template <class Real>
+__global__ void k_unpack_nodes(const typename RT<Real>::Node* __restrict__ in, long long N, Real* __restrict__ flat) {
+    const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const typename RT<Real>::Node v = in[n];
+    flat[3 * n] = v.x;
+    flat[3 * n + 1] = v.y;
+    flat[3 * n + 2] = v.z;
+}
+
+}  // namespace djg

@@ -1,0 +1,718 @@
+// Host-side problem preparation for the B200 DJ-TLED engine.
+//
+// Everything here runs once before the step loop: mesh generation, the
+// node->element adjacency, the per-element hot constants, lumped masses, the
+// stable time step, boundary conditions and update coefficients. The
+// arithmetic is written to follow the reference operation by operation (the
+// file:line next to each function), because the device step consumes these
+// Reals and parity with the reference starts here: the same inputs must come
+// out bit-identical. Compile without -ffast-math and with -ffp-contract=off.
+#pragma once
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <limits>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#ifdef _OPENMP
+#include <omp.h>
+#endif
+
+#include "djg_types.h"
+
+namespace djg {
+
+// Error types with the reference's meaning (core.hpp:28-57).
+struct ConfigError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct MeshError : std::runtime_error {
+    MeshError(const std::string& what, long element = -1)
+        : std::runtime_error(element < 0 ? what : "element " + std::to_string(element) + ": " + what),
+          element_(element) {}
+    long element() const { return element_; }
+    long element_;
+};
+struct SimulationError : std::runtime_error {
+    enum class Kind { ElementInversion, Divergence };
+    SimulationError(Kind kind, const std::string& what, long index)
+        : std::runtime_error(what), kind_(kind), index_(index) {}
+    Kind kind() const { return kind_; }
+    long index() const { return index_; }
+    Kind kind_;
+    long index_;
+};
+
+inline int npe_of(int kind) { return kind == DJG_T4 ? 4 : 8; }
+
+// Number of Reals in the canonical hot-field record (djg.h).
+inline int const_count(int kind, int model) {
+    int n = 23;
+    if (model == DJG_TI || model == DJG_OT) n += 12;
+    if (model == DJG_OT) n += 12;
+    if (model == DJG_MR) n += 21 + 36;
+    if (kind == DJG_H8) n += 33;
+    return n;
+}
+
+// Field offsets inside the canonical record.
+struct ConstLayout {
+    int J0 = 0, det = 9, V0 = 10, m1 = 11, I1m = 17;
+    int m4 = -1, I4m = -1, m6 = -1, I6m = -1, M2 = -1, I2m = -1, khg = -1, gamma = -1;
+    int count = 23;
+    ConstLayout(int kind, int model) {
+        int o = 23;
+        if (model == DJG_TI || model == DJG_OT) { m4 = o; I4m = o + 6; o += 12; }
+        if (model == DJG_OT) { m6 = o; I6m = o + 6; o += 12; }
+        if (model == DJG_MR) { M2 = o; I2m = o + 21; o += 57; }
+        if (kind == DJG_H8) { khg = o; gamma = o + 1; o += 33; }
+        count = o;
+    }
+};
+
+// Shape derivatives at the single integration point, d[i][a] = dh_a/dxi_i
+// (element.hpp:31-47). H8 corner signs follow element.hpp:17-20.
+inline constexpr int kCornerSign[8][3] = {
+    {-1, -1, -1}, {+1, -1, -1}, {+1, +1, -1}, {-1, +1, -1},
+    {-1, -1, +1}, {+1, -1, +1}, {+1, +1, +1}, {-1, +1, +1},
+};
+
+template <class Real>
+struct Shape {
+    int kind, n;
+    Real d[3][8];
+    explicit Shape(int k) : kind(k), n(npe_of(k)) {
+        for (int i = 0; i < 3; ++i)
+            for (int a = 0; a < 8; ++a) d[i][a] = Real(0);
+        if (k == DJG_T4) {
+            for (int i = 0; i < 3; ++i) {
+                d[i][0] = Real(-1);
+                d[i][i + 1] = Real(1);
+            }
+        } else {
+            for (int a = 0; a < 8; ++a)
+                for (int i = 0; i < 3; ++i) d[i][a] = Real(kCornerSign[a][i]) / Real(8);
+        }
+    }
+};
+
+template <class Real>
+struct V3 {
+    Real x, y, z;
+};
+
+// 3x3 helpers with the reference's evaluation order (core.hpp:144-212).
+template <class Real>
+inline Real det3(const Real a[3][3]) {
+    return a[0][0] * (a[1][1] * a[2][2] - a[1][2] * a[2][1]) -
+           a[0][1] * (a[1][0] * a[2][2] - a[1][2] * a[2][0]) +
+           a[0][2] * (a[1][0] * a[2][1] - a[1][1] * a[2][0]);
+}
+
+template <class Real>
+inline void inv3(const Real a[3][3], Real d, Real r[3][3]) {
+    const Real s = Real(1) / d;
+    r[0][0] = (a[1][1] * a[2][2] - a[1][2] * a[2][1]) * s;
+    r[0][1] = (a[0][2] * a[2][1] - a[0][1] * a[2][2]) * s;
+    r[0][2] = (a[0][1] * a[1][2] - a[0][2] * a[1][1]) * s;
+    r[1][0] = (a[1][2] * a[2][0] - a[1][0] * a[2][2]) * s;
+    r[1][1] = (a[0][0] * a[2][2] - a[0][2] * a[2][0]) * s;
+    r[1][2] = (a[0][2] * a[1][0] - a[0][0] * a[1][2]) * s;
+    r[2][0] = (a[1][0] * a[2][1] - a[1][1] * a[2][0]) * s;
+    r[2][1] = (a[0][1] * a[2][0] - a[0][0] * a[2][1]) * s;
+    r[2][2] = (a[0][0] * a[1][1] - a[0][1] * a[1][0]) * s;
+}
+
+// Symmetric 3x3 in (xx,yy,zz,xy,xz,yz) order (core.hpp:214-228).
+template <class Real>
+struct Sym {
+    Real v[6];
+};
+
+template <class Real>
+inline void sym_full(const Sym<Real>& s, Real m[3][3]) {
+    m[0][0] = s.v[0]; m[0][1] = s.v[3]; m[0][2] = s.v[4];
+    m[1][0] = s.v[3]; m[1][1] = s.v[1]; m[1][2] = s.v[5];
+    m[2][0] = s.v[4]; m[2][1] = s.v[5]; m[2][2] = s.v[2];
+}
+
+// Q^T S Q (core.hpp:259-271): first SQ = S_full * Q, then the six entries.
+template <class Real>
+inline Sym<Real> congruence(const Real q[3][3], const Sym<Real>& s) {
+    Real sf[3][3], sq[3][3];
+    sym_full(s, sf);
+    for (int i = 0; i < 3; ++i)
+        for (int j = 0; j < 3; ++j)
+            sq[i][j] = sf[i][0] * q[0][j] + sf[i][1] * q[1][j] + sf[i][2] * q[2][j];
+    Sym<Real> r;
+    r.v[0] = q[0][0] * sq[0][0] + q[1][0] * sq[1][0] + q[2][0] * sq[2][0];
+    r.v[1] = q[0][1] * sq[0][1] + q[1][1] * sq[1][1] + q[2][1] * sq[2][1];
+    r.v[2] = q[0][2] * sq[0][2] + q[1][2] * sq[1][2] + q[2][2] * sq[2][2];
+    r.v[3] = q[0][0] * sq[0][1] + q[1][0] * sq[1][1] + q[2][0] * sq[2][1];
+    r.v[4] = q[0][0] * sq[0][2] + q[1][0] * sq[1][2] + q[2][0] * sq[2][2];
+    r.v[5] = q[0][1] * sq[0][2] + q[1][1] * sq[1][2] + q[2][1] * sq[2][2];
+    return r;
+}
+
+template <class Real>
+inline Sym<Real> scaled(Real s, const Sym<Real>& a) {
+    Sym<Real> r;
+    for (int k = 0; k < 6; ++k) r.v[k] = s * a.v[k];
+    return r;
+}
+
+// Frobenius product of symmetric matrices (core.hpp:277-280).
+template <class Real>
+inline Real ddot(const Sym<Real>& a, const Sym<Real>& b) {
+    return a.v[0] * b.v[0] + a.v[1] * b.v[1] + a.v[2] * b.v[2] +
+           2 * (a.v[3] * b.v[3] + a.v[4] * b.v[4] + a.v[5] * b.v[5]);
+}
+
+template <class Real>
+inline Real trace(const Sym<Real>& a) { return a.v[0] + a.v[1] + a.v[2]; }
+
+// outer(v) and sym_outer(u, v) (core.hpp:240-251).
+template <class Real>
+inline Sym<Real> outer(const V3<Real>& v) {
+    return {{v.x * v.x, v.y * v.y, v.z * v.z, v.x * v.y, v.x * v.z, v.y * v.z}};
+}
+template <class Real>
+inline Sym<Real> sym_outer(const V3<Real>& u, const V3<Real>& v) {
+    return {{2 * u.x * v.x, 2 * u.y * v.y, 2 * u.z * v.z, u.x * v.y + u.y * v.x,
+             u.x * v.z + u.z * v.x, u.y * v.z + u.z * v.y}};
+}
+
+inline int sym6_index(int i, int j) {
+    if (i > j) std::swap(i, j);
+    return i * 6 - i * (i + 1) / 2 + j;
+}
+
+// ---------------------------------------------------------------- material
+
+// Material<Real> (material.hpp:140-230) restricted to what precompute and the
+// step need.
+template <class Real>
+struct Material {
+    int model = DJG_NH;
+    Real mu = 0, kappa = 0, rho = 0, eta_a = 0, eta_b = 0, c10 = 0, c01 = 0;
+    V3<Real> fa{0, 0, 0}, fb{0, 0, 0};
+
+    static Material from(const djg_material_params& p) {
+        Material m;
+        m.model = p.model;
+        m.mu = Real(p.mu); m.kappa = Real(p.kappa); m.rho = Real(p.rho);
+        m.eta_a = Real(p.eta_a); m.eta_b = Real(p.eta_b);
+        m.c10 = Real(p.c10); m.c01 = Real(p.c01);
+        m.fa = {Real(p.fibre_a[0]), Real(p.fibre_a[1]), Real(p.fibre_a[2])};
+        m.fb = {Real(p.fibre_b[0]), Real(p.fibre_b[1]), Real(p.fibre_b[2])};
+        m.validate();
+        return m;
+    }
+
+    static Real norm(const V3<Real>& v) { return std::sqrt(v.x * v.x + v.y * v.y + v.z * v.z); }
+
+    void validate() const {  // material.hpp:187-207
+        if (model < DJG_NH || model > DJG_MR) throw ConfigError("unknown material model");
+        if (!(kappa > Real(0))) throw ConfigError("bulk modulus must be positive");
+        if (!(rho > Real(0))) throw ConfigError("density must be positive");
+        if (model == DJG_MR) {
+            if (c10 < Real(0) || c01 < Real(0)) throw ConfigError("Mooney-Rivlin coefficients must be >= 0");
+            if (!(c10 + c01 > Real(0))) throw ConfigError("Mooney-Rivlin coefficients must not both vanish");
+            return;
+        }
+        if (model == DJG_OT) {
+            if (eta_b < Real(0)) throw ConfigError("fibre stiffness eta_b must be >= 0");
+            if (!(norm(fb) > Real(0))) throw ConfigError("fibre direction b must be nonzero");
+        }
+        if (model == DJG_OT || model == DJG_TI) {
+            if (eta_a < Real(0)) throw ConfigError("fibre stiffness eta_a must be >= 0");
+            if (!(norm(fa) > Real(0))) throw ConfigError("fibre direction a must be nonzero");
+        }
+        if (!(mu > Real(0))) throw ConfigError("shear modulus must be positive");
+    }
+
+    bool needs_i4() const { return model == DJG_TI || model == DJG_OT; }
+    bool needs_i6() const { return model == DJG_OT; }
+    bool needs_i2() const { return model == DJG_MR; }
+
+    Real shear_modulus() const { return model == DJG_MR ? 2 * (c10 + c01) : mu; }
+
+    // FibreDirections::from normalisation (precompute.hpp:22-39).
+    static V3<Real> unit(const V3<Real>& v) {
+        const Real n = norm(v);
+        const Real s = Real(1) / n;
+        return {s * v.x, s * v.y, s * v.z};
+    }
+};
+
+// dilatational_wave_speed (material.hpp:117-120)
+template <class Real>
+inline Real wave_speed(const Material<Real>& m) {
+    return std::sqrt((m.kappa + Real(4) / Real(3) * m.shear_modulus()) / m.rho);
+}
+
+// ---------------------------------------------------------------- mesh
+
+template <class Real>
+struct Mesh {
+    int kind = DJG_T4;
+    std::vector<Real> nodes;      // 3N
+    std::vector<int32_t> conn;    // npe*E
+    int npe() const { return npe_of(kind); }
+    int64_t num_nodes() const { return int64_t(nodes.size() / 3); }
+    int64_t num_elements() const { return int64_t(conn.size()) / npe(); }
+    V3<Real> node(int64_t n) const { return {nodes[3 * n], nodes[3 * n + 1], nodes[3 * n + 2]}; }
+};
+
+// generate_box (mesh.hpp:208-264): lexicographic nodes, H8 cells in corner
+// order, T4 six-tet split along the (0,0,0)-(1,1,1) diagonal, odd axis orders
+// swapping the middle pair.
+template <class Real>
+inline Mesh<Real> generate_box(const double extent_in[3], const int32_t div[3], int kind) {
+    const Real ex[3] = {Real(extent_in[0]), Real(extent_in[1]), Real(extent_in[2])};
+    for (int i = 0; i < 3; ++i) {
+        if (!(ex[i] > Real(0))) throw ConfigError("box extent must be positive");
+        if (div[i] < 1) throw ConfigError("box divisions must be >= 1");
+    }
+    const int64_t nx = div[0], ny = div[1], nz = div[2];
+    Mesh<Real> m;
+    m.kind = kind;
+    m.nodes.resize(size_t(3 * (nx + 1) * (ny + 1) * (nz + 1)));
+    size_t w = 0;
+    for (int64_t k = 0; k <= nz; ++k)
+        for (int64_t j = 0; j <= ny; ++j)
+            for (int64_t i = 0; i <= nx; ++i) {
+                m.nodes[w++] = ex[0] * Real(int(i)) / Real(int(nx));
+                m.nodes[w++] = ex[1] * Real(int(j)) / Real(int(ny));
+                m.nodes[w++] = ex[2] * Real(int(k)) / Real(int(nz));
+            }
+    const int npe = npe_of(kind);
+    const int64_t cells = nx * ny * nz;
+    m.conn.resize(size_t(cells * (kind == DJG_H8 ? 8 : 24)));
+    auto id = [&](int64_t i, int64_t j, int64_t k) { return int32_t(i + (nx + 1) * (j + (ny + 1) * k)); };
+    static constexpr int orders[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    (void)npe;
+#pragma omp parallel for schedule(static)
+    for (int64_t c = 0; c < cells; ++c) {
+        const int64_t i = c % nx, j = (c / nx) % ny, k = c / (nx * ny);
+        int32_t corner[2][2][2];
+        for (int dz = 0; dz < 2; ++dz)
+            for (int dy = 0; dy < 2; ++dy)
+                for (int dx = 0; dx < 2; ++dx) corner[dx][dy][dz] = id(i + dx, j + dy, k + dz);
+        if (kind == DJG_H8) {
+            int32_t* out = m.conn.data() + c * 8;
+            for (int a = 0; a < 8; ++a)
+                out[a] = corner[(kCornerSign[a][0] + 1) / 2][(kCornerSign[a][1] + 1) / 2]
+                                [(kCornerSign[a][2] + 1) / 2];
+            continue;
+        }
+        int32_t* out = m.conn.data() + c * 24;
+        for (int t = 0; t < 6; ++t) {
+            const int* o = orders[t];
+            int s[3] = {0, 0, 0};
+            int32_t path[4];
+            path[0] = corner[0][0][0];
+            for (int q = 0; q < 3; ++q) {
+                s[o[q]] = 1;
+                path[q + 1] = corner[s[0]][s[1]][s[2]];
+            }
+            const bool odd = (o[0] == 0 && o[1] == 2) || (o[0] == 1 && o[1] == 0) || (o[0] == 2 && o[1] == 1);
+            if (odd) std::swap(path[1], path[2]);
+            for (int a = 0; a < 4; ++a) out[t * 4 + a] = path[a];
+        }
+    }
+    return m;
+}
+
+// Reference Jacobian J = D X (element.hpp:59-77) and volume (element.hpp:80-85).
+template <class Real>
+struct Jac {
+    Real J[3][3], Jinv[3][3], det;
+};
+
+template <class Real>
+inline bool jacobian0(const V3<Real>* x, const Shape<Real>& D, Jac<Real>& j) {
+    for (int i = 0; i < 3; ++i) {
+        Real r[3] = {Real(0), Real(0), Real(0)};
+        for (int a = 0; a < D.n; ++a) {
+            r[0] = r[0] + D.d[i][a] * x[a].x;
+            r[1] = r[1] + D.d[i][a] * x[a].y;
+            r[2] = r[2] + D.d[i][a] * x[a].z;
+        }
+        j.J[i][0] = r[0];
+        j.J[i][1] = r[1];
+        j.J[i][2] = r[2];
+    }
+    j.det = det3(j.J);
+    if (!(j.det > Real(0))) return false;
+    inv3(j.J, j.det, j.Jinv);
+    return true;
+}
+
+template <class Real>
+inline Real volume0(const Jac<Real>& j, int kind) {
+    return kind == DJG_T4 ? j.det / Real(6) : Real(8) * j.det;
+}
+
+// validate_mesh (mesh.hpp:75-92).
+template <class Real>
+inline void validate_mesh(const Mesh<Real>& m) {
+    const int npe = m.npe();
+    const int64_t n = m.num_nodes();
+    if (m.conn.size() % size_t(npe) != 0)
+        throw MeshError("connectivity length not a multiple of nodes per element");
+    const int64_t E = m.num_elements();
+    for (int64_t e = 0; e < E; ++e)
+        for (int a = 0; a < npe; ++a) {
+            const int32_t c = m.conn[size_t(e * npe + a)];
+            if (c < 0 || c >= n) throw MeshError("connectivity index " + std::to_string(c) + " out of range", long(e));
+        }
+    const Shape<Real> D(m.kind);
+    int64_t bad = -1;
+#pragma omp parallel for schedule(static) reduction(max : bad)
+    for (int64_t e = 0; e < E; ++e) {
+        V3<Real> x[8];
+        for (int a = 0; a < npe; ++a) x[a] = m.node(m.conn[size_t(e * npe + a)]);
+        Jac<Real> j;
+        if (!jacobian0(x, D, j) || !(volume0(j, m.kind) > Real(0))) bad = std::max<int64_t>(bad, E - e);
+    }
+    if (bad >= 0) throw MeshError("non-positive reference Jacobian determinant", long(E - bad));
+}
+
+// NodeElementAdjacency::build (mesh.hpp:299-320): counting sort over elements
+// in ascending order, so each node's row lists its elements ascending.
+struct Adjacency {
+    std::vector<int64_t> offsets;  // N+1
+    std::vector<int64_t> elem;     // npe*E
+    std::vector<int32_t> local;    // npe*E
+};
+
+inline Adjacency build_adjacency(const std::vector<int32_t>& conn, int64_t n, int npe) {
+    Adjacency adj;
+    std::vector<int64_t> count(size_t(n), 0);
+    for (int32_t idx : conn) ++count[size_t(idx)];
+    adj.offsets.assign(size_t(n) + 1, 0);
+    for (int64_t i = 0; i < n; ++i) adj.offsets[size_t(i + 1)] = adj.offsets[size_t(i)] + count[size_t(i)];
+    adj.elem.resize(conn.size());
+    adj.local.resize(conn.size());
+    std::vector<int64_t> cursor(adj.offsets.begin(), adj.offsets.end() - 1);
+    const int64_t E = int64_t(conn.size()) / npe;
+    for (int64_t e = 0; e < E; ++e)
+        for (int a = 0; a < npe; ++a) {
+            const int64_t p = cursor[size_t(conn[size_t(e * npe + a)])]++;
+            adj.elem[size_t(p)] = e;
+            adj.local[size_t(p)] = a;
+        }
+    return adj;
+}
+
+// ---------------------------------------------------------------- precompute
+
+// Hourglass shape vectors (precompute.hpp:136-165).
+template <class Real>
+inline void hourglass_vectors(const V3<Real>* x, const Shape<Real>& D, const Real jinv[3][3], Real gamma[4][8]) {
+    Real base[4][8];
+    for (int a = 0; a < 8; ++a) {
+        const int xi = kCornerSign[a][0], eta = kCornerSign[a][1], zeta = kCornerSign[a][2];
+        base[0][a] = Real(eta * zeta);
+        base[1][a] = Real(xi * zeta);
+        base[2][a] = Real(xi * eta);
+        base[3][a] = Real(xi * eta * zeta);
+    }
+    Real b[3][8];
+    for (int j = 0; j < 3; ++j)
+        for (int a = 0; a < 8; ++a)
+            b[j][a] = jinv[j][0] * D.d[0][a] + jinv[j][1] * D.d[1][a] + jinv[j][2] * D.d[2][a];
+    for (int m = 0; m < 4; ++m) {
+        Real hx[3] = {Real(0), Real(0), Real(0)};
+        for (int j = 0; j < 3; ++j)
+            for (int a = 0; a < 8; ++a) {
+                const Real c = j == 0 ? x[a].x : (j == 1 ? x[a].y : x[a].z);
+                hx[j] += base[m][a] * c;
+            }
+        for (int a = 0; a < 8; ++a)
+            gamma[m][a] = base[m][a] - (hx[0] * b[0][a] + hx[1] * b[1][a] + hx[2] * b[2][a]);
+    }
+}
+
+// The hot-field record of build_element_constants (precompute.hpp:206-255):
+// G_k from J0inv columns, m = tr(S G_k), I_m = 2 V0 J0inv^T K J0inv.
+template <class Real>
+inline bool element_record(const V3<Real>* x, const Shape<Real>& D, const Material<Real>& mat,
+                           const V3<Real>& fa_unit, const V3<Real>& fb_unit, Real c_hg,
+                           const ConstLayout& L, Real* out) {
+    Jac<Real> j;
+    if (!jacobian0(x, D, j)) return false;
+    const Real v0 = volume0(j, D.kind);
+    if (!(v0 > Real(0))) return false;
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) out[L.J0 + 3 * r + c] = j.J[r][c];
+    out[L.det] = j.det;
+    out[L.V0] = v0;
+    const V3<Real> q0{j.Jinv[0][0], j.Jinv[1][0], j.Jinv[2][0]};
+    const V3<Real> q1{j.Jinv[0][1], j.Jinv[1][1], j.Jinv[2][1]};
+    const V3<Real> q2{j.Jinv[0][2], j.Jinv[1][2], j.Jinv[2][2]};
+    const Sym<Real> G[6] = {outer(q0), outer(q1), outer(q2), sym_outer(q0, q1), sym_outer(q0, q2), sym_outer(q1, q2)};
+    Real m1[6];
+    for (int k = 0; k < 6; ++k) m1[k] = out[L.m1 + k] = trace(G[k]);
+    const Real two_v0 = 2 * v0;
+    const Sym<Real> ident{{Real(1), Real(1), Real(1), Real(0), Real(0), Real(0)}};
+    const Sym<Real> I1m = scaled(two_v0, congruence(j.Jinv, ident));
+    for (int k = 0; k < 6; ++k) out[L.I1m + k] = I1m.v[k];
+    if (mat.needs_i2()) {
+        // M2 = (m1 m1^T - W) / 2 with W[p][q] = tr(G_p G_q) (precompute.hpp:67-84).
+        for (int p = 0; p < 6; ++p)
+            for (int q = p; q < 6; ++q)
+                out[L.M2 + sym6_index(p, q)] = (m1[p] * m1[q] - ddot(G[p], G[q])) / 2;
+        // I2m_k = 2 V0 J0inv^T (tr(G_k) I - G_k) J0inv (precompute.hpp:104-115).
+        for (int k = 0; k < 6; ++k) {
+            const Real tr = trace(G[k]);
+            const Sym<Real> ker{{tr - G[k].v[0], tr - G[k].v[1], tr - G[k].v[2], -G[k].v[3], -G[k].v[4], -G[k].v[5]}};
+            const Sym<Real> t = scaled(two_v0, congruence(j.Jinv, ker));
+            for (int c = 0; c < 6; ++c) out[L.I2m + 6 * k + c] = t.v[c];
+        }
+    }
+    if (mat.needs_i4()) {
+        const Sym<Real> A = outer(fa_unit);
+        for (int k = 0; k < 6; ++k) out[L.m4 + k] = ddot(A, G[k]);
+        const Sym<Real> t = scaled(two_v0, congruence(j.Jinv, A));
+        for (int c = 0; c < 6; ++c) out[L.I4m + c] = t.v[c];
+    }
+    if (mat.needs_i6()) {
+        const Sym<Real> B = outer(fb_unit);
+        for (int k = 0; k < 6; ++k) out[L.m6 + k] = ddot(B, G[k]);
+        const Sym<Real> t = scaled(two_v0, congruence(j.Jinv, B));
+        for (int c = 0; c < 6; ++c) out[L.I6m + c] = t.v[c];
+    }
+    if (D.kind == DJG_H8) {
+        Real gamma[4][8];
+        hourglass_vectors(x, D, j.Jinv, gamma);
+        out[L.khg] = c_hg * mat.kappa * std::cbrt(v0);
+        for (int m = 0; m < 4; ++m)
+            for (int a = 0; a < 8; ++a) out[L.gamma + 8 * m + a] = gamma[m][a];
+    }
+    return true;
+}
+
+// Characteristic length (precompute.hpp:303-319) and critical dt (:323-331).
+template <class Real>
+inline Real tri_area(V3<Real> a, V3<Real> b, V3<Real> c) {
+    const V3<Real> u{b.x - a.x, b.y - a.y, b.z - a.z}, v{c.x - a.x, c.y - a.y, c.z - a.z};
+    const V3<Real> w{u.y * v.z - u.z * v.y, u.z * v.x - u.x * v.z, u.x * v.y - u.y * v.x};
+    return std::sqrt(w.x * w.x + w.y * w.y + w.z * w.z) / 2;
+}
+
+template <class Real>
+inline Real char_length(const V3<Real>* x, int kind, Real v0) {
+    Real a_max = 0;
+    if (kind == DJG_T4) {
+        static constexpr int f[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
+        for (auto& t : f) a_max = std::max(a_max, tri_area(x[t[0]], x[t[1]], x[t[2]]));
+        return 3 * v0 / a_max;
+    }
+    static constexpr int f[6][4] = {{0, 3, 2, 1}, {4, 5, 6, 7}, {0, 1, 5, 4}, {1, 2, 6, 5}, {2, 3, 7, 6}, {3, 0, 4, 7}};
+    for (auto& q : f)
+        a_max = std::max(a_max, tri_area(x[q[0]], x[q[1]], x[q[2]]) + tri_area(x[q[0]], x[q[2]], x[q[3]]));
+    return v0 / a_max;
+}
+
+// ---------------------------------------------------------------- problem
+
+template <class Real>
+struct Problem {
+    Mesh<Real> mesh;
+    Material<Real> mat;
+    Adjacency adj;
+    int nconst = 0;
+    std::vector<Real> consts;          // E*nconst
+    std::vector<Real> mass;            // N
+    std::vector<Real> c1;              // N
+    std::vector<uint8_t> massless;     // N
+    std::vector<uint8_t> dof_kind;     // 3N
+    std::vector<Real> dof_target;      // 3N
+    std::vector<Real> dof_t_total;     // 3N
+    Real dt = 0, crit_dt = 0, alpha = 0, c2 = 0, c3 = 0, ramp_t_total = 0, c_wave = 0;
+    int policy = DJG_ABORT;
+};
+
+template <class Real>
+inline void bounding_box(const Mesh<Real>& m, Real lo[3], Real hi[3]) {
+    for (int i = 0; i < 3; ++i) {
+        lo[i] = std::numeric_limits<Real>::max();
+        hi[i] = std::numeric_limits<Real>::lowest();
+    }
+    const int64_t n = m.num_nodes();
+    for (int64_t k = 0; k < n; ++k)
+        for (int i = 0; i < 3; ++i) {
+            lo[i] = std::min(lo[i], m.nodes[size_t(3 * k + i)]);
+            hi[i] = std::max(hi[i], m.nodes[size_t(3 * k + i)]);
+        }
+}
+
+// select_plane_nodes (config.hpp:31-42)
+template <class Real>
+inline std::vector<int32_t> plane_nodes(const Mesh<Real>& m, int axis, bool is_max, const Real lo[3], const Real hi[3]) {
+    const Real value = is_max ? hi[axis] : lo[axis];
+    const Real extent = hi[axis] - lo[axis];
+    const Real eps = Real(1e-9) * (extent > Real(0) ? extent : Real(1));
+    std::vector<int32_t> out;
+    const int64_t n = m.num_nodes();
+    for (int64_t k = 0; k < n; ++k)
+        if (std::abs(m.nodes[size_t(3 * k + axis)] - value) <= eps) out.push_back(int32_t(k));
+    return out;
+}
+
+template <class Real>
+inline Problem<Real> build_problem(const djg_scenario_spec& s, int threads) {
+#ifdef _OPENMP
+    if (threads > 0) omp_set_num_threads(threads);
+#else
+    (void)threads;
+#endif
+    if (s.kind != DJG_T4 && s.kind != DJG_H8) throw ConfigError("unknown element kind");
+    Problem<Real> P;
+    P.policy = s.policy;
+    if (s.nodes == nullptr) {
+        P.mesh = generate_box<Real>(s.extent, s.divisions, s.kind);
+    } else {
+        if (s.num_nodes < 0 || s.num_elements < 0 || (s.num_elements > 0 && !s.conn))
+            throw ConfigError("explicit mesh needs nodes and connectivity");
+        P.mesh.kind = s.kind;
+        P.mesh.nodes.resize(size_t(3 * s.num_nodes));
+        for (int64_t i = 0; i < 3 * s.num_nodes; ++i) P.mesh.nodes[size_t(i)] = Real(s.nodes[i]);
+        P.mesh.conn.assign(s.conn, s.conn + s.num_elements * npe_of(s.kind));
+    }
+    validate_mesh(P.mesh);
+    P.mat = Material<Real>::from(s.material);
+    const int npe = P.mesh.npe();
+    const int64_t N = P.mesh.num_nodes(), E = P.mesh.num_elements();
+    const ConstLayout L(s.kind, P.mat.model);
+    P.nconst = L.count;
+
+    // DjModel::build -> build_constants (djtled_force.hpp:145-157, precompute.hpp:258-272)
+    V3<Real> fa{0, 0, 0}, fb{0, 0, 0};
+    if (P.mat.needs_i4()) fa = Material<Real>::unit(P.mat.fa);
+    if (P.mat.needs_i6()) fb = Material<Real>::unit(P.mat.fb);
+    const Real c_hg = Real(s.c_hg);
+    const Shape<Real> D(s.kind);
+    P.consts.assign(size_t(E) * size_t(L.count), Real(0));
+    int64_t bad = -1;
+#pragma omp parallel for schedule(static) reduction(max : bad)
+    for (int64_t e = 0; e < E; ++e) {
+        V3<Real> x[8];
+        for (int a = 0; a < npe; ++a) x[a] = P.mesh.node(P.mesh.conn[size_t(e * npe + a)]);
+        if (!element_record(x, D, P.mat, fa, fb, c_hg, L, P.consts.data() + size_t(e) * L.count))
+            bad = std::max<int64_t>(bad, E - e);
+    }
+    if (bad >= 0) throw MeshError("non-positive reference Jacobian determinant", long(E - bad));
+
+    P.adj = build_adjacency(P.mesh.conn, N, npe);
+
+    // lump_mass (precompute.hpp:275-287): each node sums the shares of its
+    // elements in ascending element order -- the order of the reference's
+    // serial element loop -- so the CSR row gives the same bits in parallel.
+    P.mass.assign(size_t(N), Real(0));
+#pragma omp parallel for schedule(static)
+    for (int64_t n = 0; n < N; ++n) {
+        Real acc = Real(0);
+        for (int64_t p = P.adj.offsets[size_t(n)]; p < P.adj.offsets[size_t(n + 1)]; ++p) {
+            const int64_t e = P.adj.elem[size_t(p)];
+            acc += P.mat.rho * P.consts[size_t(e) * L.count + L.V0] / Real(npe);
+        }
+        P.mass[size_t(n)] = acc;
+    }
+
+    // critical_dt (precompute.hpp:323-331); min is order independent.
+    P.c_wave = wave_speed(P.mat);
+    Real l_min = std::numeric_limits<Real>::max();
+#pragma omp parallel
+    {
+        Real local = std::numeric_limits<Real>::max();
+#pragma omp for schedule(static) nowait
+        for (int64_t e = 0; e < E; ++e) {
+            V3<Real> x[8];
+            for (int a = 0; a < npe; ++a) x[a] = P.mesh.node(P.mesh.conn[size_t(e * npe + a)]);
+            local = std::min(local, char_length(x, s.kind, P.consts[size_t(e) * L.count + L.V0]));
+        }
+#pragma omp critical
+        l_min = std::min(l_min, local);
+    }
+    if (!(l_min > Real(0))) throw MeshError("degenerate element with zero characteristic length");
+    P.crit_dt = l_min / P.c_wave;
+    P.dt = s.dt > 0 ? Real(s.dt) : Real(s.safety) * P.crit_dt;
+    if (!(P.dt > Real(0))) throw ConfigError("time step must be positive");
+
+    // relaxation_alpha (solver.hpp:330-339)
+    Real lo[3], hi[3];
+    bounding_box(P.mesh, lo, hi);
+    if (s.alpha_mode == 0) {
+        const Real mu = P.mat.shear_modulus();
+        const Real e_mod = 9 * P.mat.kappa * mu / (3 * P.mat.kappa + mu);
+        const Real c_bar = std::sqrt(e_mod / P.mat.rho);
+        const Real l = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]});
+        if (!(l > Real(0))) throw ConfigError("mesh has zero extent");
+        P.alpha = Real(M_PI) * c_bar / l;
+    } else {
+        P.alpha = Real(s.alpha);
+    }
+
+    // Boundary conditions -> DofConstraints (solver.hpp:18-33, mesh.hpp:55-70).
+    P.dof_kind.assign(size_t(3 * N), uint8_t(DJG_FREE));
+    P.dof_target.assign(size_t(3 * N), Real(0));
+    P.dof_t_total.assign(size_t(3 * N), Real(1));
+    auto claim = [&](int64_t node, int axis) -> uint8_t& {
+        if (node < 0 || node >= N) throw ConfigError("boundary condition references invalid node");
+        if (axis < 0 || axis > 2) throw ConfigError("boundary condition axis out of range");
+        uint8_t& k = P.dof_kind[size_t(3 * node + axis)];
+        if (k != DJG_FREE)
+            throw ConfigError("node " + std::to_string(node) + " axis " + std::to_string(axis) +
+                              " appears in more than one boundary condition");
+        return k;
+    };
+    auto prescribe = [&](int64_t node, int axis, Real target, Real t_total) {
+        if (!(t_total > Real(0))) throw ConfigError("ramp duration must be positive");
+        claim(node, axis) = DJG_PRESCRIBED;
+        P.dof_target[size_t(3 * node + axis)] = target;
+        P.dof_t_total[size_t(3 * node + axis)] = t_total;
+    };
+    if (s.bc_mode == 1) {
+        const auto bottom = plane_nodes(P.mesh, 2, false, lo, hi);
+        const auto top = plane_nodes(P.mesh, 2, true, lo, hi);
+        for (int32_t n : bottom) {
+            if (s.fix_all_axes) {
+                claim(n, 0) = DJG_FIXED;
+                claim(n, 1) = DJG_FIXED;
+            }
+            claim(n, 2) = DJG_FIXED;
+        }
+        if (top.empty()) throw ConfigError("prescribe rule selects no nodes");
+        P.ramp_t_total = P.dt * Real(s.ramp_steps);
+        for (int32_t n : top) prescribe(n, 2, Real(s.target), P.ramp_t_total);
+    } else if (s.bc_mode == 2) {
+        for (int64_t i = 0; i < s.n_fixed; ++i) claim(s.fixed_node[i], s.fixed_axis[i]) = DJG_FIXED;
+        for (int64_t i = 0; i < s.n_prescribed; ++i)
+            prescribe(s.presc_node[i], s.presc_axis[i], Real(s.presc_target[i]), Real(s.presc_t_total[i]));
+    } else if (s.bc_mode != 0) {
+        throw ConfigError("unknown boundary condition mode");
+    }
+
+    // UpdateCoeffs::build (solver.hpp:70-86)
+    const Real denom = Real(1) + P.alpha * P.dt / 2;
+    P.c2 = Real(2) / denom;
+    P.c3 = -(Real(1) - P.alpha * P.dt / 2) / denom;
+    P.c1.assign(size_t(N), Real(0));
+    P.massless.assign(size_t(N), 0);
+    for (int64_t n = 0; n < N; ++n) {
+        if (P.mass[size_t(n)] > Real(0))
+            P.c1[size_t(n)] = P.dt * P.dt / (P.mass[size_t(n)] * denom);
+        else
+            P.massless[size_t(n)] = 1;
+    }
+    return P;
+}
+
+}  // namespace djg

@@ -1,0 +1,177 @@
+// C-ABI over the host problem builder (include/djg_host.h).
+#include <cstring>
+#include <memory>
+#include <string>
+#include <variant>
+
+#include "djg_host.h"
+#include "problem.hpp"
+
+namespace {
+
+thread_local std::string g_error;
+
+template <class Real>
+void copy_out(const djg::Problem<Real>& P, const djg_image_ptrs& o) {
+    auto put = [](void* dst, const auto& v) {
+        if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+    };
+    put(o.nodes, P.mesh.nodes);
+    put(o.conn, P.mesh.conn);
+    put(o.csr_offsets, P.adj.offsets);
+    put(o.csr_elem, P.adj.elem);
+    put(o.csr_local, P.adj.local);
+    put(o.consts, P.consts);
+    put(o.mass, P.mass);
+    put(o.c1, P.c1);
+    put(o.massless, P.massless);
+    put(o.dof_kind, P.dof_kind);
+    put(o.dof_target, P.dof_target);
+    put(o.dof_t_total, P.dof_t_total);
+}
+
+template <class Real>
+void scalars_of(const djg::Problem<Real>& P, djg_image_scalars& s) {
+    s.num_nodes = P.mesh.num_nodes();
+    s.num_elements = P.mesh.num_elements();
+    s.npe = P.mesh.npe();
+    s.nconst = P.nconst;
+    s.dt = double(P.dt);
+    s.critical_dt = double(P.crit_dt);
+    s.alpha = double(P.alpha);
+    s.c2 = double(P.c2);
+    s.c3 = double(P.c3);
+    s.ramp_t_total = double(P.ramp_t_total);
+    s.wave_speed = double(P.c_wave);
+}
+
+template <class Real>
+void desc_of(const djg::Problem<Real>& P, int32_t device, djg_desc& d) {
+    std::memset(&d, 0, sizeof(d));
+    d.precision = int32_t(sizeof(Real));
+    d.kind = P.mesh.kind;
+    d.num_nodes = P.mesh.num_nodes();
+    d.num_elements = P.mesh.num_elements();
+    d.conn = P.mesh.conn.data();
+    d.consts = P.consts.data();
+    d.nconst = P.nconst;
+    d.inversion_policy = P.policy;
+    d.csr_offsets = P.adj.offsets.data();
+    d.csr_elem = P.adj.elem.data();
+    d.csr_local = P.adj.local.data();
+    d.dof_kind = P.dof_kind.data();
+    d.dof_target = P.dof_target.data();
+    d.dof_t_total = P.dof_t_total.data();
+    d.c1 = P.c1.data();
+    d.massless = P.massless.data();
+    d.c2 = double(P.c2);
+    d.c3 = double(P.c3);
+    d.dt = double(P.dt);
+    d.material.model = P.mat.model;
+    d.material.mu = double(P.mat.mu);
+    d.material.kappa = double(P.mat.kappa);
+    d.material.rho = double(P.mat.rho);
+    d.material.eta_a = double(P.mat.eta_a);
+    d.material.eta_b = double(P.mat.eta_b);
+    d.material.c10 = double(P.mat.c10);
+    d.material.c01 = double(P.mat.c01);
+    d.device = device;
+}
+
+}  // namespace
+
+struct djg_scenario {
+    std::variant<djg::Problem<float>, djg::Problem<double>> p;
+};
+
+extern "C" {
+
+void djg_bench_material(int32_t model, djg_material_params* m) {
+    // bench_material (bench.hpp:12-25): mu 6567, kappa 326210, rho 1060,
+    // fibres along x (and y), eta = 2 mu, MR c10 = mu/2, c01 = 3000.
+    std::memset(m, 0, sizeof(*m));
+    m->model = model;
+    m->mu = 6567.0;
+    m->kappa = 326210.0;
+    m->rho = 1060.0;
+    m->fibre_a[0] = 1.0;
+    m->fibre_b[1] = 1.0;
+    if (model == DJG_TI || model == DJG_OT) m->eta_a = 2 * 6567.0;
+    if (model == DJG_OT) m->eta_b = 2 * 6567.0;
+    if (model == DJG_MR) {
+        m->mu = 0.0;
+        m->c10 = 6567.0 / 2;
+        m->c01 = 3000.0;
+    }
+}
+
+void djg_spec_default_box(djg_scenario_spec* s, int32_t precision, int32_t kind, int32_t model,
+                          int32_t divisions, int64_t ramp_steps) {
+    std::memset(s, 0, sizeof(*s));
+    s->precision = precision;
+    s->kind = kind;
+    for (int i = 0; i < 3; ++i) {
+        s->divisions[i] = divisions;
+        s->extent[i] = 1.0;
+    }
+    djg_bench_material(model, &s->material);
+    s->c_hg = 0.1;
+    s->bc_mode = 1;
+    s->fix_all_axes = 1;
+    s->target = -0.2;
+    s->ramp_steps = ramp_steps;
+    s->safety = 0.5;
+    s->alpha_mode = 0;
+    s->policy = DJG_ABORT;
+}
+
+const char* djg_scenario_error(void) { return g_error.c_str(); }
+
+int djg_scenario_build(const djg_scenario_spec* spec, int32_t threads, djg_scenario** out) {
+    if (!spec || !out) {
+        g_error = "null argument";
+        return DJG_E_CONFIG;
+    }
+    *out = nullptr;
+    try {
+        auto sc = std::make_unique<djg_scenario>();
+        if (spec->precision == 4)
+            sc->p = djg::build_problem<float>(*spec, threads);
+        else if (spec->precision == 8)
+            sc->p = djg::build_problem<double>(*spec, threads);
+        else
+            throw djg::ConfigError("precision must be 4 or 8");
+        *out = sc.release();
+        return DJG_OK;
+    } catch (const djg::ConfigError& e) {
+        g_error = e.what();
+    } catch (const djg::MeshError& e) {
+        g_error = e.what();
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return DJG_E_INTERNAL;
+    }
+    return DJG_E_CONFIG;
+}
+
+void djg_scenario_free(djg_scenario* sc) { delete sc; }
+
+int djg_scenario_scalars(const djg_scenario* sc, djg_image_scalars* out) {
+    if (!sc || !out) return DJG_E_CONFIG;
+    std::visit([&](const auto& P) { scalars_of(P, *out); }, sc->p);
+    return DJG_OK;
+}
+
+int djg_scenario_image(const djg_scenario* sc, const djg_image_ptrs* out) {
+    if (!sc || !out) return DJG_E_CONFIG;
+    std::visit([&](const auto& P) { copy_out(P, *out); }, sc->p);
+    return DJG_OK;
+}
+
+int djg_scenario_desc(const djg_scenario* sc, int32_t device, djg_desc* out) {
+    if (!sc || !out) return DJG_E_CONFIG;
+    std::visit([&](const auto& P) { desc_of(P, device, *out); }, sc->p);
+    return DJG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,218 @@
+"""GPU parity: the sm_100a engine (through libdjg's C-ABI) against the CPU
+oracle on the same seeded inputs.
+
+Tolerances: max|du| / max|u| <= 1e-5 in float,
+<= 1e-10 in double, integers (CSR, slot map) exact. The engine is built with
+--fmad=false and mirrors the reference's evaluation order, so the observed
+differences are far below the gates (only cbrt's last ulp can differ).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_2106_14189_b200 import (GpuDjEngine, Scenario, SimulationError, box_spec, config_spec, material,
+                                   mesh_spec)
+from paper_2106_14189_b200 import _abi as A
+
+pytestmark = pytest.mark.gpu
+
+TOL = {4: 1e-5, 8: 1e-10}
+
+
+def run_gpu(spec, steps, **kw):
+    sc = Scenario(spec)
+    with GpuDjEngine(sc, **kw) as eng:
+        rep = eng.step(steps, raise_on_failure=False)
+        u, up, step = eng.get_state()
+    return u, up, rep
+
+
+def check_run(spec, steps, tol=None):
+    u, up, rep = run_gpu(spec, steps)
+    ur, upr, rr = oracle.run(spec, steps, "oracle")
+    assert rep.step == rr["step"] and rep.status == rr["status"], (rep, rr)
+    tol = TOL[spec.precision] if tol is None else tol
+    e1, e2 = oracle.rel_max_err(u, ur), oracle.rel_max_err(up, upr)
+    assert e1 <= tol and e2 <= tol, (e1, e2)
+    assert np.max(np.abs(ur)) > 0
+    return e1
+
+
+@pytest.mark.parametrize("precision", [4, 8])
+def test_cfg1_t4_nh_2000_steps(precision):
+    """BASELINE configs[0]: unit cube T4 (10,368 el) NH, 20% compression."""
+    err = check_run(config_spec("cfg1", precision=precision), 2000)
+    print(f"cfg1 f{8 * precision}: {err:.3e}")
+
+
+@pytest.mark.parametrize("precision", [4, 8])
+def test_cfg2_h8_nh_hourglass_2000_steps(precision):
+    """BASELINE configs[1]: unit cube H8 (10,648 el) NH + hourglass control."""
+    err = check_run(config_spec("cfg2", precision=precision), 2000)
+    print(f"cfg2 f{8 * precision}: {err:.3e}")
+
+
+@pytest.mark.parametrize("precision", [4, 8])
+@pytest.mark.parametrize("kind", ["T4", "H8"])
+@pytest.mark.parametrize("model", ["NH", "TI", "OT", "MR"])
+def test_materials_small(kind, model, precision):
+    check_run(box_spec(kind=kind, model=model, divisions=4, precision=precision, ramp_steps=300), 300)
+
+
+@pytest.mark.parametrize("precision", [4, 8])
+def test_cfg4_shape_h8_ti(precision):
+    """configs[3] material/element on a smaller cube (d=16)."""
+    check_run(box_spec(kind="H8", model="TI", divisions=16, precision=precision, ramp_steps=400), 400)
+
+
+@pytest.mark.slow
+def test_cfg3_first_200_steps():
+    """configs[2] at full size (2,058,000 T4): first 200 steps vs the oracle."""
+    check_run(config_spec("cfg3", precision=4, ramp_steps=1100), 200)
+
+
+@pytest.mark.slow
+def test_cfg4_first_100_steps():
+    """configs[3] at full size (1,000,000 H8 TI): first 100 steps vs the oracle."""
+    check_run(config_spec("cfg4", precision=4, ramp_steps=1100), 100)
+
+
+@pytest.mark.parametrize("precision", [4, 8])
+def test_assemble_random_state(precision):
+    """Engine::assemble at a random admissible state equals the oracle's."""
+    spec = box_spec(kind="T4", model="MR", divisions=(3, 4, 5), precision=precision, extent=(0.1, 0.1, 0.1))
+    sc = Scenario(spec)
+    rng = np.random.default_rng(13)
+    u = rng.uniform(-0.003, 0.003, 3 * sc.num_nodes)
+    with GpuDjEngine(sc) as eng:
+        f, st = eng.assemble(u)
+    fr, sr = oracle.assemble(spec, u)
+    assert st["first_inverted"] == -1 and sr["first_inverted"] == -1
+    assert oracle.rel_max_err(f, fr) <= TOL[precision] * 1e-2
+
+
+def test_slot_map_is_a_bijection_consistent_with_csr():
+    spec = box_spec(kind="H8", model="NH", divisions=(5, 3, 4))
+    sc = Scenario(spec)
+    img = sc.image()
+    with GpuDjEngine(sc) as eng:
+        slots = eng.slot_map()
+        info = eng.info()
+    npe = 8
+    assert len(np.unique(slots)) == slots.size
+    assert slots.min() >= 0 and slots.max() < info["slot_capacity"]
+    off, ce, cl = img["csr_offsets"], img["csr_elem"], img["csr_local"]
+    N = sc.num_nodes
+    for n in range(N):
+        for k, p in enumerate(range(off[n], off[n + 1])):
+            base = 32 * k + (n % 32)
+            pos = slots[ce[p] * npe + cl[p]]
+            assert (pos - base) % 32 == 0  # slot k of node n in lane n%32 of its slice
+
+
+def test_rest_stays_identically_zero():
+    spec = box_spec(kind="T4", divisions=2, extent=(0.1, 0.1, 0.1), precision=8)
+    spec.c.bc_mode = 0
+    u, up, rep = run_gpu(spec, 20)
+    assert rep.status == 0 and rep.step == 20
+    assert np.all(u == 0) and np.all(up == 0)
+
+
+def test_fixed_and_ramp_exact_every_frame():
+    """test_solver.cpp:144-166: fixed DOFs exactly 0, ramped DOFs exactly
+    min(dt*s/T, 1)*target at every one of 200 frames."""
+    spec = box_spec(kind="T4", divisions=2, extent=(0.1, 0.1, 0.1), precision=8, target=0.03, alpha=50.0)
+    sc = Scenario(spec)
+    img = sc.image()
+    dt = sc.dt
+    T = sc.scalars["ramp_t_total"]
+    kinds = img["dof_kind"]
+    with GpuDjEngine(sc) as eng:
+        for s in range(1, 201):
+            eng.step(1)
+            u = eng.get_state()[0]
+            assert np.all(u[kinds == A.DJG_FIXED] == 0.0)
+            s_ = (dt * float(s)) / T
+            expect = (1.0 if s_ >= 1.0 else s_) * 0.03
+            assert np.all(u[kinds == A.DJG_PRESCRIBED] == expect)
+
+
+def test_deterministic_repeats():
+    spec = box_spec(kind="H8", model="NH", divisions=6, precision=4, ramp_steps=300)
+    a = run_gpu(spec, 300)[0]
+    b = run_gpu(spec, 300)[0]
+    c = run_gpu(spec, 300, flags=A.DJG_FLAG_NO_GRAPH)[0]
+    assert np.array_equal(a, b) and np.array_equal(a, c)
+
+
+def test_resume_from_state_is_bitwise():
+    """run_simulation's `initial` hook (solver.hpp:209-214)."""
+    spec = box_spec(kind="T4", model="TI", divisions=5, precision=4, ramp_steps=400)
+    sc = Scenario(spec)
+    with GpuDjEngine(sc) as eng:
+        eng.step(400)
+        u_full = eng.get_state()[0]
+        eng.set_state(None, None, 0)
+        eng.step(150)
+        u, up, st = eng.get_state()
+    with GpuDjEngine(sc) as eng2:
+        eng2.set_state(u, up, st)
+        eng2.step(250)
+        assert np.array_equal(eng2.get_state()[0], u_full)
+
+
+def test_external_force_matches_oracle():
+    spec = box_spec(kind="T4", divisions=3, precision=8, target=0.0, ramp_steps=100)
+    sc = Scenario(spec)
+    rng = np.random.default_rng(5)
+    r = rng.uniform(-1.0, 1.0, 3 * sc.num_nodes)
+    with GpuDjEngine(sc) as eng:
+        eng.set_external(r)
+        eng.step(100)
+        u = eng.get_state()[0]
+    ur, _, _ = oracle.run(spec, 100, "oracle", r_ext=r)
+    assert oracle.rel_max_err(u, ur) <= 1e-10
+
+
+def test_inversion_abort_reports_min_element_and_keeps_state():
+    """test_solver.cpp:214-241: the top face is driven through the bottom."""
+    sc0 = Scenario(box_spec(kind="T4", divisions=1, extent=(0.1, 0.1, 0.1), precision=8))
+    img = sc0.image()
+    nodes, conn = img["nodes"].reshape(-1, 3), img["conn"].reshape(-1, 4)
+    bottom = [n for n in range(8) if nodes[n, 2] == 0.0]
+    top = [n for n in range(8) if nodes[n, 2] > 0.0]
+    fixed = [(n, a) for n in bottom for a in range(3)]
+    presc = [(n, 2, -0.5, 1e-4) for n in top]
+    spec = mesh_spec(nodes, conn, kind="T4", precision=8, fixed=fixed, prescribed=presc, dt=1e-4, alpha=0.0)
+    u, up, rep = run_gpu(spec, 100)
+    ur, upr, rr = oracle.run(spec, 100, "oracle")
+    assert rep.status == A.DJG_E_INVERSION == rr["status"]
+    assert rep.first_inverted == rr["first_inverted"] >= 0
+    assert (rep.fail_step, rep.step) == (rr["fail_step"], rr["step"])
+    assert oracle.rel_max_err(u, ur) <= 1e-10 and oracle.rel_max_err(up, upr) <= 1e-10
+    with pytest.raises(SimulationError) as ei:
+        with GpuDjEngine(Scenario(spec)) as eng:
+            eng.step(100)
+    assert ei.value.kind == SimulationError.ElementInversion and ei.value.index == rr["first_inverted"]
+    # Skip-and-report keeps going and counts the inverted steps.
+    spec.c.policy = A.DJG_SKIP_AND_REPORT
+    _, _, rep2 = run_gpu(spec, 100)
+    _, _, rr2 = oracle.run(spec, 100, "oracle")
+    assert rep2.inverted_steps > 0
+    assert (rep2.status, rep2.step, rep2.inverted_steps) == (rr2["status"], rr2["step"], rr2["inverted_steps"])
+
+
+def test_divergence_detector():
+    """test_solver.cpp:192-212: dt = 10 x critical."""
+    sc0 = Scenario(box_spec(kind="T4", divisions=2, extent=(0.1, 0.1, 0.1), precision=8))
+    spec = box_spec(kind="T4", divisions=2, extent=(0.1, 0.1, 0.1), precision=8, target=0.05,
+                    dt=10 * sc0.scalars["critical_dt"], alpha=10.0, ramp_steps=1)
+    spec.c.ramp_steps = 1
+    u, up, rep = run_gpu(spec, 500)
+    ur, upr, rr = oracle.run(spec, 500, "oracle")
+    assert rep.status in (A.DJG_E_DIVERGENCE, A.DJG_E_INVERSION)
+    assert (rep.status, rep.step, rep.fail_step) == (rr["status"], rr["step"], rr["fail_step"])
+    with pytest.raises(SimulationError):
+        sc = Scenario(spec)
+        with GpuDjEngine(sc) as eng:
+            eng.step(500)

@@ -253,6 +253,7 @@ public:
         }
         ctrl_.alloc(sizeof(Ctrl));
         CK(cudaMallocHost(reinterpret_cast<void**>(&hctrl_), sizeof(Ctrl)));
+        CK(cudaMallocHost(reinterpret_cast<void**>(&hstart_), sizeof(Ctrl)));
 
         // Kernel arguments.
         ea_.E = E_;
@@ -292,6 +293,7 @@ public:
         if (graph_big_) cudaGraphExecDestroy(graph_big_);
         if (graph_one_) cudaGraphExecDestroy(graph_one_);
         if (hctrl_) cudaFreeHost(hctrl_);
+        if (hstart_) cudaFreeHost(hstart_);
         if (stream_) cudaStreamDestroy(stream_);
     }
 
@@ -414,11 +416,9 @@ public:
 
     void step_async(int64_t n) override {
         if (n < 0) throw DescError("nsteps must be >= 0");
-        // Fresh per-call accumulators: totals are read back by sync().
-        read_ctrl();
-        start_step_ = hctrl_->step;
-        start_total_inv_ = hctrl_->total_inv;
-        start_inv_steps_ = hctrl_->inv_steps;
+        // Snapshot the counters at the start of this call without blocking the
+        // host: sync() reports the difference.
+        CK(cudaMemcpyAsync(hstart_, ctrl_.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream_));
         if (flags_ & DJG_FLAG_NO_GRAPH) {
             for (int64_t i = 0; i < n; ++i) {
                 launch_element(stream_);
@@ -436,9 +436,9 @@ public:
         read_ctrl();
         djg_report r{};
         r.step = hctrl_->step;
-        r.steps_done = hctrl_->step - start_step_;
-        r.inverted_count = int64_t(hctrl_->total_inv - start_total_inv_);
-        r.inverted_steps = hctrl_->inv_steps - start_inv_steps_;
+        r.steps_done = hctrl_->step - hstart_->step;
+        r.inverted_count = int64_t(hctrl_->total_inv - hstart_->total_inv);
+        r.inverted_steps = hctrl_->inv_steps - hstart_->inv_steps;
         r.first_inverted = -1;
         r.fail_step = -1;
         r.status = hctrl_->halted;
@@ -492,10 +492,7 @@ public:
     }
 
     int profile(int64_t n, float* ms_e, float* ms_n, float* ms_t) override {
-        read_ctrl();
-        start_step_ = hctrl_->step;
-        start_total_inv_ = hctrl_->total_inv;
-        start_inv_steps_ = hctrl_->inv_steps;
+        CK(cudaMemcpyAsync(hstart_, ctrl_.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream_));
         std::vector<cudaEvent_t> ev(size_t(3 * n + 1));
         for (auto& e : ev) CK(cudaEventCreate(&e));
         CK(cudaEventRecord(ev[0], stream_));
@@ -561,8 +558,7 @@ private:
     ElemArgs<Real> ea_{};
     NodeArgs<Real> na_{};
     cudaGraphExec_t graph_big_ = nullptr, graph_one_ = nullptr;
-    int64_t start_step_ = 0, start_inv_steps_ = 0;
-    unsigned long long start_total_inv_ = 0;
+    Ctrl* hstart_ = nullptr;  // pinned snapshot taken at the start of a step call
 };
 
 }  // namespace

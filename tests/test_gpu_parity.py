@@ -110,12 +110,16 @@ def test_slot_map_is_a_bijection_consistent_with_csr():
             assert (pos - base) % 32 == 0  # slot k of node n in lane n%32 of its slice
 
 
-def test_rest_stays_identically_zero():
-    spec = box_spec(kind="T4", divisions=2, extent=(0.1, 0.1, 0.1), precision=8)
+def test_rest_stays_at_rest():
+    """test_solver.cpp:52-66 (no loads, from rest). Element forces at rest
+    cancel only to rounding (the reference itself drifts to ~1e-17 m here),
+    so the field must stay at that noise level, as the oracle's does."""
+    spec = box_spec(kind="T4", divisions=2, extent=(0.1, 0.1, 0.1), precision=8, alpha=0.0, dt=1e-4)
     spec.c.bc_mode = 0
     u, up, rep = run_gpu(spec, 20)
-    assert rep.status == 0 and rep.step == 20
-    assert np.all(u == 0) and np.all(up == 0)
+    ur, _, rr = oracle.run(spec, 20, "oracle")
+    assert rep.status == 0 and rep.step == 20 == rr["step"]
+    assert np.max(np.abs(u)) < 1e-15 and np.max(np.abs(ur)) < 1e-15
 
 
 def test_fixed_and_ramp_exact_every_frame():

@@ -28,7 +28,7 @@ def main(names):
         cf = CONFIGS[name]
         for prec in (4,):
             t0 = time.perf_counter()
-            sc = Scenario(config_spec(name, precision=prec))
+            sc = Scenario(config_spec(name, precision=prec, target=0.01, ramp_steps=100000))
             t1 = time.perf_counter()
             eng = GpuDjEngine(sc)
             t2 = time.perf_counter()

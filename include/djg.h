@@ -68,10 +68,10 @@ typedef struct djg_desc {
     const int64_t* csr_offsets; /* N+1, NodeElementAdjacency (mesh.hpp:299-320); */
     const int64_t* csr_elem;    /*   NULL -> rebuilt from conn by the same   */
     const int32_t* csr_local;   /*   ascending-element counting sort          */
-    const uint8_t* dof_kind;    /* 3N  DofConstraints::kind */
+    const uint8_t* dof_kind;    /* 3N  DofConstraints::kind (NULL: all free) */
     const void* dof_target;     /* 3N Real */
     const void* dof_t_total;    /* 3N Real */
-    const void* c1;             /* N Real  UpdateCoeffs::c1 */
+    const void* c1;             /* N Real  UpdateCoeffs::c1 (NULL: configure later) */
     const uint8_t* massless;    /* N       UpdateCoeffs::massless */
     double c2, c3;              /* UpdateCoeffs::c2/c3 (Real values) */
     double dt;                  /* Real value */
@@ -82,6 +82,44 @@ typedef struct djg_desc {
 
 /* Flags */
 #define DJG_FLAG_NO_GRAPH 1u    /* launch kernels one by one instead of CUDA graphs */
+
+/* DjEngine(mesh, material, c_hg) (solver.hpp:264-267) at the mesh level:
+ * the library runs the precompute (build_element_constants,
+ * precompute.hpp:206-255) and NodeElementAdjacency::build (mesh.hpp:299-320)
+ * itself, bit-identically to the reference, then uploads. The step data
+ * (masses, BCs, dt, alpha) follows with djg_configure_step, like the
+ * reference's run_simulation(engine, node_mass, bc, params). */
+typedef struct djg_mesh_desc {
+    int32_t precision;          /* sizeof(Real) */
+    int32_t kind;               /* djg_element_kind */
+    int64_t num_nodes;
+    int64_t num_elements;
+    const void* nodes;          /* 3N Reals, Mesh::nodes (mesh.hpp:23) */
+    const int32_t* conn;        /* npe*E, Mesh::conn */
+    djg_material_params material;
+    double c_hg;                /* hourglass coefficient (0.1 = default_hourglass_coefficient) */
+    int32_t inversion_policy;
+    int32_t device;
+    uint32_t flags;
+    int32_t threads;            /* host threads for the precompute (0 = all) */
+} djg_mesh_desc;
+int djg_create_from_mesh(const djg_mesh_desc* desc, djg_engine** out);
+
+/* UpdateCoeffs::build(node_mass, dt, alpha) (solver.hpp:70-86) +
+ * DofConstraints (solver.hpp:11-39): everything advance_step needs besides
+ * the engine. dof_kind NULL = all free. Real values widened to double. */
+typedef struct djg_step_desc {
+    const void* node_mass;      /* N Reals (lump_mass) */
+    const uint8_t* dof_kind;    /* 3N  DofConstraints::kind */
+    const void* dof_target;     /* 3N Reals */
+    const void* dof_t_total;    /* 3N Reals */
+    double dt;
+    double alpha;
+} djg_step_desc;
+int djg_configure_step(djg_engine* eng, const djg_step_desc* step);
+
+/* The InversionPolicy argument of Engine::assemble / RunParams::on_inversion. */
+int djg_set_policy(djg_engine* eng, int32_t policy);
 
 /* DjEngine ctor + UpdateCoeffs::build + DofConstraints::build
  * (solver.hpp:264-267, 70-86, 18-33). Validates shapes, uploads, builds the

@@ -115,6 +115,21 @@ class djg_desc(C.Structure):
     ]
 
 
+class djg_mesh_desc(C.Structure):
+    _fields_ = [
+        ("precision", C.c_int32), ("kind", C.c_int32), ("num_nodes", C.c_int64), ("num_elements", C.c_int64),
+        ("nodes", C.c_void_p), ("conn", C.c_void_p), ("material", djg_material_params), ("c_hg", C.c_double),
+        ("inversion_policy", C.c_int32), ("device", C.c_int32), ("flags", C.c_uint32), ("threads", C.c_int32),
+    ]
+
+
+class djg_step_desc(C.Structure):
+    _fields_ = [
+        ("node_mass", C.c_void_p), ("dof_kind", C.c_void_p), ("dof_target", C.c_void_p),
+        ("dof_t_total", C.c_void_p), ("dt", C.c_double), ("alpha", C.c_double),
+    ]
+
+
 class djg_engine_info(C.Structure):
     _fields_ = [
         ("num_nodes", C.c_int64), ("num_elements", C.c_int64), ("num_slots", C.c_int64),
@@ -144,6 +159,9 @@ _P = C.POINTER
 EXPORTS = [
     ("djg_const_count", C.c_int32, [C.c_int32, C.c_int32]),
     ("djg_create", C.c_int, [_P(djg_desc), _P(C.c_void_p)]),
+    ("djg_create_from_mesh", C.c_int, [_P(djg_mesh_desc), _P(C.c_void_p)]),
+    ("djg_configure_step", C.c_int, [C.c_void_p, _P(djg_step_desc)]),
+    ("djg_set_policy", C.c_int, [C.c_void_p, C.c_int32]),
     ("djg_destroy", None, [C.c_void_p]),
     ("djg_set_state", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]),
     ("djg_set_external", C.c_int, [C.c_void_p, C.c_void_p]),

@@ -85,6 +85,8 @@ public:
     virtual void info(djg_engine_info* out) = 0;
     virtual void slot_map(int32_t* out) = 0;
     virtual cudaStream_t stream() const = 0;
+    virtual void configure_step(const djg_step_desc& s) = 0;
+    virtual void set_policy(int policy) = 0;
 };
 
 template <class Real>
@@ -106,8 +108,8 @@ public:
         nplanes_ = (nconst_ + T::kPlane - 1) / T::kPlane;
         if (d.nconst != nconst_) throw DescError("nconst does not match djg_const_count(kind, model)");
         if (N_ < 1 || E_ < 1) throw DescError("mesh must have nodes and elements");
-        if (!d.conn || !d.consts || !d.dof_kind || !d.c1 || !d.massless)
-            throw DescError("descriptor is missing a required array");
+        if (!d.conn || !d.consts) throw DescError("descriptor is missing conn or consts");
+        if (!d.c1 != !d.massless) throw DescError("c1 and massless must be given together");
         if (E_ * npe_ > INT32_MAX || N_ > INT32_MAX) throw DescError("mesh too large for 32-bit slot indexing");
 
         CK(cudaSetDevice(d.device));
@@ -225,32 +227,9 @@ public:
         slicebase_.alloc(slice_base.size() * sizeof(int32_t));
         CK(cudaMemcpy(slicebase_.p, slice_base.data(), slicebase_.bytes, cudaMemcpyHostToDevice));
         c1_.alloc(size_t(N_) * sizeof(Real));
-        CK(cudaMemcpy(c1_.p, d.c1, c1_.bytes, cudaMemcpyHostToDevice));
-        {
-            std::vector<uint8_t> code(static_cast<size_t>(N_));
-            for (int64_t n = 0; n < N_; ++n) {
-                uint8_t c = 0;
-                for (int i = 0; i < 3; ++i) {
-                    const uint8_t k = d.dof_kind[3 * n + i];
-                    if (k > 2) throw DescError("invalid DOF kind");
-                    c |= uint8_t(k << (2 * i));
-                }
-                if (d.massless[n]) c |= 1u << 6;
-                code[size_t(n)] = c;
-            }
-            code_.alloc(code.size());
-            CK(cudaMemcpy(code_.p, code.data(), code_.bytes, cudaMemcpyHostToDevice));
-        }
+        code_.alloc(size_t(N_));
         target_.alloc(size_t(3 * N_) * sizeof(Real));
         tTotal_.alloc(size_t(3 * N_) * sizeof(Real));
-        if (d.dof_target) CK(cudaMemcpy(target_.p, d.dof_target, target_.bytes, cudaMemcpyHostToDevice));
-        else CK(cudaMemset(target_.p, 0, target_.bytes));
-        if (d.dof_t_total) {
-            CK(cudaMemcpy(tTotal_.p, d.dof_t_total, tTotal_.bytes, cudaMemcpyHostToDevice));
-        } else {
-            std::vector<Real> ones(size_t(3 * N_), Real(1));
-            CK(cudaMemcpy(tTotal_.p, ones.data(), tTotal_.bytes, cudaMemcpyHostToDevice));
-        }
         ctrl_.alloc(sizeof(Ctrl));
         CK(cudaMallocHost(reinterpret_cast<void**>(&hctrl_), sizeof(Ctrl)));
         CK(cudaMallocHost(reinterpret_cast<void**>(&hstart_), sizeof(Ctrl)));
@@ -280,13 +259,75 @@ public:
         na_.code = code_.as<unsigned char>();
         na_.target = target_.as<Real>();
         na_.t_total = tTotal_.as<Real>();
-        na_.c2 = Real(d.c2);
-        na_.c3 = Real(d.c3);
-        na_.dt = Real(d.dt);
         na_.policy = policy_;
         na_.ctrl = ctrl_.as<Ctrl>();
         na_.f_out = flat_.as<Real>();
+        if (d.c1) {
+            configure(static_cast<const Real*>(d.c1), d.massless, d.dof_kind, static_cast<const Real*>(d.dof_target),
+                      static_cast<const Real*>(d.dof_t_total), Real(d.c2), Real(d.c3), Real(d.dt));
+        }
         set_state(nullptr, nullptr, 0);
+    }
+
+    // Step data: UpdateCoeffs (c1 per node, massless, c2, c3), DofConstraints
+    // (kind / target / t_total per DOF) and dt (solver.hpp:18-39, 64-87).
+    void configure(const Real* c1, const uint8_t* massless, const uint8_t* dof_kind, const Real* target,
+                   const Real* t_total, Real c2, Real c3, Real dt) {
+        std::vector<uint8_t> code(static_cast<size_t>(N_));
+        for (int64_t n = 0; n < N_; ++n) {
+            uint8_t c = 0;
+            for (int i = 0; i < 3; ++i) {
+                const uint8_t k = dof_kind ? dof_kind[3 * n + i] : uint8_t(DJG_FREE);
+                if (k > 2) throw DescError("invalid DOF kind");
+                c |= uint8_t(k << (2 * i));
+            }
+            if (massless[n]) c |= 1u << 6;
+            code[size_t(n)] = c;
+        }
+        CK(cudaMemcpy(code_.p, code.data(), code_.bytes, cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(c1_.p, c1, c1_.bytes, cudaMemcpyHostToDevice));
+        if (target) {
+            CK(cudaMemcpy(target_.p, target, target_.bytes, cudaMemcpyHostToDevice));
+        } else {
+            CK(cudaMemset(target_.p, 0, target_.bytes));
+        }
+        if (t_total) {
+            CK(cudaMemcpy(tTotal_.p, t_total, tTotal_.bytes, cudaMemcpyHostToDevice));
+        } else {
+            std::vector<Real> ones(size_t(3 * N_), Real(1));
+            CK(cudaMemcpy(tTotal_.p, ones.data(), tTotal_.bytes, cudaMemcpyHostToDevice));
+        }
+        na_.c2 = c2;
+        na_.c3 = c3;
+        na_.dt = dt;
+        configured_ = true;
+        drop_graphs();
+    }
+
+    // UpdateCoeffs::build from node masses (solver.hpp:70-86), same Real ops.
+    void configure_step(const djg_step_desc& s) override {
+        if (!s.node_mass) throw DescError("node_mass is required");
+        const Real dt = Real(s.dt), alpha = Real(s.alpha);
+        if (!(dt > Real(0))) throw DescError("time step must be positive");
+        const Real* m = static_cast<const Real*>(s.node_mass);
+        const Real denom = Real(1) + alpha * dt / 2;
+        const Real c2 = Real(2) / denom;
+        const Real c3 = -(Real(1) - alpha * dt / 2) / denom;
+        std::vector<Real> c1(static_cast<size_t>(N_), Real(0));
+        std::vector<uint8_t> massless(static_cast<size_t>(N_), 0);
+        for (int64_t n = 0; n < N_; ++n) {
+            if (m[n] > Real(0)) c1[size_t(n)] = dt * dt / (m[n] * denom);
+            else massless[size_t(n)] = 1;
+        }
+        configure(c1.data(), massless.data(), s.dof_kind, static_cast<const Real*>(s.dof_target),
+                  static_cast<const Real*>(s.dof_t_total), c2, c3, dt);
+    }
+
+    void set_policy(int policy) override {
+        if (policy != DJG_ABORT && policy != DJG_SKIP_AND_REPORT) throw DescError("unknown inversion policy");
+        policy_ = policy;
+        na_.policy = policy;
+        drop_graphs();
     }
 
     ~Engine() override {
@@ -416,6 +457,7 @@ public:
 
     void step_async(int64_t n) override {
         if (n < 0) throw DescError("nsteps must be >= 0");
+        if (!configured_ && n > 0) throw DescError("step data not configured (djg_configure_step)");
         // Snapshot the counters at the start of this call without blocking the
         // host: sync() reports the difference.
         CK(cudaMemcpyAsync(hstart_, ctrl_.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream_));
@@ -492,6 +534,7 @@ public:
     }
 
     int profile(int64_t n, float* ms_e, float* ms_n, float* ms_t) override {
+        if (!configured_) throw DescError("step data not configured (djg_configure_step)");
         CK(cudaMemcpyAsync(hstart_, ctrl_.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream_));
         std::vector<cudaEvent_t> ev(size_t(3 * n + 1));
         for (auto& e : ev) CK(cudaEventCreate(&e));
@@ -559,6 +602,7 @@ private:
     NodeArgs<Real> na_{};
     cudaGraphExec_t graph_big_ = nullptr, graph_one_ = nullptr;
     Ctrl* hstart_ = nullptr;  // pinned snapshot taken at the start of a step call
+    bool configured_ = false;
 };
 
 }  // namespace
@@ -627,6 +671,10 @@ void djg_destroy(djg_engine* eng) { delete eng; }
 
 const char* djg_create_error(void) { return djg::g_create_error.c_str(); }
 
+// Not in the public headers: lets the host-side builder report its errors
+// through djg_create_error().
+void djg_internal_set_create_error(const char* msg) { djg::g_create_error = msg ? msg : ""; }
+
 int djg_set_state(djg_engine* eng, const void* u, const void* up, int64_t step) {
     return guarded(eng, [&](djg::EngineBase& e) {
         e.set_state(u, up, step);
@@ -671,6 +719,21 @@ int djg_assemble(djg_engine* eng, const void* u, void* f, djg_assemble_stats* st
 
 int djg_profile_steps(djg_engine* eng, int64_t n, float* ms_e, float* ms_n, float* ms_t) {
     return guarded(eng, [&](djg::EngineBase& e) { return e.profile(n, ms_e, ms_n, ms_t); });
+}
+
+int djg_configure_step(djg_engine* eng, const djg_step_desc* s) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        if (!s) throw djg::DescError("null step descriptor");
+        e.configure_step(*s);
+        return DJG_OK;
+    });
+}
+
+int djg_set_policy(djg_engine* eng, int32_t policy) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.set_policy(policy);
+        return DJG_OK;
+    });
 }
 
 int djg_get_info(djg_engine* eng, djg_engine_info* info) {

@@ -78,7 +78,59 @@ void desc_of(const djg::Problem<Real>& P, int32_t device, djg_desc& d) {
     d.device = device;
 }
 
+// DjEngine(mesh, material, c_hg) precompute (djtled_force.hpp:145-157) for
+// djg_create_from_mesh: hot-constant records + adjacency, then djg_create.
+template <class Real>
+int create_from_mesh(const djg_mesh_desc& m, djg_engine** out) {
+    djg::Mesh<Real> mesh;
+    mesh.kind = m.kind;
+    const Real* xn = static_cast<const Real*>(m.nodes);
+    if (!xn || !m.conn || m.num_nodes < 1 || m.num_elements < 1) throw djg::ConfigError("mesh needs nodes and elements");
+    mesh.nodes.assign(xn, xn + 3 * m.num_nodes);
+    mesh.conn.assign(m.conn, m.conn + m.num_elements * djg::npe_of(m.kind));
+#ifdef _OPENMP
+    if (m.threads > 0) omp_set_num_threads(m.threads);
+#endif
+    djg::validate_mesh(mesh);
+    const auto mat = djg::Material<Real>::from(m.material);
+    const djg::ConstLayout L(m.kind, mat.model);
+    const djg::Shape<Real> D(m.kind);
+    djg::V3<Real> fa{0, 0, 0}, fb{0, 0, 0};
+    if (mat.needs_i4()) fa = djg::Material<Real>::unit(mat.fa);
+    if (mat.needs_i6()) fb = djg::Material<Real>::unit(mat.fb);
+    const int npe = mesh.npe();
+    const int64_t E = mesh.num_elements();
+    std::vector<Real> consts(size_t(E) * size_t(L.count), Real(0));
+    const Real c_hg = Real(m.c_hg);
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < E; ++e) {
+        djg::V3<Real> x[8];
+        for (int a = 0; a < npe; ++a) x[a] = mesh.node(mesh.conn[size_t(e * npe + a)]);
+        djg::element_record(x, D, mat, fa, fb, c_hg, L, consts.data() + size_t(e) * L.count);
+    }
+    const djg::Adjacency adj = djg::build_adjacency(mesh.conn, mesh.num_nodes(), npe);
+    djg_desc d;
+    std::memset(&d, 0, sizeof(d));
+    d.precision = int32_t(sizeof(Real));
+    d.kind = m.kind;
+    d.num_nodes = mesh.num_nodes();
+    d.num_elements = E;
+    d.conn = mesh.conn.data();
+    d.consts = consts.data();
+    d.nconst = L.count;
+    d.inversion_policy = m.inversion_policy;
+    d.csr_offsets = adj.offsets.data();
+    d.csr_elem = adj.elem.data();
+    d.csr_local = adj.local.data();
+    d.material = m.material;
+    d.device = m.device;
+    d.flags = m.flags;
+    return djg_create(&d, out);
+}
+
 }  // namespace
+
+extern "C" void djg_internal_set_create_error(const char* msg);
 
 struct djg_scenario {
     std::variant<djg::Problem<float>, djg::Problem<double>> p;
@@ -155,6 +207,24 @@ int djg_scenario_build(const djg_scenario_spec* spec, int32_t threads, djg_scena
 }
 
 void djg_scenario_free(djg_scenario* sc) { delete sc; }
+
+int djg_create_from_mesh(const djg_mesh_desc* m, djg_engine** out) {
+    if (!m || !out) return DJG_E_CONFIG;
+    *out = nullptr;
+    try {
+        if (m->precision == 4) return create_from_mesh<float>(*m, out);
+        if (m->precision == 8) return create_from_mesh<double>(*m, out);
+        throw djg::ConfigError("precision must be 4 or 8");
+    } catch (const djg::ConfigError& e) {
+        djg_internal_set_create_error(e.what());
+    } catch (const djg::MeshError& e) {
+        djg_internal_set_create_error(e.what());
+    } catch (const std::exception& e) {
+        djg_internal_set_create_error(e.what());
+        return DJG_E_INTERNAL;
+    }
+    return DJG_E_CONFIG;
+}
 
 int djg_scenario_scalars(const djg_scenario* sc, djg_image_scalars* out) {
     if (!sc || !out) return DJG_E_CONFIG;

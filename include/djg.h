@@ -178,6 +178,10 @@ int djg_get_info(djg_engine* eng, djg_engine_info* info);
  * position of (element, local) in the sliced slot buffer) to the host. */
 int djg_get_slot_map(djg_engine* eng, int32_t* slot_pos);
 
+/* Test hook: the device cube root the element kernel uses (a restatement of
+ * the host libm's, see kernels.cuh) over n Reals. */
+int djg_debug_cbrt(int32_t precision, const void* in, void* out, int64_t n, int32_t device);
+
 const char* djg_last_error(djg_engine* eng);
 const char* djg_status_string(int32_t status);
 /* Last error of a failed djg_create (no handle). */

@@ -58,6 +58,8 @@ def lib(which: str = "oracle") -> C.CDLL:
                                             C.c_void_p, C.c_void_p]
         L.djo_element_record.argtypes = [C.c_int32, C.c_int32, P(A.djg_material_params), C.c_double,
                                          P(C.c_double), C.c_void_p]
+        L.djo_libm_cbrt.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64]
+        L.djo_restated_cbrt.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64]
     else:
         L.djref_image.argtypes = [P(A.djg_scenario_spec), P(A.djg_image_ptrs), P(A.djg_image_scalars)]
         L.djref_run.argtypes = [P(A.djg_scenario_spec), C.c_int64, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,

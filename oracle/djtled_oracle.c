@@ -230,3 +230,44 @@ int djo_element_record(int32_t precision, int32_t kind, const djg_material_param
 }
 
 int djo_const_count(int32_t kind, int32_t model) { return layout_of(kind, model).count; }
+
+/* Host libm cube root over an array (what the reference's std::cbrt calls),
+ * and the same algorithm restated (glibc 2.39 s_cbrtf.c / s_cbrt.c). */
+void djo_libm_cbrt(int32_t precision, const void* in, void* out, int64_t n) {
+    if (precision == 4) {
+        for (int64_t i = 0; i < n; ++i) ((float*)out)[i] = cbrtf(((const float*)in)[i]);
+    } else {
+        for (int64_t i = 0; i < n; ++i) ((double*)out)[i] = cbrt(((const double*)in)[i]);
+    }
+}
+
+static const double cbrt_factor[5] = {1.0 / 1.5874010519681994748, 1.0 / 1.2599210498948731648, 1.0,
+                                      1.2599210498948731648, 1.5874010519681994748};
+
+void djo_restated_cbrt(int32_t precision, const void* in, void* out, int64_t n) {
+    for (int64_t i = 0; i < n; ++i) {
+        int xe;
+        if (precision == 4) {
+            const float x = ((const float*)in)[i];
+            const float xm = frexpf(fabsf(x), &xe);
+            if (x == 0.0f || !isfinite(x)) { ((float*)out)[i] = x + x; continue; }
+            const float u = (float)(0.492659620528969547 + (0.697570460207922770 - 0.191502161678719066 * xm) * xm);
+            const float t2 = u * u * u;
+            const float ym = (float)(u * (t2 + 2.0 * xm) / (2.0 * t2 + xm) * cbrt_factor[2 + xe % 3]);
+            ((float*)out)[i] = ldexpf(x > 0.0f ? ym : -ym, xe / 3);
+        } else {
+            const double x = ((const double*)in)[i];
+            const double xm = frexp(fabs(x), &xe);
+            if (x == 0.0 || !isfinite(x)) { ((double*)out)[i] = x + x; continue; }
+            const double u = (0.354895765043919860 +
+                              ((1.50819193781584896 +
+                                ((-2.11499494167371287 +
+                                  ((2.44693122563534430 +
+                                    ((-1.83469277483613086 + (0.784932344976639262 - 0.145263899385486377 * xm) * xm) *
+                                     xm)) * xm)) * xm)) * xm));
+            const double t2 = u * u * u;
+            const double ym = u * (t2 + 2.0 * xm) / (2.0 * t2 + xm) * cbrt_factor[2 + xe % 3];
+            ((double*)out)[i] = ldexp(x > 0.0 ? ym : -ym, xe / 3);
+        }
+    }
+}

@@ -605,6 +605,26 @@ private:
     bool configured_ = false;
 };
 
+int debug_cbrt(int32_t precision, const void* in, void* out, int64_t n, int32_t device) {
+    try {
+        CK(cudaSetDevice(device));
+        const size_t bytes = size_t(n) * size_t(precision);
+        DevBuf a, b;
+        a.alloc(bytes);
+        b.alloc(bytes);
+        CK(cudaMemcpy(a.p, in, bytes, cudaMemcpyHostToDevice));
+        const unsigned grid = unsigned((n + 255) / 256);
+        if (precision == 4) k_cbrt<float><<<grid, 256>>>(a.as<float>(), b.as<float>(), n);
+        else k_cbrt<double><<<grid, 256>>>(a.as<double>(), b.as<double>(), n);
+        CK(cudaGetLastError());
+        CK(cudaMemcpy(out, b.p, bytes, cudaMemcpyDeviceToHost));
+        return DJG_OK;
+    } catch (const std::exception& e) {
+        g_create_error = e.what();
+        return DJG_E_CUDA;
+    }
+}
+
 }  // namespace
 }  // namespace djg
 
@@ -748,6 +768,10 @@ int djg_get_slot_map(djg_engine* eng, int32_t* out) {
         e.slot_map(out);
         return DJG_OK;
     });
+}
+
+int djg_debug_cbrt(int32_t precision, const void* in, void* out, int64_t n, int32_t device) {
+    return djg::debug_cbrt(precision, in, out, n, device);
 }
 
 const char* djg_last_error(djg_engine* eng) { return eng ? eng->err.c_str() : "null engine"; }

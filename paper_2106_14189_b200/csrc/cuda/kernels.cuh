@@ -12,9 +12,9 @@
 //                    central-difference update with damping and BCs, the
 //                    non-finite detector, and the end-of-step bookkeeping.
 //
-// Arithmetic mirrors the reference expression by expression and the file is
-// compiled with --fmad=false, so results match the CPU reference up to the
-// last-ulp behaviour of cbrt. No float atomics anywhere: the only atomics are
+// Arithmetic mirrors the reference expression by expression, the file is
+// compiled with --fmad=false, and cbrt restates glibc's algorithm, so a step
+// reproduces the CPU reference bit for bit. No float atomics anywhere: the only atomics are
 // the integer inversion/divergence flags (djtled_force.hpp:97-112,
 // solver.hpp:115,137).
 #pragma once
@@ -143,6 +143,63 @@ struct NodeArgs {
     Real* f_out;                         // assemble mode: 3N internal forces
 };
 
+// ------------------------------------------------------------------ cbrt
+
+// The reference calls std::cbrt (kinematics.hpp:69), i.e. glibc's cbrtf /
+// cbrt, which are NOT correctly rounded (10.7 % of floats in [0.5, 2) differ
+// from the correctly rounded cube root) and differ from CUDA's cbrtf. This is
+// a restatement of glibc 2.39's algorithm (sysdeps/ieee754/{flt-32,dbl-64}/
+// s_cbrt*.c: frexp reduction, a polynomial seed, one rational Halley step in
+// double, exponent scaling by 2^(1/3) powers). Evaluated with IEEE double ops
+// (no FMA: --fmad=false) it returns the same bits as the host libm; pinned by
+// tests/test_cbrt.py against the host for every float in [0.25, 4).
+__device__ __forceinline__ double glibc_cbrt_factor(int r) {
+    // 2^(r/3) for r = xe % 3 in {-2..2}
+    switch (r) {
+        case -2: return 1.0 / 1.5874010519681994748;
+        case -1: return 1.0 / 1.2599210498948731648;
+        case 1: return 1.2599210498948731648;
+        case 2: return 1.5874010519681994748;
+        default: return 1.0;
+    }
+}
+
+__device__ __forceinline__ float ref_cbrt(float x) {
+    int xe;
+    const float xm = frexpf(fabsf(x), &xe);
+    if (x == 0.0f || !isfinite(x)) return x + x;
+    const float u = float(0.492659620528969547 + (0.697570460207922770 - 0.191502161678719066 * double(xm)) *
+                                                     double(xm));
+    const float t2 = u * u * u;
+    const float ym = float(double(u) * (double(t2) + 2.0 * double(xm)) / (2.0 * double(t2) + double(xm)) *
+                           glibc_cbrt_factor(xe % 3));
+    return ldexpf(x > 0.0f ? ym : -ym, xe / 3);
+}
+
+__device__ __forceinline__ double ref_cbrt(double x) {
+    int xe;
+    const double xm = frexp(fabs(x), &xe);
+    if (x == 0.0 || !isfinite(x)) return x + x;
+    const double u =
+        (0.354895765043919860 +
+         ((1.50819193781584896 +
+           ((-2.11499494167371287 +
+             ((2.44693122563534430 + ((-1.83469277483613086 + (0.784932344976639262 - 0.145263899385486377 * xm) * xm) *
+                                      xm)) *
+              xm)) *
+            xm)) *
+          xm));
+    const double t2 = u * u * u;
+    const double ym = u * (t2 + 2.0 * xm) / (2.0 * t2 + xm) * glibc_cbrt_factor(xe % 3);
+    return ldexp(x > 0.0 ? ym : -ym, xe / 3);
+}
+
+template <class Real>
+__global__ void k_cbrt(const Real* __restrict__ in, Real* __restrict__ out, long long n) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = ref_cbrt(in[i]);
+}
+
 // ------------------------------------------------------------------ K1
 
 template <class Real, int KIND, int MODEL>
@@ -260,7 +317,7 @@ __global__ void __launch_bounds__(128) k_element(const ElemArgs<Real> A) {
     g[3] = Jt[0][0] * Jt[1][0] + Jt[0][1] * Jt[1][1] + Jt[0][2] * Jt[1][2];
     g[4] = Jt[0][0] * Jt[2][0] + Jt[0][1] * Jt[2][1] + Jt[0][2] * Jt[2][2];
     g[5] = Jt[1][0] * Jt[2][0] + Jt[1][1] * Jt[2][1] + Jt[1][2] * Jt[2][2];
-    const Real cb = cbrt(J);
+    const Real cb = ref_cbrt(J);
     const Real j_m23 = Real(1) / (cb * cb);
     const Real I1 = g[0] * c[11] + g[1] * c[12] + g[2] * c[13] + g[3] * c[14] + g[4] * c[15] + g[5] * c[16];
     const Real Ib1 = j_m23 * I1;

@@ -1,10 +1,13 @@
 """GPU parity: the sm_100a engine (through libdjg's C-ABI) against the CPU
-oracle on the same seeded inputs.
+oracle (itself bit-identical to the reference, tests/test_oracle.py) on the
+same inputs.
 
-Tolerances: max|du| / max|u| <= 1e-5 in float,
-<= 1e-10 in double, integers (CSR, slot map) exact. The engine is built with
---fmad=false and mirrors the reference's evaluation order, so the observed
-differences are far below the gates (only cbrt's last ulp can differ).
+The gate is BITWISE equality of u_curr and u_prev (== semantics, so only the
+sign of an exact zero may differ): the engine mirrors the reference's
+evaluation order, is compiled with --fmad=false, sums each node's element
+rows in ascending element order, and restates glibc's cbrt. The SURVEY §8(c)
+tolerances (1e-5 float, 1e-10 double) are asserted as well, as the contract
+floor, and integers (CSR, slot map) are exact.
 """
 import numpy as np
 import pytest
@@ -27,13 +30,16 @@ def run_gpu(spec, steps, **kw):
     return u, up, rep
 
 
-def check_run(spec, steps, tol=None):
+def check_run(spec, steps, tol=None, exact=True):
     u, up, rep = run_gpu(spec, steps)
     ur, upr, rr = oracle.run(spec, steps, "oracle")
     assert rep.step == rr["step"] and rep.status == rr["status"], (rep, rr)
     tol = TOL[spec.precision] if tol is None else tol
     e1, e2 = oracle.rel_max_err(u, ur), oracle.rel_max_err(up, upr)
     assert e1 <= tol and e2 <= tol, (e1, e2)
+    if exact:
+        assert np.array_equal(u, ur) and np.array_equal(up, upr), \
+            f"not bit-identical: {np.count_nonzero(u != ur)} of {u.size} DOFs differ (rel {e1:.2e})"
     assert np.max(np.abs(ur)) > 0
     return e1
 
@@ -88,7 +94,7 @@ def test_assemble_random_state(precision):
         f, st = eng.assemble(u)
     fr, sr = oracle.assemble(spec, u)
     assert st["first_inverted"] == -1 and sr["first_inverted"] == -1
-    assert oracle.rel_max_err(f, fr) <= TOL[precision] * 1e-2
+    assert np.array_equal(f, fr)
 
 
 def test_slot_map_is_a_bijection_consistent_with_csr():
@@ -175,7 +181,7 @@ def test_external_force_matches_oracle():
         eng.step(100)
         u = eng.get_state()[0]
     ur, _, _ = oracle.run(spec, 100, "oracle", r_ext=r)
-    assert oracle.rel_max_err(u, ur) <= 1e-10
+    assert np.array_equal(u, ur)
 
 
 def test_inversion_abort_reports_min_element_and_keeps_state():
@@ -193,7 +199,7 @@ def test_inversion_abort_reports_min_element_and_keeps_state():
     assert rep.status == A.DJG_E_INVERSION == rr["status"]
     assert rep.first_inverted == rr["first_inverted"] >= 0
     assert (rep.fail_step, rep.step) == (rr["fail_step"], rr["step"])
-    assert oracle.rel_max_err(u, ur) <= 1e-10 and oracle.rel_max_err(up, upr) <= 1e-10
+    assert np.array_equal(u, ur) and np.array_equal(up, upr)
     with pytest.raises(SimulationError) as ei:
         with GpuDjEngine(Scenario(spec)) as eng:
             eng.step(100)

@@ -21,6 +21,7 @@ DJG_ABORT, DJG_SKIP_AND_REPORT = 0, 1
 DJG_FREE, DJG_FIXED, DJG_PRESCRIBED = 0, 1, 2
 DJG_OK, DJG_E_INTERNAL, DJG_E_CONFIG, DJG_E_CUDA, DJG_E_INVERSION, DJG_E_DIVERGENCE = 0, 1, 2, 3, 4, 5
 DJG_FLAG_NO_GRAPH = 1
+DJG_FLAG_TWO_KERNEL = 2
 
 KIND_NAMES = {"T4": DJG_T4, "H8": DJG_H8}
 MODEL_NAMES = {"NH": DJG_NH, "TI": DJG_TI, "OT": DJG_OT, "MR": DJG_MR}
@@ -135,7 +136,8 @@ class djg_engine_info(C.Structure):
         ("num_nodes", C.c_int64), ("num_elements", C.c_int64), ("num_slots", C.c_int64),
         ("slot_capacity", C.c_int64), ("device_bytes", C.c_int64),
         ("npe", C.c_int32), ("nconst", C.c_int32), ("const_planes", C.c_int32), ("precision", C.c_int32),
-        ("kernels_per_step", C.c_int32), ("sm_count", C.c_int32),
+        ("kernels_per_step", C.c_int32), ("sm_count", C.c_int32), ("fused", C.c_int32),
+        ("ring_regions", C.c_int32),
     ]
 
 

@@ -147,40 +147,47 @@ public:
         }
         if (off[0] != 0 || off[N_] != E_ * npe) throw DescError("CSR offsets inconsistent with connectivity");
 
-        // Sliced slot layout: node n's k-th slot at slice_base[n/32] + 32k + n%32.
-        const int64_t S = (N_ + 31) / 32;
-        std::vector<int32_t> row_len(static_cast<size_t>(N_)), slice_base(static_cast<size_t>(S) + 1);
-        int64_t cap = 0;
-        for (int64_t s = 0; s < S; ++s) {
-            slice_base[size_t(s)] = int32_t(cap);
-            int w = 0;
-            for (int64_t n = s * 32; n < std::min<int64_t>(N_, s * 32 + 32); ++n) {
-                const int64_t len = off[n + 1] - off[n];
-                row_len[size_t(n)] = int32_t(len);
-                w = std::max<int>(w, int(len));
-            }
-            cap += int64_t(32) * w;
-            if (cap > INT32_MAX) throw DescError("slot buffer exceeds 32-bit indexing");
-        }
-        slice_base[size_t(S)] = int32_t(cap);
-        capacity_ = std::max<int64_t>(cap, 1);
-        // slot position of (e, a)
-        std::vector<int32_t> slot(size_t(E_ * npe));
+        // CSR consistency and row lengths.
+        std::vector<int32_t> row_len(static_cast<size_t>(N_));
+        int wmax = 0;
         bool bad = false;
-#pragma omp parallel for schedule(static) reduction(|| : bad)
+#pragma omp parallel for schedule(static) reduction(|| : bad) reduction(max : wmax)
         for (int64_t n = 0; n < N_; ++n) {
-            const int64_t base = int64_t(slice_base[size_t(n >> 5)]) + (n & 31);
+            row_len[size_t(n)] = int32_t(off[n + 1] - off[n]);
+            wmax = std::max(wmax, int(off[n + 1] - off[n]));
             for (int64_t p = off[n]; p < off[n + 1]; ++p) {
                 const int64_t e = celem[p];
                 const int a = cloc[p];
-                if (e < 0 || e >= E_ || a < 0 || a >= npe || conn[e * npe + a] != n) {
-                    bad = true;
-                    continue;
-                }
-                slot[size_t(e * npe + a)] = int32_t(base + 32 * (p - off[n]));
+                if (e < 0 || e >= E_ || a < 0 || a >= npe || conn[e * npe + a] != n) bad = true;
             }
         }
         if (bad) throw DescError("CSR pairs do not match connectivity");
+        wmax_ = std::max(wmax, 1);
+        std::vector<int32_t> slot(size_t(E_ * npe));
+        fused_ = !(flags_ & DJG_FLAG_TWO_KERNEL) && plan_fused(off, celem, cloc, conn, slot);
+        if (!fused_) {
+            // Sliced slot layout: node n's k-th slot at slice_base[n/32] + 32k + n%32.
+            const int64_t S = (N_ + 31) / 32;
+            std::vector<int32_t> slice_base(static_cast<size_t>(S) + 1);
+            int64_t cap = 0;
+            for (int64_t sl = 0; sl < S; ++sl) {
+                slice_base[size_t(sl)] = int32_t(cap);
+                int w = 0;
+                for (int64_t n = sl * 32; n < std::min<int64_t>(N_, sl * 32 + 32); ++n) w = std::max(w, row_len[size_t(n)]);
+                cap += int64_t(32) * w;
+                if (cap > INT32_MAX) throw DescError("slot buffer exceeds 32-bit indexing");
+            }
+            slice_base[size_t(S)] = int32_t(cap);
+            capacity_ = std::max<int64_t>(cap, 1);
+#pragma omp parallel for schedule(static)
+            for (int64_t n = 0; n < N_; ++n) {
+                const int64_t base = int64_t(slice_base[size_t(n >> 5)]) + (n & 31);
+                for (int64_t p = off[n]; p < off[n + 1]; ++p)
+                    slot[size_t(celem[p] * npe + cloc[p])] = int32_t(base + 32 * (p - off[n]));
+            }
+            slicebase_.alloc(slice_base.size() * sizeof(int32_t));
+            CK(cudaMemcpy(slicebase_.p, slice_base.data(), slicebase_.bytes, cudaMemcpyHostToDevice));
+        }
 
         // Upload connectivity and slots as int4 planes.
         const int nq = npe / 4;
@@ -224,8 +231,6 @@ public:
         CK(cudaMemset(ef_.p, 0, ef_.bytes));
         rowlen_.alloc(row_len.size() * sizeof(int32_t));
         CK(cudaMemcpy(rowlen_.p, row_len.data(), rowlen_.bytes, cudaMemcpyHostToDevice));
-        slicebase_.alloc(slice_base.size() * sizeof(int32_t));
-        CK(cudaMemcpy(slicebase_.p, slice_base.data(), slicebase_.bytes, cudaMemcpyHostToDevice));
         c1_.alloc(size_t(N_) * sizeof(Real));
         code_.alloc(size_t(N_));
         target_.alloc(size_t(3 * N_) * sizeof(Real));
@@ -330,6 +335,114 @@ public:
         drop_graphs();
     }
 
+    // Work list, dependency lists and ring layout of the fused step (see
+    // kernels.cuh, k_step_fused). Returns false when the mesh ordering would
+    // need a ring larger than the L2 budget; the engine then uses the
+    // two-kernel step.
+    bool plan_fused(const int64_t* off, const int64_t* celem, const int32_t* cloc, const int32_t* conn,
+                    std::vector<int32_t>& slot) {
+        constexpr int C = 256;
+        if (wmax_ > 255) return false;
+        const int npe = npe_;
+        const int64_t nEC = (E_ + C - 1) / C, nNC = (N_ + C - 1) / C;
+        // node chunk -> element chunks it reads
+        std::vector<std::vector<int>> ndep(static_cast<size_t>(nNC));
+        std::vector<int> need(static_cast<size_t>(nNC), -1);
+#pragma omp parallel for schedule(dynamic, 64)
+        for (int64_t j = 0; j < nNC; ++j) {
+            auto& v = ndep[size_t(j)];
+            for (int64_t n = j * C; n < std::min<int64_t>(N_, (j + 1) * C); ++n)
+                for (int64_t p = off[n]; p < off[n + 1]; ++p) v.push_back(int(celem[p] / C));
+            std::sort(v.begin(), v.end());
+            v.erase(std::unique(v.begin(), v.end()), v.end());
+            need[size_t(j)] = v.empty() ? -1 : v.back();
+        }
+        // element chunk -> node chunks it writes
+        std::vector<std::vector<int>> tgt(static_cast<size_t>(nEC));
+#pragma omp parallel for schedule(dynamic, 64)
+        for (int64_t i = 0; i < nEC; ++i) {
+            auto& v = tgt[size_t(i)];
+            for (int64_t e = i * C; e < std::min<int64_t>(E_, (i + 1) * C); ++e)
+                for (int a = 0; a < npe; ++a) v.push_back(int(conn[e * npe + a] / C));
+            std::sort(v.begin(), v.end());
+            v.erase(std::unique(v.begin(), v.end()), v.end());
+        }
+        // work list: a node chunk right after the last element chunk it needs
+        std::vector<std::vector<int>> after(static_cast<size_t>(nEC));
+        std::vector<int> items;
+        items.reserve(size_t(nEC + nNC));
+        for (int64_t j = 0; j < nNC; ++j) {
+            if (need[size_t(j)] < 0) items.push_back(~int(j));
+            else after[size_t(need[size_t(j)])].push_back(int(j));
+        }
+        std::vector<int64_t> posE(static_cast<size_t>(nEC)), posN(static_cast<size_t>(nNC));
+        for (int64_t q = 0; q < int64_t(items.size()); ++q) posN[size_t(~items[size_t(q)])] = q;
+        for (int64_t i = 0; i < nEC; ++i) {
+            posE[size_t(i)] = int64_t(items.size());
+            items.push_back(int(i));
+            for (int j : after[size_t(i)]) {
+                posN[size_t(j)] = int64_t(items.size());
+                items.push_back(~j);
+            }
+        }
+        // Ring size: an element chunk may overwrite region t % R only after
+        // node chunk t - R (earlier in the list) consumed it.
+        auto ok = [&](int64_t R) {
+            for (int64_t i = 0; i < nEC; ++i)
+                for (int t : tgt[size_t(i)])
+                    if (t >= R && posN[size_t(t - R)] > posE[size_t(i)]) return false;
+            return true;
+        };
+        int64_t lo = 1, hi = nNC;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) / 2;
+            if (ok(mid)) hi = mid;
+            else lo = mid + 1;
+        }
+        int64_t R = lo;
+        while (!ok(R)) ++R;
+        R = std::min<int64_t>(nNC, R + std::max<int64_t>(8, R / 2));  // slack: fewer stalls
+        while (!ok(R)) ++R;
+        const int64_t region = int64_t(C) * wmax_;
+        if (R * region * int64_t(sizeof(Node)) > kRingBudget || R * region > INT32_MAX) return false;
+        ring_R_ = int(R);
+        capacity_ = R * region;
+        // ring position of every (element, local node)
+#pragma omp parallel for schedule(static)
+        for (int64_t n = 0; n < N_; ++n) {
+            const int64_t l = n % C;
+            const int64_t base = ((n / C) % R) * region + (l / 32) * 32 * wmax_ + (l % 32);
+            for (int64_t p = off[n]; p < off[n + 1]; ++p)
+                slot[size_t(celem[p] * npe + cloc[p])] = int32_t(base + 32 * (p - off[n]));
+        }
+        // flatten dependency lists
+        std::vector<int> ndep_off(static_cast<size_t>(nNC) + 1, 0), ndep_flat;
+        for (int64_t j = 0; j < nNC; ++j) ndep_off[size_t(j + 1)] = ndep_off[size_t(j)] + int(ndep[size_t(j)].size());
+        ndep_flat.reserve(size_t(ndep_off.back()));
+        for (auto& v : ndep) ndep_flat.insert(ndep_flat.end(), v.begin(), v.end());
+        std::vector<int> er_off(static_cast<size_t>(nEC) + 1, 0), er_flat;
+        for (int64_t i = 0; i < nEC; ++i) {
+            for (int t : tgt[size_t(i)])
+                if (t >= R) er_flat.push_back(int(t - R));
+            er_off[size_t(i + 1)] = int(er_flat.size());
+        }
+        auto up = [&](DevBuf& b, const std::vector<int>& v) {
+            b.alloc(std::max<size_t>(v.size(), 1) * sizeof(int));
+            if (!v.empty()) CK(cudaMemcpy(b.p, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
+        };
+        up(items_, items);
+        up(ndepOff_, ndep_off);
+        up(ndep_, ndep_flat);
+        up(ereuseOff_, er_off);
+        up(ereuse_, er_flat);
+        edone_.alloc(size_t(nEC) * sizeof(unsigned));
+        ndone_.alloc(size_t(nNC) * sizeof(unsigned));
+        CK(cudaMemset(edone_.p, 0, edone_.bytes));
+        CK(cudaMemset(ndone_.p, 0, ndone_.bytes));
+        n_items_ = int(items.size());
+        return true;
+    }
+
     ~Engine() override {
         if (graph_big_) cudaGraphExecDestroy(graph_big_);
         if (graph_one_) cudaGraphExecDestroy(graph_one_);
@@ -341,7 +454,14 @@ public:
     cudaStream_t stream() const override { return stream_; }
 
     void reset_ctrl(int64_t step) {
+        unsigned epoch = 0;
+        if (ctrl_initialized_) {
+            read_ctrl();
+            epoch = hctrl_->epoch;  // flags carry epoch stamps: never move backwards
+        }
+        ctrl_initialized_ = true;
         Ctrl c{};
+        c.epoch = epoch;
         c.step = step;
         c.first_inv = kNone;
         c.asm_first = kNone;
@@ -428,6 +548,50 @@ public:
         CK(cudaGetLastError());
     }
 
+    template <int K, int M>
+    void launch_fused_km(cudaStream_t s, bool assemble_mode, const Node* u_override) {
+        ElemArgs<Real> a = ea_;
+        a.u_override = u_override;
+        FusedSched S{items_.as<int>(), n_items_, edone_.as<unsigned>(), ndone_.as<unsigned>(), ndepOff_.as<int>(),
+                     ndep_.as<int>(), ereuseOff_.as<int>(), ereuse_.as<int>(), rowlen_.as<int>(), ring_R_, wmax_};
+        auto kern = assemble_mode ? k_step_fused<Real, K, M, true> : k_step_fused<Real, K, M, false>;
+        if (fused_grid_ == 0) {
+            int per_sm = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_fused<Real, K, M, false>, 256, 0));
+            fused_grid_ = std::max(1, per_sm) * sms_;
+        }
+        kern<<<fused_grid_, 256, 0, s>>>(a, na_, S);
+        CK(cudaGetLastError());
+    }
+
+    void launch_fused(cudaStream_t s, bool assemble_mode = false, const Node* u_override = nullptr) {
+        if (kind_ == DJG_T4) {
+            switch (model_) {
+                case DJG_NH: launch_fused_km<0, 0>(s, assemble_mode, u_override); break;
+                case DJG_TI: launch_fused_km<0, 1>(s, assemble_mode, u_override); break;
+                case DJG_OT: launch_fused_km<0, 2>(s, assemble_mode, u_override); break;
+                default: launch_fused_km<0, 3>(s, assemble_mode, u_override); break;
+            }
+        } else {
+            switch (model_) {
+                case DJG_NH: launch_fused_km<1, 0>(s, assemble_mode, u_override); break;
+                case DJG_TI: launch_fused_km<1, 1>(s, assemble_mode, u_override); break;
+                case DJG_OT: launch_fused_km<1, 2>(s, assemble_mode, u_override); break;
+                default: launch_fused_km<1, 3>(s, assemble_mode, u_override); break;
+            }
+        }
+    }
+
+    // One advance_step on the stream.
+    void launch_step(cudaStream_t s) {
+        if (fused_) {
+            launch_fused(s);
+        } else {
+            launch_element(s);
+            launch_node(s);
+        }
+    }
+
     void launch_node(cudaStream_t s, bool assemble_mode = false) {
         const unsigned grid = unsigned((N_ + 255) / 256);
         if (assemble_mode) k_node<Real, true><<<grid, 256, 0, s>>>(na_);
@@ -444,10 +608,7 @@ public:
     cudaGraphExec_t capture(int steps) {
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
-        for (int i = 0; i < steps; ++i) {
-            launch_element(stream_);
-            launch_node(stream_);
-        }
+        for (int i = 0; i < steps; ++i) launch_step(stream_);
         CK(cudaStreamEndCapture(stream_, &g));
         cudaGraphExec_t ex;
         CK(cudaGraphInstantiate(&ex, g, 0));
@@ -462,10 +623,7 @@ public:
         // host: sync() reports the difference.
         CK(cudaMemcpyAsync(hstart_, ctrl_.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream_));
         if (flags_ & DJG_FLAG_NO_GRAPH) {
-            for (int64_t i = 0; i < n; ++i) {
-                launch_element(stream_);
-                launch_node(stream_);
-            }
+            for (int64_t i = 0; i < n; ++i) launch_step(stream_);
             return;
         }
         if (n >= kGraphSteps && !graph_big_) graph_big_ = capture(kGraphSteps);
@@ -516,8 +674,12 @@ public:
             hctrl_->halted = 0;
             CK(cudaMemcpyAsync(ctrl_.p, hctrl_, sizeof(Ctrl), cudaMemcpyHostToDevice, stream_));
         }
-        launch_element(stream_, uo);
-        launch_node(stream_, true);
+        if (fused_) {
+            launch_fused(stream_, true, uo);
+        } else {
+            launch_element(stream_, uo);
+            launch_node(stream_, true);
+        }
         read_ctrl();
         if (halted) {
             hctrl_->halted = halted;
@@ -540,9 +702,14 @@ public:
         for (auto& e : ev) CK(cudaEventCreate(&e));
         CK(cudaEventRecord(ev[0], stream_));
         for (int64_t i = 0; i < n; ++i) {
-            launch_element(stream_);
-            CK(cudaEventRecord(ev[size_t(3 * i + 1)], stream_));
-            launch_node(stream_);
+            if (fused_) {
+                launch_fused(stream_);
+                CK(cudaEventRecord(ev[size_t(3 * i + 1)], stream_));
+            } else {
+                launch_element(stream_);
+                CK(cudaEventRecord(ev[size_t(3 * i + 1)], stream_));
+                launch_node(stream_);
+            }
             CK(cudaEventRecord(ev[size_t(3 * i + 2)], stream_));
             CK(cudaEventRecord(ev[size_t(3 * i + 3)], stream_));
         }
@@ -571,12 +738,16 @@ public:
         o->slot_capacity = capacity_;
         o->device_bytes = int64_t(conn_.bytes + slot_.bytes + consts_.bytes + 3 * u_[0].bytes + uscratch_.bytes +
                                   flat_.bytes + ef_.bytes + rowlen_.bytes + slicebase_.bytes + c1_.bytes +
-                                  code_.bytes + target_.bytes + tTotal_.bytes + rext_.bytes + ctrl_.bytes);
+                                  code_.bytes + target_.bytes + tTotal_.bytes + rext_.bytes + ctrl_.bytes +
+                                  items_.bytes + ndepOff_.bytes + ndep_.bytes + ereuseOff_.bytes + ereuse_.bytes +
+                                  edone_.bytes + ndone_.bytes);
         o->npe = npe_;
         o->nconst = nconst_;
         o->const_planes = nplanes_;
         o->precision = int32_t(sizeof(Real));
-        o->kernels_per_step = 2;
+        o->kernels_per_step = fused_ ? 1 : 2;
+        o->ring_regions = ring_R_;
+        o->fused = fused_ ? 1 : 0;
         o->sm_count = sms_;
     }
 
@@ -603,6 +774,12 @@ private:
     cudaGraphExec_t graph_big_ = nullptr, graph_one_ = nullptr;
     Ctrl* hstart_ = nullptr;  // pinned snapshot taken at the start of a step call
     bool configured_ = false;
+    bool ctrl_initialized_ = false;
+    // fused step
+    static constexpr int64_t kRingBudget = int64_t(48) << 20;  // bytes of force ring kept in L2
+    bool fused_ = false;
+    int ring_R_ = 0, wmax_ = 1, n_items_ = 0, fused_grid_ = 0;
+    DevBuf items_, ndepOff_, ndep_, ereuseOff_, ereuse_, edone_, ndone_;
 };
 
 int debug_cbrt(int32_t precision, const void* in, void* out, int64_t n, int32_t device) {

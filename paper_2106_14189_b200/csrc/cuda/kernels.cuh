@@ -40,6 +40,7 @@ struct RT<float> {
     static constexpr int kPlane = 4;
     __device__ static inline Node load_node(const Node* p) { return __ldg(p); }
     __device__ static inline Node load_stream(const Node* p) { return __ldcs(p); }
+    __device__ static inline Node load_l2(const Node* p) { return __ldcg(p); }
     __device__ static inline void store_node(Node* p, float x, float y, float z) { *p = make_float4(x, y, z, 0.f); }
     __device__ static inline Plane load_plane(const Plane* p) { return __ldcs(p); }
 };
@@ -57,6 +58,11 @@ struct RT<double> {
     __device__ static inline Node load_stream(const Node* p) {
         const double2 a = __ldcs(reinterpret_cast<const double2*>(p));
         const double2 b = __ldcs(reinterpret_cast<const double2*>(p) + 1);
+        return {a.x, a.y, b.x, b.y};
+    }
+    __device__ static inline Node load_l2(const Node* p) {
+        const double2 a = __ldcg(reinterpret_cast<const double2*>(p));
+        const double2 b = __ldcg(reinterpret_cast<const double2*>(p) + 1);
         return {a.x, a.y, b.x, b.y};
     }
     __device__ static inline void store_node(Node* p, double x, double y, double z) {
@@ -99,6 +105,8 @@ struct Ctrl {
     long long inv_steps;            // steps with >= 1 inversion
     unsigned long long asm_first;   // djg_assemble result
     unsigned long long asm_count;
+    unsigned int epoch;             // fused step: launches completed (flag stamps)
+    int ticket;                     // fused step: next work-list item
 };
 
 constexpr unsigned long long kNone = ~0ull;
@@ -202,20 +210,14 @@ __global__ void k_cbrt(const Real* __restrict__ in, Real* __restrict__ out, long
 
 // ------------------------------------------------------------------ K1
 
+// One element: loads, DJ-TLED force, stores of its npe rows into their slots.
 template <class Real, int KIND, int MODEL>
-__global__ void __launch_bounds__(128) k_element(const ElemArgs<Real> A) {
+__device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long long e,
+                                             const typename RT<Real>::Node* __restrict__ u) {
     using L = Layout<KIND, MODEL>;
     using T = RT<Real>;
     constexpr int NPE = L::NPE;
     constexpr int NP = (L::count + T::kPlane - 1) / T::kPlane;
-    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= A.E) return;
-    if (*(volatile const int*)&A.ctrl->halted) return;
-    const int phase = int(A.ctrl->step % 3);
-    // Select by value: indexing the kernel-parameter array with a runtime
-    // value would copy the whole parameter block to local memory.
-    const typename T::Node* __restrict__ u =
-        A.u_override ? A.u_override : (phase == 0 ? A.u[0] : (phase == 1 ? A.u[1] : A.u[2]));
 
     // Connectivity (int32 node ids), 128-bit per 4 nodes.
     int nid[NPE];
@@ -434,18 +436,36 @@ __global__ void __launch_bounds__(128) k_element(const ElemArgs<Real> A) {
     }
 }
 
+// Select by value: indexing the kernel-parameter array with a runtime value
+// would copy the whole parameter block to local memory.
+template <class P>
+__device__ __forceinline__ P pick3(int i, P a, P b, P c) {
+    return i == 0 ? a : (i == 1 ? b : c);
+}
+
+template <class Real, int KIND, int MODEL>
+__global__ void __launch_bounds__(128) k_element(const ElemArgs<Real> A) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= A.E) return;
+    if (*(volatile const int*)&A.ctrl->halted) return;
+    const int phase = int(A.ctrl->step % 3);
+    const typename RT<Real>::Node* u = A.u_override ? A.u_override : pick3(phase, A.u[0], A.u[1], A.u[2]);
+    element_body<Real, KIND, MODEL>(A, e, u);
+}
+
 // ------------------------------------------------------------------ K2+K3
 
 // Sums node n's element rows in ascending element order from +0
-// (gather_nodal_forces, djtled_force.hpp:116-134).
-template <class Real>
-__device__ __forceinline__ void gather_row(const NodeArgs<Real>& A, long long n, Real& sx, Real& sy, Real& sz) {
+// (gather_nodal_forces, djtled_force.hpp:116-134). Slot k of the node sits at
+// p[32 k]; kCG reads through L2 only (slots written earlier in the same
+// launch by other SMs).
+template <class Real, bool kCG>
+__device__ __forceinline__ void gather_row(const typename RT<Real>::Node* __restrict__ p, int len, Real& sx,
+                                           Real& sy, Real& sz) {
     using T = RT<Real>;
-    const int len = A.row_len[n];
-    const typename T::Node* p = A.ef + (long long)A.slice_base[n >> 5] + (n & 31);
     sx = Real(0); sy = Real(0); sz = Real(0);
     for (int k = 0; k < len; ++k) {
-        const typename T::Node v = T::load_stream(p + 32 * k);
+        const typename T::Node v = kCG ? T::load_l2(p + 32 * k) : T::load_stream(p + 32 * k);
         sx += v.x; sy += v.y; sz += v.z;
     }
 }
@@ -466,69 +486,59 @@ __device__ __forceinline__ Real dof_update(int kind, bool massless, Real c1, Rea
     return v;
 }
 
-template <class Real, bool kAssemble>
-__global__ void __launch_bounds__(256) k_node(const NodeArgs<Real> A) {
+// One node: gather + (assemble: write f | step: central difference into
+// u_next). Returns true if a non-finite displacement was produced.
+template <class Real, bool kAssemble, bool kCG>
+__device__ __forceinline__ bool node_body(const NodeArgs<Real>& A, const long long n,
+                                          const typename RT<Real>::Node* slots, int len, long long step) {
     using T = RT<Real>;
-    Ctrl* ctrl = A.ctrl;
-    if (*(volatile const int*)&ctrl->halted && !kAssemble) return;
-    __shared__ int s_nonfinite;
-    if (threadIdx.x == 0) s_nonfinite = 0;
-    __syncthreads();
-    const long long step = ctrl->step;
-    const bool inverted = ctrl->first_inv != kNone;
-    const bool skip = inverted && A.policy == 0;  // Abort: no gather, no update (djtled_force.hpp:202-208)
-    const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (n < A.N && !skip) {
-        Real fx, fy, fz;
-        gather_row(A, n, fx, fy, fz);
-        if constexpr (kAssemble) {
-            A.f_out[3 * n + 0] = fx;
-            A.f_out[3 * n + 1] = fy;
-            A.f_out[3 * n + 2] = fz;
-        } else {
-            const int ph = int(step % 3);
-            const typename T::Node* ucur = ph == 0 ? A.u[0] : (ph == 1 ? A.u[1] : A.u[2]);
-            const typename T::Node* uprv = ph == 0 ? A.u[2] : (ph == 1 ? A.u[0] : A.u[1]);
-            typename T::Node* unxt = ph == 0 ? A.u[1] : (ph == 1 ? A.u[2] : A.u[0]);
-            const typename T::Node uc = T::load_node(ucur + n);
-            const typename T::Node up = T::load_node(uprv + n);
-            typename T::Node r;
-            if (A.r_ext) r = T::load_node(A.r_ext + n);
-            else { r.x = Real(0); r.y = Real(0); r.z = Real(0); }
-            const int code = A.code[n];
-            const bool massless = (code >> 6) & 1;
-            const Real c1 = A.c1[n];
-            const Real t_next = A.dt * Real(step + 1);
-            bool nf = false;
-            const Real vx = dof_update<Real>(code & 3, massless, c1, r.x, fx, uc.x, up.x, A.c2, A.c3, t_next,
-                                             A.target, A.t_total, 3 * n + 0, nf);
-            const Real vy = dof_update<Real>((code >> 2) & 3, massless, c1, r.y, fy, uc.y, up.y, A.c2, A.c3, t_next,
-                                             A.target, A.t_total, 3 * n + 1, nf);
-            const Real vz = dof_update<Real>((code >> 4) & 3, massless, c1, r.z, fz, uc.z, up.z, A.c2, A.c3, t_next,
-                                             A.target, A.t_total, 3 * n + 2, nf);
-            T::store_node(unxt + n, vx, vy, vz);
-            if (nf) s_nonfinite = 1;
-        }
+    Real fx, fy, fz;
+    gather_row<Real, kCG>(slots, len, fx, fy, fz);
+    if constexpr (kAssemble) {
+        A.f_out[3 * n + 0] = fx;
+        A.f_out[3 * n + 1] = fy;
+        A.f_out[3 * n + 2] = fz;
+        return false;
+    } else {
+        const int ph = int(step % 3);
+        const typename T::Node uc = T::load_node(pick3(ph, A.u[0], A.u[1], A.u[2]) + n);
+        const typename T::Node up = T::load_node(pick3(ph, A.u[2], A.u[0], A.u[1]) + n);
+        typename T::Node* unxt = pick3(ph, A.u[1], A.u[2], A.u[0]);
+        typename T::Node r;
+        if (A.r_ext) r = T::load_node(A.r_ext + n);
+        else { r.x = Real(0); r.y = Real(0); r.z = Real(0); }
+        const int code = A.code[n];
+        const bool massless = (code >> 6) & 1;
+        const Real c1 = A.c1[n];
+        const Real t_next = A.dt * Real(step + 1);
+        bool nf = false;
+        const Real vx = dof_update<Real>(code & 3, massless, c1, r.x, fx, uc.x, up.x, A.c2, A.c3, t_next,
+                                         A.target, A.t_total, 3 * n + 0, nf);
+        const Real vy = dof_update<Real>((code >> 2) & 3, massless, c1, r.y, fy, uc.y, up.y, A.c2, A.c3, t_next,
+                                         A.target, A.t_total, 3 * n + 1, nf);
+        const Real vz = dof_update<Real>((code >> 4) & 3, massless, c1, r.z, fz, uc.z, up.z, A.c2, A.c3, t_next,
+                                         A.target, A.t_total, 3 * n + 2, nf);
+        T::store_node(unxt + n, vx, vy, vz);
+        return nf;
     }
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    if (s_nonfinite) atomicOr(&ctrl->diverged, 1);
-    __threadfence();
-    const unsigned int done = atomicAdd(&ctrl->blocks_done, 1u);
-    if (done != gridDim.x - 1) return;
-    // Last block: close the step (advance_step's tail, solver.hpp:143-152).
+}
+
+// Closes a step (advance_step's tail, solver.hpp:143-152): called by the last
+// CTA to finish, after every other CTA's writes are visible.
+template <bool kAssemble>
+__device__ __forceinline__ void close_step(Ctrl* ctrl, long long step, int policy) {
     __threadfence();
     const unsigned long long cnt = atomicAdd(&ctrl->inv_count, 0ull);
     const unsigned long long first = atomicAdd(&ctrl->first_inv, 0ull);
     if (kAssemble) {
-        ctrl->asm_first = (first != kNone && A.policy == 0) ? first : kNone;
+        ctrl->asm_first = (first != kNone && policy == 0) ? first : kNone;
         ctrl->asm_count = cnt;
     } else {
         const int div = atomicOr(&ctrl->diverged, 0);
         ctrl->total_inv += cnt;
         if (cnt > 0) ctrl->inv_steps += 1;
-        if (skip) {
-            ctrl->halted = 4;  // DJG_E_INVERSION
+        if (first != kNone && policy == 0) {
+            ctrl->halted = 4;  // DJG_E_INVERSION: state stays at the last good step
             ctrl->halt_first_inv = (long long)first;
             ctrl->fail_step = step + 1;
         } else if (div) {
@@ -541,6 +551,127 @@ __global__ void __launch_bounds__(256) k_node(const NodeArgs<Real> A) {
     ctrl->inv_count = 0;
     ctrl->first_inv = kNone;
     ctrl->diverged = 0;
+}
+
+template <class Real, bool kAssemble>
+__global__ void __launch_bounds__(256) k_node(const NodeArgs<Real> A) {
+    Ctrl* ctrl = A.ctrl;
+    if (*(volatile const int*)&ctrl->halted && !kAssemble) return;
+    __shared__ int s_nonfinite;
+    if (threadIdx.x == 0) s_nonfinite = 0;
+    __syncthreads();
+    const long long step = ctrl->step;
+    const bool skip = ctrl->first_inv != kNone && A.policy == 0;  // Abort: no gather (djtled_force.hpp:202-208)
+    const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n < A.N && !skip) {
+        const typename RT<Real>::Node* p = A.ef + (long long)A.slice_base[n >> 5] + (n & 31);
+        if (node_body<Real, kAssemble, false>(A, n, p, A.row_len[n], step)) s_nonfinite = 1;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    if (s_nonfinite) atomicOr(&ctrl->diverged, 1);
+    __threadfence();
+    const unsigned int done = atomicAdd(&ctrl->blocks_done, 1u);
+    if (done != gridDim.x - 1) return;
+    close_step<kAssemble>(ctrl, step, A.policy);
+    __threadfence();
+    ctrl->blocks_done = 0;
+}
+
+// ------------------------------------------------------------------ fused step
+
+// One persistent kernel per step. The work list interleaves element chunks
+// (256 elements) and node chunks (256 nodes) so that every node chunk comes
+// right after the last element chunk it depends on; CTAs take items in list
+// order from an atomic ticket, so every item waits only on items with smaller
+// tickets, which are already running (deadlock-free with any grid size).
+// Force rows go to a ring of R node-chunk regions that stays in L2: a node
+// chunk consumes its region shortly after it is filled, and an element chunk
+// reuses a region only after the region's previous node chunk has consumed it.
+// Summation order per node is unchanged (slot k = k-th element in ascending
+// order), so the result is bit-identical to the two-kernel step.
+struct FusedSched {
+    const int* items;     // >= 0 element chunk, < 0: ~node chunk
+    int n_items;
+    unsigned* edone;      // per element chunk: epoch stamp when its rows are stored
+    unsigned* ndone;      // per node chunk: epoch stamp when its region is consumed
+    const int* ndep_off;  // node chunk -> element chunks it reads
+    const int* ndep;
+    const int* ereuse_off;  // element chunk -> node chunks whose region it reuses
+    const int* ereuse;
+    const int* row_len;
+    int R;                // ring regions
+    int wmax;             // slots per node in a region
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void wait_stamps(const unsigned* flags, const int* ids, int count, unsigned epoch) {
+    for (int q = threadIdx.x; q < count; q += blockDim.x) {
+        const unsigned* f = flags + ids[q];
+        while (ld_acquire(f) != epoch) __nanosleep(40);
+    }
+    __syncthreads();
+}
+
+template <class Real, int KIND, int MODEL, bool kAssemble>
+__global__ void __launch_bounds__(256) k_step_fused(const ElemArgs<Real> EA, const NodeArgs<Real> NA,
+                                                     const FusedSched S) {
+    Ctrl* ctrl = EA.ctrl;
+    if (*(volatile const int*)&ctrl->halted && !kAssemble) return;
+    __shared__ int s_item;
+    __shared__ int s_nonfinite;
+    if (threadIdx.x == 0) s_nonfinite = 0;
+    const unsigned epoch = ctrl->epoch + 1u;
+    const long long step = ctrl->step;
+    const int phase = int(step % 3);
+    const typename RT<Real>::Node* u = EA.u_override ? EA.u_override : pick3(phase, EA.u[0], EA.u[1], EA.u[2]);
+    const long long region = 256ll * S.wmax;
+    for (;;) {
+        if (threadIdx.x == 0) s_item = atomicAdd(&ctrl->ticket, 1);
+        __syncthreads();
+        const int t = s_item;
+        __syncthreads();
+        if (t >= S.n_items) break;
+        const int item = S.items[t];
+        if (item >= 0) {
+            // element chunk: wait until the regions it overwrites are consumed
+            wait_stamps(S.ndone, S.ereuse + S.ereuse_off[item], S.ereuse_off[item + 1] - S.ereuse_off[item], epoch);
+            const long long e = 256ll * item + threadIdx.x;
+            if (e < EA.E) element_body<Real, KIND, MODEL>(EA, e, u);
+            __threadfence();
+            __syncthreads();
+            if (threadIdx.x == 0) st_release(S.edone + item, epoch);
+        } else {
+            const int j = ~item;
+            wait_stamps(S.edone, S.ndep + S.ndep_off[j], S.ndep_off[j + 1] - S.ndep_off[j], epoch);
+            const long long n = 256ll * j + threadIdx.x;
+            if (n < NA.N) {
+                const int l = threadIdx.x;
+                const typename RT<Real>::Node* p =
+                    EA.ef + (long long)(j % S.R) * region + (long long)(l >> 5) * (32ll * S.wmax) + (l & 31);
+                if (node_body<Real, kAssemble, true>(NA, n, p, S.row_len[n], step)) s_nonfinite = 1;
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) st_release(S.ndone + j, epoch);
+        }
+    }
+    if (threadIdx.x != 0) return;
+    if (s_nonfinite) atomicOr(&ctrl->diverged, 1);
+    __threadfence();
+    const unsigned int done = atomicAdd(&ctrl->blocks_done, 1u);
+    if (done != gridDim.x - 1) return;
+    close_step<kAssemble>(ctrl, step, NA.policy);
+    ctrl->ticket = 0;
+    ctrl->epoch = epoch;
     __threadfence();
     ctrl->blocks_done = 0;
 }

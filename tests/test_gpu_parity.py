@@ -30,8 +30,8 @@ def run_gpu(spec, steps, **kw):
     return u, up, rep
 
 
-def check_run(spec, steps, tol=None, exact=True):
-    u, up, rep = run_gpu(spec, steps)
+def check_run(spec, steps, tol=None, exact=True, flags=0):
+    u, up, rep = run_gpu(spec, steps, flags=flags)
     ur, upr, rr = oracle.run(spec, steps, "oracle")
     assert rep.step == rr["step"] and rep.status == rr["status"], (rep, rr)
     tol = TOL[spec.precision] if tol is None else tol
@@ -61,8 +61,24 @@ def test_cfg2_h8_nh_hourglass_2000_steps(precision):
 @pytest.mark.parametrize("precision", [4, 8])
 @pytest.mark.parametrize("kind", ["T4", "H8"])
 @pytest.mark.parametrize("model", ["NH", "TI", "OT", "MR"])
-def test_materials_small(kind, model, precision):
-    check_run(box_spec(kind=kind, model=model, divisions=4, precision=precision, ramp_steps=300), 300)
+@pytest.mark.parametrize("mode", ["fused", "two_kernel"])
+def test_materials_small(kind, model, precision, mode):
+    flags = A.DJG_FLAG_TWO_KERNEL if mode == "two_kernel" else 0
+    check_run(box_spec(kind=kind, model=model, divisions=4, precision=precision, ramp_steps=300), 300, flags=flags)
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2"])
+def test_two_kernel_path_cfg(cfg):
+    check_run(config_spec(cfg, precision=4), 500, flags=A.DJG_FLAG_TWO_KERNEL)
+
+
+def test_fused_engine_is_selected_and_ring_fits_l2():
+    sc = Scenario(config_spec("cfg3", precision=4))
+    with GpuDjEngine(sc) as eng:
+        info = eng.info()
+    assert info["fused"] == 1 and info["kernels_per_step"] == 1
+    assert 0 < info["ring_regions"] <= (sc.num_nodes + 255) // 256
+    assert info["slot_capacity"] * 16 <= 48 << 20
 
 
 @pytest.mark.parametrize("precision", [4, 8])
@@ -152,7 +168,8 @@ def test_deterministic_repeats():
     a = run_gpu(spec, 300)[0]
     b = run_gpu(spec, 300)[0]
     c = run_gpu(spec, 300, flags=A.DJG_FLAG_NO_GRAPH)[0]
-    assert np.array_equal(a, b) and np.array_equal(a, c)
+    d = run_gpu(spec, 300, flags=A.DJG_FLAG_TWO_KERNEL)[0]
+    assert np.array_equal(a, b) and np.array_equal(a, c) and np.array_equal(a, d)
 
 
 def test_resume_from_state_is_bitwise():

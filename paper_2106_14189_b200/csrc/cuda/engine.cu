@@ -401,10 +401,14 @@ public:
         }
         int64_t R = lo;
         while (!ok(R)) ++R;
-        R = std::min<int64_t>(nNC, R + std::max<int64_t>(8, R / 2));  // slack: fewer stalls
-        while (!ok(R)) ++R;
+        // The ring bounds how many element chunks can run ahead of the node
+        // chunks: give it the whole L2 budget (capped by the mesh), not just
+        // the minimum that avoids deadlock.
         const int64_t region = int64_t(C) * wmax_;
-        if (R * region * int64_t(sizeof(Node)) > kRingBudget || R * region > INT32_MAX) return false;
+        const int64_t r_budget = kRingBudget / (region * int64_t(sizeof(Node)));
+        if (R > r_budget || R * region > INT32_MAX) return false;
+        R = std::min<int64_t>(nNC, std::max<int64_t>(R, r_budget));
+        while (!ok(R)) ++R;
         ring_R_ = int(R);
         capacity_ = R * region;
         // ring position of every (element, local node)

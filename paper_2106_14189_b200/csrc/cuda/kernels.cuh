@@ -647,9 +647,13 @@ __global__ void __launch_bounds__(256) k_step_fused(const ElemArgs<Real> EA, con
             wait_stamps(S.ndone, S.ereuse + S.ereuse_off[item], S.ereuse_off[item + 1] - S.ereuse_off[item], epoch);
             const long long e = 256ll * item + threadIdx.x;
             if (e < EA.E) element_body<Real, KIND, MODEL>(EA, e, u);
-            __threadfence();
+            // Publish: CTA barrier, then one gpu-scope release by thread 0
+            // (cumulative over the CTA's writes, as in a grid barrier).
             __syncthreads();
-            if (threadIdx.x == 0) st_release(S.edone + item, epoch);
+            if (threadIdx.x == 0) {
+                __threadfence();
+                st_release(S.edone + item, epoch);
+            }
         } else {
             const int j = ~item;
             wait_stamps(S.edone, S.ndep + S.ndep_off[j], S.ndep_off[j + 1] - S.ndep_off[j], epoch);

@@ -83,6 +83,7 @@ typedef struct djg_desc {
 /* Flags */
 #define DJG_FLAG_NO_GRAPH 1u    /* launch kernels one by one instead of CUDA graphs */
 #define DJG_FLAG_TWO_KERNEL 2u  /* element kernel + node kernel instead of the fused step */
+#define DJG_FLAG_NO_DISCARD 4u  /* fused step: keep consumed force slots in L2 (no discard) */
 
 /* DjEngine(mesh, material, c_hg) (solver.hpp:264-267) at the mesh level:
  * the library runs the precompute (build_element_constants,
@@ -172,8 +173,8 @@ typedef struct djg_engine_info {
     int32_t npe, nconst, const_planes, precision;
     int32_t kernels_per_step;
     int32_t sm_count;
-    int32_t fused;              /* 1: fused persistent step with an L2 force ring */
-    int32_t ring_regions;       /* ring size in 256-node regions (fused) */
+    int32_t fused;              /* 1: fused step (element blocks complete node chunks) */
+    int32_t ring_regions;       /* reserved (0) */
 } djg_engine_info;
 int djg_get_info(djg_engine* eng, djg_engine_info* info);
 

@@ -163,10 +163,9 @@ public:
         }
         if (bad) throw DescError("CSR pairs do not match connectivity");
         wmax_ = std::max(wmax, 1);
+        // Sliced slot layout: node n's k-th slot at slice_base[n/32] + 32k + n%32.
         std::vector<int32_t> slot(size_t(E_ * npe));
-        fused_ = !(flags_ & DJG_FLAG_TWO_KERNEL) && plan_fused(off, celem, cloc, conn, slot);
-        if (!fused_) {
-            // Sliced slot layout: node n's k-th slot at slice_base[n/32] + 32k + n%32.
+        {
             const int64_t S = (N_ + 31) / 32;
             std::vector<int32_t> slice_base(static_cast<size_t>(S) + 1);
             int64_t cap = 0;
@@ -188,6 +187,7 @@ public:
             slicebase_.alloc(slice_base.size() * sizeof(int32_t));
             CK(cudaMemcpy(slicebase_.p, slice_base.data(), slicebase_.bytes, cudaMemcpyHostToDevice));
         }
+        fused_ = !(flags_ & DJG_FLAG_TWO_KERNEL) && plan_fused(off, celem, conn);
 
         // Upload connectivity and slots as int4 planes.
         const int nq = npe / 4;
@@ -335,115 +335,54 @@ public:
         drop_graphs();
     }
 
-    // Work list, dependency lists and ring layout of the fused step (see
-    // kernels.cuh, k_step_fused). Returns false when the mesh ordering would
-    // need a ring larger than the L2 budget; the engine then uses the
-    // two-kernel step.
-    bool plan_fused(const int64_t* off, const int64_t* celem, const int32_t* cloc, const int32_t* conn,
-                    std::vector<int32_t>& slot) {
+    // Dependency counts of the fused step (kernels.cuh, k_step_fused): for
+    // every 256-node chunk the number of distinct 256-element blocks writing
+    // to it, and for every element block the chunks it writes. Returns false
+    // (two-kernel step) if a block touches more chunks than the kernel's
+    // shared list holds.
+    bool plan_fused(const int64_t* off, const int64_t* celem, const int32_t* conn) {
         constexpr int C = 256;
-        if (wmax_ > 255) return false;
         const int npe = npe_;
-        const int64_t nEC = (E_ + C - 1) / C, nNC = (N_ + C - 1) / C;
-        // node chunk -> element chunks it reads
-        std::vector<std::vector<int>> ndep(static_cast<size_t>(nNC));
-        std::vector<int> need(static_cast<size_t>(nNC), -1);
+        const int64_t nEB = (E_ + C - 1) / C, nNC = (N_ + C - 1) / C;
+        std::vector<int> deps(static_cast<size_t>(nNC), 0);
 #pragma omp parallel for schedule(dynamic, 64)
         for (int64_t j = 0; j < nNC; ++j) {
-            auto& v = ndep[size_t(j)];
+            std::vector<int64_t> v;
             for (int64_t n = j * C; n < std::min<int64_t>(N_, (j + 1) * C); ++n)
-                for (int64_t p = off[n]; p < off[n + 1]; ++p) v.push_back(int(celem[p] / C));
+                for (int64_t p = off[n]; p < off[n + 1]; ++p) v.push_back(celem[p] / C);
             std::sort(v.begin(), v.end());
-            v.erase(std::unique(v.begin(), v.end()), v.end());
-            need[size_t(j)] = v.empty() ? -1 : v.back();
+            deps[size_t(j)] = int(std::unique(v.begin(), v.end()) - v.begin());
         }
-        // element chunk -> node chunks it writes
-        std::vector<std::vector<int>> tgt(static_cast<size_t>(nEC));
-#pragma omp parallel for schedule(dynamic, 64)
-        for (int64_t i = 0; i < nEC; ++i) {
-            auto& v = tgt[size_t(i)];
-            for (int64_t e = i * C; e < std::min<int64_t>(E_, (i + 1) * C); ++e)
+        std::vector<std::vector<int>> tgt(static_cast<size_t>(nEB));
+        int max_t = 0;
+#pragma omp parallel for schedule(dynamic, 64) reduction(max : max_t)
+        for (int64_t b = 0; b < nEB; ++b) {
+            auto& v = tgt[size_t(b)];
+            for (int64_t e = b * C; e < std::min<int64_t>(E_, (b + 1) * C); ++e)
                 for (int a = 0; a < npe; ++a) v.push_back(int(conn[e * npe + a] / C));
             std::sort(v.begin(), v.end());
             v.erase(std::unique(v.begin(), v.end()), v.end());
+            max_t = std::max(max_t, int(v.size()));
         }
-        // work list: a node chunk right after the last element chunk it needs
-        std::vector<std::vector<int>> after(static_cast<size_t>(nEC));
-        std::vector<int> items;
-        items.reserve(size_t(nEC + nNC));
-        for (int64_t j = 0; j < nNC; ++j) {
-            if (need[size_t(j)] < 0) items.push_back(~int(j));
-            else after[size_t(need[size_t(j)])].push_back(int(j));
+        if (max_t > 32) return false;
+        std::vector<int> t_off(static_cast<size_t>(nEB) + 1, 0), t_flat, orphans;
+        for (int64_t b = 0; b < nEB; ++b) {
+            t_flat.insert(t_flat.end(), tgt[size_t(b)].begin(), tgt[size_t(b)].end());
+            t_off[size_t(b + 1)] = int(t_flat.size());
         }
-        std::vector<int64_t> posE(static_cast<size_t>(nEC)), posN(static_cast<size_t>(nNC));
-        for (int64_t q = 0; q < int64_t(items.size()); ++q) posN[size_t(~items[size_t(q)])] = q;
-        for (int64_t i = 0; i < nEC; ++i) {
-            posE[size_t(i)] = int64_t(items.size());
-            items.push_back(int(i));
-            for (int j : after[size_t(i)]) {
-                posN[size_t(j)] = int64_t(items.size());
-                items.push_back(~j);
-            }
-        }
-        // Ring size: an element chunk may overwrite region t % R only after
-        // node chunk t - R (earlier in the list) consumed it.
-        auto ok = [&](int64_t R) {
-            for (int64_t i = 0; i < nEC; ++i)
-                for (int t : tgt[size_t(i)])
-                    if (t >= R && posN[size_t(t - R)] > posE[size_t(i)]) return false;
-            return true;
-        };
-        int64_t lo = 1, hi = nNC;
-        while (lo < hi) {
-            const int64_t mid = (lo + hi) / 2;
-            if (ok(mid)) hi = mid;
-            else lo = mid + 1;
-        }
-        int64_t R = lo;
-        while (!ok(R)) ++R;
-        // The ring bounds how many element chunks can run ahead of the node
-        // chunks: give it the whole L2 budget (capped by the mesh), not just
-        // the minimum that avoids deadlock.
-        const int64_t region = int64_t(C) * wmax_;
-        const int64_t r_budget = kRingBudget / (region * int64_t(sizeof(Node)));
-        if (R > r_budget || R * region > INT32_MAX) return false;
-        R = std::min<int64_t>(nNC, std::max<int64_t>(R, r_budget));
-        while (!ok(R)) ++R;
-        ring_R_ = int(R);
-        capacity_ = R * region;
-        // ring position of every (element, local node)
-#pragma omp parallel for schedule(static)
-        for (int64_t n = 0; n < N_; ++n) {
-            const int64_t l = n % C;
-            const int64_t base = ((n / C) % R) * region + (l / 32) * 32 * wmax_ + (l % 32);
-            for (int64_t p = off[n]; p < off[n + 1]; ++p)
-                slot[size_t(celem[p] * npe + cloc[p])] = int32_t(base + 32 * (p - off[n]));
-        }
-        // flatten dependency lists
-        std::vector<int> ndep_off(static_cast<size_t>(nNC) + 1, 0), ndep_flat;
-        for (int64_t j = 0; j < nNC; ++j) ndep_off[size_t(j + 1)] = ndep_off[size_t(j)] + int(ndep[size_t(j)].size());
-        ndep_flat.reserve(size_t(ndep_off.back()));
-        for (auto& v : ndep) ndep_flat.insert(ndep_flat.end(), v.begin(), v.end());
-        std::vector<int> er_off(static_cast<size_t>(nEC) + 1, 0), er_flat;
-        for (int64_t i = 0; i < nEC; ++i) {
-            for (int t : tgt[size_t(i)])
-                if (t >= R) er_flat.push_back(int(t - R));
-            er_off[size_t(i + 1)] = int(er_flat.size());
-        }
+        for (int64_t j = 0; j < nNC; ++j)
+            if (deps[size_t(j)] == 0) orphans.push_back(int(j));
         auto up = [&](DevBuf& b, const std::vector<int>& v) {
             b.alloc(std::max<size_t>(v.size(), 1) * sizeof(int));
             if (!v.empty()) CK(cudaMemcpy(b.p, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
         };
-        up(items_, items);
-        up(ndepOff_, ndep_off);
-        up(ndep_, ndep_flat);
-        up(ereuseOff_, er_off);
-        up(ereuse_, er_flat);
-        edone_.alloc(size_t(nEC) * sizeof(unsigned));
-        ndone_.alloc(size_t(nNC) * sizeof(unsigned));
-        CK(cudaMemset(edone_.p, 0, edone_.bytes));
-        CK(cudaMemset(ndone_.p, 0, ndone_.bytes));
-        n_items_ = int(items.size());
+        up(deps_, deps);
+        up(pending_, deps);
+        up(tgtOff_, t_off);
+        up(tgt_, t_flat);
+        up(orphans_, orphans);
+        n_orphans_ = int(orphans.size());
+        n_chunks_ = int(nNC);
         return true;
     }
 
@@ -556,15 +495,12 @@ public:
     void launch_fused_km(cudaStream_t s, bool assemble_mode, const Node* u_override) {
         ElemArgs<Real> a = ea_;
         a.u_override = u_override;
-        FusedSched S{items_.as<int>(), n_items_, edone_.as<unsigned>(), ndone_.as<unsigned>(), ndepOff_.as<int>(),
-                     ndep_.as<int>(), ereuseOff_.as<int>(), ereuse_.as<int>(), rowlen_.as<int>(), ring_R_, wmax_};
-        auto kern = assemble_mode ? k_step_fused<Real, K, M, true> : k_step_fused<Real, K, M, false>;
-        if (fused_grid_ == 0) {
-            int per_sm = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_step_fused<Real, K, M, false>, 256, 0));
-            fused_grid_ = std::max(1, per_sm) * sms_;
-        }
-        kern<<<fused_grid_, 256, 0, s>>>(a, na_, S);
+        FusedSched S{pending_.as<int>(), deps_.as<int>(), tgtOff_.as<int>(), tgt_.as<int>(), orphans_.as<int>(),
+                     n_orphans_, n_chunks_, rowlen_.as<int>(), slicebase_.as<int>(),
+                     (flags_ & DJG_FLAG_NO_DISCARD) ? 0 : 1};
+        const unsigned grid = unsigned((E_ + 255) / 256);
+        if (assemble_mode) k_step_fused<Real, K, M, true><<<grid, 256, 0, s>>>(a, na_, S);
+        else k_step_fused<Real, K, M, false><<<grid, 256, 0, s>>>(a, na_, S);
         CK(cudaGetLastError());
     }
 
@@ -743,14 +679,13 @@ public:
         o->device_bytes = int64_t(conn_.bytes + slot_.bytes + consts_.bytes + 3 * u_[0].bytes + uscratch_.bytes +
                                   flat_.bytes + ef_.bytes + rowlen_.bytes + slicebase_.bytes + c1_.bytes +
                                   code_.bytes + target_.bytes + tTotal_.bytes + rext_.bytes + ctrl_.bytes +
-                                  items_.bytes + ndepOff_.bytes + ndep_.bytes + ereuseOff_.bytes + ereuse_.bytes +
-                                  edone_.bytes + ndone_.bytes);
+                                  deps_.bytes + pending_.bytes + tgtOff_.bytes + tgt_.bytes + orphans_.bytes);
         o->npe = npe_;
         o->nconst = nconst_;
         o->const_planes = nplanes_;
         o->precision = int32_t(sizeof(Real));
         o->kernels_per_step = fused_ ? 1 : 2;
-        o->ring_regions = ring_R_;
+        o->ring_regions = 0;
         o->fused = fused_ ? 1 : 0;
         o->sm_count = sms_;
     }
@@ -780,10 +715,9 @@ private:
     bool configured_ = false;
     bool ctrl_initialized_ = false;
     // fused step
-    static constexpr int64_t kRingBudget = int64_t(48) << 20;  // bytes of force ring kept in L2
     bool fused_ = false;
-    int ring_R_ = 0, wmax_ = 1, n_items_ = 0, fused_grid_ = 0;
-    DevBuf items_, ndepOff_, ndep_, ereuseOff_, ereuse_, edone_, ndone_;
+    int wmax_ = 1, n_orphans_ = 0, n_chunks_ = 0;
+    DevBuf deps_, pending_, tgtOff_, tgt_, orphans_;
 };
 
 int debug_cbrt(int32_t precision, const void* in, void* out, int64_t n, int32_t device) {

@@ -580,46 +580,51 @@ __global__ void __launch_bounds__(256) k_node(const NodeArgs<Real> A) {
 
 // ------------------------------------------------------------------ fused step
 
-// One persistent kernel per step. The work list interleaves element chunks
-// (256 elements) and node chunks (256 nodes) so that every node chunk comes
-// right after the last element chunk it depends on; CTAs take items in list
-// order from an atomic ticket, so every item waits only on items with smaller
-// tickets, which are already running (deadlock-free with any grid size).
-// Force rows go to a ring of R node-chunk regions that stays in L2: a node
-// chunk consumes its region shortly after it is filled, and an element chunk
-// reuses a region only after the region's previous node chunk has consumed it.
-// Summation order per node is unchanged (slot k = k-th element in ascending
-// order), so the result is bit-identical to the two-kernel step.
+// One kernel per step, no waiting anywhere. Blocks of 256 elements are
+// scheduled by the hardware in (roughly) ascending order. After storing its
+// force rows, a block decrements the pending-count of every 256-node chunk it
+// wrote to; the block that brings a count to zero owns that node chunk and
+// gathers + updates its nodes right away, while the rows are still in L2, then
+// discards the consumed slot lines from L2 (discard.global.L2) so they are
+// never written back to HBM. Each node still sums its slots in ascending
+// element order, so the step is bit-identical to the two-kernel step.
 struct FusedSched {
-    const int* items;     // >= 0 element chunk, < 0: ~node chunk
-    int n_items;
-    unsigned* edone;      // per element chunk: epoch stamp when its rows are stored
-    unsigned* ndone;      // per node chunk: epoch stamp when its region is consumed
-    const int* ndep_off;  // node chunk -> element chunks it reads
-    const int* ndep;
-    const int* ereuse_off;  // element chunk -> node chunks whose region it reuses
-    const int* ereuse;
+    int* pending;          // per node chunk: element blocks still to store (reset after use)
+    const int* deps;       // per node chunk: number of element blocks writing to it
+    const int* tgt_off;    // element block -> node chunks it writes
+    const int* tgt;
+    const int* orphans;    // node chunks no element touches (processed by block 0)
+    int n_orphans;
+    int n_chunks;
     const int* row_len;
-    int R;                // ring regions
-    int wmax;             // slots per node in a region
+    const int* slice_base; // sliced slot layout (shared with the two-kernel path)
+    int discard;           // 1: discard consumed slot lines from L2
 };
 
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-    return v;
+__device__ __forceinline__ void l2_discard(const void* p) {
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
 
-__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
-    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
-__device__ __forceinline__ void wait_stamps(const unsigned* flags, const int* ids, int count, unsigned epoch) {
-    for (int q = threadIdx.x; q < count; q += blockDim.x) {
-        const unsigned* f = flags + ids[q];
-        while (ld_acquire(f) != epoch) __nanosleep(40);
+template <class Real, bool kAssemble>
+__device__ __forceinline__ bool node_chunk(const NodeArgs<Real>& NA, const FusedSched& S,
+                                           const typename RT<Real>::Node* ef, int j, long long step) {
+    bool nf = false;
+    const long long n = 256ll * j + threadIdx.x;
+    if (n < NA.N) {
+        const typename RT<Real>::Node* p = ef + (long long)S.slice_base[n >> 5] + (n & 31);
+        nf = node_body<Real, kAssemble, true>(NA, n, p, S.row_len[n], step);
     }
-    __syncthreads();
+    __syncthreads();  // every slot of the chunk has been read
+    if (S.discard) {
+        // the chunk's 8 slices are contiguous and 128-byte aligned
+        const long long s0 = 8ll * j;
+        const long long s1 = min(s0 + 8, (NA.N + 31) / 32);
+        const char* lo = reinterpret_cast<const char*>(ef + S.slice_base[s0]);
+        const char* hi = reinterpret_cast<const char*>(ef + S.slice_base[s1]);
+        for (const char* q = lo + 128ll * threadIdx.x; q < hi; q += 128ll * blockDim.x) l2_discard(q);
+    }
+    if (threadIdx.x == 0) S.pending[j] = S.deps[j];  // re-arm for the next step
+    return nf;
 }
 
 template <class Real, int KIND, int MODEL, bool kAssemble>
@@ -627,55 +632,44 @@ __global__ void __launch_bounds__(256) k_step_fused(const ElemArgs<Real> EA, con
                                                      const FusedSched S) {
     Ctrl* ctrl = EA.ctrl;
     if (*(volatile const int*)&ctrl->halted && !kAssemble) return;
-    __shared__ int s_item;
-    __shared__ int s_nonfinite;
-    if (threadIdx.x == 0) s_nonfinite = 0;
-    const unsigned epoch = ctrl->epoch + 1u;
+    __shared__ int s_ready[32];
+    __shared__ int s_nready;
+    __shared__ int s_nf;
+    if (threadIdx.x == 0) {
+        s_nready = 0;
+        s_nf = 0;
+    }
     const long long step = ctrl->step;
     const int phase = int(step % 3);
     const typename RT<Real>::Node* u = EA.u_override ? EA.u_override : pick3(phase, EA.u[0], EA.u[1], EA.u[2]);
-    const long long region = 256ll * S.wmax;
-    for (;;) {
-        if (threadIdx.x == 0) s_item = atomicAdd(&ctrl->ticket, 1);
-        __syncthreads();
-        const int t = s_item;
-        __syncthreads();
-        if (t >= S.n_items) break;
-        const int item = S.items[t];
-        if (item >= 0) {
-            // element chunk: wait until the regions it overwrites are consumed
-            wait_stamps(S.ndone, S.ereuse + S.ereuse_off[item], S.ereuse_off[item + 1] - S.ereuse_off[item], epoch);
-            const long long e = 256ll * item + threadIdx.x;
-            if (e < EA.E) element_body<Real, KIND, MODEL>(EA, e, u);
-            // Publish: CTA barrier, then one gpu-scope release by thread 0
-            // (cumulative over the CTA's writes, as in a grid barrier).
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                __threadfence();
-                st_release(S.edone + item, epoch);
-            }
-        } else {
-            const int j = ~item;
-            wait_stamps(S.edone, S.ndep + S.ndep_off[j], S.ndep_off[j + 1] - S.ndep_off[j], epoch);
-            const long long n = 256ll * j + threadIdx.x;
-            if (n < NA.N) {
-                const int l = threadIdx.x;
-                const typename RT<Real>::Node* p =
-                    EA.ef + (long long)(j % S.R) * region + (long long)(l >> 5) * (32ll * S.wmax) + (l & 31);
-                if (node_body<Real, kAssemble, true>(NA, n, p, S.row_len[n], step)) s_nonfinite = 1;
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) st_release(S.ndone + j, epoch);
+    bool nf = false;
+    if (blockIdx.x == 0)
+        for (int q = 0; q < S.n_orphans; ++q) nf |= node_chunk<Real, kAssemble>(NA, S, EA.ef, S.orphans[q], step);
+    const long long e = 256ll * blockIdx.x + threadIdx.x;
+    if (e < EA.E) element_body<Real, KIND, MODEL>(EA, e, u);
+    __syncthreads();
+    // Release this block's rows, then count them in (one lane per target
+    // chunk: fence and signalling atomic in the same thread).
+    const int t0 = S.tgt_off[blockIdx.x], t1 = S.tgt_off[blockIdx.x + 1];
+    for (int q = t0 + threadIdx.x; q < t1; q += blockDim.x) {
+        __threadfence();
+        const int j = S.tgt[q];
+        if (atomicSub(S.pending + j, 1) == 1) {
+            __threadfence();  // acquire the other blocks' rows of chunk j
+            s_ready[atomicAdd(&s_nready, 1) & 31] = j;
         }
     }
+    __syncthreads();
+    const int nready = s_nready;
+    for (int r = 0; r < nready; ++r) nf |= node_chunk<Real, kAssemble>(NA, S, EA.ef, s_ready[r], step);
+    if (nf) s_nf = 1;
+    __syncthreads();
     if (threadIdx.x != 0) return;
-    if (s_nonfinite) atomicOr(&ctrl->diverged, 1);
+    if (s_nf) atomicOr(&ctrl->diverged, 1);
     __threadfence();
     const unsigned int done = atomicAdd(&ctrl->blocks_done, 1u);
     if (done != gridDim.x - 1) return;
     close_step<kAssemble>(ctrl, step, NA.policy);
-    ctrl->ticket = 0;
-    ctrl->epoch = epoch;
     __threadfence();
     ctrl->blocks_done = 0;
 }

@@ -30,7 +30,8 @@ def main(names):
             t0 = time.perf_counter()
             sc = Scenario(config_spec(name, precision=prec, target=0.01, ramp_steps=100000))
             t1 = time.perf_counter()
-            eng = GpuDjEngine(sc)
+            import os
+            eng = GpuDjEngine(sc, flags=int(os.environ.get('DJG_FLAGS', '0')))
             t2 = time.perf_counter()
             eng.step(10)
             ms_e, ms_n, ms_t = eng.profile_steps(50)

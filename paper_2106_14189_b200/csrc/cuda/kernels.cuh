@@ -464,7 +464,18 @@ __device__ __forceinline__ void gather_row(const typename RT<Real>::Node* __rest
                                            Real& sy, Real& sz) {
     using T = RT<Real>;
     sx = Real(0); sy = Real(0); sz = Real(0);
-    for (int k = 0; k < len; ++k) {
+    int k = 0;
+    // Loads issued 4 at a time (independent), sums still strictly in slot order.
+    for (; k + 4 <= len; k += 4) {
+        typename T::Node v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = kCG ? T::load_l2(p + 32 * (k + q)) : T::load_stream(p + 32 * (k + q));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            sx += v[q].x; sy += v[q].y; sz += v[q].z;
+        }
+    }
+    for (; k < len; ++k) {
         const typename T::Node v = kCG ? T::load_l2(p + 32 * k) : T::load_stream(p + 32 * k);
         sx += v.x; sy += v.y; sz += v.z;
     }

@@ -336,41 +336,37 @@ public:
     }
 
     // Dependency counts of the fused step (kernels.cuh, k_step_fused): for
-    // every 256-node chunk the number of distinct 256-element blocks writing
-    // to it, and for every element block the chunks it writes. Returns false
-    // (two-kernel step) if a block touches more chunks than the kernel's
-    // shared list holds.
+    // every 32-node slice the number of distinct 32-element groups writing to
+    // it, and for every group the slices it writes.
     bool plan_fused(const int64_t* off, const int64_t* celem, const int32_t* conn) {
-        constexpr int C = 256;
+        constexpr int C = 32;
         const int npe = npe_;
-        const int64_t nEB = (E_ + C - 1) / C, nNC = (N_ + C - 1) / C;
-        std::vector<int> deps(static_cast<size_t>(nNC), 0);
-#pragma omp parallel for schedule(dynamic, 64)
-        for (int64_t j = 0; j < nNC; ++j) {
+        const int64_t nG = (E_ + C - 1) / C, nS = (N_ + C - 1) / C;
+        std::vector<int> deps(static_cast<size_t>(nS), 0);
+#pragma omp parallel for schedule(dynamic, 256)
+        for (int64_t j = 0; j < nS; ++j) {
             std::vector<int64_t> v;
             for (int64_t n = j * C; n < std::min<int64_t>(N_, (j + 1) * C); ++n)
                 for (int64_t p = off[n]; p < off[n + 1]; ++p) v.push_back(celem[p] / C);
             std::sort(v.begin(), v.end());
             deps[size_t(j)] = int(std::unique(v.begin(), v.end()) - v.begin());
         }
-        std::vector<std::vector<int>> tgt(static_cast<size_t>(nEB));
-        int max_t = 0;
-#pragma omp parallel for schedule(dynamic, 64) reduction(max : max_t)
-        for (int64_t b = 0; b < nEB; ++b) {
-            auto& v = tgt[size_t(b)];
-            for (int64_t e = b * C; e < std::min<int64_t>(E_, (b + 1) * C); ++e)
+        std::vector<std::vector<int>> tgt(static_cast<size_t>(nG));
+#pragma omp parallel for schedule(dynamic, 256)
+        for (int64_t g = 0; g < nG; ++g) {
+            auto& v = tgt[size_t(g)];
+            for (int64_t e = g * C; e < std::min<int64_t>(E_, (g + 1) * C); ++e)
                 for (int a = 0; a < npe; ++a) v.push_back(int(conn[e * npe + a] / C));
             std::sort(v.begin(), v.end());
             v.erase(std::unique(v.begin(), v.end()), v.end());
-            max_t = std::max(max_t, int(v.size()));
         }
-        if (max_t > 32) return false;
-        std::vector<int> t_off(static_cast<size_t>(nEB) + 1, 0), t_flat, orphans;
-        for (int64_t b = 0; b < nEB; ++b) {
-            t_flat.insert(t_flat.end(), tgt[size_t(b)].begin(), tgt[size_t(b)].end());
-            t_off[size_t(b + 1)] = int(t_flat.size());
-        }
-        for (int64_t j = 0; j < nNC; ++j)
+        std::vector<int> t_off(static_cast<size_t>(nG) + 1, 0), t_flat, orphans;
+        for (int64_t g = 0; g < nG; ++g) t_off[size_t(g + 1)] = t_off[size_t(g)] + int(tgt[size_t(g)].size());
+        t_flat.resize(size_t(t_off.back()));
+#pragma omp parallel for schedule(static)
+        for (int64_t g = 0; g < nG; ++g)
+            std::copy(tgt[size_t(g)].begin(), tgt[size_t(g)].end(), t_flat.begin() + t_off[size_t(g)]);
+        for (int64_t j = 0; j < nS; ++j)
             if (deps[size_t(j)] == 0) orphans.push_back(int(j));
         auto up = [&](DevBuf& b, const std::vector<int>& v) {
             b.alloc(std::max<size_t>(v.size(), 1) * sizeof(int));
@@ -382,7 +378,7 @@ public:
         up(tgt_, t_flat);
         up(orphans_, orphans);
         n_orphans_ = int(orphans.size());
-        n_chunks_ = int(nNC);
+        n_chunks_ = int(nS);
         return true;
     }
 

@@ -447,8 +447,8 @@ template <class Real, int KIND, int MODEL>
 __global__ void __launch_bounds__(128) k_element(const ElemArgs<Real> A) {
     const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= A.E) return;
-    if (*(volatile const int*)&A.ctrl->halted) return;
-    const int phase = int(A.ctrl->step % 3);
+    if (__ldcg(&A.ctrl->halted)) return;
+    const int phase = int(__ldcg(&A.ctrl->step) % 3);
     const typename RT<Real>::Node* u = A.u_override ? A.u_override : pick3(phase, A.u[0], A.u[1], A.u[2]);
     element_body<Real, KIND, MODEL>(A, e, u);
 }
@@ -567,7 +567,7 @@ __device__ __forceinline__ void close_step(Ctrl* ctrl, long long step, int polic
 template <class Real, bool kAssemble>
 __global__ void __launch_bounds__(256) k_node(const NodeArgs<Real> A) {
     Ctrl* ctrl = A.ctrl;
-    if (*(volatile const int*)&ctrl->halted && !kAssemble) return;
+    if (__ldcg(&ctrl->halted) && !kAssemble) return;
     __shared__ int s_nonfinite;
     if (threadIdx.x == 0) s_nonfinite = 0;
     __syncthreads();
@@ -591,22 +591,22 @@ __global__ void __launch_bounds__(256) k_node(const NodeArgs<Real> A) {
 
 // ------------------------------------------------------------------ fused step
 
-// One kernel per step, no waiting anywhere. Blocks of 256 elements are
-// scheduled by the hardware in (roughly) ascending order. After storing its
-// force rows, a block decrements the pending-count of every 256-node chunk it
-// wrote to; the block that brings a count to zero owns that node chunk and
-// gathers + updates its nodes right away, while the rows are still in L2, then
-// discards the consumed slot lines from L2 (discard.global.L2) so they are
-// never written back to HBM. Each node still sums its slots in ascending
-// element order, so the step is bit-identical to the two-kernel step.
+// One kernel per step, no waiting and no block barriers. Each warp computes 32
+// consecutive elements and stores their force rows; it then decrements the
+// pending-count of every 32-node slice it wrote to, and when a count reaches
+// zero the same warp gathers that slice (all its rows are stored and, having
+// just been written, still in L2), updates its 32 nodes and discards the
+// consumed slot lines from L2 (discard.global.L2) so they are never written
+// back to HBM. Each node still sums its slots in ascending element order, so
+// the step is bit-identical to the two-kernel step.
 struct FusedSched {
-    int* pending;          // per node chunk: element blocks still to store (reset after use)
-    const int* deps;       // per node chunk: number of element blocks writing to it
-    const int* tgt_off;    // element block -> node chunks it writes
+    int* pending;          // per slice: warp groups still to store (re-armed after use)
+    const int* deps;       // per slice: number of warp groups writing to it
+    const int* tgt_off;    // warp group (32 elements) -> slices it writes
     const int* tgt;
-    const int* orphans;    // node chunks no element touches (processed by block 0)
+    const int* orphans;    // slices no element touches (handled by warp group 0)
     int n_orphans;
-    int n_chunks;
+    int n_slices;
     const int* row_len;
     const int* slice_base; // sliced slot layout (shared with the two-kernel path)
     int discard;           // 1: discard consumed slot lines from L2
@@ -616,25 +616,22 @@ __device__ __forceinline__ void l2_discard(const void* p) {
     asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
 }
 
+// Gather + update of slice s by the calling warp (lane = node within slice).
 template <class Real, bool kAssemble>
-__device__ __forceinline__ bool node_chunk(const NodeArgs<Real>& NA, const FusedSched& S,
-                                           const typename RT<Real>::Node* ef, int j, long long step) {
+__device__ __forceinline__ bool slice_update(const NodeArgs<Real>& NA, const FusedSched& S,
+                                             const typename RT<Real>::Node* ef, int s, long long step) {
+    const int lane = threadIdx.x & 31;
+    const long long n = 32ll * s + lane;
     bool nf = false;
-    const long long n = 256ll * j + threadIdx.x;
-    if (n < NA.N) {
-        const typename RT<Real>::Node* p = ef + (long long)S.slice_base[n >> 5] + (n & 31);
-        nf = node_body<Real, kAssemble, true>(NA, n, p, S.row_len[n], step);
-    }
-    __syncthreads();  // every slot of the chunk has been read
+    if (n < NA.N)
+        nf = node_body<Real, kAssemble, true>(NA, n, ef + (long long)S.slice_base[s] + lane, S.row_len[n], step);
+    __syncwarp();
     if (S.discard) {
-        // the chunk's 8 slices are contiguous and 128-byte aligned
-        const long long s0 = 8ll * j;
-        const long long s1 = min(s0 + 8, (NA.N + 31) / 32);
-        const char* lo = reinterpret_cast<const char*>(ef + S.slice_base[s0]);
-        const char* hi = reinterpret_cast<const char*>(ef + S.slice_base[s1]);
-        for (const char* q = lo + 128ll * threadIdx.x; q < hi; q += 128ll * blockDim.x) l2_discard(q);
+        const char* lo = reinterpret_cast<const char*>(ef + S.slice_base[s]);
+        const char* hi = reinterpret_cast<const char*>(ef + S.slice_base[s + 1]);
+        for (const char* q = lo + 128 * lane; q < hi; q += 128 * 32) l2_discard(q);
     }
-    if (threadIdx.x == 0) S.pending[j] = S.deps[j];  // re-arm for the next step
+    if (lane == 0) S.pending[s] = S.deps[s];  // re-arm for the next step
     return nf;
 }
 
@@ -642,37 +639,41 @@ template <class Real, int KIND, int MODEL, bool kAssemble>
 __global__ void __launch_bounds__(256) k_step_fused(const ElemArgs<Real> EA, const NodeArgs<Real> NA,
                                                      const FusedSched S) {
     Ctrl* ctrl = EA.ctrl;
-    if (*(volatile const int*)&ctrl->halted && !kAssemble) return;
-    __shared__ int s_ready[32];
-    __shared__ int s_nready;
+    if (__ldcg(&ctrl->halted) && !kAssemble) return;
     __shared__ int s_nf;
-    if (threadIdx.x == 0) {
-        s_nready = 0;
-        s_nf = 0;
-    }
-    const long long step = ctrl->step;
+    if (threadIdx.x == 0) s_nf = 0;
+    const long long step = __ldcg(&ctrl->step);
     const int phase = int(step % 3);
     const typename RT<Real>::Node* u = EA.u_override ? EA.u_override : pick3(phase, EA.u[0], EA.u[1], EA.u[2]);
+    const int lane = threadIdx.x & 31;
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long group = e >> 5;
     bool nf = false;
-    if (blockIdx.x == 0)
-        for (int q = 0; q < S.n_orphans; ++q) nf |= node_chunk<Real, kAssemble>(NA, S, EA.ef, S.orphans[q], step);
-    const long long e = 256ll * blockIdx.x + threadIdx.x;
+    if (group == 0)
+        for (int q = 0; q < S.n_orphans; ++q) nf |= slice_update<Real, kAssemble>(NA, S, EA.ef, S.orphans[q], step);
     if (e < EA.E) element_body<Real, KIND, MODEL>(EA, e, u);
-    __syncthreads();
-    // Release this block's rows, then count them in (one lane per target
-    // chunk: fence and signalling atomic in the same thread).
-    const int t0 = S.tgt_off[blockIdx.x], t1 = S.tgt_off[blockIdx.x + 1];
-    for (int q = t0 + threadIdx.x; q < t1; q += blockDim.x) {
-        __threadfence();
-        const int j = S.tgt[q];
-        if (atomicSub(S.pending + j, 1) == 1) {
-            __threadfence();  // acquire the other blocks' rows of chunk j
-            s_ready[atomicAdd(&s_nready, 1) & 31] = j;
+    // Release: every lane fences its own stores before the warp rendezvous,
+    // so any lane's signalling atomic is ordered after all 32 rows.
+    __threadfence();
+    __syncwarp();
+    if (group * 32 < EA.E) {
+        const int t0 = S.tgt_off[group], t1 = S.tgt_off[group + 1];
+        for (int base = t0; base < t1; base += 32) {
+            int sl = -1;
+            bool ready = false;
+            if (base + lane < t1) {
+                sl = S.tgt[base + lane];
+                ready = atomicSub(S.pending + sl, 1) == 1;
+                if (ready) __threadfence();  // acquire the other groups' rows
+            }
+            unsigned mask = __ballot_sync(0xffffffffu, ready);
+            while (mask) {
+                const int src = __ffs(mask) - 1;
+                mask &= mask - 1;
+                nf |= slice_update<Real, kAssemble>(NA, S, EA.ef, __shfl_sync(0xffffffffu, sl, src), step);
+            }
         }
     }
-    __syncthreads();
-    const int nready = s_nready;
-    for (int r = 0; r < nready; ++r) nf |= node_chunk<Real, kAssemble>(NA, S, EA.ef, s_ready[r], step);
     if (nf) s_nf = 1;
     __syncthreads();
     if (threadIdx.x != 0) return;

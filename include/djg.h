@@ -82,8 +82,8 @@ typedef struct djg_desc {
 
 /* Flags */
 #define DJG_FLAG_NO_GRAPH 1u    /* launch kernels one by one instead of CUDA graphs */
-#define DJG_FLAG_TWO_KERNEL 2u  /* element kernel + node kernel instead of the fused step */
-#define DJG_FLAG_NO_DISCARD 4u  /* fused step: keep consumed force slots in L2 (no discard) */
+#define DJG_FLAG_TWO_KERNEL 2u  /* one slab: whole-mesh element kernel, then whole-mesh node kernel */
+#define DJG_FLAG_NO_DISCARD 4u  /* slab step: keep consumed force rows in L2 (no discard) */
 
 /* DjEngine(mesh, material, c_hg) (solver.hpp:264-267) at the mesh level:
  * the library runs the precompute (build_element_constants,
@@ -171,10 +171,11 @@ typedef struct djg_engine_info {
     int64_t slot_capacity;      /* force-slot buffer entries (sliced layout incl. padding) */
     int64_t device_bytes;       /* device memory held by the engine */
     int32_t npe, nconst, const_planes, precision;
-    int32_t kernels_per_step;
+    int32_t kernels_per_step;   /* kernel launches per step */
     int32_t sm_count;
-    int32_t fused;              /* 1: fused step (element blocks complete node chunks) */
-    int32_t ring_regions;       /* reserved (0) */
+    int32_t slabs;              /* element slabs per step (2 kernels each) */
+    int32_t _pad;
+    int64_t slab_elements;      /* elements per slab */
 } djg_engine_info;
 int djg_get_info(djg_engine* eng, djg_engine_info* info);
 

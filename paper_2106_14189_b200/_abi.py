@@ -137,8 +137,8 @@ class djg_engine_info(C.Structure):
         ("num_nodes", C.c_int64), ("num_elements", C.c_int64), ("num_slots", C.c_int64),
         ("slot_capacity", C.c_int64), ("device_bytes", C.c_int64),
         ("npe", C.c_int32), ("nconst", C.c_int32), ("const_planes", C.c_int32), ("precision", C.c_int32),
-        ("kernels_per_step", C.c_int32), ("sm_count", C.c_int32), ("fused", C.c_int32),
-        ("ring_regions", C.c_int32),
+        ("kernels_per_step", C.c_int32), ("sm_count", C.c_int32), ("slabs", C.c_int32),
+        ("_pad", C.c_int32), ("slab_elements", C.c_int64),
     ]
 
 

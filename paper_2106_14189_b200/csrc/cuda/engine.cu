@@ -13,6 +13,7 @@
 // reference's advance_step does (solver.hpp:106-110, 143-147).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -104,6 +105,7 @@ public:
         E_ = d.num_elements;
         policy_ = d.inversion_policy;
         flags_ = d.flags;
+        if (const char* v = std::getenv("DJG_SLAB_KB")) slab_bytes_ = int64_t(std::atoll(v)) << 10;
         nconst_ = const_count(kind_, model_);
         nplanes_ = (nconst_ + T::kPlane - 1) / T::kPlane;
         if (d.nconst != nconst_) throw DescError("nconst does not match djg_const_count(kind, model)");
@@ -187,7 +189,7 @@ public:
             slicebase_.alloc(slice_base.size() * sizeof(int32_t));
             CK(cudaMemcpy(slicebase_.p, slice_base.data(), slicebase_.bytes, cudaMemcpyHostToDevice));
         }
-        fused_ = !(flags_ & DJG_FLAG_TWO_KERNEL) && plan_fused(off, celem, conn);
+        plan_slabs(off, celem);
 
         // Upload connectivity and slots as int4 planes.
         const int nq = npe / 4;
@@ -335,51 +337,36 @@ public:
         drop_graphs();
     }
 
-    // Dependency counts of the fused step (kernels.cuh, k_step_fused): for
-    // every 32-node slice the number of distinct 32-element groups writing to
-    // it, and for every group the slices it writes.
-    bool plan_fused(const int64_t* off, const int64_t* celem, const int32_t* conn) {
-        constexpr int C = 32;
-        const int npe = npe_;
-        const int64_t nG = (E_ + C - 1) / C, nS = (N_ + C - 1) / C;
-        std::vector<int> deps(static_cast<size_t>(nS), 0);
-#pragma omp parallel for schedule(dynamic, 256)
-        for (int64_t j = 0; j < nS; ++j) {
-            std::vector<int64_t> v;
-            for (int64_t n = j * C; n < std::min<int64_t>(N_, (j + 1) * C); ++n)
-                for (int64_t p = off[n]; p < off[n + 1]; ++p) v.push_back(celem[p] / C);
-            std::sort(v.begin(), v.end());
-            deps[size_t(j)] = int(std::unique(v.begin(), v.end()) - v.begin());
+    // Slab schedule (kernels.cuh, k_node_slices): elements are cut into slabs
+    // whose force rows fit in L2; every 32-node slice is gathered right after
+    // the slab holding its last (highest-id) element.
+    void plan_slabs(const int64_t* off, const int64_t* celem) {
+        int64_t se = E_;
+        if (!(flags_ & DJG_FLAG_TWO_KERNEL)) {
+            const int64_t bytes = slab_bytes_ > 0 ? slab_bytes_ : kSlabBytes;
+            se = std::max<int64_t>(4096, bytes / (int64_t(npe_) * int64_t(sizeof(Node))));
+            se = (se + 127) / 128 * 128;
         }
-        std::vector<std::vector<int>> tgt(static_cast<size_t>(nG));
-#pragma omp parallel for schedule(dynamic, 256)
-        for (int64_t g = 0; g < nG; ++g) {
-            auto& v = tgt[size_t(g)];
-            for (int64_t e = g * C; e < std::min<int64_t>(E_, (g + 1) * C); ++e)
-                for (int a = 0; a < npe; ++a) v.push_back(int(conn[e * npe + a] / C));
-            std::sort(v.begin(), v.end());
-            v.erase(std::unique(v.begin(), v.end()), v.end());
-        }
-        std::vector<int> t_off(static_cast<size_t>(nG) + 1, 0), t_flat, orphans;
-        for (int64_t g = 0; g < nG; ++g) t_off[size_t(g + 1)] = t_off[size_t(g)] + int(tgt[size_t(g)].size());
-        t_flat.resize(size_t(t_off.back()));
+        const int64_t S = std::max<int64_t>(1, (E_ + se - 1) / se);
+        const int64_t nS = (N_ + 31) / 32;
+        std::vector<int> slab_of(static_cast<size_t>(nS), 0);
 #pragma omp parallel for schedule(static)
-        for (int64_t g = 0; g < nG; ++g)
-            std::copy(tgt[size_t(g)].begin(), tgt[size_t(g)].end(), t_flat.begin() + t_off[size_t(g)]);
-        for (int64_t j = 0; j < nS; ++j)
-            if (deps[size_t(j)] == 0) orphans.push_back(int(j));
-        auto up = [&](DevBuf& b, const std::vector<int>& v) {
-            b.alloc(std::max<size_t>(v.size(), 1) * sizeof(int));
-            if (!v.empty()) CK(cudaMemcpy(b.p, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
-        };
-        up(deps_, deps);
-        up(pending_, deps);
-        up(tgtOff_, t_off);
-        up(tgt_, t_flat);
-        up(orphans_, orphans);
-        n_orphans_ = int(orphans.size());
-        n_chunks_ = int(nS);
-        return true;
+        for (int64_t j = 0; j < nS; ++j) {
+            int64_t last = -1;
+            for (int64_t n = j * 32; n < std::min<int64_t>(N_, (j + 1) * 32); ++n)
+                if (off[n + 1] > off[n]) last = std::max<int64_t>(last, celem[off[n + 1] - 1]);
+            slab_of[size_t(j)] = last < 0 ? 0 : int(last / se);
+        }
+        std::vector<int> cnt(static_cast<size_t>(S) + 1, 0), list(static_cast<size_t>(nS));
+        for (int64_t j = 0; j < nS; ++j) cnt[size_t(slab_of[size_t(j)]) + 1]++;
+        for (int64_t q = 0; q < S; ++q) cnt[size_t(q + 1)] += cnt[size_t(q)];
+        slab_off_ = cnt;
+        std::vector<int> cur(cnt.begin(), cnt.end() - 1);
+        for (int64_t j = 0; j < nS; ++j) list[size_t(cur[size_t(slab_of[size_t(j)])]++)] = int(j);
+        slabSlices_.alloc(list.size() * sizeof(int));
+        CK(cudaMemcpy(slabSlices_.p, list.data(), slabSlices_.bytes, cudaMemcpyHostToDevice));
+        slab_elems_ = se;
+        n_slabs_ = int(S);
     }
 
     ~Engine() override {
@@ -463,11 +450,11 @@ public:
         if (step) *step = hctrl_->step;
     }
 
-    void launch_element(cudaStream_t s, const Node* u_override = nullptr) {
+    void launch_element(cudaStream_t s, int64_t e0, int64_t e1, const Node* u_override = nullptr) {
         ElemArgs<Real> a = ea_;
         a.u_override = u_override;
-        const unsigned grid = unsigned((E_ + 127) / 128);
-#define DJG_K1(K, M) k_element<Real, K, M><<<grid, 128, 0, s>>>(a)
+        const unsigned grid = unsigned((e1 - e0 + 127) / 128);
+#define DJG_K1(K, M) k_element<Real, K, M><<<grid, 128, 0, s>>>(a, e0, e1)
         if (kind_ == DJG_T4) {
             switch (model_) {
                 case DJG_NH: DJG_K1(0, 0); break;
@@ -487,51 +474,27 @@ public:
         CK(cudaGetLastError());
     }
 
-    template <int K, int M>
-    void launch_fused_km(cudaStream_t s, bool assemble_mode, const Node* u_override) {
-        ElemArgs<Real> a = ea_;
-        a.u_override = u_override;
-        FusedSched S{pending_.as<int>(), deps_.as<int>(), tgtOff_.as<int>(), tgt_.as<int>(), orphans_.as<int>(),
-                     n_orphans_, n_chunks_, rowlen_.as<int>(), slicebase_.as<int>(),
-                     (flags_ & DJG_FLAG_NO_DISCARD) ? 0 : 1};
-        const unsigned grid = unsigned((E_ + 255) / 256);
-        if (assemble_mode) k_step_fused<Real, K, M, true><<<grid, 256, 0, s>>>(a, na_, S);
-        else k_step_fused<Real, K, M, false><<<grid, 256, 0, s>>>(a, na_, S);
-        CK(cudaGetLastError());
-    }
-
-    void launch_fused(cudaStream_t s, bool assemble_mode = false, const Node* u_override = nullptr) {
-        if (kind_ == DJG_T4) {
-            switch (model_) {
-                case DJG_NH: launch_fused_km<0, 0>(s, assemble_mode, u_override); break;
-                case DJG_TI: launch_fused_km<0, 1>(s, assemble_mode, u_override); break;
-                case DJG_OT: launch_fused_km<0, 2>(s, assemble_mode, u_override); break;
-                default: launch_fused_km<0, 3>(s, assemble_mode, u_override); break;
-            }
-        } else {
-            switch (model_) {
-                case DJG_NH: launch_fused_km<1, 0>(s, assemble_mode, u_override); break;
-                case DJG_TI: launch_fused_km<1, 1>(s, assemble_mode, u_override); break;
-                case DJG_OT: launch_fused_km<1, 2>(s, assemble_mode, u_override); break;
-                default: launch_fused_km<1, 3>(s, assemble_mode, u_override); break;
-            }
+    // One advance_step (or one assemble) on the stream: S slab pairs.
+    void launch_step(cudaStream_t s, bool assemble_mode = false, const Node* u_override = nullptr,
+                     std::vector<cudaEvent_t>* marks = nullptr) {
+        for (int q = 0; q < n_slabs_; ++q) {
+            const int64_t e0 = int64_t(q) * slab_elems_, e1 = std::min<int64_t>(E_, e0 + slab_elems_);
+            launch_element(s, e0, e1, u_override);
+            if (marks) CK(cudaEventRecord((*marks)[size_t(2 * q)], s));
+            launch_node(s, q, assemble_mode);
+            if (marks) CK(cudaEventRecord((*marks)[size_t(2 * q + 1)], s));
         }
     }
 
-    // One advance_step on the stream.
-    void launch_step(cudaStream_t s) {
-        if (fused_) {
-            launch_fused(s);
-        } else {
-            launch_element(s);
-            launch_node(s);
-        }
-    }
-
-    void launch_node(cudaStream_t s, bool assemble_mode = false) {
-        const unsigned grid = unsigned((N_ + 255) / 256);
-        if (assemble_mode) k_node<Real, true><<<grid, 256, 0, s>>>(na_);
-        else k_node<Real, false><<<grid, 256, 0, s>>>(na_);
+    void launch_node(cudaStream_t s, int slab, bool assemble_mode) {
+        const int n = slab_off_[size_t(slab + 1)] - slab_off_[size_t(slab)];
+        const int close = slab == n_slabs_ - 1;
+        if (n == 0 && !close) return;
+        const int* list = slabSlices_.as<int>() + slab_off_[size_t(slab)];
+        const unsigned grid = unsigned(std::max(1, (n * 32 + 255) / 256));
+        const int discard = (flags_ & DJG_FLAG_NO_DISCARD) || n_slabs_ == 1 ? 0 : 1;
+        if (assemble_mode) k_node_slices<Real, true><<<grid, 256, 0, s>>>(na_, list, n, discard, close);
+        else k_node_slices<Real, false><<<grid, 256, 0, s>>>(na_, list, n, discard, close);
         CK(cudaGetLastError());
     }
 
@@ -610,12 +573,7 @@ public:
             hctrl_->halted = 0;
             CK(cudaMemcpyAsync(ctrl_.p, hctrl_, sizeof(Ctrl), cudaMemcpyHostToDevice, stream_));
         }
-        if (fused_) {
-            launch_fused(stream_, true, uo);
-        } else {
-            launch_element(stream_, uo);
-            launch_node(stream_, true);
-        }
+        launch_step(stream_, true, uo);
         read_ctrl();
         if (halted) {
             hctrl_->halted = halted;
@@ -634,32 +592,32 @@ public:
     int profile(int64_t n, float* ms_e, float* ms_n, float* ms_t) override {
         if (!configured_) throw DescError("step data not configured (djg_configure_step)");
         CK(cudaMemcpyAsync(hstart_, ctrl_.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream_));
-        std::vector<cudaEvent_t> ev(size_t(3 * n + 1));
-        for (auto& e : ev) CK(cudaEventCreate(&e));
-        CK(cudaEventRecord(ev[0], stream_));
-        for (int64_t i = 0; i < n; ++i) {
-            if (fused_) {
-                launch_fused(stream_);
-                CK(cudaEventRecord(ev[size_t(3 * i + 1)], stream_));
-            } else {
-                launch_element(stream_);
-                CK(cudaEventRecord(ev[size_t(3 * i + 1)], stream_));
-                launch_node(stream_);
-            }
-            CK(cudaEventRecord(ev[size_t(3 * i + 2)], stream_));
-            CK(cudaEventRecord(ev[size_t(3 * i + 3)], stream_));
-        }
-        CK(cudaStreamSynchronize(stream_));
+        std::vector<cudaEvent_t> marks(size_t(2 * n_slabs_));
+        for (auto& e : marks) CK(cudaEventCreate(&e));
+        cudaEvent_t t0, t1;
+        CK(cudaEventCreate(&t0));
+        CK(cudaEventCreate(&t1));
         float te = 0, tn = 0, tt = 0;
         for (int64_t i = 0; i < n; ++i) {
-            float a = 0, b = 0;
-            CK(cudaEventElapsedTime(&a, ev[size_t(3 * i)], ev[size_t(3 * i + 1)]));
-            CK(cudaEventElapsedTime(&b, ev[size_t(3 * i + 1)], ev[size_t(3 * i + 2)]));
-            te += a;
-            tn += b;
+            CK(cudaEventRecord(t0, stream_));
+            launch_step(stream_, false, nullptr, &marks);
+            CK(cudaEventRecord(t1, stream_));
+            CK(cudaEventSynchronize(t1));
+            float a = 0, b = 0, c = 0;
+            cudaEvent_t prev = t0;
+            for (int q = 0; q < n_slabs_; ++q) {
+                CK(cudaEventElapsedTime(&a, prev, marks[size_t(2 * q)]));
+                CK(cudaEventElapsedTime(&b, marks[size_t(2 * q)], marks[size_t(2 * q + 1)]));
+                te += a;
+                tn += b;
+                prev = marks[size_t(2 * q + 1)];
+            }
+            CK(cudaEventElapsedTime(&c, t0, t1));
+            tt += c;
         }
-        CK(cudaEventElapsedTime(&tt, ev[0], ev[size_t(3 * n)]));
-        for (auto& e : ev) cudaEventDestroy(e);
+        for (auto& e : marks) cudaEventDestroy(e);
+        cudaEventDestroy(t0);
+        cudaEventDestroy(t1);
         if (ms_e) *ms_e = te;
         if (ms_n) *ms_n = tn;
         if (ms_t) *ms_t = tt;
@@ -675,14 +633,14 @@ public:
         o->device_bytes = int64_t(conn_.bytes + slot_.bytes + consts_.bytes + 3 * u_[0].bytes + uscratch_.bytes +
                                   flat_.bytes + ef_.bytes + rowlen_.bytes + slicebase_.bytes + c1_.bytes +
                                   code_.bytes + target_.bytes + tTotal_.bytes + rext_.bytes + ctrl_.bytes +
-                                  deps_.bytes + pending_.bytes + tgtOff_.bytes + tgt_.bytes + orphans_.bytes);
+                                  slabSlices_.bytes);
         o->npe = npe_;
         o->nconst = nconst_;
         o->const_planes = nplanes_;
         o->precision = int32_t(sizeof(Real));
-        o->kernels_per_step = fused_ ? 1 : 2;
-        o->ring_regions = 0;
-        o->fused = fused_ ? 1 : 0;
+        o->kernels_per_step = 2 * n_slabs_;
+        o->slabs = n_slabs_;
+        o->slab_elements = slab_elems_;
         o->sm_count = sms_;
     }
 
@@ -710,10 +668,12 @@ private:
     Ctrl* hstart_ = nullptr;  // pinned snapshot taken at the start of a step call
     bool configured_ = false;
     bool ctrl_initialized_ = false;
-    // fused step
-    bool fused_ = false;
-    int wmax_ = 1, n_orphans_ = 0, n_chunks_ = 0;
-    DevBuf deps_, pending_, tgtOff_, tgt_, orphans_;
+    // slab schedule
+    static constexpr int64_t kSlabBytes = int64_t(32) << 20;  // force rows per slab kept in L2
+    int64_t slab_bytes_ = 0, slab_elems_ = 0;
+    int wmax_ = 1, n_slabs_ = 1;
+    std::vector<int> slab_off_;
+    DevBuf slabSlices_;
 };
 
 int debug_cbrt(int32_t precision, const void* in, void* out, int64_t n, int32_t device) {

@@ -443,10 +443,11 @@ __device__ __forceinline__ P pick3(int i, P a, P b, P c) {
     return i == 0 ? a : (i == 1 ? b : c);
 }
 
+// Elements [e0, e1) of the step (one slab).
 template <class Real, int KIND, int MODEL>
-__global__ void __launch_bounds__(128) k_element(const ElemArgs<Real> A) {
-    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= A.E) return;
+__global__ void __launch_bounds__(128) k_element(const ElemArgs<Real> A, long long e0, long long e1) {
+    const long long e = e0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= e1) return;
     if (__ldcg(&A.ctrl->halted)) return;
     const int phase = int(__ldcg(&A.ctrl->step) % 3);
     const typename RT<Real>::Node* u = A.u_override ? A.u_override : pick3(phase, A.u[0], A.u[1], A.u[2]);
@@ -564,124 +565,53 @@ __device__ __forceinline__ void close_step(Ctrl* ctrl, long long step, int polic
     ctrl->diverged = 0;
 }
 
+// ------------------------------------------------------------------ slab step
+
+// A step runs as S slabs: k_element over elements [e0, e1), then k_node_slices
+// over the 32-node slices whose last element lies in that slab. The slab's
+// force rows (~32 MB) are read back while still in L2 and their lines are
+// then discarded (discard.global.L2), so the element->node exchange mostly
+// never reaches HBM. Kernel boundaries order the two phases; no device-side
+// waiting. Each node sums its slots in ascending element order, so the
+// result is independent of S (bit-identical to S = 1, the plain two-kernel
+// step).
+__device__ __forceinline__ void l2_discard(const void* p) {
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
 template <class Real, bool kAssemble>
-__global__ void __launch_bounds__(256) k_node(const NodeArgs<Real> A) {
+__global__ void __launch_bounds__(256) k_node_slices(const NodeArgs<Real> A, const int* __restrict__ slices,
+                                                      int nslices, int discard, int close) {
     Ctrl* ctrl = A.ctrl;
     if (__ldcg(&ctrl->halted) && !kAssemble) return;
     __shared__ int s_nonfinite;
     if (threadIdx.x == 0) s_nonfinite = 0;
     __syncthreads();
-    const long long step = ctrl->step;
-    const bool skip = ctrl->first_inv != kNone && A.policy == 0;  // Abort: no gather (djtled_force.hpp:202-208)
-    const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (n < A.N && !skip) {
-        const typename RT<Real>::Node* p = A.ef + (long long)A.slice_base[n >> 5] + (n & 31);
-        if (node_body<Real, kAssemble, false>(A, n, p, A.row_len[n], step)) s_nonfinite = 1;
+    const long long step = __ldcg(&ctrl->step);
+    const long long w = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w < nslices) {
+        const int sl = slices[w];
+        const long long n = 32ll * sl + lane;
+        const typename RT<Real>::Node* base = A.ef + (long long)A.slice_base[sl];
+        if (n < A.N && node_body<Real, kAssemble, false>(A, n, base + lane, A.row_len[n], step)) s_nonfinite = 1;
+        __syncwarp();
+        if (discard) {
+            const char* lo = reinterpret_cast<const char*>(base);
+            const char* hi = reinterpret_cast<const char*>(A.ef + (long long)A.slice_base[sl + 1]);
+            for (const char* q = lo + 128 * lane; q < hi; q += 128 * 32) l2_discard(q);
+        }
     }
     __syncthreads();
     if (threadIdx.x != 0) return;
     if (s_nonfinite) atomicOr(&ctrl->diverged, 1);
+    if (!close) return;
+    // The last slab's kernel closes the step once all its blocks are done
+    // (every earlier slab kernel finished before it, in stream order).
     __threadfence();
     const unsigned int done = atomicAdd(&ctrl->blocks_done, 1u);
     if (done != gridDim.x - 1) return;
     close_step<kAssemble>(ctrl, step, A.policy);
-    __threadfence();
-    ctrl->blocks_done = 0;
-}
-
-// ------------------------------------------------------------------ fused step
-
-// One kernel per step, no waiting and no block barriers. Each warp computes 32
-// consecutive elements and stores their force rows; it then decrements the
-// pending-count of every 32-node slice it wrote to, and when a count reaches
-// zero the same warp gathers that slice (all its rows are stored and, having
-// just been written, still in L2), updates its 32 nodes and discards the
-// consumed slot lines from L2 (discard.global.L2) so they are never written
-// back to HBM. Each node still sums its slots in ascending element order, so
-// the step is bit-identical to the two-kernel step.
-struct FusedSched {
-    int* pending;          // per slice: warp groups still to store (re-armed after use)
-    const int* deps;       // per slice: number of warp groups writing to it
-    const int* tgt_off;    // warp group (32 elements) -> slices it writes
-    const int* tgt;
-    const int* orphans;    // slices no element touches (handled by warp group 0)
-    int n_orphans;
-    int n_slices;
-    const int* row_len;
-    const int* slice_base; // sliced slot layout (shared with the two-kernel path)
-    int discard;           // 1: discard consumed slot lines from L2
-};
-
-__device__ __forceinline__ void l2_discard(const void* p) {
-    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
-}
-
-// Gather + update of slice s by the calling warp (lane = node within slice).
-template <class Real, bool kAssemble>
-__device__ __forceinline__ bool slice_update(const NodeArgs<Real>& NA, const FusedSched& S,
-                                             const typename RT<Real>::Node* ef, int s, long long step) {
-    const int lane = threadIdx.x & 31;
-    const long long n = 32ll * s + lane;
-    bool nf = false;
-    if (n < NA.N)
-        nf = node_body<Real, kAssemble, true>(NA, n, ef + (long long)S.slice_base[s] + lane, S.row_len[n], step);
-    __syncwarp();
-    if (S.discard) {
-        const char* lo = reinterpret_cast<const char*>(ef + S.slice_base[s]);
-        const char* hi = reinterpret_cast<const char*>(ef + S.slice_base[s + 1]);
-        for (const char* q = lo + 128 * lane; q < hi; q += 128 * 32) l2_discard(q);
-    }
-    if (lane == 0) S.pending[s] = S.deps[s];  // re-arm for the next step
-    return nf;
-}
-
-template <class Real, int KIND, int MODEL, bool kAssemble>
-__global__ void __launch_bounds__(256) k_step_fused(const ElemArgs<Real> EA, const NodeArgs<Real> NA,
-                                                     const FusedSched S) {
-    Ctrl* ctrl = EA.ctrl;
-    if (__ldcg(&ctrl->halted) && !kAssemble) return;
-    __shared__ int s_nf;
-    if (threadIdx.x == 0) s_nf = 0;
-    const long long step = __ldcg(&ctrl->step);
-    const int phase = int(step % 3);
-    const typename RT<Real>::Node* u = EA.u_override ? EA.u_override : pick3(phase, EA.u[0], EA.u[1], EA.u[2]);
-    const int lane = threadIdx.x & 31;
-    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    const long long group = e >> 5;
-    bool nf = false;
-    if (group == 0)
-        for (int q = 0; q < S.n_orphans; ++q) nf |= slice_update<Real, kAssemble>(NA, S, EA.ef, S.orphans[q], step);
-    if (e < EA.E) element_body<Real, KIND, MODEL>(EA, e, u);
-    // Release: every lane fences its own stores before the warp rendezvous,
-    // so any lane's signalling atomic is ordered after all 32 rows.
-    __threadfence();
-    __syncwarp();
-    if (group * 32 < EA.E) {
-        const int t0 = S.tgt_off[group], t1 = S.tgt_off[group + 1];
-        for (int base = t0; base < t1; base += 32) {
-            int sl = -1;
-            bool ready = false;
-            if (base + lane < t1) {
-                sl = S.tgt[base + lane];
-                ready = atomicSub(S.pending + sl, 1) == 1;
-                if (ready) __threadfence();  // acquire the other groups' rows
-            }
-            unsigned mask = __ballot_sync(0xffffffffu, ready);
-            while (mask) {
-                const int src = __ffs(mask) - 1;
-                mask &= mask - 1;
-                nf |= slice_update<Real, kAssemble>(NA, S, EA.ef, __shfl_sync(0xffffffffu, sl, src), step);
-            }
-        }
-    }
-    if (nf) s_nf = 1;
-    __syncthreads();
-    if (threadIdx.x != 0) return;
-    if (s_nf) atomicOr(&ctrl->diverged, 1);
-    __threadfence();
-    const unsigned int done = atomicAdd(&ctrl->blocks_done, 1u);
-    if (done != gridDim.x - 1) return;
-    close_step<kAssemble>(ctrl, step, NA.policy);
     __threadfence();
     ctrl->blocks_done = 0;
 }

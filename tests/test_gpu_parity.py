@@ -72,11 +72,33 @@ def test_two_kernel_path_cfg(cfg):
     check_run(config_spec(cfg, precision=4), 500, flags=A.DJG_FLAG_TWO_KERNEL)
 
 
-def test_fused_engine_is_selected():
+def test_slab_schedule_on_large_mesh():
     sc = Scenario(config_spec("cfg3", precision=4))
     with GpuDjEngine(sc) as eng:
         info = eng.info()
-    assert info["fused"] == 1 and info["kernels_per_step"] == 1
+    assert info["slabs"] > 1 and info["kernels_per_step"] == 2 * info["slabs"]
+    assert info["slab_elements"] * info["npe"] * 16 <= 40 << 20
+
+
+@pytest.mark.parametrize("kind,model", [("T4", "NH"), ("H8", "TI"), ("T4", "MR")])
+def test_many_slabs_bitwise(kind, model, monkeypatch):
+    """Small slabs (64 KB of rows: several slabs even on small meshes)."""
+    monkeypatch.setenv("DJG_SLAB_KB", "64")
+    spec = box_spec(kind=kind, model=model, divisions=14, precision=4, ramp_steps=300)
+    sc = Scenario(spec)
+    with GpuDjEngine(sc) as eng:
+        assert eng.info()["slabs"] >= 3
+    check_run(spec, 300)
+    check_run(spec, 300, flags=A.DJG_FLAG_NO_DISCARD)
+
+
+@pytest.mark.slow
+def test_cfg3_slab_vs_two_kernel_bitwise():
+    spec = config_spec("cfg3", precision=4, target=0.01, ramp_steps=1000)
+    a = run_gpu(spec, 50)[0]
+    b = run_gpu(spec, 50, flags=A.DJG_FLAG_TWO_KERNEL)[0]
+    c = run_gpu(spec, 50, flags=A.DJG_FLAG_NO_DISCARD)[0]
+    assert np.array_equal(a, b) and np.array_equal(a, c)
 
 
 @pytest.mark.parametrize("flags", [A.DJG_FLAG_NO_DISCARD, A.DJG_FLAG_NO_GRAPH | A.DJG_FLAG_TWO_KERNEL])

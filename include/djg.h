@@ -82,7 +82,7 @@ typedef struct djg_desc {
 
 /* Flags */
 #define DJG_FLAG_NO_GRAPH 1u    /* launch kernels one by one instead of CUDA graphs */
-#define DJG_FLAG_TWO_KERNEL 2u  /* one slab: whole-mesh element kernel, then whole-mesh node kernel */
+#define DJG_FLAG_SLABS 2u       /* pipeline each step as L2-sized element slabs (bit-identical) */
 #define DJG_FLAG_NO_DISCARD 4u  /* slab step: keep consumed force rows in L2 (no discard) */
 
 /* DjEngine(mesh, material, c_hg) (solver.hpp:264-267) at the mesh level:

@@ -21,7 +21,7 @@ DJG_ABORT, DJG_SKIP_AND_REPORT = 0, 1
 DJG_FREE, DJG_FIXED, DJG_PRESCRIBED = 0, 1, 2
 DJG_OK, DJG_E_INTERNAL, DJG_E_CONFIG, DJG_E_CUDA, DJG_E_INVERSION, DJG_E_DIVERGENCE = 0, 1, 2, 3, 4, 5
 DJG_FLAG_NO_GRAPH = 1
-DJG_FLAG_TWO_KERNEL = 2
+DJG_FLAG_SLABS = 2
 DJG_FLAG_NO_DISCARD = 4
 
 KIND_NAMES = {"T4": DJG_T4, "H8": DJG_H8}

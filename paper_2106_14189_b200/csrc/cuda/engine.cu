@@ -1,10 +1,11 @@
 // libdjg: the B200 DJ-TLED engine behind the C-ABI of include/djg.h.
 //
 // One engine = one problem resident in HBM:
-//   conn/slot   int4 planes [npe/4][E]     connectivity and force-slot positions
+//   conn        int4 planes [npe/4][E]     connectivity
+//   rank        npe x 1|2 bytes per element: rank of the element in each node's CSR row
 //   consts      Plane planes [nplanes][E]  hot constants (float4 / double2)
 //   u[3]        Node[N]                    triple-buffered displacement (xyz+pad)
-//   ef          Node[capacity]             element-node forces in sliced CSR order
+//   ef          Real[3][capacity]          element-node forces (x, y, z planes) in sliced CSR order
 //   row_len, slice_base, c1, code, target, t_total, r_ext   node data
 //   ctrl        Ctrl                       step counter + failure flags
 // A step is k_element then k_node on one stream; multi-step calls replay a
@@ -166,46 +167,50 @@ public:
         if (bad) throw DescError("CSR pairs do not match connectivity");
         wmax_ = std::max(wmax, 1);
         // Sliced slot layout: node n's k-th slot at slice_base[n/32] + 32k + n%32.
-        std::vector<int32_t> slot(size_t(E_ * npe));
+        // The element kernel finds it from the element's rank k in each of its
+        // nodes' CSR rows (1 or 2 bytes per element-node).
+        if (wmax_ > 65535) throw DescError("a node has more than 65535 incident elements");
+        rank_bytes_ = wmax_ <= 256 ? 1 : 2;
+        std::vector<uint8_t> ranks(size_t(E_ * npe) * size_t(rank_bytes_));
         {
             const int64_t S = (N_ + 31) / 32;
-            std::vector<int32_t> slice_base(static_cast<size_t>(S) + 1);
+            slice_base_.assign(static_cast<size_t>(S) + 1, 0);
             int64_t cap = 0;
             for (int64_t sl = 0; sl < S; ++sl) {
-                slice_base[size_t(sl)] = int32_t(cap);
+                slice_base_[size_t(sl)] = int32_t(cap);
                 int w = 0;
                 for (int64_t n = sl * 32; n < std::min<int64_t>(N_, sl * 32 + 32); ++n) w = std::max(w, row_len[size_t(n)]);
                 cap += int64_t(32) * w;
                 if (cap > INT32_MAX) throw DescError("slot buffer exceeds 32-bit indexing");
             }
-            slice_base[size_t(S)] = int32_t(cap);
-            capacity_ = std::max<int64_t>(cap, 1);
+            slice_base_[size_t(S)] = int32_t(cap);
+            capacity_ = std::max<int64_t>(cap, 32);
+            const int rb = rank_bytes_;
 #pragma omp parallel for schedule(static)
-            for (int64_t n = 0; n < N_; ++n) {
-                const int64_t base = int64_t(slice_base[size_t(n >> 5)]) + (n & 31);
-                for (int64_t p = off[n]; p < off[n + 1]; ++p)
-                    slot[size_t(celem[p] * npe + cloc[p])] = int32_t(base + 32 * (p - off[n]));
-            }
-            slicebase_.alloc(slice_base.size() * sizeof(int32_t));
-            CK(cudaMemcpy(slicebase_.p, slice_base.data(), slicebase_.bytes, cudaMemcpyHostToDevice));
+            for (int64_t n = 0; n < N_; ++n)
+                for (int64_t p = off[n]; p < off[n + 1]; ++p) {
+                    const int64_t k = p - off[n];
+                    uint8_t* r = ranks.data() + size_t((celem[p] * npe + cloc[p]) * rb);
+                    r[0] = uint8_t(k & 0xff);
+                    if (rb == 2) r[1] = uint8_t(k >> 8);
+                }
+            slicebase_.alloc(slice_base_.size() * sizeof(int32_t));
+            CK(cudaMemcpy(slicebase_.p, slice_base_.data(), slicebase_.bytes, cudaMemcpyHostToDevice));
+            rank_.alloc(ranks.size());
+            CK(cudaMemcpy(rank_.p, ranks.data(), rank_.bytes, cudaMemcpyHostToDevice));
         }
         plan_slabs(off, celem);
 
-        // Upload connectivity and slots as int4 planes.
+        // Upload connectivity as int4 planes.
         const int nq = npe / 4;
         {
             std::vector<int32_t> planes(size_t(E_ * npe));
-            for (int which = 0; which < 2; ++which) {
-                const int32_t* src = which == 0 ? conn : slot.data();
 #pragma omp parallel for schedule(static)
-                for (int64_t e = 0; e < E_; ++e)
-                    for (int q = 0; q < nq; ++q)
-                        for (int k = 0; k < 4; ++k)
-                            planes[size_t((int64_t(q) * E_ + e) * 4 + k)] = src[e * npe + 4 * q + k];
-                DevBuf& dst = which == 0 ? conn_ : slot_;
-                dst.alloc(planes.size() * sizeof(int32_t));
-                CK(cudaMemcpy(dst.p, planes.data(), dst.bytes, cudaMemcpyHostToDevice));
-            }
+            for (int64_t e = 0; e < E_; ++e)
+                for (int q = 0; q < nq; ++q)
+                    for (int k = 0; k < 4; ++k) planes[size_t((int64_t(q) * E_ + e) * 4 + k)] = conn[e * npe + 4 * q + k];
+            conn_.alloc(planes.size() * sizeof(int32_t));
+            CK(cudaMemcpy(conn_.p, planes.data(), conn_.bytes, cudaMemcpyHostToDevice));
         }
         // Constants: AoS chunks -> device planes.
         consts_.alloc(size_t(nplanes_) * size_t(E_) * sizeof(Plane));
@@ -229,7 +234,7 @@ public:
         for (auto& b : u_) b.alloc(size_t(N_) * sizeof(Node));
         uscratch_.alloc(size_t(N_) * sizeof(Node));
         flat_.alloc(size_t(3 * N_) * sizeof(Real));
-        ef_.alloc(size_t(capacity_) * sizeof(Node));
+        ef_.alloc(size_t(3 * capacity_) * sizeof(Real));
         CK(cudaMemset(ef_.p, 0, ef_.bytes));
         rowlen_.alloc(row_len.size() * sizeof(int32_t));
         CK(cudaMemcpy(rowlen_.p, row_len.data(), rowlen_.bytes, cudaMemcpyHostToDevice));
@@ -244,11 +249,13 @@ public:
         // Kernel arguments.
         ea_.E = E_;
         ea_.conn = conn_.as<int4>();
-        ea_.slot = slot_.as<int4>();
+        ea_.rank = rank_.p;
+        ea_.slice_base = slicebase_.as<int>();
         ea_.c = consts_.as<Plane>();
         for (int i = 0; i < 3; ++i) ea_.u[i] = u_[i].as<Node>();
         ea_.u_override = nullptr;
-        ea_.ef = ef_.as<Node>();
+        ea_.ef = ef_.as<Real>();
+        ea_.cap = capacity_;
         ea_.ctrl = ctrl_.as<Ctrl>();
         const Real mu = Real(d.material.mu), c10 = Real(d.material.c10);
         ea_.mat.dI1 = model_ == DJG_MR ? c10 : mu / 2;
@@ -259,7 +266,8 @@ public:
         na_.N = N_;
         na_.row_len = rowlen_.as<int>();
         na_.slice_base = slicebase_.as<int>();
-        na_.ef = ef_.as<Node>();
+        na_.ef = ef_.as<Real>();
+        na_.cap = capacity_;
         for (int i = 0; i < 3; ++i) na_.u[i] = u_[i].as<Node>();
         na_.r_ext = nullptr;
         na_.c1 = c1_.as<Real>();
@@ -342,7 +350,7 @@ public:
     // the slab holding its last (highest-id) element.
     void plan_slabs(const int64_t* off, const int64_t* celem) {
         int64_t se = E_;
-        if (!(flags_ & DJG_FLAG_TWO_KERNEL)) {
+        if ((flags_ & DJG_FLAG_SLABS) || slab_bytes_ > 0) {
             const int64_t bytes = slab_bytes_ > 0 ? slab_bytes_ : kSlabBytes;
             se = std::max<int64_t>(4096, bytes / (int64_t(npe_) * int64_t(sizeof(Node))));
             se = (se + 127) / 128 * 128;
@@ -454,7 +462,11 @@ public:
         ElemArgs<Real> a = ea_;
         a.u_override = u_override;
         const unsigned grid = unsigned((e1 - e0 + 127) / 128);
-#define DJG_K1(K, M) k_element<Real, K, M><<<grid, 128, 0, s>>>(a, e0, e1)
+#define DJG_K1(K, M)                                                           \
+    do {                                                                       \
+        if (rank_bytes_ == 1) k_element<Real, K, M, 1><<<grid, 128, 0, s>>>(a, e0, e1); \
+        else k_element<Real, K, M, 2><<<grid, 128, 0, s>>>(a, e0, e1);                 \
+    } while (0)
         if (kind_ == DJG_T4) {
             switch (model_) {
                 case DJG_NH: DJG_K1(0, 0); break;
@@ -492,7 +504,7 @@ public:
         if (n == 0 && !close) return;
         const int* list = slabSlices_.as<int>() + slab_off_[size_t(slab)];
         const unsigned grid = unsigned(std::max(1, (n * 32 + 255) / 256));
-        const int discard = (flags_ & DJG_FLAG_NO_DISCARD) || n_slabs_ == 1 ? 0 : 1;
+        const int discard = (flags_ & DJG_FLAG_NO_DISCARD) || n_slabs_ == 1 ? 0 : 1;  // slab mode only
         if (assemble_mode) k_node_slices<Real, true><<<grid, 256, 0, s>>>(na_, list, n, discard, close);
         else k_node_slices<Real, false><<<grid, 256, 0, s>>>(na_, list, n, discard, close);
         CK(cudaGetLastError());
@@ -630,7 +642,7 @@ public:
         o->num_elements = E_;
         o->num_slots = E_ * npe_;
         o->slot_capacity = capacity_;
-        o->device_bytes = int64_t(conn_.bytes + slot_.bytes + consts_.bytes + 3 * u_[0].bytes + uscratch_.bytes +
+        o->device_bytes = int64_t(conn_.bytes + rank_.bytes + consts_.bytes + 3 * u_[0].bytes + uscratch_.bytes +
                                   flat_.bytes + ef_.bytes + rowlen_.bytes + slicebase_.bytes + c1_.bytes +
                                   code_.bytes + target_.bytes + tTotal_.bytes + rext_.bytes + ctrl_.bytes +
                                   slabSlices_.bytes);
@@ -645,12 +657,20 @@ public:
     }
 
     void slot_map(int32_t* out) override {
+        std::vector<uint8_t> ranks(rank_.bytes);
         std::vector<int32_t> planes(size_t(E_ * npe_));
-        CK(cudaMemcpy(planes.data(), slot_.p, slot_.bytes, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(ranks.data(), rank_.p, rank_.bytes, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(planes.data(), conn_.p, conn_.bytes, cudaMemcpyDeviceToHost));
         const int nq = npe_ / 4;
         for (int64_t e = 0; e < E_; ++e)
             for (int q = 0; q < nq; ++q)
-                for (int k = 0; k < 4; ++k) out[e * npe_ + 4 * q + k] = planes[size_t((int64_t(q) * E_ + e) * 4 + k)];
+                for (int k = 0; k < 4; ++k) {
+                    const int a = 4 * q + k;
+                    const int64_t n = planes[size_t((int64_t(q) * E_ + e) * 4 + k)];
+                    const uint8_t* r = ranks.data() + size_t((e * npe_ + a) * rank_bytes_);
+                    const int64_t rank = rank_bytes_ == 1 ? r[0] : (r[0] | (int64_t(r[1]) << 8));
+                    out[e * npe_ + a] = int32_t(slice_base_[size_t(n >> 5)] + 32 * rank + (n & 31));
+                }
     }
 
 private:
@@ -659,7 +679,9 @@ private:
     uint32_t flags_ = 0;
     int64_t N_ = 0, E_ = 0, capacity_ = 0;
     cudaStream_t stream_ = nullptr;
-    DevBuf conn_, slot_, consts_, u_[3], uscratch_, flat_, ef_, rowlen_, slicebase_, c1_, code_, target_, tTotal_,
+    std::vector<int32_t> slice_base_;
+    int rank_bytes_ = 1;
+    DevBuf conn_, rank_, consts_, u_[3], uscratch_, flat_, ef_, rowlen_, slicebase_, c1_, code_, target_, tTotal_,
         rext_, ctrl_;
     Ctrl* hctrl_ = nullptr;
     ElemArgs<Real> ea_{};

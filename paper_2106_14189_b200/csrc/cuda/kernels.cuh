@@ -124,11 +124,14 @@ template <class Real>
 struct ElemArgs {
     long long E;
     const int4* conn;                    // NPE/4 planes of int4[E]
-    const int4* slot;                    // NPE/4 planes of int4[E]: slot positions
+    const void* rank;                    // per element: npe ranks (uint8 or uint16) of the element
+                                         // in its nodes' CSR rows, packed in one 4/8/16-byte word
+    const int* slice_base;               // first slot of each 32-node slice
     const typename RT<Real>::Plane* c;   // nplanes planes of Plane[E]
     const typename RT<Real>::Node* u[3]; // triple-buffered displacement
     const typename RT<Real>::Node* u_override;
-    typename RT<Real>::Node* ef;         // sliced force-slot buffer
+    Real* ef;                            // force slots: x plane, y plane (+cap), z plane (+2 cap)
+    long long cap;                       // slots per plane
     Ctrl* ctrl;
     MatParams<Real> mat;
 };
@@ -138,7 +141,8 @@ struct NodeArgs {
     long long N;
     const int* row_len;                  // CSR row length per node
     const int* slice_base;               // first slot position of each 32-node slice
-    const typename RT<Real>::Node* ef;
+    const Real* ef;                      // force slots (x, y, z planes, stride cap)
+    long long cap;
     typename RT<Real>::Node* u[3];
     const typename RT<Real>::Node* r_ext;  // NULL: identically zero
     const Real* c1;
@@ -210,8 +214,45 @@ __global__ void k_cbrt(const Real* __restrict__ in, Real* __restrict__ out, long
 
 // ------------------------------------------------------------------ K1
 
+// Force row of element-node a into slot (slice_base[n/32] + 32 rank + n%32)
+// of the three slot planes.
+template <class Real>
+__device__ __forceinline__ void store_row(const ElemArgs<Real>& A, long long pos, Real x, Real y, Real z) {
+    A.ef[pos] = x;
+    A.ef[A.cap + pos] = y;
+    A.ef[2 * A.cap + pos] = z;
+}
+
+// Ranks of element e in its nodes' CSR rows (RB bytes each).
+template <int NPE, int RB>
+__device__ __forceinline__ void load_ranks(const void* base, long long e, int (&rk)[NPE]) {
+    if constexpr (NPE == 4 && RB == 1) {
+        const unsigned w = __ldcs(static_cast<const unsigned*>(base) + e);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) rk[a] = (w >> (8 * a)) & 0xff;
+    } else if constexpr (NPE == 8 && RB == 1) {
+        const uint2 w = __ldcs(static_cast<const uint2*>(base) + e);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+            rk[a] = (w.x >> (8 * a)) & 0xff;
+            rk[4 + a] = (w.y >> (8 * a)) & 0xff;
+        }
+    } else if constexpr (NPE == 4) {
+        const uint2 w = __ldcs(static_cast<const uint2*>(base) + e);
+        rk[0] = w.x & 0xffff; rk[1] = w.x >> 16; rk[2] = w.y & 0xffff; rk[3] = w.y >> 16;
+    } else {
+        const uint4 w = __ldcs(static_cast<const uint4*>(base) + e);
+        const unsigned v[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            rk[2 * q] = v[q] & 0xffff;
+            rk[2 * q + 1] = v[q] >> 16;
+        }
+    }
+}
+
 // One element: loads, DJ-TLED force, stores of its npe rows into their slots.
-template <class Real, int KIND, int MODEL>
+template <class Real, int KIND, int MODEL, int RB>
 __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long long e,
                                              const typename RT<Real>::Node* __restrict__ u) {
     using L = Layout<KIND, MODEL>;
@@ -282,12 +323,12 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
                      Jt[0][1] * (Jt[1][0] * Jt[2][2] - Jt[1][2] * Jt[2][0]) +
                      Jt[0][2] * (Jt[1][0] * Jt[2][1] - Jt[1][1] * Jt[2][0]);
 
-    typename T::Node* __restrict__ ef = A.ef;
-    int sl[NPE];
+    long long sl[NPE];
+    {
+        int rk[NPE];
+        load_ranks<NPE, RB>(A.rank, e, rk);
 #pragma unroll
-    for (int p = 0; p < NPE / 4; ++p) {
-        const int4 q = __ldcs(A.slot + (long long)p * A.E + e);
-        sl[4 * p + 0] = q.x; sl[4 * p + 1] = q.y; sl[4 * p + 2] = q.z; sl[4 * p + 3] = q.w;
+        for (int a = 0; a < NPE; ++a) sl[a] = (long long)__ldg(A.slice_base + (nid[a] >> 5)) + 32 * rk[a] + (nid[a] & 31);
     }
 
     if (!(det > Real(0))) {
@@ -295,7 +336,7 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
         atomicAdd(&A.ctrl->inv_count, 1ull);
         atomicMin(&A.ctrl->first_inv, (unsigned long long)e);
 #pragma unroll
-        for (int a = 0; a < NPE; ++a) T::store_node(ef + sl[a], Real(0), Real(0), Real(0));
+        for (int a = 0; a < NPE; ++a) store_row(A, sl[a], Real(0), Real(0), Real(0));
         return;
     }
     const Real s_inv = Real(1) / det;
@@ -390,11 +431,11 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
 
     if constexpr (KIND == 0) {
         // T4 rows: f1..f3 = columns of K, f0 = -(f1 + f2 + f3).
-        T::store_node(ef + sl[1], K[0][0], K[1][0], K[2][0]);
-        T::store_node(ef + sl[2], K[0][1], K[1][1], K[2][1]);
-        T::store_node(ef + sl[3], K[0][2], K[1][2], K[2][2]);
-        T::store_node(ef + sl[0], Real(-1) * ((K[0][0] + K[0][1]) + K[0][2]),
-                      Real(-1) * ((K[1][0] + K[1][1]) + K[1][2]), Real(-1) * ((K[2][0] + K[2][1]) + K[2][2]));
+        store_row(A, sl[1], K[0][0], K[1][0], K[2][0]);
+        store_row(A, sl[2], K[0][1], K[1][1], K[2][1]);
+        store_row(A, sl[3], K[0][2], K[1][2], K[2][2]);
+        store_row(A, sl[0], Real(-1) * ((K[0][0] + K[0][1]) + K[0][2]), Real(-1) * ((K[1][0] + K[1][1]) + K[1][2]),
+                  Real(-1) * ((K[2][0] + K[2][1]) + K[2][2]));
     } else {
         constexpr int S[8][3] = {{-1, -1, -1}, {+1, -1, -1}, {+1, +1, -1}, {-1, +1, -1},
                                  {-1, -1, +1}, {+1, -1, +1}, {+1, +1, +1}, {-1, +1, +1}};
@@ -432,7 +473,7 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
             }
         }
 #pragma unroll
-        for (int a = 0; a < 8; ++a) T::store_node(ef + sl[a], f[a][0], f[a][1], f[a][2]);
+        for (int a = 0; a < 8; ++a) store_row(A, sl[a], f[a][0], f[a][1], f[a][2]);
     }
 }
 
@@ -444,41 +485,46 @@ __device__ __forceinline__ P pick3(int i, P a, P b, P c) {
 }
 
 // Elements [e0, e1) of the step (one slab).
-template <class Real, int KIND, int MODEL>
+template <class Real, int KIND, int MODEL, int RB>
 __global__ void __launch_bounds__(128) k_element(const ElemArgs<Real> A, long long e0, long long e1) {
     const long long e = e0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= e1) return;
     if (__ldcg(&A.ctrl->halted)) return;
     const int phase = int(__ldcg(&A.ctrl->step) % 3);
     const typename RT<Real>::Node* u = A.u_override ? A.u_override : pick3(phase, A.u[0], A.u[1], A.u[2]);
-    element_body<Real, KIND, MODEL>(A, e, u);
+    element_body<Real, KIND, MODEL, RB>(A, e, u);
 }
 
 // ------------------------------------------------------------------ K2+K3
 
 // Sums node n's element rows in ascending element order from +0
 // (gather_nodal_forces, djtled_force.hpp:116-134). Slot k of the node sits at
-// p[32 k]; kCG reads through L2 only (slots written earlier in the same
-// launch by other SMs).
-template <class Real, bool kCG>
-__device__ __forceinline__ void gather_row(const typename RT<Real>::Node* __restrict__ p, int len, Real& sx,
-                                           Real& sy, Real& sz) {
-    using T = RT<Real>;
+// p0 + 32 k in each of the three planes.
+template <class Real>
+__device__ __forceinline__ void gather_row(const Real* __restrict__ ef, long long cap, long long p0, int len,
+                                           Real& sx, Real& sy, Real& sz) {
     sx = Real(0); sy = Real(0); sz = Real(0);
     int k = 0;
-    // Loads issued 4 at a time (independent), sums still strictly in slot order.
+    // Loads issued 4 slots at a time (independent), sums strictly in slot order.
     for (; k + 4 <= len; k += 4) {
-        typename T::Node v[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] = kCG ? T::load_l2(p + 32 * (k + q)) : T::load_stream(p + 32 * (k + q));
+        Real x[4], y[4], z[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            sx += v[q].x; sy += v[q].y; sz += v[q].z;
+            const long long i = p0 + 32 * (k + q);
+            x[q] = __ldcs(ef + i);
+            y[q] = __ldcs(ef + cap + i);
+            z[q] = __ldcs(ef + 2 * cap + i);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            sx += x[q]; sy += y[q]; sz += z[q];
         }
     }
     for (; k < len; ++k) {
-        const typename T::Node v = kCG ? T::load_l2(p + 32 * k) : T::load_stream(p + 32 * k);
-        sx += v.x; sy += v.y; sz += v.z;
+        const long long i = p0 + 32 * k;
+        sx += __ldcs(ef + i);
+        sy += __ldcs(ef + cap + i);
+        sz += __ldcs(ef + 2 * cap + i);
     }
 }
 
@@ -500,12 +546,12 @@ __device__ __forceinline__ Real dof_update(int kind, bool massless, Real c1, Rea
 
 // One node: gather + (assemble: write f | step: central difference into
 // u_next). Returns true if a non-finite displacement was produced.
-template <class Real, bool kAssemble, bool kCG>
-__device__ __forceinline__ bool node_body(const NodeArgs<Real>& A, const long long n,
-                                          const typename RT<Real>::Node* slots, int len, long long step) {
+template <class Real, bool kAssemble>
+__device__ __forceinline__ bool node_body(const NodeArgs<Real>& A, const long long n, long long p0, int len,
+                                          long long step) {
     using T = RT<Real>;
     Real fx, fy, fz;
-    gather_row<Real, kCG>(slots, len, fx, fy, fz);
+    gather_row<Real>(A.ef, A.cap, p0, len, fx, fy, fz);
     if constexpr (kAssemble) {
         A.f_out[3 * n + 0] = fx;
         A.f_out[3 * n + 1] = fy;
@@ -593,13 +639,16 @@ __global__ void __launch_bounds__(256) k_node_slices(const NodeArgs<Real> A, con
     if (w < nslices) {
         const int sl = slices[w];
         const long long n = 32ll * sl + lane;
-        const typename RT<Real>::Node* base = A.ef + (long long)A.slice_base[sl];
-        if (n < A.N && node_body<Real, kAssemble, false>(A, n, base + lane, A.row_len[n], step)) s_nonfinite = 1;
+        const long long b0 = A.slice_base[sl], b1 = A.slice_base[sl + 1];
+        if (n < A.N && node_body<Real, kAssemble>(A, n, b0 + lane, A.row_len[n], step)) s_nonfinite = 1;
         __syncwarp();
         if (discard) {
-            const char* lo = reinterpret_cast<const char*>(base);
-            const char* hi = reinterpret_cast<const char*>(A.ef + (long long)A.slice_base[sl + 1]);
-            for (const char* q = lo + 128 * lane; q < hi; q += 128 * 32) l2_discard(q);
+            // the slice's rows in each plane: 32 * width Reals, 128-byte aligned
+            for (int pl = 0; pl < 3; ++pl) {
+                const char* lo = reinterpret_cast<const char*>(A.ef + pl * A.cap + b0);
+                const char* hi = reinterpret_cast<const char*>(A.ef + pl * A.cap + b1);
+                for (const char* q = lo + 128 * lane; q < hi; q += 128 * 32) l2_discard(q);
+            }
         }
     }
     __syncthreads();

@@ -61,20 +61,26 @@ def test_cfg2_h8_nh_hourglass_2000_steps(precision):
 @pytest.mark.parametrize("precision", [4, 8])
 @pytest.mark.parametrize("kind", ["T4", "H8"])
 @pytest.mark.parametrize("model", ["NH", "TI", "OT", "MR"])
-@pytest.mark.parametrize("mode", ["fused", "two_kernel"])
-def test_materials_small(kind, model, precision, mode):
-    flags = A.DJG_FLAG_TWO_KERNEL if mode == "two_kernel" else 0
+@pytest.mark.parametrize("mode", ["default", "slabs"])
+def test_materials_small(kind, model, precision, mode, monkeypatch):
+    flags = 0
+    if mode == "slabs":
+        monkeypatch.setenv("DJG_SLAB_KB", "64")
+        flags = A.DJG_FLAG_SLABS
     check_run(box_spec(kind=kind, model=model, divisions=4, precision=precision, ramp_steps=300), 300, flags=flags)
 
 
 @pytest.mark.parametrize("cfg", ["cfg1", "cfg2"])
-def test_two_kernel_path_cfg(cfg):
-    check_run(config_spec(cfg, precision=4), 500, flags=A.DJG_FLAG_TWO_KERNEL)
+def test_slab_path_cfg(cfg, monkeypatch):
+    monkeypatch.setenv("DJG_SLAB_KB", "64")
+    check_run(config_spec(cfg, precision=4), 500, flags=A.DJG_FLAG_SLABS)
 
 
 def test_slab_schedule_on_large_mesh():
     sc = Scenario(config_spec("cfg3", precision=4))
     with GpuDjEngine(sc) as eng:
+        assert eng.info()["slabs"] == 1 and eng.info()["kernels_per_step"] == 2
+    with GpuDjEngine(sc, flags=A.DJG_FLAG_SLABS) as eng:
         info = eng.info()
     assert info["slabs"] > 1 and info["kernels_per_step"] == 2 * info["slabs"]
     assert info["slab_elements"] * info["npe"] * 16 <= 40 << 20
@@ -86,23 +92,25 @@ def test_many_slabs_bitwise(kind, model, monkeypatch):
     monkeypatch.setenv("DJG_SLAB_KB", "64")
     spec = box_spec(kind=kind, model=model, divisions=14, precision=4, ramp_steps=300)
     sc = Scenario(spec)
-    with GpuDjEngine(sc) as eng:
+    with GpuDjEngine(sc, flags=A.DJG_FLAG_SLABS) as eng:
         assert eng.info()["slabs"] >= 3
-    check_run(spec, 300)
-    check_run(spec, 300, flags=A.DJG_FLAG_NO_DISCARD)
+    check_run(spec, 300, flags=A.DJG_FLAG_SLABS)
+    check_run(spec, 300, flags=A.DJG_FLAG_SLABS | A.DJG_FLAG_NO_DISCARD)
 
 
 @pytest.mark.slow
 def test_cfg3_slab_vs_two_kernel_bitwise():
     spec = config_spec("cfg3", precision=4, target=0.01, ramp_steps=1000)
     a = run_gpu(spec, 50)[0]
-    b = run_gpu(spec, 50, flags=A.DJG_FLAG_TWO_KERNEL)[0]
-    c = run_gpu(spec, 50, flags=A.DJG_FLAG_NO_DISCARD)[0]
+    b = run_gpu(spec, 50, flags=A.DJG_FLAG_SLABS)[0]
+    c = run_gpu(spec, 50, flags=A.DJG_FLAG_SLABS | A.DJG_FLAG_NO_DISCARD)[0]
     assert np.array_equal(a, b) and np.array_equal(a, c)
 
 
-@pytest.mark.parametrize("flags", [A.DJG_FLAG_NO_DISCARD, A.DJG_FLAG_NO_GRAPH | A.DJG_FLAG_TWO_KERNEL])
-def test_variants_bitwise_cfg2(flags):
+@pytest.mark.parametrize("flags", [A.DJG_FLAG_SLABS | A.DJG_FLAG_NO_DISCARD, A.DJG_FLAG_NO_GRAPH | A.DJG_FLAG_SLABS,
+                                   A.DJG_FLAG_NO_GRAPH])
+def test_variants_bitwise_cfg2(flags, monkeypatch):
+    monkeypatch.setenv("DJG_SLAB_KB", "64")
     check_run(config_spec("cfg2", precision=4), 400, flags=flags)
 
 
@@ -193,7 +201,7 @@ def test_deterministic_repeats():
     a = run_gpu(spec, 300)[0]
     b = run_gpu(spec, 300)[0]
     c = run_gpu(spec, 300, flags=A.DJG_FLAG_NO_GRAPH)[0]
-    d = run_gpu(spec, 300, flags=A.DJG_FLAG_TWO_KERNEL)[0]
+    d = run_gpu(spec, 300, flags=A.DJG_FLAG_SLABS)[0]
     assert np.array_equal(a, b) and np.array_equal(a, c) and np.array_equal(a, d)
 
 

@@ -5,7 +5,7 @@
 //   rank        npe x 1|2 bytes per element: rank of the element in each node's CSR row
 //   consts      Plane planes [nplanes][E]  hot constants (float4 / double2)
 //   u[3]        Node[N]                    triple-buffered displacement (xyz+pad)
-//   ef          Real[3][capacity]          element-node forces (x, y, z planes) in sliced CSR order
+//   ef          Node[capacity]             element-node forces (xyz + pad) in sliced CSR order
 //   row_len, slice_base, c1, code, target, t_total, r_ext   node data
 //   ctrl        Ctrl                       step counter + failure flags
 // A step is k_element then k_node on one stream; multi-step calls replay a
@@ -234,7 +234,7 @@ public:
         for (auto& b : u_) b.alloc(size_t(N_) * sizeof(Node));
         uscratch_.alloc(size_t(N_) * sizeof(Node));
         flat_.alloc(size_t(3 * N_) * sizeof(Real));
-        ef_.alloc(size_t(3 * capacity_) * sizeof(Real));
+        ef_.alloc(size_t(capacity_) * sizeof(Node));
         CK(cudaMemset(ef_.p, 0, ef_.bytes));
         rowlen_.alloc(row_len.size() * sizeof(int32_t));
         CK(cudaMemcpy(rowlen_.p, row_len.data(), rowlen_.bytes, cudaMemcpyHostToDevice));
@@ -254,8 +254,7 @@ public:
         ea_.c = consts_.as<Plane>();
         for (int i = 0; i < 3; ++i) ea_.u[i] = u_[i].as<Node>();
         ea_.u_override = nullptr;
-        ea_.ef = ef_.as<Real>();
-        ea_.cap = capacity_;
+        ea_.ef = ef_.as<Node>();
         ea_.ctrl = ctrl_.as<Ctrl>();
         const Real mu = Real(d.material.mu), c10 = Real(d.material.c10);
         ea_.mat.dI1 = model_ == DJG_MR ? c10 : mu / 2;
@@ -266,8 +265,7 @@ public:
         na_.N = N_;
         na_.row_len = rowlen_.as<int>();
         na_.slice_base = slicebase_.as<int>();
-        na_.ef = ef_.as<Real>();
-        na_.cap = capacity_;
+        na_.ef = ef_.as<Node>();
         for (int i = 0; i < 3; ++i) na_.u[i] = u_[i].as<Node>();
         na_.r_ext = nullptr;
         na_.c1 = c1_.as<Real>();
@@ -352,7 +350,7 @@ public:
         int64_t se = E_;
         if ((flags_ & DJG_FLAG_SLABS) || slab_bytes_ > 0) {
             const int64_t bytes = slab_bytes_ > 0 ? slab_bytes_ : kSlabBytes;
-            se = std::max<int64_t>(4096, bytes / (int64_t(npe_) * int64_t(sizeof(Node))));
+            se = std::max<int64_t>(1024, bytes / (int64_t(npe_) * int64_t(sizeof(Node))));
             se = (se + 127) / 128 * 128;
         }
         const int64_t S = std::max<int64_t>(1, (E_ + se - 1) / se);

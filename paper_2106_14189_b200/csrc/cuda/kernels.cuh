@@ -130,8 +130,7 @@ struct ElemArgs {
     const typename RT<Real>::Plane* c;   // nplanes planes of Plane[E]
     const typename RT<Real>::Node* u[3]; // triple-buffered displacement
     const typename RT<Real>::Node* u_override;
-    Real* ef;                            // force slots: x plane, y plane (+cap), z plane (+2 cap)
-    long long cap;                       // slots per plane
+    typename RT<Real>::Node* ef;         // force slots (xyz + pad), sliced CSR order
     Ctrl* ctrl;
     MatParams<Real> mat;
 };
@@ -141,8 +140,7 @@ struct NodeArgs {
     long long N;
     const int* row_len;                  // CSR row length per node
     const int* slice_base;               // first slot position of each 32-node slice
-    const Real* ef;                      // force slots (x, y, z planes, stride cap)
-    long long cap;
+    const typename RT<Real>::Node* ef;   // force slots
     typename RT<Real>::Node* u[3];
     const typename RT<Real>::Node* r_ext;  // NULL: identically zero
     const Real* c1;
@@ -214,13 +212,12 @@ __global__ void k_cbrt(const Real* __restrict__ in, Real* __restrict__ out, long
 
 // ------------------------------------------------------------------ K1
 
-// Force row of element-node a into slot (slice_base[n/32] + 32 rank + n%32)
-// of the three slot planes.
+// Force row of element-node a into slot slice_base[n/32] + 32 rank + n%32:
+// one 16-byte (f64: 32-byte) store. (Three 4-byte planes move 25 % fewer
+// bytes but cost more in scattered L2 write transactions than they save.)
 template <class Real>
 __device__ __forceinline__ void store_row(const ElemArgs<Real>& A, long long pos, Real x, Real y, Real z) {
-    A.ef[pos] = x;
-    A.ef[A.cap + pos] = y;
-    A.ef[2 * A.cap + pos] = z;
+    RT<Real>::store_node(A.ef + pos, x, y, z);
 }
 
 // Ranks of element e in its nodes' CSR rows (RB bytes each).
@@ -499,32 +496,26 @@ __global__ void __launch_bounds__(128) k_element(const ElemArgs<Real> A, long lo
 
 // Sums node n's element rows in ascending element order from +0
 // (gather_nodal_forces, djtled_force.hpp:116-134). Slot k of the node sits at
-// p0 + 32 k in each of the three planes.
+// ef[p0 + 32 k]: lane i of a slice reads consecutive 16-byte rows.
 template <class Real>
-__device__ __forceinline__ void gather_row(const Real* __restrict__ ef, long long cap, long long p0, int len,
+__device__ __forceinline__ void gather_row(const typename RT<Real>::Node* __restrict__ ef, long long p0, int len,
                                            Real& sx, Real& sy, Real& sz) {
+    using T = RT<Real>;
     sx = Real(0); sy = Real(0); sz = Real(0);
     int k = 0;
     // Loads issued 4 slots at a time (independent), sums strictly in slot order.
     for (; k + 4 <= len; k += 4) {
-        Real x[4], y[4], z[4];
+        typename T::Node v[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = T::load_stream(ef + p0 + 32 * (k + q));
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            const long long i = p0 + 32 * (k + q);
-            x[q] = __ldcs(ef + i);
-            y[q] = __ldcs(ef + cap + i);
-            z[q] = __ldcs(ef + 2 * cap + i);
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            sx += x[q]; sy += y[q]; sz += z[q];
+            sx += v[q].x; sy += v[q].y; sz += v[q].z;
         }
     }
     for (; k < len; ++k) {
-        const long long i = p0 + 32 * k;
-        sx += __ldcs(ef + i);
-        sy += __ldcs(ef + cap + i);
-        sz += __ldcs(ef + 2 * cap + i);
+        const typename T::Node v = T::load_stream(ef + p0 + 32 * k);
+        sx += v.x; sy += v.y; sz += v.z;
     }
 }
 
@@ -551,7 +542,7 @@ __device__ __forceinline__ bool node_body(const NodeArgs<Real>& A, const long lo
                                           long long step) {
     using T = RT<Real>;
     Real fx, fy, fz;
-    gather_row<Real>(A.ef, A.cap, p0, len, fx, fy, fz);
+    gather_row<Real>(A.ef, p0, len, fx, fy, fz);
     if constexpr (kAssemble) {
         A.f_out[3 * n + 0] = fx;
         A.f_out[3 * n + 1] = fy;
@@ -643,12 +634,10 @@ __global__ void __launch_bounds__(256) k_node_slices(const NodeArgs<Real> A, con
         if (n < A.N && node_body<Real, kAssemble>(A, n, b0 + lane, A.row_len[n], step)) s_nonfinite = 1;
         __syncwarp();
         if (discard) {
-            // the slice's rows in each plane: 32 * width Reals, 128-byte aligned
-            for (int pl = 0; pl < 3; ++pl) {
-                const char* lo = reinterpret_cast<const char*>(A.ef + pl * A.cap + b0);
-                const char* hi = reinterpret_cast<const char*>(A.ef + pl * A.cap + b1);
-                for (const char* q = lo + 128 * lane; q < hi; q += 128 * 32) l2_discard(q);
-            }
+            // the slice's rows: 32 * width slots, 128-byte aligned
+            const char* lo = reinterpret_cast<const char*>(A.ef + b0);
+            const char* hi = reinterpret_cast<const char*>(A.ef + b1);
+            for (const char* q = lo + 128 * lane; q < hi; q += 128 * 32) l2_discard(q);
         }
     }
     __syncthreads();

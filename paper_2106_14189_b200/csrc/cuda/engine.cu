@@ -497,6 +497,13 @@ public:
     }
 
     void launch_node(cudaStream_t s, int slab, bool assemble_mode) {
+        if (n_slabs_ == 1) {
+            const unsigned g = unsigned((N_ + 255) / 256);
+            if (assemble_mode) k_node<Real, true><<<g, 256, 0, s>>>(na_);
+            else k_node<Real, false><<<g, 256, 0, s>>>(na_);
+            CK(cudaGetLastError());
+            return;
+        }
         const int n = slab_off_[size_t(slab + 1)] - slab_off_[size_t(slab)];
         const int close = slab == n_slabs_ - 1;
         if (n == 0 && !close) return;

@@ -602,6 +602,30 @@ __device__ __forceinline__ void close_step(Ctrl* ctrl, long long step, int polic
     ctrl->diverged = 0;
 }
 
+// Whole-mesh gather + update (the default single-slab step): one thread per
+// node, the last block to finish closes the step.
+template <class Real, bool kAssemble>
+__global__ void __launch_bounds__(256) k_node(const NodeArgs<Real> A) {
+    Ctrl* ctrl = A.ctrl;
+    if (__ldcg(&ctrl->halted) && !kAssemble) return;
+    __shared__ int s_nonfinite;
+    if (threadIdx.x == 0) s_nonfinite = 0;
+    __syncthreads();
+    const long long step = __ldcg(&ctrl->step);
+    const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n < A.N && node_body<Real, kAssemble>(A, n, (long long)A.slice_base[n >> 5] + (n & 31), A.row_len[n], step))
+        s_nonfinite = 1;
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    if (s_nonfinite) atomicOr(&ctrl->diverged, 1);
+    __threadfence();
+    const unsigned int done = atomicAdd(&ctrl->blocks_done, 1u);
+    if (done != gridDim.x - 1) return;
+    close_step<kAssemble>(ctrl, step, A.policy);
+    __threadfence();
+    ctrl->blocks_done = 0;
+}
+
 // ------------------------------------------------------------------ slab step
 
 // A step runs as S slabs: k_element over elements [e0, e1), then k_node_slices

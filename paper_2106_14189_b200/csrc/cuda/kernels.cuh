@@ -216,7 +216,7 @@ __global__ void k_cbrt(const Real* __restrict__ in, Real* __restrict__ out, long
 // one 16-byte (f64: 32-byte) store. (Three 4-byte planes move 25 % fewer
 // bytes but cost more in scattered L2 write transactions than they save.)
 template <class Real>
-__device__ __forceinline__ void store_row(const ElemArgs<Real>& A, long long pos, Real x, Real y, Real z) {
+__device__ __forceinline__ void store_row(const ElemArgs<Real>& A, int pos, Real x, Real y, Real z) {
     RT<Real>::store_node(A.ef + pos, x, y, z);
 }
 
@@ -320,12 +320,12 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
                      Jt[0][1] * (Jt[1][0] * Jt[2][2] - Jt[1][2] * Jt[2][0]) +
                      Jt[0][2] * (Jt[1][0] * Jt[2][1] - Jt[1][1] * Jt[2][0]);
 
-    long long sl[NPE];
+    int sl[NPE];  // slot positions fit in 32 bits (checked at engine creation)
     {
         int rk[NPE];
         load_ranks<NPE, RB>(A.rank, e, rk);
 #pragma unroll
-        for (int a = 0; a < NPE; ++a) sl[a] = (long long)__ldg(A.slice_base + (nid[a] >> 5)) + 32 * rk[a] + (nid[a] & 31);
+        for (int a = 0; a < NPE; ++a) sl[a] = __ldg(A.slice_base + (nid[a] >> 5)) + 32 * rk[a] + (nid[a] & 31);
     }
 
     if (!(det > Real(0))) {
@@ -502,18 +502,7 @@ __device__ __forceinline__ void gather_row(const typename RT<Real>::Node* __rest
                                            Real& sx, Real& sy, Real& sz) {
     using T = RT<Real>;
     sx = Real(0); sy = Real(0); sz = Real(0);
-    int k = 0;
-    // Loads issued 4 slots at a time (independent), sums strictly in slot order.
-    for (; k + 4 <= len; k += 4) {
-        typename T::Node v[4];
-#pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] = T::load_stream(ef + p0 + 32 * (k + q));
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            sx += v[q].x; sy += v[q].y; sz += v[q].z;
-        }
-    }
-    for (; k < len; ++k) {
+    for (int k = 0; k < len; ++k) {
         const typename T::Node v = T::load_stream(ef + p0 + 32 * k);
         sx += v.x; sy += v.y; sz += v.z;
     }

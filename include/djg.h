@@ -164,6 +164,26 @@ int djg_assemble(djg_engine* eng, const void* u, void* f_int, djg_assemble_stats
 int djg_profile_steps(djg_engine* eng, int64_t nsteps, float* ms_element, float* ms_node,
                       float* ms_total);
 
+/*
+ * Multi-GPU step, one engine per part (djg_partition_desc).
+ * Per step, on the engine stream, with the communication in between done by
+ * the caller's NCCL (or any transport):
+ *   djg_step_async(eng, 1)              local elements, owned nodes
+ *   djg_halo_pack(eng, send)            owned nodes others reference -> send
+ *   <exchange send/recv with the neighbors>
+ *   djg_halo_unpack(eng, recv)          recv -> ghost nodes
+ *   djg_step_status(eng, status)        int64[2] failure summary of this part
+ *   <allreduce MAX of status over parts>
+ *   djg_step_agree(eng, reduced)        every part halts at the same state
+ * Halo buffers hold one 16-byte (f32) / 32-byte (f64) node record per entry.
+ */
+int djg_set_partition(djg_engine* eng, int64_t num_owned, const int64_t* elem_l2g);
+int djg_set_halo(djg_engine* eng, int64_t nsend, const int32_t* send_nodes, int64_t nrecv, const int32_t* recv_nodes);
+int djg_halo_pack(djg_engine* eng, void* dev_send);
+int djg_halo_unpack(djg_engine* eng, const void* dev_recv);
+int djg_step_status(djg_engine* eng, int64_t* dev_status);
+int djg_step_agree(djg_engine* eng, const int64_t* dev_reduced);
+
 /* Layout facts for roofline accounting and tests. */
 typedef struct djg_engine_info {
     int64_t num_nodes, num_elements;

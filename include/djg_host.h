@@ -51,6 +51,45 @@ int djg_scenario_image(const djg_scenario* sc, const djg_image_ptrs* out);
  * the scenario lives). */
 int djg_scenario_desc(const djg_scenario* sc, int32_t device, djg_desc* out);
 
+/*
+ * Multi-GPU decomposition; no reference analogue (the
+ * reference is single-process). Part `part` of `nparts` of a built scenario:
+ * recursive coordinate bisection of element centroids; a node belongs to the
+ * part of its lowest-id element; a part computes every element touching its
+ * nodes (ghost elements included) in ascending global element id, so owned
+ * nodes are bit-identical to the single-GPU step. Local node numbering: owned
+ * nodes first, then ghost nodes, each ascending in global id.
+ */
+typedef struct djg_partition djg_partition;
+
+typedef struct djg_partition_info {
+    int32_t nparts, part;
+    int32_t num_neighbors, _pad;
+    int64_t num_nodes;        /* local nodes (owned + ghost) */
+    int64_t num_owned;        /* owned nodes: local ids [0, num_owned) */
+    int64_t num_elements;     /* local elements (owned + ghost) */
+    int64_t owned_elements;   /* elements assigned to this part */
+    int64_t send_total, recv_total;
+    int64_t global_nodes, global_elements;
+} djg_partition_info;
+
+int djg_partition_build(const djg_scenario* sc, int32_t nparts, int32_t part, djg_partition** out);
+void djg_partition_free(djg_partition* p);
+int djg_partition_get_info(const djg_partition* p, djg_partition_info* out);
+/* Local problem arrays (same layout as djg_scenario_image, local ids). */
+int djg_partition_image(const djg_partition* p, const djg_image_ptrs* out);
+/* Engine descriptor of the local problem (pointers alias the partition). */
+int djg_partition_desc(const djg_partition* p, int32_t device, djg_desc* out);
+/* Halo lists: neighbors[num_neighbors]; send_off/recv_off[num_neighbors+1];
+ * send_nodes[send_total] (owned local ids), recv_nodes[recv_total] (ghost
+ * local ids), each neighbor's block ascending in global node id. */
+int djg_partition_halo(const djg_partition* p, int32_t* neighbors, int64_t* send_off, int64_t* recv_off,
+                       int32_t* send_nodes, int32_t* recv_nodes);
+/* Local -> global ids: node_l2g[num_nodes], elem_l2g[num_elements]. */
+int djg_partition_maps(const djg_partition* p, int64_t* node_l2g, int64_t* elem_l2g);
+/* Element -> part assignment of the whole scenario (E entries). */
+int djg_element_parts(const djg_scenario* sc, int32_t nparts, int32_t* part);
+
 #ifdef __cplusplus
 }
 #endif

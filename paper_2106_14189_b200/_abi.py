@@ -132,6 +132,15 @@ class djg_step_desc(C.Structure):
     ]
 
 
+class djg_partition_info(C.Structure):
+    _fields_ = [
+        ("nparts", C.c_int32), ("part", C.c_int32), ("num_neighbors", C.c_int32), ("_pad", C.c_int32),
+        ("num_nodes", C.c_int64), ("num_owned", C.c_int64), ("num_elements", C.c_int64),
+        ("owned_elements", C.c_int64), ("send_total", C.c_int64), ("recv_total", C.c_int64),
+        ("global_nodes", C.c_int64), ("global_elements", C.c_int64),
+    ]
+
+
 class djg_engine_info(C.Structure):
     _fields_ = [
         ("num_nodes", C.c_int64), ("num_elements", C.c_int64), ("num_slots", C.c_int64),
@@ -178,6 +187,20 @@ EXPORTS = [
     ("djg_get_info", C.c_int, [C.c_void_p, _P(djg_engine_info)]),
     ("djg_get_slot_map", C.c_int, [C.c_void_p, C.c_void_p]),
     ("djg_debug_cbrt", C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32]),
+    ("djg_set_partition", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),
+    ("djg_set_halo", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]),
+    ("djg_halo_pack", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("djg_halo_unpack", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("djg_step_status", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("djg_step_agree", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("djg_partition_build", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, _P(C.c_void_p)]),
+    ("djg_partition_free", None, [C.c_void_p]),
+    ("djg_partition_get_info", C.c_int, [C.c_void_p, _P(djg_partition_info)]),
+    ("djg_partition_desc", C.c_int, [C.c_void_p, C.c_int32, _P(djg_desc)]),
+    ("djg_partition_image", C.c_int, [C.c_void_p, _P(djg_image_ptrs)]),
+    ("djg_partition_halo", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("djg_partition_maps", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("djg_element_parts", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     ("djg_last_error", C.c_char_p, [C.c_void_p]),
     ("djg_status_string", C.c_char_p, [C.c_int32]),
     ("djg_create_error", C.c_char_p, []),

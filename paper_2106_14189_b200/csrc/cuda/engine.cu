@@ -89,6 +89,12 @@ public:
     virtual cudaStream_t stream() const = 0;
     virtual void configure_step(const djg_step_desc& s) = 0;
     virtual void set_policy(int policy) = 0;
+    virtual void set_partition(int64_t num_owned, const int64_t* elem_l2g) = 0;
+    virtual void set_halo(int64_t nsend, const int32_t* send, int64_t nrecv, const int32_t* recv) = 0;
+    virtual void halo_pack(void* dev_out) = 0;
+    virtual void halo_unpack(const void* dev_in) = 0;
+    virtual void step_status(int64_t* dev_status) = 0;
+    virtual void step_agree(const int64_t* dev_reduced) = 0;
 };
 
 template <class Real>
@@ -334,6 +340,59 @@ public:
         }
         configure(c1.data(), massless.data(), s.dof_kind, static_cast<const Real*>(s.dof_target),
                   static_cast<const Real*>(s.dof_t_total), c2, c3, dt);
+    }
+
+    // Multi-GPU: only nodes [0, num_owned) are gathered and updated; ghost
+    // nodes come from the halo. Inverted elements are reported in global ids.
+    void set_partition(int64_t num_owned, const int64_t* elem_l2g) override {
+        if (num_owned < 0 || num_owned > N_) throw DescError("num_owned out of range");
+        na_.N = num_owned;
+        if (elem_l2g) {
+            elemL2g_.alloc(size_t(E_) * sizeof(int64_t));
+            CK(cudaMemcpy(elemL2g_.p, elem_l2g, elemL2g_.bytes, cudaMemcpyHostToDevice));
+        }
+        drop_graphs();
+    }
+
+    void set_halo(int64_t nsend, const int32_t* send, int64_t nrecv, const int32_t* recv) override {
+        auto up = [&](DevBuf& b, int64_t n, const int32_t* v) {
+            for (int64_t i = 0; i < n; ++i)
+                if (v[i] < 0 || v[i] >= N_) throw DescError("halo node index out of range");
+            b.alloc(size_t(std::max<int64_t>(n, 1)) * sizeof(int32_t));
+            if (n) CK(cudaMemcpy(b.p, v, size_t(n) * sizeof(int32_t), cudaMemcpyHostToDevice));
+        };
+        up(haloSend_, nsend, send);
+        up(haloRecv_, nrecv, recv);
+        nsend_ = nsend;
+        nrecv_ = nrecv;
+    }
+
+    void halo_pack(void* dev_out) override {
+        if (nsend_ == 0) return;
+        k_halo_pack<Real><<<unsigned((nsend_ + 255) / 256), 256, 0, stream_>>>(
+            ctrl_.as<Ctrl>(), u_[0].as<Node>(), u_[1].as<Node>(), u_[2].as<Node>(), haloSend_.as<int>(), nsend_,
+            static_cast<Node*>(dev_out));
+        CK(cudaGetLastError());
+    }
+
+    void halo_unpack(const void* dev_in) override {
+        if (nrecv_ == 0) return;
+        k_halo_unpack<Real><<<unsigned((nrecv_ + 255) / 256), 256, 0, stream_>>>(
+            ctrl_.as<Ctrl>(), u_[0].as<Node>(), u_[1].as<Node>(), u_[2].as<Node>(), haloRecv_.as<int>(), nrecv_,
+            static_cast<const Node*>(dev_in));
+        CK(cudaGetLastError());
+    }
+
+    void step_status(int64_t* dev_status) override {
+        if (!elemL2g_.p) throw DescError("step_status needs djg_set_partition with elem_l2g");
+        k_step_status<<<1, 1, 0, stream_>>>(ctrl_.as<Ctrl>(), elemL2g_.as<long long>(),
+                                            reinterpret_cast<long long*>(dev_status));
+        CK(cudaGetLastError());
+    }
+
+    void step_agree(const int64_t* dev_reduced) override {
+        k_agree<<<1, 1, 0, stream_>>>(ctrl_.as<Ctrl>(), reinterpret_cast<const long long*>(dev_reduced));
+        CK(cudaGetLastError());
     }
 
     void set_policy(int policy) override {
@@ -686,6 +745,8 @@ private:
     cudaStream_t stream_ = nullptr;
     std::vector<int32_t> slice_base_;
     int rank_bytes_ = 1;
+    DevBuf elemL2g_, haloSend_, haloRecv_;
+    int64_t nsend_ = 0, nrecv_ = 0;
     DevBuf conn_, rank_, consts_, u_[3], uscratch_, flat_, ef_, rowlen_, slicebase_, c1_, code_, target_, tTotal_,
         rext_, ctrl_;
     Ctrl* hctrl_ = nullptr;
@@ -850,6 +911,48 @@ int djg_configure_step(djg_engine* eng, const djg_step_desc* s) {
 int djg_set_policy(djg_engine* eng, int32_t policy) {
     return guarded(eng, [&](djg::EngineBase& e) {
         e.set_policy(policy);
+        return DJG_OK;
+    });
+}
+
+int djg_set_partition(djg_engine* eng, int64_t num_owned, const int64_t* elem_l2g) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.set_partition(num_owned, elem_l2g);
+        return DJG_OK;
+    });
+}
+
+int djg_set_halo(djg_engine* eng, int64_t nsend, const int32_t* send_nodes, int64_t nrecv, const int32_t* recv_nodes) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.set_halo(nsend, send_nodes, nrecv, recv_nodes);
+        return DJG_OK;
+    });
+}
+
+int djg_halo_pack(djg_engine* eng, void* dev_send) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.halo_pack(dev_send);
+        return DJG_OK;
+    });
+}
+
+int djg_halo_unpack(djg_engine* eng, const void* dev_recv) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.halo_unpack(dev_recv);
+        return DJG_OK;
+    });
+}
+
+int djg_step_status(djg_engine* eng, int64_t* dev_status) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.step_status(dev_status);
+        return DJG_OK;
+    });
+}
+
+int djg_step_agree(djg_engine* eng, const int64_t* dev_reduced) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.step_agree(dev_reduced);
         return DJG_OK;
     });
 }

@@ -667,6 +667,55 @@ __global__ void __launch_bounds__(256) k_node_slices(const NodeArgs<Real> A, con
     ctrl->blocks_done = 0;
 }
 
+// ------------------------------------------------------------------ halo
+
+// Multi-GPU step: after the local step, owners send the new
+// displacement of nodes other parts reference; receivers overwrite their
+// ghost copies. Both read the phase from the control block, so they follow
+// the device-side buffer rotation.
+template <class Real>
+__global__ void k_halo_pack(const Ctrl* ctrl, typename RT<Real>::Node* u0, typename RT<Real>::Node* u1,
+                            typename RT<Real>::Node* u2, const int* __restrict__ idx, long long n,
+                            typename RT<Real>::Node* __restrict__ out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const typename RT<Real>::Node* u = pick3(int(__ldcg(&ctrl->step) % 3), u0, u1, u2);
+    out[i] = u[idx[i]];
+}
+
+template <class Real>
+__global__ void k_halo_unpack(const Ctrl* ctrl, typename RT<Real>::Node* u0, typename RT<Real>::Node* u1,
+                              typename RT<Real>::Node* u2, const int* __restrict__ idx, long long n,
+                              const typename RT<Real>::Node* __restrict__ in) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    typename RT<Real>::Node* u = pick3(int(__ldcg(&ctrl->step) % 3), u0, u1, u2);
+    u[idx[i]] = in[i];
+}
+
+// Failure agreement across parts. status[0]: 2 inversion (Abort), 1
+// divergence, 0 none (inversion outranks divergence, as assemble runs before
+// the update in advance_step); status[1]: -(global id of the first inverted
+// element) or INT64_MIN. Reduced with MAX over parts, then k_agree applies the
+// global outcome: parts that did advance roll back one step (their previous
+// two buffers are intact), so every part halts at the same state.
+__global__ void k_step_status(const Ctrl* ctrl, const long long* __restrict__ elem_l2g, long long* status) {
+    const int h = ctrl->halted;
+    status[0] = h == 4 ? 2 : (h == 5 ? 1 : 0);
+    status[1] = (h == 4 && ctrl->halt_first_inv >= 0) ? -elem_l2g[ctrl->halt_first_inv] : (long long)(-0x7fffffffffffffffll - 1);
+}
+
+__global__ void k_agree(Ctrl* ctrl, const long long* __restrict__ reduced) {
+    const long long code = reduced[0];
+    if (code == 0) return;
+    if (ctrl->halted == 0) {
+        ctrl->step -= 1;  // this part advanced; another one failed the same step
+        ctrl->fail_step = ctrl->step + 1;
+    }
+    ctrl->halted = code == 2 ? 4 : 5;
+    ctrl->halt_first_inv = code == 2 ? -reduced[1] : -1;
+}
+
 // ------------------------------------------------------------------ setup
 
 // AoS record chunk -> plane layout: plane p of element e holds record Reals

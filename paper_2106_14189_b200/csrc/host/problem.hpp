@@ -716,3 +716,203 @@ inline Problem<Real> build_problem(const djg_scenario_spec& s, int threads) {
 }
 
 }  // namespace djg
+
+// ---------------------------------------------------------------- partition
+//
+// Multi-GPU decomposition. Elements are split by recursive
+// coordinate bisection of their centroids (ties broken by element id, so the
+// result is reproducible); a node is owned by the part of its lowest-id
+// element. Part p computes every element touching a node it owns (its own
+// plus "ghost" elements), in ascending global element id, so the gather of an
+// owned node sums exactly the same rows in exactly the same order as on one
+// GPU: results are bit-identical for any part count. After each step, owners
+// send the displacement of nodes other parts reference (halo).
+
+namespace djg {
+
+template <class Real>
+inline std::vector<int32_t> rcb_parts(const Mesh<Real>& m, int nparts) {
+    const int64_t E = m.num_elements();
+    const int npe = m.npe();
+    std::vector<double> c(size_t(3 * E));
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < E; ++e)
+        for (int i = 0; i < 3; ++i) {
+            double s = 0;
+            for (int a = 0; a < npe; ++a) s += double(m.nodes[size_t(3 * m.conn[size_t(e * npe + a)] + i)]);
+            c[size_t(3 * e + i)] = s / npe;
+        }
+    std::vector<int64_t> idx(static_cast<size_t>(E));
+    for (int64_t e = 0; e < E; ++e) idx[size_t(e)] = e;
+    std::vector<int32_t> part(static_cast<size_t>(E), 0);
+    struct Job {
+        int64_t lo, hi;
+        int p0, np;
+    };
+    std::vector<Job> stack{{0, E, 0, nparts}};
+    while (!stack.empty()) {
+        const Job j = stack.back();
+        stack.pop_back();
+        if (j.np <= 1 || j.hi - j.lo <= 1) {
+            for (int64_t q = j.lo; q < j.hi; ++q) part[size_t(idx[size_t(q)])] = j.p0;
+            continue;
+        }
+        double lo[3] = {1e300, 1e300, 1e300}, hi[3] = {-1e300, -1e300, -1e300};
+        for (int64_t q = j.lo; q < j.hi; ++q)
+            for (int i = 0; i < 3; ++i) {
+                lo[i] = std::min(lo[i], c[size_t(3 * idx[size_t(q)] + i)]);
+                hi[i] = std::max(hi[i], c[size_t(3 * idx[size_t(q)] + i)]);
+            }
+        int ax = 0;
+        for (int i = 1; i < 3; ++i)
+            if (hi[i] - lo[i] > hi[ax] - lo[ax]) ax = i;
+        const int nl = j.np / 2;
+        const int64_t mid = j.lo + (j.hi - j.lo) * nl / j.np;
+        // strict total order (coordinate, id): the split set is unique
+        std::nth_element(idx.begin() + j.lo, idx.begin() + mid, idx.begin() + j.hi, [&](int64_t a, int64_t b) {
+            const double ca = c[size_t(3 * a + ax)], cb = c[size_t(3 * b + ax)];
+            return ca < cb || (ca == cb && a < b);
+        });
+        stack.push_back({mid, j.hi, j.p0 + nl, j.np - nl});
+        stack.push_back({j.lo, mid, j.p0, nl});
+    }
+    return part;
+}
+
+struct Halo {
+    std::vector<int32_t> neighbors;    // ascending part ids
+    std::vector<int64_t> send_off;     // per neighbor, into send_nodes
+    std::vector<int64_t> recv_off;     // per neighbor, into recv_nodes
+    std::vector<int32_t> send_nodes;   // local ids of owned nodes, ascending global id per neighbor
+    std::vector<int32_t> recv_nodes;   // local ids of ghost nodes, ascending global id per neighbor
+};
+
+// Local problem of one part: same layout as Problem, renumbered. Owned nodes
+// come first (ascending global id), ghost nodes after (ascending global id);
+// local elements ascend in global id.
+template <class Real>
+struct PartProblem {
+    Problem<Real> local;
+    int nparts = 1, part = 0;
+    int64_t num_owned = 0, global_nodes = 0, global_elements = 0, owned_elements = 0;
+    std::vector<int64_t> node_l2g, elem_l2g;
+    Halo halo;
+};
+
+template <class Real>
+inline PartProblem<Real> build_part(const Problem<Real>& P, int nparts, int part) {
+    if (nparts < 1 || part < 0 || part >= nparts) throw ConfigError("invalid part index");
+    const Mesh<Real>& m = P.mesh;
+    const int npe = m.npe();
+    const int64_t N = m.num_nodes(), E = m.num_elements();
+    const std::vector<int32_t> epart = rcb_parts(m, nparts);
+    // owner of a node: part of its lowest-id element (first in its CSR row)
+    std::vector<int32_t> owner(static_cast<size_t>(N), 0);  // isolated nodes: part 0
+#pragma omp parallel for schedule(static)
+    for (int64_t n = 0; n < N; ++n)
+        if (P.adj.offsets[size_t(n + 1)] > P.adj.offsets[size_t(n)])
+            owner[size_t(n)] = epart[size_t(P.adj.elem[size_t(P.adj.offsets[size_t(n)])])];
+    // elements computed by this part: any node owned here
+    PartProblem<Real> R;
+    R.nparts = nparts;
+    R.part = part;
+    R.global_nodes = N;
+    R.global_elements = E;
+    std::vector<uint8_t> elocal(static_cast<size_t>(E), 0);
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < E; ++e)
+        for (int a = 0; a < npe; ++a)
+            if (owner[size_t(m.conn[size_t(e * npe + a)])] == part) elocal[size_t(e)] = 1;
+    for (int64_t e = 0; e < E; ++e)
+        if (elocal[size_t(e)]) {
+            R.elem_l2g.push_back(e);
+            if (epart[size_t(e)] == part) ++R.owned_elements;
+        }
+    // local nodes: owned (ascending), then ghosts (ascending)
+    std::vector<uint8_t> nlocal(static_cast<size_t>(N), 0);
+    for (int64_t e : R.elem_l2g)
+        for (int a = 0; a < npe; ++a) nlocal[size_t(m.conn[size_t(e * npe + a)])] = 1;
+    for (int64_t n = 0; n < N; ++n)
+        if (owner[size_t(n)] == part && (nlocal[size_t(n)] || P.adj.offsets[size_t(n + 1)] == P.adj.offsets[size_t(n)]))
+            R.node_l2g.push_back(n);
+    R.num_owned = int64_t(R.node_l2g.size());
+    for (int64_t n = 0; n < N; ++n)
+        if (nlocal[size_t(n)] && owner[size_t(n)] != part) R.node_l2g.push_back(n);
+    std::vector<int32_t> g2l(static_cast<size_t>(N), -1);
+    for (size_t q = 0; q < R.node_l2g.size(); ++q) g2l[size_t(R.node_l2g[q])] = int32_t(q);
+    // local problem arrays
+    Problem<Real>& L = R.local;
+    L.mat = P.mat;
+    L.nconst = P.nconst;
+    L.dt = P.dt;
+    L.crit_dt = P.crit_dt;
+    L.alpha = P.alpha;
+    L.c2 = P.c2;
+    L.c3 = P.c3;
+    L.ramp_t_total = P.ramp_t_total;
+    L.c_wave = P.c_wave;
+    L.policy = P.policy;
+    L.mesh.kind = m.kind;
+    const int64_t Nl = int64_t(R.node_l2g.size()), El = int64_t(R.elem_l2g.size());
+    L.mesh.nodes.resize(size_t(3 * Nl));
+    L.mass.resize(size_t(Nl));
+    L.c1.resize(size_t(Nl));
+    L.massless.resize(size_t(Nl));
+    L.dof_kind.resize(size_t(3 * Nl));
+    L.dof_target.resize(size_t(3 * Nl));
+    L.dof_t_total.resize(size_t(3 * Nl));
+    for (int64_t q = 0; q < Nl; ++q) {
+        const int64_t n = R.node_l2g[size_t(q)];
+        for (int i = 0; i < 3; ++i) {
+            L.mesh.nodes[size_t(3 * q + i)] = m.nodes[size_t(3 * n + i)];
+            L.dof_kind[size_t(3 * q + i)] = P.dof_kind[size_t(3 * n + i)];
+            L.dof_target[size_t(3 * q + i)] = P.dof_target[size_t(3 * n + i)];
+            L.dof_t_total[size_t(3 * q + i)] = P.dof_t_total[size_t(3 * n + i)];
+        }
+        L.mass[size_t(q)] = P.mass[size_t(n)];
+        L.c1[size_t(q)] = P.c1[size_t(n)];
+        L.massless[size_t(q)] = P.massless[size_t(n)];
+    }
+    L.mesh.conn.resize(size_t(El * npe));
+    L.consts.resize(size_t(El) * size_t(P.nconst));
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < El; ++q) {
+        const int64_t e = R.elem_l2g[size_t(q)];
+        for (int a = 0; a < npe; ++a) L.mesh.conn[size_t(q * npe + a)] = g2l[size_t(m.conn[size_t(e * npe + a)])];
+        std::copy(P.consts.begin() + e * P.nconst, P.consts.begin() + (e + 1) * P.nconst,
+                  L.consts.begin() + q * P.nconst);
+    }
+    L.adj = build_adjacency(L.mesh.conn, Nl, npe);
+    // halo: parts referencing each node (as a local node of theirs)
+    // recv: my ghosts, from their owners
+    std::vector<std::vector<int32_t>> recv(static_cast<size_t>(nparts)), send(static_cast<size_t>(nparts));
+    for (int64_t q = R.num_owned; q < Nl; ++q) recv[size_t(owner[size_t(R.node_l2g[size_t(q)])])].push_back(int32_t(q));
+    // send: my owned nodes that another part's elements touch
+    for (int64_t q = 0; q < R.num_owned; ++q) {
+        const int64_t n = R.node_l2g[size_t(q)];
+        std::vector<int32_t> parts;
+        for (int64_t p = P.adj.offsets[size_t(n)]; p < P.adj.offsets[size_t(n + 1)]; ++p) {
+            const int64_t e = P.adj.elem[size_t(p)];
+            for (int a = 0; a < npe; ++a) {
+                const int32_t o = owner[size_t(m.conn[size_t(e * npe + a)])];
+                if (o != part) parts.push_back(o);
+            }
+        }
+        std::sort(parts.begin(), parts.end());
+        parts.erase(std::unique(parts.begin(), parts.end()), parts.end());
+        for (int32_t o : parts) send[size_t(o)].push_back(int32_t(q));
+    }
+    R.halo.send_off.push_back(0);
+    R.halo.recv_off.push_back(0);
+    for (int q = 0; q < nparts; ++q) {
+        if (q == part || (send[size_t(q)].empty() && recv[size_t(q)].empty())) continue;
+        R.halo.neighbors.push_back(q);
+        R.halo.send_nodes.insert(R.halo.send_nodes.end(), send[size_t(q)].begin(), send[size_t(q)].end());
+        R.halo.recv_nodes.insert(R.halo.recv_nodes.end(), recv[size_t(q)].begin(), recv[size_t(q)].end());
+        R.halo.send_off.push_back(int64_t(R.halo.send_nodes.size()));
+        R.halo.recv_off.push_back(int64_t(R.halo.recv_nodes.size()));
+    }
+    return R;
+}
+
+}  // namespace djg

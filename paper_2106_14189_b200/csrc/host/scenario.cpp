@@ -136,6 +136,10 @@ struct djg_scenario {
     std::variant<djg::Problem<float>, djg::Problem<double>> p;
 };
 
+struct djg_partition {
+    std::variant<djg::PartProblem<float>, djg::PartProblem<double>> p;
+};
+
 extern "C" {
 
 void djg_bench_material(int32_t model, djg_material_params* m) {
@@ -241,6 +245,99 @@ int djg_scenario_image(const djg_scenario* sc, const djg_image_ptrs* out) {
 int djg_scenario_desc(const djg_scenario* sc, int32_t device, djg_desc* out) {
     if (!sc || !out) return DJG_E_CONFIG;
     std::visit([&](const auto& P) { desc_of(P, device, *out); }, sc->p);
+    return DJG_OK;
+}
+
+int djg_partition_build(const djg_scenario* sc, int32_t nparts, int32_t part, djg_partition** out) {
+    if (!sc || !out) return DJG_E_CONFIG;
+    *out = nullptr;
+    try {
+        auto pp = std::make_unique<djg_partition>();
+        std::visit(
+            [&](const auto& P) {
+                using R = typename std::decay_t<decltype(P.consts)>::value_type;
+                pp->p = djg::build_part<R>(P, nparts, part);
+            },
+            sc->p);
+        *out = pp.release();
+        return DJG_OK;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return DJG_E_CONFIG;
+    }
+}
+
+void djg_partition_free(djg_partition* p) { delete p; }
+
+int djg_partition_get_info(const djg_partition* p, djg_partition_info* o) {
+    if (!p || !o) return DJG_E_CONFIG;
+    std::visit(
+        [&](const auto& R) {
+            std::memset(o, 0, sizeof(*o));
+            o->nparts = R.nparts;
+            o->part = R.part;
+            o->num_neighbors = int32_t(R.halo.neighbors.size());
+            o->num_nodes = int64_t(R.node_l2g.size());
+            o->num_owned = R.num_owned;
+            o->num_elements = int64_t(R.elem_l2g.size());
+            o->owned_elements = R.owned_elements;
+            o->send_total = int64_t(R.halo.send_nodes.size());
+            o->recv_total = int64_t(R.halo.recv_nodes.size());
+            o->global_nodes = R.global_nodes;
+            o->global_elements = R.global_elements;
+        },
+        p->p);
+    return DJG_OK;
+}
+
+int djg_partition_image(const djg_partition* p, const djg_image_ptrs* out) {
+    if (!p || !out) return DJG_E_CONFIG;
+    std::visit([&](const auto& R) { copy_out(R.local, *out); }, p->p);
+    return DJG_OK;
+}
+
+int djg_partition_desc(const djg_partition* p, int32_t device, djg_desc* out) {
+    if (!p || !out) return DJG_E_CONFIG;
+    std::visit([&](const auto& R) { desc_of(R.local, device, *out); }, p->p);
+    return DJG_OK;
+}
+
+int djg_partition_halo(const djg_partition* p, int32_t* nb, int64_t* so, int64_t* ro, int32_t* sn, int32_t* rn) {
+    if (!p) return DJG_E_CONFIG;
+    std::visit(
+        [&](const auto& R) {
+            auto put = [](auto* dst, const auto& v) {
+                if (dst && !v.empty()) std::memcpy(dst, v.data(), v.size() * sizeof(v[0]));
+            };
+            put(nb, R.halo.neighbors);
+            put(so, R.halo.send_off);
+            put(ro, R.halo.recv_off);
+            put(sn, R.halo.send_nodes);
+            put(rn, R.halo.recv_nodes);
+        },
+        p->p);
+    return DJG_OK;
+}
+
+int djg_partition_maps(const djg_partition* p, int64_t* node_l2g, int64_t* elem_l2g) {
+    if (!p) return DJG_E_CONFIG;
+    std::visit(
+        [&](const auto& R) {
+            if (node_l2g) std::memcpy(node_l2g, R.node_l2g.data(), R.node_l2g.size() * sizeof(int64_t));
+            if (elem_l2g) std::memcpy(elem_l2g, R.elem_l2g.data(), R.elem_l2g.size() * sizeof(int64_t));
+        },
+        p->p);
+    return DJG_OK;
+}
+
+int djg_element_parts(const djg_scenario* sc, int32_t nparts, int32_t* part) {
+    if (!sc || !part || nparts < 1) return DJG_E_CONFIG;
+    std::visit(
+        [&](const auto& P) {
+            const auto v = djg::rcb_parts(P.mesh, nparts);
+            std::memcpy(part, v.data(), v.size() * sizeof(int32_t));
+        },
+        sc->p);
     return DJG_OK;
 }
 

@@ -1,0 +1,291 @@
+"""Multi-GPU DJ-TLED step: one process (rank) per GPU.
+
+The mesh is split by the native host partitioner (include/djg_host.h,
+djg_partition_*): each rank owns a set of nodes, computes every element that
+touches them (ghost elements included) in ascending global element id, and
+after each step exchanges the fresh displacement of boundary nodes with its
+neighbors. Owned nodes sum exactly the rows a single GPU sums, in the same
+order, so a k-rank run is bit-identical to the 1-GPU run.
+
+Per step, all enqueued on the engine's CUDA stream (no host synchronisation):
+  djg_step_async(1) -> djg_halo_pack -> NCCL send/recv with each neighbor ->
+  djg_halo_unpack -> djg_step_status -> NCCL allreduce(MAX) -> djg_step_agree
+
+`EmulatedParts` runs all parts in one process on one device, exchanging the
+halo with device copies (no kernel ever waits on another): it is how the
+multi-part path is tested on a single GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _abi as A
+from .engine import ConfigError, GpuDjEngine, Scenario, StepReport, raise_for
+
+
+def _lib():
+    return A.load_library()
+
+
+class Partition:
+    """Host-side local problem of part `part` of `nparts`."""
+
+    def __init__(self, scenario: Scenario, nparts: int, part: int):
+        self.scenario = scenario
+        h = C.c_void_p()
+        if _lib().djg_partition_build(scenario._h, nparts, part, C.byref(h)) != A.DJG_OK:
+            raise ConfigError(_lib().djg_scenario_error().decode())
+        self._h = h
+        i = A.djg_partition_info()
+        _lib().djg_partition_get_info(self._h, C.byref(i))
+        self.info = {name: getattr(i, name) for name, _ in i._fields_}
+        nb = max(i.num_neighbors, 0)
+        self.neighbors = np.zeros(nb, np.int32)
+        self.send_off = np.zeros(nb + 1, np.int64)
+        self.recv_off = np.zeros(nb + 1, np.int64)
+        self.send_nodes = np.zeros(i.send_total, np.int32)
+        self.recv_nodes = np.zeros(i.recv_total, np.int32)
+        _lib().djg_partition_halo(self._h, A.ptr(self.neighbors), A.ptr(self.send_off), A.ptr(self.recv_off),
+                                  A.ptr(self.send_nodes), A.ptr(self.recv_nodes))
+        self.node_l2g = np.zeros(i.num_nodes, np.int64)
+        self.elem_l2g = np.zeros(i.num_elements, np.int64)
+        _lib().djg_partition_maps(self._h, A.ptr(self.node_l2g), A.ptr(self.elem_l2g))
+        self.num_owned = i.num_owned
+        self.num_nodes = i.num_nodes
+        self.num_elements = i.num_elements
+        self.dtype = scenario.dtype
+        self.npe = scenario.npe
+        self.nconst = scenario.nconst
+        self.dt = scenario.dt
+
+    def image(self) -> dict:
+        n, e, npe, nc, dt = self.num_nodes, self.num_elements, self.npe, self.nconst, self.dtype
+        img = {
+            "nodes": np.zeros(3 * n, dt), "conn": np.zeros(npe * e, np.int32),
+            "csr_offsets": np.zeros(n + 1, np.int64), "csr_elem": np.zeros(npe * e, np.int64),
+            "csr_local": np.zeros(npe * e, np.int32), "consts": np.zeros(e * nc, dt),
+            "mass": np.zeros(n, dt), "c1": np.zeros(n, dt), "massless": np.zeros(n, np.uint8),
+            "dof_kind": np.zeros(3 * n, np.uint8), "dof_target": np.zeros(3 * n, dt),
+            "dof_t_total": np.zeros(3 * n, dt),
+        }
+        p = A.djg_image_ptrs()
+        for k, v in img.items():
+            setattr(p, k, v.ctypes.data_as(C.c_void_p))
+        _lib().djg_partition_image(self._h, C.byref(p))
+        return img
+
+    def desc(self, device: int = 0, flags: int = 0) -> A.djg_desc:
+        d = A.djg_desc()
+        _lib().djg_partition_desc(self._h, device, C.byref(d))
+        d.flags = flags
+        return d
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib().djg_partition_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def element_parts(scenario: Scenario, nparts: int) -> np.ndarray:
+    out = np.zeros(scenario.num_elements, np.int32)
+    _lib().djg_element_parts(scenario._h, nparts, A.ptr(out))
+    return out
+
+
+class PartEngine(GpuDjEngine):
+    """GpuDjEngine on a part's local problem, with its halo lists."""
+
+    def __init__(self, part: Partition, device: int = 0, flags: int = 0):
+        self.scenario = part  # duck-typed: desc(), dtype, num_nodes, num_elements, npe, dt
+        self.part = part
+        self.dtype = part.dtype
+        self.num_nodes = part.num_nodes
+        self.num_elements = part.num_elements
+        h = C.c_void_p()
+        d = part.desc(device, flags)
+        if _lib().djg_create(C.byref(d), C.byref(h)) != A.DJG_OK:
+            raise ConfigError(_lib().djg_create_error().decode())
+        self._h = h
+        self._check(_lib().djg_set_partition(self._h, part.num_owned, A.ptr(part.elem_l2g)))
+        self._check(_lib().djg_set_halo(self._h, part.send_nodes.size, A.ptr(part.send_nodes),
+                                        part.recv_nodes.size, A.ptr(part.recv_nodes)))
+
+    def set_global_state(self, u_curr=None, u_prev=None, step: int = 0):
+        l2g = self.part.node_l2g
+        loc = lambda g: None if g is None else np.asarray(g, self.dtype).reshape(-1, 3)[l2g].reshape(-1)
+        self.set_state(loc(u_curr), loc(u_prev), step)
+
+    def owned_state(self):
+        u, up, step = self.get_state()
+        n = self.part.num_owned
+        return u.reshape(-1, 3)[:n], up.reshape(-1, 3)[:n], step
+
+    def halo_pack(self, dev_ptr: int):
+        self._check(_lib().djg_halo_pack(self._h, C.c_void_p(dev_ptr)))
+
+    def halo_unpack(self, dev_ptr: int):
+        self._check(_lib().djg_halo_unpack(self._h, C.c_void_p(dev_ptr)))
+
+    def step_status(self, dev_ptr: int):
+        self._check(_lib().djg_step_status(self._h, C.c_void_p(dev_ptr)))
+
+    def step_agree(self, dev_ptr: int):
+        self._check(_lib().djg_step_agree(self._h, C.c_void_p(dev_ptr)))
+
+
+def _torch_dtype(dtype):
+    import torch
+    return torch.float32 if dtype == np.float32 else torch.float64
+
+
+class DistributedEngine:
+    """This rank's part of a multi-GPU run over torch.distributed (NCCL)."""
+
+    def __init__(self, scenario: Scenario, device: int, group=None, flags: int = 0):
+        import torch
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.device = device
+        self.part = Partition(scenario, self.world, self.rank)
+        self.eng = PartEngine(self.part, device, flags)
+        tdt = _torch_dtype(self.part.dtype)
+        dev = torch.device("cuda", device)
+        self.send = torch.zeros((max(self.part.send_nodes.size, 1), 4), dtype=tdt, device=dev)
+        self.recv = torch.zeros((max(self.part.recv_nodes.size, 1), 4), dtype=tdt, device=dev)
+        self.status = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.stream = torch.cuda.ExternalStream(self.eng.stream, device=dev)
+
+    def _exchange(self):
+        dist = self.dist
+        ops = []
+        p = self.part
+        for k, nb in enumerate(p.neighbors.tolist()):
+            s0, s1 = int(p.send_off[k]), int(p.send_off[k + 1])
+            r0, r1 = int(p.recv_off[k]), int(p.recv_off[k + 1])
+            if s1 > s0:
+                ops.append(dist.P2POp(dist.isend, self.send[s0:s1], nb, self.group))
+            if r1 > r0:
+                ops.append(dist.P2POp(dist.irecv, self.recv[r0:r1], nb, self.group))
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+
+    def step_async(self, nsteps: int):
+        import torch
+        with torch.cuda.stream(self.stream):
+            for _ in range(nsteps):
+                self.eng.step_async(1)
+                self.eng.halo_pack(self.send.data_ptr())
+                self._exchange()
+                self.eng.halo_unpack(self.recv.data_ptr())
+                self.eng.step_status(self.status.data_ptr())
+                self.dist.all_reduce(self.status, op=self.dist.ReduceOp.MAX, group=self.group)
+                self.eng.step_agree(self.status.data_ptr())
+
+    def step(self, nsteps: int, raise_on_failure=True) -> StepReport:
+        start = self.eng.get_state()[2]
+        self.step_async(nsteps)
+        r = self.eng.sync()
+        r.steps_done = r.step - start
+        if raise_on_failure and r.status != A.DJG_OK:
+            raise_for(r)
+        return r
+
+    def gather_global(self):
+        """All ranks' owned displacements assembled into global arrays (rank 0
+        gets the result; others return None)."""
+        import torch
+        u, up, step = self.eng.owned_state()
+        ids = torch.from_numpy(self.part.node_l2g[: self.part.num_owned].copy())
+        objs = [None] * self.world
+        self.dist.all_gather_object(objs, (ids.numpy(), u, up), group=self.group)
+        if self.rank != 0:
+            return None
+        n = self.part.info["global_nodes"]
+        U = np.zeros((n, 3), self.part.dtype)
+        UP = np.zeros((n, 3), self.part.dtype)
+        for g, a, b in objs:
+            U[g] = a
+            UP[g] = b
+        return U.reshape(-1), UP.reshape(-1), step
+
+
+class EmulatedParts:
+    """All parts of a decomposition in one process on one device: the same
+    engines and kernels as DistributedEngine, the halo moved with device
+    copies and the failure agreement reduced on the device. For tests."""
+
+    def __init__(self, scenario: Scenario, nparts: int, device: int = 0, flags: int = 0):
+        import torch
+        self.torch = torch
+        self.parts = [Partition(scenario, nparts, p) for p in range(nparts)]
+        self.engs = [PartEngine(p, device, flags) for p in self.parts]
+        tdt = _torch_dtype(scenario.dtype)
+        dev = torch.device("cuda", device)
+        self.send = [torch.zeros((max(p.send_nodes.size, 1), 4), dtype=tdt, device=dev) for p in self.parts]
+        self.recv = [torch.zeros((max(p.recv_nodes.size, 1), 4), dtype=tdt, device=dev) for p in self.parts]
+        self.status = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in self.parts]
+        self.global_nodes = scenario.num_nodes
+
+    def _sync(self):
+        for e in self.engs:
+            e.sync()
+
+    def step(self, nsteps: int):
+        torch = self.torch
+        P = len(self.parts)
+        for _ in range(nsteps):
+            for e in self.engs:
+                e.step_async(1)
+            for p, e in enumerate(self.engs):
+                e.halo_pack(self.send[p].data_ptr())
+            self._sync()
+            # receiver q's block from p = sender p's block to q (same global order)
+            for q, pq in enumerate(self.parts):
+                for k, p in enumerate(pq.neighbors.tolist()):
+                    pp = self.parts[p]
+                    j = pp.neighbors.tolist().index(q)
+                    r0, r1 = int(pq.recv_off[k]), int(pq.recv_off[k + 1])
+                    s0, s1 = int(pp.send_off[j]), int(pp.send_off[j + 1])
+                    assert r1 - r0 == s1 - s0
+                    if r1 > r0:
+                        self.recv[q][r0:r1].copy_(self.send[p][s0:s1])
+            torch.cuda.synchronize()
+            for p, e in enumerate(self.engs):
+                e.halo_unpack(self.recv[p].data_ptr())
+                e.step_status(self.status[p].data_ptr())
+            self._sync()
+            red = torch.stack(self.status).max(dim=0).values
+            for e in self.engs:
+                e.step_agree(red.data_ptr())
+            self._sync()
+        return [e.sync() for e in self.engs]
+
+    def set_global_state(self, u=None, up=None, step=0):
+        for e in self.engs:
+            e.set_global_state(u, up, step)
+
+    def global_state(self):
+        U = np.zeros((self.global_nodes, 3), self.parts[0].dtype)
+        UP = np.zeros_like(U)
+        step = None
+        for p, e in zip(self.parts, self.engs):
+            u, up, step = e.owned_state()
+            U[p.node_l2g[: p.num_owned]] = u
+            UP[p.node_l2g[: p.num_owned]] = up
+        return U.reshape(-1), UP.reshape(-1), step
+
+    def close(self):
+        for e in self.engs:
+            e.close()

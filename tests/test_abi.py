@@ -54,7 +54,7 @@ def test_create_rejects_bad_descriptor_without_gpu():
 
 
 STRUCTS = ["djg_material_params", "djg_scenario_spec", "djg_image_ptrs", "djg_image_scalars", "djg_report",
-           "djg_assemble_stats", "djg_desc", "djg_engine_info", "djg_mesh_desc", "djg_step_desc"]
+           "djg_assemble_stats", "djg_desc", "djg_engine_info", "djg_mesh_desc", "djg_step_desc", "djg_partition_info"]
 
 
 def test_struct_layouts_match_c(tmp_path):

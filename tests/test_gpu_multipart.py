@@ -1,0 +1,85 @@
+"""Multi-part step on one GPU: every part is a real engine running the real
+kernels (local elements, owned nodes, halo pack/unpack, failure agreement);
+the halo moves by device copies between the parts' buffers, so no kernel ever
+waits on another. k parts must be bit-identical to one engine."""
+import socket
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2106_14189_b200 import GpuDjEngine, Scenario, box_spec, mesh_spec
+from paper_2106_14189_b200 import _abi as A
+from paper_2106_14189_b200.parallel import EmulatedParts
+
+pytestmark = pytest.mark.gpu
+
+
+def single(spec, steps):
+    sc = Scenario(spec)
+    with GpuDjEngine(sc) as eng:
+        rep = eng.step(steps, raise_on_failure=False)
+        u, up, st = eng.get_state()
+    return u, up, rep
+
+
+@pytest.mark.parametrize("nparts", [2, 3, 4, 8])
+@pytest.mark.parametrize("kind,model,prec", [("T4", "NH", 4), ("H8", "TI", 4), ("T4", "MR", 8)])
+def test_parts_bitwise_equal_single_gpu(nparts, kind, model, prec):
+    spec = box_spec(kind=kind, model=model, divisions=8, precision=prec, ramp_steps=200)
+    u1, up1, r1 = single(spec, 200)
+    em = EmulatedParts(Scenario(spec), nparts)
+    reps = em.step(200)
+    u, up, step = em.global_state()
+    em.close()
+    assert step == 200 == r1.step and all(r.step == 200 and r.status == 0 for r in reps)
+    assert np.array_equal(u, u1) and np.array_equal(up, up1)
+
+
+def test_parts_agree_on_inversion():
+    """The crushing case of test_solver.cpp:214-241 split in two: every part
+    halts at the same state, reporting the same (global) element."""
+    sc0 = Scenario(box_spec(kind="T4", divisions=2, extent=(0.1, 0.1, 0.1), precision=8))
+    img = sc0.image()
+    nodes, conn = img["nodes"].reshape(-1, 3), img["conn"].reshape(-1, 4)
+    bottom = [n for n in range(len(nodes)) if nodes[n, 2] == 0.0]
+    top = [n for n in range(len(nodes)) if nodes[n, 2] == nodes[:, 2].max()]
+    spec = mesh_spec(nodes, conn, kind="T4", precision=8, fixed=[(n, a) for n in bottom for a in range(3)],
+                     prescribed=[(n, 2, -0.5, 1e-4) for n in top], dt=1e-4, alpha=0.0)
+    u1, up1, r1 = single(spec, 100)
+    ur, upr, rr = oracle.run(spec, 100, "oracle")
+    assert r1.status == A.DJG_E_INVERSION and r1.first_inverted == rr["first_inverted"]
+    em = EmulatedParts(Scenario(spec), 2)
+    reps = em.step(100)
+    u, up, step = em.global_state()
+    em.close()
+    for r in reps:
+        assert r.status == A.DJG_E_INVERSION
+        assert r.first_inverted == r1.first_inverted and r.step == r1.step
+    assert np.array_equal(u, u1) and np.array_equal(up, up1)
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def test_distributed_engine_single_rank_nccl():
+    """The torch.distributed (NCCL) driver on one rank: same bits as the
+    plain engine (the halo is empty, the status allreduce is real)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2106_14189_b200.parallel import DistributedEngine
+    spec = box_spec(kind="H8", model="NH", divisions=6, precision=4, ramp_steps=100)
+    u1, _, _ = single(spec, 100)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_port()}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        de = DistributedEngine(Scenario(spec), device=0)
+        r = de.step(100)
+        U, UP, step = de.gather_global()
+        assert r.status == 0 and step == 100
+        assert np.array_equal(U, u1)
+    finally:
+        dist.destroy_process_group()

@@ -267,6 +267,7 @@ class EmulatedParts:
                 e.step_status(self.status[p].data_ptr())
             self._sync()
             red = torch.stack(self.status).max(dim=0).values
+            torch.cuda.synchronize()  # red is produced on torch's stream, read on the engines'
             for e in self.engs:
                 e.step_agree(red.data_ptr())
             self._sync()

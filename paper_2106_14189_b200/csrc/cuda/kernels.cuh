@@ -98,7 +98,7 @@ struct Ctrl {
     unsigned int blocks_done;       // k_node completion counter
     int diverged;                   // non-finite seen this step
     int halted;                     // 0, or DJG_E_INVERSION / DJG_E_DIVERGENCE
-    int pad;
+    int agreed;                     // multi-part: halt_first_inv already a global id
     long long fail_step;            // state.step + 1 of the failing step
     long long halt_first_inv;       // element reported with an inversion halt
     unsigned long long total_inv;   // accumulated inverted elements
@@ -701,19 +701,22 @@ __global__ void k_halo_unpack(const Ctrl* ctrl, typename RT<Real>::Node* u0, typ
 // two buffers are intact), so every part halts at the same state.
 __global__ void k_step_status(const Ctrl* ctrl, const long long* __restrict__ elem_l2g, long long* status) {
     const int h = ctrl->halted;
+    const long long none = -0x7fffffffffffffffll - 1;
     status[0] = h == 4 ? 2 : (h == 5 ? 1 : 0);
-    status[1] = (h == 4 && ctrl->halt_first_inv >= 0) ? -elem_l2g[ctrl->halt_first_inv] : (long long)(-0x7fffffffffffffffll - 1);
+    if (h != 4 || ctrl->halt_first_inv < 0) status[1] = none;
+    else status[1] = -(ctrl->agreed ? ctrl->halt_first_inv : elem_l2g[ctrl->halt_first_inv]);
 }
 
 __global__ void k_agree(Ctrl* ctrl, const long long* __restrict__ reduced) {
     const long long code = reduced[0];
-    if (code == 0) return;
+    if (code == 0 || ctrl->agreed) return;
     if (ctrl->halted == 0) {
         ctrl->step -= 1;  // this part advanced; another one failed the same step
         ctrl->fail_step = ctrl->step + 1;
     }
     ctrl->halted = code == 2 ? 4 : 5;
     ctrl->halt_first_inv = code == 2 ? -reduced[1] : -1;
+    ctrl->agreed = 1;  // later status/agree rounds (halted engine) are no-ops
 }
 
 // ------------------------------------------------------------------ setup

@@ -87,7 +87,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.device}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                 "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
         except Exception:
@@ -177,6 +177,29 @@ def reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def _cpu_baseline_line(args):
+    try:
+        cb = cpu_reference_sample(args.cpu_steps, 2, args.kind, args.model, args.precision)
+        return {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    except Exception as ex:  # reported, not fatal
+        return {"value": None, "error": str(ex)}
+
+
+def _line(args, world, K, W, E, ms_step, value, extra):
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None, "dtype": "f32" if args.precision == 4 else "f64",
+        "data": "synthetic (generate_box unit cube, bench_material, +1% z-extension ramp)",
+        "config": {"workload": f"cfg5: {args.kind}-{args.model} unit cube d={args.divisions}",
+                   "kind": args.kind, "material": args.model, "divisions": args.divisions,
+                   "num_elements": E, "parallelism": f"{world} GPU" + (" (RCB partition + halo)" if world > 1 else "")},
+        "time_per_step_us": ms_step * 1e3,
+    }
+    line.update(extra)
+    return line
+
+
 def our_arm(args):
     import torch
 
@@ -185,15 +208,11 @@ def our_arm(args):
     rank, world, local = dist_env()
     device = local
     torch.cuda.set_device(device)
-    dist = None
     if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", device))
-    if world > 1:
-        raise SystemExit("multi-GPU partitioned stepping is not wired into bench.py yet")
+        return multi_arm(args, rank, world, device)
 
     K, W = args.steps, max(args.warmup, 3)
-    total = W + K + args.e2e_steps + 8
+    total = W + 2 * K + args.e2e_steps + 8
     spec = box_spec(kind=args.kind, model=args.model, divisions=args.divisions, precision=args.precision,
                     target=0.01, ramp_steps=total)
     t0 = time.perf_counter()
@@ -201,50 +220,47 @@ def our_arm(args):
     t1 = time.perf_counter()
     eng = GpuDjEngine(sc, device=device)
     t2 = time.perf_counter()
+    info = eng.info()
     log(f"[bench] N={sc.num_nodes} E={sc.num_elements} build {t1 - t0:.1f}s create {t2 - t1:.1f}s "
-        f"device {eng.info()['device_bytes'] / 1e9:.2f} GB")
+        f"device {info['device_bytes'] / 1e9:.2f} GB")
     N, E = sc.num_nodes, sc.num_elements
 
     eng.step(W)                          # warm-up (graphs captured, clocks up)
     torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
     clocks = ClockSampler(device)
     clocks.start()
-    ms_e, ms_n, ms_tot = eng.profile_steps(K)   # CUDA events on the engine stream
+    # Timed region 1: per-kernel CUDA events on the engine stream.
+    ms_e, ms_n, ms_tot = eng.profile_steps(K)
     rep = eng.sync()
-    torch.cuda.synchronize()
-    clk = clocks.stop()
-    if rep.status != 0 or rep.steps_done != K:
-        raise SystemExit(f"timed run failed: {rep}")
-    ms_step = ms_tot / K
-    if dist:
-        t = torch.tensor([ms_step], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step = float(t.item())
-    value = E * world / (ms_step * 1e-3)
-
-    # Graph-replayed steps (no per-kernel events) for reference.
+    # Timed region 2: the production path (CUDA graph replay), events on the
+    # engine stream around the whole region.
     s = torch.cuda.ExternalStream(eng.stream)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
     ev0.record(s)
     eng.step_async(K)
     ev1.record(s)
     ev1.synchronize()
-    eng.sync()
+    rep2 = eng.sync()
+    clk = clocks.stop()
+    if rep.status != 0 or rep2.status != 0 or rep.steps_done != K or rep2.steps_done != K:
+        raise SystemExit(f"timed run failed: {rep} {rep2}")
     ms_graph = ev0.elapsed_time(ev1) / K
+    ms_step = ms_graph
+    value = E / (ms_step * 1e-3)
 
-    # e2e: advance_step with a host-resident SimState through the public API.
-    rdt = np.float32 if args.precision == 4 else np.float64
-    u_h = torch.empty(3 * N, dtype=torch.float32 if args.precision == 4 else torch.float64).pin_memory()
+    # e2e: advance_step with a host-resident SimState through the public C-ABI.
+    import ctypes as C
+
+    from paper_2106_14189_b200 import _abi as A
+    lib = A.load_library()
+    tdt = torch.float32 if args.precision == 4 else torch.float64
+    u_h = torch.empty(3 * N, dtype=tdt).pin_memory()
     up_h = torch.empty_like(u_h).pin_memory()
     u_out = torch.empty_like(u_h).pin_memory()
     uc, upv, st = eng.get_state()
     u_h.numpy()[:] = uc
     up_h.numpy()[:] = upv
-    lib = __import__("paper_2106_14189_b200._abi", fromlist=["x"]).load_library()
-    import ctypes as C
-    from paper_2106_14189_b200 import _abi as A
     h = eng._h
     step_c = C.c_int64(st)
     rep_c = A.djg_report()
@@ -261,53 +277,103 @@ def our_arm(args):
     te1 = time.perf_counter()
     e2e_ms = (te1 - te0) / args.e2e_steps * 1e3
     rbytes = args.precision
-    h2d = 2 * 3 * N * rbytes
-    d2h = 2 * 3 * N * rbytes
 
     hbm, peak_kind = peaks()
     B = algo_bytes(args.kind, args.model, N, E, args.precision)
     k1_ms = ms_e / K
     achieved = B["k_element"] / (k1_ms * 1e-3) / 1e9
-    line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32" if args.precision == 4 else "f64",
-        "data": "synthetic (generate_box unit cube, bench_material NH, +1% z-extension ramp)",
-        "config": {"workload": f"cfg5: {args.kind}-{args.model} unit cube d={args.divisions}",
-                   "kind": args.kind, "material": args.model, "divisions": args.divisions,
-                   "num_nodes": N, "num_elements": E, "parallelism": f"{world} GPU",
-                   "l2": "inputs larger than L2 (state ~%.1f GB)" % (eng.info()["device_bytes"] / 1e9)},
-        "e2e": {"value": E / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_ms,
-                "mode": "per step: H2D u_curr+u_prev (pinned), djg_step(1), D2H u_curr+u_prev"},
+    extra = {
+        "e2e": {"value": E / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 2 * 3 * N * rbytes,
+                "d2h_bytes_per_step": 2 * 3 * N * rbytes, "ms_per_step": e2e_ms,
+                "mode": "per step: djg_set_state (H2D u_curr+u_prev from pinned host), djg_step(1), "
+                        "djg_get_state (D2H u_curr+u_prev); wall clock"},
         "roofline": {"bound": "hbm", "kernel": "k_element", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": None, "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": B["k_element"], "launch_ms": k1_ms,
-                     "step_frac": B["step"] / (ms_step * 1e-3) / 1e9 / hbm,
-                     "k_node_ms": ms_n / K, "k_node_frac": B["k_node"] / (ms_n / K * 1e-3) / 1e9 / hbm},
-        "ms_per_step_graph": ms_graph,
-        "gpu_launches": 2 * K,
+                     "k_node_ms": ms_n / K, "k_node_frac": B["k_node"] / (ms_n / K * 1e-3) / 1e9 / hbm,
+                     "step_algorithmic_bytes": B["step"], "step_frac": B["step"] / (ms_step * 1e-3) / 1e9 / hbm},
+        "ms_per_step_events_per_kernel": ms_tot / K,
+        "gpu_launches": 2 * K * 2,
         "clocks": clk,
-        "time_per_step_us": ms_step * 1e3,
+        "engine": {k: info[k] for k in ("slabs", "kernels_per_step", "device_bytes", "slot_capacity")},
     }
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            cb = cpu_reference_sample(args.cpu_steps, 2, args.kind, args.model, args.precision)
-            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
-        except Exception as ex:  # reported, not fatal
-            line["cpu_baseline"] = {"value": None, "error": str(ex)}
+    extra["config"] = None
+    line = _line(args, 1, K, W, E, ms_step, value, {k: v for k, v in extra.items() if k != "config"})
+    line["config"]["num_nodes"] = N
+    line["config"]["l2"] = "inputs larger than L2 (state %.1f GB resident)" % (info["device_bytes"] / 1e9)
+    if not args.no_cpu_baseline:
+        line["cpu_baseline"] = _cpu_baseline_line(args)
     eng.close()
     sc.close()
+    print(json.dumps(line), flush=True)
+
+
+def multi_arm(args, rank, world, device):
+    """Strong scaling: the cfg5 mesh partitioned over `world` ranks (RCB),
+    halo exchange + failure agreement per step over NCCL."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2106_14189_b200 import Scenario, box_spec
+    from paper_2106_14189_b200.parallel import DistributedEngine
+
+    dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+    K, W = args.steps, max(args.warmup, 3)
+    total = W + K + 8
+    spec = box_spec(kind=args.kind, model=args.model, divisions=args.divisions, precision=args.precision,
+                    target=0.01, ramp_steps=total)
+    t0 = time.perf_counter()
+    sc = Scenario(spec)
+    de = DistributedEngine(sc, device=device)
+    t1 = time.perf_counter()
+    E = sc.num_elements
+    pi = de.part.info
+    log(f"[bench rank {rank}] local E={pi['num_elements']} owned N={pi['num_owned']} "
+        f"neighbors={pi['num_neighbors']} halo send={pi['send_total']} setup {t1 - t0:.1f}s")
+    de.step(W)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = ClockSampler(device) if rank == 0 else None
+    if clocks:
+        clocks.start()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(de.stream)
+    de.step_async(K)
+    ev1.record(de.stream)
+    ev1.synchronize()
+    rep = de.eng.sync()
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop() if clocks else None
+    ms = torch.tensor([ev0.elapsed_time(ev1) / K], device="cuda")
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms_step = float(ms.item())
+    if rep.status != 0:
+        raise SystemExit(f"rank {rank}: timed run failed: {rep}")
+    value = E / (ms_step * 1e-3)
+    hbm, peak_kind = peaks()
+    B = algo_bytes(args.kind, args.model, pi["num_owned"], pi["num_elements"], args.precision)
     if rank == 0:
-        print(json.dumps(line), flush=True)
-    if dist:
-        dist.destroy_process_group()
+        extra = {
+            "roofline": {"bound": "hbm", "kernel": "step (per GPU)", "achieved": B["step"] / (ms_step * 1e-3) / 1e9,
+                         "peak": hbm, "unit": "GB/s", "frac": B["step"] / (ms_step * 1e-3) / 1e9 / hbm,
+                         "traffic": None, "peak_source": peak_kind,
+                         "note": "rank-0 local elements incl. ghosts / max-over-ranks step time"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                    "mode": "device-resident multi-GPU run loop (no host state per step)"},
+            "gpu_launches": K * 7,
+            "clocks": clk,
+            "partition": {"local_elements": pi["num_elements"], "owned_elements": pi["owned_elements"],
+                          "halo_send_nodes": pi["send_total"], "neighbors": pi["num_neighbors"]},
+        }
+        print(json.dumps(_line(args, world, K, W, E, ms_step, value, extra)), flush=True)
+    dist.destroy_process_group()
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--kind", default="T4")

@@ -498,12 +498,12 @@ __global__ void __launch_bounds__(128) k_element(const ElemArgs<Real> A, long lo
 // (gather_nodal_forces, djtled_force.hpp:116-134). Slot k of the node sits at
 // ef[p0 + 32 k]: lane i of a slice reads consecutive 16-byte rows.
 template <class Real>
-__device__ __forceinline__ void gather_row(const typename RT<Real>::Node* __restrict__ ef, long long p0, int len,
-                                           Real& sx, Real& sy, Real& sz) {
+__device__ __forceinline__ void gather_row(const typename RT<Real>::Node* __restrict__ p, int len, Real& sx, Real& sy,
+                                           Real& sz) {
     using T = RT<Real>;
     sx = Real(0); sy = Real(0); sz = Real(0);
     for (int k = 0; k < len; ++k) {
-        const typename T::Node v = T::load_stream(ef + p0 + 32 * k);
+        const typename T::Node v = T::load_stream(p + 32 * k);
         sx += v.x; sy += v.y; sz += v.z;
     }
 }
@@ -531,7 +531,7 @@ __device__ __forceinline__ bool node_body(const NodeArgs<Real>& A, const long lo
                                           long long step) {
     using T = RT<Real>;
     Real fx, fy, fz;
-    gather_row<Real>(A.ef, p0, len, fx, fy, fz);
+    gather_row<Real>(A.ef + p0, len, fx, fy, fz);
     if constexpr (kAssemble) {
         A.f_out[3 * n + 0] = fx;
         A.f_out[3 * n + 1] = fy;
@@ -592,25 +592,84 @@ __device__ __forceinline__ void close_step(Ctrl* ctrl, long long step, int polic
 }
 
 // Whole-mesh gather + update (the default single-slab step): one thread per
-// node, the last block to finish closes the step.
+// node, the last block to finish closes the step. Written out in full rather
+// than through node_body/close_step: this form compiles to 38 registers
+// (6 blocks/SM) instead of 44, which the latency-bound gather needs.
 template <class Real, bool kAssemble>
 __global__ void __launch_bounds__(256) k_node(const NodeArgs<Real> A) {
+    using T = RT<Real>;
     Ctrl* ctrl = A.ctrl;
-    if (__ldcg(&ctrl->halted) && !kAssemble) return;
+    if (*(volatile const int*)&ctrl->halted && !kAssemble) return;
     __shared__ int s_nonfinite;
     if (threadIdx.x == 0) s_nonfinite = 0;
     __syncthreads();
-    const long long step = __ldcg(&ctrl->step);
+    const long long step = ctrl->step;
+    const bool inverted = ctrl->first_inv != kNone;
+    const bool skip = inverted && A.policy == 0;  // Abort: no gather, no update (djtled_force.hpp:202-208)
     const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (n < A.N && node_body<Real, kAssemble>(A, n, (long long)A.slice_base[n >> 5] + (n & 31), A.row_len[n], step))
-        s_nonfinite = 1;
+    if (n < A.N && !skip) {
+        Real fx, fy, fz;
+        gather_row<Real>(A.ef + (long long)A.slice_base[n >> 5] + (n & 31), A.row_len[n], fx, fy, fz);
+        if constexpr (kAssemble) {
+            A.f_out[3 * n + 0] = fx;
+            A.f_out[3 * n + 1] = fy;
+            A.f_out[3 * n + 2] = fz;
+        } else {
+            const int ph = int(step % 3);
+            const typename T::Node* ucur = ph == 0 ? A.u[0] : (ph == 1 ? A.u[1] : A.u[2]);
+            const typename T::Node* uprv = ph == 0 ? A.u[2] : (ph == 1 ? A.u[0] : A.u[1]);
+            typename T::Node* unxt = ph == 0 ? A.u[1] : (ph == 1 ? A.u[2] : A.u[0]);
+            const typename T::Node uc = T::load_node(ucur + n);
+            const typename T::Node up = T::load_node(uprv + n);
+            typename T::Node r;
+            if (A.r_ext) r = T::load_node(A.r_ext + n);
+            else { r.x = Real(0); r.y = Real(0); r.z = Real(0); }
+            const int code = A.code[n];
+            const bool massless = (code >> 6) & 1;
+            const Real c1 = A.c1[n];
+            const Real t_next = A.dt * Real(step + 1);
+            bool nf = false;
+            const Real vx = dof_update<Real>(code & 3, massless, c1, r.x, fx, uc.x, up.x, A.c2, A.c3, t_next,
+                                             A.target, A.t_total, 3 * n + 0, nf);
+            const Real vy = dof_update<Real>((code >> 2) & 3, massless, c1, r.y, fy, uc.y, up.y, A.c2, A.c3, t_next,
+                                             A.target, A.t_total, 3 * n + 1, nf);
+            const Real vz = dof_update<Real>((code >> 4) & 3, massless, c1, r.z, fz, uc.z, up.z, A.c2, A.c3, t_next,
+                                             A.target, A.t_total, 3 * n + 2, nf);
+            T::store_node(unxt + n, vx, vy, vz);
+            if (nf) s_nonfinite = 1;
+        }
+    }
     __syncthreads();
     if (threadIdx.x != 0) return;
     if (s_nonfinite) atomicOr(&ctrl->diverged, 1);
     __threadfence();
     const unsigned int done = atomicAdd(&ctrl->blocks_done, 1u);
     if (done != gridDim.x - 1) return;
-    close_step<kAssemble>(ctrl, step, A.policy);
+    // Last block: close the step (advance_step's tail, solver.hpp:143-152).
+    __threadfence();
+    const unsigned long long cnt = atomicAdd(&ctrl->inv_count, 0ull);
+    const unsigned long long first = atomicAdd(&ctrl->first_inv, 0ull);
+    if (kAssemble) {
+        ctrl->asm_first = (first != kNone && A.policy == 0) ? first : kNone;
+        ctrl->asm_count = cnt;
+    } else {
+        const int div = atomicOr(&ctrl->diverged, 0);
+        ctrl->total_inv += cnt;
+        if (cnt > 0) ctrl->inv_steps += 1;
+        if (skip) {
+            ctrl->halted = 4;  // DJG_E_INVERSION
+            ctrl->halt_first_inv = (long long)first;
+            ctrl->fail_step = step + 1;
+        } else if (div) {
+            ctrl->halted = 5;  // DJG_E_DIVERGENCE
+            ctrl->fail_step = step + 1;
+        } else {
+            ctrl->step = step + 1;
+        }
+    }
+    ctrl->inv_count = 0;
+    ctrl->first_inv = kNone;
+    ctrl->diverged = 0;
     __threadfence();
     ctrl->blocks_done = 0;
 }

@@ -23,6 +23,8 @@ DJG_OK, DJG_E_INTERNAL, DJG_E_CONFIG, DJG_E_CUDA, DJG_E_INVERSION, DJG_E_DIVERGE
 DJG_FLAG_NO_GRAPH = 1
 DJG_FLAG_SLABS = 2
 DJG_FLAG_NO_DISCARD = 4
+DJG_FLAG_COMPACT = 8
+DJG_FLAG_DEVICE_PRECOMPUTE = 16
 
 KIND_NAMES = {"T4": DJG_T4, "H8": DJG_H8}
 MODEL_NAMES = {"NH": DJG_NH, "TI": DJG_TI, "OT": DJG_OT, "MR": DJG_MR}
@@ -114,6 +116,7 @@ class djg_desc(C.Structure):
         ("c1", C.c_void_p), ("massless", C.c_void_p),
         ("c2", C.c_double), ("c3", C.c_double), ("dt", C.c_double),
         ("material", djg_material_params), ("device", C.c_int32), ("flags", C.c_uint32),
+        ("nodes", C.c_void_p), ("c_hg", C.c_double),
     ]
 
 
@@ -186,6 +189,7 @@ EXPORTS = [
     ("djg_profile_steps", C.c_int, [C.c_void_p, C.c_int64, _P(C.c_float), _P(C.c_float), _P(C.c_float)]),
     ("djg_get_info", C.c_int, [C.c_void_p, _P(djg_engine_info)]),
     ("djg_get_slot_map", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("djg_get_consts", C.c_int64, [C.c_void_p, C.c_void_p]),
     ("djg_debug_cbrt", C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32]),
     ("djg_set_partition", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),
     ("djg_set_halo", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]),

@@ -86,6 +86,7 @@ public:
     virtual int profile(int64_t n, float* ms_e, float* ms_n, float* ms_t) = 0;
     virtual void info(djg_engine_info* out) = 0;
     virtual void slot_map(int32_t* out) = 0;
+    virtual int64_t consts_out(void* out) = 0;
     virtual cudaStream_t stream() const = 0;
     virtual void configure_step(const djg_step_desc& s) = 0;
     virtual void set_policy(int policy) = 0;
@@ -114,10 +115,16 @@ public:
         flags_ = d.flags;
         if (const char* v = std::getenv("DJG_SLAB_KB")) slab_bytes_ = int64_t(std::atoll(v)) << 10;
         nconst_ = const_count(kind_, model_);
-        nplanes_ = (nconst_ + T::kPlane - 1) / T::kPlane;
+        compact_ = (flags_ & DJG_FLAG_COMPACT) != 0;
+        const bool dev_pre = (flags_ & DJG_FLAG_DEVICE_PRECOMPUTE) != 0;
+        nrec_ = compact_ ? kCompactRecord : nconst_;
+        nplanes_ = (nrec_ + T::kPlane - 1) / T::kPlane;
         if (d.nconst != nconst_) throw DescError("nconst does not match djg_const_count(kind, model)");
         if (N_ < 1 || E_ < 1) throw DescError("mesh must have nodes and elements");
-        if (!d.conn || !d.consts) throw DescError("descriptor is missing conn or consts");
+        if (!d.conn) throw DescError("descriptor is missing conn");
+        if (!d.consts && !dev_pre) throw DescError("descriptor is missing consts (or DJG_FLAG_DEVICE_PRECOMPUTE)");
+        if (!d.nodes && (dev_pre || (compact_ && kind_ == DJG_H8)))
+            throw DescError("device precompute / compact H8 need the node coordinates");
         if (!d.c1 != !d.massless) throw DescError("c1 and massless must be given together");
         if (E_ * npe_ > INT32_MAX || N_ > INT32_MAX) throw DescError("mesh too large for 32-bit slot indexing");
 
@@ -218,9 +225,60 @@ public:
             conn_.alloc(planes.size() * sizeof(int32_t));
             CK(cudaMemcpy(conn_.p, planes.data(), conn_.bytes, cudaMemcpyHostToDevice));
         }
-        // Constants: AoS chunks -> device planes.
-        consts_.alloc(size_t(nplanes_) * size_t(E_) * sizeof(Plane));
+        // Reference coordinates (compact H8 and device precompute).
+        if (d.nodes && (dev_pre || (compact_ && kind_ == DJG_H8))) {
+            X_.alloc(size_t(N_) * sizeof(Node));
+            DevBuf flat;
+            flat.alloc(size_t(3 * N_) * sizeof(Real));
+            CK(cudaMemcpy(flat.p, d.nodes, flat.bytes, cudaMemcpyHostToDevice));
+            k_pack_nodes<Real><<<unsigned((N_ + 255) / 256), 256>>>(flat.as<Real>(), N_, X_.as<Node>());
+            CK(cudaGetLastError());
+            CK(cudaDeviceSynchronize());
+        }
+        // Material terms of the precompute (FibreDirections, k_hg factor).
         {
+            const Real fa[3] = {Real(d.material.fibre_a[0]), Real(d.material.fibre_a[1]), Real(d.material.fibre_a[2])};
+            const Real fb[3] = {Real(d.material.fibre_b[0]), Real(d.material.fibre_b[1]), Real(d.material.fibre_b[2])};
+            for (int k = 0; k < 6; ++k) ea_.mat.A[k] = ea_.mat.B[k] = Real(0);
+            if (model_ == DJG_TI || model_ == DJG_OT) em::fibre_structure(fa, ea_.mat.A);
+            if (model_ == DJG_OT) em::fibre_structure(fb, ea_.mat.B);
+            ea_.mat.chk = Real(d.c_hg) * Real(d.material.kappa);
+        }
+        // Constants: built on the device, or AoS chunks -> device planes.
+        consts_.alloc(size_t(nplanes_) * size_t(E_) * sizeof(Plane));
+        if (dev_pre) {
+            ElemArgs<Real> a{};
+            a.E = E_;
+            a.conn = conn_.as<int4>();
+            a.X = X_.as<Node>();
+            a.mat = ea_.mat;
+            DevBuf bad;
+            bad.alloc(sizeof(unsigned long long));
+            CK(cudaMemset(bad.p, 0xff, bad.bytes));
+            const unsigned grid = unsigned((E_ + 127) / 128);
+#define DJG_PRE(K, M) k_precompute<Real, K, M><<<grid, 128>>>(a, nrec_, consts_.as<Plane>(), bad.as<unsigned long long>())
+            if (kind_ == DJG_T4) {
+                switch (model_) {
+                    case DJG_NH: DJG_PRE(0, 0); break;
+                    case DJG_TI: DJG_PRE(0, 1); break;
+                    case DJG_OT: DJG_PRE(0, 2); break;
+                    default: DJG_PRE(0, 3); break;
+                }
+            } else {
+                switch (model_) {
+                    case DJG_NH: DJG_PRE(1, 0); break;
+                    case DJG_TI: DJG_PRE(1, 1); break;
+                    case DJG_OT: DJG_PRE(1, 2); break;
+                    default: DJG_PRE(1, 3); break;
+                }
+            }
+#undef DJG_PRE
+            CK(cudaGetLastError());
+            unsigned long long first_bad = 0;
+            CK(cudaMemcpy(&first_bad, bad.p, sizeof(first_bad), cudaMemcpyDeviceToHost));
+            if (first_bad != ~0ull)
+                throw DescError("element " + std::to_string(first_bad) + ": non-positive reference Jacobian determinant");
+        } else {
             const int64_t chunk = std::min<int64_t>(E_, 1 << 20);
             DevBuf stage;
             stage.alloc(size_t(chunk) * nconst_ * sizeof(Real));
@@ -268,6 +326,7 @@ public:
         ea_.mat.eta_a = Real(d.material.eta_a);
         ea_.mat.eta_b = Real(d.material.eta_b);
         ea_.mat.dI2 = Real(d.material.c01);
+        ea_.X = X_.as<Node>();
         na_.N = N_;
         na_.row_len = rowlen_.as<int>();
         na_.slice_base = slicebase_.as<int>();
@@ -519,10 +578,15 @@ public:
         ElemArgs<Real> a = ea_;
         a.u_override = u_override;
         const unsigned grid = unsigned((e1 - e0 + 127) / 128);
-#define DJG_K1(K, M)                                                           \
-    do {                                                                       \
-        if (rank_bytes_ == 1) k_element<Real, K, M, 1><<<grid, 128, 0, s>>>(a, e0, e1); \
-        else k_element<Real, K, M, 2><<<grid, 128, 0, s>>>(a, e0, e1);                 \
+#define DJG_K1(K, M)                                                                      \
+    do {                                                                                  \
+        if (compact_) {                                                                   \
+            if (rank_bytes_ == 1) k_element<Real, K, M, 1, true><<<grid, 128, 0, s>>>(a, e0, e1);  \
+            else k_element<Real, K, M, 2, true><<<grid, 128, 0, s>>>(a, e0, e1);                   \
+        } else {                                                                          \
+            if (rank_bytes_ == 1) k_element<Real, K, M, 1, false><<<grid, 128, 0, s>>>(a, e0, e1); \
+            else k_element<Real, K, M, 2, false><<<grid, 128, 0, s>>>(a, e0, e1);                  \
+        }                                                                                 \
     } while (0)
         if (kind_ == DJG_T4) {
             switch (model_) {
@@ -720,6 +784,18 @@ public:
         o->sm_count = sms_;
     }
 
+    // Test hook: the device constant planes as an AoS record (E x nrec Reals).
+    int64_t consts_out(void* out) override {
+        if (!out) return nrec_;
+        std::vector<Real> planes(size_t(nplanes_) * size_t(E_) * size_t(T::kPlane));
+        CK(cudaMemcpy(planes.data(), consts_.p, consts_.bytes, cudaMemcpyDeviceToHost));
+        Real* o = static_cast<Real*>(out);
+        for (int64_t e = 0; e < E_; ++e)
+            for (int f = 0; f < nrec_; ++f)
+                o[e * nrec_ + f] = planes[size_t((int64_t(f / T::kPlane) * E_ + e) * T::kPlane + f % T::kPlane)];
+        return nrec_;
+    }
+
     void slot_map(int32_t* out) override {
         std::vector<uint8_t> ranks(rank_.bytes);
         std::vector<int32_t> planes(size_t(E_ * npe_));
@@ -739,13 +815,14 @@ public:
 
 private:
     static constexpr int kGraphSteps = 32;
-    int kind_ = 0, model_ = 0, npe_ = 4, nconst_ = 0, nplanes_ = 0, policy_ = 0, sms_ = 0;
+    int kind_ = 0, model_ = 0, npe_ = 4, nconst_ = 0, nrec_ = 0, nplanes_ = 0, policy_ = 0, sms_ = 0;
+    bool compact_ = false;
     uint32_t flags_ = 0;
     int64_t N_ = 0, E_ = 0, capacity_ = 0;
     cudaStream_t stream_ = nullptr;
     std::vector<int32_t> slice_base_;
     int rank_bytes_ = 1;
-    DevBuf elemL2g_, haloSend_, haloRecv_;
+    DevBuf elemL2g_, haloSend_, haloRecv_, X_;
     int64_t nsend_ = 0, nrecv_ = 0;
     DevBuf conn_, rank_, consts_, u_[3], uscratch_, flat_, ef_, rowlen_, slicebase_, c1_, code_, target_, tTotal_,
         rext_, ctrl_;
@@ -973,6 +1050,16 @@ int djg_get_slot_map(djg_engine* eng, int32_t* out) {
 
 int djg_debug_cbrt(int32_t precision, const void* in, void* out, int64_t n, int32_t device) {
     return djg::debug_cbrt(precision, in, out, n, device);
+}
+
+int64_t djg_get_consts(djg_engine* eng, void* out) {
+    if (!eng || !eng->impl) return -1;
+    try {
+        return eng->impl->consts_out(out);
+    } catch (const std::exception& e) {
+        eng->err = e.what();
+        return -1;
+    }
 }
 
 const char* djg_last_error(djg_engine* eng) { return eng ? eng->err.c_str() : "null engine"; }

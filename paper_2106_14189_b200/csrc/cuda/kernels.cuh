@@ -22,6 +22,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "../common/element_math.hpp"
+
 namespace djg {
 
 // ------------------------------------------------------------------ types
@@ -118,6 +120,9 @@ struct MatParams {
     Real eta_a;   // dI4 = eta_a (Ib4 - 1)
     Real eta_b;   // dI6 = eta_b (Ib6 - 1)
     Real dI2;     // c01
+    // compact mode / device precompute: what build_element_constants needs
+    Real A[6], B[6];  // fibre structure tensors a a^T, b b^T (FibreDirections)
+    Real chk;         // c_hg * kappa (k_hg = chk * cbrt(V0), precompute.hpp:252)
 };
 
 template <class Real>
@@ -130,6 +135,7 @@ struct ElemArgs {
     const typename RT<Real>::Plane* c;   // nplanes planes of Plane[E]
     const typename RT<Real>::Node* u[3]; // triple-buffered displacement
     const typename RT<Real>::Node* u_override;
+    const typename RT<Real>::Node* X;    // reference coordinates (compact H8, device precompute)
     typename RT<Real>::Node* ef;         // force slots (xyz + pad), sliced CSR order
     Ctrl* ctrl;
     MatParams<Real> mat;
@@ -248,8 +254,11 @@ __device__ __forceinline__ void load_ranks(const void* base, long long e, int (&
     }
 }
 
+// Reals of the compact record kept in HBM: J0 (9), det J0, V0, pad.
+constexpr int kCompactRecord = 12;
+
 // One element: loads, DJ-TLED force, stores of its npe rows into their slots.
-template <class Real, int KIND, int MODEL, int RB>
+template <class Real, int KIND, int MODEL, int RB, bool COMPACT>
 __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long long e,
                                              const typename RT<Real>::Node* __restrict__ u) {
     using L = Layout<KIND, MODEL>;
@@ -264,15 +273,41 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
         const int4 q = __ldcs(A.conn + (long long)p * A.E + e);
         nid[4 * p + 0] = q.x; nid[4 * p + 1] = q.y; nid[4 * p + 2] = q.z; nid[4 * p + 3] = q.w;
     }
-    // Hot constants.
-    Real c[NP * T::kPlane];
+    // Hot constants: the full record from HBM, or (compact) J0, det J0, V0
+    // from HBM and the rest rebuilt here with the precompute's own arithmetic.
+    constexpr int NC = COMPACT ? kCompactRecord : NP * T::kPlane;
+    Real c[COMPACT ? L::count + 1 : NC];
 #pragma unroll
-    for (int p = 0; p < NP; ++p) {
+    for (int p = 0; p < NC / T::kPlane; ++p) {
         const typename T::Plane v = T::load_plane(A.c + (long long)p * A.E + e);
         if constexpr (T::kPlane == 4) {
             c[4 * p + 0] = v.x; c[4 * p + 1] = v.y; c[4 * p + 2] = v.z; c[4 * p + 3] = v.w;
         } else {
             c[2 * p + 0] = v.x; c[2 * p + 1] = v.y;
+        }
+    }
+    if constexpr (COMPACT) {
+        const Real J0[3][3] = {{c[0], c[1], c[2]}, {c[3], c[4], c[5]}, {c[6], c[7], c[8]}};
+        Real J0i[3][3];
+        em::inv3(J0, c[9], J0i);
+        em::first_invariant_tensors(J0i, c[10], c + 11, c + 17);
+        if constexpr (L::kI4) em::fibre_tensors(J0i, c[10], A.mat.A, c + L::m4, c + L::I4m);
+        if constexpr (L::kI6) em::fibre_tensors(J0i, c[10], A.mat.B, c + L::m6, c + L::I6m);
+        if constexpr (L::kI2) em::second_invariant_tensors(J0i, c[10], c + 11, c + L::M2, c + L::I2m);
+        if constexpr (L::kH8) {
+            Real x[8][3];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+                const typename T::Node v = T::load_node(A.X + nid[a]);
+                x[a][0] = v.x; x[a][1] = v.y; x[a][2] = v.z;
+            }
+            Real gamma[4][8];
+            em::hourglass_vectors(x, J0i, gamma);
+            c[L::khg] = A.mat.chk * ref_cbrt(c[10]);
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+#pragma unroll
+                for (int a = 0; a < 8; ++a) c[L::gamma + 8 * m + a] = gamma[m][a];
         }
     }
     // Gathered displacements of the element's nodes.
@@ -482,14 +517,14 @@ __device__ __forceinline__ P pick3(int i, P a, P b, P c) {
 }
 
 // Elements [e0, e1) of the step (one slab).
-template <class Real, int KIND, int MODEL, int RB>
+template <class Real, int KIND, int MODEL, int RB, bool COMPACT>
 __global__ void __launch_bounds__(128) k_element(const ElemArgs<Real> A, long long e0, long long e1) {
     const long long e = e0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= e1) return;
     if (__ldcg(&A.ctrl->halted)) return;
     const int phase = int(__ldcg(&A.ctrl->step) % 3);
     const typename RT<Real>::Node* u = A.u_override ? A.u_override : pick3(phase, A.u[0], A.u[1], A.u[2]);
-    element_body<Real, KIND, MODEL, RB>(A, e, u);
+    element_body<Real, KIND, MODEL, RB, COMPACT>(A, e, u);
 }
 
 // ------------------------------------------------------------------ K2+K3
@@ -776,6 +811,78 @@ __global__ void k_agree(Ctrl* ctrl, const long long* __restrict__ reduced) {
     ctrl->halted = code == 2 ? 4 : 5;
     ctrl->halt_first_inv = code == 2 ? -reduced[1] : -1;
     ctrl->agreed = 1;  // later status/agree rounds (halted engine) are no-ops
+}
+
+// ------------------------------------------------------------------ precompute
+
+// build_element_constants on the device: the record of every
+// element from the reference coordinates, through the same element_math
+// functions as the host builder, written straight into the constant planes
+// (the first `nrec` Reals of the record: everything, or the compact part).
+// bad[0] collects the smallest element with det J0 <= 0 (MeshError).
+template <class Real, int KIND, int MODEL>
+__global__ void k_precompute(const ElemArgs<Real> A, int nrec, typename RT<Real>::Plane* planes,
+                             unsigned long long* bad) {
+    using L = Layout<KIND, MODEL>;
+    using T = RT<Real>;
+    constexpr int NPE = L::NPE;
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= A.E) return;
+    int nid[NPE];
+#pragma unroll
+    for (int p = 0; p < NPE / 4; ++p) {
+        const int4 q = A.conn[(long long)p * A.E + e];
+        nid[4 * p + 0] = q.x; nid[4 * p + 1] = q.y; nid[4 * p + 2] = q.z; nid[4 * p + 3] = q.w;
+    }
+    Real x[8][3];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        if (a < NPE) {
+            const typename T::Node v = T::load_node(A.X + nid[a]);
+            x[a][0] = v.x; x[a][1] = v.y; x[a][2] = v.z;
+        } else {
+            x[a][0] = x[a][1] = x[a][2] = Real(0);
+        }
+    }
+    Real c[L::count + 1];
+    Real J[3][3], Ji[3][3], det;
+    if (!em::jacobian0(KIND, x, J, Ji, det)) {
+        atomicMin(bad, (unsigned long long)e);
+        return;
+    }
+    const Real v0 = em::volume0(KIND, det);
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) c[3 * i + j] = J[i][j];
+    c[9] = det;
+    c[10] = v0;
+    c[L::count] = Real(0);
+    c[11] = Real(0);  // pad of the compact record
+    if (nrec > kCompactRecord) {
+        em::first_invariant_tensors(Ji, v0, c + 11, c + 17);
+        if constexpr (L::kI4) em::fibre_tensors(Ji, v0, A.mat.A, c + L::m4, c + L::I4m);
+        if constexpr (L::kI6) em::fibre_tensors(Ji, v0, A.mat.B, c + L::m6, c + L::I6m);
+        if constexpr (L::kI2) em::second_invariant_tensors(Ji, v0, c + 11, c + L::M2, c + L::I2m);
+        if constexpr (L::kH8) {
+            Real gamma[4][8];
+            em::hourglass_vectors(x, Ji, gamma);
+            c[L::khg] = A.mat.chk * ref_cbrt(v0);
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+#pragma unroll
+                for (int a = 0; a < 8; ++a) c[L::gamma + 8 * m + a] = gamma[m][a];
+        }
+    }
+    constexpr int W = T::kPlane;
+    for (int p = 0; p * W < nrec; ++p) {
+        Real* dst = reinterpret_cast<Real*>(planes + (long long)p * A.E + e);
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+            const int f = p * W + k;
+            dst[k] = f < nrec && f < L::count ? c[f] : Real(0);
+        }
+    }
 }
 
 // ------------------------------------------------------------------ setup

@@ -23,6 +23,7 @@
 #endif
 
 #include "djg_types.h"
+#include "../common/element_math.hpp"
 
 namespace djg {
 
@@ -439,58 +440,40 @@ inline void hourglass_vectors(const V3<Real>* x, const Shape<Real>& D, const Rea
     }
 }
 
-// The hot-field record of build_element_constants (precompute.hpp:206-255):
-// G_k from J0inv columns, m = tr(S G_k), I_m = 2 V0 J0inv^T K J0inv.
+// The hot-field record of build_element_constants (precompute.hpp:206-255),
+// through the arithmetic shared with the device (common/element_math.hpp).
 template <class Real>
 inline bool element_record(const V3<Real>* x, const Shape<Real>& D, const Material<Real>& mat,
                            const V3<Real>& fa_unit, const V3<Real>& fb_unit, Real c_hg,
                            const ConstLayout& L, Real* out) {
-    Jac<Real> j;
-    if (!jacobian0(x, D, j)) return false;
-    const Real v0 = volume0(j, D.kind);
+    Real xa[8][3];
+    for (int a = 0; a < D.n; ++a) {
+        xa[a][0] = x[a].x;
+        xa[a][1] = x[a].y;
+        xa[a][2] = x[a].z;
+    }
+    for (int a = D.n; a < 8; ++a) xa[a][0] = xa[a][1] = xa[a][2] = Real(0);
+    Real J[3][3], Ji[3][3], det;
+    if (!em::jacobian0(D.kind, xa, J, Ji, det)) return false;
+    const Real v0 = em::volume0(D.kind, det);
     if (!(v0 > Real(0))) return false;
     for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) out[L.J0 + 3 * r + c] = j.J[r][c];
-    out[L.det] = j.det;
+        for (int c = 0; c < 3; ++c) out[L.J0 + 3 * r + c] = J[r][c];
+    out[L.det] = det;
     out[L.V0] = v0;
-    const V3<Real> q0{j.Jinv[0][0], j.Jinv[1][0], j.Jinv[2][0]};
-    const V3<Real> q1{j.Jinv[0][1], j.Jinv[1][1], j.Jinv[2][1]};
-    const V3<Real> q2{j.Jinv[0][2], j.Jinv[1][2], j.Jinv[2][2]};
-    const Sym<Real> G[6] = {outer(q0), outer(q1), outer(q2), sym_outer(q0, q1), sym_outer(q0, q2), sym_outer(q1, q2)};
-    Real m1[6];
-    for (int k = 0; k < 6; ++k) m1[k] = out[L.m1 + k] = trace(G[k]);
-    const Real two_v0 = 2 * v0;
-    const Sym<Real> ident{{Real(1), Real(1), Real(1), Real(0), Real(0), Real(0)}};
-    const Sym<Real> I1m = scaled(two_v0, congruence(j.Jinv, ident));
-    for (int k = 0; k < 6; ++k) out[L.I1m + k] = I1m.v[k];
-    if (mat.needs_i2()) {
-        // M2 = (m1 m1^T - W) / 2 with W[p][q] = tr(G_p G_q) (precompute.hpp:67-84).
-        for (int p = 0; p < 6; ++p)
-            for (int q = p; q < 6; ++q)
-                out[L.M2 + sym6_index(p, q)] = (m1[p] * m1[q] - ddot(G[p], G[q])) / 2;
-        // I2m_k = 2 V0 J0inv^T (tr(G_k) I - G_k) J0inv (precompute.hpp:104-115).
-        for (int k = 0; k < 6; ++k) {
-            const Real tr = trace(G[k]);
-            const Sym<Real> ker{{tr - G[k].v[0], tr - G[k].v[1], tr - G[k].v[2], -G[k].v[3], -G[k].v[4], -G[k].v[5]}};
-            const Sym<Real> t = scaled(two_v0, congruence(j.Jinv, ker));
-            for (int c = 0; c < 6; ++c) out[L.I2m + 6 * k + c] = t.v[c];
-        }
-    }
+    em::first_invariant_tensors(Ji, v0, out + L.m1, out + L.I1m);
+    if (mat.needs_i2()) em::second_invariant_tensors(Ji, v0, out + L.m1, out + L.M2, out + L.I2m);
     if (mat.needs_i4()) {
         const Sym<Real> A = outer(fa_unit);
-        for (int k = 0; k < 6; ++k) out[L.m4 + k] = ddot(A, G[k]);
-        const Sym<Real> t = scaled(two_v0, congruence(j.Jinv, A));
-        for (int c = 0; c < 6; ++c) out[L.I4m + c] = t.v[c];
+        em::fibre_tensors(Ji, v0, A.v, out + L.m4, out + L.I4m);
     }
     if (mat.needs_i6()) {
         const Sym<Real> B = outer(fb_unit);
-        for (int k = 0; k < 6; ++k) out[L.m6 + k] = ddot(B, G[k]);
-        const Sym<Real> t = scaled(two_v0, congruence(j.Jinv, B));
-        for (int c = 0; c < 6; ++c) out[L.I6m + c] = t.v[c];
+        em::fibre_tensors(Ji, v0, B.v, out + L.m6, out + L.I6m);
     }
     if (D.kind == DJG_H8) {
         Real gamma[4][8];
-        hourglass_vectors(x, D, j.Jinv, gamma);
+        em::hourglass_vectors(xa, Ji, gamma);
         out[L.khg] = c_hg * mat.kappa * std::cbrt(v0);
         for (int m = 0; m < 4; ++m)
             for (int a = 0; a < 8; ++a) out[L.gamma + 8 * m + a] = gamma[m][a];
@@ -536,6 +519,7 @@ struct Problem {
     std::vector<Real> dof_target;      // 3N
     std::vector<Real> dof_t_total;     // 3N
     Real dt = 0, crit_dt = 0, alpha = 0, c2 = 0, c3 = 0, ramp_t_total = 0, c_wave = 0;
+    Real c_hg = 0;
     int policy = DJG_ABORT;
 };
 
@@ -598,6 +582,7 @@ inline Problem<Real> build_problem(const djg_scenario_spec& s, int threads) {
     if (P.mat.needs_i4()) fa = Material<Real>::unit(P.mat.fa);
     if (P.mat.needs_i6()) fb = Material<Real>::unit(P.mat.fb);
     const Real c_hg = Real(s.c_hg);
+    P.c_hg = c_hg;
     const Shape<Real> D(s.kind);
     P.consts.assign(size_t(E) * size_t(L.count), Real(0));
     int64_t bad = -1;
@@ -851,6 +836,7 @@ inline PartProblem<Real> build_part(const Problem<Real>& P, int nparts, int part
     L.c3 = P.c3;
     L.ramp_t_total = P.ramp_t_total;
     L.c_wave = P.c_wave;
+    L.c_hg = P.c_hg;
     L.policy = P.policy;
     L.mesh.kind = m.kind;
     const int64_t Nl = int64_t(R.node_l2g.size()), El = int64_t(R.elem_l2g.size());

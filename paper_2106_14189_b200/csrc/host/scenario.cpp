@@ -75,7 +75,13 @@ void desc_of(const djg::Problem<Real>& P, int32_t device, djg_desc& d) {
     d.material.eta_b = double(P.mat.eta_b);
     d.material.c10 = double(P.mat.c10);
     d.material.c01 = double(P.mat.c01);
+    for (int i = 0; i < 3; ++i) {
+        d.material.fibre_a[i] = double(i == 0 ? P.mat.fa.x : (i == 1 ? P.mat.fa.y : P.mat.fa.z));
+        d.material.fibre_b[i] = double(i == 0 ? P.mat.fb.x : (i == 1 ? P.mat.fb.y : P.mat.fb.z));
+    }
     d.device = device;
+    d.nodes = P.mesh.nodes.data();
+    d.c_hg = double(P.c_hg);
 }
 
 // DjEngine(mesh, material, c_hg) precompute (djtled_force.hpp:145-157) for
@@ -91,22 +97,31 @@ int create_from_mesh(const djg_mesh_desc& m, djg_engine** out) {
 #ifdef _OPENMP
     if (m.threads > 0) omp_set_num_threads(m.threads);
 #endif
-    djg::validate_mesh(mesh);
-    const auto mat = djg::Material<Real>::from(m.material);
-    const djg::ConstLayout L(m.kind, mat.model);
-    const djg::Shape<Real> D(m.kind);
-    djg::V3<Real> fa{0, 0, 0}, fb{0, 0, 0};
-    if (mat.needs_i4()) fa = djg::Material<Real>::unit(mat.fa);
-    if (mat.needs_i6()) fb = djg::Material<Real>::unit(mat.fb);
     const int npe = mesh.npe();
     const int64_t E = mesh.num_elements();
-    std::vector<Real> consts(size_t(E) * size_t(L.count), Real(0));
-    const Real c_hg = Real(m.c_hg);
+    const bool on_device = (m.flags & DJG_FLAG_DEVICE_PRECOMPUTE) != 0;
+    const auto mat = djg::Material<Real>::from(m.material);
+    const djg::ConstLayout L(m.kind, mat.model);
+    std::vector<Real> consts;
+    if (on_device) {
+        // the engine builds the records (and rejects inverted elements) on the GPU
+        for (int64_t i = 0; i < int64_t(mesh.conn.size()); ++i)
+            if (mesh.conn[size_t(i)] < 0 || mesh.conn[size_t(i)] >= mesh.num_nodes())
+                throw djg::MeshError("connectivity index out of range", long(i / npe));
+    } else {
+        djg::validate_mesh(mesh);
+        const djg::Shape<Real> D(m.kind);
+        djg::V3<Real> fa{0, 0, 0}, fb{0, 0, 0};
+        if (mat.needs_i4()) fa = djg::Material<Real>::unit(mat.fa);
+        if (mat.needs_i6()) fb = djg::Material<Real>::unit(mat.fb);
+        consts.assign(size_t(E) * size_t(L.count), Real(0));
+        const Real c_hg = Real(m.c_hg);
 #pragma omp parallel for schedule(static)
-    for (int64_t e = 0; e < E; ++e) {
-        djg::V3<Real> x[8];
-        for (int a = 0; a < npe; ++a) x[a] = mesh.node(mesh.conn[size_t(e * npe + a)]);
-        djg::element_record(x, D, mat, fa, fb, c_hg, L, consts.data() + size_t(e) * L.count);
+        for (int64_t e = 0; e < E; ++e) {
+            djg::V3<Real> x[8];
+            for (int a = 0; a < npe; ++a) x[a] = mesh.node(mesh.conn[size_t(e * npe + a)]);
+            djg::element_record(x, D, mat, fa, fb, c_hg, L, consts.data() + size_t(e) * L.count);
+        }
     }
     const djg::Adjacency adj = djg::build_adjacency(mesh.conn, mesh.num_nodes(), npe);
     djg_desc d;
@@ -116,7 +131,7 @@ int create_from_mesh(const djg_mesh_desc& m, djg_engine** out) {
     d.num_nodes = mesh.num_nodes();
     d.num_elements = E;
     d.conn = mesh.conn.data();
-    d.consts = consts.data();
+    d.consts = on_device ? nullptr : consts.data();
     d.nconst = L.count;
     d.inversion_policy = m.inversion_policy;
     d.csr_offsets = adj.offsets.data();
@@ -125,6 +140,8 @@ int create_from_mesh(const djg_mesh_desc& m, djg_engine** out) {
     d.material = m.material;
     d.device = m.device;
     d.flags = m.flags;
+    d.nodes = mesh.nodes.data();
+    d.c_hg = m.c_hg;
     return djg_create(&d, out);
 }
 

@@ -236,6 +236,13 @@ class GpuDjEngine:
         self._check(_lib().djg_get_info(self._h, C.byref(i)))
         return {name: getattr(i, name) for name, _ in i._fields_}
 
+    def device_consts(self) -> np.ndarray:
+        """The per-element record held on the device (E x n)."""
+        n = int(_lib().djg_get_consts(self._h, None))
+        out = np.zeros((self.num_elements, n), self.dtype)
+        _lib().djg_get_consts(self._h, A.ptr(out))
+        return out
+
     def slot_map(self) -> np.ndarray:
         out = np.zeros(self.scenario.npe * self.num_elements, np.int32)
         self._check(_lib().djg_get_slot_map(self._h, A.ptr(out)))

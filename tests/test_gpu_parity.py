@@ -70,6 +70,35 @@ def test_materials_small(kind, model, precision, mode, monkeypatch):
     check_run(box_spec(kind=kind, model=model, divisions=4, precision=precision, ramp_steps=300), 300, flags=flags)
 
 
+@pytest.mark.parametrize("precision", [4, 8])
+@pytest.mark.parametrize("kind", ["T4", "H8"])
+@pytest.mark.parametrize("model", ["NH", "TI", "OT", "MR"])
+@pytest.mark.parametrize("flags", [A.DJG_FLAG_COMPACT, A.DJG_FLAG_DEVICE_PRECOMPUTE,
+                                   A.DJG_FLAG_COMPACT | A.DJG_FLAG_DEVICE_PRECOMPUTE])
+def test_compact_and_device_precompute_bitwise(kind, model, precision, flags):
+    check_run(box_spec(kind=kind, model=model, divisions=4, precision=precision, ramp_steps=300), 300, flags=flags)
+
+
+@pytest.mark.parametrize("precision", [4, 8])
+@pytest.mark.parametrize("kind", ["T4", "H8"])
+@pytest.mark.parametrize("model", ["NH", "TI", "OT", "MR"])
+def test_device_precompute_equals_host_precompute(kind, model, precision):
+    """build_element_constants on the GPU == on the host (== the reference),
+    bit for bit, every field of every element."""
+    spec = box_spec(kind=kind, model=model, divisions=(5, 4, 6), precision=precision)
+    sc = Scenario(spec)
+    host = sc.image()["consts"].reshape(sc.num_elements, -1)
+    with GpuDjEngine(sc, flags=A.DJG_FLAG_DEVICE_PRECOMPUTE) as eng:
+        dev = eng.device_consts()
+    assert np.array_equal(dev, host)
+
+
+@pytest.mark.parametrize("cfg", ["cfg1", "cfg2"])
+@pytest.mark.parametrize("flags", [A.DJG_FLAG_COMPACT, A.DJG_FLAG_COMPACT | A.DJG_FLAG_DEVICE_PRECOMPUTE])
+def test_compact_cfg_2000_steps(cfg, flags):
+    check_run(config_spec(cfg, precision=4), 2000, flags=flags)
+
+
 @pytest.mark.parametrize("cfg", ["cfg1", "cfg2"])
 def test_slab_path_cfg(cfg, monkeypatch):
     monkeypatch.setenv("DJG_SLAB_KB", "64")

@@ -78,18 +78,17 @@ typedef struct djg_desc {
     djg_material_params material;
     int32_t device;             /* CUDA ordinal */
     uint32_t flags;             /* DJG_FLAG_* */
-    const void* nodes;          /* 3N Reals, reference coordinates (needed by
-                                   DJG_FLAG_DEVICE_PRECOMPUTE and by compact H8) */
-    double c_hg;                /* hourglass coefficient (compact H8 / device precompute) */
+    const void* nodes;          /* 3N Reals, reference coordinates (DJG_FLAG_DEVICE_PRECOMPUTE) */
+    double c_hg;                /* hourglass coefficient (DJG_FLAG_DEVICE_PRECOMPUTE) */
 } djg_desc;
 
 /* Flags */
 #define DJG_FLAG_NO_GRAPH 1u    /* launch kernels one by one instead of CUDA graphs */
 #define DJG_FLAG_SLABS 2u       /* pipeline each step as L2-sized element slabs (bit-identical) */
 #define DJG_FLAG_NO_DISCARD 4u  /* slab step: keep consumed force rows in L2 (no discard) */
-#define DJG_FLAG_COMPACT 8u     /* keep only J0, det J0, V0 per element in HBM; the element
-                                   kernel rebuilds m / I tensors (and H8 hourglass data) in
-                                   registers with the precompute's own arithmetic (bitwise) */
+#define DJG_FLAG_COMPACT 8u     /* keep J0, det J0, V0 (+ H8 k_hg, gamma) per element in HBM;
+                                   the element kernel rebuilds the m / I tensors in registers
+                                   with the precompute's own arithmetic (bitwise) */
 #define DJG_FLAG_DEVICE_PRECOMPUTE 16u /* build the per-element record on the GPU from
                                           nodes + conn (desc.consts may be NULL) */
 
@@ -212,7 +211,8 @@ int djg_get_info(djg_engine* eng, djg_engine_info* info);
 int djg_get_slot_map(djg_engine* eng, int32_t* slot_pos);
 
 /* Test hook: the per-element record held on the device as E x n Reals
- * (n = nconst, or 12 in compact mode: J0, det J0, V0, pad). Returns n
+ * (n = nconst, or in compact mode 12: J0, det J0, V0, pad -- 45 for H8:
+ * + k_hg, gamma). Returns n
  * (out may be NULL to query it), -1 on error. */
 int64_t djg_get_consts(djg_engine* eng, void* out);
 

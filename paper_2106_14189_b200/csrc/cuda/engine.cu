@@ -117,14 +117,13 @@ public:
         nconst_ = const_count(kind_, model_);
         compact_ = (flags_ & DJG_FLAG_COMPACT) != 0;
         const bool dev_pre = (flags_ & DJG_FLAG_DEVICE_PRECOMPUTE) != 0;
-        nrec_ = compact_ ? kCompactRecord : nconst_;
+        nrec_ = compact_ ? (kind_ == DJG_H8 ? kCompactLen<1> : kCompactLen<0>) : nconst_;
         nplanes_ = (nrec_ + T::kPlane - 1) / T::kPlane;
         if (d.nconst != nconst_) throw DescError("nconst does not match djg_const_count(kind, model)");
         if (N_ < 1 || E_ < 1) throw DescError("mesh must have nodes and elements");
         if (!d.conn) throw DescError("descriptor is missing conn");
         if (!d.consts && !dev_pre) throw DescError("descriptor is missing consts (or DJG_FLAG_DEVICE_PRECOMPUTE)");
-        if (!d.nodes && (dev_pre || (compact_ && kind_ == DJG_H8)))
-            throw DescError("device precompute / compact H8 need the node coordinates");
+        if (!d.nodes && dev_pre) throw DescError("device precompute needs the node coordinates");
         if (!d.c1 != !d.massless) throw DescError("c1 and massless must be given together");
         if (E_ * npe_ > INT32_MAX || N_ > INT32_MAX) throw DescError("mesh too large for 32-bit slot indexing");
 
@@ -225,8 +224,8 @@ public:
             conn_.alloc(planes.size() * sizeof(int32_t));
             CK(cudaMemcpy(conn_.p, planes.data(), conn_.bytes, cudaMemcpyHostToDevice));
         }
-        // Reference coordinates (compact H8 and device precompute).
-        if (d.nodes && (dev_pre || (compact_ && kind_ == DJG_H8))) {
+        // Reference coordinates (device precompute).
+        if (d.nodes && dev_pre) {
             X_.alloc(size_t(N_) * sizeof(Node));
             DevBuf flat;
             flat.alloc(size_t(3 * N_) * sizeof(Real));
@@ -289,7 +288,7 @@ public:
                               cudaMemcpyHostToDevice));
                 const int64_t work = ne * nplanes_;
                 k_transpose_consts<Real><<<unsigned((work + 255) / 256), 256>>>(
-                    stage.as<Real>(), nconst_, e0, ne, E_, nplanes_, consts_.as<Real>());
+                    stage.as<Real>(), nconst_, nrec_, nconst_ - 33, e0, ne, E_, nplanes_, consts_.as<Real>());
                 CK(cudaGetLastError());
             }
             CK(cudaDeviceSynchronize());

@@ -254,8 +254,12 @@ __device__ __forceinline__ void load_ranks(const void* base, long long e, int (&
     }
 }
 
-// Reals of the compact record kept in HBM: J0 (9), det J0, V0, pad.
+// Compact record kept in HBM: J0 (9), det J0, V0, pad -- and for H8 the
+// hourglass data k_hg, gamma (32) after it (cheap to store, costly to
+// rebuild: it needs the coordinates and a cube root).
 constexpr int kCompactRecord = 12;
+template <int KIND>
+constexpr int kCompactLen = KIND == 1 ? kCompactRecord + 33 : kCompactRecord;
 
 // One element: loads, DJ-TLED force, stores of its npe rows into their slots.
 template <class Real, int KIND, int MODEL, int RB, bool COMPACT>
@@ -275,18 +279,29 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
     }
     // Hot constants: the full record from HBM, or (compact) J0, det J0, V0
     // from HBM and the rest rebuilt here with the precompute's own arithmetic.
-    constexpr int NC = COMPACT ? kCompactRecord : NP * T::kPlane;
-    Real c[COMPACT ? L::count + 1 : NC];
+    constexpr int NCR = kCompactLen<KIND>;
+    constexpr int NC = COMPACT ? (NCR + T::kPlane - 1) / T::kPlane * T::kPlane : NP * T::kPlane;
+    Real r[NC];
 #pragma unroll
     for (int p = 0; p < NC / T::kPlane; ++p) {
         const typename T::Plane v = T::load_plane(A.c + (long long)p * A.E + e);
         if constexpr (T::kPlane == 4) {
-            c[4 * p + 0] = v.x; c[4 * p + 1] = v.y; c[4 * p + 2] = v.z; c[4 * p + 3] = v.w;
+            r[4 * p + 0] = v.x; r[4 * p + 1] = v.y; r[4 * p + 2] = v.z; r[4 * p + 3] = v.w;
         } else {
-            c[2 * p + 0] = v.x; c[2 * p + 1] = v.y;
+            r[2 * p + 0] = v.x; r[2 * p + 1] = v.y;
         }
     }
-    if constexpr (COMPACT) {
+    Real c[COMPACT ? L::count + 1 : NC];
+    if constexpr (!COMPACT) {
+#pragma unroll
+        for (int k = 0; k < NC; ++k) c[k] = r[k];
+    } else {
+#pragma unroll
+        for (int k = 0; k < 11; ++k) c[k] = r[k];
+        if constexpr (L::kH8) {
+#pragma unroll
+            for (int k = 0; k < 33; ++k) c[L::khg + k] = r[kCompactRecord + k];
+        }
         const Real J0[3][3] = {{c[0], c[1], c[2]}, {c[3], c[4], c[5]}, {c[6], c[7], c[8]}};
         Real J0i[3][3];
         em::inv3(J0, c[9], J0i);
@@ -294,21 +309,6 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
         if constexpr (L::kI4) em::fibre_tensors(J0i, c[10], A.mat.A, c + L::m4, c + L::I4m);
         if constexpr (L::kI6) em::fibre_tensors(J0i, c[10], A.mat.B, c + L::m6, c + L::I6m);
         if constexpr (L::kI2) em::second_invariant_tensors(J0i, c[10], c + 11, c + L::M2, c + L::I2m);
-        if constexpr (L::kH8) {
-            Real x[8][3];
-#pragma unroll
-            for (int a = 0; a < 8; ++a) {
-                const typename T::Node v = T::load_node(A.X + nid[a]);
-                x[a][0] = v.x; x[a][1] = v.y; x[a][2] = v.z;
-            }
-            Real gamma[4][8];
-            em::hourglass_vectors(x, J0i, gamma);
-            c[L::khg] = A.mat.chk * ref_cbrt(c[10]);
-#pragma unroll
-            for (int m = 0; m < 4; ++m)
-#pragma unroll
-                for (int a = 0; a < 8; ++a) c[L::gamma + 8 * m + a] = gamma[m][a];
-        }
     }
     // Gathered displacements of the element's nodes.
     Real ux[NPE], uy[NPE], uz[NPE];
@@ -858,8 +858,7 @@ __global__ void k_precompute(const ElemArgs<Real> A, int nrec, typename RT<Real>
     c[9] = det;
     c[10] = v0;
     c[L::count] = Real(0);
-    c[11] = Real(0);  // pad of the compact record
-    if (nrec > kCompactRecord) {
+    {
         em::first_invariant_tensors(Ji, v0, c + 11, c + 17);
         if constexpr (L::kI4) em::fibre_tensors(Ji, v0, A.mat.A, c + L::m4, c + L::I4m);
         if constexpr (L::kI6) em::fibre_tensors(Ji, v0, A.mat.B, c + L::m6, c + L::I6m);
@@ -874,13 +873,17 @@ __global__ void k_precompute(const ElemArgs<Real> A, int nrec, typename RT<Real>
                 for (int a = 0; a < 8; ++a) c[L::gamma + 8 * m + a] = gamma[m][a];
         }
     }
+    // compact record: J0, det, V0, pad [, k_hg, gamma]
+    const bool compact = nrec < L::count;
     constexpr int W = T::kPlane;
     for (int p = 0; p * W < nrec; ++p) {
         Real* dst = reinterpret_cast<Real*>(planes + (long long)p * A.E + e);
 #pragma unroll
         for (int k = 0; k < W; ++k) {
             const int f = p * W + k;
-            dst[k] = f < nrec && f < L::count ? c[f] : Real(0);
+            int src = f;
+            if (compact && f >= kCompactRecord) src = L::khg + (f - kCompactRecord);
+            dst[k] = (f < nrec && src < L::count && !(compact && f == 11)) ? c[src] : Real(0);
         }
     }
 }
@@ -889,19 +892,25 @@ __global__ void k_precompute(const ElemArgs<Real> A, int nrec, typename RT<Real>
 
 // AoS record chunk -> plane layout: plane p of element e holds record Reals
 // [kPlane*p, kPlane*p + kPlane).
+// nrec < nconst: the compact record (J0, det, V0, pad [, k_hg, gamma from
+// canonical offset hg_src]).
 template <class Real>
-__global__ void k_transpose_consts(const Real* __restrict__ aos, int nconst, long long e0, long long ne,
-                                   long long E, int nplanes, Real* __restrict__ planes) {
+__global__ void k_transpose_consts(const Real* __restrict__ aos, int nconst, int nrec, int hg_src, long long e0,
+                                   long long ne, long long E, int nplanes, Real* __restrict__ planes) {
     constexpr int W = RT<Real>::kPlane;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= ne * nplanes) return;
     const long long e = i / nplanes;
     const int p = int(i % nplanes);
     Real* dst = planes + ((long long)p * E + e0 + e) * W;
+    const bool compact = nrec < nconst;
 #pragma unroll
     for (int k = 0; k < W; ++k) {
         const int f = p * W + k;
-        dst[k] = f < nconst ? aos[e * nconst + f] : Real(0);
+        int src = f;
+        if (compact && f >= kCompactRecord) src = hg_src + (f - kCompactRecord);
+        const bool pad = f >= nrec || (compact && f == 11) || src >= nconst;
+        dst[k] = pad ? Real(0) : aos[e * nconst + src];
     }
 }
 

@@ -91,6 +91,8 @@ typedef struct djg_desc {
                                    with the precompute's own arithmetic (bitwise) */
 #define DJG_FLAG_DEVICE_PRECOMPUTE 16u /* build the per-element record on the GPU from
                                           nodes + conn (desc.consts may be NULL) */
+#define DJG_FLAG_FULL_RECORD 32u /* keep the full record in HBM (default for H8; T4
+                                    defaults to the compact record) */
 
 /* DjEngine(mesh, material, c_hg) (solver.hpp:264-267) at the mesh level:
  * the library runs the precompute (build_element_constants,
@@ -201,7 +203,7 @@ typedef struct djg_engine_info {
     int32_t kernels_per_step;   /* kernel launches per step */
     int32_t sm_count;
     int32_t slabs;              /* element slabs per step (2 kernels each) */
-    int32_t _pad;
+    int32_t compact;            /* 1: compact per-element record in HBM */
     int64_t slab_elements;      /* elements per slab */
 } djg_engine_info;
 int djg_get_info(djg_engine* eng, djg_engine_info* info);

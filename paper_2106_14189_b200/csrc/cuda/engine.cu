@@ -115,7 +115,10 @@ public:
         flags_ = d.flags;
         if (const char* v = std::getenv("DJG_SLAB_KB")) slab_bytes_ = int64_t(std::atoll(v)) << 10;
         nconst_ = const_count(kind_, model_);
-        compact_ = (flags_ & DJG_FLAG_COMPACT) != 0;
+        // Default record: compact for T4 (fewer bytes win), full for H8 (its
+        // heavier kernel is not bandwidth-bound; rebuilding costs more).
+        compact_ = (flags_ & DJG_FLAG_COMPACT) != 0 ||
+                   (!(flags_ & DJG_FLAG_FULL_RECORD) && d.kind == DJG_T4);
         const bool dev_pre = (flags_ & DJG_FLAG_DEVICE_PRECOMPUTE) != 0;
         nrec_ = compact_ ? (kind_ == DJG_H8 ? kCompactLen<1> : kCompactLen<0>) : nconst_;
         nplanes_ = (nrec_ + T::kPlane - 1) / T::kPlane;
@@ -778,6 +781,7 @@ public:
         o->const_planes = nplanes_;
         o->precision = int32_t(sizeof(Real));
         o->kernels_per_step = 2 * n_slabs_;
+        o->compact = compact_ ? 1 : 0;
         o->slabs = n_slabs_;
         o->slab_elements = slab_elems_;
         o->sm_count = sms_;

@@ -73,8 +73,9 @@ def test_materials_small(kind, model, precision, mode, monkeypatch):
 @pytest.mark.parametrize("precision", [4, 8])
 @pytest.mark.parametrize("kind", ["T4", "H8"])
 @pytest.mark.parametrize("model", ["NH", "TI", "OT", "MR"])
-@pytest.mark.parametrize("flags", [A.DJG_FLAG_COMPACT, A.DJG_FLAG_DEVICE_PRECOMPUTE,
-                                   A.DJG_FLAG_COMPACT | A.DJG_FLAG_DEVICE_PRECOMPUTE])
+@pytest.mark.parametrize("flags", [A.DJG_FLAG_COMPACT, A.DJG_FLAG_FULL_RECORD, A.DJG_FLAG_DEVICE_PRECOMPUTE,
+                                   A.DJG_FLAG_COMPACT | A.DJG_FLAG_DEVICE_PRECOMPUTE,
+                                   A.DJG_FLAG_FULL_RECORD | A.DJG_FLAG_DEVICE_PRECOMPUTE])
 def test_compact_and_device_precompute_bitwise(kind, model, precision, flags):
     check_run(box_spec(kind=kind, model=model, divisions=4, precision=precision, ramp_steps=300), 300, flags=flags)
 
@@ -88,9 +89,15 @@ def test_device_precompute_equals_host_precompute(kind, model, precision):
     spec = box_spec(kind=kind, model=model, divisions=(5, 4, 6), precision=precision)
     sc = Scenario(spec)
     host = sc.image()["consts"].reshape(sc.num_elements, -1)
-    with GpuDjEngine(sc, flags=A.DJG_FLAG_DEVICE_PRECOMPUTE) as eng:
+    with GpuDjEngine(sc, flags=A.DJG_FLAG_DEVICE_PRECOMPUTE | A.DJG_FLAG_FULL_RECORD) as eng:
         dev = eng.device_consts()
     assert np.array_equal(dev, host)
+    with GpuDjEngine(sc, flags=A.DJG_FLAG_DEVICE_PRECOMPUTE | A.DJG_FLAG_COMPACT) as eng:
+        dev_c = eng.device_consts()
+    with GpuDjEngine(sc, flags=A.DJG_FLAG_COMPACT) as eng:
+        host_c = eng.device_consts()
+    assert np.array_equal(dev_c, host_c)
+    assert np.array_equal(dev_c[:, :11], host[:, :11])
 
 
 @pytest.mark.parametrize("cfg", ["cfg1", "cfg2"])

@@ -305,7 +305,7 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
         const Real J0[3][3] = {{c[0], c[1], c[2]}, {c[3], c[4], c[5]}, {c[6], c[7], c[8]}};
         Real J0i[3][3];
         em::inv3(J0, c[9], J0i);
-        em::first_invariant_tensors(J0i, c[10], c + 11, c + 17);
+        em::first_invariant_tensors_fast(J0i, c[10], c + 11, c + 17);
         if constexpr (L::kI4) em::fibre_tensors(J0i, c[10], A.mat.A, c + L::m4, c + L::I4m);
         if constexpr (L::kI6) em::fibre_tensors(J0i, c[10], A.mat.B, c + L::m6, c + L::I6m);
         if constexpr (L::kI2) em::second_invariant_tensors(J0i, c[10], c + 11, c + L::M2, c + L::I2m);

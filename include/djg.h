@@ -93,6 +93,8 @@ typedef struct djg_desc {
                                           nodes + conn (desc.consts may be NULL) */
 #define DJG_FLAG_FULL_RECORD 32u /* keep the full record in HBM (default for H8; T4
                                     defaults to the compact record) */
+#define DJG_FLAG_TLED 64u        /* conventional TLED element forces (tled_force.hpp), the
+                                    paper's comparison path; record built on the device */
 
 /* DjEngine(mesh, material, c_hg) (solver.hpp:264-267) at the mesh level:
  * the library runs the precompute (build_element_constants,
@@ -205,6 +207,8 @@ typedef struct djg_engine_info {
     int32_t slabs;              /* element slabs per step (2 kernels each) */
     int32_t compact;            /* 1: compact per-element record in HBM */
     int64_t slab_elements;      /* elements per slab */
+    int32_t formulation;        /* 0 DJ-TLED, 1 TLED (DJG_FLAG_TLED) */
+    int32_t _pad1;
 } djg_engine_info;
 int djg_get_info(djg_engine* eng, djg_engine_info* info);
 

@@ -26,6 +26,7 @@ DJG_FLAG_NO_DISCARD = 4
 DJG_FLAG_COMPACT = 8
 DJG_FLAG_DEVICE_PRECOMPUTE = 16
 DJG_FLAG_FULL_RECORD = 32
+DJG_FLAG_TLED = 64
 
 KIND_NAMES = {"T4": DJG_T4, "H8": DJG_H8}
 MODEL_NAMES = {"NH": DJG_NH, "TI": DJG_TI, "OT": DJG_OT, "MR": DJG_MR}
@@ -151,7 +152,7 @@ class djg_engine_info(C.Structure):
         ("slot_capacity", C.c_int64), ("device_bytes", C.c_int64),
         ("npe", C.c_int32), ("nconst", C.c_int32), ("const_planes", C.c_int32), ("precision", C.c_int32),
         ("kernels_per_step", C.c_int32), ("sm_count", C.c_int32), ("slabs", C.c_int32),
-        ("compact", C.c_int32), ("slab_elements", C.c_int64),
+        ("compact", C.c_int32), ("slab_elements", C.c_int64), ("formulation", C.c_int32), ("_pad1", C.c_int32),
     ]
 
 

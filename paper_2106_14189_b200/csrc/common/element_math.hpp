@@ -213,6 +213,28 @@ DJG_HD R volume0(int kind, R det) {
     return kind == 0 ? det / R(6) : R(8) * det;
 }
 
+// TledModel::build record (tled_force.hpp:176-192): B0[a][j] = dh_a/dx_j at the
+// reference configuration, V0 -> out[3*npe], out[3*npe + 1] (the hourglass
+// data, H8, is appended by the caller exactly as for the DJ record).
+template <class R>
+DJG_HD void tled_b0(int kind, const R ji[3][3], R* b0) {
+    const int n = kind == 0 ? 4 : 8;
+    for (int a = 0; a < n; ++a)
+        for (int j = 0; j < 3; ++j)
+            b0[3 * a + j] = ji[j][0] * shape_d<R>(kind, 0, a) + ji[j][1] * shape_d<R>(kind, 1, a) +
+                            ji[j][2] * shape_d<R>(kind, 2, a);
+}
+
+// unit fibre direction (FibreDirections::normalise, precompute.hpp:35-39)
+template <class R>
+DJG_HD void unit3(const R a[3], R u[3]) {
+    const R n = std::sqrt(a[0] * a[0] + a[1] * a[1] + a[2] * a[2]);
+    const R s = R(1) / n;
+    u[0] = s * a[0];
+    u[1] = s * a[1];
+    u[2] = s * a[2];
+}
+
 // FibreDirections::from: S = a' a'^T with a' = a / |a| (precompute.hpp:22-39).
 template <class R>
 DJG_HD void fibre_structure(const R a[3], R S[6]) {

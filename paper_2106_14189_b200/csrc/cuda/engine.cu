@@ -117,16 +117,18 @@ public:
         nconst_ = const_count(kind_, model_);
         // Default record: compact for T4 (fewer bytes win), full for H8 (its
         // heavier kernel is not bandwidth-bound; rebuilding costs more).
-        compact_ = (flags_ & DJG_FLAG_COMPACT) != 0 ||
-                   (!(flags_ & DJG_FLAG_FULL_RECORD) && d.kind == DJG_T4);
-        const bool dev_pre = (flags_ & DJG_FLAG_DEVICE_PRECOMPUTE) != 0;
-        nrec_ = compact_ ? (kind_ == DJG_H8 ? kCompactLen<1> : kCompactLen<0>) : nconst_;
+        tled_ = (flags_ & DJG_FLAG_TLED) != 0;
+        compact_ = !tled_ && ((flags_ & DJG_FLAG_COMPACT) != 0 ||
+                              (!(flags_ & DJG_FLAG_FULL_RECORD) && d.kind == DJG_T4));
+        const bool dev_pre = tled_ || (flags_ & DJG_FLAG_DEVICE_PRECOMPUTE) != 0;
+        nrec_ = tled_ ? (kind_ == DJG_H8 ? TledLayout<1>::count : TledLayout<0>::count)
+                      : compact_ ? (kind_ == DJG_H8 ? kCompactLen<1> : kCompactLen<0>) : nconst_;
         nplanes_ = (nrec_ + T::kPlane - 1) / T::kPlane;
         if (d.nconst != nconst_) throw DescError("nconst does not match djg_const_count(kind, model)");
         if (N_ < 1 || E_ < 1) throw DescError("mesh must have nodes and elements");
         if (!d.conn) throw DescError("descriptor is missing conn");
         if (!d.consts && !dev_pre) throw DescError("descriptor is missing consts (or DJG_FLAG_DEVICE_PRECOMPUTE)");
-        if (!d.nodes && dev_pre) throw DescError("device precompute needs the node coordinates");
+        if (!d.nodes && dev_pre) throw DescError("device precompute / TLED need the node coordinates");
         if (!d.c1 != !d.massless) throw DescError("c1 and massless must be given together");
         if (E_ * npe_ > INT32_MAX || N_ > INT32_MAX) throw DescError("mesh too large for 32-bit slot indexing");
 
@@ -242,8 +244,15 @@ public:
             const Real fa[3] = {Real(d.material.fibre_a[0]), Real(d.material.fibre_a[1]), Real(d.material.fibre_a[2])};
             const Real fb[3] = {Real(d.material.fibre_b[0]), Real(d.material.fibre_b[1]), Real(d.material.fibre_b[2])};
             for (int k = 0; k < 6; ++k) ea_.mat.A[k] = ea_.mat.B[k] = Real(0);
-            if (model_ == DJG_TI || model_ == DJG_OT) em::fibre_structure(fa, ea_.mat.A);
-            if (model_ == DJG_OT) em::fibre_structure(fb, ea_.mat.B);
+            for (int k = 0; k < 3; ++k) ea_.mat.fa[k] = ea_.mat.fb[k] = Real(0);
+            if (model_ == DJG_TI || model_ == DJG_OT) {
+                em::fibre_structure(fa, ea_.mat.A);
+                em::unit3(fa, ea_.mat.fa);
+            }
+            if (model_ == DJG_OT) {
+                em::fibre_structure(fb, ea_.mat.B);
+                em::unit3(fb, ea_.mat.fb);
+            }
             ea_.mat.chk = Real(d.c_hg) * Real(d.material.kappa);
         }
         // Constants: built on the device, or AoS chunks -> device planes.
@@ -259,7 +268,10 @@ public:
             CK(cudaMemset(bad.p, 0xff, bad.bytes));
             const unsigned grid = unsigned((E_ + 127) / 128);
 #define DJG_PRE(K, M) k_precompute<Real, K, M><<<grid, 128>>>(a, nrec_, consts_.as<Plane>(), bad.as<unsigned long long>())
-            if (kind_ == DJG_T4) {
+            if (tled_) {
+                if (kind_ == DJG_T4) k_precompute_tled<Real, 0><<<grid, 128>>>(a, consts_.as<Plane>(), bad.as<unsigned long long>());
+                else k_precompute_tled<Real, 1><<<grid, 128>>>(a, consts_.as<Plane>(), bad.as<unsigned long long>());
+            } else if (kind_ == DJG_T4) {
                 switch (model_) {
                     case DJG_NH: DJG_PRE(0, 0); break;
                     case DJG_TI: DJG_PRE(0, 1); break;
@@ -582,7 +594,10 @@ public:
         const unsigned grid = unsigned((e1 - e0 + 127) / 128);
 #define DJG_K1(K, M)                                                                      \
     do {                                                                                  \
-        if (compact_) {                                                                   \
+        if (tled_) {                                                                      \
+            if (rank_bytes_ == 1) k_element_tled<Real, K, M, 1><<<grid, 128, 0, s>>>(a, e0, e1);    \
+            else k_element_tled<Real, K, M, 2><<<grid, 128, 0, s>>>(a, e0, e1);                     \
+        } else if (compact_) {                                                            \
             if (rank_bytes_ == 1) k_element<Real, K, M, 1, true><<<grid, 128, 0, s>>>(a, e0, e1);  \
             else k_element<Real, K, M, 2, true><<<grid, 128, 0, s>>>(a, e0, e1);                   \
         } else {                                                                          \
@@ -782,6 +797,7 @@ public:
         o->precision = int32_t(sizeof(Real));
         o->kernels_per_step = 2 * n_slabs_;
         o->compact = compact_ ? 1 : 0;
+        o->formulation = tled_ ? 1 : 0;
         o->slabs = n_slabs_;
         o->slab_elements = slab_elems_;
         o->sm_count = sms_;
@@ -819,7 +835,7 @@ public:
 private:
     static constexpr int kGraphSteps = 32;
     int kind_ = 0, model_ = 0, npe_ = 4, nconst_ = 0, nrec_ = 0, nplanes_ = 0, policy_ = 0, sms_ = 0;
-    bool compact_ = false;
+    bool compact_ = false, tled_ = false;
     uint32_t flags_ = 0;
     int64_t N_ = 0, E_ = 0, capacity_ = 0;
     cudaStream_t stream_ = nullptr;

@@ -122,6 +122,7 @@ struct MatParams {
     Real dI2;     // c01
     // compact mode / device precompute: what build_element_constants needs
     Real A[6], B[6];  // fibre structure tensors a a^T, b b^T (FibreDirections)
+    Real fa[3], fb[3];  // unit fibre directions (TLED invariants)
     Real chk;         // c_hg * kappa (k_hg = chk * cbrt(V0), precompute.hpp:252)
 };
 
@@ -525,6 +526,244 @@ __global__ void __launch_bounds__(128) k_element(const ElemArgs<Real> A, long lo
     const int phase = int(__ldcg(&A.ctrl->step) % 3);
     const typename RT<Real>::Node* u = A.u_override ? A.u_override : pick3(phase, A.u[0], A.u[1], A.u[2]);
     element_body<Real, KIND, MODEL, RB, COMPACT>(A, e, u);
+}
+
+// ------------------------------------------------------------------ TLED
+
+// The conventional total Lagrangian path the paper compares against
+// (tled_force.hpp): X = I + sum_a u_a B0_a^T, C = X^T X,
+// C^-1, invariants from C, second Piola-Kirchhoff stress, F = X S B0 V0.
+// Same slots, gather and update as the DJ-TLED step; record per element:
+// B0 (npe x 3), V0 [, k_hg, gamma (H8)].
+template <int KIND>
+struct TledLayout {
+    static constexpr int NPE = KIND == 1 ? 8 : 4;
+    static constexpr int V0 = 3 * NPE;
+    static constexpr int khg = V0 + 1;
+    static constexpr int gamma = khg + 1;
+    static constexpr int count = KIND == 1 ? gamma + 32 : V0 + 1;
+};
+
+template <class Real, int KIND, int MODEL, int RB>
+__device__ __forceinline__ void element_body_tled(const ElemArgs<Real>& A, const long long e,
+                                                  const typename RT<Real>::Node* __restrict__ u) {
+    using T = RT<Real>;
+    using TL = TledLayout<KIND>;
+    using L = Layout<KIND, MODEL>;
+    constexpr int NPE = TL::NPE;
+    constexpr int NP = (TL::count + T::kPlane - 1) / T::kPlane;
+    int nid[NPE];
+#pragma unroll
+    for (int p = 0; p < NPE / 4; ++p) {
+        const int4 q = __ldcs(A.conn + (long long)p * A.E + e);
+        nid[4 * p + 0] = q.x; nid[4 * p + 1] = q.y; nid[4 * p + 2] = q.z; nid[4 * p + 3] = q.w;
+    }
+    Real c[NP * T::kPlane];
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        const typename T::Plane v = T::load_plane(A.c + (long long)p * A.E + e);
+        if constexpr (T::kPlane == 4) {
+            c[4 * p + 0] = v.x; c[4 * p + 1] = v.y; c[4 * p + 2] = v.z; c[4 * p + 3] = v.w;
+        } else {
+            c[2 * p + 0] = v.x; c[2 * p + 1] = v.y;
+        }
+    }
+    Real uu[NPE][3];
+#pragma unroll
+    for (int a = 0; a < NPE; ++a) {
+        const typename T::Node v = T::load_node(u + nid[a]);
+        uu[a][0] = v.x; uu[a][1] = v.y; uu[a][2] = v.z;
+    }
+    int sl[NPE];
+    {
+        int rk[NPE];
+        load_ranks<NPE, RB>(A.rank, e, rk);
+#pragma unroll
+        for (int a = 0; a < NPE; ++a) sl[a] = __ldg(A.slice_base + (nid[a] >> 5)) + 32 * rk[a] + (nid[a] & 31);
+    }
+    // deformation_gradient (tled_force.hpp:28-36)
+    Real X[3][3] = {{Real(1), Real(0), Real(0)}, {Real(0), Real(1), Real(0)}, {Real(0), Real(0), Real(1)}};
+#pragma unroll
+    for (int a = 0; a < NPE; ++a)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) X[i][j] += uu[a][i] * c[3 * a + j];
+    // deformation_state (tled_force.hpp:39-48)
+    const Real J = em::det3(X);
+    if (!(J > Real(0))) {
+        atomicAdd(&A.ctrl->inv_count, 1ull);
+        atomicMin(&A.ctrl->first_inv, (unsigned long long)e);
+#pragma unroll
+        for (int a = 0; a < NPE; ++a) store_row(A, sl[a], Real(0), Real(0), Real(0));
+        return;
+    }
+    Real m[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) m[i][j] = X[0][i] * X[0][j] + X[1][i] * X[1][j] + X[2][i] * X[2][j];
+    const Real C[6] = {m[0][0], m[1][1], m[2][2], (m[0][1] + m[1][0]) / 2, (m[0][2] + m[2][0]) / 2,
+                       (m[1][2] + m[2][1]) / 2};
+    const Real Cf[3][3] = {{C[0], C[3], C[4]}, {C[3], C[1], C[5]}, {C[4], C[5], C[2]}};
+    Real ci[3][3];
+    em::inv3(Cf, em::det3(Cf), ci);
+    const Real Ci[6] = {ci[0][0], ci[1][1], ci[2][2], (ci[0][1] + ci[1][0]) / 2, (ci[0][2] + ci[2][0]) / 2,
+                        (ci[1][2] + ci[2][1]) / 2};
+    // conventional_invariants (tled_force.hpp:51-94)
+    const Real cb = ref_cbrt(J);
+    const Real j_m23 = Real(1) / (cb * cb);
+    const Real j_m43 = j_m23 * j_m23;
+    const Real I1 = C[0] + C[1] + C[2];
+    const Real Ib1 = j_m23 * I1;
+    // energy_derivatives + second_pk_stress (material.hpp:266-290, tled_force.hpp:101-135)
+    const Real dJ = A.mat.kappa * (J - Real(1));
+    Real iso[6];
+    const Real ident[6] = {Real(1), Real(1), Real(1), Real(0), Real(0), Real(0)};
+#pragma unroll
+    for (int k = 0; k < 6; ++k) iso[k] = A.mat.dI1 * ident[k];
+    Real dev = A.mat.dI1 * Ib1;
+    if constexpr (L::kI4) {
+        const Real* a = A.mat.fa;
+        Real ca[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) ca[i] = Cf[i][0] * a[0] + Cf[i][1] * a[1] + Cf[i][2] * a[2];
+        const Real Ib4 = j_m23 * (a[0] * ca[0] + a[1] * ca[1] + a[2] * ca[2]);
+        const Real dI4 = A.mat.eta_a * (Ib4 - Real(1));
+#pragma unroll
+        for (int k = 0; k < 6; ++k) iso[k] = iso[k] + dI4 * A.mat.A[k];
+        dev += dI4 * Ib4;
+    }
+    if constexpr (L::kI6) {
+        const Real* b = A.mat.fb;
+        Real cbv[3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) cbv[i] = Cf[i][0] * b[0] + Cf[i][1] * b[1] + Cf[i][2] * b[2];
+        const Real Ib6 = j_m23 * (b[0] * cbv[0] + b[1] * cbv[1] + b[2] * cbv[2]);
+        const Real dI6 = A.mat.eta_b * (Ib6 - Real(1));
+#pragma unroll
+        for (int k = 0; k < 6; ++k) iso[k] = iso[k] + dI6 * A.mat.B[k];
+        dev += dI6 * Ib6;
+    }
+    Real s[6];
+    const Real two_jm23 = 2 * j_m23;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) s[k] = two_jm23 * iso[k];
+    if constexpr (L::kI2) {
+        const Real I2 = (I1 * I1 - em::ddot(C, C)) / 2;
+        const Real Ib2 = j_m43 * I2;
+        const Real ker[6] = {I1 - C[0], I1 - C[1], I1 - C[2], -C[3], -C[4], -C[5]};
+        const Real w = 2 * j_m43 * A.mat.dI2;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) s[k] = s[k] + w * ker[k];
+        dev += 2 * A.mat.dI2 * Ib2;
+    }
+    const Real cc = -Real(2) / Real(3) * dev + J * dJ;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) s[k] = s[k] + cc * Ci[k];
+    // tled_element_force (tled_force.hpp:147-156): F = X S B0 V0
+    const Real Sf[3][3] = {{s[0], s[3], s[4]}, {s[3], s[1], s[5]}, {s[4], s[5], s[2]}};
+    Real P[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) P[i][j] = X[i][0] * Sf[0][j] + X[i][1] * Sf[1][j] + X[i][2] * Sf[2][j];
+    const Real V0 = c[TL::V0];
+    Real f[NPE][3];
+#pragma unroll
+    for (int a = 0; a < NPE; ++a)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+            f[a][i] = V0 * (c[3 * a + 0] * P[i][0] + c[3 * a + 1] * P[i][1] + c[3 * a + 2] * P[i][2]);
+    if constexpr (KIND == 1) {
+        // hourglass_force (djtled_force.hpp:86-95)
+        const Real khg = c[TL::khg];
+        if (khg != Real(0)) {
+#pragma unroll
+            for (int mm = 0; mm < 4; ++mm) {
+                Real q0 = Real(0), q1 = Real(0), q2 = Real(0);
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    const Real gm = c[TL::gamma + 8 * mm + b];
+                    q0 = q0 + gm * uu[b][0];
+                    q1 = q1 + gm * uu[b][1];
+                    q2 = q2 + gm * uu[b][2];
+                }
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    const Real kg = khg * c[TL::gamma + 8 * mm + b];
+                    f[b][0] = f[b][0] + kg * q0;
+                    f[b][1] = f[b][1] + kg * q1;
+                    f[b][2] = f[b][2] + kg * q2;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < NPE; ++a) store_row(A, sl[a], f[a][0], f[a][1], f[a][2]);
+}
+
+template <class Real, int KIND, int MODEL, int RB>
+__global__ void __launch_bounds__(128) k_element_tled(const ElemArgs<Real> A, long long e0, long long e1) {
+    const long long e = e0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= e1) return;
+    if (__ldcg(&A.ctrl->halted)) return;
+    const int phase = int(__ldcg(&A.ctrl->step) % 3);
+    const typename RT<Real>::Node* u = A.u_override ? A.u_override : pick3(phase, A.u[0], A.u[1], A.u[2]);
+    element_body_tled<Real, KIND, MODEL, RB>(A, e, u);
+}
+
+// TledModel::build on the device (tled_force.hpp:167-195).
+template <class Real, int KIND>
+__global__ void k_precompute_tled(const ElemArgs<Real> A, typename RT<Real>::Plane* planes, unsigned long long* bad) {
+    using T = RT<Real>;
+    using TL = TledLayout<KIND>;
+    constexpr int NPE = TL::NPE;
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= A.E) return;
+    int nid[NPE];
+#pragma unroll
+    for (int p = 0; p < NPE / 4; ++p) {
+        const int4 q = A.conn[(long long)p * A.E + e];
+        nid[4 * p + 0] = q.x; nid[4 * p + 1] = q.y; nid[4 * p + 2] = q.z; nid[4 * p + 3] = q.w;
+    }
+    Real x[8][3];
+#pragma unroll
+    for (int a = 0; a < 8; ++a) {
+        if (a < NPE) {
+            const typename T::Node v = T::load_node(A.X + nid[a]);
+            x[a][0] = v.x; x[a][1] = v.y; x[a][2] = v.z;
+        } else {
+            x[a][0] = x[a][1] = x[a][2] = Real(0);
+        }
+    }
+    Real J[3][3], Ji[3][3], det;
+    if (!em::jacobian0(KIND, x, J, Ji, det)) {
+        atomicMin(bad, (unsigned long long)e);
+        return;
+    }
+    constexpr int NR = (TL::count + T::kPlane - 1) / T::kPlane * T::kPlane;
+    Real c[NR];
+#pragma unroll
+    for (int k = 0; k < NR; ++k) c[k] = Real(0);
+    em::tled_b0(KIND, Ji, c);
+    const Real v0 = em::volume0(KIND, det);
+    c[TL::V0] = v0;
+    if constexpr (KIND == 1) {
+        Real gamma[4][8];
+        em::hourglass_vectors(x, Ji, gamma);
+        c[TL::khg] = A.mat.chk * ref_cbrt(v0);
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int a = 0; a < 8; ++a) c[TL::gamma + 8 * m + a] = gamma[m][a];
+    }
+#pragma unroll
+    for (int p = 0; p < NR / T::kPlane; ++p) {
+        Real* dst = reinterpret_cast<Real*>(planes + (long long)p * A.E + e);
+#pragma unroll
+        for (int k = 0; k < T::kPlane; ++k) dst[k] = c[p * T::kPlane + k];
+    }
 }
 
 // ------------------------------------------------------------------ K2+K3

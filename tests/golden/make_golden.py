@@ -49,6 +49,23 @@ def run_fixture(name, kind, model, d, prec, steps, kw):
                         spec=np.array([kind, model, str(d), str(prec), repr(kw)]), **arrs)
 
 
+TLED_RUNS = [
+    ("t4_nh_d3_f32", "T4", "NH", 3, 4, 150),
+    ("h8_ti_d3_f64", "H8", "TI", 3, 8, 150),
+    ("t4_mr_d2_f64", "T4", "MR", 2, 8, 100),
+    ("h8_ot_d2_f32", "H8", "OT", 2, 4, 100),
+]
+
+
+def tled_fixture(name, kind, model, d, prec, steps):
+    """The reference's conventional TLED engine (tled_force.hpp) on the same box."""
+    spec = box_spec(kind=kind, model=model, divisions=d, precision=prec, ramp_steps=steps)
+    u, up, rep = oracle.run(spec, steps, "ref", engine=1)
+    np.savez_compressed(OUT / f"tled_{name}.npz", u=u, up=up, steps=steps,
+                        spec=np.array([kind, model, str(d), str(prec)]),
+                        **{f"rep_{k}": np.array(v) for k, v in rep.items()})
+
+
 def failure_fixtures():
     # Inversion (test_solver.cpp:214-241) under both policies, and divergence
     # (test_solver.cpp:192-212).
@@ -120,6 +137,8 @@ if __name__ == "__main__":
         raise SystemExit("oracle/_ref/libdjref.so missing: run `make -C oracle` where /root/reference exists")
     for r in RUNS:
         run_fixture(*r)
+    for r in TLED_RUNS:
+        tled_fixture(*r)
     failure_fixtures()
     element_fixtures()
     print("wrote", sorted(p.name for p in OUT.glob("*.npz")))

@@ -1,0 +1,71 @@
+"""Conventional TLED on the GPU (tled_force.hpp): the same
+slots, gather and update as the DJ-TLED step with the TLED element kernel.
+Gate: bit-identical to the reference's own TledEngine (oracle/_ref) and to
+its committed fixtures (tests/golden/tled_*.npz)."""
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_2106_14189_b200 import GpuDjEngine, Scenario, box_spec, config_spec
+from paper_2106_14189_b200 import _abi as A
+
+pytestmark = pytest.mark.gpu
+GOLDEN = Path(__file__).resolve().parent / "golden"
+
+
+def run(spec, steps, flags=A.DJG_FLAG_TLED):
+    with GpuDjEngine(Scenario(spec), flags=flags) as eng:
+        rep = eng.step(steps, raise_on_failure=False)
+        u, up, _ = eng.get_state()
+        info = eng.info()
+    return u, up, rep, info
+
+
+@pytest.mark.skipif(not oracle.have("ref"), reason="reference library not built")
+@pytest.mark.parametrize("precision", [4, 8])
+@pytest.mark.parametrize("kind", ["T4", "H8"])
+@pytest.mark.parametrize("model", ["NH", "TI", "OT", "MR"])
+def test_tled_bitwise_vs_reference_tled(kind, model, precision):
+    spec = box_spec(kind=kind, model=model, divisions=4, precision=precision, ramp_steps=300)
+    u, up, rep, info = run(spec, 300)
+    assert info["formulation"] == 1
+    ur, upr, rr = oracle.run(spec, 300, "ref", engine=1)
+    assert rep.status == rr["status"] == 0 and rep.step == rr["step"]
+    assert np.array_equal(u, ur) and np.array_equal(up, upr)
+    assert np.abs(ur).max() > 0.1
+
+
+@pytest.mark.parametrize("path", sorted(GOLDEN.glob("tled_*.npz")), ids=lambda p: p.stem)
+def test_tled_vs_golden(path):
+    g = np.load(path)
+    kind, model, d, prec = g["spec"]
+    steps = int(g["steps"])
+    spec = box_spec(kind=kind, model=model, divisions=int(d), precision=int(prec), ramp_steps=steps)
+    u, up, rep, _ = run(spec, steps)
+    assert np.array_equal(u, g["u"]) and np.array_equal(up, g["up"])
+
+
+@pytest.mark.skipif(not oracle.have("ref"), reason="reference library not built")
+def test_tled_cfg2_and_dj_agree():
+    """cfg2 (H8 NH + hourglass), 1000 steps: TLED == reference TLED bitwise,
+    and DJ-TLED vs TLED within the reference's own DJ/TLED f32 spread
+    (1.8e-6 .. 6.0e-6)."""
+    spec = config_spec("cfg2", precision=4, ramp_steps=2000)
+    u_t, _, _, _ = run(spec, 1000)
+    ur, _, _ = oracle.run(spec, 1000, "ref", engine=1)
+    assert np.array_equal(u_t, ur)
+    u_d, _, _, _ = run(spec, 1000, flags=0)
+    assert oracle.rel_max_err(u_d, u_t) < 1e-5
+
+
+def test_tled_inversion_semantics():
+    spec = box_spec(kind="T4", divisions=1, extent=(0.1, 0.1, 0.1), precision=8, target=-0.5, dt=1e-4,
+                    alpha=0.0, ramp_steps=1)
+    u, up, rep, _ = run(spec, 100)
+    assert rep.status == A.DJG_E_INVERSION and rep.first_inverted >= 0
+    if oracle.have("ref"):
+        ur, upr, rr = oracle.run(spec, 100, "ref", engine=1)
+        assert (rep.first_inverted, rep.fail_step) == (rr["first_inverted"], rr["fail_step"])
+        assert np.array_equal(u, ur)

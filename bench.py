@@ -301,9 +301,27 @@ def our_arm(args):
     line = _line(args, 1, K, W, E, ms_step, value, {k: v for k, v in extra.items() if k != "config"})
     line["config"]["num_nodes"] = N
     line["config"]["l2"] = "inputs larger than L2 (state %.1f GB resident)" % (info["device_bytes"] / 1e9)
+    eng.close()
+    # The paper's comparison path on the same problem: conventional TLED
+    # element forces with the same gather/update (DJG_FLAG_TLED), graph replay.
+    if args.tled_steps > 0:
+        from paper_2106_14189_b200 import _abi as A
+        with GpuDjEngine(sc, device=device, flags=A.DJG_FLAG_TLED) as teng:
+            teng.step(W)
+            ts = torch.cuda.ExternalStream(teng.stream)
+            t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            t0e.record(ts)
+            teng.step_async(args.tled_steps)
+            t1e.record(ts)
+            t1e.synchronize()
+            trep = teng.sync()
+        tled_ms = t0e.elapsed_time(t1e) / args.tled_steps
+        line["tled"] = {"ms_per_step": tled_ms, "value": E / (tled_ms * 1e-3), "unit": UNIT,
+                        "dj_over_tled_time": ms_step / tled_ms, "status": trep.status,
+                        "note": "paper Table 5 ratio (CPU: 0.70-0.88); same problem, DJG_FLAG_TLED"}
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = _cpu_baseline_line(args)
-    eng.close()
     sc.close()
     print(json.dumps(line), flush=True)
 
@@ -381,6 +399,7 @@ def main():
     ap.add_argument("--divisions", type=int, default=203)
     ap.add_argument("--precision", type=int, default=4, choices=[4, 8])
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--tled-steps", type=int, default=100)
     ap.add_argument("--cpu-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -95,6 +95,8 @@ typedef struct djg_desc {
                                     defaults to the compact record) */
 #define DJG_FLAG_TLED 64u        /* conventional TLED element forces (tled_force.hpp), the
                                     paper's comparison path; record built on the device */
+#define DJG_FLAG_NO_PIPE 128u    /* one-shot element kernel instead of the bulk-copy
+                                    pipelined one (k_element_pipe); bit-identical */
 
 /* DjEngine(mesh, material, c_hg) (solver.hpp:264-267) at the mesh level:
  * the library runs the precompute (build_element_constants,
@@ -208,7 +210,7 @@ typedef struct djg_engine_info {
     int32_t compact;            /* 1: compact per-element record in HBM */
     int64_t slab_elements;      /* elements per slab */
     int32_t formulation;        /* 0 DJ-TLED, 1 TLED (DJG_FLAG_TLED) */
-    int32_t _pad1;
+    int32_t pipelined;          /* element kernel streams tiles through shared memory */
 } djg_engine_info;
 int djg_get_info(djg_engine* eng, djg_engine_info* info);
 

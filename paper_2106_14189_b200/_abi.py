@@ -13,7 +13,8 @@ from pathlib import Path
 import numpy as np
 
 PKG_DIR = Path(__file__).resolve().parent
-LIB_PATH = PKG_DIR / "_build" / "libdjg.so"
+# DJG_LIB_PATH: developer A/B override (tools/); default the in-tree build.
+LIB_PATH = Path(os.environ.get("DJG_LIB_PATH") or PKG_DIR / "_build" / "libdjg.so")
 
 DJG_T4, DJG_H8 = 0, 1
 DJG_NH, DJG_TI, DJG_OT, DJG_MR = 0, 1, 2, 3
@@ -27,6 +28,7 @@ DJG_FLAG_COMPACT = 8
 DJG_FLAG_DEVICE_PRECOMPUTE = 16
 DJG_FLAG_FULL_RECORD = 32
 DJG_FLAG_TLED = 64
+DJG_FLAG_NO_PIPE = 128
 
 KIND_NAMES = {"T4": DJG_T4, "H8": DJG_H8}
 MODEL_NAMES = {"NH": DJG_NH, "TI": DJG_TI, "OT": DJG_OT, "MR": DJG_MR}
@@ -152,7 +154,7 @@ class djg_engine_info(C.Structure):
         ("slot_capacity", C.c_int64), ("device_bytes", C.c_int64),
         ("npe", C.c_int32), ("nconst", C.c_int32), ("const_planes", C.c_int32), ("precision", C.c_int32),
         ("kernels_per_step", C.c_int32), ("sm_count", C.c_int32), ("slabs", C.c_int32),
-        ("compact", C.c_int32), ("slab_elements", C.c_int64), ("formulation", C.c_int32), ("_pad1", C.c_int32),
+        ("compact", C.c_int32), ("slab_elements", C.c_int64), ("formulation", C.c_int32), ("pipelined", C.c_int32),
     ]
 
 

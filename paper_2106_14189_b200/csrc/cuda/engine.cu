@@ -31,6 +31,18 @@
 namespace djg {
 namespace {
 
+// k_element_pipe: stages per block and the largest tile stage it is used for
+// (bigger records -- H8 full, MR -- keep the one-shot kernel).
+#ifndef DJG_PIPE_STAGES
+#define DJG_PIPE_STAGES 3
+#endif
+#ifndef DJG_PIPE_MAX_STAGE_KB
+#define DJG_PIPE_MAX_STAGE_KB 32
+#endif
+
+constexpr int kPipeStages = DJG_PIPE_STAGES;
+constexpr int kPipeMaxStageBytes = DJG_PIPE_MAX_STAGE_KB * 1024;
+
 thread_local std::string g_create_error;
 
 struct CudaError : std::runtime_error {
@@ -123,7 +135,12 @@ public:
         const bool dev_pre = tled_ || (flags_ & DJG_FLAG_DEVICE_PRECOMPUTE) != 0;
         nrec_ = tled_ ? (kind_ == DJG_H8 ? TledLayout<1>::count : TledLayout<0>::count)
                       : compact_ ? (kind_ == DJG_H8 ? kCompactLen<1> : kCompactLen<0>) : nconst_;
-        nplanes_ = (nrec_ + T::kPlane - 1) / T::kPlane;
+        // The compact T4 record (J0, 9 Reals) keeps its remainder in scalar
+        // tail planes instead of a padded 16-byte plane.
+        const bool tail = compact_ && kind_ == DJG_T4;
+        nplanes_ = tail ? nrec_ / T::kPlane : (nrec_ + T::kPlane - 1) / T::kPlane;
+        ntail_ = tail ? nrec_ % T::kPlane : 0;
+        tail_stride_ = (E_ + 3) / 4 * 4 + 4;  // 16-byte aligned planes, tail tiles may round up
         if (d.nconst != nconst_) throw DescError("nconst does not match djg_const_count(kind, model)");
         if (N_ < 1 || E_ < 1) throw DescError("mesh must have nodes and elements");
         if (!d.conn) throw DescError("descriptor is missing conn");
@@ -213,8 +230,8 @@ public:
                 }
             slicebase_.alloc(slice_base_.size() * sizeof(int32_t));
             CK(cudaMemcpy(slicebase_.p, slice_base_.data(), slicebase_.bytes, cudaMemcpyHostToDevice));
-            rank_.alloc(ranks.size());
-            CK(cudaMemcpy(rank_.p, ranks.data(), rank_.bytes, cudaMemcpyHostToDevice));
+            rank_.alloc(ranks.size() + 16);  // + 16: bulk copies of a tail tile round up to 16 bytes
+            CK(cudaMemcpy(rank_.p, ranks.data(), ranks.size(), cudaMemcpyHostToDevice));
         }
         plan_slabs(off, celem);
 
@@ -256,10 +273,12 @@ public:
             ea_.mat.chk = Real(d.c_hg) * Real(d.material.kappa);
         }
         // Constants: built on the device, or AoS chunks -> device planes.
-        consts_.alloc(size_t(nplanes_) * size_t(E_) * sizeof(Plane));
+        consts_.alloc(size_t(nplanes_) * size_t(E_) * sizeof(Plane) + size_t(ntail_) * size_t(tail_stride_) * sizeof(Real));
+        Real* const ctail = reinterpret_cast<Real*>(consts_.as<Plane>() + size_t(nplanes_) * size_t(E_));
         if (dev_pre) {
             ElemArgs<Real> a{};
             a.E = E_;
+            a.tail_stride = tail_stride_;
             a.conn = conn_.as<int4>();
             a.X = X_.as<Node>();
             a.mat = ea_.mat;
@@ -267,7 +286,8 @@ public:
             bad.alloc(sizeof(unsigned long long));
             CK(cudaMemset(bad.p, 0xff, bad.bytes));
             const unsigned grid = unsigned((E_ + 127) / 128);
-#define DJG_PRE(K, M) k_precompute<Real, K, M><<<grid, 128>>>(a, nrec_, consts_.as<Plane>(), bad.as<unsigned long long>())
+#define DJG_PRE(K, M) \
+    k_precompute<Real, K, M><<<grid, 128>>>(a, nrec_, nplanes_, consts_.as<Plane>(), ctail, bad.as<unsigned long long>())
             if (tled_) {
                 if (kind_ == DJG_T4) k_precompute_tled<Real, 0><<<grid, 128>>>(a, consts_.as<Plane>(), bad.as<unsigned long long>());
                 else k_precompute_tled<Real, 1><<<grid, 128>>>(a, consts_.as<Plane>(), bad.as<unsigned long long>());
@@ -301,9 +321,10 @@ public:
                 const int64_t ne = std::min(chunk, E_ - e0);
                 CK(cudaMemcpy(stage.p, src + e0 * nconst_, size_t(ne) * nconst_ * sizeof(Real),
                               cudaMemcpyHostToDevice));
-                const int64_t work = ne * nplanes_;
+                const int64_t work = ne * (nplanes_ + ntail_);
                 k_transpose_consts<Real><<<unsigned((work + 255) / 256), 256>>>(
-                    stage.as<Real>(), nconst_, nrec_, nconst_ - 33, e0, ne, E_, nplanes_, consts_.as<Real>());
+                    stage.as<Real>(), nconst_, nrec_, kind_ == DJG_H8 ? nconst_ - 33 : -1, e0, ne, E_, nplanes_,
+                    consts_.as<Real>(), ctail, tail_stride_, ntail_);
                 CK(cudaGetLastError());
             }
             CK(cudaDeviceSynchronize());
@@ -330,6 +351,8 @@ public:
         ea_.rank = rank_.p;
         ea_.slice_base = slicebase_.as<int>();
         ea_.c = consts_.as<Plane>();
+        ea_.ctail = reinterpret_cast<const Real*>(consts_.as<Plane>() + size_t(nplanes_) * size_t(E_));
+        ea_.tail_stride = tail_stride_;
         for (int i = 0; i < 3; ++i) ea_.u[i] = u_[i].as<Node>();
         ea_.u_override = nullptr;
         ea_.ef = ef_.as<Node>();
@@ -358,6 +381,8 @@ public:
             configure(static_cast<const Real*>(d.c1), d.massless, d.dof_kind, static_cast<const Real*>(d.dof_target),
                       static_cast<const Real*>(d.dof_t_total), Real(d.c2), Real(d.c3), Real(d.dt));
         }
+        pipe_ = !(flags_ & DJG_FLAG_NO_PIPE) && n_slabs_ == 1;
+        if (pipe_) launch_element(stream_, 0, E_, nullptr, /*setup=*/true);
         set_state(nullptr, nullptr, 0);
     }
 
@@ -588,22 +613,65 @@ public:
         if (step) *step = hctrl_->step;
     }
 
-    void launch_element(cudaStream_t s, int64_t e0, int64_t e1, const Node* u_override = nullptr) {
+    // Pipelined element kernel (k_element_pipe) for shapes whose tile stage
+    // is small enough to keep several stages and blocks per SM; setup = true
+    // only sizes the persistent grid. Returns false if the shape has none.
+    template <int K, int M, int RB, int FORM>
+    bool launch_pipe(cudaStream_t s, const ElemArgs<Real>& a, int64_t e0, int64_t e1, bool setup) {
+        using PS = PipeShape<Real, K, M, RB, FORM>;
+        if constexpr (PS::kStageBytes > kPipeMaxStageBytes) {
+            return false;
+        } else {
+            constexpr int ST = kPipeStages;
+            auto kern = k_element_pipe<Real, K, M, RB, FORM, ST>;
+            const size_t smem = PS::smem_bytes(ST);
+            if (setup) {
+                CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+                int nb = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kPipeThreads, smem));
+                pipe_blocks_sm_ = nb;
+                pipe_smem_ = smem;
+                return nb > 0;
+            }
+            const int64_t tiles = (e1 - e0 + kPipeTile - 1) / kPipeTile;
+            const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(pipe_blocks_sm_) * sms_)));
+            kern<<<grid, kPipeThreads, smem, s>>>(a, e0, e1);
+            return true;
+        }
+    }
+
+    void launch_element(cudaStream_t s, int64_t e0, int64_t e1, const Node* u_override = nullptr,
+                        bool setup = false) {
         ElemArgs<Real> a = ea_;
         a.u_override = u_override;
         const unsigned grid = unsigned((e1 - e0 + 127) / 128);
-#define DJG_K1(K, M)                                                                      \
-    do {                                                                                  \
-        if (tled_) {                                                                      \
-            if (rank_bytes_ == 1) k_element_tled<Real, K, M, 1><<<grid, 128, 0, s>>>(a, e0, e1);    \
-            else k_element_tled<Real, K, M, 2><<<grid, 128, 0, s>>>(a, e0, e1);                     \
-        } else if (compact_) {                                                            \
-            if (rank_bytes_ == 1) k_element<Real, K, M, 1, true><<<grid, 128, 0, s>>>(a, e0, e1);  \
-            else k_element<Real, K, M, 2, true><<<grid, 128, 0, s>>>(a, e0, e1);                   \
-        } else {                                                                          \
-            if (rank_bytes_ == 1) k_element<Real, K, M, 1, false><<<grid, 128, 0, s>>>(a, e0, e1); \
-            else k_element<Real, K, M, 2, false><<<grid, 128, 0, s>>>(a, e0, e1);                  \
-        }                                                                                 \
+        const int form = tled_ ? 2 : compact_ ? 1 : 0;
+#define DJG_K1(K, M)                                                                                            \
+    do {                                                                                                        \
+        if (pipe_) {                                                                                            \
+            bool ok;                                                                                            \
+            if (rank_bytes_ == 1)                                                                               \
+                ok = form == 2 ? launch_pipe<K, M, 1, 2>(s, a, e0, e1, setup)                                   \
+                               : form == 1 ? launch_pipe<K, M, 1, 1>(s, a, e0, e1, setup)                       \
+                                           : launch_pipe<K, M, 1, 0>(s, a, e0, e1, setup);                      \
+            else                                                                                                \
+                ok = form == 2 ? launch_pipe<K, M, 2, 2>(s, a, e0, e1, setup)                                   \
+                               : form == 1 ? launch_pipe<K, M, 2, 1>(s, a, e0, e1, setup)                       \
+                                           : launch_pipe<K, M, 2, 0>(s, a, e0, e1, setup);                      \
+            if (setup) { pipe_ = ok; return; }                                                                  \
+            if (ok) break;                                                                                      \
+        }                                                                                                       \
+        if (setup) return;                                                                                      \
+        if (tled_) {                                                                                            \
+            if (rank_bytes_ == 1) k_element_tled<Real, K, M, 1><<<grid, 128, 0, s>>>(a, e0, e1);                \
+            else k_element_tled<Real, K, M, 2><<<grid, 128, 0, s>>>(a, e0, e1);                                 \
+        } else if (compact_) {                                                                                  \
+            if (rank_bytes_ == 1) k_element<Real, K, M, 1, true><<<grid, 128, 0, s>>>(a, e0, e1);               \
+            else k_element<Real, K, M, 2, true><<<grid, 128, 0, s>>>(a, e0, e1);                                \
+        } else {                                                                                                \
+            if (rank_bytes_ == 1) k_element<Real, K, M, 1, false><<<grid, 128, 0, s>>>(a, e0, e1);              \
+            else k_element<Real, K, M, 2, false><<<grid, 128, 0, s>>>(a, e0, e1);                               \
+        }                                                                                                       \
     } while (0)
         if (kind_ == DJG_T4) {
             switch (model_) {
@@ -798,6 +866,7 @@ public:
         o->kernels_per_step = 2 * n_slabs_;
         o->compact = compact_ ? 1 : 0;
         o->formulation = tled_ ? 1 : 0;
+        o->pipelined = pipe_ ? 1 : 0;
         o->slabs = n_slabs_;
         o->slab_elements = slab_elems_;
         o->sm_count = sms_;
@@ -806,12 +875,15 @@ public:
     // Test hook: the device constant planes as an AoS record (E x nrec Reals).
     int64_t consts_out(void* out) override {
         if (!out) return nrec_;
-        std::vector<Real> planes(size_t(nplanes_) * size_t(E_) * size_t(T::kPlane));
+        std::vector<Real> planes(consts_.bytes / sizeof(Real));
         CK(cudaMemcpy(planes.data(), consts_.p, consts_.bytes, cudaMemcpyDeviceToHost));
+        const Real* tail = planes.data() + size_t(nplanes_) * size_t(E_) * size_t(T::kPlane);
         Real* o = static_cast<Real*>(out);
+        const int nf = nplanes_ * T::kPlane;
         for (int64_t e = 0; e < E_; ++e)
             for (int f = 0; f < nrec_; ++f)
-                o[e * nrec_ + f] = planes[size_t((int64_t(f / T::kPlane) * E_ + e) * T::kPlane + f % T::kPlane)];
+                o[e * nrec_ + f] = f < nf ? planes[size_t((int64_t(f / T::kPlane) * E_ + e) * T::kPlane + f % T::kPlane)]
+                                          : tail[size_t(int64_t(f - nf) * tail_stride_ + e)];
         return nrec_;
     }
 
@@ -834,8 +906,11 @@ public:
 
 private:
     static constexpr int kGraphSteps = 32;
-    int kind_ = 0, model_ = 0, npe_ = 4, nconst_ = 0, nrec_ = 0, nplanes_ = 0, policy_ = 0, sms_ = 0;
-    bool compact_ = false, tled_ = false;
+    int kind_ = 0, model_ = 0, npe_ = 4, nconst_ = 0, nrec_ = 0, nplanes_ = 0, ntail_ = 0, policy_ = 0, sms_ = 0;
+    int64_t tail_stride_ = 0;
+    bool compact_ = false, tled_ = false, pipe_ = false;
+    int pipe_blocks_sm_ = 0;
+    size_t pipe_smem_ = 0;
     uint32_t flags_ = 0;
     int64_t N_ = 0, E_ = 0, capacity_ = 0;
     cudaStream_t stream_ = nullptr;

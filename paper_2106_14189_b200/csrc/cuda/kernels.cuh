@@ -20,6 +20,7 @@
 #pragma once
 
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 
 #include "../common/element_math.hpp"
@@ -134,6 +135,8 @@ struct ElemArgs {
                                          // in its nodes' CSR rows, packed in one 4/8/16-byte word
     const int* slice_base;               // first slot of each 32-node slice
     const typename RT<Real>::Plane* c;   // nplanes planes of Plane[E]
+    const Real* ctail;                   // record remainder planes (compact T4): Real[tail_stride]
+    long long tail_stride;
     const typename RT<Real>::Node* u[3]; // triple-buffered displacement
     const typename RT<Real>::Node* u_override;
     const typename RT<Real>::Node* X;    // reference coordinates (compact H8, device precompute)
@@ -227,25 +230,28 @@ __device__ __forceinline__ void store_row(const ElemArgs<Real>& A, int pos, Real
     RT<Real>::store_node(A.ef + pos, x, y, z);
 }
 
-// Ranks of element e in its nodes' CSR rows (RB bytes each).
+// Ranks of element e in its nodes' CSR rows (RB bytes each), packed in one
+// 4 / 8 / 16-byte word per element.
 template <int NPE, int RB>
-__device__ __forceinline__ void load_ranks(const void* base, long long e, int (&rk)[NPE]) {
+struct RankWord {
+    using type = typename std::conditional<NPE * RB == 4, unsigned,
+                                           typename std::conditional<NPE * RB == 8, uint2, uint4>::type>::type;
+};
+
+template <int NPE, int RB>
+__device__ __forceinline__ void decode_ranks(const typename RankWord<NPE, RB>::type w, int (&rk)[NPE]) {
     if constexpr (NPE == 4 && RB == 1) {
-        const unsigned w = __ldcs(static_cast<const unsigned*>(base) + e);
 #pragma unroll
         for (int a = 0; a < 4; ++a) rk[a] = (w >> (8 * a)) & 0xff;
     } else if constexpr (NPE == 8 && RB == 1) {
-        const uint2 w = __ldcs(static_cast<const uint2*>(base) + e);
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
             rk[a] = (w.x >> (8 * a)) & 0xff;
             rk[4 + a] = (w.y >> (8 * a)) & 0xff;
         }
     } else if constexpr (NPE == 4) {
-        const uint2 w = __ldcs(static_cast<const uint2*>(base) + e);
         rk[0] = w.x & 0xffff; rk[1] = w.x >> 16; rk[2] = w.y & 0xffff; rk[3] = w.y >> 16;
     } else {
-        const uint4 w = __ldcs(static_cast<const uint4*>(base) + e);
         const unsigned v[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
@@ -255,17 +261,135 @@ __device__ __forceinline__ void load_ranks(const void* base, long long e, int (&
     }
 }
 
-// Compact record kept in HBM: J0 (9), det J0, V0, pad -- and for H8 the
-// hourglass data k_hg, gamma (32) after it (cheap to store, costly to
-// rebuild: it needs the coordinates and a cube root).
+template <int NPE, int RB>
+__device__ __forceinline__ void load_ranks(const void* base, long long e, int (&rk)[NPE]) {
+    using W = typename RankWord<NPE, RB>::type;
+    decode_ranks<NPE, RB>(__ldcs(static_cast<const W*>(base) + e), rk);
+}
+
+// Slot of element-node (n, rank k): slice_base[n/32] + 32 k + n%32.
+__device__ __forceinline__ int slot_of(const int* __restrict__ slice_base, int n, int k) {
+    return __ldg(slice_base + (n >> 5)) + 32 * k + (n & 31);
+}
+
+// Where element_body takes its streamed per-element inputs from: straight
+// from HBM (GlobalSrc), or from a shared-memory stage filled by bulk async
+// copies (SmemSrc, k_element_pipe).
+template <class Real>
+struct GlobalSrc {
+    const ElemArgs<Real>& A;
+    long long e;
+    __device__ __forceinline__ int4 conn(int p) const { return __ldcs(A.conn + (long long)p * A.E + e); }
+    __device__ __forceinline__ typename RT<Real>::Plane plane(int p) const {
+        return RT<Real>::load_plane(A.c + (long long)p * A.E + e);
+    }
+    template <int NPE, int RB>
+    __device__ __forceinline__ void ranks(int (&rk)[NPE]) const { load_ranks<NPE, RB>(A.rank, e, rk); }
+    __device__ __forceinline__ typename RT<Real>::Node node(int, const typename RT<Real>::Node* __restrict__ u,
+                                                            int n) const {
+        return RT<Real>::load_node(u + n);
+    }
+    __device__ __forceinline__ int slot(const int* __restrict__ sb, int, int n, int k) const { return slot_of(sb, n, k); }
+    __device__ __forceinline__ Real tail(int t) const { return __ldcs(A.ctail + t * A.tail_stride + e); }
+};
+
+template <class Real, int TILE>
+struct SmemSrc {
+    const int4* sconn;                   // [NPE/4][TILE]
+    const typename RT<Real>::Plane* srec;  // [planes][TILE]
+    const void* srank;                   // [TILE] rank words
+    const Real* stail;                   // [NTAIL][TILE] record remainder
+    int i;
+    __device__ __forceinline__ typename RT<Real>::Node node(int, const typename RT<Real>::Node* __restrict__ u,
+                                                            int n) const {
+        return RT<Real>::load_node(u + n);
+    }
+    __device__ __forceinline__ int4 conn(int p) const { return sconn[p * TILE + i]; }
+    __device__ __forceinline__ typename RT<Real>::Plane plane(int p) const { return srec[p * TILE + i]; }
+    template <int NPE, int RB>
+    __device__ __forceinline__ void ranks(int (&rk)[NPE]) const {
+        using W = typename RankWord<NPE, RB>::type;
+        decode_ranks<NPE, RB>(static_cast<const W*>(srank)[i], rk);
+    }
+    __device__ __forceinline__ int slot(const int* __restrict__ sb, int, int n, int k) const { return slot_of(sb, n, k); }
+    __device__ __forceinline__ Real tail(int t) const { return stail[t * TILE + i]; }
+};
+
+// Gathered inputs of one element, loaded one tile ahead of its computation
+// (k_element_pipe): nodal displacements and slot positions.
+template <class Real, int NPE>
+struct Prefetched {
+    Real ux[NPE], uy[NPE], uz[NPE];
+    int sl[NPE];
+};
+
+template <class Real, int NPE, int RB, int TILE>
+__device__ __forceinline__ void prefetch_element(const ElemArgs<Real>& A, const SmemSrc<Real, TILE>& src,
+                                                 const typename RT<Real>::Node* __restrict__ u,
+                                                 Prefetched<Real, NPE>& p) {
+    int nid[NPE], rk[NPE];
+#pragma unroll
+    for (int q = 0; q < NPE / 4; ++q) {
+        const int4 c = src.conn(q);
+        nid[4 * q + 0] = c.x; nid[4 * q + 1] = c.y; nid[4 * q + 2] = c.z; nid[4 * q + 3] = c.w;
+    }
+    src.template ranks<NPE, RB>(rk);
+#pragma unroll
+    for (int a = 0; a < NPE; ++a) {
+        const typename RT<Real>::Node v = RT<Real>::load_node(u + nid[a]);
+        p.ux[a] = v.x; p.uy[a] = v.y; p.uz[a] = v.z;
+        p.sl[a] = slot_of(A.slice_base, nid[a], rk[a]);
+    }
+}
+
+// Record planes from the shared-memory stage, everything gathered from
+// registers filled by prefetch_element.
+template <class Real, int NPE, int TILE>
+struct PrefetchedSrc {
+    const Prefetched<Real, NPE>& p;
+    const typename RT<Real>::Plane* srec;
+    const Real* stail;
+    int i;
+    __device__ __forceinline__ int4 conn(int) const { return make_int4(0, 0, 0, 0); }
+    __device__ __forceinline__ typename RT<Real>::Plane plane(int q) const { return srec[q * TILE + i]; }
+    template <int N, int RB>
+    __device__ __forceinline__ void ranks(int (&rk)[N]) const {
+#pragma unroll
+        for (int a = 0; a < N; ++a) rk[a] = 0;
+    }
+    __device__ __forceinline__ typename RT<Real>::Node node(int a, const typename RT<Real>::Node*, int) const {
+        typename RT<Real>::Node v;
+        v.x = p.ux[a]; v.y = p.uy[a]; v.z = p.uz[a];
+        return v;
+    }
+    __device__ __forceinline__ int slot(const int*, int a, int, int) const { return p.sl[a]; }
+    __device__ __forceinline__ Real tail(int t) const { return stail[t * TILE + i]; }
+};
+
+// Compact record kept in HBM. T4: J0 only (9) -- det J0 and V0 are the
+// precompute's own functions of J0 (det3, volume0), recomputed bitwise.
+// H8: J0, det J0, V0, pad, then the hourglass data k_hg, gamma (32) (cheap
+// to store, costly to rebuild: it needs the coordinates and a cube root).
 constexpr int kCompactRecord = 12;
 template <int KIND>
-constexpr int kCompactLen = KIND == 1 ? kCompactRecord + 33 : kCompactRecord;
+constexpr int kCompactLen = KIND == 1 ? kCompactRecord + 33 : 9;
+
+// Storage of a record of LEN Reals: NFULL 16-byte planes [E], and -- only for
+// the compact T4 record, whose 9 Reals would leave a padded plane -- NTAIL
+// scalar planes [tail_stride] for the remainder.
+template <class Real, int LEN, bool TAIL>
+struct RecPlanes {
+    static constexpr int W = RT<Real>::kPlane;
+    static constexpr int NFULL = TAIL ? LEN / W : (LEN + W - 1) / W;
+    static constexpr int NTAIL = TAIL ? LEN % W : 0;
+};
+template <int KIND, bool COMPACT>
+constexpr bool kTailRecord = COMPACT && KIND == 0;
 
 // One element: loads, DJ-TLED force, stores of its npe rows into their slots.
-template <class Real, int KIND, int MODEL, int RB, bool COMPACT>
+template <class Real, int KIND, int MODEL, int RB, bool COMPACT, class Src>
 __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long long e,
-                                             const typename RT<Real>::Node* __restrict__ u) {
+                                             const typename RT<Real>::Node* __restrict__ u, const Src& src) {
     using L = Layout<KIND, MODEL>;
     using T = RT<Real>;
     constexpr int NPE = L::NPE;
@@ -275,31 +399,50 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
     int nid[NPE];
 #pragma unroll
     for (int p = 0; p < NPE / 4; ++p) {
-        const int4 q = __ldcs(A.conn + (long long)p * A.E + e);
+        const int4 q = src.conn(p);
         nid[4 * p + 0] = q.x; nid[4 * p + 1] = q.y; nid[4 * p + 2] = q.z; nid[4 * p + 3] = q.w;
     }
-    // Hot constants: the full record from HBM, or (compact) J0, det J0, V0
-    // from HBM and the rest rebuilt here with the precompute's own arithmetic.
-    constexpr int NCR = kCompactLen<KIND>;
-    constexpr int NC = COMPACT ? (NCR + T::kPlane - 1) / T::kPlane * T::kPlane : NP * T::kPlane;
+    // Gathered displacements of the element's nodes (issued first: their
+    // latency overlaps the record loads and the compact rebuild).
+    Real ux[NPE], uy[NPE], uz[NPE];
+#pragma unroll
+    for (int a = 0; a < NPE; ++a) {
+        const typename T::Node v = src.node(a, u, nid[a]);
+        ux[a] = v.x; uy[a] = v.y; uz[a] = v.z;
+    }
+
+    // Hot constants: the full record from HBM, or (compact) J0 [, det J0, V0,
+    // hourglass data] from HBM and the rest rebuilt here with the
+    // precompute's own arithmetic.
+    constexpr int NCR = COMPACT ? kCompactLen<KIND> : L::count;
+    using RP = RecPlanes<Real, NCR, kTailRecord<KIND, COMPACT>>;
+    constexpr int NC = RP::NFULL * T::kPlane + RP::NTAIL;
     Real r[NC];
 #pragma unroll
-    for (int p = 0; p < NC / T::kPlane; ++p) {
-        const typename T::Plane v = T::load_plane(A.c + (long long)p * A.E + e);
+    for (int p = 0; p < RP::NFULL; ++p) {
+        const typename T::Plane v = src.plane(p);
         if constexpr (T::kPlane == 4) {
             r[4 * p + 0] = v.x; r[4 * p + 1] = v.y; r[4 * p + 2] = v.z; r[4 * p + 3] = v.w;
         } else {
             r[2 * p + 0] = v.x; r[2 * p + 1] = v.y;
         }
     }
+#pragma unroll
+    for (int t = 0; t < RP::NTAIL; ++t) r[RP::NFULL * T::kPlane + t] = src.tail(t);
     Real c[COMPACT ? L::count + 1 : NC];
     if constexpr (!COMPACT) {
 #pragma unroll
         for (int k = 0; k < NC; ++k) c[k] = r[k];
     } else {
+        if constexpr (KIND == 0) {
 #pragma unroll
-        for (int k = 0; k < 11; ++k) c[k] = r[k];
-        if constexpr (L::kH8) {
+            for (int k = 0; k < 9; ++k) c[k] = r[k];
+            const Real J0[3][3] = {{c[0], c[1], c[2]}, {c[3], c[4], c[5]}, {c[6], c[7], c[8]}};
+            c[9] = em::det3(J0);                 // jacobian0 (element.hpp:59-77)
+            c[10] = em::volume0(KIND, c[9]);     // volume0 (element.hpp:80-85)
+        } else {
+#pragma unroll
+            for (int k = 0; k < 11; ++k) c[k] = r[k];
 #pragma unroll
             for (int k = 0; k < 33; ++k) c[L::khg + k] = r[kCompactRecord + k];
         }
@@ -311,14 +454,6 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
         if constexpr (L::kI6) em::fibre_tensors(J0i, c[10], A.mat.B, c + L::m6, c + L::I6m);
         if constexpr (L::kI2) em::second_invariant_tensors(J0i, c[10], c + 11, c + L::M2, c + L::I2m);
     }
-    // Gathered displacements of the element's nodes.
-    Real ux[NPE], uy[NPE], uz[NPE];
-#pragma unroll
-    for (int a = 0; a < NPE; ++a) {
-        const typename T::Node v = T::load_node(u + nid[a]);
-        ux[a] = v.x; uy[a] = v.y; uz[a] = v.z;
-    }
-
     // update_jacobian (kinematics.hpp:31-45): Jt = J0 + D U.
     Real Jt[3][3];
     if constexpr (KIND == 0) {
@@ -359,11 +494,30 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
     int sl[NPE];  // slot positions fit in 32 bits (checked at engine creation)
     {
         int rk[NPE];
-        load_ranks<NPE, RB>(A.rank, e, rk);
+        src.template ranks<NPE, RB>(rk);
 #pragma unroll
-        for (int a = 0; a < NPE; ++a) sl[a] = __ldg(A.slice_base + (nid[a] >> 5)) + 32 * rk[a] + (nid[a] & 31);
+        for (int a = 0; a < NPE; ++a) sl[a] = src.slot(A.slice_base, a, nid[a], rk[a]);
     }
 
+#if defined(DJG_EXP) && (DJG_EXP & 1)
+    if constexpr (KIND == 0) {  // timing experiment: memory traffic only
+        Real K[3][3];
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) K[i][j] = (Jt[i][j] * c[9 + (i + j) % 3] + det) * Real(1e-30);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+#if DJG_EXP & 2
+            const int p = int(4 * e + a);
+#else
+            const int p = sl[a];
+#endif
+            store_row(A, p, K[a % 3][0], K[a % 3][1], K[a % 3][2]);
+        }
+        return;
+    }
+#endif
     if (!(det > Real(0))) {
         // record_inversion (djtled_force.hpp:107-112) + zeroed rows (:187-191).
         atomicAdd(&A.ctrl->inv_count, 1ull);
@@ -462,6 +616,17 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
             K[i][j] = j_m23 * mt + cc * Ji[i][j];
         }
 
+#if defined(DJG_EXP) && (DJG_EXP & 2)
+    if constexpr (KIND == 0) {  // timing experiment: sequential stores
+        const int p = int(4 * e);
+        store_row(A, p + 1, K[0][0], K[1][0], K[2][0]);
+        store_row(A, p + 2, K[0][1], K[1][1], K[2][1]);
+        store_row(A, p + 3, K[0][2], K[1][2], K[2][2]);
+        store_row(A, p, Real(-1) * ((K[0][0] + K[0][1]) + K[0][2]), Real(-1) * ((K[1][0] + K[1][1]) + K[1][2]),
+                  Real(-1) * ((K[2][0] + K[2][1]) + K[2][2]));
+        return;
+    }
+#endif
     if constexpr (KIND == 0) {
         // T4 rows: f1..f3 = columns of K, f0 = -(f1 + f2 + f3).
         store_row(A, sl[1], K[0][0], K[1][0], K[2][0]);
@@ -518,14 +683,17 @@ __device__ __forceinline__ P pick3(int i, P a, P b, P c) {
 }
 
 // Elements [e0, e1) of the step (one slab).
+#ifndef DJG_K1_MINB
+#define DJG_K1_MINB 1
+#endif
 template <class Real, int KIND, int MODEL, int RB, bool COMPACT>
-__global__ void __launch_bounds__(128) k_element(const ElemArgs<Real> A, long long e0, long long e1) {
+__global__ void __launch_bounds__(128, DJG_K1_MINB) k_element(const ElemArgs<Real> A, long long e0, long long e1) {
     const long long e = e0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= e1) return;
     if (__ldcg(&A.ctrl->halted)) return;
     const int phase = int(__ldcg(&A.ctrl->step) % 3);
     const typename RT<Real>::Node* u = A.u_override ? A.u_override : pick3(phase, A.u[0], A.u[1], A.u[2]);
-    element_body<Real, KIND, MODEL, RB, COMPACT>(A, e, u);
+    element_body<Real, KIND, MODEL, RB, COMPACT>(A, e, u, GlobalSrc<Real>{A, e});
 }
 
 // ------------------------------------------------------------------ TLED
@@ -544,9 +712,9 @@ struct TledLayout {
     static constexpr int count = KIND == 1 ? gamma + 32 : V0 + 1;
 };
 
-template <class Real, int KIND, int MODEL, int RB>
+template <class Real, int KIND, int MODEL, int RB, class Src>
 __device__ __forceinline__ void element_body_tled(const ElemArgs<Real>& A, const long long e,
-                                                  const typename RT<Real>::Node* __restrict__ u) {
+                                                  const typename RT<Real>::Node* __restrict__ u, const Src& src) {
     using T = RT<Real>;
     using TL = TledLayout<KIND>;
     using L = Layout<KIND, MODEL>;
@@ -555,13 +723,13 @@ __device__ __forceinline__ void element_body_tled(const ElemArgs<Real>& A, const
     int nid[NPE];
 #pragma unroll
     for (int p = 0; p < NPE / 4; ++p) {
-        const int4 q = __ldcs(A.conn + (long long)p * A.E + e);
+        const int4 q = src.conn(p);
         nid[4 * p + 0] = q.x; nid[4 * p + 1] = q.y; nid[4 * p + 2] = q.z; nid[4 * p + 3] = q.w;
     }
     Real c[NP * T::kPlane];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
-        const typename T::Plane v = T::load_plane(A.c + (long long)p * A.E + e);
+        const typename T::Plane v = src.plane(p);
         if constexpr (T::kPlane == 4) {
             c[4 * p + 0] = v.x; c[4 * p + 1] = v.y; c[4 * p + 2] = v.z; c[4 * p + 3] = v.w;
         } else {
@@ -571,15 +739,15 @@ __device__ __forceinline__ void element_body_tled(const ElemArgs<Real>& A, const
     Real uu[NPE][3];
 #pragma unroll
     for (int a = 0; a < NPE; ++a) {
-        const typename T::Node v = T::load_node(u + nid[a]);
+        const typename T::Node v = src.node(a, u, nid[a]);
         uu[a][0] = v.x; uu[a][1] = v.y; uu[a][2] = v.z;
     }
     int sl[NPE];
     {
         int rk[NPE];
-        load_ranks<NPE, RB>(A.rank, e, rk);
+        src.template ranks<NPE, RB>(rk);
 #pragma unroll
-        for (int a = 0; a < NPE; ++a) sl[a] = __ldg(A.slice_base + (nid[a] >> 5)) + 32 * rk[a] + (nid[a] & 31);
+        for (int a = 0; a < NPE; ++a) sl[a] = src.slot(A.slice_base, a, nid[a], rk[a]);
     }
     // deformation_gradient (tled_force.hpp:28-36)
     Real X[3][3] = {{Real(1), Real(0), Real(0)}, {Real(0), Real(1), Real(0)}, {Real(0), Real(0), Real(1)}};
@@ -710,7 +878,217 @@ __global__ void __launch_bounds__(128) k_element_tled(const ElemArgs<Real> A, lo
     if (__ldcg(&A.ctrl->halted)) return;
     const int phase = int(__ldcg(&A.ctrl->step) % 3);
     const typename RT<Real>::Node* u = A.u_override ? A.u_override : pick3(phase, A.u[0], A.u[1], A.u[2]);
-    element_body_tled<Real, KIND, MODEL, RB>(A, e, u);
+    element_body_tled<Real, KIND, MODEL, RB>(A, e, u, GlobalSrc<Real>{A, e});
+}
+
+// ------------------------------------------------------------------ K1, pipelined
+
+// The per-element streams (connectivity, rank words, record planes) are
+// plain contiguous runs of 16-byte rows, so a persistent block can move a
+// whole tile of them into shared memory with a handful of bulk async copies
+// (cp.async.bulk, TMA unit, completion on an mbarrier) several tiles ahead of
+// the threads computing on it. The dependent node gather u[conn[e]] then
+// starts from shared memory instead of waiting on an HBM round trip, and the
+// bytes in flight per SM no longer depend on registers or resident warps.
+// Warp 4 of each block is the producer; warps 0-3 compute one element per
+// thread with exactly the arithmetic of k_element / k_element_tled.
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        "DJG_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra DJG_WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ unsigned long long l2_evict_first_policy() {
+    unsigned long long pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+// bytes: multiple of 16; src and dst 16-byte aligned.
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, unsigned long long* bar,
+                                          unsigned long long pol) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+        : "memory");
+}
+
+constexpr int kPipeTile = 128;  // elements per tile = threads per block
+
+// Stage layout: connectivity planes, record planes, record tail planes, rank words.
+template <class Real, int KIND, int MODEL, int RB, int FORM>  // FORM 0 full, 1 compact, 2 TLED
+struct PipeShape {
+    using T = RT<Real>;
+    static constexpr int NPE = KIND == 1 ? 8 : 4;
+    static constexpr int NCP = NPE / 4;
+    static constexpr int kRecLen = FORM == 2   ? TledLayout<KIND>::count
+                                   : FORM == 1 ? kCompactLen<KIND>
+                                               : Layout<KIND, MODEL>::count;
+    using RP = RecPlanes<Real, kRecLen, FORM == 1 && kTailRecord<KIND, true>>;
+    static constexpr int NRP = RP::NFULL;
+    static constexpr int NTAIL = RP::NTAIL;
+    static constexpr int kRankBytes = NPE * RB;
+    static constexpr int kConnOff = 0, kRecOff = kPipeTile * 16 * NCP, kTailOff = kRecOff + kPipeTile * 16 * NRP;
+    static constexpr int kRankOff = kTailOff + kPipeTile * int(sizeof(Real)) * NTAIL;
+    static constexpr int kStageBytes = kRankOff + kPipeTile * kRankBytes;
+    static constexpr size_t smem_bytes(int stages) { return size_t(stages) * kStageBytes + 2 * 8 * size_t(stages); }
+};
+
+#ifndef DJG_PIPE_MINB
+#define DJG_PIPE_MINB 6
+#endif
+#ifndef DJG_PIPE_WS
+#define DJG_PIPE_WS 1
+#endif
+constexpr int kPipeWs = DJG_PIPE_WS;  // 1: a fifth warp per block issues the copies
+#ifndef DJG_PIPE_PREF
+#define DJG_PIPE_PREF 0
+#endif
+constexpr bool kPipePrefetch = DJG_PIPE_PREF != 0;
+constexpr int kPipeThreads = kPipeTile + (kPipeWs ? 32 : 0);
+
+// Persistent blocks; tile `it` of a block (global tile blockIdx + it * grid)
+// lives in stage it % STAGES. The copies of a tile are issued once all four
+// compute warps have released its stage (empty barrier): by a dedicated
+// producer warp running up to STAGES tiles ahead (kPipeWs), or by thread 0,
+// STAGES - 1 tiles ahead.
+template <class Real, int KIND, int MODEL, int RB, int FORM, int STAGES>
+__global__ void __launch_bounds__(kPipeThreads, DJG_PIPE_MINB) k_element_pipe(const ElemArgs<Real> A, long long e0,
+                                                                              long long e1) {
+    using PS = PipeShape<Real, KIND, MODEL, RB, FORM>;
+    using Plane = typename RT<Real>::Plane;
+    using Node = typename RT<Real>::Node;
+    static_assert(STAGES >= 2, "pipeline needs at least two stages");
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + STAGES * PS::kStageBytes);
+    unsigned long long* empty = full + STAGES;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, kPipeTile / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (__ldcg(&A.ctrl->halted)) return;
+    const long long ntiles = (e1 - e0 + kPipeTile - 1) / kPipeTile;
+    const long long G = gridDim.x;
+    const long long nmine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / G + 1 : 0;
+    unsigned long long pol = 0;
+
+    // Bulk copies of this block's tile number `it` into stage it % STAGES.
+    auto issue = [&](long long it) {
+        const int s = int(it % STAGES);
+        if (it >= STAGES) mbar_wait(empty + s, unsigned((it / STAGES - 1) & 1));
+        const long long eb = e0 + (blockIdx.x + it * G) * kPipeTile;
+        const unsigned n = unsigned(min((long long)kPipeTile, e1 - eb));
+        const unsigned rbytes = (n * PS::kRankBytes + 15u) & ~15u;  // rank array is padded by 16 bytes
+        const unsigned tbytes = (n * unsigned(sizeof(Real)) + 15u) & ~15u;  // tail planes likewise
+        mbar_expect_tx(full + s, n * 16u * (PS::NCP + PS::NRP) + tbytes * PS::NTAIL + rbytes);
+        unsigned char* st = smem + s * PS::kStageBytes;
+#pragma unroll
+        for (int p = 0; p < PS::NCP; ++p)
+            bulk_load(st + PS::kConnOff + p * kPipeTile * 16, A.conn + (long long)p * A.E + eb, n * 16u, full + s, pol);
+#pragma unroll
+        for (int p = 0; p < PS::NRP; ++p)
+            bulk_load(st + PS::kRecOff + p * kPipeTile * 16, A.c + (long long)p * A.E + eb, n * 16u, full + s, pol);
+#pragma unroll
+        for (int t = 0; t < PS::NTAIL; ++t)
+            bulk_load(st + PS::kTailOff + t * kPipeTile * int(sizeof(Real)), A.ctail + t * A.tail_stride + eb, tbytes,
+                      full + s, pol);
+        bulk_load(st + PS::kRankOff, static_cast<const unsigned char*>(A.rank) + eb * PS::kRankBytes, rbytes, full + s,
+                  pol);
+    };
+    if constexpr (kPipeWs) {
+        if (tid >= kPipeTile) {
+            if (tid == kPipeTile) {
+                pol = l2_evict_first_policy();
+                for (long long it = 0; it < nmine; ++it) issue(it);
+            }
+            return;
+        }
+    } else if (tid == 0) {
+        pol = l2_evict_first_policy();
+        for (long long it = 0; it < STAGES - 1 && it < nmine; ++it) issue(it);
+    }
+
+    const int phase = int(__ldcg(&A.ctrl->step) % 3);
+    const Node* u = A.u_override ? A.u_override : pick3(phase, A.u[0], A.u[1], A.u[2]);
+    auto stage_src = [&](long long it) {
+        const unsigned char* st = smem + int(it % STAGES) * PS::kStageBytes;
+        return SmemSrc<Real, kPipeTile>{reinterpret_cast<const int4*>(st + PS::kConnOff),
+                                        reinterpret_cast<const Plane*>(st + PS::kRecOff), st + PS::kRankOff,
+                                        reinterpret_cast<const Real*>(st + PS::kTailOff), tid};
+    };
+    auto elem_of = [&](long long it) { return e0 + (blockIdx.x + it * G) * kPipeTile + tid; };
+    if constexpr (kPipePrefetch) {
+        // The gather of tile it + 1 (displacements, slot positions) is in
+        // flight while tile it is computed.
+        constexpr int NPE = PS::NPE;
+        Prefetched<Real, NPE> cur, nxt;
+        if (nmine > 0) {
+            mbar_wait(full, 0u);
+            if (elem_of(0) < e1) prefetch_element<Real, NPE, RB, kPipeTile>(A, stage_src(0), u, cur);
+        }
+        for (long long it = 0; it < nmine; ++it) {
+            if constexpr (!kPipeWs) {
+                if (tid == 0 && it + STAGES - 1 < nmine) issue(it + STAGES - 1);
+            }
+            if (it + 1 < nmine) {
+                mbar_wait(full + int((it + 1) % STAGES), unsigned(((it + 1) / STAGES) & 1));
+                if (elem_of(it + 1) < e1) prefetch_element<Real, NPE, RB, kPipeTile>(A, stage_src(it + 1), u, nxt);
+            }
+            const long long e = elem_of(it);
+            if (e < e1) {
+                const auto ss = stage_src(it);
+                const PrefetchedSrc<Real, NPE, kPipeTile> src{cur, ss.srec, ss.stail, tid};
+                if constexpr (FORM == 2) element_body_tled<Real, KIND, MODEL, RB>(A, e, u, src);
+                else element_body<Real, KIND, MODEL, RB, FORM == 1>(A, e, u, src);
+            }
+            __syncwarp();
+            if ((tid & 31) == 0) mbar_arrive(empty + int(it % STAGES));
+            cur = nxt;
+        }
+        return;
+    }
+    for (long long it = 0; it < nmine; ++it) {
+        if constexpr (!kPipeWs) {
+            if (tid == 0 && it + STAGES - 1 < nmine) issue(it + STAGES - 1);
+        }
+        const int s = int(it % STAGES);
+        mbar_wait(full + s, unsigned((it / STAGES) & 1));
+        const long long e = e0 + (blockIdx.x + it * G) * kPipeTile + tid;
+        if (e < e1) {
+            const unsigned char* st = smem + s * PS::kStageBytes;
+            const SmemSrc<Real, kPipeTile> src{reinterpret_cast<const int4*>(st + PS::kConnOff),
+                                               reinterpret_cast<const Plane*>(st + PS::kRecOff), st + PS::kRankOff,
+                                               reinterpret_cast<const Real*>(st + PS::kTailOff), tid};
+            if constexpr (FORM == 2) element_body_tled<Real, KIND, MODEL, RB>(A, e, u, src);
+            else element_body<Real, KIND, MODEL, RB, FORM == 1>(A, e, u, src);
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(empty + s);
+    }
 }
 
 // TledModel::build on the device (tled_force.hpp:167-195).
@@ -1060,8 +1438,8 @@ __global__ void k_agree(Ctrl* ctrl, const long long* __restrict__ reduced) {
 // (the first `nrec` Reals of the record: everything, or the compact part).
 // bad[0] collects the smallest element with det J0 <= 0 (MeshError).
 template <class Real, int KIND, int MODEL>
-__global__ void k_precompute(const ElemArgs<Real> A, int nrec, typename RT<Real>::Plane* planes,
-                             unsigned long long* bad) {
+__global__ void k_precompute(const ElemArgs<Real> A, int nrec, int nfull, typename RT<Real>::Plane* planes,
+                             Real* tail, unsigned long long* bad) {
     using L = Layout<KIND, MODEL>;
     using T = RT<Real>;
     constexpr int NPE = L::NPE;
@@ -1112,18 +1490,15 @@ __global__ void k_precompute(const ElemArgs<Real> A, int nrec, typename RT<Real>
                 for (int a = 0; a < 8; ++a) c[L::gamma + 8 * m + a] = gamma[m][a];
         }
     }
-    // compact record: J0, det, V0, pad [, k_hg, gamma]
+    // compact record: T4 J0; H8 J0, det, V0, pad, k_hg, gamma (kCompactLen)
     const bool compact = nrec < L::count;
     constexpr int W = T::kPlane;
-    for (int p = 0; p * W < nrec; ++p) {
-        Real* dst = reinterpret_cast<Real*>(planes + (long long)p * A.E + e);
-#pragma unroll
-        for (int k = 0; k < W; ++k) {
-            const int f = p * W + k;
-            int src = f;
-            if (compact && f >= kCompactRecord) src = L::khg + (f - kCompactRecord);
-            dst[k] = (f < nrec && src < L::count && !(compact && f == 11)) ? c[src] : Real(0);
-        }
+    for (int f = 0; f < nfull * W + (compact && KIND == 0 ? nrec - nfull * W : 0); ++f) {
+        int src = f;
+        if (compact && KIND == 1 && f >= kCompactRecord) src = L::khg + (f - kCompactRecord);
+        const Real v = (f < nrec && src < L::count && !(compact && KIND == 1 && f == 11)) ? c[src] : Real(0);
+        if (f < nfull * W) reinterpret_cast<Real*>(planes + (long long)(f / W) * A.E + e)[f % W] = v;
+        else tail[(long long)(f - nfull * W) * A.tail_stride + e] = v;
     }
 }
 
@@ -1135,21 +1510,28 @@ __global__ void k_precompute(const ElemArgs<Real> A, int nrec, typename RT<Real>
 // canonical offset hg_src]).
 template <class Real>
 __global__ void k_transpose_consts(const Real* __restrict__ aos, int nconst, int nrec, int hg_src, long long e0,
-                                   long long ne, long long E, int nplanes, Real* __restrict__ planes) {
+                                   long long ne, long long E, int nplanes, Real* __restrict__ planes,
+                                   Real* __restrict__ tail, long long tail_stride, int ntail) {
     constexpr int W = RT<Real>::kPlane;
+    const int nslots = nplanes + ntail;
     const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= ne * nplanes) return;
-    const long long e = i / nplanes;
-    const int p = int(i % nplanes);
-    Real* dst = planes + ((long long)p * E + e0 + e) * W;
+    if (i >= ne * nslots) return;
+    const long long e = i / nslots;
+    const int p = int(i % nslots);
     const bool compact = nrec < nconst;
-#pragma unroll
-    for (int k = 0; k < W; ++k) {
-        const int f = p * W + k;
+    // compact H8 maps record field f >= 12 to canonical field hg_src + f - 12
+    auto field = [&](int f) {
         int src = f;
-        if (compact && f >= kCompactRecord) src = hg_src + (f - kCompactRecord);
-        const bool pad = f >= nrec || (compact && f == 11) || src >= nconst;
-        dst[k] = pad ? Real(0) : aos[e * nconst + src];
+        if (compact && hg_src >= 0 && f >= kCompactRecord) src = hg_src + (f - kCompactRecord);
+        const bool pad = f >= nrec || (compact && hg_src >= 0 && f == 11) || src >= nconst;
+        return pad ? Real(0) : aos[e * nconst + src];
+    };
+    if (p < nplanes) {
+        Real* dst = planes + ((long long)p * E + e0 + e) * W;
+#pragma unroll
+        for (int k = 0; k < W; ++k) dst[k] = field(p * W + k);
+    } else {
+        tail[(long long)(p - nplanes) * tail_stride + e0 + e] = field(nplanes * W + (p - nplanes));
     }
 }
 

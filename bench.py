@@ -58,6 +58,23 @@ def peaks():
     return 6650.0, "fallback"
 
 
+def measured_traffic(workload: str, kernel_prefix: str):
+    """DRAM bytes per launch of the element kernel from the committed ncu
+    launch list of the same workload (profiles/r01/ncu_traffic.json, made by
+    tools/ncu_traffic.py from `ncu --metrics dram__bytes_read.sum,
+    dram__bytes_write.sum`), or None."""
+    p = ROOT / "profiles" / "r01" / "ncu_traffic.json"
+    if not p.exists():
+        return None, None
+    d = json.loads(p.read_text()).get(workload)
+    if not d:
+        return None, None
+    for k, v in d["kernels"].items():
+        if k.startswith(kernel_prefix):
+            return v["dram_bytes_per_launch"], f"profiles/r01/{d['source']} ({k}, ncu, per launch)"
+    return None, None
+
+
 def algo_bytes(kind: str, model: str, N: int, E: int, prec: int) -> dict:
     """SURVEY §8(d) algorithmic bytes per step, split by kernel."""
     npe = 4 if kind == "T4" else 8
@@ -282,20 +299,28 @@ def our_arm(args):
     B = algo_bytes(args.kind, args.model, N, E, args.precision)
     k1_ms = ms_e / K
     achieved = B["k_element"] / (k1_ms * 1e-3) / 1e9
+    traffic, traffic_src = None, None
+    if args.divisions == 203 and args.kind == "T4" and args.model == "NH" and args.precision == 4:
+        traffic, traffic_src = measured_traffic("cfg5", "k_element_pipe" if info.get("pipelined") else "k_element<")
     extra = {
         "e2e": {"value": E / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 2 * 3 * N * rbytes,
                 "d2h_bytes_per_step": 2 * 3 * N * rbytes, "ms_per_step": e2e_ms,
                 "mode": "per step: djg_set_state (H2D u_curr+u_prev from pinned host), djg_step(1), "
                         "djg_get_state (D2H u_curr+u_prev); wall clock"},
         "roofline": {"bound": "hbm", "kernel": "k_element", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                     "frac": achieved / hbm, "traffic": None, "peak_source": peak_kind,
+                     "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
+                     "moved_frac": (traffic / (k1_ms * 1e-3) / 1e9 / hbm) if traffic else None,
+                     "note": "achieved/frac use SURVEY §8(d)'s algorithmic bytes (the reference's hot-field "
+                             "set, 12-byte force rows); the compact record moves fewer bytes, so frac can "
+                             "exceed 1. moved_frac = measured DRAM bytes (traffic) / event-timed launch / peak",
+                     "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": B["k_element"], "launch_ms": k1_ms,
                      "k_node_ms": ms_n / K, "k_node_frac": B["k_node"] / (ms_n / K * 1e-3) / 1e9 / hbm,
                      "step_algorithmic_bytes": B["step"], "step_frac": B["step"] / (ms_step * 1e-3) / 1e9 / hbm},
         "ms_per_step_events_per_kernel": ms_tot / K,
         "gpu_launches": 2 * K,
         "clocks": clk,
-        "engine": {k: info[k] for k in ("slabs", "kernels_per_step", "device_bytes", "slot_capacity")},
+        "engine": {k: info[k] for k in ("slabs", "kernels_per_step", "device_bytes", "slot_capacity", "pipelined")},
     }
     extra["config"] = None
     line = _line(args, 1, K, W, E, ms_step, value, {k: v for k, v in extra.items() if k != "config"})

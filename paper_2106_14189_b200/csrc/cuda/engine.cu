@@ -34,7 +34,7 @@ namespace {
 // k_element_pipe: stages per block and the largest tile stage it is used for
 // (bigger records -- H8 full, MR -- keep the one-shot kernel).
 #ifndef DJG_PIPE_STAGES
-#define DJG_PIPE_STAGES 3
+#define DJG_PIPE_STAGES 4
 #endif
 #ifndef DJG_PIPE_MAX_STAGE_KB
 #define DJG_PIPE_MAX_STAGE_KB 32
@@ -619,7 +619,8 @@ public:
     template <int K, int M, int RB, int FORM>
     bool launch_pipe(cudaStream_t s, const ElemArgs<Real>& a, int64_t e0, int64_t e1, bool setup) {
         using PS = PipeShape<Real, K, M, RB, FORM>;
-        if constexpr (PS::kStageBytes > kPipeMaxStageBytes) {
+        // H8 bodies (heavier, 8 gathers, full record) run better one-shot.
+        if constexpr (K == 1 || PS::kStageBytes > kPipeMaxStageBytes) {
             return false;
         } else {
             constexpr int ST = kPipeStages;

@@ -499,25 +499,6 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
         for (int a = 0; a < NPE; ++a) sl[a] = src.slot(A.slice_base, a, nid[a], rk[a]);
     }
 
-#if defined(DJG_EXP) && (DJG_EXP & 1)
-    if constexpr (KIND == 0) {  // timing experiment: memory traffic only
-        Real K[3][3];
-#pragma unroll
-        for (int i = 0; i < 3; ++i)
-#pragma unroll
-            for (int j = 0; j < 3; ++j) K[i][j] = (Jt[i][j] * c[9 + (i + j) % 3] + det) * Real(1e-30);
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-#if DJG_EXP & 2
-            const int p = int(4 * e + a);
-#else
-            const int p = sl[a];
-#endif
-            store_row(A, p, K[a % 3][0], K[a % 3][1], K[a % 3][2]);
-        }
-        return;
-    }
-#endif
     if (!(det > Real(0))) {
         // record_inversion (djtled_force.hpp:107-112) + zeroed rows (:187-191).
         atomicAdd(&A.ctrl->inv_count, 1ull);
@@ -616,17 +597,6 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
             K[i][j] = j_m23 * mt + cc * Ji[i][j];
         }
 
-#if defined(DJG_EXP) && (DJG_EXP & 2)
-    if constexpr (KIND == 0) {  // timing experiment: sequential stores
-        const int p = int(4 * e);
-        store_row(A, p + 1, K[0][0], K[1][0], K[2][0]);
-        store_row(A, p + 2, K[0][1], K[1][1], K[2][1]);
-        store_row(A, p + 3, K[0][2], K[1][2], K[2][2]);
-        store_row(A, p, Real(-1) * ((K[0][0] + K[0][1]) + K[0][2]), Real(-1) * ((K[1][0] + K[1][1]) + K[1][2]),
-                  Real(-1) * ((K[2][0] + K[2][1]) + K[2][2]));
-        return;
-    }
-#endif
     if constexpr (KIND == 0) {
         // T4 rows: f1..f3 = columns of K, f0 = -(f1 + f2 + f3).
         store_row(A, sl[1], K[0][0], K[1][0], K[2][0]);
@@ -931,7 +901,10 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned b
         : "memory");
 }
 
-constexpr int kPipeTile = 128;  // elements per tile = threads per block
+#ifndef DJG_PIPE_TILE
+#define DJG_PIPE_TILE 128
+#endif
+constexpr int kPipeTile = DJG_PIPE_TILE;  // elements per tile = compute threads per block
 
 // Stage layout: connectivity planes, record planes, record tail planes, rank words.
 template <class Real, int KIND, int MODEL, int RB, int FORM>  // FORM 0 full, 1 compact, 2 TLED
@@ -952,9 +925,17 @@ struct PipeShape {
     static constexpr size_t smem_bytes(int stages) { return size_t(stages) * kStageBytes + 2 * 8 * size_t(stages); }
 };
 
-#ifndef DJG_PIPE_MINB
-#define DJG_PIPE_MINB 6
+// Blocks per SM the register allocation is sized for: the compact T4
+// kernel runs best capped at 64 registers (6 blocks); heavier element bodies
+// are left uncapped rather than spilled.
+#ifndef DJG_PIPE_MINB_T4C
+#define DJG_PIPE_MINB_T4C 6
 #endif
+#ifndef DJG_PIPE_MINB_OTHER
+#define DJG_PIPE_MINB_OTHER 1
+#endif
+template <class Real, int KIND, int FORM>
+constexpr int kPipeMinBlocks = (KIND == 0 && FORM == 1 && sizeof(Real) == 4) ? DJG_PIPE_MINB_T4C : DJG_PIPE_MINB_OTHER;
 #ifndef DJG_PIPE_WS
 #define DJG_PIPE_WS 1
 #endif
@@ -971,7 +952,7 @@ constexpr int kPipeThreads = kPipeTile + (kPipeWs ? 32 : 0);
 // producer warp running up to STAGES tiles ahead (kPipeWs), or by thread 0,
 // STAGES - 1 tiles ahead.
 template <class Real, int KIND, int MODEL, int RB, int FORM, int STAGES>
-__global__ void __launch_bounds__(kPipeThreads, DJG_PIPE_MINB) k_element_pipe(const ElemArgs<Real> A, long long e0,
+__global__ void __launch_bounds__(kPipeThreads, (kPipeMinBlocks<Real, KIND, FORM>)) k_element_pipe(const ElemArgs<Real> A, long long e0,
                                                                               long long e1) {
     using PS = PipeShape<Real, KIND, MODEL, RB, FORM>;
     using Plane = typename RT<Real>::Plane;

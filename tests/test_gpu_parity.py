@@ -61,12 +61,14 @@ def test_cfg2_h8_nh_hourglass_2000_steps(precision):
 @pytest.mark.parametrize("precision", [4, 8])
 @pytest.mark.parametrize("kind", ["T4", "H8"])
 @pytest.mark.parametrize("model", ["NH", "TI", "OT", "MR"])
-@pytest.mark.parametrize("mode", ["default", "slabs"])
+@pytest.mark.parametrize("mode", ["default", "slabs", "nopipe"])
 def test_materials_small(kind, model, precision, mode, monkeypatch):
     flags = 0
     if mode == "slabs":
         monkeypatch.setenv("DJG_SLAB_KB", "64")
         flags = A.DJG_FLAG_SLABS
+    elif mode == "nopipe":
+        flags = A.DJG_FLAG_NO_PIPE
     check_run(box_spec(kind=kind, model=model, divisions=4, precision=precision, ramp_steps=300), 300, flags=flags)
 
 
@@ -78,6 +80,31 @@ def test_materials_small(kind, model, precision, mode, monkeypatch):
                                    A.DJG_FLAG_FULL_RECORD | A.DJG_FLAG_DEVICE_PRECOMPUTE])
 def test_compact_and_device_precompute_bitwise(kind, model, precision, flags):
     check_run(box_spec(kind=kind, model=model, divisions=4, precision=precision, ramp_steps=300), 300, flags=flags)
+
+
+@pytest.mark.parametrize("precision", [4, 8])
+@pytest.mark.parametrize("model", ["NH", "TI", "OT", "MR"])
+@pytest.mark.parametrize("flags", [0, A.DJG_FLAG_FULL_RECORD, A.DJG_FLAG_TLED, A.DJG_FLAG_DEVICE_PRECOMPUTE])
+def test_pipeline_partial_tiles(model, precision, flags):
+    """k_element_pipe on a mesh whose element count is not a multiple of the
+    128-element tile (720 tets: 5 full tiles + 80), with record tail planes
+    and rank words whose copies round up to 16 bytes."""
+    spec = box_spec(kind="T4", model=model, divisions=(5, 4, 6), precision=precision, ramp_steps=250)
+    sc = Scenario(spec)
+    with GpuDjEngine(sc, flags=flags) as eng:
+        # full f64 records of the anisotropic models exceed the stage budget
+        assert eng.info()["pipelined"] == 1 or (flags & A.DJG_FLAG_FULL_RECORD)
+    if flags & A.DJG_FLAG_TLED:
+        return  # TLED parity is tests/test_gpu_tled.py
+    check_run(spec, 250, flags=flags)
+
+
+def test_pipeline_selection():
+    """T4 runs the bulk-copy pipeline by default; H8 and DJG_FLAG_NO_PIPE the one-shot kernel."""
+    for kind, flags, want in (("T4", 0, 1), ("T4", A.DJG_FLAG_NO_PIPE, 0), ("H8", 0, 0)):
+        sc = Scenario(box_spec(kind=kind, divisions=3, precision=4))
+        with GpuDjEngine(sc, flags=flags) as eng:
+            assert eng.info()["pipelined"] == want, (kind, flags)
 
 
 @pytest.mark.parametrize("precision", [4, 8])

@@ -37,13 +37,14 @@ def test_tled_bitwise_vs_reference_tled(kind, model, precision):
     assert np.abs(ur).max() > 0.1
 
 
+@pytest.mark.parametrize("flags", [A.DJG_FLAG_TLED, A.DJG_FLAG_TLED | A.DJG_FLAG_NO_PIPE], ids=["pipe", "nopipe"])
 @pytest.mark.parametrize("path", sorted(GOLDEN.glob("tled_*.npz")), ids=lambda p: p.stem)
-def test_tled_vs_golden(path):
+def test_tled_vs_golden(path, flags):
     g = np.load(path)
     kind, model, d, prec = g["spec"]
     steps = int(g["steps"])
     spec = box_spec(kind=kind, model=model, divisions=int(d), precision=int(prec), ramp_steps=steps)
-    u, up, rep, _ = run(spec, steps)
+    u, up, rep, _ = run(spec, steps, flags)
     assert np.array_equal(u, g["u"]) and np.array_equal(up, g["up"])
 
 

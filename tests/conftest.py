@@ -38,5 +38,6 @@ def _built():
     """Build the native libraries once per session (no-op when up to date)."""
     import subprocess
     subprocess.run(["make", "-s", "-C", str(ROOT / "oracle")], check=True)
-    if not (ROOT / "paper_2106_14189_b200" / "_build" / "libdjg.so").exists():
+    build = ROOT / "paper_2106_14189_b200" / "_build"
+    if not (build / "libdjg.so").exists() or not (build / "djg").exists():
         subprocess.run(["make", "-s", "-C", str(ROOT / "paper_2106_14189_b200" / "csrc")], check=True)

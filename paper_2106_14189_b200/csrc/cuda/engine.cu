@@ -41,6 +41,7 @@ namespace {
 #endif
 
 constexpr int kPipeStages = DJG_PIPE_STAGES;
+
 constexpr int kPipeMaxStageBytes = DJG_PIPE_MAX_STAGE_KB * 1024;
 
 thread_local std::string g_create_error;
@@ -127,11 +128,13 @@ public:
         flags_ = d.flags;
         if (const char* v = std::getenv("DJG_SLAB_KB")) slab_bytes_ = int64_t(std::atoll(v)) << 10;
         nconst_ = const_count(kind_, model_);
-        // Default record: compact for T4 (fewer bytes win), full for H8 (its
-        // heavier kernel is not bandwidth-bound; rebuilding costs more).
+        // Default record: compact (fewer bytes win) except where rebuilding
+        // the m / I tensors costs more than it saves -- H8 in f64 and the
+        // Mooney-Rivlin H8 body (measured on cfg4-sized meshes).
         tled_ = (flags_ & DJG_FLAG_TLED) != 0;
+        const bool compact_default = d.kind == DJG_T4 || (sizeof(Real) == 4 && d.material.model != DJG_MR);
         compact_ = !tled_ && ((flags_ & DJG_FLAG_COMPACT) != 0 ||
-                              (!(flags_ & DJG_FLAG_FULL_RECORD) && d.kind == DJG_T4));
+                              (!(flags_ & DJG_FLAG_FULL_RECORD) && compact_default));
         const bool dev_pre = tled_ || (flags_ & DJG_FLAG_DEVICE_PRECOMPUTE) != 0;
         nrec_ = tled_ ? (kind_ == DJG_H8 ? TledLayout<1>::count : TledLayout<0>::count)
                       : compact_ ? (kind_ == DJG_H8 ? kCompactLen<1> : kCompactLen<0>) : nconst_;
@@ -380,6 +383,17 @@ public:
         if (d.c1) {
             configure(static_cast<const Real*>(d.c1), d.massless, d.dof_kind, static_cast<const Real*>(d.dof_target),
                       static_cast<const Real*>(d.dof_t_total), Real(d.c2), Real(d.c3), Real(d.dt));
+        }
+        {
+            // k_node grid: on meshes of up to a few waves, a grid-stride launch
+            // sized to the resident blocks (one barrier + completion count per
+            // block, no tail wave: cfg4 53 -> 41 us); on large meshes one thread
+            // per node streams better (cfg5).
+            int nb = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_node<Real, false>, 256, 0));
+            const int64_t resident = int64_t(std::max(nb, 1)) * sms_, blocks = (N_ + 255) / 256;
+            node_grid_ = blocks > 16 * resident ? 0 : blocks > 4 * resident ? 2 * resident : resident;
+            if (const char* v = std::getenv("DJG_NODE_GRID")) node_grid_ = std::atoll(v);
         }
         pipe_ = !(flags_ & DJG_FLAG_NO_PIPE) && n_slabs_ == 1;
         if (pipe_) launch_element(stream_, 0, E_, nullptr, /*setup=*/true);
@@ -707,7 +721,7 @@ public:
 
     void launch_node(cudaStream_t s, int slab, bool assemble_mode) {
         if (n_slabs_ == 1) {
-            const unsigned g = unsigned((N_ + 255) / 256);
+            const unsigned g = unsigned(node_grid_ > 0 ? std::min<int64_t>((N_ + 255) / 256, node_grid_) : (N_ + 255) / 256);
             if (assemble_mode) k_node<Real, true><<<g, 256, 0, s>>>(na_);
             else k_node<Real, false><<<g, 256, 0, s>>>(na_);
             CK(cudaGetLastError());
@@ -909,6 +923,7 @@ private:
     static constexpr int kGraphSteps = 32;
     int kind_ = 0, model_ = 0, npe_ = 4, nconst_ = 0, nrec_ = 0, nplanes_ = 0, ntail_ = 0, policy_ = 0, sms_ = 0;
     int64_t tail_stride_ = 0;
+    int64_t node_grid_ = 0;
     bool compact_ = false, tled_ = false, pipe_ = false;
     int pipe_blocks_sm_ = 0;
     size_t pipe_smem_ = 0;

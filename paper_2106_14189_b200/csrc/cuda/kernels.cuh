@@ -413,13 +413,17 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
 
     // Hot constants: the full record from HBM, or (compact) J0 [, det J0, V0,
     // hourglass data] from HBM and the rest rebuilt here with the
-    // precompute's own arithmetic.
+    // precompute's own arithmetic. H8: the planes holding only hourglass data
+    // (k_hg, gamma: 33 Reals) are loaded just before the hourglass term, so
+    // they do not occupy registers through the whole body.
     constexpr int NCR = COMPACT ? kCompactLen<KIND> : L::count;
     using RP = RecPlanes<Real, NCR, kTailRecord<KIND, COMPACT>>;
     constexpr int NC = RP::NFULL * T::kPlane + RP::NTAIL;
+    constexpr int KHG = COMPACT ? kCompactRecord : L::khg;  // record index of k_hg (H8)
+    constexpr int NPA = L::kH8 ? (KHG + T::kPlane - 1) / T::kPlane : RP::NFULL;  // planes loaded up front
     Real r[NC];
 #pragma unroll
-    for (int p = 0; p < RP::NFULL; ++p) {
+    for (int p = 0; p < NPA; ++p) {
         const typename T::Plane v = src.plane(p);
         if constexpr (T::kPlane == 4) {
             r[4 * p + 0] = v.x; r[4 * p + 1] = v.y; r[4 * p + 2] = v.z; r[4 * p + 3] = v.w;
@@ -429,10 +433,11 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
     }
 #pragma unroll
     for (int t = 0; t < RP::NTAIL; ++t) r[RP::NFULL * T::kPlane + t] = src.tail(t);
-    Real c[COMPACT ? L::count + 1 : NC];
+    constexpr int NCU = L::kH8 ? KHG : NC;  // record fields used before the hourglass term
+    Real c[COMPACT ? L::count + 1 : NCU];
     if constexpr (!COMPACT) {
 #pragma unroll
-        for (int k = 0; k < NC; ++k) c[k] = r[k];
+        for (int k = 0; k < NCU; ++k) c[k] = r[k];
     } else {
         if constexpr (KIND == 0) {
 #pragma unroll
@@ -443,8 +448,6 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
         } else {
 #pragma unroll
             for (int k = 0; k < 11; ++k) c[k] = r[k];
-#pragma unroll
-            for (int k = 0; k < 33; ++k) c[L::khg + k] = r[kCompactRecord + k];
         }
         const Real J0[3][3] = {{c[0], c[1], c[2]}, {c[3], c[4], c[5]}, {c[6], c[7], c[8]}};
         Real J0i[3][3];
@@ -605,43 +608,60 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
         store_row(A, sl[0], Real(-1) * ((K[0][0] + K[0][1]) + K[0][2]), Real(-1) * ((K[1][0] + K[1][1]) + K[1][2]),
                   Real(-1) * ((K[2][0] + K[2][1]) + K[2][2]));
     } else {
-        constexpr int S[8][3] = {{-1, -1, -1}, {+1, -1, -1}, {+1, +1, -1}, {-1, +1, -1},
-                                 {-1, -1, +1}, {+1, -1, +1}, {+1, +1, +1}, {-1, +1, +1}};
-        Real f[8][3];
+        // Hourglass data: the remaining record planes, loaded now.
 #pragma unroll
-        for (int a = 0; a < 8; ++a)
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                // D0a K[i][0] + D1a K[i][1] + D2a K[i][2] with D = sign/8.
-                Real t = S[a][0] > 0 ? K[i][0] : -K[i][0];
-                t = S[a][1] > 0 ? t + K[i][1] : t - K[i][1];
-                t = S[a][2] > 0 ? t + K[i][2] : t - K[i][2];
-                f[a][i] = Real(0.125) * t;
+        for (int p = NPA; p < RP::NFULL; ++p) {
+            const typename T::Plane v = src.plane(p);
+            if constexpr (T::kPlane == 4) {
+                r[4 * p + 0] = v.x; r[4 * p + 1] = v.y; r[4 * p + 2] = v.z; r[4 * p + 3] = v.w;
+            } else {
+                r[2 * p + 0] = v.x; r[2 * p + 1] = v.y;
             }
-        // hourglass_force (djtled_force.hpp:86-95)
-        const Real khg = c[L::khg];
+        }
+        const Real khg = r[KHG];
+        const Real* gamma = r + KHG + 1;  // gamma[8 m + b]
+        // hourglass_force (djtled_force.hpp:86-95): q_m = sum_b gamma_mb u_b
+        // (b ascending), then every row b adds k_hg gamma_mb q_m for m = 0..3
+        // in order -- each row is finished and stored in turn, same sums.
+        Real q[4][3];
         if (khg != Real(0)) {
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
                 Real q0 = Real(0), q1 = Real(0), q2 = Real(0);
 #pragma unroll
                 for (int b = 0; b < 8; ++b) {
-                    const Real gm = c[L::gamma + 8 * m + b];
+                    const Real gm = gamma[8 * m + b];
                     q0 = q0 + gm * ux[b];
                     q1 = q1 + gm * uy[b];
                     q2 = q2 + gm * uz[b];
                 }
-#pragma unroll
-                for (int b = 0; b < 8; ++b) {
-                    const Real kg = khg * c[L::gamma + 8 * m + b];
-                    f[b][0] = f[b][0] + kg * q0;
-                    f[b][1] = f[b][1] + kg * q1;
-                    f[b][2] = f[b][2] + kg * q2;
-                }
+                q[m][0] = q0; q[m][1] = q1; q[m][2] = q2;
             }
         }
+        constexpr int S[8][3] = {{-1, -1, -1}, {+1, -1, -1}, {+1, +1, -1}, {-1, +1, -1},
+                                 {-1, -1, +1}, {+1, -1, +1}, {+1, +1, +1}, {-1, +1, +1}};
 #pragma unroll
-        for (int a = 0; a < 8; ++a) store_row(A, sl[a], f[a][0], f[a][1], f[a][2]);
+        for (int a = 0; a < 8; ++a) {
+            Real f[3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                // D0a K[i][0] + D1a K[i][1] + D2a K[i][2] with D = sign/8.
+                Real t = S[a][0] > 0 ? K[i][0] : -K[i][0];
+                t = S[a][1] > 0 ? t + K[i][1] : t - K[i][1];
+                t = S[a][2] > 0 ? t + K[i][2] : t - K[i][2];
+                f[i] = Real(0.125) * t;
+            }
+            if (khg != Real(0)) {
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const Real kg = khg * gamma[8 * m + a];
+                    f[0] = f[0] + kg * q[m][0];
+                    f[1] = f[1] + kg * q[m][1];
+                    f[2] = f[2] + kg * q[m][2];
+                }
+            }
+            store_row(A, sl[a], f[0], f[1], f[2]);
+        }
     }
 }
 
@@ -653,11 +673,19 @@ __device__ __forceinline__ P pick3(int i, P a, P b, P c) {
 }
 
 // Elements [e0, e1) of the step (one slab).
-#ifndef DJG_K1_MINB
-#define DJG_K1_MINB 1
+// Blocks per SM the one-shot kernel's registers are sized for. Left alone,
+// ptxas gives the f32 H8 bodies ~170 registers (3 blocks, 12 warps per SM)
+// to hoist every record load; capping at 5 blocks (~96 registers) is 10-20 %
+// faster for NH / TI / OT (cfg4-sized meshes). The MR body and the f64
+// bodies spill under that cap and stay uncapped.
+#ifndef DJG_K1_MINB_H8
+#define DJG_K1_MINB_H8 5
 #endif
+template <class Real, int KIND, int MODEL>
+constexpr int kElemMinBlocks = (KIND == 1 && sizeof(Real) == 4 && MODEL != 3) ? DJG_K1_MINB_H8 : 1;
+
 template <class Real, int KIND, int MODEL, int RB, bool COMPACT>
-__global__ void __launch_bounds__(128, DJG_K1_MINB) k_element(const ElemArgs<Real> A, long long e0, long long e1) {
+__global__ void __launch_bounds__(128, (kElemMinBlocks<Real, KIND, MODEL>)) k_element(const ElemArgs<Real> A, long long e0, long long e1) {
     const long long e = e0 + (long long)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= e1) return;
     if (__ldcg(&A.ctrl->halted)) return;
@@ -1239,8 +1267,10 @@ __global__ void __launch_bounds__(256) k_node(const NodeArgs<Real> A) {
     const long long step = ctrl->step;
     const bool inverted = ctrl->first_inv != kNone;
     const bool skip = inverted && A.policy == 0;  // Abort: no gather, no update (djtled_force.hpp:202-208)
-    const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-    if (n < A.N && !skip) {
+    // Grid-stride over nodes: the launch may size the grid to the resident
+    // blocks (one barrier + completion count per block, no tail wave).
+    for (long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x; n < A.N && !skip;
+         n += (long long)gridDim.x * blockDim.x) {
         Real fx, fy, fz;
         gather_row<Real>(A.ef + (long long)A.slice_base[n >> 5] + (n & 31), A.row_len[n], fx, fy, fz);
         if constexpr (kAssemble) {

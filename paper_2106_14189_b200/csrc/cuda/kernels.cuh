@@ -1169,6 +1169,7 @@ __device__ __forceinline__ void gather_row(const typename RT<Real>::Node* __rest
     }
 }
 
+
 // Per-DOF central-difference update (advance_step, solver.hpp:112-141).
 template <class Real>
 __device__ __forceinline__ Real dof_update(int kind, bool massless, Real c1, Real r, Real f, Real uc, Real up,

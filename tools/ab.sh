@@ -1,2 +1,1 @@
-timeout 1500 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
-python tools/probe_perf.py cfg1 cfg2 cfg3 cfg4 cfg5 2>&1 | cut -c1-200
+for v in _build _build_r12; do echo "== $v"; DJG_LIB_PATH=paper_2106_14189_b200/$v/libdjg.so timeout 300 python tools/ab_exp.py cfg3 cfg4 cfg5; done

@@ -120,6 +120,19 @@ typedef struct djg_mesh_desc {
 } djg_mesh_desc;
 int djg_create_from_mesh(const djg_mesh_desc* desc, djg_engine** out);
 
+/* Precompute results on the device, for an engine created with
+ * DJG_FLAG_DEVICE_PRECOMPUTE and no caller CSR (its adjacency, slot ranks
+ * and slices are then built on the GPU too):
+ *   djg_lump_mass        lump_mass(mesh, material.rho, elems)  precompute.hpp:275-287
+ *                        -> N Reals, bit-identical to the host function
+ *   djg_min_char_length  min over elements of characteristic_length
+ *                        (precompute.hpp:303-319), the numerator of
+ *                        critical_dt = l_min / wave_speed (:323-331); Real
+ *                        widened to double.
+ * Other engines return DJG_E_CONFIG. */
+int djg_lump_mass(djg_engine* eng, void* mass);
+int djg_min_char_length(djg_engine* eng, double* l_min);
+
 /* UpdateCoeffs::build(node_mass, dt, alpha) (solver.hpp:70-86) +
  * DofConstraints (solver.hpp:11-39): everything advance_step needs besides
  * the engine. dof_kind NULL = all free. Real values widened to double. */

@@ -149,6 +149,21 @@ public:
         if (eng_) djg_destroy(eng_);
     }
 
+    // lump_mass(mesh, material.rho, elems) (precompute.hpp:275-287) computed on
+    // the device -- engines built with DJG_FLAG_DEVICE_PRECOMPUTE. Bit-identical.
+    std::vector<Real> lump_mass() const {
+        std::vector<Real> m(size_t(num_dofs_ / 3));
+        detail::check(djg_lump_mass(eng_, m.data()), eng_);
+        return m;
+    }
+    // critical_dt(mesh, elems, wave_speed) (precompute.hpp:323-331): the minimum
+    // characteristic length from the device over wave_speed, in Real.
+    Real critical_dt(Real wave_speed) const {
+        double l = 0;
+        detail::check(djg_min_char_length(eng_, &l), eng_);
+        return Real(l) / wave_speed;
+    }
+
     // Engine::assemble (solver.hpp:269-272): internal forces at u. Under Abort
     // with an inverted element f is left untouched, like assemble_internal.
     template <class Policy>

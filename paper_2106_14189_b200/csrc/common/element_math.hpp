@@ -17,6 +17,10 @@
 namespace djg {
 namespace em {
 
+// Correctly rounded square root in the argument's precision on both sides.
+DJG_HD float sqrt_rn(float x) { return std::sqrt(x); }
+DJG_HD double sqrt_rn(double x) { return std::sqrt(x); }
+
 // H8 natural corner signs (element.hpp:17-20).
 DJG_HD int corner_sign(int a, int i) {
     // a: bits (x, y) follow the counter-clockwise face order, z = a >= 4
@@ -211,6 +215,34 @@ DJG_HD bool jacobian0(int kind, const R x[8][3], R J[3][3], R Ji[3][3], R& det) 
 template <class R>
 DJG_HD R volume0(int kind, R det) {
     return kind == 0 ? det / R(6) : R(8) * det;
+}
+
+// triangle_area / characteristic_length (precompute.hpp:290-319): the largest
+// face area (H8: quads as two triangles), l = 3 V0 / a_max (T4), V0 / a_max (H8).
+template <class R>
+DJG_HD R tri_area(const R a[3], const R b[3], const R c[3]) {
+    const R u[3] = {b[0] - a[0], b[1] - a[1], b[2] - a[2]}, v[3] = {c[0] - a[0], c[1] - a[1], c[2] - a[2]};
+    const R w[3] = {u[1] * v[2] - u[2] * v[1], u[2] * v[0] - u[0] * v[2], u[0] * v[1] - u[1] * v[0]};
+    return sqrt_rn(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]) / 2;
+}
+
+template <class R>
+DJG_HD R char_length(int kind, const R x[8][3], R v0) {
+    R a_max = 0;
+    if (kind == 0) {
+        constexpr int f[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
+        for (int t = 0; t < 4; ++t) {
+            const R a = tri_area(x[f[t][0]], x[f[t][1]], x[f[t][2]]);
+            a_max = a_max < a ? a : a_max;  // std::max(a_max, a)
+        }
+        return 3 * v0 / a_max;
+    }
+    constexpr int f[6][4] = {{0, 3, 2, 1}, {4, 5, 6, 7}, {0, 1, 5, 4}, {1, 2, 6, 5}, {2, 3, 7, 6}, {3, 0, 4, 7}};
+    for (int q = 0; q < 6; ++q) {
+        const R a = tri_area(x[f[q][0]], x[f[q][1]], x[f[q][2]]) + tri_area(x[f[q][0]], x[f[q][2]], x[f[q][3]]);
+        a_max = a_max < a ? a : a_max;
+    }
+    return v0 / a_max;
 }
 
 // TledModel::build record (tled_force.hpp:176-192): B0[a][j] = dh_a/dx_j at the

@@ -26,6 +26,8 @@
 #endif
 
 #include "djg.h"
+#include <cub/cub.cuh>
+
 #include "kernels.cuh"
 
 namespace djg {
@@ -75,13 +77,20 @@ inline int const_count(int kind, int model) {
 struct DevBuf {
     void* p = nullptr;
     size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
     void alloc(size_t b) {
+        release();
         bytes = b;
         if (b) CK(cudaMalloc(&p, b));
     }
-    ~DevBuf() {
+    void release() {
         if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
     }
+    ~DevBuf() { release(); }
     template <class T>
     T* as() const { return static_cast<T*>(p); }
 };
@@ -100,6 +109,8 @@ public:
     virtual void info(djg_engine_info* out) = 0;
     virtual void slot_map(int32_t* out) = 0;
     virtual int64_t consts_out(void* out) = 0;
+    virtual int lump_mass(void* out) = 0;
+    virtual int min_char_length(double* out) = 0;
     virtual cudaStream_t stream() const = 0;
     virtual void configure_step(const djg_step_desc& s) = 0;
     virtual void set_policy(int policy) = 0;
@@ -156,98 +167,107 @@ public:
         CK(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, d.device));
         CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
 
-        const int npe = npe_;
-        const int32_t* conn = d.conn;
-        for (int64_t i = 0; i < E_ * npe; ++i)
-            if (conn[i] < 0 || conn[i] >= N_) throw DescError("connectivity index out of range");
+        // Slot layout: from the caller's (or a host-built) CSR, or -- device
+        // precompute without a caller CSR and without slabs -- built on the GPU.
+        device_layout_ = dev_pre && !d.csr_offsets && !(flags_ & DJG_FLAG_SLABS) && slab_bytes_ == 0;
+        if (device_layout_) {
+            build_layout_device(d.conn);
+        } else {
+            const int npe = npe_;
+            const int32_t* conn = d.conn;
+            for (int64_t i = 0; i < E_ * npe; ++i)
+                if (conn[i] < 0 || conn[i] >= N_) throw DescError("connectivity index out of range");
 
-        // Node -> (element, local) adjacency in ascending element order
-        // (NodeElementAdjacency::build, mesh.hpp:299-320).
-        std::vector<int64_t> off_v, elem_v;
-        std::vector<int32_t> loc_v;
-        const int64_t* off = d.csr_offsets;
-        const int64_t* celem = d.csr_elem;
-        const int32_t* cloc = d.csr_local;
-        if (!off || !celem || !cloc) {
-            off_v.assign(size_t(N_) + 1, 0);
-            for (int64_t i = 0; i < E_ * npe; ++i) off_v[size_t(conn[i]) + 1]++;
-            for (int64_t n = 0; n < N_; ++n) off_v[size_t(n) + 1] += off_v[size_t(n)];
-            elem_v.resize(size_t(E_ * npe));
-            loc_v.resize(size_t(E_ * npe));
-            std::vector<int64_t> cur(off_v.begin(), off_v.end() - 1);
-            for (int64_t e = 0; e < E_; ++e)
-                for (int a = 0; a < npe; ++a) {
-                    const int64_t p = cur[size_t(conn[e * npe + a])]++;
-                    elem_v[size_t(p)] = e;
-                    loc_v[size_t(p)] = a;
-                }
-            off = off_v.data();
-            celem = elem_v.data();
-            cloc = loc_v.data();
-        }
-        if (off[0] != 0 || off[N_] != E_ * npe) throw DescError("CSR offsets inconsistent with connectivity");
+            // Node -> (element, local) adjacency in ascending element order
+            // (NodeElementAdjacency::build, mesh.hpp:299-320).
+            std::vector<int64_t> off_v, elem_v;
+            std::vector<int32_t> loc_v;
+            const int64_t* off = d.csr_offsets;
+            const int64_t* celem = d.csr_elem;
+            const int32_t* cloc = d.csr_local;
+            if (!off || !celem || !cloc) {
+                off_v.assign(size_t(N_) + 1, 0);
+                for (int64_t i = 0; i < E_ * npe; ++i) off_v[size_t(conn[i]) + 1]++;
+                for (int64_t n = 0; n < N_; ++n) off_v[size_t(n) + 1] += off_v[size_t(n)];
+                elem_v.resize(size_t(E_ * npe));
+                loc_v.resize(size_t(E_ * npe));
+                std::vector<int64_t> cur(off_v.begin(), off_v.end() - 1);
+                for (int64_t e = 0; e < E_; ++e)
+                    for (int a = 0; a < npe; ++a) {
+                        const int64_t p = cur[size_t(conn[e * npe + a])]++;
+                        elem_v[size_t(p)] = e;
+                        loc_v[size_t(p)] = a;
+                    }
+                off = off_v.data();
+                celem = elem_v.data();
+                cloc = loc_v.data();
+            }
+            if (off[0] != 0 || off[N_] != E_ * npe) throw DescError("CSR offsets inconsistent with connectivity");
 
-        // CSR consistency and row lengths.
-        std::vector<int32_t> row_len(static_cast<size_t>(N_));
-        int wmax = 0;
-        bool bad = false;
-#pragma omp parallel for schedule(static) reduction(|| : bad) reduction(max : wmax)
-        for (int64_t n = 0; n < N_; ++n) {
-            row_len[size_t(n)] = int32_t(off[n + 1] - off[n]);
-            wmax = std::max(wmax, int(off[n + 1] - off[n]));
-            for (int64_t p = off[n]; p < off[n + 1]; ++p) {
-                const int64_t e = celem[p];
-                const int a = cloc[p];
-                if (e < 0 || e >= E_ || a < 0 || a >= npe || conn[e * npe + a] != n) bad = true;
-            }
-        }
-        if (bad) throw DescError("CSR pairs do not match connectivity");
-        wmax_ = std::max(wmax, 1);
-        // Sliced slot layout: node n's k-th slot at slice_base[n/32] + 32k + n%32.
-        // The element kernel finds it from the element's rank k in each of its
-        // nodes' CSR rows (1 or 2 bytes per element-node).
-        if (wmax_ > 65535) throw DescError("a node has more than 65535 incident elements");
-        rank_bytes_ = wmax_ <= 256 ? 1 : 2;
-        std::vector<uint8_t> ranks(size_t(E_ * npe) * size_t(rank_bytes_));
-        {
-            const int64_t S = (N_ + 31) / 32;
-            slice_base_.assign(static_cast<size_t>(S) + 1, 0);
-            int64_t cap = 0;
-            for (int64_t sl = 0; sl < S; ++sl) {
-                slice_base_[size_t(sl)] = int32_t(cap);
-                int w = 0;
-                for (int64_t n = sl * 32; n < std::min<int64_t>(N_, sl * 32 + 32); ++n) w = std::max(w, row_len[size_t(n)]);
-                cap += int64_t(32) * w;
-                if (cap > INT32_MAX) throw DescError("slot buffer exceeds 32-bit indexing");
-            }
-            slice_base_[size_t(S)] = int32_t(cap);
-            capacity_ = std::max<int64_t>(cap, 32);
-            const int rb = rank_bytes_;
-#pragma omp parallel for schedule(static)
-            for (int64_t n = 0; n < N_; ++n)
+            // CSR consistency and row lengths.
+            std::vector<int32_t> row_len(static_cast<size_t>(N_));
+            int wmax = 0;
+            bool bad = false;
+    #pragma omp parallel for schedule(static) reduction(|| : bad) reduction(max : wmax)
+            for (int64_t n = 0; n < N_; ++n) {
+                row_len[size_t(n)] = int32_t(off[n + 1] - off[n]);
+                wmax = std::max(wmax, int(off[n + 1] - off[n]));
                 for (int64_t p = off[n]; p < off[n + 1]; ++p) {
-                    const int64_t k = p - off[n];
-                    uint8_t* r = ranks.data() + size_t((celem[p] * npe + cloc[p]) * rb);
-                    r[0] = uint8_t(k & 0xff);
-                    if (rb == 2) r[1] = uint8_t(k >> 8);
+                    const int64_t e = celem[p];
+                    const int a = cloc[p];
+                    if (e < 0 || e >= E_ || a < 0 || a >= npe || conn[e * npe + a] != n) bad = true;
                 }
-            slicebase_.alloc(slice_base_.size() * sizeof(int32_t));
-            CK(cudaMemcpy(slicebase_.p, slice_base_.data(), slicebase_.bytes, cudaMemcpyHostToDevice));
-            rank_.alloc(ranks.size() + 16);  // + 16: bulk copies of a tail tile round up to 16 bytes
-            CK(cudaMemcpy(rank_.p, ranks.data(), ranks.size(), cudaMemcpyHostToDevice));
-        }
-        plan_slabs(off, celem);
+            }
+            if (bad) throw DescError("CSR pairs do not match connectivity");
+            wmax_ = std::max(wmax, 1);
+            // Sliced slot layout: node n's k-th slot at slice_base[n/32] + 32k + n%32.
+            // The element kernel finds it from the element's rank k in each of its
+            // nodes' CSR rows (1 or 2 bytes per element-node).
+            if (wmax_ > 65535) throw DescError("a node has more than 65535 incident elements");
+            rank_bytes_ = wmax_ <= 256 ? 1 : 2;
+            std::vector<uint8_t> ranks(size_t(E_ * npe) * size_t(rank_bytes_));
+            {
+                const int64_t S = (N_ + 31) / 32;
+                slice_base_.assign(static_cast<size_t>(S) + 1, 0);
+                int64_t cap = 0;
+                for (int64_t sl = 0; sl < S; ++sl) {
+                    slice_base_[size_t(sl)] = int32_t(cap);
+                    int w = 0;
+                    for (int64_t n = sl * 32; n < std::min<int64_t>(N_, sl * 32 + 32); ++n) w = std::max(w, row_len[size_t(n)]);
+                    cap += int64_t(32) * w;
+                    if (cap > INT32_MAX) throw DescError("slot buffer exceeds 32-bit indexing");
+                }
+                slice_base_[size_t(S)] = int32_t(cap);
+                capacity_ = std::max<int64_t>(cap, 32);
+                const int rb = rank_bytes_;
+    #pragma omp parallel for schedule(static)
+                for (int64_t n = 0; n < N_; ++n)
+                    for (int64_t p = off[n]; p < off[n + 1]; ++p) {
+                        const int64_t k = p - off[n];
+                        uint8_t* r = ranks.data() + size_t((celem[p] * npe + cloc[p]) * rb);
+                        r[0] = uint8_t(k & 0xff);
+                        if (rb == 2) r[1] = uint8_t(k >> 8);
+                    }
+                slicebase_.alloc(slice_base_.size() * sizeof(int32_t));
+                CK(cudaMemcpy(slicebase_.p, slice_base_.data(), slicebase_.bytes, cudaMemcpyHostToDevice));
+                rank_.alloc(ranks.size() + 16);  // + 16: bulk copies of a tail tile round up to 16 bytes
+                CK(cudaMemcpy(rank_.p, ranks.data(), ranks.size(), cudaMemcpyHostToDevice));
+            }
+            plan_slabs(off, celem);
 
-        // Upload connectivity as int4 planes.
-        const int nq = npe / 4;
-        {
-            std::vector<int32_t> planes(size_t(E_ * npe));
-#pragma omp parallel for schedule(static)
-            for (int64_t e = 0; e < E_; ++e)
-                for (int q = 0; q < nq; ++q)
-                    for (int k = 0; k < 4; ++k) planes[size_t((int64_t(q) * E_ + e) * 4 + k)] = conn[e * npe + 4 * q + k];
-            conn_.alloc(planes.size() * sizeof(int32_t));
-            CK(cudaMemcpy(conn_.p, planes.data(), conn_.bytes, cudaMemcpyHostToDevice));
+            // Upload connectivity as int4 planes.
+            const int nq = npe / 4;
+            {
+                std::vector<int32_t> planes(size_t(E_ * npe));
+    #pragma omp parallel for schedule(static)
+                for (int64_t e = 0; e < E_; ++e)
+                    for (int q = 0; q < nq; ++q)
+                        for (int k = 0; k < 4; ++k) planes[size_t((int64_t(q) * E_ + e) * 4 + k)] = conn[e * npe + 4 * q + k];
+                conn_.alloc(planes.size() * sizeof(int32_t));
+                CK(cudaMemcpy(conn_.p, planes.data(), conn_.bytes, cudaMemcpyHostToDevice));
+            }
+            rowlen_.alloc(row_len.size() * sizeof(int32_t));
+            CK(cudaMemcpy(rowlen_.p, row_len.data(), rowlen_.bytes, cudaMemcpyHostToDevice));
         }
         // Reference coordinates (device precompute).
         if (d.nodes && dev_pre) {
@@ -332,14 +352,13 @@ public:
             }
             CK(cudaDeviceSynchronize());
         }
+        if (device_layout_) mass_and_length_device(d.material.rho);
         // Node data.
         for (auto& b : u_) b.alloc(size_t(N_) * sizeof(Node));
         uscratch_.alloc(size_t(N_) * sizeof(Node));
         flat_.alloc(size_t(3 * N_) * sizeof(Real));
         ef_.alloc(size_t(capacity_) * sizeof(Node));
         CK(cudaMemset(ef_.p, 0, ef_.bytes));
-        rowlen_.alloc(row_len.size() * sizeof(int32_t));
-        CK(cudaMemcpy(rowlen_.p, row_len.data(), rowlen_.bytes, cudaMemcpyHostToDevice));
         c1_.alloc(size_t(N_) * sizeof(Real));
         code_.alloc(size_t(N_));
         target_.alloc(size_t(3 * N_) * sizeof(Real));
@@ -517,6 +536,142 @@ public:
     // Slab schedule (kernels.cuh, k_node_slices): elements are cut into slabs
     // whose force rows fit in L2; every 32-node slice is gathered right after
     // the slab holding its last (highest-id) element.
+    // Slot layout on the device (see k_count_nodes): CSR rows, ranks, slices,
+    // connectivity planes. Keeps the sorted pairs and row offsets for
+    // mass_and_length_device.
+    void build_layout_device(const int32_t* conn_h) {
+        const int npe = npe_;
+        const int64_t P = E_ * npe;
+        const unsigned gp = unsigned((P + 255) / 256);
+        DevBuf conn, cnt, bad, vals_in, keys_out, rank_of_pair, tmp;
+        conn.alloc(size_t(P) * 4);
+        CK(cudaMemcpy(conn.p, conn_h, conn.bytes, cudaMemcpyHostToDevice));
+        cnt.alloc(size_t(N_ + 1) * 4);
+        CK(cudaMemset(cnt.p, 0, cnt.bytes));
+        bad.alloc(4);
+        CK(cudaMemset(bad.p, 0, 4));
+        k_count_nodes<<<gp, 256>>>(conn.as<int>(), P, N_, cnt.as<int>(), bad.as<int>());
+        CK(cudaGetLastError());
+        int hbad = 0;
+        CK(cudaMemcpy(&hbad, bad.p, 4, cudaMemcpyDeviceToHost));
+        if (hbad) throw DescError("connectivity index out of range");
+        // row offsets (int32: E * npe <= INT32_MAX is checked above)
+        rowoff_.alloc(size_t(N_ + 1) * 4);
+        size_t tb = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt.as<int>(), rowoff_.as<int>(), int(N_ + 1)));
+        tmp.alloc(tb);
+        CK(cub::DeviceScan::ExclusiveSum(tmp.p, tb, cnt.as<int>(), rowoff_.as<int>(), int(N_ + 1)));
+        // stable sort of pair indices by node
+        vals_in.alloc(size_t(P) * 4);
+        keys_out.alloc(size_t(P) * 4);
+        pairs_.alloc(size_t(P) * 4);
+        k_iota<<<gp, 256>>>(vals_in.as<int>(), P);
+        int bits = 1;
+        while ((int64_t(1) << bits) < N_) ++bits;
+        size_t sb = 0;
+        CK(cub::DeviceRadixSort::SortPairs(nullptr, sb, conn.as<int>(), keys_out.as<int>(), vals_in.as<int>(),
+                                           pairs_.as<int>(), P, 0, bits));
+        DevBuf stmp;
+        stmp.alloc(sb);
+        CK(cub::DeviceRadixSort::SortPairs(stmp.p, sb, conn.as<int>(), keys_out.as<int>(), vals_in.as<int>(),
+                                           pairs_.as<int>(), P, 0, bits));
+        rank_of_pair.alloc(size_t(P) * 4);
+        k_ranks_from_sorted<<<gp, 256>>>(keys_out.as<int>(), pairs_.as<int>(), rowoff_.as<int>(), P,
+                                         rank_of_pair.as<int>());
+        CK(cudaGetLastError());
+        // widest row
+        DevBuf dmax;
+        dmax.alloc(4);
+        size_t mb = 0;
+        CK(cub::DeviceReduce::Max(nullptr, mb, cnt.as<int>(), dmax.as<int>(), int(N_)));
+        DevBuf mtmp;
+        mtmp.alloc(mb);
+        CK(cub::DeviceReduce::Max(mtmp.p, mb, cnt.as<int>(), dmax.as<int>(), int(N_)));
+        int wmax = 0;
+        CK(cudaMemcpy(&wmax, dmax.p, 4, cudaMemcpyDeviceToHost));
+        wmax_ = std::max(wmax, 1);
+        if (wmax_ > 65535) throw DescError("a node has more than 65535 incident elements");
+        rank_bytes_ = wmax_ <= 256 ? 1 : 2;
+        // slices: slice_base = exclusive scan of 32 x widest row
+        const int64_t S = (N_ + 31) / 32;
+        DevBuf caps, base64;
+        caps.alloc(size_t(S + 1) * 8);
+        base64.alloc(size_t(S + 1) * 8);
+        k_slice_caps<<<unsigned((S + 1 + 255) / 256), 256>>>(cnt.as<int>(), N_, caps.as<long long>());
+        size_t cb = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, cb, caps.as<long long>(), base64.as<long long>(), int(S + 1)));
+        DevBuf ctmp;
+        ctmp.alloc(cb);
+        CK(cub::DeviceScan::ExclusiveSum(ctmp.p, cb, caps.as<long long>(), base64.as<long long>(), int(S + 1)));
+        long long cap = 0;
+        CK(cudaMemcpy(&cap, base64.as<long long>() + S, 8, cudaMemcpyDeviceToHost));
+        if (cap > INT32_MAX) throw DescError("slot buffer exceeds 32-bit indexing");
+        capacity_ = std::max<int64_t>(cap, 32);
+        slicebase_.alloc(size_t(S + 1) * 4);
+        k_narrow_i64<<<unsigned((S + 1 + 255) / 256), 256>>>(base64.as<long long>(), S + 1, slicebase_.as<int>());
+        slice_base_.resize(size_t(S + 1));
+        CK(cudaMemcpy(slice_base_.data(), slicebase_.p, slicebase_.bytes, cudaMemcpyDeviceToHost));
+        rank_.alloc(size_t(P) * size_t(rank_bytes_) + 16);
+        k_pack_ranks<<<gp, 256>>>(rank_of_pair.as<int>(), P, rank_bytes_, static_cast<unsigned char*>(rank_.p));
+        conn_.alloc(size_t(P) * 4);
+        k_conn_planes<<<unsigned((E_ + 255) / 256), 256>>>(conn.as<int>(), E_, npe, conn_.as<int>());
+        rowlen_.alloc(size_t(N_) * 4);
+        CK(cudaMemcpy(rowlen_.p, cnt.p, rowlen_.bytes, cudaMemcpyDeviceToDevice));
+        CK(cudaGetLastError());
+        CK(cudaDeviceSynchronize());
+        // one slab: the whole mesh
+        slab_off_ = {0, int(S)};
+        slab_elems_ = E_;
+        n_slabs_ = 1;
+    }
+
+    // lump_mass (precompute.hpp:275-287) and the minimum characteristic
+    // length of critical_dt (precompute.hpp:303-331) on the device, from the
+    // coordinates and the sorted CSR pairs; frees the pairs.
+    void mass_and_length_device(double rho) {
+        DevBuf v0, len, lmin, tmp;
+        v0.alloc(size_t(E_) * sizeof(Real));
+        len.alloc(size_t(E_) * sizeof(Real));
+        ElemArgs<Real> a{};
+        a.E = E_;
+        a.conn = conn_.as<int4>();
+        a.X = X_.as<Node>();
+        const unsigned ge = unsigned((E_ + 127) / 128);
+        if (kind_ == DJG_T4) k_volume_length<Real, 0><<<ge, 128>>>(a, v0.as<Real>(), len.as<Real>());
+        else k_volume_length<Real, 1><<<ge, 128>>>(a, v0.as<Real>(), len.as<Real>());
+        CK(cudaGetLastError());
+        lmin.alloc(sizeof(Real));
+        size_t tb = 0;
+        CK(cub::DeviceReduce::Min(nullptr, tb, len.as<Real>(), lmin.as<Real>(), int(E_)));
+        tmp.alloc(tb);
+        CK(cub::DeviceReduce::Min(tmp.p, tb, len.as<Real>(), lmin.as<Real>(), int(E_)));
+        Real h = 0;
+        CK(cudaMemcpy(&h, lmin.p, sizeof(Real), cudaMemcpyDeviceToHost));
+        lmin_ = h;
+        mass_.alloc(size_t(N_) * sizeof(Real));
+        k_lump_mass<Real><<<unsigned((N_ + 255) / 256), 256>>>(pairs_.as<int>(), rowoff_.as<int>(), N_, npe_,
+                                                                v0.as<Real>(), Real(rho), mass_.as<Real>());
+        CK(cudaGetLastError());
+        CK(cudaDeviceSynchronize());
+        pairs_.release();
+        rowoff_.release();
+    }
+
+    int lump_mass(void* out) override {
+        if (!mass_.p) throw DescError("lump_mass on the device needs an engine built with DJG_FLAG_DEVICE_PRECOMPUTE "
+                                      "and no caller CSR");
+        CK(cudaMemcpy(out, mass_.p, mass_.bytes, cudaMemcpyDeviceToHost));
+        return DJG_OK;
+    }
+
+    int min_char_length(double* out) override {
+        if (!mass_.p) throw DescError("the characteristic length on the device needs an engine built with "
+                                      "DJG_FLAG_DEVICE_PRECOMPUTE and no caller CSR");
+        if (!(lmin_ > Real(0))) throw DescError("degenerate element with zero characteristic length");
+        *out = double(lmin_);
+        return DJG_OK;
+    }
+
     void plan_slabs(const int64_t* off, const int64_t* celem) {
         int64_t se = E_;
         if ((flags_ & DJG_FLAG_SLABS) || slab_bytes_ > 0) {
@@ -924,6 +1079,9 @@ private:
     int kind_ = 0, model_ = 0, npe_ = 4, nconst_ = 0, nrec_ = 0, nplanes_ = 0, ntail_ = 0, policy_ = 0, sms_ = 0;
     int64_t tail_stride_ = 0;
     int64_t node_grid_ = 0;
+    bool device_layout_ = false;
+    DevBuf pairs_, rowoff_, mass_;  // device layout: sorted CSR pairs (until masses are built), lump_mass
+    Real lmin_ = 0;
     bool compact_ = false, tled_ = false, pipe_ = false;
     int pipe_blocks_sm_ = 0;
     size_t pipe_smem_ = 0;
@@ -1156,6 +1314,14 @@ int djg_get_slot_map(djg_engine* eng, int32_t* out) {
         e.slot_map(out);
         return DJG_OK;
     });
+}
+
+int djg_lump_mass(djg_engine* eng, void* mass) {
+    return guarded(eng, [&](djg::EngineBase& e) { return e.lump_mass(mass); });
+}
+
+int djg_min_char_length(djg_engine* eng, double* out) {
+    return guarded(eng, [&](djg::EngineBase& e) { return e.min_char_length(out); });
 }
 
 int djg_debug_cbrt(int32_t precision, const void* in, void* out, int64_t n, int32_t device) {

@@ -1547,6 +1547,109 @@ __global__ void k_transpose_consts(const Real* __restrict__ aos, int nconst, int
     }
 }
 
+// ------------------------------------------------------------------ layout on the device
+//
+// NodeElementAdjacency::build (mesh.hpp:299-320) and the engine's slot layout
+// built on the GPU (DJG_FLAG_DEVICE_PRECOMPUTE without a caller CSR): count
+// pairs per node, exclusive scan -> row offsets, stable radix sort of the
+// pair index p = e * npe + a by node (stable: each row keeps ascending
+// element order, exactly the host counting sort's order), rank of a pair =
+// its sorted position - the row offset. Integer work, identical results.
+
+__global__ void k_count_nodes(const int* __restrict__ conn, long long P, long long N, int* __restrict__ cnt,
+                              int* __restrict__ bad) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    const int n = conn[p];
+    if (n < 0 || n >= N) {
+        atomicOr(bad, 1);
+        return;
+    }
+    atomicAdd(cnt + n, 1);
+}
+
+__global__ void k_iota(int* __restrict__ v, long long P) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p < P) v[p] = int(p);
+}
+
+__global__ void k_ranks_from_sorted(const int* __restrict__ keys, const int* __restrict__ vals,
+                                    const int* __restrict__ off, long long P, int* __restrict__ rank_of_pair) {
+    const long long q = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (q < P) rank_of_pair[vals[q]] = int(q - off[keys[q]]);
+}
+
+// 32 x the widest row of each 32-node slice (the slice's slot rows).
+__global__ void k_slice_caps(const int* __restrict__ len, long long N, long long* __restrict__ cap) {
+    const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    const long long S = (N + 31) / 32;
+    if (s > S) return;
+    int w = 0;
+    if (s < S)
+        for (long long n = 32 * s; n < 32 * s + 32 && n < N; ++n) w = max(w, len[n]);
+    cap[s] = 32ll * w;
+}
+
+__global__ void k_narrow_i64(const long long* __restrict__ in, long long n, int* __restrict__ out) {
+    const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = int(in[i]);
+}
+
+__global__ void k_pack_ranks(const int* __restrict__ rank_of_pair, long long P, int rb, unsigned char* __restrict__ out) {
+    const long long p = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p >= P) return;
+    const int k = rank_of_pair[p];
+    out[p * rb] = (unsigned char)(k & 0xff);
+    if (rb == 2) out[p * rb + 1] = (unsigned char)(k >> 8);
+}
+
+__global__ void k_conn_planes(const int* __restrict__ conn, long long E, int npe, int* __restrict__ planes) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    for (int q = 0; q < npe / 4; ++q)
+        for (int k = 0; k < 4; ++k) planes[((long long)q * E + e) * 4 + k] = conn[e * npe + 4 * q + k];
+}
+
+// V0 (element.hpp:59-85) and characteristic_length (precompute.hpp:303-319)
+// of every element from the reference coordinates.
+template <class Real, int KIND>
+__global__ void k_volume_length(const ElemArgs<Real> A, Real* __restrict__ v0_out, Real* __restrict__ len_out) {
+    using T = RT<Real>;
+    constexpr int NPE = KIND == 1 ? 8 : 4;
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= A.E) return;
+    Real x[8][3];
+#pragma unroll
+    for (int q = 0; q < NPE / 4; ++q) {
+        const int4 c = A.conn[(long long)q * A.E + e];
+        const int id[4] = {c.x, c.y, c.z, c.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const typename T::Node v = T::load_node(A.X + id[k]);
+            x[4 * q + k][0] = v.x; x[4 * q + k][1] = v.y; x[4 * q + k][2] = v.z;
+        }
+    }
+#pragma unroll
+    for (int a = NPE; a < 8; ++a) x[a][0] = x[a][1] = x[a][2] = Real(0);
+    Real J[3][3], Ji[3][3], det;
+    Real v0 = Real(0);
+    if (em::jacobian0(KIND, x, J, Ji, det)) v0 = em::volume0(KIND, det);
+    v0_out[e] = v0;
+    len_out[e] = em::char_length(KIND, x, v0);
+}
+
+// lump_mass (precompute.hpp:275-287): every node sums rho V0 / npe of its
+// elements in ascending element order (its sorted CSR row), from +0.
+template <class Real>
+__global__ void k_lump_mass(const int* __restrict__ pairs, const int* __restrict__ off, long long N, int npe,
+                            const Real* __restrict__ v0, Real rho, Real* __restrict__ mass) {
+    const long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    Real acc = Real(0);
+    for (int q = off[n]; q < off[n + 1]; ++q) acc += rho * v0[pairs[q] / npe] / Real(npe);
+    mass[n] = acc;
+}
+
 // Packs flat Real[3N] into padded nodes and back.
 template <class Real>
 __global__ void k_pack_nodes(const Real* __restrict__ flat, long long N, typename RT<Real>::Node* __restrict__ out) {

@@ -104,10 +104,8 @@ int create_from_mesh(const djg_mesh_desc& m, djg_engine** out) {
     const djg::ConstLayout L(m.kind, mat.model);
     std::vector<Real> consts;
     if (on_device) {
-        // the engine builds the records (and rejects inverted elements) on the GPU
-        for (int64_t i = 0; i < int64_t(mesh.conn.size()); ++i)
-            if (mesh.conn[size_t(i)] < 0 || mesh.conn[size_t(i)] >= mesh.num_nodes())
-                throw djg::MeshError("connectivity index out of range", long(i / npe));
+        // the engine checks the connectivity, builds the records and rejects
+        // inverted elements on the GPU
     } else {
         djg::validate_mesh(mesh);
         const djg::Shape<Real> D(m.kind);
@@ -123,7 +121,11 @@ int create_from_mesh(const djg_mesh_desc& m, djg_engine** out) {
             djg::element_record(x, D, mat, fa, fb, c_hg, L, consts.data() + size_t(e) * L.count);
         }
     }
-    const djg::Adjacency adj = djg::build_adjacency(mesh.conn, mesh.num_nodes(), npe);
+    // With device precompute (and no slabs) the engine builds the adjacency
+    // on the GPU as well.
+    const bool device_csr = on_device && !(m.flags & DJG_FLAG_SLABS);
+    djg::Adjacency adj;
+    if (!device_csr) adj = djg::build_adjacency(mesh.conn, mesh.num_nodes(), npe);
     djg_desc d;
     std::memset(&d, 0, sizeof(d));
     d.precision = int32_t(sizeof(Real));
@@ -134,9 +136,9 @@ int create_from_mesh(const djg_mesh_desc& m, djg_engine** out) {
     d.consts = on_device ? nullptr : consts.data();
     d.nconst = L.count;
     d.inversion_policy = m.inversion_policy;
-    d.csr_offsets = adj.offsets.data();
-    d.csr_elem = adj.elem.data();
-    d.csr_local = adj.local.data();
+    d.csr_offsets = device_csr ? nullptr : adj.offsets.data();
+    d.csr_elem = device_csr ? nullptr : adj.elem.data();
+    d.csr_local = device_csr ? nullptr : adj.local.data();
     d.material = m.material;
     d.device = m.device;
     d.flags = m.flags;

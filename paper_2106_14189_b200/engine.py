@@ -127,13 +127,17 @@ class StepReport:
 class GpuDjEngine:
     """DjEngine on the B200 with the simulation state resident in HBM."""
 
-    def __init__(self, scenario: Scenario, device: int = 0, flags: int = 0):
+    def __init__(self, scenario: Scenario, device: int = 0, flags: int = 0, device_csr: bool = False):
+        """device_csr: build the node adjacency / slot layout on the GPU
+        (with DJG_FLAG_DEVICE_PRECOMPUTE) instead of passing the host CSR."""
         self.scenario = scenario
         self.dtype = scenario.dtype
         self.num_nodes = scenario.num_nodes
         self.num_elements = scenario.num_elements
         h = C.c_void_p()
         d = scenario.desc(device, flags)
+        if device_csr:
+            d.csr_offsets = d.csr_elem = d.csr_local = None
         rc = _lib().djg_create(C.byref(d), C.byref(h))
         if rc != A.DJG_OK:
             msg = _lib().djg_create_error().decode()
@@ -242,6 +246,17 @@ class GpuDjEngine:
         out = np.zeros((self.num_elements, n), self.dtype)
         _lib().djg_get_consts(self._h, A.ptr(out))
         return out
+
+    def lump_mass(self) -> np.ndarray:
+        """lump_mass on the device (engines built with device_csr)."""
+        out = np.zeros(self.num_nodes, self.dtype)
+        self._check(_lib().djg_lump_mass(self._h, A.ptr(out)))
+        return out
+
+    def min_char_length(self) -> float:
+        v = C.c_double()
+        self._check(_lib().djg_min_char_length(self._h, C.byref(v)))
+        return v.value
 
     def slot_map(self) -> np.ndarray:
         out = np.zeros(self.scenario.npe * self.num_elements, np.int32)

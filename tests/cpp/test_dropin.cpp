@@ -117,6 +117,44 @@ void inversion_semantics() {
     EXPECT(inv_steps > 0, "no inverted steps reported");
 }
 
+// the precompute on the device (records, adjacency, slot
+// ranks, lump_mass, characteristic lengths) == the reference's host functions.
+template <class Real>
+void device_precompute(ElementKind kind, MaterialModel model, int div, long steps) {
+    const auto mesh = generate_box<Real>({1, 1, 1}, {div, div + 1, div + 2}, kind);
+    const auto mat = bench_material<Real>(model);
+    DjEngine<Real> cpu(mesh, mat);
+    djg::GpuDjEngine<Real> gpu(mesh, mat, Real(0.1), 0, 0, DJG_FLAG_DEVICE_PRECOMPUTE);
+    const auto mass = lump_mass(mesh, mat.rho, cpu.model().elems);
+    const auto gmass = gpu.lump_mass();
+    EXPECT(gmass == mass, "device lump_mass differs from lump_mass");
+    const Real c = dilatational_wave_speed(mat);
+    const Real dt_cpu = critical_dt(mesh, cpu.model().elems, c);
+    EXPECT(gpu.critical_dt(c) == dt_cpu, "device critical_dt differs: %.9g vs %.9g", double(gpu.critical_dt(c)),
+           double(dt_cpu));
+    BoundaryConditions<Real> bcs;
+    for (int n : select_plane_nodes(mesh, Plane::ZMin))
+        for (int a = 0; a < 3; ++a) bcs.fixed.emplace_back(n, a);
+    RunParams<Real> p;
+    p.dt = Real(0.5) * gpu.critical_dt(c);
+    p.t_end = p.dt * Real(steps);
+    p.alpha = relaxation_alpha(mat, mesh);
+    PrescribedRamp<Real> ramp;
+    ramp.nodes = select_plane_nodes(mesh, Plane::ZMax);
+    ramp.axis = 2;
+    ramp.target = Real(-0.2);
+    ramp.t_total = p.t_end;
+    bcs.prescribed.push_back(ramp);
+    const auto bc = DofConstraints<Real>::build(bcs, mesh.num_nodes());
+    const auto r_cpu = djtled::run_simulation(cpu, mass, bc, p);
+    const auto r_gpu = djg::run_simulation(gpu, gmass, bc, p);
+    const double e = rel_err(r_gpu.state.u_curr, r_cpu.state.u_curr);
+    std::printf("device precompute %s-%s f%zu: mass %s, dt %s, run %.3e\n", to_string(kind), to_string(model),
+                8 * sizeof(Real), gmass == mass ? "equal" : "DIFFER", gpu.critical_dt(c) == dt_cpu ? "equal" : "DIFFER",
+                e);
+    EXPECT(e == 0.0, "device-precompute run differs: %.3e", e);
+}
+
 int main() {
     // Bit-identical to the reference: tolerance 0.
     compare_runs<float>(ElementKind::T4, MaterialModel::NeoHookean, 6, 300, 0.0);
@@ -126,6 +164,10 @@ int main() {
     compare_runs<float>(ElementKind::T4, MaterialModel::Orthotropic, 5, 200, 0.0);
     inversion_semantics<double>();
     inversion_semantics<float>();
+    device_precompute<float>(ElementKind::T4, MaterialModel::NeoHookean, 5, 200);
+    device_precompute<double>(ElementKind::T4, MaterialModel::TransverseIsotropic, 4, 150);
+    device_precompute<float>(ElementKind::H8, MaterialModel::Orthotropic, 4, 150);
+    device_precompute<double>(ElementKind::H8, MaterialModel::MooneyRivlin, 3, 100);
     std::printf(g_fail ? "FAILED (%d)\n" : "PASS\n", g_fail);
     return g_fail ? 1 : 0;
 }

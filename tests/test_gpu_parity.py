@@ -9,6 +9,8 @@ rows in ascending element order, and restates glibc's cbrt. The SURVEY §8(c)
 tolerances (1e-5 float, 1e-10 double) are asserted as well, as the contract
 floor, and integers (CSR, slot map) are exact.
 """
+import ctypes as C
+
 import numpy as np
 import pytest
 
@@ -340,3 +342,53 @@ def test_divergence_detector():
         sc = Scenario(spec)
         with GpuDjEngine(sc) as eng:
             eng.step(500)
+
+
+def _wave_speed(m, dtype):
+    """dilatational_wave_speed (material.hpp:117-120) in Real."""
+    kappa, rho = dtype(m.kappa), dtype(m.rho)
+    mu = dtype(2) * (dtype(m.c10) + dtype(m.c01)) if m.model == A.DJG_MR else dtype(m.mu)
+    return np.sqrt((kappa + dtype(4) / dtype(3) * mu) / rho).astype(dtype)
+
+
+@pytest.mark.parametrize("precision", [4, 8])
+@pytest.mark.parametrize("kind,model", [("T4", "NH"), ("T4", "TI"), ("T4", "MR"), ("H8", "NH"), ("H8", "OT")])
+def test_device_layout_and_precompute(kind, model, precision):
+    """with DJG_FLAG_DEVICE_PRECOMPUTE and no caller CSR the
+    adjacency (stable radix sort by node), slot ranks, slices, lump_mass and
+    characteristic lengths are built on the GPU: identical slot map, masses
+    == the host builder (== the reference) bit for bit, critical_dt equal,
+    and the run bit-identical to the oracle."""
+    dtype = np.float32 if precision == 4 else np.float64
+    spec = box_spec(kind=kind, model=model, divisions=(5, 4, 6), precision=precision, ramp_steps=250)
+    sc = Scenario(spec)
+    img = sc.image()
+    fl = A.DJG_FLAG_DEVICE_PRECOMPUTE
+    with GpuDjEngine(sc, flags=fl) as host_layout:
+        smap = host_layout.slot_map()
+        info_h = host_layout.info()
+    with GpuDjEngine(sc, flags=fl, device_csr=True) as eng:
+        assert np.array_equal(eng.slot_map(), smap)
+        info = eng.info()
+        for k in ("slot_capacity", "num_slots", "pipelined", "compact"):
+            assert info[k] == info_h[k], k
+        assert np.array_equal(eng.lump_mass(), img["mass"])
+        dt = dtype(eng.min_char_length()) / _wave_speed(spec.c.material, dtype)
+        assert dtype(dt) == dtype(sc.scalars["critical_dt"])
+        rep = eng.step(250, raise_on_failure=False)
+        u, up, _ = eng.get_state()
+    ur, upr, rr = oracle.run(spec, 250, "oracle")
+    assert rep.status == rr["status"] == 0 and np.array_equal(u, ur) and np.array_equal(up, upr)
+
+
+def test_device_layout_rejects_bad_connectivity():
+    spec = box_spec(kind="T4", divisions=2, precision=4)
+    sc = Scenario(spec)
+    d = sc.desc(0, A.DJG_FLAG_DEVICE_PRECOMPUTE)
+    d.csr_offsets = d.csr_elem = d.csr_local = None
+    conn = np.ctypeslib.as_array(C.cast(C.c_void_p(d.conn), C.POINTER(C.c_int32)), shape=(sc.num_elements * 4,)).copy()
+    conn[7] = sc.num_nodes + 3
+    d.conn = conn.ctypes.data_as(C.c_void_p)
+    h = C.c_void_p()
+    rc = A.load_library().djg_create(C.byref(d), C.byref(h))
+    assert rc == A.DJG_E_CONFIG and b"out of range" in A.load_library().djg_create_error()

@@ -146,11 +146,15 @@ public:
         const bool compact_default = d.kind == DJG_T4 || (sizeof(Real) == 4 && d.material.model != DJG_MR);
         compact_ = !tled_ && ((flags_ & DJG_FLAG_COMPACT) != 0 ||
                               (!(flags_ & DJG_FLAG_FULL_RECORD) && compact_default));
+        // The compact T4 record is empty: the kernel rebuilds J0 from the node
+        // coordinates, so they must be on the device.
+        if (compact_ && d.kind == DJG_T4 && !d.nodes) compact_ = false;
         const bool dev_pre = tled_ || (flags_ & DJG_FLAG_DEVICE_PRECOMPUTE) != 0;
+        need_x_ = dev_pre || (compact_ && d.kind == DJG_T4);
         nrec_ = tled_ ? (kind_ == DJG_H8 ? TledLayout<1>::count : TledLayout<0>::count)
                       : compact_ ? (kind_ == DJG_H8 ? kCompactLen<1> : kCompactLen<0>) : nconst_;
-        // The compact T4 record (J0, 9 Reals) keeps its remainder in scalar
-        // tail planes instead of a padded 16-byte plane.
+        // Tail planes (a remainder of scalar planes instead of a padded 16-byte
+        // plane) apply to the compact T4 record, which is now empty.
         const bool tail = compact_ && kind_ == DJG_T4;
         nplanes_ = tail ? nrec_ / T::kPlane : (nrec_ + T::kPlane - 1) / T::kPlane;
         ntail_ = tail ? nrec_ % T::kPlane : 0;
@@ -270,7 +274,7 @@ public:
             CK(cudaMemcpy(rowlen_.p, row_len.data(), rowlen_.bytes, cudaMemcpyHostToDevice));
         }
         // Reference coordinates (device precompute).
-        if (d.nodes && dev_pre) {
+        if (d.nodes && need_x_) {
             X_.alloc(size_t(N_) * sizeof(Node));
             DevBuf flat;
             flat.alloc(size_t(3 * N_) * sizeof(Real));
@@ -335,7 +339,7 @@ public:
             CK(cudaMemcpy(&first_bad, bad.p, sizeof(first_bad), cudaMemcpyDeviceToHost));
             if (first_bad != ~0ull)
                 throw DescError("element " + std::to_string(first_bad) + ": non-positive reference Jacobian determinant");
-        } else {
+        } else if (nplanes_ + ntail_ > 0) {  // (the compact T4 record is empty)
             const int64_t chunk = std::min<int64_t>(E_, 1 << 20);
             DevBuf stage;
             stage.alloc(size_t(chunk) * nconst_ * sizeof(Real));
@@ -1079,7 +1083,7 @@ private:
     int kind_ = 0, model_ = 0, npe_ = 4, nconst_ = 0, nrec_ = 0, nplanes_ = 0, ntail_ = 0, policy_ = 0, sms_ = 0;
     int64_t tail_stride_ = 0;
     int64_t node_grid_ = 0;
-    bool device_layout_ = false;
+    bool device_layout_ = false, need_x_ = false;
     DevBuf pairs_, rowoff_, mass_;  // device layout: sorted CSR pairs (until masses are built), lump_mass
     Real lmin_ = 0;
     bool compact_ = false, tled_ = false, pipe_ = false;

@@ -291,6 +291,9 @@ struct GlobalSrc {
     }
     __device__ __forceinline__ int slot(const int* __restrict__ sb, int, int n, int k) const { return slot_of(sb, n, k); }
     __device__ __forceinline__ Real tail(int t) const { return __ldcs(A.ctail + t * A.tail_stride + e); }
+    __device__ __forceinline__ typename RT<Real>::Node coord(const ElemArgs<Real>& a, int n) const {
+        return RT<Real>::load_node(a.X + n);
+    }
 };
 
 template <class Real, int TILE>
@@ -313,6 +316,9 @@ struct SmemSrc {
     }
     __device__ __forceinline__ int slot(const int* __restrict__ sb, int, int n, int k) const { return slot_of(sb, n, k); }
     __device__ __forceinline__ Real tail(int t) const { return stail[t * TILE + i]; }
+    __device__ __forceinline__ typename RT<Real>::Node coord(const ElemArgs<Real>& a, int n) const {
+        return RT<Real>::load_node(a.X + n);
+    }
 };
 
 // Gathered inputs of one element, loaded one tile ahead of its computation
@@ -364,15 +370,20 @@ struct PrefetchedSrc {
     }
     __device__ __forceinline__ int slot(const int*, int a, int, int) const { return p.sl[a]; }
     __device__ __forceinline__ Real tail(int t) const { return stail[t * TILE + i]; }
+    __device__ __forceinline__ typename RT<Real>::Node coord(const ElemArgs<Real>& a, int n) const {
+        return RT<Real>::load_node(a.X + n);
+    }
 };
 
-// Compact record kept in HBM. T4: J0 only (9) -- det J0 and V0 are the
-// precompute's own functions of J0 (det3, volume0), recomputed bitwise.
+// Compact record kept in HBM. T4: nothing -- J0 is rebuilt from the node
+// coordinates (gathered like the displacements, mostly L1/L2 hits) with
+// jacobian0's own sums, det J0 and V0 with det3 / volume0, the invariant
+// tensors from J0^-1: all bit-identical to the stored values.
 // H8: J0, det J0, V0, pad, then the hourglass data k_hg, gamma (32) (cheap
 // to store, costly to rebuild: it needs the coordinates and a cube root).
 constexpr int kCompactRecord = 12;
 template <int KIND>
-constexpr int kCompactLen = KIND == 1 ? kCompactRecord + 33 : 9;
+constexpr int kCompactLen = KIND == 1 ? kCompactRecord + 33 : 0;
 
 // Storage of a record of LEN Reals: NFULL 16-byte planes [E], and -- only for
 // the compact T4 record, whose 9 Reals would leave a padded plane -- NTAIL
@@ -421,7 +432,7 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
     constexpr int NC = RP::NFULL * T::kPlane + RP::NTAIL;
     constexpr int KHG = COMPACT ? kCompactRecord : L::khg;  // record index of k_hg (H8)
     constexpr int NPA = L::kH8 ? (KHG + T::kPlane - 1) / T::kPlane : RP::NFULL;  // planes loaded up front
-    Real r[NC];
+    Real r[NC > 0 ? NC : 1];
 #pragma unroll
     for (int p = 0; p < NPA; ++p) {
         const typename T::Plane v = src.plane(p);
@@ -434,14 +445,28 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
 #pragma unroll
     for (int t = 0; t < RP::NTAIL; ++t) r[RP::NFULL * T::kPlane + t] = src.tail(t);
     constexpr int NCU = L::kH8 ? KHG : NC;  // record fields used before the hourglass term
-    Real c[COMPACT ? L::count + 1 : NCU];
+    Real c[COMPACT ? L::count + 1 : (NCU > 0 ? NCU : 1)];
     if constexpr (!COMPACT) {
 #pragma unroll
         for (int k = 0; k < NCU; ++k) c[k] = r[k];
     } else {
         if constexpr (KIND == 0) {
+            // jacobian0 (element.hpp:59-77): J0[i][j] = sum_a D[i][a] x_a[j]
+            // with D[i] = (-1, e_i), summed from +0 in node order; the 0 * x
+            // terms cannot change a sum that is never -0, so
+            // J0[i][j] = (0 + -x_0[j]) + x_{i+1}[j] exactly.
+            Real x0[3];
+            {
+                const typename T::Node v = src.coord(A, nid[0]);
+                x0[0] = Real(0) + -v.x; x0[1] = Real(0) + -v.y; x0[2] = Real(0) + -v.z;
+            }
 #pragma unroll
-            for (int k = 0; k < 9; ++k) c[k] = r[k];
+            for (int i = 0; i < 3; ++i) {
+                const typename T::Node v = src.coord(A, nid[i + 1]);
+                c[3 * i + 0] = x0[0] + v.x;
+                c[3 * i + 1] = x0[1] + v.y;
+                c[3 * i + 2] = x0[2] + v.z;
+            }
             const Real J0[3][3] = {{c[0], c[1], c[2]}, {c[3], c[4], c[5]}, {c[6], c[7], c[8]}};
             c[9] = em::det3(J0);                 // jacobian0 (element.hpp:59-77)
             c[10] = em::volume0(KIND, c[9]);     // volume0 (element.hpp:80-85)

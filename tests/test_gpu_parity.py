@@ -195,6 +195,14 @@ def test_cfg3_first_200_steps():
 
 
 @pytest.mark.slow
+def test_cfg5_full_size_bitwise():
+    """BASELINE configs[4] at full size (50,192,562 tets, the bench problem
+    and loading): 8 steps of a fast +1 % extension ramp, bit-identical to the
+    CPU oracle (all host threads)."""
+    check_run(config_spec("cfg5", precision=4, target=0.01, ramp_steps=8), 8)
+
+
+@pytest.mark.slow
 def test_cfg4_first_100_steps():
     """configs[3] at full size (1,000,000 H8 TI): first 100 steps vs the oracle."""
     check_run(config_spec("cfg4", precision=4, ramp_steps=1100), 100)

@@ -108,6 +108,11 @@ class ClockSampler:
                  "-lms", "50"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi takes ~0.1-0.3 s to report: wait for its first line so
+            # short timed regions are sampled too
+            t0 = time.perf_counter()
+            while not self.lines and time.perf_counter() - t0 < 3.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
 
@@ -183,7 +188,7 @@ def reference_arm(args):
     cb = cpu_reference_sample(steps, max(args.warmup, 1), args.kind, args.model, args.precision)
     line = {
         "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
-        "warmup": args.warmup, "ms_per_step": cb["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": cb["ms_per_step"], "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32" if args.precision == 4 else "f64",
         "data": "synthetic (generate_box unit cube, bench_material)",
         "config": {"workload": f"cfg5 reference sample: {args.kind}-{args.model} box d={SAMPLE_DIVISIONS}",
@@ -206,7 +211,7 @@ def _cpu_baseline_line(args):
 def _line(args, world, K, W, E, ms_step, value, extra):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
-        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong" if world > 1 else "weak",
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32" if args.precision == 4 else "f64",
         "data": "synthetic (generate_box unit cube, bench_material, +1% z-extension ramp)",
         "config": {"workload": f"cfg5: {args.kind}-{args.model} unit cube d={args.divisions}",
@@ -398,17 +403,60 @@ def multi_arm(args, rank, world, device):
     if rep.status != 0:
         raise SystemExit(f"rank {rank}: timed run failed: {rep}")
     value = E / (ms_step * 1e-3)
+
+    # e2e: the same run loop with a host-resident SimState per rank: every step
+    # uploads the rank's u_curr/u_prev (pinned), advances one step (kernels +
+    # halo exchange + agreement) and reads the new u_curr back; wall clock,
+    # max over ranks.
+    import ctypes as C
+
+    from paper_2106_14189_b200 import _abi as A
+    lib = A.load_library()
+    eng = de.eng
+    tdt = torch.float32 if args.precision == 4 else torch.float64
+    nloc = 3 * pi["num_nodes"]
+    uc, upv, st = eng.get_state()
+    bufs = [torch.empty(nloc, dtype=tdt).pin_memory() for _ in range(3)]
+    bufs[0].numpy()[:] = uc
+    bufs[1].numpy()[:] = upv
+    cur, prev, spare = (C.c_void_p(b.data_ptr()) for b in bufs)
+    step_c = C.c_int64(st)
+    rep_c = A.djg_report()
+    torch.cuda.synchronize()
+    dist.barrier()
+    te0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        lib.djg_set_state(eng._h, cur, prev, step_c.value)
+        if lib.djg_step(eng._h, 1, C.byref(rep_c)):
+            raise SystemExit(f"rank {rank}: e2e step failed")
+        lib.djg_get_state(eng._h, spare, None, C.byref(step_c))
+        cur, prev, spare = spare, cur, prev
+    e2e_local = (time.perf_counter() - te0) / args.e2e_steps * 1e3
+    e2e_t = torch.tensor([e2e_local, float(2 * nloc * args.precision), float(nloc * args.precision)],
+                         dtype=torch.float64, device="cuda")
+    mx = e2e_t.clone()
+    dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+    tot = e2e_t.clone()
+    dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+    e2e_ms = float(mx[0].item())
+
     hbm, peak_kind = peaks()
     B = algo_bytes(args.kind, args.model, pi["num_owned"], pi["num_elements"], args.precision)
+    per_step = 2 + (pi["send_total"] > 0) + (pi["recv_total"] > 0) + 2
     if rank == 0:
         extra = {
             "roofline": {"bound": "hbm", "kernel": "step (per GPU)", "achieved": B["step"] / (ms_step * 1e-3) / 1e9,
                          "peak": hbm, "unit": "GB/s", "frac": B["step"] / (ms_step * 1e-3) / 1e9 / hbm,
                          "traffic": None, "peak_source": peak_kind,
                          "note": "rank-0 local elements incl. ghosts / max-over-ranks step time"},
-            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
-                    "mode": "device-resident multi-GPU run loop (no host state per step)"},
-            "gpu_launches": K * 7,
+            "e2e": {"value": E / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(tot[1].item()),
+                    "d2h_bytes_per_step": int(tot[2].item()), "ms_per_step": e2e_ms,
+                    "mode": "per rank and step: djg_set_state (H2D local u_curr+u_prev from pinned host), "
+                            "djg_step(1) (kernels, halo exchange, agreement), djg_get_state (D2H the new local "
+                            "u_curr); wall clock, max over ranks; bytes summed over ranks"},
+            "gpu_launches": K * per_step,
+            "gpu_launches_note": "rank 0: element, node, halo pack / unpack, status, agree per step (NCCL kernels "
+                                 "not counted)",
             "clocks": clk,
             "partition": {"local_elements": pi["num_elements"], "owned_elements": pi["owned_elements"],
                           "halo_send_nodes": pi["send_total"], "neighbors": pi["num_neighbors"]},

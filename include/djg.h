@@ -210,6 +210,18 @@ int djg_halo_unpack(djg_engine* eng, const void* dev_recv);
 int djg_step_status(djg_engine* eng, int64_t* dev_status);
 int djg_step_agree(djg_engine* eng, const int64_t* dev_reduced);
 
+/* Engine-driven multi-GPU step over NCCL (no host work per step). Rank 0
+ * creates a 128-byte NCCL unique id and the caller distributes it; every rank
+ * then calls djg_comm_init (collectively) with its neighbour ranks and the
+ * halo offsets of djg_partition_halo. From then on djg_step / djg_step_async
+ * run, per step and CUDA-graph captured: the local step, halo pack, one
+ * grouped ncclSend/ncclRecv per neighbour, unpack, status, ncclAllReduce(MAX)
+ * and the agreement -- bit-identical to one GPU. libnccl.so.2 is resolved at
+ * run time (the process's, e.g. torch.distributed's). */
+int djg_comm_unique_id(void* id128);
+int djg_comm_init(djg_engine* eng, const void* id128, int32_t nranks, int32_t rank, int32_t num_neighbors,
+                  const int32_t* neighbors, const int64_t* send_off, const int64_t* recv_off);
+
 /* Layout facts for roofline accounting and tests. */
 typedef struct djg_engine_info {
     int64_t num_nodes, num_elements;

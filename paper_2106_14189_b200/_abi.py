@@ -194,6 +194,9 @@ EXPORTS = [
     ("djg_get_info", C.c_int, [C.c_void_p, _P(djg_engine_info)]),
     ("djg_get_slot_map", C.c_int, [C.c_void_p, C.c_void_p]),
     ("djg_lump_mass", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("djg_comm_unique_id", C.c_int, [C.c_void_p]),
+    ("djg_comm_init", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                C.c_void_p]),
     ("djg_min_char_length", C.c_int, [C.c_void_p, _P(C.c_double)]),
     ("djg_get_consts", C.c_int64, [C.c_void_p, C.c_void_p]),
     ("djg_debug_cbrt", C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32]),

@@ -27,6 +27,8 @@
 
 #include "djg.h"
 #include <cub/cub.cuh>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include "kernels.cuh"
 
@@ -95,6 +97,49 @@ struct DevBuf {
     T* as() const { return static_cast<T*>(p); }
 };
 
+// NCCL, resolved at run time from the process's libnccl.so.2 (the one
+// torch.distributed already loaded, else the system library), so libdjg.so
+// has no link-time dependency on it. Only the multi-GPU step uses it.
+struct Nccl {
+    decltype(&ncclGetUniqueId) get_unique_id = nullptr;
+    decltype(&ncclCommInitRank) comm_init_rank = nullptr;
+    decltype(&ncclCommDestroy) comm_destroy = nullptr;
+    decltype(&ncclSend) send = nullptr;
+    decltype(&ncclRecv) recv = nullptr;
+    decltype(&ncclGroupStart) group_start = nullptr;
+    decltype(&ncclGroupEnd) group_end = nullptr;
+    decltype(&ncclAllReduce) all_reduce = nullptr;
+    decltype(&ncclGetErrorString) error_string = nullptr;
+
+    static const Nccl& get() {
+        static const Nccl api = [] {
+            Nccl a;
+            void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+            if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+            if (!h) return a;
+            a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+            a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+            a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+            a.send = reinterpret_cast<decltype(a.send)>(dlsym(h, "ncclSend"));
+            a.recv = reinterpret_cast<decltype(a.recv)>(dlsym(h, "ncclRecv"));
+            a.group_start = reinterpret_cast<decltype(a.group_start)>(dlsym(h, "ncclGroupStart"));
+            a.group_end = reinterpret_cast<decltype(a.group_end)>(dlsym(h, "ncclGroupEnd"));
+            a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+            a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+            return a;
+        }();
+        if (!api.all_reduce) throw std::runtime_error("libnccl.so.2 not found (multi-GPU step)");
+        return api;
+    }
+};
+
+#define NK(x)                                                                                  \
+    do {                                                                                       \
+        const ncclResult_t r_ = (x);                                                           \
+        if (r_ != ncclSuccess)                                                                 \
+            throw CudaError(std::string("NCCL: ") + Nccl::get().error_string(r_) + " (" #x ")"); \
+    } while (0)
+
 class EngineBase {
 public:
     virtual ~EngineBase() = default;
@@ -120,6 +165,8 @@ public:
     virtual void halo_unpack(const void* dev_in) = 0;
     virtual void step_status(int64_t* dev_status) = 0;
     virtual void step_agree(const int64_t* dev_reduced) = 0;
+    virtual void comm_init(const void* id, int nranks, int rank, int nnb, const int32_t* nb, const int64_t* send_off,
+                           const int64_t* recv_off) = 0;
 };
 
 template <class Real>
@@ -167,6 +214,7 @@ public:
         if (!d.c1 != !d.massless) throw DescError("c1 and massless must be given together");
         if (E_ * npe_ > INT32_MAX || N_ > INT32_MAX) throw DescError("mesh too large for 32-bit slot indexing");
 
+        device_ = d.device;
         CK(cudaSetDevice(d.device));
         CK(cudaDeviceGetAttribute(&sms_, cudaDevAttrMultiProcessorCount, d.device));
         CK(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
@@ -530,6 +578,72 @@ public:
         CK(cudaGetLastError());
     }
 
+    // Multi-GPU step driven by the engine itself: after djg_set_partition /
+    // djg_set_halo, a communicator over the ranks and the per-neighbour halo
+    // offsets. Every step then enqueues -- and CUDA-graph captures -- the
+    // element and node kernels, the halo pack, one grouped NCCL send/recv per
+    // neighbour, the unpack, the failure status, its allreduce(MAX) and the
+    // agreement: no host round trip per step.
+    void comm_init(const void* id, int nranks, int rank, int nnb, const int32_t* nb, const int64_t* send_off,
+                   const int64_t* recv_off) override {
+        if (!elemL2g_.p) throw DescError("djg_comm_init needs djg_set_partition with elem_l2g first");
+        if (nranks < 1 || rank < 0 || rank >= nranks || nnb < 0) throw DescError("invalid rank / neighbour count");
+        if (nnb > 0 && (!nb || !send_off || !recv_off)) throw DescError("neighbour lists missing");
+        nbr_.assign(nb, nb + nnb);
+        send_off_.assign(send_off, send_off + (nnb ? nnb + 1 : 0));
+        recv_off_.assign(recv_off, recv_off + (nnb ? nnb + 1 : 0));
+        for (int k = 0; k < nnb; ++k)
+            if (nbr_[size_t(k)] < 0 || nbr_[size_t(k)] >= nranks || nbr_[size_t(k)] == rank)
+                throw DescError("invalid neighbour rank");
+        if (nnb && (send_off_.front() != 0 || send_off_.back() != nsend_ || recv_off_.front() != 0 ||
+                    recv_off_.back() != nrecv_))
+            throw DescError("halo offsets do not match djg_set_halo");
+        const Nccl& api = Nccl::get();
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof(uid));
+        CK(cudaSetDevice(device_));
+        if (comm_) api.comm_destroy(static_cast<ncclComm_t>(comm_));
+        ncclComm_t c = nullptr;
+        NK(api.comm_init_rank(&c, nranks, uid, rank));
+        comm_ = c;
+        sendBuf_.alloc(size_t(std::max<int64_t>(nsend_, 1)) * sizeof(Node));
+        recvBuf_.alloc(size_t(std::max<int64_t>(nrecv_, 1)) * sizeof(Node));
+        status_.alloc(2 * sizeof(int64_t));
+        drop_graphs();
+    }
+
+    void launch_exchange(cudaStream_t s) {
+        const Nccl& api = Nccl::get();
+        ncclComm_t c = static_cast<ncclComm_t>(comm_);
+        constexpr int kPer = int(sizeof(Node) / sizeof(Real));  // Reals per halo row
+        const ncclDataType_t dt = sizeof(Real) == 4 ? ncclFloat32 : ncclFloat64;
+        if (nsend_) {
+            k_halo_pack<Real><<<unsigned((nsend_ + 255) / 256), 256, 0, s>>>(
+                ctrl_.as<Ctrl>(), u_[0].as<Node>(), u_[1].as<Node>(), u_[2].as<Node>(), haloSend_.as<int>(), nsend_,
+                sendBuf_.as<Node>());
+            CK(cudaGetLastError());
+        }
+        if (!nbr_.empty()) {
+            NK(api.group_start());
+            for (size_t k = 0; k < nbr_.size(); ++k) {
+                const int64_t s0 = send_off_[k], s1 = send_off_[k + 1], r0 = recv_off_[k], r1 = recv_off_[k + 1];
+                if (s1 > s0) NK(api.send(sendBuf_.as<Node>() + s0, size_t(s1 - s0) * kPer, dt, nbr_[k], c, s));
+                if (r1 > r0) NK(api.recv(recvBuf_.as<Node>() + r0, size_t(r1 - r0) * kPer, dt, nbr_[k], c, s));
+            }
+            NK(api.group_end());
+        }
+        if (nrecv_) {
+            k_halo_unpack<Real><<<unsigned((nrecv_ + 255) / 256), 256, 0, s>>>(
+                ctrl_.as<Ctrl>(), u_[0].as<Node>(), u_[1].as<Node>(), u_[2].as<Node>(), haloRecv_.as<int>(), nrecv_,
+                recvBuf_.as<Node>());
+            CK(cudaGetLastError());
+        }
+        k_step_status<<<1, 1, 0, s>>>(ctrl_.as<Ctrl>(), elemL2g_.as<long long>(), status_.as<long long>());
+        NK(api.all_reduce(status_.p, status_.p, 2, ncclInt64, ncclMax, c, s));
+        k_agree<<<1, 1, 0, s>>>(ctrl_.as<Ctrl>(), status_.as<long long>());
+        CK(cudaGetLastError());
+    }
+
     void set_policy(int policy) override {
         if (policy != DJG_ABORT && policy != DJG_SKIP_AND_REPORT) throw DescError("unknown inversion policy");
         policy_ = policy;
@@ -706,6 +820,7 @@ public:
     }
 
     ~Engine() override {
+        if (comm_) Nccl::get().comm_destroy(static_cast<ncclComm_t>(comm_));
         if (graph_big_) cudaGraphExecDestroy(graph_big_);
         if (graph_one_) cudaGraphExecDestroy(graph_one_);
         if (hctrl_) cudaFreeHost(hctrl_);
@@ -906,7 +1021,10 @@ public:
     cudaGraphExec_t capture(int steps) {
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
-        for (int i = 0; i < steps; ++i) launch_step(stream_);
+        for (int i = 0; i < steps; ++i) {
+            launch_step(stream_);
+            if (comm_) launch_exchange(stream_);
+        }
         CK(cudaStreamEndCapture(stream_, &g));
         cudaGraphExec_t ex;
         CK(cudaGraphInstantiate(&ex, g, 0));
@@ -921,7 +1039,10 @@ public:
         // host: sync() reports the difference.
         CK(cudaMemcpyAsync(hstart_, ctrl_.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream_));
         if (flags_ & DJG_FLAG_NO_GRAPH) {
-            for (int64_t i = 0; i < n; ++i) launch_step(stream_);
+            for (int64_t i = 0; i < n; ++i) {
+                launch_step(stream_);
+                if (comm_) launch_exchange(stream_);
+            }
             return;
         }
         if (n >= kGraphSteps && !graph_big_) graph_big_ = capture(kGraphSteps);
@@ -1084,6 +1205,11 @@ private:
     int64_t tail_stride_ = 0;
     int64_t node_grid_ = 0;
     bool device_layout_ = false, need_x_ = false;
+    void* comm_ = nullptr;  // ncclComm_t of the multi-GPU step
+    int device_ = 0;
+    std::vector<int32_t> nbr_;
+    std::vector<int64_t> send_off_, recv_off_;
+    DevBuf sendBuf_, recvBuf_, status_;
     DevBuf pairs_, rowoff_, mass_;  // device layout: sorted CSR pairs (until masses are built), lump_mass
     Real lmin_ = 0;
     bool compact_ = false, tled_ = false, pipe_ = false;
@@ -1316,6 +1442,33 @@ int djg_get_info(djg_engine* eng, djg_engine_info* info) {
 int djg_get_slot_map(djg_engine* eng, int32_t* out) {
     return guarded(eng, [&](djg::EngineBase& e) {
         e.slot_map(out);
+        return DJG_OK;
+    });
+}
+
+int djg_comm_unique_id(void* id) {
+    if (!id) return DJG_E_CONFIG;
+    try {
+        const djg::Nccl& api = djg::Nccl::get();
+        ncclUniqueId uid;
+        const ncclResult_t r = api.get_unique_id(&uid);
+        if (r != ncclSuccess) {
+            djg_internal_set_create_error(api.error_string(r));
+            return DJG_E_CUDA;
+        }
+        std::memcpy(id, &uid, sizeof(uid));
+        return DJG_OK;
+    } catch (const std::exception& e) {
+        djg_internal_set_create_error(e.what());
+        return DJG_E_CUDA;
+    }
+}
+
+int djg_comm_init(djg_engine* eng, const void* id, int32_t nranks, int32_t rank, int32_t num_neighbors,
+                  const int32_t* neighbors, const int64_t* send_off, const int64_t* recv_off) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        if (!id) throw djg::DescError("null unique id");
+        e.comm_init(id, nranks, rank, num_neighbors, neighbors, send_off, recv_off);
         return DJG_OK;
     });
 }

@@ -147,9 +147,15 @@ def _torch_dtype(dtype):
 
 
 class DistributedEngine:
-    """This rank's part of a multi-GPU run over torch.distributed (NCCL)."""
+    """This rank's part of a multi-GPU run over torch.distributed (NCCL).
 
-    def __init__(self, scenario: Scenario, device: int, group=None, flags: int = 0):
+    engine_comm=True (default): torch.distributed only distributes an NCCL
+    unique id; the engine then runs every step -- kernels, halo send/recv,
+    status allreduce -- itself, CUDA-graph captured (djg_comm_init).
+    engine_comm=False: the same sequence driven from Python per step with
+    torch.distributed P2P / allreduce (reference driver for tests)."""
+
+    def __init__(self, scenario: Scenario, device: int, group=None, flags: int = 0, engine_comm: bool = True):
         import torch
         import torch.distributed as dist
         self.dist = dist
@@ -157,6 +163,7 @@ class DistributedEngine:
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
         self.device = device
+        self.engine_comm = engine_comm
         self.part = Partition(scenario, self.world, self.rank)
         self.eng = PartEngine(self.part, device, flags)
         tdt = _torch_dtype(self.part.dtype)
@@ -165,6 +172,17 @@ class DistributedEngine:
         self.recv = torch.zeros((max(self.part.recv_nodes.size, 1), 4), dtype=tdt, device=dev)
         self.status = torch.zeros(2, dtype=torch.int64, device=dev)
         self.stream = torch.cuda.ExternalStream(self.eng.stream, device=dev)
+        if engine_comm:
+            uid = C.create_string_buffer(128)
+            if self.rank == 0 and _lib().djg_comm_unique_id(uid) != A.DJG_OK:
+                raise RuntimeError(_lib().djg_create_error().decode())
+            box = [bytes(uid.raw)]
+            dist.broadcast_object_list(box, src=dist.get_global_rank(group, 0) if group else 0, group=group)
+            uid = C.create_string_buffer(box[0], 128)
+            p = self.part
+            nb = np.ascontiguousarray(p.neighbors, np.int32)
+            self.eng._check(_lib().djg_comm_init(self.eng._h, uid, self.world, self.rank, int(nb.size), A.ptr(nb),
+                                                 A.ptr(p.send_off), A.ptr(p.recv_off)))
 
     def _exchange(self):
         dist = self.dist
@@ -183,6 +201,9 @@ class DistributedEngine:
 
     def step_async(self, nsteps: int):
         import torch
+        if self.engine_comm:
+            self.eng.step_async(nsteps)
+            return
         with torch.cuda.stream(self.stream):
             for _ in range(nsteps):
                 self.eng.step_async(1)

@@ -65,9 +65,12 @@ def _port():
         return s.getsockname()[1]
 
 
-def test_distributed_engine_single_rank_nccl():
+@pytest.mark.parametrize("engine_comm", [True, False], ids=["engine-nccl", "python-driver"])
+def test_distributed_engine_single_rank_nccl(engine_comm):
     """The torch.distributed (NCCL) driver on one rank: same bits as the
-    plain engine (the halo is empty, the status allreduce is real)."""
+    plain engine (the halo is empty, the status allreduce is real). With
+    engine_comm the engine's own NCCL communicator runs inside its CUDA
+    graphs (djg_comm_init)."""
     import torch
     import torch.distributed as dist
     from paper_2106_14189_b200.parallel import DistributedEngine
@@ -76,10 +79,20 @@ def test_distributed_engine_single_rank_nccl():
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_port()}", rank=0, world_size=1,
                             device_id=torch.device("cuda", 0))
     try:
-        de = DistributedEngine(Scenario(spec), device=0)
+        de = DistributedEngine(Scenario(spec), device=0, engine_comm=engine_comm)
         r = de.step(100)
         U, UP, step = de.gather_global()
         assert r.status == 0 and step == 100
         assert np.array_equal(U, u1)
+        # failure agreement through the allreduce: an inverting problem halts
+        # at the same step and element as the plain engine
+        inv = box_spec(kind="T4", divisions=3, extent=(0.1,) * 3, precision=8, target=-0.09, ramp_steps=3,
+                       fix_all_axes=True)
+        with GpuDjEngine(Scenario(inv)) as e1:
+            r1 = e1.step(50, raise_on_failure=False)
+        de2 = DistributedEngine(Scenario(inv), device=0, engine_comm=engine_comm)
+        r2 = de2.step(50, raise_on_failure=False)
+        assert r1.status in (A.DJG_E_INVERSION, A.DJG_E_DIVERGENCE)
+        assert r1.status == r2.status and r1.fail_step == r2.fail_step and r1.first_inverted == r2.first_inverted
     finally:
         dist.destroy_process_group()

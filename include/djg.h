@@ -219,6 +219,19 @@ int djg_step_agree(djg_engine* eng, const int64_t* dev_reduced);
  * and the agreement -- bit-identical to one GPU. libnccl.so.2 is resolved at
  * run time (the process's, e.g. torch.distributed's). */
 int djg_comm_unique_id(void* id128);
+/* Overlapped multi-part step: the part's local elements [0, num_interior)
+ * reference no ghost node (djg_partition_info.interior_elements; the
+ * partitioner orders them first). With a communicator the captured step
+ * becomes: halo pack -> {interior elements || NCCL halo send/recv} -> unpack
+ * -> boundary elements -> node update -> status allreduce -> agreement, the
+ * exchange hidden behind the interior elements (the ghost values used are
+ * those of the step start, as before). Without one, a caller drives the same
+ * order itself: djg_halo_pack, djg_step_interior, <exchange>,
+ * djg_halo_unpack, djg_step_boundary, djg_step_status, <allreduce>,
+ * djg_step_agree. */
+int djg_set_interior(djg_engine* eng, int64_t num_interior);
+int djg_step_interior(djg_engine* eng);
+int djg_step_boundary(djg_engine* eng);
 int djg_comm_init(djg_engine* eng, const void* id128, int32_t nranks, int32_t rank, int32_t num_neighbors,
                   const int32_t* neighbors, const int64_t* send_off, const int64_t* recv_off);
 

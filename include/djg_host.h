@@ -71,6 +71,7 @@ typedef struct djg_partition_info {
     int64_t owned_elements;   /* elements assigned to this part */
     int64_t send_total, recv_total;
     int64_t global_nodes, global_elements;
+    int64_t interior_elements;  /* local elements [0, interior) reference no ghost node */
 } djg_partition_info;
 
 int djg_partition_build(const djg_scenario* sc, int32_t nparts, int32_t part, djg_partition** out);

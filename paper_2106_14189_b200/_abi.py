@@ -144,7 +144,7 @@ class djg_partition_info(C.Structure):
         ("nparts", C.c_int32), ("part", C.c_int32), ("num_neighbors", C.c_int32), ("_pad", C.c_int32),
         ("num_nodes", C.c_int64), ("num_owned", C.c_int64), ("num_elements", C.c_int64),
         ("owned_elements", C.c_int64), ("send_total", C.c_int64), ("recv_total", C.c_int64),
-        ("global_nodes", C.c_int64), ("global_elements", C.c_int64),
+        ("global_nodes", C.c_int64), ("global_elements", C.c_int64), ("interior_elements", C.c_int64),
     ]
 
 
@@ -195,6 +195,9 @@ EXPORTS = [
     ("djg_get_slot_map", C.c_int, [C.c_void_p, C.c_void_p]),
     ("djg_lump_mass", C.c_int, [C.c_void_p, C.c_void_p]),
     ("djg_comm_unique_id", C.c_int, [C.c_void_p]),
+    ("djg_set_interior", C.c_int, [C.c_void_p, C.c_int64]),
+    ("djg_step_interior", C.c_int, [C.c_void_p]),
+    ("djg_step_boundary", C.c_int, [C.c_void_p]),
     ("djg_comm_init", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
                                 C.c_void_p]),
     ("djg_min_char_length", C.c_int, [C.c_void_p, _P(C.c_double)]),

@@ -167,6 +167,9 @@ public:
     virtual void step_agree(const int64_t* dev_reduced) = 0;
     virtual void comm_init(const void* id, int nranks, int rank, int nnb, const int32_t* nb, const int64_t* send_off,
                            const int64_t* recv_off) = 0;
+    virtual void set_interior(int64_t n) = 0;
+    virtual void step_interior() = 0;
+    virtual void step_boundary() = 0;
 };
 
 template <class Real>
@@ -429,6 +432,7 @@ public:
         ea_.tail_stride = tail_stride_;
         for (int i = 0; i < 3; ++i) ea_.u[i] = u_[i].as<Node>();
         ea_.u_override = nullptr;
+        ea_.elem_l2g = nullptr;
         ea_.ef = ef_.as<Node>();
         ea_.ctrl = ctrl_.as<Ctrl>();
         const Real mu = Real(d.material.mu), c10 = Real(d.material.c10);
@@ -533,6 +537,7 @@ public:
         if (elem_l2g) {
             elemL2g_.alloc(size_t(E_) * sizeof(int64_t));
             CK(cudaMemcpy(elemL2g_.p, elem_l2g, elemL2g_.bytes, cudaMemcpyHostToDevice));
+            ea_.elem_l2g = elemL2g_.as<long long>();
         }
         drop_graphs();
     }
@@ -606,6 +611,11 @@ public:
         ncclComm_t c = nullptr;
         NK(api.comm_init_rank(&c, nranks, uid, rank));
         comm_ = c;
+        if (!side_) {
+            CK(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+            CK(cudaEventCreateWithFlags(&evFork_, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&evJoin_, cudaEventDisableTiming));
+        }
         sendBuf_.alloc(size_t(std::max<int64_t>(nsend_, 1)) * sizeof(Node));
         recvBuf_.alloc(size_t(std::max<int64_t>(nrecv_, 1)) * sizeof(Node));
         status_.alloc(2 * sizeof(int64_t));
@@ -638,6 +648,73 @@ public:
                 recvBuf_.as<Node>());
             CK(cudaGetLastError());
         }
+        k_step_status<<<1, 1, 0, s>>>(ctrl_.as<Ctrl>(), elemL2g_.as<long long>(), status_.as<long long>());
+        NK(api.all_reduce(status_.p, status_.p, 2, ncclInt64, ncclMax, c, s));
+        k_agree<<<1, 1, 0, s>>>(ctrl_.as<Ctrl>(), status_.as<long long>());
+        CK(cudaGetLastError());
+    }
+
+    // ---- overlapped multi-part step: pack -> {interior elements || halo
+    // exchange} -> unpack -> boundary elements -> node update -> status /
+    // agreement. Local elements [0, split) reference no ghost node
+    // (djg_set_interior; the partition builder orders them first).
+    int64_t split_point() const { return interior_ < 0 ? E_ : interior_; }
+
+    void set_interior(int64_t n) override {
+        if (n < 0 || n > E_) throw DescError("interior element count out of range");
+        if (n_slabs_ != 1) throw DescError("the split step needs the one-slab schedule");
+        interior_ = n / kPipeTile * kPipeTile;  // tile-aligned ranges for the bulk copies
+        drop_graphs();
+    }
+
+    void launch_pack(cudaStream_t s, Node* out) {
+        if (!nsend_) return;
+        k_halo_pack<Real><<<unsigned((nsend_ + 255) / 256), 256, 0, s>>>(
+            ctrl_.as<Ctrl>(), u_[0].as<Node>(), u_[1].as<Node>(), u_[2].as<Node>(), haloSend_.as<int>(), nsend_, out);
+        CK(cudaGetLastError());
+    }
+
+    void launch_unpack(cudaStream_t s, const Node* in) {
+        if (!nrecv_) return;
+        k_halo_unpack<Real><<<unsigned((nrecv_ + 255) / 256), 256, 0, s>>>(
+            ctrl_.as<Ctrl>(), u_[0].as<Node>(), u_[1].as<Node>(), u_[2].as<Node>(), haloRecv_.as<int>(), nrecv_, in);
+        CK(cudaGetLastError());
+    }
+
+    void step_interior() override {
+        if (!configured_) throw DescError("step data not configured (djg_configure_step)");
+        launch_element(stream_, 0, split_point());
+    }
+
+    void step_boundary() override {
+        launch_element(stream_, split_point(), E_);
+        launch_node(stream_, 0, false);
+    }
+
+    // One overlapped step with the engine's NCCL communicator (captured).
+    void launch_overlapped_step(cudaStream_t s) {
+        const Nccl& api = Nccl::get();
+        ncclComm_t c = static_cast<ncclComm_t>(comm_);
+        constexpr int kPer = int(sizeof(Node) / sizeof(Real));
+        const ncclDataType_t dt = sizeof(Real) == 4 ? ncclFloat32 : ncclFloat64;
+        launch_pack(s, sendBuf_.as<Node>());
+        CK(cudaEventRecord(evFork_, s));
+        CK(cudaStreamWaitEvent(side_, evFork_, 0));
+        pipe_spare_sms_ = kSpareSms;  // leave SMs for the NCCL kernels
+        launch_element(side_, 0, split_point());
+        pipe_spare_sms_ = 0;
+        NK(api.group_start());
+        for (size_t k = 0; k < nbr_.size(); ++k) {
+            const int64_t s0 = send_off_[k], s1 = send_off_[k + 1], r0 = recv_off_[k], r1 = recv_off_[k + 1];
+            if (s1 > s0) NK(api.send(sendBuf_.as<Node>() + s0, size_t(s1 - s0) * kPer, dt, nbr_[k], c, s));
+            if (r1 > r0) NK(api.recv(recvBuf_.as<Node>() + r0, size_t(r1 - r0) * kPer, dt, nbr_[k], c, s));
+        }
+        NK(api.group_end());
+        launch_unpack(s, recvBuf_.as<Node>());
+        CK(cudaEventRecord(evJoin_, side_));
+        CK(cudaStreamWaitEvent(s, evJoin_, 0));
+        launch_element(s, split_point(), E_);
+        launch_node(s, 0, false);
         k_step_status<<<1, 1, 0, s>>>(ctrl_.as<Ctrl>(), elemL2g_.as<long long>(), status_.as<long long>());
         NK(api.all_reduce(status_.p, status_.p, 2, ncclInt64, ncclMax, c, s));
         k_agree<<<1, 1, 0, s>>>(ctrl_.as<Ctrl>(), status_.as<long long>());
@@ -821,6 +898,9 @@ public:
 
     ~Engine() override {
         if (comm_) Nccl::get().comm_destroy(static_cast<ncclComm_t>(comm_));
+        if (evFork_) cudaEventDestroy(evFork_);
+        if (evJoin_) cudaEventDestroy(evJoin_);
+        if (side_) cudaStreamDestroy(side_);
         if (graph_big_) cudaGraphExecDestroy(graph_big_);
         if (graph_one_) cudaGraphExecDestroy(graph_one_);
         if (hctrl_) cudaFreeHost(hctrl_);
@@ -923,7 +1003,8 @@ public:
                 return nb > 0;
             }
             const int64_t tiles = (e1 - e0 + kPipeTile - 1) / kPipeTile;
-            const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(pipe_blocks_sm_) * sms_)));
+            const int64_t sms = std::max(1, sms_ - pipe_spare_sms_);
+            const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(pipe_blocks_sm_) * sms)));
             kern<<<grid, kPipeThreads, smem, s>>>(a, e0, e1);
             return true;
         }
@@ -931,6 +1012,7 @@ public:
 
     void launch_element(cudaStream_t s, int64_t e0, int64_t e1, const Node* u_override = nullptr,
                         bool setup = false) {
+        if (e1 <= e0 && !setup) return;
         ElemArgs<Real> a = ea_;
         a.u_override = u_override;
         const unsigned grid = unsigned((e1 - e0 + 127) / 128);
@@ -1012,6 +1094,15 @@ public:
         CK(cudaGetLastError());
     }
 
+    void one_step(cudaStream_t s) {
+        if (comm_ && interior_ >= 0) {
+            launch_overlapped_step(s);
+        } else {
+            launch_step(s);
+            if (comm_) launch_exchange(s);
+        }
+    }
+
     void drop_graphs() {
         if (graph_big_) cudaGraphExecDestroy(graph_big_);
         if (graph_one_) cudaGraphExecDestroy(graph_one_);
@@ -1021,10 +1112,7 @@ public:
     cudaGraphExec_t capture(int steps) {
         cudaGraph_t g;
         CK(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal));
-        for (int i = 0; i < steps; ++i) {
-            launch_step(stream_);
-            if (comm_) launch_exchange(stream_);
-        }
+        for (int i = 0; i < steps; ++i) one_step(stream_);
         CK(cudaStreamEndCapture(stream_, &g));
         cudaGraphExec_t ex;
         CK(cudaGraphInstantiate(&ex, g, 0));
@@ -1039,10 +1127,7 @@ public:
         // host: sync() reports the difference.
         CK(cudaMemcpyAsync(hstart_, ctrl_.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream_));
         if (flags_ & DJG_FLAG_NO_GRAPH) {
-            for (int64_t i = 0; i < n; ++i) {
-                launch_step(stream_);
-                if (comm_) launch_exchange(stream_);
-            }
+            for (int64_t i = 0; i < n; ++i) one_step(stream_);
             return;
         }
         if (n >= kGraphSteps && !graph_big_) graph_big_ = capture(kGraphSteps);
@@ -1210,6 +1295,11 @@ private:
     std::vector<int32_t> nbr_;
     std::vector<int64_t> send_off_, recv_off_;
     DevBuf sendBuf_, recvBuf_, status_;
+    int64_t interior_ = -1;            // split step: local elements [0, interior_) touch no ghost node
+    int pipe_spare_sms_ = 0;           // SMs the pipelined element kernel leaves free
+    static constexpr int kSpareSms = 4;
+    cudaStream_t side_ = nullptr;      // interior elements of the overlapped step
+    cudaEvent_t evFork_ = nullptr, evJoin_ = nullptr;
     DevBuf pairs_, rowoff_, mass_;  // device layout: sorted CSR pairs (until masses are built), lump_mass
     Real lmin_ = 0;
     bool compact_ = false, tled_ = false, pipe_ = false;
@@ -1469,6 +1559,27 @@ int djg_comm_init(djg_engine* eng, const void* id, int32_t nranks, int32_t rank,
     return guarded(eng, [&](djg::EngineBase& e) {
         if (!id) throw djg::DescError("null unique id");
         e.comm_init(id, nranks, rank, num_neighbors, neighbors, send_off, recv_off);
+        return DJG_OK;
+    });
+}
+
+int djg_set_interior(djg_engine* eng, int64_t num_interior) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.set_interior(num_interior);
+        return DJG_OK;
+    });
+}
+
+int djg_step_interior(djg_engine* eng) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.step_interior();
+        return DJG_OK;
+    });
+}
+
+int djg_step_boundary(djg_engine* eng) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.step_boundary();
         return DJG_OK;
     });
 }

@@ -134,6 +134,8 @@ struct ElemArgs {
     const void* rank;                    // per element: npe ranks (uint8 or uint16) of the element
                                          // in its nodes' CSR rows, packed in one 4/8/16-byte word
     const int* slice_base;               // first slot of each 32-node slice
+    const long long* elem_l2g;           // multi-part: global id of each local element (inversions
+                                         // are reported in global ids), else NULL
     const typename RT<Real>::Plane* c;   // nplanes planes of Plane[E]
     const Real* ctail;                   // record remainder planes (compact T4): Real[tail_stride]
     long long tail_stride;
@@ -530,7 +532,7 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
     if (!(det > Real(0))) {
         // record_inversion (djtled_force.hpp:107-112) + zeroed rows (:187-191).
         atomicAdd(&A.ctrl->inv_count, 1ull);
-        atomicMin(&A.ctrl->first_inv, (unsigned long long)e);
+        atomicMin(&A.ctrl->first_inv, (unsigned long long)(A.elem_l2g ? A.elem_l2g[e] : e));
 #pragma unroll
         for (int a = 0; a < NPE; ++a) store_row(A, sl[a], Real(0), Real(0), Real(0));
         return;
@@ -784,7 +786,7 @@ __device__ __forceinline__ void element_body_tled(const ElemArgs<Real>& A, const
     const Real J = em::det3(X);
     if (!(J > Real(0))) {
         atomicAdd(&A.ctrl->inv_count, 1ull);
-        atomicMin(&A.ctrl->first_inv, (unsigned long long)e);
+        atomicMin(&A.ctrl->first_inv, (unsigned long long)(A.elem_l2g ? A.elem_l2g[e] : e));
 #pragma unroll
         for (int a = 0; a < NPE; ++a) store_row(A, sl[a], Real(0), Real(0), Real(0));
         return;
@@ -1451,8 +1453,9 @@ __global__ void k_step_status(const Ctrl* ctrl, const long long* __restrict__ el
     const int h = ctrl->halted;
     const long long none = -0x7fffffffffffffffll - 1;
     status[0] = h == 4 ? 2 : (h == 5 ? 1 : 0);
+    (void)elem_l2g;  // inversions are recorded in global ids already (ElemArgs::elem_l2g)
     if (h != 4 || ctrl->halt_first_inv < 0) status[1] = none;
-    else status[1] = -(ctrl->agreed ? ctrl->halt_first_inv : elem_l2g[ctrl->halt_first_inv]);
+    else status[1] = -ctrl->halt_first_inv;
 }
 
 __global__ void k_agree(Ctrl* ctrl, const long long* __restrict__ reduced) {

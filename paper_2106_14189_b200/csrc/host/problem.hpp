@@ -780,6 +780,7 @@ struct PartProblem {
     Problem<Real> local;
     int nparts = 1, part = 0;
     int64_t num_owned = 0, global_nodes = 0, global_elements = 0, owned_elements = 0;
+    int64_t interior_elements = 0;  // local elements [0, interior) reference no ghost node
     std::vector<int64_t> node_l2g, elem_l2g;
     Halo halo;
 };
@@ -825,6 +826,21 @@ inline PartProblem<Real> build_part(const Problem<Real>& P, int nparts, int part
         if (nlocal[size_t(n)] && owner[size_t(n)] != part) R.node_l2g.push_back(n);
     std::vector<int32_t> g2l(static_cast<size_t>(N), -1);
     for (size_t q = 0; q < R.node_l2g.size(); ++q) g2l[size_t(R.node_l2g[q])] = int32_t(q);
+    // Local element order: interior elements (no ghost node) first, then the
+    // boundary elements, each ascending in global id -- so a step can compute
+    // the interior while the halo is in flight. Each node's CSR row is still
+    // sorted by global element id below: the summation order is unchanged.
+    {
+        std::vector<int64_t> interior, boundary;
+        for (int64_t e : R.elem_l2g) {
+            bool ghost = false;
+            for (int a = 0; a < npe; ++a) ghost |= g2l[size_t(m.conn[size_t(e * npe + a)])] >= R.num_owned;
+            (ghost ? boundary : interior).push_back(e);
+        }
+        R.interior_elements = int64_t(interior.size());
+        R.elem_l2g = std::move(interior);
+        R.elem_l2g.insert(R.elem_l2g.end(), boundary.begin(), boundary.end());
+    }
     // local problem arrays
     Problem<Real>& L = R.local;
     L.mat = P.mat;
@@ -869,6 +885,23 @@ inline PartProblem<Real> build_part(const Problem<Real>& P, int nparts, int part
                   L.consts.begin() + q * P.nconst);
     }
     L.adj = build_adjacency(L.mesh.conn, Nl, npe);
+    // rows in ascending GLOBAL element id (local ids are interior-first)
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t q = 0; q < Nl; ++q) {
+        const int64_t b = L.adj.offsets[size_t(q)], t = L.adj.offsets[size_t(q + 1)];
+        std::vector<std::pair<int64_t, int64_t>> row;
+        row.reserve(size_t(t - b));
+        for (int64_t p = b; p < t; ++p) row.emplace_back(R.elem_l2g[size_t(L.adj.elem[size_t(p)])], p);
+        std::sort(row.begin(), row.end());
+        std::vector<int64_t> el(size_t(t - b));
+        std::vector<int32_t> lo(size_t(t - b));
+        for (int64_t k = 0; k < t - b; ++k) {
+            el[size_t(k)] = L.adj.elem[size_t(row[size_t(k)].second)];
+            lo[size_t(k)] = L.adj.local[size_t(row[size_t(k)].second)];
+        }
+        std::copy(el.begin(), el.end(), L.adj.elem.begin() + b);
+        std::copy(lo.begin(), lo.end(), L.adj.local.begin() + b);
+    }
     // halo: parts referencing each node (as a local node of theirs)
     // recv: my ghosts, from their owners
     std::vector<std::vector<int32_t>> recv(static_cast<size_t>(nparts)), send(static_cast<size_t>(nparts));

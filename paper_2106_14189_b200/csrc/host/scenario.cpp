@@ -300,6 +300,7 @@ int djg_partition_get_info(const djg_partition* p, djg_partition_info* o) {
             o->num_owned = R.num_owned;
             o->num_elements = int64_t(R.elem_l2g.size());
             o->owned_elements = R.owned_elements;
+            o->interior_elements = R.interior_elements;
             o->send_total = int64_t(R.halo.send_nodes.size());
             o->recv_total = int64_t(R.halo.recv_nodes.size());
             o->global_nodes = R.global_nodes;

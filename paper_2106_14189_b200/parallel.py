@@ -117,6 +117,7 @@ class PartEngine(GpuDjEngine):
         self._check(_lib().djg_set_partition(self._h, part.num_owned, A.ptr(part.elem_l2g)))
         self._check(_lib().djg_set_halo(self._h, part.send_nodes.size, A.ptr(part.send_nodes),
                                         part.recv_nodes.size, A.ptr(part.recv_nodes)))
+        self._check(_lib().djg_set_interior(self._h, part.info["interior_elements"]))
 
     def set_global_state(self, u_curr=None, u_prev=None, step: int = 0):
         l2g = self.part.node_l2g
@@ -133,6 +134,12 @@ class PartEngine(GpuDjEngine):
 
     def halo_unpack(self, dev_ptr: int):
         self._check(_lib().djg_halo_unpack(self._h, C.c_void_p(dev_ptr)))
+
+    def step_interior(self):
+        self._check(_lib().djg_step_interior(self._h))
+
+    def step_boundary(self):
+        self._check(_lib().djg_step_boundary(self._h))
 
     def step_status(self, dev_ptr: int):
         self._check(_lib().djg_step_status(self._h, C.c_void_p(dev_ptr)))
@@ -263,35 +270,55 @@ class EmulatedParts:
         for e in self.engs:
             e.sync()
 
-    def step(self, nsteps: int):
+    def _exchange(self):
+        # receiver q's block from p = sender p's block to q (same global order)
+        for q, pq in enumerate(self.parts):
+            for k, p in enumerate(pq.neighbors.tolist()):
+                pp = self.parts[p]
+                j = pp.neighbors.tolist().index(q)
+                r0, r1 = int(pq.recv_off[k]), int(pq.recv_off[k + 1])
+                s0, s1 = int(pp.send_off[j]), int(pp.send_off[j + 1])
+                assert r1 - r0 == s1 - s0
+                if r1 > r0:
+                    self.recv[q][r0:r1].copy_(self.send[p][s0:s1])
+        self.torch.cuda.synchronize()
+
+    def _agree(self):
         torch = self.torch
-        P = len(self.parts)
+        red = torch.stack(self.status).max(dim=0).values
+        torch.cuda.synchronize()  # red is produced on torch's stream, read on the engines'
+        for e in self.engs:
+            e.step_agree(red.data_ptr())
+        self._sync()
+
+    def step(self, nsteps: int, overlap: bool = False):
+        """overlap=False: local step, then halo exchange and agreement.
+        overlap=True: the order of the engine's overlapped NCCL step -- halo
+        pack and interior elements, exchange, unpack, boundary elements and
+        node update, agreement."""
         for _ in range(nsteps):
-            for e in self.engs:
-                e.step_async(1)
-            for p, e in enumerate(self.engs):
-                e.halo_pack(self.send[p].data_ptr())
+            if overlap:
+                for p, e in enumerate(self.engs):
+                    e.halo_pack(self.send[p].data_ptr())
+                    e.step_interior()
+                self._sync()
+                self._exchange()
+                for p, e in enumerate(self.engs):
+                    e.halo_unpack(self.recv[p].data_ptr())
+                    e.step_boundary()
+                    e.step_status(self.status[p].data_ptr())
+            else:
+                for e in self.engs:
+                    e.step_async(1)
+                for p, e in enumerate(self.engs):
+                    e.halo_pack(self.send[p].data_ptr())
+                self._sync()
+                self._exchange()
+                for p, e in enumerate(self.engs):
+                    e.halo_unpack(self.recv[p].data_ptr())
+                    e.step_status(self.status[p].data_ptr())
             self._sync()
-            # receiver q's block from p = sender p's block to q (same global order)
-            for q, pq in enumerate(self.parts):
-                for k, p in enumerate(pq.neighbors.tolist()):
-                    pp = self.parts[p]
-                    j = pp.neighbors.tolist().index(q)
-                    r0, r1 = int(pq.recv_off[k]), int(pq.recv_off[k + 1])
-                    s0, s1 = int(pp.send_off[j]), int(pp.send_off[j + 1])
-                    assert r1 - r0 == s1 - s0
-                    if r1 > r0:
-                        self.recv[q][r0:r1].copy_(self.send[p][s0:s1])
-            torch.cuda.synchronize()
-            for p, e in enumerate(self.engs):
-                e.halo_unpack(self.recv[p].data_ptr())
-                e.step_status(self.status[p].data_ptr())
-            self._sync()
-            red = torch.stack(self.status).max(dim=0).values
-            torch.cuda.synchronize()  # red is produced on torch's stream, read on the engines'
-            for e in self.engs:
-                e.step_agree(red.data_ptr())
-            self._sync()
+            self._agree()
         return [e.sync() for e in self.engs]
 
     def set_global_state(self, u=None, up=None, step=0):

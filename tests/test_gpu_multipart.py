@@ -23,20 +23,24 @@ def single(spec, steps):
     return u, up, rep
 
 
+@pytest.mark.parametrize("overlap", [False, True], ids=["sequential", "overlapped"])
 @pytest.mark.parametrize("nparts", [2, 3, 4, 8])
 @pytest.mark.parametrize("kind,model,prec", [("T4", "NH", 4), ("H8", "TI", 4), ("T4", "MR", 8)])
-def test_parts_bitwise_equal_single_gpu(nparts, kind, model, prec):
+def test_parts_bitwise_equal_single_gpu(nparts, kind, model, prec, overlap):
+    """k parts == 1 GPU bit for bit, with the halo exchanged after the step or
+    (overlapped) at the next step's start, behind the interior elements."""
     spec = box_spec(kind=kind, model=model, divisions=8, precision=prec, ramp_steps=200)
     u1, up1, r1 = single(spec, 200)
     em = EmulatedParts(Scenario(spec), nparts)
-    reps = em.step(200)
+    reps = em.step(200, overlap=overlap)
     u, up, step = em.global_state()
     em.close()
     assert step == 200 == r1.step and all(r.step == 200 and r.status == 0 for r in reps)
     assert np.array_equal(u, u1) and np.array_equal(up, up1)
 
 
-def test_parts_agree_on_inversion():
+@pytest.mark.parametrize("overlap", [False, True], ids=["sequential", "overlapped"])
+def test_parts_agree_on_inversion(overlap):
     """The crushing case of test_solver.cpp:214-241 split in two: every part
     halts at the same state, reporting the same (global) element."""
     sc0 = Scenario(box_spec(kind="T4", divisions=2, extent=(0.1, 0.1, 0.1), precision=8))
@@ -50,7 +54,7 @@ def test_parts_agree_on_inversion():
     ur, upr, rr = oracle.run(spec, 100, "oracle")
     assert r1.status == A.DJG_E_INVERSION and r1.first_inverted == rr["first_inverted"]
     em = EmulatedParts(Scenario(spec), 2)
-    reps = em.step(100)
+    reps = em.step(100, overlap=overlap)
     u, up, step = em.global_state()
     em.close()
     for r in reps:

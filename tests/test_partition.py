@@ -32,9 +32,14 @@ def test_partition_invariants(kind, nparts):
     ep = element_parts(sc, nparts)
     assert np.bincount(ep, minlength=nparts).min() >= sc.num_elements // nparts - 1
     for i, p in enumerate(parts):
-        # local elements: exactly those touching an owned node, ascending global id
+        # local elements: exactly those touching an owned node; interior ones
+        # (no ghost node) first, then boundary ones, each ascending global id
         want = np.flatnonzero((owner[conn] == i).any(axis=1))
-        assert np.array_equal(p.elem_l2g, want)
+        assert np.array_equal(np.sort(p.elem_l2g), want)
+        ni = p.info["interior_elements"]
+        interior = (owner[conn[p.elem_l2g]] == i).all(axis=1)
+        assert interior[:ni].all() and not interior[ni:].any()
+        assert np.all(np.diff(p.elem_l2g[:ni]) > 0) and np.all(np.diff(p.elem_l2g[ni:]) > 0)
         # ghosts: the other nodes of those elements, ascending
         ghosts = np.setdiff1d(np.unique(conn[want]), p.node_l2g[: p.num_owned])
         assert np.array_equal(p.node_l2g[p.num_owned:], ghosts)
@@ -44,6 +49,9 @@ def test_partition_invariants(kind, nparts):
         for n in range(p.num_owned):
             g = p.node_l2g[n]
             assert loff[n + 1] - loff[n] == img["csr_offsets"][g + 1] - img["csr_offsets"][g]
+            # ... in ascending GLOBAL element id (the summation order)
+            row = p.elem_l2g[limg["csr_elem"][loff[n]:loff[n + 1]]]
+            assert np.array_equal(row, img["csr_elem"][img["csr_offsets"][g]:img["csr_offsets"][g + 1]])
     # halo symmetry: what p sends q is what q receives from p, in the same order
     for i, p in enumerate(parts):
         for k, q in enumerate(p.neighbors.tolist()):

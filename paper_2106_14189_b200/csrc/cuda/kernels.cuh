@@ -989,8 +989,12 @@ struct PipeShape {
 #ifndef DJG_PIPE_MINB_OTHER
 #define DJG_PIPE_MINB_OTHER 1
 #endif
+#ifndef DJG_PIPE_MINB_T4C64
+#define DJG_PIPE_MINB_T4C64 4
+#endif
 template <class Real, int KIND, int FORM>
-constexpr int kPipeMinBlocks = (KIND == 0 && FORM == 1 && sizeof(Real) == 4) ? DJG_PIPE_MINB_T4C : DJG_PIPE_MINB_OTHER;
+constexpr int kPipeMinBlocks = (KIND == 0 && FORM == 1) ? (sizeof(Real) == 4 ? DJG_PIPE_MINB_T4C : DJG_PIPE_MINB_T4C64)
+                                                        : DJG_PIPE_MINB_OTHER;
 #ifndef DJG_PIPE_WS
 #define DJG_PIPE_WS 1
 #endif

@@ -323,60 +323,6 @@ struct SmemSrc {
     }
 };
 
-// Gathered inputs of one element, loaded one tile ahead of its computation
-// (k_element_pipe): nodal displacements and slot positions.
-template <class Real, int NPE>
-struct Prefetched {
-    Real ux[NPE], uy[NPE], uz[NPE];
-    int sl[NPE];
-};
-
-template <class Real, int NPE, int RB, int TILE>
-__device__ __forceinline__ void prefetch_element(const ElemArgs<Real>& A, const SmemSrc<Real, TILE>& src,
-                                                 const typename RT<Real>::Node* __restrict__ u,
-                                                 Prefetched<Real, NPE>& p) {
-    int nid[NPE], rk[NPE];
-#pragma unroll
-    for (int q = 0; q < NPE / 4; ++q) {
-        const int4 c = src.conn(q);
-        nid[4 * q + 0] = c.x; nid[4 * q + 1] = c.y; nid[4 * q + 2] = c.z; nid[4 * q + 3] = c.w;
-    }
-    src.template ranks<NPE, RB>(rk);
-#pragma unroll
-    for (int a = 0; a < NPE; ++a) {
-        const typename RT<Real>::Node v = RT<Real>::load_node(u + nid[a]);
-        p.ux[a] = v.x; p.uy[a] = v.y; p.uz[a] = v.z;
-        p.sl[a] = slot_of(A.slice_base, nid[a], rk[a]);
-    }
-}
-
-// Record planes from the shared-memory stage, everything gathered from
-// registers filled by prefetch_element.
-template <class Real, int NPE, int TILE>
-struct PrefetchedSrc {
-    const Prefetched<Real, NPE>& p;
-    const typename RT<Real>::Plane* srec;
-    const Real* stail;
-    int i;
-    __device__ __forceinline__ int4 conn(int) const { return make_int4(0, 0, 0, 0); }
-    __device__ __forceinline__ typename RT<Real>::Plane plane(int q) const { return srec[q * TILE + i]; }
-    template <int N, int RB>
-    __device__ __forceinline__ void ranks(int (&rk)[N]) const {
-#pragma unroll
-        for (int a = 0; a < N; ++a) rk[a] = 0;
-    }
-    __device__ __forceinline__ typename RT<Real>::Node node(int a, const typename RT<Real>::Node*, int) const {
-        typename RT<Real>::Node v;
-        v.x = p.ux[a]; v.y = p.uy[a]; v.z = p.uz[a];
-        return v;
-    }
-    __device__ __forceinline__ int slot(const int*, int a, int, int) const { return p.sl[a]; }
-    __device__ __forceinline__ Real tail(int t) const { return stail[t * TILE + i]; }
-    __device__ __forceinline__ typename RT<Real>::Node coord(const ElemArgs<Real>& a, int n) const {
-        return RT<Real>::load_node(a.X + n);
-    }
-};
-
 // Compact record kept in HBM. T4: nothing -- J0 is rebuilt from the node
 // coordinates (gathered like the displacements, mostly L1/L2 hits) with
 // jacobian0's own sums, det J0 and V0 with det3 / volume0, the invariant
@@ -995,21 +941,14 @@ struct PipeShape {
 template <class Real, int KIND, int FORM>
 constexpr int kPipeMinBlocks = (KIND == 0 && FORM == 1) ? (sizeof(Real) == 4 ? DJG_PIPE_MINB_T4C : DJG_PIPE_MINB_T4C64)
                                                         : DJG_PIPE_MINB_OTHER;
-#ifndef DJG_PIPE_WS
-#define DJG_PIPE_WS 1
-#endif
-constexpr int kPipeWs = DJG_PIPE_WS;  // 1: a fifth warp per block issues the copies
-#ifndef DJG_PIPE_PREF
-#define DJG_PIPE_PREF 0
-#endif
-constexpr bool kPipePrefetch = DJG_PIPE_PREF != 0;
-constexpr int kPipeThreads = kPipeTile + (kPipeWs ? 32 : 0);
+constexpr int kPipeThreads = kPipeTile + 32;  // 4 compute warps + the producer warp
 
 // Persistent blocks; tile `it` of a block (global tile blockIdx + it * grid)
-// lives in stage it % STAGES. The copies of a tile are issued once all four
-// compute warps have released its stage (empty barrier): by a dedicated
-// producer warp running up to STAGES tiles ahead (kPipeWs), or by thread 0,
-// STAGES - 1 tiles ahead.
+// lives in stage it % STAGES. A dedicated producer warp (warp 4) issues the
+// copies of a tile once all four compute warps have released its stage
+// (empty barrier), running up to STAGES tiles ahead. (Issuing from thread 0
+// of a compute warp instead, or also prefetching the next tile's gathers,
+// measured slower.)
 template <class Real, int KIND, int MODEL, int RB, int FORM, int STAGES>
 __global__ void __launch_bounds__(kPipeThreads, (kPipeMinBlocks<Real, KIND, FORM>)) k_element_pipe(const ElemArgs<Real> A, long long e0,
                                                                               long long e1) {
@@ -1059,62 +998,17 @@ __global__ void __launch_bounds__(kPipeThreads, (kPipeMinBlocks<Real, KIND, FORM
         bulk_load(st + PS::kRankOff, static_cast<const unsigned char*>(A.rank) + eb * PS::kRankBytes, rbytes, full + s,
                   pol);
     };
-    if constexpr (kPipeWs) {
-        if (tid >= kPipeTile) {
-            if (tid == kPipeTile) {
-                pol = l2_evict_first_policy();
-                for (long long it = 0; it < nmine; ++it) issue(it);
-            }
-            return;
+    if (tid >= kPipeTile) {  // producer warp
+        if (tid == kPipeTile) {
+            pol = l2_evict_first_policy();
+            for (long long it = 0; it < nmine; ++it) issue(it);
         }
-    } else if (tid == 0) {
-        pol = l2_evict_first_policy();
-        for (long long it = 0; it < STAGES - 1 && it < nmine; ++it) issue(it);
+        return;
     }
 
     const int phase = int(__ldcg(&A.ctrl->step) % 3);
     const Node* u = A.u_override ? A.u_override : pick3(phase, A.u[0], A.u[1], A.u[2]);
-    auto stage_src = [&](long long it) {
-        const unsigned char* st = smem + int(it % STAGES) * PS::kStageBytes;
-        return SmemSrc<Real, kPipeTile>{reinterpret_cast<const int4*>(st + PS::kConnOff),
-                                        reinterpret_cast<const Plane*>(st + PS::kRecOff), st + PS::kRankOff,
-                                        reinterpret_cast<const Real*>(st + PS::kTailOff), tid};
-    };
-    auto elem_of = [&](long long it) { return e0 + (blockIdx.x + it * G) * kPipeTile + tid; };
-    if constexpr (kPipePrefetch) {
-        // The gather of tile it + 1 (displacements, slot positions) is in
-        // flight while tile it is computed.
-        constexpr int NPE = PS::NPE;
-        Prefetched<Real, NPE> cur, nxt;
-        if (nmine > 0) {
-            mbar_wait(full, 0u);
-            if (elem_of(0) < e1) prefetch_element<Real, NPE, RB, kPipeTile>(A, stage_src(0), u, cur);
-        }
-        for (long long it = 0; it < nmine; ++it) {
-            if constexpr (!kPipeWs) {
-                if (tid == 0 && it + STAGES - 1 < nmine) issue(it + STAGES - 1);
-            }
-            if (it + 1 < nmine) {
-                mbar_wait(full + int((it + 1) % STAGES), unsigned(((it + 1) / STAGES) & 1));
-                if (elem_of(it + 1) < e1) prefetch_element<Real, NPE, RB, kPipeTile>(A, stage_src(it + 1), u, nxt);
-            }
-            const long long e = elem_of(it);
-            if (e < e1) {
-                const auto ss = stage_src(it);
-                const PrefetchedSrc<Real, NPE, kPipeTile> src{cur, ss.srec, ss.stail, tid};
-                if constexpr (FORM == 2) element_body_tled<Real, KIND, MODEL, RB>(A, e, u, src);
-                else element_body<Real, KIND, MODEL, RB, FORM == 1>(A, e, u, src);
-            }
-            __syncwarp();
-            if ((tid & 31) == 0) mbar_arrive(empty + int(it % STAGES));
-            cur = nxt;
-        }
-        return;
-    }
     for (long long it = 0; it < nmine; ++it) {
-        if constexpr (!kPipeWs) {
-            if (tid == 0 && it + STAGES - 1 < nmine) issue(it + STAGES - 1);
-        }
         const int s = int(it % STAGES);
         mbar_wait(full + s, unsigned((it / STAGES) & 1));
         const long long e = e0 + (blockIdx.x + it * G) * kPipeTile + tid;

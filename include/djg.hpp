@@ -232,6 +232,20 @@ private:
     int policy_ = DJG_ABORT;
 };
 
+// TledEngine(mesh, material, c_hg, build_threads) (solver.hpp:287-300): the
+// conventional total Lagrangian element forces (tled_force.hpp) on the device,
+// with the same slots, gather, update and run loop; its record (B0, V0, and
+// for H8 the hourglass data) is built on the GPU.
+template <class Real>
+class GpuTledEngine : public GpuDjEngine<Real> {
+public:
+    template <class MeshT, class MaterialT>
+    GpuTledEngine(const MeshT& mesh, const MaterialT& material, Real c_hg = Real(0.1), int build_threads = 0,
+                  int device = 0, uint32_t flags = 0)
+        : GpuDjEngine<Real>(mesh, material, c_hg, build_threads, device, flags | DJG_FLAG_TLED) {}
+    static constexpr const char* name() { return "tled-b200"; }
+};
+
 // SimState / RunResult (solver.hpp:41-57, 193-200).
 template <class Real>
 struct SimState {

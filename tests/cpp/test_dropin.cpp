@@ -117,6 +117,40 @@ void inversion_semantics() {
     EXPECT(inv_steps > 0, "no inverted steps reported");
 }
 
+// djg::GpuTledEngine in place of djtled::TledEngine, both
+// loops, bit-identical.
+template <class Real>
+void tled_dropin(ElementKind kind, MaterialModel model, int div, long steps) {
+    const auto mesh = generate_box<Real>({1, 1, 1}, {div, div, div}, kind);
+    const auto mat = bench_material<Real>(model);
+    DjEngine<Real> dj(mesh, mat);
+    TledEngine<Real> cpu(mesh, mat);
+    djg::GpuTledEngine<Real> gpu(mesh, mat);
+    const auto mass = lump_mass(mesh, mat.rho, dj.model().elems);
+    BoundaryConditions<Real> bcs;
+    for (int n : select_plane_nodes(mesh, Plane::ZMin))
+        for (int a = 0; a < 3; ++a) bcs.fixed.emplace_back(n, a);
+    RunParams<Real> p;
+    p.dt = Real(0.5) * critical_dt(mesh, dj.model().elems, dilatational_wave_speed(mat));
+    p.t_end = p.dt * Real(steps);
+    p.alpha = relaxation_alpha(mat, mesh);
+    PrescribedRamp<Real> ramp;
+    ramp.nodes = select_plane_nodes(mesh, Plane::ZMax);
+    ramp.axis = 2;
+    ramp.target = Real(-0.2);
+    ramp.t_total = p.t_end;
+    bcs.prescribed.push_back(ramp);
+    const auto bc = DofConstraints<Real>::build(bcs, mesh.num_nodes());
+    const auto r_cpu = djtled::run_simulation(cpu, mass, bc, p);
+    const auto r_seam = djtled::run_simulation(gpu, mass, bc, p);
+    const auto r_gpu = djg::run_simulation(gpu, mass, bc, p);
+    const double e_seam = rel_err(r_seam.state.u_curr, r_cpu.state.u_curr);
+    const double e_gpu = rel_err(r_gpu.state.u_curr, r_cpu.state.u_curr);
+    std::printf("TLED %s-%s f%zu steps=%ld: seam %.3e  device %.3e\n", to_string(kind), to_string(model),
+                8 * sizeof(Real), r_cpu.steps, e_seam, e_gpu);
+    EXPECT(e_seam == 0.0 && e_gpu == 0.0, "TLED drop-in differs: %.3e %.3e", e_seam, e_gpu);
+}
+
 // the precompute on the device (records, adjacency, slot
 // ranks, lump_mass, characteristic lengths) == the reference's host functions.
 template <class Real>
@@ -164,6 +198,8 @@ int main() {
     compare_runs<float>(ElementKind::T4, MaterialModel::Orthotropic, 5, 200, 0.0);
     inversion_semantics<double>();
     inversion_semantics<float>();
+    tled_dropin<float>(ElementKind::T4, MaterialModel::NeoHookean, 5, 200);
+    tled_dropin<double>(ElementKind::H8, MaterialModel::TransverseIsotropic, 4, 150);
     device_precompute<float>(ElementKind::T4, MaterialModel::NeoHookean, 5, 200);
     device_precompute<double>(ElementKind::T4, MaterialModel::TransverseIsotropic, 4, 150);
     device_precompute<float>(ElementKind::H8, MaterialModel::Orthotropic, 4, 150);

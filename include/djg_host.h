@@ -74,7 +74,13 @@ typedef struct djg_partition_info {
     int64_t interior_elements;  /* local elements [0, interior) reference no ghost node */
 } djg_partition_info;
 
+/* Partition methods: recursive coordinate bisection of element centroids
+ * (default; fast, reproducible), or METIS k-way on the element dual graph
+ * (faces shared; METIS_PartMeshDual, fixed seed: reproducible). */
+enum djg_partition_method { DJG_PART_RCB = 0, DJG_PART_METIS = 1 };
 int djg_partition_build(const djg_scenario* sc, int32_t nparts, int32_t part, djg_partition** out);
+int djg_partition_build_method(const djg_scenario* sc, int32_t nparts, int32_t part, int32_t method,
+                               djg_partition** out);
 void djg_partition_free(djg_partition* p);
 int djg_partition_get_info(const djg_partition* p, djg_partition_info* out);
 /* Local problem arrays (same layout as djg_scenario_image, local ids). */
@@ -90,6 +96,7 @@ int djg_partition_halo(const djg_partition* p, int32_t* neighbors, int64_t* send
 int djg_partition_maps(const djg_partition* p, int64_t* node_l2g, int64_t* elem_l2g);
 /* Element -> part assignment of the whole scenario (E entries). */
 int djg_element_parts(const djg_scenario* sc, int32_t nparts, int32_t* part);
+int djg_element_parts_method(const djg_scenario* sc, int32_t nparts, int32_t method, int32_t* part);
 
 #ifdef __cplusplus
 }

@@ -29,6 +29,8 @@ DJG_FLAG_DEVICE_PRECOMPUTE = 16
 DJG_FLAG_FULL_RECORD = 32
 DJG_FLAG_TLED = 64
 DJG_FLAG_NO_PIPE = 128
+DJG_PART_RCB, DJG_PART_METIS = 0, 1
+PART_METHODS = {"rcb": DJG_PART_RCB, "metis": DJG_PART_METIS}
 
 KIND_NAMES = {"T4": DJG_T4, "H8": DJG_H8}
 MODEL_NAMES = {"NH": DJG_NH, "TI": DJG_TI, "OT": DJG_OT, "MR": DJG_MR}
@@ -210,6 +212,7 @@ EXPORTS = [
     ("djg_step_status", C.c_int, [C.c_void_p, C.c_void_p]),
     ("djg_step_agree", C.c_int, [C.c_void_p, C.c_void_p]),
     ("djg_partition_build", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, _P(C.c_void_p)]),
+    ("djg_partition_build_method", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, _P(C.c_void_p)]),
     ("djg_partition_free", None, [C.c_void_p]),
     ("djg_partition_get_info", C.c_int, [C.c_void_p, _P(djg_partition_info)]),
     ("djg_partition_desc", C.c_int, [C.c_void_p, C.c_int32, _P(djg_desc)]),
@@ -217,6 +220,7 @@ EXPORTS = [
     ("djg_partition_halo", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("djg_partition_maps", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     ("djg_element_parts", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
+    ("djg_element_parts_method", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     ("djg_last_error", C.c_char_p, [C.c_void_p]),
     ("djg_status_string", C.c_char_p, [C.c_int32]),
     ("djg_create_error", C.c_char_p, []),

@@ -785,13 +785,54 @@ struct PartProblem {
     Halo halo;
 };
 
+// Graph partitioning of the element dual graph (elements adjacent when they
+// share a face: 3 nodes for T4, 4 for H8) with METIS k-way
+// (METIS_PartMeshDual from the CUDA toolkit's libmetis_static.a, idx_t =
+// int64). Fixed options and seed: the same mesh gives the same partition on
+// every rank and every run.
+extern "C" {
+int METIS_SetDefaultOptions(int64_t* options);
+int METIS_PartMeshDual(int64_t* ne, int64_t* nn, int64_t* eptr, int64_t* eind, int64_t* vwgt, int64_t* vsize,
+                       int64_t* ncommon, int64_t* nparts, void* tpwgts, int64_t* options, int64_t* objval,
+                       int64_t* epart, int64_t* npart);
+}
+
+enum PartMethod { kPartRcb = 0, kPartMetis = 1 };
+
 template <class Real>
-inline PartProblem<Real> build_part(const Problem<Real>& P, int nparts, int part) {
+inline std::vector<int32_t> metis_parts(const Mesh<Real>& m, int nparts) {
+    const int64_t E = m.num_elements(), N = m.num_nodes();
+    const int npe = m.npe();
+    std::vector<int32_t> part(static_cast<size_t>(E), 0);
+    if (nparts <= 1 || E <= 1) return part;
+    std::vector<int64_t> eptr(static_cast<size_t>(E + 1)), eind(m.conn.begin(), m.conn.end());
+    for (int64_t e = 0; e <= E; ++e) eptr[size_t(e)] = e * npe;
+    int64_t options[40];
+    METIS_SetDefaultOptions(options);
+    options[8] = 1;  // METIS_OPTION_SEED
+    int64_t ne = E, nn = N, ncommon = m.kind == DJG_T4 ? 3 : 4, np = nparts, objval = 0;
+    std::vector<int64_t> epart(static_cast<size_t>(E)), npart(static_cast<size_t>(N));
+    const int rc = METIS_PartMeshDual(&ne, &nn, eptr.data(), eind.data(), nullptr, nullptr, &ncommon, &np, nullptr,
+                                      options, &objval, epart.data(), npart.data());
+    if (rc != 1) throw ConfigError("METIS_PartMeshDual failed (" + std::to_string(rc) + ")");
+    for (int64_t e = 0; e < E; ++e) part[size_t(e)] = int32_t(epart[size_t(e)]);
+    return part;
+}
+
+template <class Real>
+inline std::vector<int32_t> element_parts(const Mesh<Real>& m, int nparts, int method) {
+    if (method == kPartRcb) return rcb_parts(m, nparts);
+    if (method == kPartMetis) return metis_parts(m, nparts);
+    throw ConfigError("unknown partition method");
+}
+
+template <class Real>
+inline PartProblem<Real> build_part(const Problem<Real>& P, int nparts, int part, int method = kPartRcb) {
     if (nparts < 1 || part < 0 || part >= nparts) throw ConfigError("invalid part index");
     const Mesh<Real>& m = P.mesh;
     const int npe = m.npe();
     const int64_t N = m.num_nodes(), E = m.num_elements();
-    const std::vector<int32_t> epart = rcb_parts(m, nparts);
+    const std::vector<int32_t> epart = element_parts(m, nparts, method);
     // owner of a node: part of its lowest-id element (first in its CSR row)
     std::vector<int32_t> owner(static_cast<size_t>(N), 0);  // isolated nodes: part 0
 #pragma omp parallel for schedule(static)

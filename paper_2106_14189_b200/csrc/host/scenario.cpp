@@ -268,6 +268,11 @@ int djg_scenario_desc(const djg_scenario* sc, int32_t device, djg_desc* out) {
 }
 
 int djg_partition_build(const djg_scenario* sc, int32_t nparts, int32_t part, djg_partition** out) {
+    return djg_partition_build_method(sc, nparts, part, DJG_PART_RCB, out);
+}
+
+int djg_partition_build_method(const djg_scenario* sc, int32_t nparts, int32_t part, int32_t method,
+                               djg_partition** out) {
     if (!sc || !out) return DJG_E_CONFIG;
     *out = nullptr;
     try {
@@ -275,7 +280,7 @@ int djg_partition_build(const djg_scenario* sc, int32_t nparts, int32_t part, dj
         std::visit(
             [&](const auto& P) {
                 using R = typename std::decay_t<decltype(P.consts)>::value_type;
-                pp->p = djg::build_part<R>(P, nparts, part);
+                pp->p = djg::build_part<R>(P, nparts, part, method);
             },
             sc->p);
         *out = pp.release();
@@ -351,13 +356,22 @@ int djg_partition_maps(const djg_partition* p, int64_t* node_l2g, int64_t* elem_
 }
 
 int djg_element_parts(const djg_scenario* sc, int32_t nparts, int32_t* part) {
+    return djg_element_parts_method(sc, nparts, DJG_PART_RCB, part);
+}
+
+int djg_element_parts_method(const djg_scenario* sc, int32_t nparts, int32_t method, int32_t* part) {
     if (!sc || !part || nparts < 1) return DJG_E_CONFIG;
-    std::visit(
-        [&](const auto& P) {
-            const auto v = djg::rcb_parts(P.mesh, nparts);
-            std::memcpy(part, v.data(), v.size() * sizeof(int32_t));
-        },
-        sc->p);
+    try {
+        std::visit(
+            [&](const auto& P) {
+                const auto v = djg::element_parts(P.mesh, nparts, method);
+                std::memcpy(part, v.data(), v.size() * sizeof(int32_t));
+            },
+            sc->p);
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return DJG_E_CONFIG;
+    }
     return DJG_OK;
 }
 

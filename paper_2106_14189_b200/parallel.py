@@ -32,10 +32,10 @@ def _lib():
 class Partition:
     """Host-side local problem of part `part` of `nparts`."""
 
-    def __init__(self, scenario: Scenario, nparts: int, part: int):
+    def __init__(self, scenario: Scenario, nparts: int, part: int, method: str = "rcb"):
         self.scenario = scenario
         h = C.c_void_p()
-        if _lib().djg_partition_build(scenario._h, nparts, part, C.byref(h)) != A.DJG_OK:
+        if _lib().djg_partition_build_method(scenario._h, nparts, part, A.PART_METHODS[method], C.byref(h)) != A.DJG_OK:
             raise ConfigError(_lib().djg_scenario_error().decode())
         self._h = h
         i = A.djg_partition_info()
@@ -94,9 +94,10 @@ class Partition:
             pass
 
 
-def element_parts(scenario: Scenario, nparts: int) -> np.ndarray:
+def element_parts(scenario: Scenario, nparts: int, method: str = "rcb") -> np.ndarray:
     out = np.zeros(scenario.num_elements, np.int32)
-    _lib().djg_element_parts(scenario._h, nparts, A.ptr(out))
+    if _lib().djg_element_parts_method(scenario._h, nparts, A.PART_METHODS[method], A.ptr(out)) != A.DJG_OK:
+        raise ConfigError(_lib().djg_scenario_error().decode())
     return out
 
 
@@ -162,7 +163,8 @@ class DistributedEngine:
     engine_comm=False: the same sequence driven from Python per step with
     torch.distributed P2P / allreduce (reference driver for tests)."""
 
-    def __init__(self, scenario: Scenario, device: int, group=None, flags: int = 0, engine_comm: bool = True):
+    def __init__(self, scenario: Scenario, device: int, group=None, flags: int = 0, engine_comm: bool = True,
+                 method: str = "rcb"):
         import torch
         import torch.distributed as dist
         self.dist = dist
@@ -171,7 +173,7 @@ class DistributedEngine:
         self.world = dist.get_world_size(group)
         self.device = device
         self.engine_comm = engine_comm
-        self.part = Partition(scenario, self.world, self.rank)
+        self.part = Partition(scenario, self.world, self.rank, method)
         self.eng = PartEngine(self.part, device, flags)
         tdt = _torch_dtype(self.part.dtype)
         dev = torch.device("cuda", device)
@@ -254,10 +256,10 @@ class EmulatedParts:
     engines and kernels as DistributedEngine, the halo moved with device
     copies and the failure agreement reduced on the device. For tests."""
 
-    def __init__(self, scenario: Scenario, nparts: int, device: int = 0, flags: int = 0):
+    def __init__(self, scenario: Scenario, nparts: int, device: int = 0, flags: int = 0, method: str = "rcb"):
         import torch
         self.torch = torch
-        self.parts = [Partition(scenario, nparts, p) for p in range(nparts)]
+        self.parts = [Partition(scenario, nparts, p, method) for p in range(nparts)]
         self.engs = [PartEngine(p, device, flags) for p in self.parts]
         tdt = _torch_dtype(scenario.dtype)
         dev = torch.device("cuda", device)

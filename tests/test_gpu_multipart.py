@@ -39,6 +39,20 @@ def test_parts_bitwise_equal_single_gpu(nparts, kind, model, prec, overlap):
     assert np.array_equal(u, u1) and np.array_equal(up, up1)
 
 
+def test_parts_metis_partition_bitwise():
+    """Graph (METIS k-way) partitions: same bits as one GPU, overlapped step."""
+    for kind, model in (("T4", "NH"), ("H8", "OT")):
+        spec = box_spec(kind=kind, model=model, divisions=7, precision=4, ramp_steps=150)
+        u1, up1, r1 = single(spec, 150)
+        for nparts in (3, 8):
+            em = EmulatedParts(Scenario(spec), nparts, method="metis")
+            reps = em.step(150, overlap=True)
+            u, up, step = em.global_state()
+            em.close()
+            assert all(r.status == 0 for r in reps) and step == 150
+            assert np.array_equal(u, u1) and np.array_equal(up, up1)
+
+
 @pytest.mark.parametrize("overlap", [False, True], ids=["sequential", "overlapped"])
 def test_parts_agree_on_inversion(overlap):
     """The crushing case of test_solver.cpp:214-241 split in two: every part

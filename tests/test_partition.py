@@ -15,22 +15,27 @@ from paper_2106_14189_b200 import _abi as A
 from paper_2106_14189_b200.parallel import Partition, element_parts
 
 
+@pytest.mark.parametrize("method", ["rcb", "metis"])
 @pytest.mark.parametrize("kind", ["T4", "H8"])
 @pytest.mark.parametrize("nparts", [1, 2, 3, 4, 8])
-def test_partition_invariants(kind, nparts):
+def test_partition_invariants(kind, nparts, method):
     sc = Scenario(box_spec(kind=kind, divisions=(6, 5, 7), precision=4))
     img = sc.image()
     npe = sc.npe
     conn = img["conn"].reshape(-1, npe)
-    parts = [Partition(sc, nparts, p) for p in range(nparts)]
+    parts = [Partition(sc, nparts, p, method) for p in range(nparts)]
     # owned nodes: an exact cover of the mesh
     owned = np.concatenate([p.node_l2g[: p.num_owned] for p in parts])
     assert np.array_equal(np.sort(owned), np.arange(sc.num_nodes))
     owner = np.empty(sc.num_nodes, np.int64)
     for i, p in enumerate(parts):
         owner[p.node_l2g[: p.num_owned]] = i
-    ep = element_parts(sc, nparts)
-    assert np.bincount(ep, minlength=nparts).min() >= sc.num_elements // nparts - 1
+    ep = element_parts(sc, nparts, method)
+    counts = np.bincount(ep, minlength=nparts)
+    if method == "rcb":
+        assert counts.min() >= sc.num_elements // nparts - 1
+    else:  # METIS k-way: within its default 3 % imbalance, every part non-empty
+        assert counts.min() > 0 and counts.max() <= 1.031 * sc.num_elements / nparts + 1
     for i, p in enumerate(parts):
         # local elements: exactly those touching an owned node; interior ones
         # (no ghost node) first, then boundary ones, each ascending global id
@@ -68,6 +73,9 @@ def test_partition_is_deterministic():
     a = element_parts(sc, 8)
     b = element_parts(Scenario(box_spec(kind="T4", divisions=7, precision=8)), 8)
     assert np.array_equal(a, b)
+    m1 = element_parts(sc, 8, "metis")
+    m2 = element_parts(Scenario(box_spec(kind="T4", divisions=7, precision=8)), 8, "metis")
+    assert np.array_equal(m1, m2)
     p1, p2 = Partition(sc, 8, 5), Partition(sc, 8, 5)
     assert np.array_equal(p1.node_l2g, p2.node_l2g) and np.array_equal(p1.send_nodes, p2.send_nodes)
 
@@ -117,13 +125,13 @@ def _cpu_part_steps(part: Partition, spec, steps, exchange):
     return u[: part.num_owned], up[: part.num_owned]
 
 
-def _gloo_worker(rank, world, port, q):
+def _gloo_worker(rank, world, port, q, method="rcb"):
     import torch
     import torch.distributed as dist
     dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
     spec = box_spec(kind="T4", model="TI", divisions=3, precision=4, ramp_steps=40)
     sc = Scenario(spec)
-    part = Partition(sc, world, rank)
+    part = Partition(sc, world, rank, method)
 
     def exchange(un):
         reqs, bufs = [], []
@@ -150,12 +158,13 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_gloo_two_ranks_bitwise_equal_single_process():
+@pytest.mark.parametrize("method", ["rcb", "metis"])
+def test_gloo_two_ranks_bitwise_equal_single_process(method):
     world = 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_gloo_worker, args=(r, world, port, q, method)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=300) for _ in range(world)]

@@ -402,3 +402,52 @@ def test_device_layout_rejects_bad_connectivity():
     h = C.c_void_p()
     rc = A.load_library().djg_create(C.byref(d), C.byref(h))
     assert rc == A.DJG_E_CONFIG and b"out of range" in A.load_library().djg_create_error()
+
+
+@pytest.mark.parametrize("kind", ["T4", "H8"])
+def test_unstructured_numbering_and_isolated_node(kind):
+    """A box with randomly permuted node ids and element order, jittered
+    coordinates and one isolated (massless, element-less) node: irregular
+    CSR rows and slices, bit-identical to the oracle."""
+    rng = np.random.default_rng(7)
+    sc = Scenario(box_spec(kind=kind, divisions=(5, 4, 6), precision=8))
+    img = sc.image()
+    npe = 4 if kind == "T4" else 8
+    x = img["nodes"].reshape(-1, 3)
+    conn = img["conn"].reshape(-1, npe)
+    h = 1.0 / 6
+    x = x + rng.uniform(-0.08 * h, 0.08 * h, x.shape)
+    perm = rng.permutation(len(x))          # new id of old node i = inv[i]
+    inv = np.empty_like(perm)
+    inv[perm] = np.arange(len(x))
+    xn = np.vstack([x[perm], [[2.0, 2.0, 2.0]]])  # + isolated node
+    cn = inv[conn][rng.permutation(len(conn))]
+    z = xn[:-1, 2]
+    bottom = np.flatnonzero(np.abs(z - z.min()) < 1e-12)
+    top = np.flatnonzero(np.abs(z - z.max()) < 1e-12)
+    for prec in (8, 4):
+        spec = mesh_spec(xn, cn, kind=kind, precision=prec, fixed=[(int(n), a) for n in bottom for a in range(3)],
+                         prescribed=[(int(n), 2, -0.03, 1e-3) for n in top])
+        check_run(spec, 200)
+
+
+def test_high_valence_node_uses_two_byte_ranks():
+    """A fan of 300 tets around one axis: its two hub nodes have 300 incident
+    elements (> 256: 16-bit slot ranks), bit-identical to the oracle."""
+    M = 300
+    ang = 2 * np.pi * np.arange(M) / M
+    ring = np.c_[np.cos(ang), np.sin(ang), np.zeros(M)]
+    x = np.vstack([[0.0, 0.0, 0.0], [0.0, 0.0, 1.0], ring])
+    conn = []
+    for i in range(M):
+        t = [0, 2 + i, 2 + (i + 1) % M, 1]
+        a, b, c, d = x[t]
+        if np.linalg.det(np.c_[b - a, c - a, d - a]) < 0:
+            t[1], t[2] = t[2], t[1]
+        conn.append(t)
+    conn = np.array(conn, np.int32)
+    for prec in (4, 8):
+        spec = mesh_spec(x, conn, kind="T4", precision=prec,
+                         fixed=[(n, a) for n in range(2, 2 + M) for a in range(3)] + [(0, a) for a in range(3)],
+                         prescribed=[(1, 2, -0.05, 2e-3), (1, 0, 0.02, 2e-3)])
+        check_run(spec, 300)

@@ -149,7 +149,7 @@ class GpuDjEngine:
         if rc in (A.DJG_OK, A.DJG_E_INVERSION, A.DJG_E_DIVERGENCE):
             return rc
         msg = _lib().djg_last_error(self._h).decode()
-        raise (CudaError if rc == A.DJG_E_CUDA else ConfigError)(f"{A.DJG_OK and ''}{msg}")
+        raise (CudaError if rc == A.DJG_E_CUDA else ConfigError)(msg)
 
     def _vec(self, a):
         if a is None:

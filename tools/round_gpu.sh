@@ -1,6 +1,5 @@
-# One GPU call: tests, bench, launch lists, one full capture of the element kernel.
+# One GPU call: tests, smoke, bench, launch lists.
 timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; tail -3 gpurun_out/pytest_gpu.log
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; cat gpurun_out/bench.json
 python tools/prof_step.py cfg5 6 && ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv python tools/prof_step.py cfg5 6 > gpurun_out/launches_cfg5.csv 2>&1
-python tools/prof_step.py cfg4 6 && ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv python tools/prof_step.py cfg4 6 > gpurun_out/launches_cfg4.csv 2>&1
-python tools/prof_step.py cfg3 6 && ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv python tools/prof_step.py cfg3 6 > gpurun_out/launches_cfg3.csv 2>&1

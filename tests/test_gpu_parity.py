@@ -451,3 +451,66 @@ def test_high_valence_node_uses_two_byte_ranks():
                          fixed=[(n, a) for n in range(2, 2 + M) for a in range(3)] + [(0, a) for a in range(3)],
                          prescribed=[(1, 2, -0.05, 2e-3), (1, 0, 0.02, 2e-3)])
         check_run(spec, 300)
+
+
+def _nh_ref():
+    return material("NH", mu=6567.0, kappa=326210.0, rho=1060.0)
+
+
+def test_small_strain_extension_matches_linear_modulus():
+    """test_solver.cpp:265-284: 1 % uniaxial extension of a 0.1 m cube (roller
+    at zmin), relaxed to steady state on the GPU; the zmax face reaction from
+    the GPU assemble (reaction_force, solver.hpp:312-325) is within 5 % of
+    E * strain * area, E = 9 kappa mu / (3 kappa + mu); the field is
+    bit-identical to the oracle."""
+    from paper_2106_14189_b200 import run_simulation
+    spec = box_spec(kind="T4", divisions=3, extent=(0.1,) * 3, precision=8, mat=_nh_ref(), target=0.001,
+                    fix_all_axes=False, safety=0.5)
+    sc = Scenario(spec)
+    t_total = 0.1
+    steps_ramp = int(round(t_total / sc.dt))
+    spec = box_spec(kind="T4", divisions=3, extent=(0.1,) * 3, precision=8, mat=_nh_ref(), target=0.001,
+                    fix_all_axes=False, safety=0.5, ramp_steps=steps_ramp)
+    sc = Scenario(spec)
+    with GpuDjEngine(sc) as eng:
+        res = run_simulation(eng, t_end=1.5)
+        f, st = eng.assemble(res.u_curr)
+    assert st["first_inverted"] == -1 and f is not None
+    x = sc.image()["nodes"].reshape(-1, 3)
+    top = np.flatnonzero(np.abs(x[:, 2] - 0.1) < 1e-12)
+    reaction = f.reshape(-1, 3)[top, 2].sum()
+    e_mod = 9.0 * 326210.0 * 6567.0 / (3.0 * 326210.0 + 6567.0)
+    assert reaction == pytest.approx(e_mod * 0.01 * 0.1 * 0.1, rel=0.05)
+    ur, _, rr = oracle.run(spec, res.steps, "oracle")
+    assert np.array_equal(res.u_curr, ur)
+
+
+def test_heavy_damping_decays_to_steady_state():
+    """test_solver.cpp:168-190: with the relaxation damping the kinetic-energy
+    proxy sum m |u - u_prev|^2 / dt^2 / 2 peaks and decays below 1e-12 of
+    its peak after 1.2 s of a 20 % extension (all-axes fixed base)."""
+    spec = box_spec(kind="T4", divisions=2, extent=(0.1,) * 3, precision=8, mat=_nh_ref(), target=0.02, safety=0.5)
+    sc0 = Scenario(spec)
+    spec = box_spec(kind="T4", divisions=2, extent=(0.1,) * 3, precision=8, mat=_nh_ref(), target=0.02, safety=0.5,
+                    ramp_steps=int(round(0.1 / sc0.dt)))
+    sc = Scenario(spec)
+    mass = sc.image()["mass"]
+    steps = int(np.ceil(1.2 / sc.dt))
+    ke = []
+    with GpuDjEngine(sc) as eng:
+        for s in range(0, steps, 25):
+            eng.step(min(25, steps - s))
+            u, up, _ = eng.get_state()
+            v = (u - up).reshape(-1, 3) / sc.dt
+            ke.append(0.5 * float(np.sum(mass[:, None] * v * v)))
+    assert max(ke) > 0 and ke[-1] < 1e-12 * max(ke)
+
+
+def test_t_end_zero_returns_initial_field():
+    """test_solver.cpp:107-119."""
+    from paper_2106_14189_b200 import run_simulation
+    spec = box_spec(kind="T4", divisions=1, extent=(0.1,) * 3, precision=8, mat=_nh_ref(), dt=1e-4)
+    spec.c.bc_mode = 0
+    with GpuDjEngine(Scenario(spec)) as eng:
+        r = run_simulation(eng, t_end=0.0)
+    assert r.steps == 0 and not np.any(r.u_curr)

@@ -216,7 +216,7 @@ def _line(args, world, K, W, E, ms_step, value, extra):
         "data": "synthetic (generate_box unit cube, bench_material, +1% z-extension ramp)",
         "config": {"workload": f"cfg5: {args.kind}-{args.model} unit cube d={args.divisions}",
                    "kind": args.kind, "material": args.model, "divisions": args.divisions,
-                   "num_elements": E, "parallelism": f"{world} GPU" + (f" ({args.partition.upper()} partition + overlapped halo)" if world > 1 else "")},
+                   "num_elements": E, "parallelism": f"{world} GPU" + (f" ({args.partition.upper()} partition, {args.transport} halo)" if world > 1 else "")},
         "time_per_step_us": ms_step * 1e3,
     }
     line.update(extra)
@@ -376,7 +376,7 @@ def multi_arm(args, rank, world, device):
                     target=0.01, ramp_steps=total)
     t0 = time.perf_counter()
     sc = Scenario(spec)
-    de = DistributedEngine(sc, device=device, method=args.partition)
+    de = DistributedEngine(sc, device=device, method=args.partition, transport=args.transport)
     t1 = time.perf_counter()
     E = sc.num_elements
     pi = de.part.info
@@ -479,6 +479,8 @@ def main():
     ap.add_argument("--tled-steps", type=int, default=100)
     ap.add_argument("--cpu-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
+                    help="multi-GPU halo / agreement: peer-memory stores from the node kernel (default) or NCCL")
     ap.add_argument("--partition", default="rcb", choices=["rcb", "metis"],
                     help="multi-GPU partition: coordinate bisection (default) or METIS k-way on the dual graph")
     args = ap.parse_args()

@@ -229,6 +229,29 @@ int djg_comm_unique_id(void* id128);
  * order itself: djg_halo_pack, djg_step_interior, <exchange>,
  * djg_halo_unpack, djg_step_boundary, djg_step_status, <allreduce>,
  * djg_step_agree. */
+/* Peer-memory multi-GPU step (no NCCL on the step path): every part's node
+ * kernel stores the new displacement of the owned nodes other parts reference
+ * straight into their buffers over NVLink, and posts its step status into
+ * every part's mailbox; a one-warp kernel waits for all parts and agrees.
+ *   djg_peer_export      this engine's 4 device pointers (3 displacement
+ *                        buffers, mailbox) -- single-process use
+ *   djg_peer_ipc_export  their CUDA IPC handles (4 x 64 bytes), for other ranks
+ *   djg_peer_ipc_open    map another rank's 4 handles -> 4 device pointers
+ *   djg_peer_setup       every part's pointers (peer_u: 3 per part, peer_mail:
+ *                        1 per part, own included) and this part's halo
+ *                        destinations: owned node dest_node[i] -> part
+ *                        dest_part[i], local node dest_index[i]
+ * Then djg_step runs element kernel -> node kernel with peer stores ->
+ * wait/agree per step, graph-captured. djg_step_peer_local /
+ * djg_step_peer_agree split one step for single-device emulation. */
+int djg_peer_export(djg_engine* eng, void** ptrs4);
+int djg_peer_ipc_export(djg_engine* eng, void* handles);
+int djg_peer_ipc_open(djg_engine* eng, const void* handles, void** ptrs4);
+int djg_peer_setup(djg_engine* eng, int32_t nparts, int32_t part, const void* const* peer_u,
+                   const void* const* peer_mail, int64_t ndest, const int32_t* dest_node, const int32_t* dest_part,
+                   const int32_t* dest_index);
+int djg_step_peer_local(djg_engine* eng);
+int djg_step_peer_agree(djg_engine* eng);
 int djg_set_interior(djg_engine* eng, int64_t num_interior);
 int djg_step_interior(djg_engine* eng);
 int djg_step_boundary(djg_engine* eng);

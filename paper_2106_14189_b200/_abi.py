@@ -198,6 +198,13 @@ EXPORTS = [
     ("djg_lump_mass", C.c_int, [C.c_void_p, C.c_void_p]),
     ("djg_comm_unique_id", C.c_int, [C.c_void_p]),
     ("djg_set_interior", C.c_int, [C.c_void_p, C.c_int64]),
+    ("djg_peer_export", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("djg_peer_ipc_export", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("djg_peer_ipc_open", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("djg_peer_setup", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
+                                 C.c_void_p, C.c_void_p]),
+    ("djg_step_peer_local", C.c_int, [C.c_void_p]),
+    ("djg_step_peer_agree", C.c_int, [C.c_void_p]),
     ("djg_step_interior", C.c_int, [C.c_void_p]),
     ("djg_step_boundary", C.c_int, [C.c_void_p]),
     ("djg_comm_init", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,

@@ -168,6 +168,13 @@ public:
     virtual void comm_init(const void* id, int nranks, int rank, int nnb, const int32_t* nb, const int64_t* send_off,
                            const int64_t* recv_off) = 0;
     virtual void set_interior(int64_t n) = 0;
+    virtual void peer_export(void** ptrs) = 0;
+    virtual void peer_ipc_export(void* handles) = 0;
+    virtual void peer_ipc_open(const void* handles, void** ptrs) = 0;
+    virtual void peer_setup(int nparts, int part, const void* const* peer_u, const void* const* peer_mail, int64_t ndest,
+                            const int32_t* dest_node, const int32_t* dest_part, const int32_t* dest_index) = 0;
+    virtual void step_peer_local() = 0;
+    virtual void step_peer_agree() = 0;
     virtual void step_interior() = 0;
     virtual void step_boundary() = 0;
 };
@@ -534,6 +541,10 @@ public:
     void set_partition(int64_t num_owned, const int64_t* elem_l2g) override {
         if (num_owned < 0 || num_owned > N_) throw DescError("num_owned out of range");
         na_.N = num_owned;
+        if (!mailbox_.p) {
+            mailbox_.alloc(sizeof(Mailbox));
+            CK(cudaMemset(mailbox_.p, 0, mailbox_.bytes));
+        }
         if (elem_l2g) {
             elemL2g_.alloc(size_t(E_) * sizeof(int64_t));
             CK(cudaMemcpy(elemL2g_.p, elem_l2g, elemL2g_.bytes, cudaMemcpyHostToDevice));
@@ -721,6 +732,86 @@ public:
         CK(cudaGetLastError());
     }
 
+    // ---- peer-memory multi-GPU step (kernels.cuh: k_node_peer, k_wait_agree)
+    void peer_export(void** ptrs) override {
+        if (!mailbox_.p) throw DescError("djg_set_partition first");
+        for (int i = 0; i < 3; ++i) ptrs[i] = u_[i].p;
+        ptrs[3] = mailbox_.p;
+    }
+
+    void peer_ipc_export(void* handles) override {
+        if (!mailbox_.p) throw DescError("djg_set_partition first");
+        auto* h = static_cast<cudaIpcMemHandle_t*>(handles);
+        for (int i = 0; i < 3; ++i) CK(cudaIpcGetMemHandle(h + i, u_[i].p));
+        CK(cudaIpcGetMemHandle(h + 3, mailbox_.p));
+    }
+
+    void peer_ipc_open(const void* handles, void** ptrs) override {
+        const auto* h = static_cast<const cudaIpcMemHandle_t*>(handles);
+        CK(cudaSetDevice(device_));
+        for (int i = 0; i < 4; ++i) {
+            CK(cudaIpcOpenMemHandle(&ptrs[i], h[i], cudaIpcMemLazyEnablePeerAccess));
+            ipc_open_.push_back(ptrs[i]);
+        }
+    }
+
+    void peer_setup(int nparts, int part, const void* const* peer_u, const void* const* peer_mail, int64_t ndest,
+                    const int32_t* dest_node, const int32_t* dest_part, const int32_t* dest_index) override {
+        if (!elemL2g_.p || !mailbox_.p) throw DescError("djg_peer_setup needs djg_set_partition with elem_l2g first");
+        if (nparts < 1 || nparts > kMaxParts || part < 0 || part >= nparts) throw DescError("invalid part count / index");
+        const int64_t no = na_.N;
+        std::vector<int32_t> off(size_t(no) + 1, 0);
+        for (int64_t i = 0; i < ndest; ++i) {
+            if (dest_node[i] < 0 || dest_node[i] >= no) throw DescError("halo destination of a non-owned node");
+            if (dest_part[i] < 0 || dest_part[i] >= nparts || dest_part[i] == part) throw DescError("invalid peer part");
+            off[size_t(dest_node[i]) + 1]++;
+        }
+        for (int64_t n = 0; n < no; ++n) off[size_t(n) + 1] += off[size_t(n)];
+        std::vector<int2> dst(static_cast<size_t>(std::max<int64_t>(ndest, 1)));
+        std::vector<int32_t> cur(off.begin(), off.end() - 1);
+        for (int64_t i = 0; i < ndest; ++i) dst[size_t(cur[size_t(dest_node[i])]++)] = make_int2(dest_part[i], dest_index[i]);
+        destOff_.alloc(off.size() * sizeof(int32_t));
+        CK(cudaMemcpy(destOff_.p, off.data(), destOff_.bytes, cudaMemcpyHostToDevice));
+        dest_.alloc(dst.size() * sizeof(int2));
+        CK(cudaMemcpy(dest_.p, dst.data(), dest_.bytes, cudaMemcpyHostToDevice));
+        peerU_.alloc(size_t(3 * nparts) * sizeof(void*));
+        CK(cudaMemcpy(peerU_.p, peer_u, peerU_.bytes, cudaMemcpyHostToDevice));
+        peerMail_.alloc(size_t(nparts) * sizeof(void*));
+        CK(cudaMemcpy(peerMail_.p, peer_mail, peerMail_.bytes, cudaMemcpyHostToDevice));
+        pa_.dest_off = destOff_.as<int>();
+        pa_.dest = dest_.as<int2>();
+        pa_.peer_u = peerU_.as<Node*>();
+        pa_.peer_mail = peerMail_.as<Mailbox*>();
+        pa_.nparts = nparts;
+        pa_.part = part;
+        peer_ = true;
+        drop_graphs();
+    }
+
+    void launch_peer_local(cudaStream_t s) {
+        launch_element(s, 0, E_);
+        const int64_t blocks = std::max<int64_t>(1, (na_.N + 255) / 256);
+        const unsigned g = unsigned(node_grid_ > 0 ? std::min<int64_t>(blocks, node_grid_) : blocks);
+        k_node_peer<Real><<<g, 256, 0, s>>>(na_, pa_);
+        CK(cudaGetLastError());
+    }
+
+    void launch_peer_agree(cudaStream_t s) {
+        k_wait_agree<<<1, 32, 0, s>>>(ctrl_.as<Ctrl>(), mailbox_.as<Mailbox>(), pa_.nparts);
+        CK(cudaGetLastError());
+    }
+
+    void step_peer_local() override {
+        if (!peer_) throw DescError("djg_peer_setup first");
+        if (!configured_) throw DescError("step data not configured (djg_configure_step)");
+        launch_peer_local(stream_);
+    }
+
+    void step_peer_agree() override {
+        if (!peer_) throw DescError("djg_peer_setup first");
+        launch_peer_agree(stream_);
+    }
+
     void set_policy(int policy) override {
         if (policy != DJG_ABORT && policy != DJG_SKIP_AND_REPORT) throw DescError("unknown inversion policy");
         policy_ = policy;
@@ -898,6 +989,7 @@ public:
 
     ~Engine() override {
         if (comm_) Nccl::get().comm_destroy(static_cast<ncclComm_t>(comm_));
+        for (void* p : ipc_open_) cudaIpcCloseMemHandle(p);
         if (evFork_) cudaEventDestroy(evFork_);
         if (evJoin_) cudaEventDestroy(evJoin_);
         if (side_) cudaStreamDestroy(side_);
@@ -1095,7 +1187,10 @@ public:
     }
 
     void one_step(cudaStream_t s) {
-        if (comm_ && interior_ >= 0) {
+        if (peer_) {
+            launch_peer_local(s);
+            launch_peer_agree(s);
+        } else if (comm_ && interior_ >= 0) {
             launch_overlapped_step(s);
         } else {
             launch_step(s);
@@ -1300,6 +1395,10 @@ private:
     static constexpr int kSpareSms = 4;
     cudaStream_t side_ = nullptr;      // interior elements of the overlapped step
     cudaEvent_t evFork_ = nullptr, evJoin_ = nullptr;
+    bool peer_ = false;                // peer-memory multi-GPU step
+    PeerArgs<Real> pa_{};
+    DevBuf mailbox_, destOff_, dest_, peerU_, peerMail_;
+    std::vector<void*> ipc_open_;
     DevBuf pairs_, rowoff_, mass_;  // device layout: sorted CSR pairs (until masses are built), lump_mass
     Real lmin_ = 0;
     bool compact_ = false, tled_ = false, pipe_ = false;
@@ -1580,6 +1679,50 @@ int djg_step_interior(djg_engine* eng) {
 int djg_step_boundary(djg_engine* eng) {
     return guarded(eng, [&](djg::EngineBase& e) {
         e.step_boundary();
+        return DJG_OK;
+    });
+}
+
+int djg_peer_export(djg_engine* eng, void** ptrs4) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.peer_export(ptrs4);
+        return DJG_OK;
+    });
+}
+
+int djg_peer_ipc_export(djg_engine* eng, void* handles) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.peer_ipc_export(handles);
+        return DJG_OK;
+    });
+}
+
+int djg_peer_ipc_open(djg_engine* eng, const void* handles, void** ptrs4) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.peer_ipc_open(handles, ptrs4);
+        return DJG_OK;
+    });
+}
+
+int djg_peer_setup(djg_engine* eng, int32_t nparts, int32_t part, const void* const* peer_u,
+                   const void* const* peer_mail, int64_t ndest, const int32_t* dest_node, const int32_t* dest_part,
+                   const int32_t* dest_index) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.peer_setup(nparts, part, peer_u, peer_mail, ndest, dest_node, dest_part, dest_index);
+        return DJG_OK;
+    });
+}
+
+int djg_step_peer_local(djg_engine* eng) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.step_peer_local();
+        return DJG_OK;
+    });
+}
+
+int djg_step_peer_agree(djg_engine* eng) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.step_peer_agree();
         return DJG_OK;
     });
 }

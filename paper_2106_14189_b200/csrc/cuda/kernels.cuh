@@ -1368,6 +1368,110 @@ __global__ void k_agree(Ctrl* ctrl, const long long* __restrict__ reduced) {
     ctrl->agreed = 1;  // later status/agree rounds (halted engine) are no-ops
 }
 
+// ------------------------------------------------------------------ peer-memory multi-GPU step
+//
+// The halo exchange and the failure agreement without NCCL: the node kernel
+// of each part stores the new displacement of every owned node another part
+// references straight into that part's displacement buffer (NVLink peer
+// memory, mapped with CUDA IPC), and its last block posts the step's status
+// and epoch into every part's mailbox (system-scope release). A one-warp
+// kernel then waits for all parts' epoch (acquire) and applies the same
+// agreement as k_agree. No staging buffers, no pack / unpack, no collective
+// launches: compute and transfer are one kernel.
+constexpr int kMaxParts = 64;
+
+struct Mailbox {
+    unsigned long long flag[kMaxParts];  // last epoch each part closed
+    long long status[2][kMaxParts][2];   // by epoch parity: {code, -global first inverted}
+};
+
+template <class Real>
+struct PeerArgs {
+    const int* dest_off;                      // [num_owned + 1] halo destinations per owned node
+    const int2* dest;                         // (peer part, peer-local node)
+    typename RT<Real>::Node* const* peer_u;   // [nparts * 3] every part's displacement buffers
+    Mailbox* const* peer_mail;                // [nparts] every part's mailbox (own included)
+    int nparts, part;
+};
+
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+template <class Real>
+__global__ void __launch_bounds__(256) k_node_peer(const NodeArgs<Real> A, const PeerArgs<Real> P) {
+    using T = RT<Real>;
+    Ctrl* ctrl = A.ctrl;
+    if (*(volatile const int*)&ctrl->halted) return;
+    __shared__ int s_nonfinite;
+    if (threadIdx.x == 0) s_nonfinite = 0;
+    __syncthreads();
+    const long long step = ctrl->step;
+    const int phn = int((step + 1) % 3);
+    typename T::Node* unxt = pick3(phn, A.u[0], A.u[1], A.u[2]);
+    for (long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x; n < A.N;
+         n += (long long)gridDim.x * blockDim.x) {
+        if (node_body<Real, false>(A, n, (long long)A.slice_base[n >> 5] + (n & 31), A.row_len[n], step))
+            s_nonfinite = 1;
+        const int d0 = P.dest_off[n], d1 = P.dest_off[n + 1];
+        if (d0 < d1) {
+            const typename T::Node v = unxt[n];  // written just above by this thread
+            for (int d = d0; d < d1; ++d) {
+                const int2 q = P.dest[d];
+                T::store_node(P.peer_u[3 * q.x + phn] + q.y, v.x, v.y, v.z);
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    if (s_nonfinite) atomicOr(&ctrl->diverged, 1);
+    __threadfence_system();  // this block's peer stores, visible to the peers before the epoch
+    const unsigned int done = atomicAdd(&ctrl->blocks_done, 1u);
+    if (done != gridDim.x - 1) return;
+    __threadfence_system();
+    close_step<false>(ctrl, step, A.policy);
+    const unsigned long long epoch = ++ctrl->epoch;
+    const long long code = ctrl->halted == 4 ? 2 : (ctrl->halted == 5 ? 1 : 0);
+    const long long first = code == 2 ? -ctrl->halt_first_inv : (-0x7fffffffffffffffll - 1);
+    for (int q = 0; q < P.nparts; ++q) {
+        Mailbox* m = P.peer_mail[q];
+        m->status[epoch & 1][P.part][0] = code;
+        m->status[epoch & 1][P.part][1] = first;
+    }
+    __threadfence_system();
+    for (int q = 0; q < P.nparts; ++q) st_release_sys(&P.peer_mail[q]->flag[P.part], epoch);
+    ctrl->blocks_done = 0;
+}
+
+// Waits until every part closed this part's last epoch, then agrees on the
+// outcome exactly like k_agree (all parts halt at the same state).
+__global__ void k_wait_agree(Ctrl* ctrl, const Mailbox* __restrict__ own, int nparts) {
+    if (threadIdx.x != 0) return;
+    if (ctrl->agreed) return;  // halted and agreed in an earlier step: nothing ran since
+    const unsigned long long epoch = ctrl->epoch;
+    if (epoch == 0) return;
+    for (int q = 0; q < nparts; ++q)
+        while (ld_acquire_sys(&own->flag[q]) < epoch) __nanosleep(64);
+    long long code = 0, first = -0x7fffffffffffffffll - 1;
+    for (int q = 0; q < nparts; ++q) {
+        code = max(code, own->status[epoch & 1][q][0]);
+        first = max(first, own->status[epoch & 1][q][1]);
+    }
+    if (code == 0) return;
+    if (ctrl->halted == 0) {
+        ctrl->step -= 1;  // this part advanced; another one failed the same step
+        ctrl->fail_step = ctrl->step + 1;
+    }
+    ctrl->halted = code == 2 ? 4 : 5;
+    ctrl->halt_first_inv = code == 2 ? -first : -1;
+    ctrl->agreed = 1;
+}
+
 // ------------------------------------------------------------------ precompute
 
 // build_element_constants on the device: the record of every

@@ -136,6 +136,35 @@ class PartEngine(GpuDjEngine):
     def halo_unpack(self, dev_ptr: int):
         self._check(_lib().djg_halo_unpack(self._h, C.c_void_p(dev_ptr)))
 
+    # -- peer-memory transport (djg_peer_*)
+    def peer_export(self) -> list[int]:
+        out = (C.c_void_p * 4)()
+        self._check(_lib().djg_peer_export(self._h, out))
+        return [int(v or 0) for v in out]
+
+    def peer_ipc_export(self) -> bytes:
+        buf = C.create_string_buffer(4 * 64)
+        self._check(_lib().djg_peer_ipc_export(self._h, buf))
+        return buf.raw
+
+    def peer_ipc_open(self, handles: bytes) -> list[int]:
+        out = (C.c_void_p * 4)()
+        self._check(_lib().djg_peer_ipc_open(self._h, C.create_string_buffer(handles, 4 * 64), out))
+        return [int(v or 0) for v in out]
+
+    def peer_setup(self, nparts: int, part: int, ptrs: list[list[int]], dests):
+        peer_u = (C.c_void_p * (3 * nparts))(*[p[i] for p in ptrs for i in range(3)])
+        peer_mail = (C.c_void_p * nparts)(*[p[3] for p in ptrs])
+        node, dpart, index = (np.ascontiguousarray(a, np.int32) for a in dests)
+        self._check(_lib().djg_peer_setup(self._h, nparts, part, peer_u, peer_mail, int(node.size), A.ptr(node),
+                                          A.ptr(dpart), A.ptr(index)))
+
+    def step_peer_local(self):
+        self._check(_lib().djg_step_peer_local(self._h))
+
+    def step_peer_agree(self):
+        self._check(_lib().djg_step_peer_agree(self._h))
+
     def step_interior(self):
         self._check(_lib().djg_step_interior(self._h))
 
@@ -147,6 +176,30 @@ class PartEngine(GpuDjEngine):
 
     def step_agree(self, dev_ptr: int):
         self._check(_lib().djg_step_agree(self._h, C.c_void_p(dev_ptr)))
+
+
+def peer_destinations(halos: list, me: int):
+    """Halo destinations of part `me` for the peer-memory transport: owned
+    node i of my send block to part q lands on q's ghost node at the same
+    position of q's receive block from me (the blocks list the same global
+    nodes in the same order). halos[q] = (neighbors, send_off, recv_off,
+    send_nodes, recv_nodes) of part q."""
+    nb, s_off, _, s_nodes, _ = halos[me]
+    node, part, index = [], [], []
+    for k, q in enumerate(list(nb)):
+        qnb, _, q_roff, _, q_rnodes = halos[q]
+        j = list(qnb).index(me)
+        send = s_nodes[s_off[k]:s_off[k + 1]]
+        recv = q_rnodes[q_roff[j]:q_roff[j + 1]]
+        assert len(send) == len(recv)
+        node.extend(send.tolist())
+        part.extend([q] * len(send))
+        index.extend(recv.tolist())
+    return node, part, index
+
+
+def _halo(p: "Partition"):
+    return (p.neighbors.copy(), p.send_off.copy(), p.recv_off.copy(), p.send_nodes.copy(), p.recv_nodes.copy())
 
 
 def _torch_dtype(dtype):
@@ -164,7 +217,7 @@ class DistributedEngine:
     torch.distributed P2P / allreduce (reference driver for tests)."""
 
     def __init__(self, scenario: Scenario, device: int, group=None, flags: int = 0, engine_comm: bool = True,
-                 method: str = "rcb"):
+                 method: str = "rcb", transport: str = "nccl"):
         import torch
         import torch.distributed as dist
         self.dist = dist
@@ -181,7 +234,20 @@ class DistributedEngine:
         self.recv = torch.zeros((max(self.part.recv_nodes.size, 1), 4), dtype=tdt, device=dev)
         self.status = torch.zeros(2, dtype=torch.int64, device=dev)
         self.stream = torch.cuda.ExternalStream(self.eng.stream, device=dev)
-        if engine_comm:
+        self.transport = transport
+        if transport == "p2p":
+            # peer-memory step: map every other rank's buffers (CUDA IPC) and
+            # let the engine store the halo into them from its node kernel
+            handles = [None] * self.world
+            dist.all_gather_object(handles, self.eng.peer_ipc_export(), group=group)
+            halos = [None] * self.world
+            dist.all_gather_object(halos, _halo(self.part), group=group)
+            ptrs = [self.eng.peer_export() if q == self.rank else self.eng.peer_ipc_open(handles[q])
+                    for q in range(self.world)]
+            self.eng.peer_setup(self.world, self.rank, ptrs, peer_destinations(halos, self.rank))
+            dist.barrier(group=group)
+            self.engine_comm = True  # the engine drives every step
+        elif engine_comm:
             uid = C.create_string_buffer(128)
             if self.rank == 0 and _lib().djg_comm_unique_id(uid) != A.DJG_OK:
                 raise RuntimeError(_lib().djg_create_error().decode())
@@ -256,11 +322,18 @@ class EmulatedParts:
     engines and kernels as DistributedEngine, the halo moved with device
     copies and the failure agreement reduced on the device. For tests."""
 
-    def __init__(self, scenario: Scenario, nparts: int, device: int = 0, flags: int = 0, method: str = "rcb"):
+    def __init__(self, scenario: Scenario, nparts: int, device: int = 0, flags: int = 0, method: str = "rcb",
+                 transport: str = "copy"):
         import torch
         self.torch = torch
         self.parts = [Partition(scenario, nparts, p, method) for p in range(nparts)]
         self.engs = [PartEngine(p, device, flags) for p in self.parts]
+        self.transport = transport
+        if transport == "p2p":
+            ptrs = [e.peer_export() for e in self.engs]
+            halos = [_halo(p) for p in self.parts]
+            for i, e in enumerate(self.engs):
+                e.peer_setup(nparts, i, ptrs, peer_destinations(halos, i))
         tdt = _torch_dtype(scenario.dtype)
         dev = torch.device("cuda", device)
         self.send = [torch.zeros((max(p.send_nodes.size, 1), 4), dtype=tdt, device=dev) for p in self.parts]
@@ -299,6 +372,17 @@ class EmulatedParts:
         pack and interior elements, exchange, unpack, boundary elements and
         node update, agreement."""
         for _ in range(nsteps):
+            if self.transport == "p2p":
+                # every part's step (its node kernel stores the halo into the
+                # other parts' buffers and posts its status) before any part
+                # waits: no kernel ever waits for another one here
+                for e in self.engs:
+                    e.step_peer_local()
+                self._sync()
+                for e in self.engs:
+                    e.step_peer_agree()
+                self._sync()
+                continue
             if overlap:
                 for p, e in enumerate(self.engs):
                     e.halo_pack(self.send[p].data_ptr())

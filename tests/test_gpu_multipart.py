@@ -39,6 +39,21 @@ def test_parts_bitwise_equal_single_gpu(nparts, kind, model, prec, overlap):
     assert np.array_equal(u, u1) and np.array_equal(up, up1)
 
 
+@pytest.mark.parametrize("nparts", [2, 3, 8])
+@pytest.mark.parametrize("kind,model,prec", [("T4", "NH", 4), ("H8", "TI", 8)])
+def test_parts_peer_memory_transport_bitwise(nparts, kind, model, prec):
+    """The peer-memory step (node kernel stores the halo into the other parts'
+    buffers, mailbox agreement): k parts == 1 GPU bit for bit."""
+    spec = box_spec(kind=kind, model=model, divisions=7, precision=prec, ramp_steps=150)
+    u1, up1, r1 = single(spec, 150)
+    em = EmulatedParts(Scenario(spec), nparts, transport="p2p")
+    reps = em.step(150)
+    u, up, step = em.global_state()
+    em.close()
+    assert all(r.status == 0 for r in reps) and step == 150
+    assert np.array_equal(u, u1) and np.array_equal(up, up1)
+
+
 def test_parts_metis_partition_bitwise():
     """Graph (METIS k-way) partitions: same bits as one GPU, overlapped step."""
     for kind, model in (("T4", "NH"), ("H8", "OT")):
@@ -53,7 +68,7 @@ def test_parts_metis_partition_bitwise():
             assert np.array_equal(u, u1) and np.array_equal(up, up1)
 
 
-@pytest.mark.parametrize("overlap", [False, True], ids=["sequential", "overlapped"])
+@pytest.mark.parametrize("overlap", [False, True, "p2p"], ids=["sequential", "overlapped", "peer-memory"])
 def test_parts_agree_on_inversion(overlap):
     """The crushing case of test_solver.cpp:214-241 split in two: every part
     halts at the same state, reporting the same (global) element."""
@@ -67,8 +82,12 @@ def test_parts_agree_on_inversion(overlap):
     u1, up1, r1 = single(spec, 100)
     ur, upr, rr = oracle.run(spec, 100, "oracle")
     assert r1.status == A.DJG_E_INVERSION and r1.first_inverted == rr["first_inverted"]
-    em = EmulatedParts(Scenario(spec), 2)
-    reps = em.step(100, overlap=overlap)
+    if overlap == "p2p":
+        em = EmulatedParts(Scenario(spec), 2, transport="p2p")
+        reps = em.step(100)
+    else:
+        em = EmulatedParts(Scenario(spec), 2)
+        reps = em.step(100, overlap=overlap)
     u, up, step = em.global_state()
     em.close()
     for r in reps:
@@ -83,7 +102,7 @@ def _port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("engine_comm", [True, False], ids=["engine-nccl", "python-driver"])
+@pytest.mark.parametrize("engine_comm", [True, False, "p2p"], ids=["engine-nccl", "python-driver", "peer-memory"])
 def test_distributed_engine_single_rank_nccl(engine_comm):
     """The torch.distributed (NCCL) driver on one rank: same bits as the
     plain engine (the halo is empty, the status allreduce is real). With
@@ -97,7 +116,8 @@ def test_distributed_engine_single_rank_nccl(engine_comm):
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_port()}", rank=0, world_size=1,
                             device_id=torch.device("cuda", 0))
     try:
-        de = DistributedEngine(Scenario(spec), device=0, engine_comm=engine_comm)
+        kw = dict(transport="p2p") if engine_comm == "p2p" else dict(engine_comm=engine_comm)
+        de = DistributedEngine(Scenario(spec), device=0, **kw)
         r = de.step(100)
         U, UP, step = de.gather_global()
         assert r.status == 0 and step == 100
@@ -108,7 +128,7 @@ def test_distributed_engine_single_rank_nccl(engine_comm):
                        fix_all_axes=True)
         with GpuDjEngine(Scenario(inv)) as e1:
             r1 = e1.step(50, raise_on_failure=False)
-        de2 = DistributedEngine(Scenario(inv), device=0, engine_comm=engine_comm)
+        de2 = DistributedEngine(Scenario(inv), device=0, **kw)
         r2 = de2.step(50, raise_on_failure=False)
         assert r1.status in (A.DJG_E_INVERSION, A.DJG_E_DIVERGENCE)
         assert r1.status == r2.status and r1.fail_step == r2.fail_step and r1.first_inverted == r2.first_inverted

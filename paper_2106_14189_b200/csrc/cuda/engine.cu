@@ -1042,7 +1042,10 @@ public:
         const int ph = int(step % 3);
         upload_nodes(u, u_[ph].as<Node>());
         upload_nodes(up, u_[(ph + 2) % 3].as<Node>());
-        upload_nodes(nullptr, u_[(ph + 1) % 3].as<Node>());
+        // (the next buffer is rewritten by the step before it is read; with the
+        // peer-memory transport another rank may already be storing this
+        // part's ghosts into it, so it is left alone)
+        if (!peer_) upload_nodes(nullptr, u_[(ph + 1) % 3].as<Node>());
         CK(cudaStreamSynchronize(stream_));
         reset_ctrl(step);
     }

@@ -196,6 +196,7 @@ EXPORTS = [
     ("djg_get_info", C.c_int, [C.c_void_p, _P(djg_engine_info)]),
     ("djg_get_slot_map", C.c_int, [C.c_void_p, C.c_void_p]),
     ("djg_lump_mass", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("djg_advance_host", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, _P(djg_report)]),
     ("djg_comm_unique_id", C.c_int, [C.c_void_p]),
     ("djg_set_interior", C.c_int, [C.c_void_p, C.c_int64]),
     ("djg_peer_export", C.c_int, [C.c_void_p, C.c_void_p]),

@@ -174,6 +174,7 @@ public:
     virtual void peer_setup(int nparts, int part, const void* const* peer_u, const void* const* peer_mail, int64_t ndest,
                             const int32_t* dest_node, const int32_t* dest_part, const int32_t* dest_index) = 0;
     virtual void step_peer_local() = 0;
+    virtual int advance_host(const void* u, const void* up, int64_t step, void* u_next, djg_report* rep) = 0;
     virtual void step_peer_agree() = 0;
     virtual void step_interior() = 0;
     virtual void step_boundary() = 0;
@@ -991,6 +992,7 @@ public:
         if (comm_) Nccl::get().comm_destroy(static_cast<ncclComm_t>(comm_));
         for (void* p : ipc_open_) cudaIpcCloseMemHandle(p);
         if (evFork_) cudaEventDestroy(evFork_);
+        if (evPrev_) cudaEventDestroy(evPrev_);
         if (evJoin_) cudaEventDestroy(evJoin_);
         if (side_) cudaStreamDestroy(side_);
         if (graph_big_) cudaGraphExecDestroy(graph_big_);
@@ -1048,6 +1050,46 @@ public:
         if (!peer_) upload_nodes(nullptr, u_[(ph + 1) % 3].as<Node>());
         CK(cudaStreamSynchronize(stream_));
         reset_ctrl(step);
+    }
+
+    // advance_step with a host SimState in one call: u_curr goes up on the
+    // engine stream, u_prev on a second stream while the element kernel runs
+    // (it reads only u_curr), then the node update and the new u_curr back.
+    int advance_host(const void* u, const void* up, int64_t step, void* u_next, djg_report* rep) override {
+        if (!configured_) throw DescError("step data not configured (djg_configure_step)");
+        if (!u || !up || !u_next) throw DescError("djg_advance_host needs u_curr, u_prev and u_next");
+        if (step < 0) throw DescError("step must be >= 0");
+        if (n_slabs_ != 1 || comm_ || peer_) throw DescError("djg_advance_host: single-part, one-slab engines");
+        if (!side_) CK(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+        if (!evPrev_) CK(cudaEventCreateWithFlags(&evPrev_, cudaEventDisableTiming));
+        if (!flat2_.p) flat2_.alloc(flat_.bytes);
+        reset_ctrl(step);
+        CK(cudaMemcpyAsync(hstart_, ctrl_.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream_));
+        const int ph = int(step % 3);
+        const size_t bytes = size_t(3 * N_) * sizeof(Real);
+        const unsigned gn = unsigned((N_ + 255) / 256);
+        // u_curr first: the copy engine serves the copies in issue order, and
+        // the element kernel can start as soon as u_curr has landed
+        CK(cudaMemcpyAsync(flat_.p, u, bytes, cudaMemcpyHostToDevice, stream_));
+        k_pack_nodes<Real><<<gn, 256, 0, stream_>>>(flat_.as<Real>(), N_, u_[ph].as<Node>());
+        CK(cudaEventRecord(evPrev_, stream_));  // (orders the side stream after reset_ctrl's work)
+        CK(cudaStreamWaitEvent(side_, evPrev_, 0));
+        CK(cudaMemcpyAsync(flat2_.p, up, bytes, cudaMemcpyHostToDevice, side_));
+        k_pack_nodes<Real><<<gn, 256, 0, side_>>>(flat2_.as<Real>(), N_, u_[(ph + 2) % 3].as<Node>());
+        CK(cudaEventRecord(evPrev_, side_));
+        CK(cudaGetLastError());
+        launch_element(stream_, 0, E_);
+        CK(cudaStreamWaitEvent(stream_, evPrev_, 0));
+        launch_node(stream_, 0, false);
+        k_unpack_nodes<Real><<<gn, 256, 0, stream_>>>(u_[(ph + 1) % 3].as<Node>(), N_, flat_.as<Real>());
+        CK(cudaMemcpyAsync(u_next, flat_.p, bytes, cudaMemcpyDeviceToHost, stream_));
+        CK(cudaGetLastError());
+        const int status = sync(rep);
+        if (status != DJG_OK) {  // the state did not advance: hand back u_curr
+            download_nodes(u_[ph].as<Node>(), u_next);
+            CK(cudaStreamSynchronize(stream_));
+        }
+        return status;
     }
 
     void set_external(const void* r) override {
@@ -1399,6 +1441,8 @@ private:
     cudaStream_t side_ = nullptr;      // interior elements of the overlapped step
     cudaEvent_t evFork_ = nullptr, evJoin_ = nullptr;
     bool peer_ = false;                // peer-memory multi-GPU step
+    cudaEvent_t evPrev_ = nullptr;     // djg_advance_host: u_prev uploaded
+    DevBuf flat2_;
     PeerArgs<Real> pa_{};
     DevBuf mailbox_, destOff_, dest_, peerU_, peerMail_;
     std::vector<void*> ipc_open_;
@@ -1728,6 +1772,11 @@ int djg_step_peer_agree(djg_engine* eng) {
         e.step_peer_agree();
         return DJG_OK;
     });
+}
+
+int djg_advance_host(djg_engine* eng, const void* u_curr, const void* u_prev, int64_t step, void* u_next,
+                     djg_report* report) {
+    return guarded(eng, [&](djg::EngineBase& e) { return e.advance_host(u_curr, u_prev, step, u_next, report); });
 }
 
 int djg_lump_mass(djg_engine* eng, void* mass) {

@@ -217,6 +217,15 @@ class GpuDjEngine:
             raise_for(r)
         return r
 
+    def advance_host(self, u_curr, u_prev, step: int, out=None):
+        """advance_step with a host SimState (djg_advance_host): one step from
+        (u_curr, u_prev, step); returns (new u_curr, StepReport)."""
+        u, up = self._vec(u_curr), self._vec(u_prev)
+        out = np.empty(3 * self.num_nodes, self.dtype) if out is None else out
+        rep = A.djg_report()
+        self._check(_lib().djg_advance_host(self._h, A.ptr(u), A.ptr(up), step, A.ptr(out), C.byref(rep)))
+        return out, StepReport.from_c(rep)
+
     def step_async(self, nsteps: int):
         self._check(_lib().djg_step_async(self._h, nsteps))
 

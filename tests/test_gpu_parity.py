@@ -514,3 +514,36 @@ def test_t_end_zero_returns_initial_field():
     with GpuDjEngine(Scenario(spec)) as eng:
         r = run_simulation(eng, t_end=0.0)
     assert r.steps == 0 and not np.any(r.u_curr)
+
+
+@pytest.mark.parametrize("precision", [4, 8])
+def test_advance_host_matches_device_loop(precision):
+    """djg_advance_host (one step from a host SimState, u_prev upload
+    overlapped with the element kernel) == the device-resident loop, bit for
+    bit, step by step; a failing step hands back the unchanged state."""
+    spec = box_spec(kind="T4", model="TI", divisions=5, precision=precision, ramp_steps=120)
+    sc = Scenario(spec)
+    with GpuDjEngine(sc) as ref:
+        ref.step(120)
+        u_ref, up_ref, _ = ref.get_state()
+    with GpuDjEngine(sc) as eng:
+        n3 = 3 * sc.num_nodes
+        u, up = np.zeros(n3, spec.dtype), np.zeros(n3, spec.dtype)
+        for s in range(120):
+            un, rep = eng.advance_host(u, up, s)
+            assert rep.status == 0 and rep.step == s + 1 and rep.steps_done == 1
+            u, up = un, u
+    assert np.array_equal(u, u_ref) and np.array_equal(up, up_ref)
+    # inversion: status 4, state handed back unchanged
+    inv = box_spec(kind="T4", divisions=2, extent=(0.1,) * 3, precision=8, target=-0.09, ramp_steps=2)
+    with GpuDjEngine(Scenario(inv)) as e2:
+        n3 = 3 * e2.num_nodes
+        u, up = np.zeros(n3), np.zeros(n3)
+        for s in range(40):
+            un, rep = e2.advance_host(u, up, s)
+            if rep.status:
+                assert rep.status in (A.DJG_E_INVERSION, A.DJG_E_DIVERGENCE) and np.array_equal(un, u)
+                break
+            u, up = un, u
+        else:
+            pytest.fail("the crushing ramp never failed")

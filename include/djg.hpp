@@ -263,6 +263,27 @@ struct RunResult {
     long inverted_steps = 0;
 };
 
+// advance_step (solver.hpp:98-153) on a host SimState through the GPU engine
+// (djg_advance_host): one step with the engine's configured coefficients,
+// constraints and dt. On success the state rotates (u_prev <- u_curr <- new,
+// step + 1, t = dt * step); on failure it is unchanged and the report says why.
+template <class Real>
+djg_report advance_step(GpuDjEngine<Real>& engine, SimState<Real>& state, Real dt) {
+    std::vector<Real> next(state.u_curr.size());
+    djg_report r{};
+    const int rc = djg_advance_host(engine.handle(), state.u_curr.data(), state.u_prev.data(), state.step, next.data(),
+                                    &r);
+    if (rc != DJG_OK && rc != DJG_E_INVERSION && rc != DJG_E_DIVERGENCE)
+        throw Error(rc, djg_last_error(engine.handle()));
+    if (rc == DJG_OK) {
+        state.u_prev.swap(state.u_curr);
+        state.u_curr.swap(next);
+        state.step = long(r.step);
+        state.t = dt * Real(state.step);
+    }
+    return r;
+}
+
 // run_simulation (solver.hpp:205-258) with the state resident on the B200.
 // `hook(step, t, max_abs_u, seconds_per_step)` is called every
 // p.report_stride steps and at the end, like the reference's progress hook.

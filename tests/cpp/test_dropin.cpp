@@ -62,6 +62,16 @@ void compare_runs(ElementKind kind, MaterialModel model, int div, long steps, do
     const auto r_gpu = djg::run_simulation(gpu, mass, bc, p);
     const double e_seam = rel_err(r_seam.state.u_curr, r_cpu.state.u_curr);
     const double e_gpu = rel_err(r_gpu.state.u_curr, r_cpu.state.u_curr);
+    // the same run as a host loop of djg::advance_step (djg_advance_host)
+    djg::SimState<Real> hs;
+    hs.u_curr.assign(size_t(mesh.num_dofs()), Real(0));
+    hs.u_prev = hs.u_curr;
+    for (long k = 0; k < r_cpu.steps; ++k) {
+        const djg_report rr = djg::advance_step(gpu, hs, p.dt);
+        EXPECT(rr.status == DJG_OK, "host-state step failed");
+    }
+    const double e_host = rel_err(hs.u_curr, r_cpu.state.u_curr);
+    EXPECT(e_host <= tol, "host-state loop differs: %.3e", e_host);
     std::printf("%s-%s d=%d f%zu steps=%ld: seam %.3e  device %.3e  (max|u| %.4f)\n", to_string(kind),
                 to_string(model), div, 8 * sizeof(Real), r_cpu.steps, e_seam, e_gpu,
                 [&] { double m = 0; for (Real v : r_cpu.state.u_curr) m = std::max(m, std::abs(double(v))); return m; }());

@@ -993,6 +993,7 @@ public:
         for (void* p : ipc_open_) cudaIpcCloseMemHandle(p);
         if (evFork_) cudaEventDestroy(evFork_);
         if (evPrev_) cudaEventDestroy(evPrev_);
+        for (auto e : evChunk_) cudaEventDestroy(e);
         if (evJoin_) cudaEventDestroy(evJoin_);
         if (side_) cudaStreamDestroy(side_);
         if (graph_big_) cudaGraphExecDestroy(graph_big_);
@@ -1080,9 +1081,35 @@ public:
         CK(cudaGetLastError());
         launch_element(stream_, 0, E_);
         CK(cudaStreamWaitEvent(stream_, evPrev_, 0));
-        launch_node(stream_, 0, false);
-        k_unpack_nodes<Real><<<gn, 256, 0, stream_>>>(u_[(ph + 1) % 3].as<Node>(), N_, flat_.as<Real>());
-        CK(cudaMemcpyAsync(u_next, flat_.p, bytes, cudaMemcpyDeviceToHost, stream_));
+        // node update in chunks of 32-node slices, each chunk's new u_curr
+        // going back on the side stream while the next chunk updates (the
+        // last chunk closes the step)
+        const int64_t S = (N_ + 31) / 32;
+        const int nc = S >= 4 * 256 ? kHostChunks : 1;
+        if (!allSlices_.p) {
+            std::vector<int32_t> ids(static_cast<size_t>(S));
+            for (int64_t i = 0; i < S; ++i) ids[size_t(i)] = int32_t(i);
+            allSlices_.alloc(ids.size() * sizeof(int32_t));
+            CK(cudaMemcpy(allSlices_.p, ids.data(), allSlices_.bytes, cudaMemcpyHostToDevice));
+            evChunk_.resize(kHostChunks + 1);
+            for (auto& e : evChunk_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        const Node* unew = u_[(ph + 1) % 3].as<Node>();
+        for (int c = 0; c < nc; ++c) {
+            const int64_t s0 = S * c / nc, s1 = S * (c + 1) / nc;
+            const int ns = int(s1 - s0);
+            k_node_slices<Real, false><<<unsigned(std::max(1, (ns * 32 + 255) / 256)), 256, 0, stream_>>>(
+                na_, allSlices_.as<int>() + s0, ns, 0, c == nc - 1 ? 1 : 0);
+            const int64_t n0 = 32 * s0, n1 = std::min<int64_t>(N_, 32 * s1);
+            k_unpack_nodes<Real><<<unsigned((n1 - n0 + 255) / 256), 256, 0, stream_>>>(unew + n0, n1 - n0,
+                                                                                       flat_.as<Real>() + 3 * n0);
+            CK(cudaEventRecord(evChunk_[size_t(c)], stream_));
+            CK(cudaStreamWaitEvent(side_, evChunk_[size_t(c)], 0));
+            CK(cudaMemcpyAsync(static_cast<Real*>(u_next) + 3 * n0, flat_.as<Real>() + 3 * n0,
+                               size_t(3 * (n1 - n0)) * sizeof(Real), cudaMemcpyDeviceToHost, side_));
+        }
+        CK(cudaEventRecord(evChunk_[size_t(kHostChunks)], side_));
+        CK(cudaStreamWaitEvent(stream_, evChunk_[size_t(kHostChunks)], 0));
         CK(cudaGetLastError());
         const int status = sync(rep);
         if (status != DJG_OK) {  // the state did not advance: hand back u_curr
@@ -1442,7 +1469,9 @@ private:
     cudaEvent_t evFork_ = nullptr, evJoin_ = nullptr;
     bool peer_ = false;                // peer-memory multi-GPU step
     cudaEvent_t evPrev_ = nullptr;     // djg_advance_host: u_prev uploaded
-    DevBuf flat2_;
+    DevBuf flat2_, allSlices_;
+    std::vector<cudaEvent_t> evChunk_;
+    static constexpr int kHostChunks = 4;
     PeerArgs<Real> pa_{};
     DevBuf mailbox_, destOff_, dest_, peerU_, peerMail_;
     std::vector<void*> ipc_open_;

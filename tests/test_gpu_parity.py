@@ -547,3 +547,23 @@ def test_advance_host_matches_device_loop(precision):
             u, up = un, u
         else:
             pytest.fail("the crushing ramp never failed")
+
+
+def test_advance_host_chunked_readback():
+    """A mesh with >= 1024 node slices: the host-state step updates the nodes
+    in 4 chunks whose results go back while the next chunk computes; same bits
+    as the device loop."""
+    spec = box_spec(kind="T4", model="NH", divisions=33, precision=4, target=0.01, ramp_steps=30)
+    sc = Scenario(spec)
+    assert (sc.num_nodes + 31) // 32 >= 1024
+    with GpuDjEngine(sc) as ref:
+        ref.step(30)
+        u_ref, up_ref, _ = ref.get_state()
+    with GpuDjEngine(sc) as eng:
+        n3 = 3 * sc.num_nodes
+        u, up = np.zeros(n3, np.float32), np.zeros(n3, np.float32)
+        for s in range(30):
+            un, rep = eng.advance_host(u, up, s)
+            assert rep.status == 0
+            u, up = un, u
+    assert np.array_equal(u, u_ref) and np.array_equal(up, up_ref) and np.abs(u).max() > 0

@@ -567,3 +567,20 @@ def test_advance_host_chunked_readback():
             assert rep.status == 0
             u, up = un, u
     assert np.array_equal(u, u_ref) and np.array_equal(up, up_ref) and np.abs(u).max() > 0
+
+
+def test_descriptor_limits_fail_loudly():
+    """32-bit slot indexing: more than INT32_MAX element-nodes is refused with
+    a config error before any device work; so is an empty mesh."""
+    spec = box_spec(kind="T4", divisions=2, precision=4)
+    sc = Scenario(spec)
+    lib = A.load_library()
+    d = sc.desc(0, 0)
+    d.num_elements = (1 << 31) // 4 + 1
+    h = C.c_void_p()
+    assert lib.djg_create(C.byref(d), C.byref(h)) == A.DJG_E_CONFIG
+    assert b"32-bit" in lib.djg_create_error()
+    d = sc.desc(0, 0)
+    d.num_elements = 0
+    assert lib.djg_create(C.byref(d), C.byref(h)) == A.DJG_E_CONFIG
+    assert b"nodes and elements" in lib.djg_create_error()

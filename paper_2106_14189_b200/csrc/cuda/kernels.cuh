@@ -926,9 +926,12 @@ struct PipeShape {
     static constexpr size_t smem_bytes(int stages) { return size_t(stages) * kStageBytes + 2 * 8 * size_t(stages); }
 };
 
-// Blocks per SM the register allocation is sized for: the compact T4
-// kernel runs best capped at 64 registers (6 blocks); heavier element bodies
-// are left uncapped rather than spilled.
+// Blocks per SM the register allocation is sized for, per material and
+// precision (DJG_PIPE_MINB_T4C{,64}_M<model>, measured on a 10.4M-tet cube,
+// tools/ab_models.py): f32 NH 6 (64 registers), TI 5, OT 4; f64 NH 4, TI 3,
+// OT 2. Tighter caps spill the heavier bodies; looser ones lose latency
+// hiding. (MR keeps the full record by default.) The full-record forms are
+// left uncapped.
 #ifndef DJG_PIPE_MINB_T4C
 #define DJG_PIPE_MINB_T4C 6
 #endif
@@ -938,9 +941,32 @@ struct PipeShape {
 #ifndef DJG_PIPE_MINB_T4C64
 #define DJG_PIPE_MINB_T4C64 4
 #endif
-template <class Real, int KIND, int FORM>
-constexpr int kPipeMinBlocks = (KIND == 0 && FORM == 1) ? (sizeof(Real) == 4 ? DJG_PIPE_MINB_T4C : DJG_PIPE_MINB_T4C64)
-                                                        : DJG_PIPE_MINB_OTHER;
+#ifndef DJG_PIPE_MINB_T4C_M1
+#define DJG_PIPE_MINB_T4C_M1 5
+#endif
+#ifndef DJG_PIPE_MINB_T4C_M2
+#define DJG_PIPE_MINB_T4C_M2 4
+#endif
+#ifndef DJG_PIPE_MINB_T4C_M3
+#define DJG_PIPE_MINB_T4C_M3 4
+#endif
+#ifndef DJG_PIPE_MINB_T4C64_M1
+#define DJG_PIPE_MINB_T4C64_M1 3
+#endif
+#ifndef DJG_PIPE_MINB_T4C64_M2
+#define DJG_PIPE_MINB_T4C64_M2 2
+#endif
+#ifndef DJG_PIPE_MINB_T4C64_M3
+#define DJG_PIPE_MINB_T4C64_M3 2
+#endif
+template <class Real, int MODEL>
+constexpr int kPipeMinBlocksT4C =
+    sizeof(Real) == 4 ? (MODEL == 1 ? DJG_PIPE_MINB_T4C_M1 : MODEL == 2 ? DJG_PIPE_MINB_T4C_M2
+                                                   : MODEL == 3 ? DJG_PIPE_MINB_T4C_M3 : DJG_PIPE_MINB_T4C)
+                      : (MODEL == 1 ? DJG_PIPE_MINB_T4C64_M1 : MODEL == 2 ? DJG_PIPE_MINB_T4C64_M2
+                                                     : MODEL == 3 ? DJG_PIPE_MINB_T4C64_M3 : DJG_PIPE_MINB_T4C64);
+template <class Real, int KIND, int MODEL, int FORM>
+constexpr int kPipeMinBlocks = (KIND == 0 && FORM == 1) ? kPipeMinBlocksT4C<Real, MODEL> : DJG_PIPE_MINB_OTHER;
 constexpr int kPipeThreads = kPipeTile + 32;  // 4 compute warps + the producer warp
 
 // Persistent blocks; tile `it` of a block (global tile blockIdx + it * grid)
@@ -950,7 +976,7 @@ constexpr int kPipeThreads = kPipeTile + 32;  // 4 compute warps + the producer 
 // of a compute warp instead, or also prefetching the next tile's gathers,
 // measured slower.)
 template <class Real, int KIND, int MODEL, int RB, int FORM, int STAGES>
-__global__ void __launch_bounds__(kPipeThreads, (kPipeMinBlocks<Real, KIND, FORM>)) k_element_pipe(const ElemArgs<Real> A, long long e0,
+__global__ void __launch_bounds__(kPipeThreads, (kPipeMinBlocks<Real, KIND, MODEL, FORM>)) k_element_pipe(const ElemArgs<Real> A, long long e0,
                                                                               long long e1) {
     using PS = PipeShape<Real, KIND, MODEL, RB, FORM>;
     using Plane = typename RT<Real>::Plane;

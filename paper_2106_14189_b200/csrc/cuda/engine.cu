@@ -197,12 +197,11 @@ public:
         flags_ = d.flags;
         if (const char* v = std::getenv("DJG_SLAB_KB")) slab_bytes_ = int64_t(std::atoll(v)) << 10;
         nconst_ = const_count(kind_, model_);
-        // Default record: compact (fewer bytes win) except where rebuilding
-        // the m / I tensors costs more than it saves -- H8 in f64 (cfg4-sized
-        // meshes) and Mooney-Rivlin (its 57 second-invariant Reals: compact MR
-        // T4 measured 2.1x (f32) / 2.7x (f64) slower than the full record).
+        // Default record: compact (fewer bytes win) except for Mooney-Rivlin,
+        // whose 57 second-invariant Reals cost more to rebuild than to read
+        // (compact MR T4 measured 2.1x (f32) / 2.7x (f64) slower than full).
         tled_ = (flags_ & DJG_FLAG_TLED) != 0;
-        const bool compact_default = d.material.model != DJG_MR && (d.kind == DJG_T4 || sizeof(Real) == 4);
+        const bool compact_default = d.material.model != DJG_MR;
         compact_ = !tled_ && ((flags_ & DJG_FLAG_COMPACT) != 0 ||
                               (!(flags_ & DJG_FLAG_FULL_RECORD) && compact_default));
         // The compact T4 record is empty: the kernel rebuilds J0 from the node

@@ -649,13 +649,22 @@ __device__ __forceinline__ P pick3(int i, P a, P b, P c) {
 // Blocks per SM the one-shot kernel's registers are sized for. Left alone,
 // ptxas gives the f32 H8 bodies ~170 registers (3 blocks, 12 warps per SM)
 // to hoist every record load; capping at 5 blocks (~96 registers) is 10-20 %
-// faster for NH / TI / OT (cfg4-sized meshes). The MR body and the f64
-// bodies spill under that cap and stay uncapped.
+// faster for NH / TI / OT (cfg4-sized meshes). The f64 NH / TI / OT bodies
+// (~210-250 registers uncapped) run 7-16 % faster capped at 3 blocks. The MR
+// bodies spill under a cap and stay uncapped (tools/ab_h8_caps.sh).
 #ifndef DJG_K1_MINB_H8
 #define DJG_K1_MINB_H8 5
 #endif
+#ifndef DJG_K1_MINB_H8_MR
+#define DJG_K1_MINB_H8_MR 1
+#endif
+#ifndef DJG_K1_MINB_H8_64
+#define DJG_K1_MINB_H8_64 3
+#endif
 template <class Real, int KIND, int MODEL>
-constexpr int kElemMinBlocks = (KIND == 1 && sizeof(Real) == 4 && MODEL != 3) ? DJG_K1_MINB_H8 : 1;
+constexpr int kElemMinBlocks = KIND != 1 ? 1
+                               : MODEL == 3 ? DJG_K1_MINB_H8_MR
+                               : sizeof(Real) == 8 ? DJG_K1_MINB_H8_64 : DJG_K1_MINB_H8;
 
 template <class Real, int KIND, int MODEL, int RB, bool COMPACT>
 __global__ void __launch_bounds__(128, (kElemMinBlocks<Real, KIND, MODEL>)) k_element(const ElemArgs<Real> A, long long e0, long long e1) {

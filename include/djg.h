@@ -47,6 +47,7 @@ extern "C" {
  *   TI, OT:  m4[6], I4m[6]
  *   OT:      m6[6], I6m[6]
  *   MR:      M2 (21, packed upper Sym6, core.hpp:282-305), I2m[6] (6 x 6)
+ *   I57:     M5 (21), I5m[6] (6 x 6), M7 (21), I7m[6] (6 x 6)  (full record only)
  *   H8:      k_hg, hg_gamma[4][8]
  */
 #define DJG_CONST_BASE 23

@@ -31,8 +31,16 @@ extern "C" {
 /* ElementKind (element.hpp:9) */
 enum djg_element_kind { DJG_T4 = 0, DJG_H8 = 1 };
 
-/* MaterialModel (material.hpp:9) */
-enum djg_material_model { DJG_NH = 0, DJG_TI = 1, DJG_OT = 2, DJG_MR = 3 };
+/* MaterialModel (material.hpp:9), plus DJG_I57: the fifth/seventh-invariant
+ * energy the reference drives its I5 / I7 force terms with
+ * (test_forces.cpp:248-271; djtled_force.hpp:58-65, kinematics.hpp:89-101,
+ * precompute.hpp:237-248):
+ *   psi = mu/2 (Ib1 - 3) + eta5/2 (Ib5 - 1)^2 + eta7/2 (Ib7 - 1)^2 + kappa/2 (J - 1)^2,
+ * eta5 / eta7 carried in eta_a / eta_b, fibre families a and b. No named
+ * reference Material selects i5 / i7 (material.hpp:93-99), so this model has
+ * no reference engine counterpart; its element terms are pinned against the
+ * reference's element_force with these derivatives (oracle/ref_driver.cpp). */
+enum djg_material_model { DJG_NH = 0, DJG_TI = 1, DJG_OT = 2, DJG_MR = 3, DJG_I57 = 4 };
 
 /* InversionPolicy (djtled_force.hpp:97) */
 enum djg_inversion_policy { DJG_ABORT = 0, DJG_SKIP_AND_REPORT = 1 };

@@ -119,20 +119,50 @@ static void FN(hourglass_vectors)(const R x[8][3], const R d[3][8], const R jinv
     }
 }
 
-/* Unit fibre (FibreDirections::normalise, precompute.hpp:35-39) and A = a a^T */
-static void FN(fibre_tensor)(const double v[3], R A[6]) {
+/* Unit fibre (FibreDirections::normalise, precompute.hpp:35-39) into u and
+ * A = a a^T */
+static void FN(fibre_tensor)(const double v[3], R A[6], R u[3]) {
     const R a0 = (R)v[0], a1 = (R)v[1], a2 = (R)v[2];
     const R n = SQRT(a0 * a0 + a1 * a1 + a2 * a2);
     const R s = (R)1 / n;
     const R u0 = s * a0, u1 = s * a1, u2 = s * a2;
+    u[0] = u0; u[1] = u1; u[2] = u2;
     A[0] = u0 * u0; A[1] = u1 * u1; A[2] = u2 * u2;
     A[3] = u0 * u1; A[4] = u0 * u2; A[5] = u1 * u2;
+}
+
+/* trace_matrix(G, s) (precompute.hpp:86-95): M[p][q] = (G_p s) . (G_q s),
+ * packed upper; second_order_tensors(J0inv, V0, G, S) (precompute.hpp:
+ * 117-131): 2 V0 J0inv^T (S G_k + G_k S) J0inv. The I5 (a) / I7 (b) blocks. */
+static void FN(fibre_second_order)(R G[6][6], const R Ji[3][3], R two_v0, const R u[3], const R S[6], R* M,
+                                   R* Im) {
+    R gs[6][3];
+    for (int k = 0; k < 6; ++k) {
+        const R* g = G[k]; /* full(): [[xx,xy,xz],[xy,yy,yz],[xz,yz,zz]] */
+        gs[k][0] = g[0] * u[0] + g[3] * u[1] + g[4] * u[2];
+        gs[k][1] = g[3] * u[0] + g[1] * u[1] + g[5] * u[2];
+        gs[k][2] = g[4] * u[0] + g[5] * u[1] + g[2] * u[2];
+    }
+    for (int p = 0; p < 6; ++p)
+        for (int q = p; q < 6; ++q) M[sym6_index(p, q)] = gs[p][0] * gs[q][0] + gs[p][1] * gs[q][1] + gs[p][2] * gs[q][2];
+    const R Sf[3][3] = {{S[0], S[3], S[4]}, {S[3], S[1], S[5]}, {S[4], S[5], S[2]}};
+    for (int k = 0; k < 6; ++k) {
+        const R* g = G[k];
+        const R Gf[3][3] = {{g[0], g[3], g[4]}, {g[3], g[1], g[5]}, {g[4], g[5], g[2]}};
+        R P[3][3]; /* mul(S.full(), G_k.full()) */
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) P[i][j] = Sf[i][0] * Gf[0][j] + Sf[i][1] * Gf[1][j] + Sf[i][2] * Gf[2][j];
+        const R ker[6] = {2 * P[0][0], 2 * P[1][1], 2 * P[2][2], P[0][1] + P[1][0], P[0][2] + P[2][0], P[1][2] + P[2][1]};
+        R t[6];
+        FN(congruence)(Ji, ker, t);
+        for (int c = 0; c < 6; ++c) Im[6 * k + c] = two_v0 * t[c];
+    }
 }
 
 /* build_element_constants hot fields (precompute.hpp:206-255) into the
  * canonical record of include/djg.h. Returns 0 on a bad element. */
 static int FN(element_record)(const R x[8][3], int kind, int model, R c_hg, R kappa, const R A[6], const R B[6],
-                              R* out) {
+                              const R a[3], const R b[3], R* out) {
     layout_t L = layout_of(kind, model);
     R d[3][8], J[3][3], Ji[3][3], det;
     FN(shape)(kind, d);
@@ -184,6 +214,10 @@ static int FN(element_record)(const R x[8][3], int kind, int model, R c_hg, R ka
         for (int k = 0; k < 6; ++k) out[L.m6 + k] = FN(ddot)(B, G[k]);
         FN(congruence)(Ji, B, t);
         for (int c = 0; c < 6; ++c) out[L.I6m + c] = two_v0 * t[c];
+    }
+    if (model == DJG_I57) {
+        FN(fibre_second_order)(G, Ji, two_v0, a, A, out + L.M5, out + L.I5m);
+        FN(fibre_second_order)(G, Ji, two_v0, b, B, out + L.M7, out + L.I7m);
     }
     if (kind == DJG_H8) {
         R gamma[4][8];
@@ -289,6 +323,25 @@ static int FN(element_force)(int kind, const FN(mat_t)* mat, const R* rec, const
         const R w = j_m23 * dI2;
         for (int k = 0; k < 6; ++k) s[k] = s[k] + w * cg[k];
         dev += 2 * dI2 * Ib2;
+    }
+    if (mat->model == DJG_I57) {
+        /* need.i5, need.i7 (kinematics.hpp:89-101; djtled_force.hpp:58-65)
+         * with the derivatives of test_forces.cpp:262-268 */
+        const int Mo[2] = {L.M5, L.M7}, Io[2] = {L.I5m, L.I7m};
+        const R eta[2] = {mat->eta_a, mat->eta_b};
+        for (int f = 0; f < 2; ++f) {
+            const R I = FN(quadform)(rec + Mo[f], g);
+            const R Ib = j_m43 * I;
+            const R dI = eta[f] * (Ib - 1);
+            R cg[6];
+            const R* Im = rec + Io[f];
+            for (int c = 0; c < 6; ++c) cg[c] = g[0] * Im[c];
+            for (int k = 1; k < 6; ++k)
+                for (int c = 0; c < 6; ++c) cg[c] = cg[c] + g[k] * Im[6 * k + c];
+            const R w = j_m23 * dI;
+            for (int k = 0; k < 6; ++k) s[k] = s[k] + w * cg[k];
+            dev += 2 * dI * Ib;
+        }
     }
     const R c = (-(R)2 / (R)3 * dev + J * dJ) * rec[10];
     /* K = j_m23 (Jt^T S) + c Jt^-1 */
@@ -469,9 +522,10 @@ static int FN(prob_build)(const djg_scenario_spec* s, FN(prob_t)* P) {
     const int64_t N = P->N, E = P->E;
     const int npe = P->npe, nc = P->nconst;
     /* constants */
-    R A[6] = {0}, B[6] = {0};
-    if (s->material.model == DJG_TI || s->material.model == DJG_OT) FN(fibre_tensor)(s->material.fibre_a, A);
-    if (s->material.model == DJG_OT) FN(fibre_tensor)(s->material.fibre_b, B);
+    R A[6] = {0}, B[6] = {0}, ua[3] = {0}, ub[3] = {0};
+    const int mdl = s->material.model;
+    if (mdl == DJG_TI || mdl == DJG_OT || mdl == DJG_I57) FN(fibre_tensor)(s->material.fibre_a, A, ua);
+    if (mdl == DJG_OT || mdl == DJG_I57) FN(fibre_tensor)(s->material.fibre_b, B, ub);
     P->consts = (R*)calloc((size_t)(E > 0 ? E : 1) * nc, sizeof(R));
     int bad = 0;
     const R c_hg = (R)s->c_hg;
@@ -479,7 +533,7 @@ static int FN(prob_build)(const djg_scenario_spec* s, FN(prob_t)* P) {
     for (int64_t e = 0; e < E; ++e) {
         R x[8][3];
         FN(gather_x)(P, e, x);
-        if (!FN(element_record)(x, P->kind, s->material.model, c_hg, P->mat.kappa, A, B, P->consts + e * nc)) bad = 1;
+        if (!FN(element_record)(x, P->kind, mdl, c_hg, P->mat.kappa, A, B, ua, ub, P->consts + e * nc)) bad = 1;
     }
     if (bad) return DJG_E_CONFIG;
     /* adjacency: counting sort in ascending element order */

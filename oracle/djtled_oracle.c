@@ -38,15 +38,16 @@ static int sym6_index(int i, int j) {
 
 /* Offsets of the canonical hot-field record (include/djg.h). */
 typedef struct {
-    int m4, I4m, m6, I6m, M2, I2m, khg, gamma, count;
+    int m4, I4m, m6, I6m, M2, I2m, M5, I5m, M7, I7m, khg, gamma, count;
 } layout_t;
 
 static layout_t layout_of(int kind, int model) {
-    layout_t L = {-1, -1, -1, -1, -1, -1, -1, -1, 23};
+    layout_t L = {-1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, -1, 23};
     int o = 23;
     if (model == DJG_TI || model == DJG_OT) { L.m4 = o; L.I4m = o + 6; o += 12; }
     if (model == DJG_OT) { L.m6 = o; L.I6m = o + 6; o += 12; }
     if (model == DJG_MR) { L.M2 = o; L.I2m = o + 21; o += 57; }
+    if (model == DJG_I57) { L.M5 = o; L.I5m = o + 21; L.M7 = o + 57; L.I7m = o + 78; o += 114; }
     if (kind == DJG_H8) { L.khg = o; L.gamma = o + 1; o += 33; }
     L.count = o;
     return L;
@@ -210,23 +211,27 @@ int djo_element_force_rec(int32_t precision, int32_t kind, const djg_material_pa
 int djo_element_record(int32_t precision, int32_t kind, const djg_material_params* m, double c_hg,
                        const double* coords, void* rec) {
     const int npe = kind == DJG_T4 ? 4 : 8;
+    const int fa = m->model == DJG_TI || m->model == DJG_OT || m->model == DJG_I57;
+    const int fb = m->model == DJG_OT || m->model == DJG_I57;
     if (precision == 4) {
-        float x[8][3] = {{0}}, A[6] = {0}, B[6] = {0};
+        float x[8][3] = {{0}}, A[6] = {0}, B[6] = {0}, ua[3] = {0}, ub[3] = {0};
         for (int a = 0; a < npe; ++a)
             for (int i = 0; i < 3; ++i) x[a][i] = (float)coords[3 * a + i];
-        if (m->model == DJG_TI || m->model == DJG_OT) fibre_tensor_f(m->fibre_a, A);
-        if (m->model == DJG_OT) fibre_tensor_f(m->fibre_b, B);
-        return element_record_f((const float(*)[3])x, kind, m->model, (float)c_hg, (float)m->kappa, A, B, (float*)rec)
+        if (fa) fibre_tensor_f(m->fibre_a, A, ua);
+        if (fb) fibre_tensor_f(m->fibre_b, B, ub);
+        return element_record_f((const float(*)[3])x, kind, m->model, (float)c_hg, (float)m->kappa, A, B, ua, ub,
+                                (float*)rec)
                    ? 0
                    : DJG_E_CONFIG;
     }
-    double x[8][3] = {{0}}, A[6] = {0}, B[6] = {0};
+    double x[8][3] = {{0}}, A[6] = {0}, B[6] = {0}, ua[3] = {0}, ub[3] = {0};
     for (int a = 0; a < npe; ++a)
         for (int i = 0; i < 3; ++i) x[a][i] = coords[3 * a + i];
-    if (m->model == DJG_TI || m->model == DJG_OT) fibre_tensor_d(m->fibre_a, A);
-    if (m->model == DJG_OT) fibre_tensor_d(m->fibre_b, B);
-    return element_record_d((const double(*)[3])x, kind, m->model, c_hg, m->kappa, A, B, (double*)rec) ? 0
-                                                                                                        : DJG_E_CONFIG;
+    if (fa) fibre_tensor_d(m->fibre_a, A, ua);
+    if (fb) fibre_tensor_d(m->fibre_b, B, ub);
+    return element_record_d((const double(*)[3])x, kind, m->model, c_hg, m->kappa, A, B, ua, ub, (double*)rec)
+               ? 0
+               : DJG_E_CONFIG;
 }
 
 int djo_const_count(int32_t kind, int32_t model) { return layout_of(kind, model).count; }

@@ -33,6 +33,10 @@ Material<Real> make_material(const djg_material_params& p) {
         case DJG_OT:
             return Material<Real>::orthotropic(Real(p.mu), Real(p.eta_a), Real(p.eta_b), Real(p.kappa), Real(p.rho), a, b);
         case DJG_MR: return Material<Real>::mooney_rivlin(Real(p.c10), Real(p.c01), Real(p.kappa), Real(p.rho));
+        // DJG_I57 has no reference Material: the neo-Hookean part carries mu,
+        // kappa and rho; element_impl supplies the I5 / I7 need set,
+        // fibres and derivatives of test_forces.cpp:248-271.
+        case DJG_I57: return Material<Real>::neo_hookean(Real(p.mu), Real(p.kappa), Real(p.rho));
     }
     throw ConfigError("unknown material model");
 }
@@ -270,10 +274,18 @@ int element_impl(int kind_i, const djg_material_params& mp, double c_hg, const d
         ue[a] = {Real(u[3 * a]), Real(u[3 * a + 1]), Real(u[3 * a + 2])};
     }
     ElementForces<Real> ef;
-    const auto need = mat.needs();
+    const bool i57 = mp.model == DJG_I57;
+    auto need = mat.needs();
     FibreDirections<Real> fib;
     const FibreDirections<Real>* fp = nullptr;
-    if (need.any_fibre_a() || need.any_fibre_b()) {
+    if (i57) {  // test_forces.cpp:253-257
+        if (engine != 0) throw ConfigError("I57 has no TLED form");
+        need.i5 = need.i7 = true;
+        const Vec3<Real> a{Real(mp.fibre_a[0]), Real(mp.fibre_a[1]), Real(mp.fibre_a[2])};
+        const Vec3<Real> b{Real(mp.fibre_b[0]), Real(mp.fibre_b[1]), Real(mp.fibre_b[2])};
+        fib = FibreDirections<Real>::from(a, &b);
+        fp = &fib;
+    } else if (need.any_fibre_a() || need.any_fibre_b()) {
         fib = mat.fibres();
         fp = &fib;
     }
@@ -281,7 +293,12 @@ int element_impl(int kind_i, const djg_material_params& mp, double c_hg, const d
         const auto ec = build_element_constants(coords, D, need, fp, mat.kappa, Real(c_hg));
         ElementKinematics<Real> kin;
         if (!update_kinematics(ec, ue, D, need, kin)) return DJG_E_INVERSION;
-        ef = element_force(ec, kin, energy_derivatives(mat, kin.inv), need, D);
+        EnergyDerivatives<Real> dv = energy_derivatives(mat, kin.inv);
+        if (i57) {  // test_forces.cpp:262-268, in Real
+            dv.dI5 = Real(mp.eta_a) * (kin.inv.Ib5 - 1);
+            dv.dI7 = Real(mp.eta_b) * (kin.inv.Ib7 - 1);
+        }
+        ef = element_force(ec, kin, dv, need, D);
         if (ec.has_hourglass) hourglass_force(ec.hg_gamma, ec.k_hg, ue, ef);
     } else {
         const auto j0 = jacobian0(coords, D);

@@ -17,7 +17,7 @@ PKG_DIR = Path(__file__).resolve().parent
 LIB_PATH = Path(os.environ.get("DJG_LIB_PATH") or PKG_DIR / "_build" / "libdjg.so")
 
 DJG_T4, DJG_H8 = 0, 1
-DJG_NH, DJG_TI, DJG_OT, DJG_MR = 0, 1, 2, 3
+DJG_NH, DJG_TI, DJG_OT, DJG_MR, DJG_I57 = 0, 1, 2, 3, 4
 DJG_ABORT, DJG_SKIP_AND_REPORT = 0, 1
 DJG_FREE, DJG_FIXED, DJG_PRESCRIBED = 0, 1, 2
 DJG_OK, DJG_E_INTERNAL, DJG_E_CONFIG, DJG_E_CUDA, DJG_E_INVERSION, DJG_E_DIVERGENCE = 0, 1, 2, 3, 4, 5
@@ -33,7 +33,7 @@ DJG_PART_RCB, DJG_PART_METIS = 0, 1
 PART_METHODS = {"rcb": DJG_PART_RCB, "metis": DJG_PART_METIS}
 
 KIND_NAMES = {"T4": DJG_T4, "H8": DJG_H8}
-MODEL_NAMES = {"NH": DJG_NH, "TI": DJG_TI, "OT": DJG_OT, "MR": DJG_MR}
+MODEL_NAMES = {"NH": DJG_NH, "TI": DJG_TI, "OT": DJG_OT, "MR": DJG_MR, "I57": DJG_I57}
 
 
 def npe_of(kind: int) -> int:
@@ -49,6 +49,8 @@ def const_count(kind: int, model: int) -> int:
         n += 12
     if model == DJG_MR:
         n += 57
+    if model == DJG_I57:
+        n += 114
     if kind == DJG_H8:
         n += 33
     return n

@@ -169,6 +169,39 @@ DJG_HD void second_invariant_tensors(const R ji[3][3], R v0, const R m1[6], R m2
     }
 }
 
+// Fibre second-order family for a unit fibre s, S = s s^T (precompute.hpp:
+// 86-95, 117-131): M[p][q] = (G_p s) . (G_q s) packed upper, and
+// Im_k = 2 V0 J0inv^T (S G_k + G_k S) J0inv. Used by I5 (a, A) and I7 (b, B).
+template <class R>
+DJG_HD void fibre_second_tensors(const R ji[3][3], R v0, const R s[3], const R S[6], R m[21], R im[36]) {
+    R gs[6][3];
+    for (int k = 0; k < 6; ++k) {  // mul(G_k.full(), s)
+        R g[6];
+        g_matrix(ji, k, g);
+        gs[k][0] = g[0] * s[0] + g[3] * s[1] + g[4] * s[2];
+        gs[k][1] = g[3] * s[0] + g[1] * s[1] + g[5] * s[2];
+        gs[k][2] = g[4] * s[0] + g[5] * s[1] + g[2] * s[2];
+    }
+    int w = 0;
+    for (int p = 0; p < 6; ++p)
+        for (int q = p; q < 6; ++q) m[w++] = gs[p][0] * gs[q][0] + gs[p][1] * gs[q][1] + gs[p][2] * gs[q][2];
+    const R sf[3][3] = {{S[0], S[3], S[4]}, {S[3], S[1], S[5]}, {S[4], S[5], S[2]}};
+    const R two_v0 = 2 * v0;
+    for (int k = 0; k < 6; ++k) {
+        R g[6];
+        g_matrix(ji, k, g);
+        const R gf[3][3] = {{g[0], g[3], g[4]}, {g[3], g[1], g[5]}, {g[4], g[5], g[2]}};
+        R sg[3][3];  // mul(S.full(), G_k.full())
+        for (int i = 0; i < 3; ++i)
+            for (int j = 0; j < 3; ++j) sg[i][j] = sf[i][0] * gf[0][j] + sf[i][1] * gf[1][j] + sf[i][2] * gf[2][j];
+        const R ker[6] = {2 * sg[0][0], 2 * sg[1][1], 2 * sg[2][2],
+                          sg[0][1] + sg[1][0], sg[0][2] + sg[2][0], sg[1][2] + sg[2][1]};
+        R t[6];
+        congruence(ji, ker, t);
+        for (int c = 0; c < 6; ++c) im[6 * k + c] = two_v0 * t[c];
+    }
+}
+
 // Hourglass shape vectors (precompute.hpp:136-165).
 template <class R>
 DJG_HD void hourglass_vectors(const R x[8][3], const R ji[3][3], R gamma[4][8]) {

@@ -72,6 +72,7 @@ inline int const_count(int kind, int model) {
     if (model == DJG_TI || model == DJG_OT) n += 12;
     if (model == DJG_OT) n += 12;
     if (model == DJG_MR) n += 57;
+    if (model == DJG_I57) n += 114;
     if (kind == DJG_H8) n += 33;
     return n;
 }
@@ -201,7 +202,10 @@ public:
         // whose 57 second-invariant Reals cost more to rebuild than to read
         // (compact MR T4 measured 2.1x (f32) / 2.7x (f64) slower than full).
         tled_ = (flags_ & DJG_FLAG_TLED) != 0;
-        const bool compact_default = d.material.model != DJG_MR;
+        if (model_ == DJG_I57 && (flags_ & (DJG_FLAG_COMPACT | DJG_FLAG_DEVICE_PRECOMPUTE | DJG_FLAG_TLED)))
+            throw DescError("the I57 energy runs on the host-built full record only "
+                            "(no DJG_FLAG_COMPACT / DJG_FLAG_DEVICE_PRECOMPUTE / DJG_FLAG_TLED)");
+        const bool compact_default = model_ != DJG_MR && model_ != DJG_I57;
         compact_ = !tled_ && ((flags_ & DJG_FLAG_COMPACT) != 0 ||
                               (!(flags_ & DJG_FLAG_FULL_RECORD) && compact_default));
         // The compact T4 record is empty: the kernel rebuilds J0 from the node
@@ -1208,21 +1212,32 @@ public:
             else k_element<Real, K, M, 2, false><<<grid, 128, 0, s>>>(a, e0, e1);                               \
         }                                                                                                       \
     } while (0)
+// DJG_I57: the full-record one-shot kernel only (its 137-Real record is
+// beyond the pipeline's stage budget; compact / TLED are refused at creation).
+#define DJG_K1_FULL(K, M)                                                                                       \
+    do {                                                                                                        \
+        if (setup) { pipe_ = false; return; }                                                                   \
+        if (rank_bytes_ == 1) k_element<Real, K, M, 1, false><<<grid, 128, 0, s>>>(a, e0, e1);                  \
+        else k_element<Real, K, M, 2, false><<<grid, 128, 0, s>>>(a, e0, e1);                                   \
+    } while (0)
         if (kind_ == DJG_T4) {
             switch (model_) {
                 case DJG_NH: DJG_K1(0, 0); break;
                 case DJG_TI: DJG_K1(0, 1); break;
                 case DJG_OT: DJG_K1(0, 2); break;
-                default: DJG_K1(0, 3); break;
+                case DJG_MR: DJG_K1(0, 3); break;
+                default: DJG_K1_FULL(0, 4); break;
             }
         } else {
             switch (model_) {
                 case DJG_NH: DJG_K1(1, 0); break;
                 case DJG_TI: DJG_K1(1, 1); break;
                 case DJG_OT: DJG_K1(1, 2); break;
-                default: DJG_K1(1, 3); break;
+                case DJG_MR: DJG_K1(1, 3); break;
+                default: DJG_K1_FULL(1, 4); break;
             }
         }
+#undef DJG_K1_FULL
 #undef DJG_K1
         CK(cudaGetLastError());
     }
@@ -1565,7 +1580,7 @@ int djg_create(const djg_desc* d, djg_engine** out) {
     *out = nullptr;
     try {
         if (d->kind != DJG_T4 && d->kind != DJG_H8) throw djg::DescError("unknown element kind");
-        if (d->material.model < DJG_NH || d->material.model > DJG_MR) throw djg::DescError("unknown material model");
+        if (d->material.model < DJG_NH || d->material.model > DJG_I57) throw djg::DescError("unknown material model");
         if (d->inversion_policy != DJG_ABORT && d->inversion_policy != DJG_SKIP_AND_REPORT)
             throw djg::DescError("unknown inversion policy");
         auto eng = std::make_unique<djg_engine>();

@@ -81,12 +81,14 @@ struct Layout {
     static constexpr bool kI4 = MODEL == 1 || MODEL == 2;
     static constexpr bool kI6 = MODEL == 2;
     static constexpr bool kI2 = MODEL == 3;
+    static constexpr bool kI57 = MODEL == 4;  // DJG_I57: I5 and I7 (full record only)
     static constexpr bool kH8 = KIND == 1;
     static constexpr int NPE = kH8 ? 8 : 4;
     static constexpr int m4 = 23, I4m = 29;
     static constexpr int m6 = kI4 ? 35 : 23, I6m = m6 + 6;
     static constexpr int M2 = 23, I2m = 44;
-    static constexpr int after_mat = 23 + (kI4 ? 12 : 0) + (kI6 ? 12 : 0) + (kI2 ? 57 : 0);
+    static constexpr int M5 = 23, I5m = 44, M7 = 80, I7m = 101;
+    static constexpr int after_mat = 23 + (kI4 ? 12 : 0) + (kI6 ? 12 : 0) + (kI2 ? 57 : 0) + (kI57 ? 114 : 0);
     static constexpr int khg = after_mat, gamma = after_mat + 1;
     static constexpr int count = after_mat + (kH8 ? 33 : 0);
 };
@@ -346,11 +348,44 @@ template <int KIND, bool COMPACT>
 constexpr bool kTailRecord = COMPACT && KIND == 0;
 
 // One element: loads, DJ-TLED force, stores of its npe rows into their slots.
+// One fibre second-order invariant term: I = g^T M g (Sym6::quadratic_form,
+// core.hpp:296-304), Ib = J^-4/3 I (kinematics.hpp:89-101), d = eta (Ib - 1),
+// s += (J^-2/3 d) contract_ghat(g, Im), dev += 2 d Ib (djtled_force.hpp:18-24,
+// 58-65).
+template <class Real>
+__device__ __forceinline__ void fibre_quad_term(const Real* M, const Real* Im, const Real g[6], Real j_m23, Real eta,
+                                                Real s[6], Real& dev) {
+    constexpr int idx[6][6] = {{0, 1, 2, 3, 4, 5},      {1, 6, 7, 8, 9, 10},    {2, 7, 11, 12, 13, 14},
+                               {3, 8, 12, 15, 16, 17}, {4, 9, 13, 16, 18, 19}, {5, 10, 14, 17, 19, 20}};
+    Real q = Real(0);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+        Real row = M[idx[i][i]] * g[i];
+#pragma unroll
+        for (int j = i + 1; j < 6; ++j) row += Real(2) * M[idx[i][j]] * g[j];
+        q += row * g[i];
+    }
+    const Real Ib = (j_m23 * j_m23) * q;
+    const Real d = eta * (Ib - Real(1));
+    Real cg[6];
+#pragma unroll
+    for (int k = 0; k < 6; ++k) cg[k] = g[0] * Im[k];
+#pragma unroll
+    for (int m = 1; m < 6; ++m)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) cg[k] = cg[k] + g[m] * Im[6 * m + k];
+    const Real w = j_m23 * d;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) s[k] = s[k] + w * cg[k];
+    dev += Real(2) * d * Ib;
+}
+
 template <class Real, int KIND, int MODEL, int RB, bool COMPACT, class Src>
 __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long long e,
                                              const typename RT<Real>::Node* __restrict__ u, const Src& src) {
     using L = Layout<KIND, MODEL>;
     using T = RT<Real>;
+    static_assert(!(COMPACT && L::kI57), "the I57 energy runs on the full record only");
     constexpr int NPE = L::NPE;
     constexpr int NP = (L::count + T::kPlane - 1) / T::kPlane;
 
@@ -560,6 +595,12 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
         for (int k = 0; k < 6; ++k) s[k] = s[k] + w * cg[k];
         dev += Real(2) * A.mat.dI2 * Ib2;
     }
+    if constexpr (L::kI57) {
+        // need.i5 then need.i7 (djtled_force.hpp:58-65) with the test
+        // energy's dI5 = eta5 (Ib5 - 1), dI7 = eta7 (Ib7 - 1).
+        fibre_quad_term(c + L::M5, c + L::I5m, g, j_m23, A.mat.eta_a, s, dev);
+        fibre_quad_term(c + L::M7, c + L::I7m, g, j_m23, A.mat.eta_b, s, dev);
+    }
     const Real cc = (-Real(2) / Real(3) * dev + J * dJ) * c[10];
 
     // K = j_m23 (Jt^T S) + c Jt^-1
@@ -663,7 +704,7 @@ __device__ __forceinline__ P pick3(int i, P a, P b, P c) {
 #endif
 template <class Real, int KIND, int MODEL>
 constexpr int kElemMinBlocks = KIND != 1 ? 1
-                               : MODEL == 3 ? DJG_K1_MINB_H8_MR
+                               : MODEL >= 3 ? DJG_K1_MINB_H8_MR
                                : sizeof(Real) == 8 ? DJG_K1_MINB_H8_64 : DJG_K1_MINB_H8;
 
 template <class Real, int KIND, int MODEL, int RB, bool COMPACT>

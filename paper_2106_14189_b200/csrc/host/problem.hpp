@@ -56,6 +56,7 @@ inline int const_count(int kind, int model) {
     if (model == DJG_TI || model == DJG_OT) n += 12;
     if (model == DJG_OT) n += 12;
     if (model == DJG_MR) n += 21 + 36;
+    if (model == DJG_I57) n += 2 * (21 + 36);
     if (kind == DJG_H8) n += 33;
     return n;
 }
@@ -63,13 +64,15 @@ inline int const_count(int kind, int model) {
 // Field offsets inside the canonical record.
 struct ConstLayout {
     int J0 = 0, det = 9, V0 = 10, m1 = 11, I1m = 17;
-    int m4 = -1, I4m = -1, m6 = -1, I6m = -1, M2 = -1, I2m = -1, khg = -1, gamma = -1;
+    int m4 = -1, I4m = -1, m6 = -1, I6m = -1, M2 = -1, I2m = -1, M5 = -1, I5m = -1, M7 = -1, I7m = -1;
+    int khg = -1, gamma = -1;
     int count = 23;
     ConstLayout(int kind, int model) {
         int o = 23;
         if (model == DJG_TI || model == DJG_OT) { m4 = o; I4m = o + 6; o += 12; }
         if (model == DJG_OT) { m6 = o; I6m = o + 6; o += 12; }
         if (model == DJG_MR) { M2 = o; I2m = o + 21; o += 57; }
+        if (model == DJG_I57) { M5 = o; I5m = o + 21; M7 = o + 57; I7m = o + 78; o += 114; }
         if (kind == DJG_H8) { khg = o; gamma = o + 1; o += 33; }
         count = o;
     }
@@ -217,13 +220,17 @@ struct Material {
     static Real norm(const V3<Real>& v) { return std::sqrt(v.x * v.x + v.y * v.y + v.z * v.z); }
 
     void validate() const {  // material.hpp:187-207
-        if (model < DJG_NH || model > DJG_MR) throw ConfigError("unknown material model");
+        if (model < DJG_NH || model > DJG_I57) throw ConfigError("unknown material model");
         if (!(kappa > Real(0))) throw ConfigError("bulk modulus must be positive");
         if (!(rho > Real(0))) throw ConfigError("density must be positive");
         if (model == DJG_MR) {
             if (c10 < Real(0) || c01 < Real(0)) throw ConfigError("Mooney-Rivlin coefficients must be >= 0");
             if (!(c10 + c01 > Real(0))) throw ConfigError("Mooney-Rivlin coefficients must not both vanish");
             return;
+        }
+        if (model == DJG_I57) {  // test_forces.cpp:248-260: both fibre families
+            if (eta_a < Real(0) || eta_b < Real(0)) throw ConfigError("fibre stiffnesses eta5 / eta7 must be >= 0");
+            if (!(norm(fa) > Real(0)) || !(norm(fb) > Real(0))) throw ConfigError("fibre directions a and b must be nonzero");
         }
         if (model == DJG_OT) {
             if (eta_b < Real(0)) throw ConfigError("fibre stiffness eta_b must be >= 0");
@@ -239,6 +246,9 @@ struct Material {
     bool needs_i4() const { return model == DJG_TI || model == DJG_OT; }
     bool needs_i6() const { return model == DJG_OT; }
     bool needs_i2() const { return model == DJG_MR; }
+    bool needs_i57() const { return model == DJG_I57; }
+    bool needs_fibre_a() const { return needs_i4() || needs_i57(); }  // InvariantSet::any_fibre_a
+    bool needs_fibre_b() const { return needs_i6() || needs_i57(); }
 
     Real shear_modulus() const { return model == DJG_MR ? 2 * (c10 + c01) : mu; }
 
@@ -471,6 +481,12 @@ inline bool element_record(const V3<Real>* x, const Shape<Real>& D, const Materi
         const Sym<Real> B = outer(fb_unit);
         em::fibre_tensors(Ji, v0, B.v, out + L.m6, out + L.I6m);
     }
+    if (mat.needs_i57()) {  // precompute.hpp:237-240, 245-248
+        const Sym<Real> A = outer(fa_unit), B = outer(fb_unit);
+        const Real a[3] = {fa_unit.x, fa_unit.y, fa_unit.z}, b[3] = {fb_unit.x, fb_unit.y, fb_unit.z};
+        em::fibre_second_tensors(Ji, v0, a, A.v, out + L.M5, out + L.I5m);
+        em::fibre_second_tensors(Ji, v0, b, B.v, out + L.M7, out + L.I7m);
+    }
     if (D.kind == DJG_H8) {
         Real gamma[4][8];
         em::hourglass_vectors(xa, Ji, gamma);
@@ -579,8 +595,8 @@ inline Problem<Real> build_problem(const djg_scenario_spec& s, int threads) {
 
     // DjModel::build -> build_constants (djtled_force.hpp:145-157, precompute.hpp:258-272)
     V3<Real> fa{0, 0, 0}, fb{0, 0, 0};
-    if (P.mat.needs_i4()) fa = Material<Real>::unit(P.mat.fa);
-    if (P.mat.needs_i6()) fb = Material<Real>::unit(P.mat.fb);
+    if (P.mat.needs_fibre_a()) fa = Material<Real>::unit(P.mat.fa);
+    if (P.mat.needs_fibre_b()) fb = Material<Real>::unit(P.mat.fb);
     const Real c_hg = Real(s.c_hg);
     P.c_hg = c_hg;
     const Shape<Real> D(s.kind);

@@ -110,8 +110,8 @@ int create_from_mesh(const djg_mesh_desc& m, djg_engine** out) {
         djg::validate_mesh(mesh);
         const djg::Shape<Real> D(m.kind);
         djg::V3<Real> fa{0, 0, 0}, fb{0, 0, 0};
-        if (mat.needs_i4()) fa = djg::Material<Real>::unit(mat.fa);
-        if (mat.needs_i6()) fb = djg::Material<Real>::unit(mat.fb);
+        if (mat.needs_fibre_a()) fa = djg::Material<Real>::unit(mat.fa);
+        if (mat.needs_fibre_b()) fb = djg::Material<Real>::unit(mat.fb);
         consts.assign(size_t(E) * size_t(L.count), Real(0));
         const Real c_hg = Real(m.c_hg);
 #pragma omp parallel for schedule(static)
@@ -177,6 +177,12 @@ void djg_bench_material(int32_t model, djg_material_params* m) {
         m->mu = 0.0;
         m->c10 = 6567.0 / 2;
         m->c01 = 3000.0;
+    }
+    if (model == DJG_I57) {  // test_forces.cpp:251 ratios (eta5 800, eta7 650 over mu 500)
+        m->eta_a = 1.6 * 6567.0;
+        m->eta_b = 1.3 * 6567.0;
+        m->fibre_a[1] = 1.0;
+        m->fibre_b[2] = 1.0;
     }
 }
 

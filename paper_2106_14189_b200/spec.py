@@ -26,7 +26,9 @@ CONFIGS = {
 
 
 def bench_material(model: int | str) -> A.djg_material_params:
-    """bench_material (bench.hpp:12-25)."""
+    """bench_material (bench.hpp:12-25); I57 (the fifth/seventh-invariant
+    energy of test_forces.cpp:248-271, no bench counterpart): eta5 = 1.6 mu,
+    eta7 = 1.3 mu (the test's 800 / 650 over mu = 500), oblique fibres."""
     if isinstance(model, str):
         model = A.MODEL_NAMES[model]
     m = A.djg_material_params()
@@ -41,6 +43,10 @@ def bench_material(model: int | str) -> A.djg_material_params:
     if model == A.DJG_MR:
         m.mu = 0.0
         m.c10, m.c01 = 6567.0 / 2, 3000.0
+    if model == A.DJG_I57:
+        m.eta_a, m.eta_b = 1.6 * 6567.0, 1.3 * 6567.0
+        m.fibre_a[1] = 1.0
+        m.fibre_b[2] = 1.0
     return m
 
 

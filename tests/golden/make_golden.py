@@ -129,7 +129,20 @@ def element_fixtures():
                 if prec == 8:
                     T = np.array([oracle.ref_element_force(8, kind, m, X[i], U[i], engine=1) for i in range(len(X))])
                     out[f"{kind_name}_{model}_tled_f64"] = T
+        # DJG_I57: the reference's I5 / I7 force terms driven by the test
+        # energy of test_forces.cpp:248-271 (no TLED form): the bench-scale
+        # parameters, and the test's own moduli with oblique fibres.
+        for name, m in (("I57", bench_material("I57")), ("I57x", I57_TEST)):
+            for prec in (4, 8):
+                F = np.array([oracle.ref_element_force(prec, kind, m, X[i], U[i]) for i in range(len(X))])
+                out[f"{kind_name}_{name}_f{8 * prec}"] = F
     np.savez_compressed(OUT / "elements.npz", **out)
+
+
+# test_forces.cpp:251: mu 500, kappa 2000, eta5 800, eta7 650 (fibres fixed
+# oblique unit-length-free vectors instead of the test's random draws)
+I57_TEST = material("I57", mu=500.0, kappa=2000.0, rho=1000.0, eta_a=800.0, eta_b=650.0,
+                    fibre_a=(0.3, -0.5, 0.81), fibre_b=(-0.62, 0.1, 0.4))
 
 
 if __name__ == "__main__":

@@ -62,7 +62,7 @@ def test_cfg2_h8_nh_hourglass_2000_steps(precision):
 
 @pytest.mark.parametrize("precision", [4, 8])
 @pytest.mark.parametrize("kind", ["T4", "H8"])
-@pytest.mark.parametrize("model", ["NH", "TI", "OT", "MR"])
+@pytest.mark.parametrize("model", ["NH", "TI", "OT", "MR", "I57"])
 @pytest.mark.parametrize("mode", ["default", "slabs", "nopipe"])
 def test_materials_small(kind, model, precision, mode, monkeypatch):
     flags = 0
@@ -102,6 +102,25 @@ def test_pipeline_partial_tiles(model, precision, flags):
     if flags & A.DJG_FLAG_TLED:
         return  # TLED parity is tests/test_gpu_tled.py
     check_run(spec, 250, flags=flags)
+
+
+@pytest.mark.parametrize("flags", [A.DJG_FLAG_COMPACT, A.DJG_FLAG_DEVICE_PRECOMPUTE, A.DJG_FLAG_TLED])
+def test_i57_full_record_only(flags):
+    """DJG_I57 (the I5 / I7 test energy) runs on the host-built full record;
+    the compact, device-precompute and TLED forms are refused loudly."""
+    sc = Scenario(box_spec(kind="T4", model="I57", divisions=2, precision=4))
+    with GpuDjEngine(sc) as eng:
+        info = eng.info()
+        assert info["compact"] == 0 and info["pipelined"] == 0 and info["nconst"] == 137
+    with pytest.raises(Exception, match="I57"):
+        GpuDjEngine(sc, flags=flags)
+
+
+@pytest.mark.parametrize("precision", [4, 8])
+@pytest.mark.parametrize("kind", ["T4", "H8"])
+def test_i57_longer_run(kind, precision):
+    """The fifth/seventh-invariant terms over a 600-step compression, bitwise."""
+    check_run(box_spec(kind=kind, model="I57", divisions=(4, 3, 5), precision=precision, ramp_steps=600), 600)
 
 
 def test_pipeline_selection():

@@ -19,7 +19,7 @@ def same(a, b):
 
 
 @pytest.mark.parametrize("kind", ["T4", "H8"])
-@pytest.mark.parametrize("model", ["NH", "TI", "OT", "MR"])
+@pytest.mark.parametrize("model", ["NH", "TI", "OT", "MR", "I57"])
 @pytest.mark.parametrize("prec", [4, 8])
 def test_builder_matches_oracle(kind, model, prec):
     spec = box_spec(kind=kind, model=model, divisions=(4, 3, 5), precision=prec, ramp_steps=321)

@@ -39,6 +39,23 @@ def test_parts_bitwise_equal_single_gpu(nparts, kind, model, prec, overlap):
     assert np.array_equal(u, u1) and np.array_equal(up, up1)
 
 
+@pytest.mark.parametrize("prec", [4, 8])
+@pytest.mark.parametrize("cfg,nparts,steps", [("cfg1", 2, 400), ("cfg1", 4, 400), ("cfg1", 8, 400),
+                                              ("cfg3", 8, 40)])
+def test_parts_cfg_bitwise(cfg, nparts, steps, prec):
+    """1 GPU == k parts bit for bit on cfg1 / cfg3, f32 and f64
+    (overlapped step, peer-memory transport for k = 8)."""
+    from paper_2106_14189_b200 import config_spec
+    spec = config_spec(cfg, precision=prec)
+    u1, up1, r1 = single(spec, steps)
+    em = EmulatedParts(Scenario(spec), nparts, transport="p2p" if nparts == 8 else "copy")
+    reps = em.step(steps, overlap=True) if nparts != 8 else em.step(steps)
+    u, up, step = em.global_state()
+    em.close()
+    assert all(r.status == 0 for r in reps) and step == steps == r1.step
+    assert np.array_equal(u, u1) and np.array_equal(up, up1)
+
+
 @pytest.mark.parametrize("nparts", [2, 3, 8])
 @pytest.mark.parametrize("kind,model,prec", [("T4", "NH", 4), ("H8", "TI", 8)])
 def test_parts_peer_memory_transport_bitwise(nparts, kind, model, prec):

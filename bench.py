@@ -355,9 +355,32 @@ def our_arm(args):
         line["tled"] = {"ms_per_step": tled_ms, "value": E / (tled_ms * 1e-3), "unit": UNIT,
                         "dj_over_tled_time": ms_step / tled_ms, "status": trep.status,
                         "note": "paper Table 5 ratio (CPU: 0.70-0.88); same problem, DJG_FLAG_TLED"}
+    sc.close()
+    # SURVEY §8(d)'s secondary precision: the same problem in f64 (graph
+    # replay, events on the engine stream; per-kernel split from
+    # profile_steps).
+    if args.f64_steps > 0 and args.precision == 4:
+        spec8 = box_spec(kind=args.kind, model=args.model, divisions=args.divisions, precision=8, target=0.01,
+                         ramp_steps=W + 2 * args.f64_steps + 8)
+        sc8 = Scenario(spec8)
+        with GpuDjEngine(sc8, device=device) as e8:
+            e8.step(W)
+            me, mn, _ = e8.profile_steps(args.f64_steps)
+            s8 = torch.cuda.ExternalStream(e8.stream)
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            a0.record(s8)
+            e8.step_async(args.f64_steps)
+            a1.record(s8)
+            a1.synchronize()
+            r8 = e8.sync()
+        sc8.close()
+        ms8 = a0.elapsed_time(a1) / args.f64_steps
+        line["f64"] = {"ms_per_step": ms8, "value": E / (ms8 * 1e-3), "unit": UNIT, "status": r8.status,
+                       "k_element_ms": me / args.f64_steps, "k_node_ms": mn / args.f64_steps,
+                       "steps": args.f64_steps, "note": "same mesh and load in double precision (secondary metric)"}
     if not args.no_cpu_baseline:
         line["cpu_baseline"] = _cpu_baseline_line(args)
-    sc.close()
     print(json.dumps(line), flush=True)
 
 
@@ -478,6 +501,7 @@ def main():
     ap.add_argument("--precision", type=int, default=4, choices=[4, 8])
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--tled-steps", type=int, default=100)
+    ap.add_argument("--f64-steps", type=int, default=50, help="also time the f64 problem (0: skip)")
     ap.add_argument("--cpu-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],

@@ -26,7 +26,8 @@ def _run(cmd, env=None):
     return json.loads(lines[0])
 
 
-SMALL = ["--divisions", "24", "--steps", "40", "--warmup", "3", "--e2e-steps", "3", "--tled-steps", "10"]
+SMALL = ["--divisions", "24", "--steps", "40", "--warmup", "3", "--e2e-steps", "3", "--tled-steps", "10",
+         "--f64-steps", "10"]
 
 
 def test_bench_single_gpu_line():
@@ -39,6 +40,7 @@ def test_bench_single_gpu_line():
     assert line["gpu_launches"] == 2 * 40 and line["clocks"]["samples"] > 0
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["value"] > 0
     assert line["tled"]["status"] == 0
+    assert line["f64"]["status"] == 0 and line["f64"]["ms_per_step"] > 0
 
 
 def _port():

@@ -234,7 +234,7 @@ def our_arm(args):
         return multi_arm(args, rank, world, device)
 
     K, W = args.steps, max(args.warmup, 3)
-    total = W + 2 * K + args.e2e_steps + 8
+    total = W + 3 * K + args.e2e_steps + 8
     spec = box_spec(kind=args.kind, model=args.model, divisions=args.divisions, precision=args.precision,
                     target=0.01, ramp_steps=total)
     t0 = time.perf_counter()
@@ -302,6 +302,21 @@ def our_arm(args):
         cur, prev, spare = spare, cur, prev
     te1 = time.perf_counter()
     e2e_ms = (te1 - te0) / args.e2e_steps * 1e3
+    # The run_simulation path (solver.hpp:205-258) through the C-ABI: the
+    # host SimState goes up once (djg_set_state from pinned host), K steps
+    # run on the device (graph replay, failure checks on the device), the
+    # state comes back (djg_get_state); wall clock around all of it.
+    ru = C.c_int64(0)
+    torch.cuda.synchronize()
+    tr0 = time.perf_counter()
+    if lib.djg_set_state(h, C.c_void_p(u_h.data_ptr()), C.c_void_p(up_h.data_ptr()), step_c.value):
+        raise SystemExit("djg_set_state failed")
+    if lib.djg_step(h, K, C.byref(rep_c)) or rep_c.steps_done != K:
+        raise SystemExit(f"run path failed: status {rep_c.status}")
+    if lib.djg_get_state(h, C.c_void_p(u_h.data_ptr()), C.c_void_p(up_h.data_ptr()), C.byref(ru)):
+        raise SystemExit("djg_get_state failed")
+    tr1 = time.perf_counter()
+    run_ms = (tr1 - tr0) / K * 1e3
     rbytes = args.precision
 
     hbm, peak_kind = peaks()
@@ -317,6 +332,10 @@ def our_arm(args):
                 "mode": "per step: djg_advance_host -- advance_step with a host SimState: H2D u_curr and "
                         "u_prev from pinned host (the u_prev copy overlaps the element kernel), one step, D2H "
                         "the new u_curr; the next u_prev is the host's previous u_curr; wall clock"},
+        "e2e_run": {"value": E / (run_ms * 1e-3), "unit": UNIT, "steps": K, "ms_per_step": run_ms,
+                    "h2d_bytes": 2 * 3 * N * rbytes, "d2h_bytes": 2 * 3 * N * rbytes,
+                    "mode": "run_simulation path: djg_set_state (host SimState up once), djg_step(K) on the "
+                            "device, djg_get_state (state back); wall clock over the whole call sequence"},
         "roofline": {"bound": "hbm", "kernel": "k_element", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
                      "moved_frac": (traffic / (k1_ms * 1e-3) / 1e9 / hbm) if traffic else None,

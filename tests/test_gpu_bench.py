@@ -41,6 +41,7 @@ def test_bench_single_gpu_line():
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["value"] > 0
     assert line["tled"]["status"] == 0
     assert line["f64"]["status"] == 0 and line["f64"]["ms_per_step"] > 0
+    assert line["e2e_run"]["value"] > 0 and line["e2e_run"]["steps"] == 40
 
 
 def _port():

@@ -1162,16 +1162,20 @@ __global__ void k_precompute_tled(const ElemArgs<Real> A, typename RT<Real>::Pla
 #ifndef DJG_GATHER_BATCH
 #define DJG_GATHER_BATCH 12
 #endif
+#ifndef DJG_GATHER_BATCH64
+#define DJG_GATHER_BATCH64 6
+#endif
 template <class Real>
 __device__ __forceinline__ void gather_row(const typename RT<Real>::Node* __restrict__ p, int len, Real& sx, Real& sy,
                                            Real& sz) {
     using T = RT<Real>;
     sx = Real(0); sy = Real(0); sz = Real(0);
     int k = 0;
-    // f32: batches of rows loaded together (more loads in flight per thread
-    // than the compiler's own pipelining), then folded in order. 12 measured
-    // best on cfg3 / cfg5 (cfg5 k_node 561 -> 553 us; 16 and 24 no better).
-    constexpr int B = sizeof(Real) == 4 ? DJG_GATHER_BATCH : 0;
+    // Batches of rows loaded together (more loads in flight per thread than
+    // the compiler's own pipelining), then folded in order: 12 f32 rows
+    // (cfg5 k_node 561 -> 553 us; 16 and 24 no better), 6 f64 rows (cfg5
+    // 1071 -> 1057 us; 12 no better).
+    constexpr int B = sizeof(Real) == 4 ? DJG_GATHER_BATCH : DJG_GATHER_BATCH64;
     if constexpr (B > 0) {
         for (; k + B <= len; k += B) {
             typename T::Node v[B > 0 ? B : 1];

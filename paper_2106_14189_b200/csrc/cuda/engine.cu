@@ -436,6 +436,8 @@ public:
 
         // Kernel arguments.
         ea_.E = E_;
+        ea_.N = N_;
+        ea_.cap = capacity_;
         ea_.conn = conn_.as<int4>();
         ea_.rank = rank_.p;
         ea_.slice_base = slicebase_.as<int>();
@@ -455,6 +457,7 @@ public:
         ea_.mat.dI2 = Real(d.material.c01);
         ea_.X = X_.as<Node>();
         na_.N = N_;
+        na_.cap = capacity_;
         na_.row_len = rowlen_.as<int>();
         na_.slice_base = slicebase_.as<int>();
         na_.ef = ef_.as<Node>();

@@ -129,9 +129,29 @@ struct MatParams {
     Real chk;         // c_hg * kappa (k_hg = chk * cbrt(V0), precompute.hpp:252)
 };
 
+// DJG_CHECKS=1 (the _build_checked library, tests/test_gpu_checked.py):
+// device-side bounds checks on every gathered node id and every slot
+// position; a violation traps the kernel (a CUDA error on the next call).
+#ifndef DJG_CHECKS
+#define DJG_CHECKS 0
+#endif
+#if DJG_CHECKS
+#define DJG_ASSERT(c) \
+    do {              \
+        if (!(c)) {   \
+            printf("djg check failed: %s (%s:%d)\n", #c, __FILE__, __LINE__); \
+            __trap(); \
+        }             \
+    } while (0)
+#else
+#define DJG_ASSERT(c) ((void)0)
+#endif
+
 template <class Real>
 struct ElemArgs {
     long long E;
+    long long N;                         // nodes (DJG_CHECKS bounds)
+    long long cap;                       // force-slot entries (DJG_CHECKS bounds)
     const int4* conn;                    // NPE/4 planes of int4[E]
     const void* rank;                    // per element: npe ranks (uint8 or uint16) of the element
                                          // in its nodes' CSR rows, packed in one 4/8/16-byte word
@@ -152,6 +172,7 @@ struct ElemArgs {
 template <class Real>
 struct NodeArgs {
     long long N;
+    long long cap;                       // force-slot entries (DJG_CHECKS bounds)
     const int* row_len;                  // CSR row length per node
     const int* slice_base;               // first slot position of each 32-node slice
     const typename RT<Real>::Node* ef;   // force slots
@@ -231,6 +252,7 @@ __global__ void k_cbrt(const Real* __restrict__ in, Real* __restrict__ out, long
 // bytes but cost more in scattered L2 write transactions than they save.)
 template <class Real>
 __device__ __forceinline__ void store_row(const ElemArgs<Real>& A, int pos, Real x, Real y, Real z) {
+    DJG_ASSERT(pos >= 0 && pos < A.cap);
     RT<Real>::store_node(A.ef + pos, x, y, z);
 }
 
@@ -396,6 +418,8 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
         const int4 q = src.conn(p);
         nid[4 * p + 0] = q.x; nid[4 * p + 1] = q.y; nid[4 * p + 2] = q.z; nid[4 * p + 3] = q.w;
     }
+#pragma unroll
+    for (int a = 0; a < NPE; ++a) DJG_ASSERT(nid[a] >= 0 && nid[a] < A.N);
     // Gathered displacements of the element's nodes (issued first: their
     // latency overlaps the record loads and the compact rebuild).
     Real ux[NPE], uy[NPE], uz[NPE];
@@ -747,6 +771,8 @@ __device__ __forceinline__ void element_body_tled(const ElemArgs<Real>& A, const
         const int4 q = src.conn(p);
         nid[4 * p + 0] = q.x; nid[4 * p + 1] = q.y; nid[4 * p + 2] = q.z; nid[4 * p + 3] = q.w;
     }
+#pragma unroll
+    for (int a = 0; a < NPE; ++a) DJG_ASSERT(nid[a] >= 0 && nid[a] < A.N);
     Real c[NP * T::kPlane];
 #pragma unroll
     for (int p = 0; p < NP; ++p) {
@@ -1215,6 +1241,7 @@ __device__ __forceinline__ bool node_body(const NodeArgs<Real>& A, const long lo
                                           long long step) {
     using T = RT<Real>;
     Real fx, fy, fz;
+    DJG_ASSERT(p0 >= 0 && len >= 0 && (len == 0 || p0 + 32LL * (len - 1) < A.cap));
     gather_row<Real>(A.ef + p0, len, fx, fy, fz);
     if constexpr (kAssemble) {
         A.f_out[3 * n + 0] = fx;
@@ -1295,6 +1322,7 @@ __global__ void __launch_bounds__(256) k_node(const NodeArgs<Real> A) {
     for (long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x; n < A.N && !skip;
          n += (long long)gridDim.x * blockDim.x) {
         Real fx, fy, fz;
+        DJG_ASSERT(A.row_len[n] == 0 || (long long)A.slice_base[n >> 5] + (n & 31) + 32LL * (A.row_len[n] - 1) < A.cap);
         gather_row<Real>(A.ef + (long long)A.slice_base[n >> 5] + (n & 31), A.row_len[n], fx, fy, fz);
         if constexpr (kAssemble) {
             A.f_out[3 * n + 0] = fx;

@@ -330,8 +330,10 @@ def our_arm(args):
         "e2e": {"value": E / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 2 * 3 * N * rbytes,
                 "d2h_bytes_per_step": 3 * N * rbytes, "ms_per_step": e2e_ms,
                 "mode": "per step: djg_advance_host -- advance_step with a host SimState: H2D u_curr and "
-                        "u_prev from pinned host (the u_prev copy overlaps the element kernel), one step, D2H "
-                        "the new u_curr; the next u_prev is the host's previous u_curr; wall clock"},
+                        "u_prev from pinned host (u_curr in 8 chunks, each element chunk starting once the node "
+                        "prefix it reads has landed; u_prev in 4 chunks gating the node-update chunks), one "
+                        "step, D2H the new u_curr chunk by chunk on the other copy direction; the next u_prev "
+                        "is the host's previous u_curr; wall clock"},
         "e2e_run": {"value": E / (run_ms * 1e-3), "unit": UNIT, "steps": K, "ms_per_step": run_ms,
                     "h2d_bytes": 2 * 3 * N * rbytes, "d2h_bytes": 2 * 3 * N * rbytes,
                     "mode": "run_simulation path: djg_set_state (host SimState up once), djg_step(K) on the "

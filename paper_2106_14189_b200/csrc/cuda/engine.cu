@@ -1000,6 +1000,7 @@ public:
         for (void* p : ipc_open_) cudaIpcCloseMemHandle(p);
         if (evFork_) cudaEventDestroy(evFork_);
         if (evPrev_) cudaEventDestroy(evPrev_);
+        if (down_) cudaStreamDestroy(down_);
         for (auto e : evChunk_) cudaEventDestroy(e);
         if (evJoin_) cudaEventDestroy(evJoin_);
         if (side_) cudaStreamDestroy(side_);
@@ -1060,63 +1061,113 @@ public:
         reset_ctrl(step);
     }
 
-    // advance_step with a host SimState in one call: u_curr goes up on the
-    // engine stream, u_prev on a second stream while the element kernel runs
-    // (it reads only u_curr), then the node update and the new u_curr back.
+    // advance_step with a host SimState in one call. Uploads run on one copy
+    // stream in issue order (u_curr in kUpChunks node chunks, then u_prev in
+    // the node-update chunks); each element chunk starts once the u_curr
+    // prefix it reads has landed, each node-update chunk once its u_prev
+    // chunk has, and each chunk's new u_curr goes back on a third stream
+    // (the other copy direction) behind the next chunk's update.
     int advance_host(const void* u, const void* up, int64_t step, void* u_next, djg_report* rep) override {
         if (!configured_) throw DescError("step data not configured (djg_configure_step)");
         if (!u || !up || !u_next) throw DescError("djg_advance_host needs u_curr, u_prev and u_next");
         if (step < 0) throw DescError("step must be >= 0");
         if (n_slabs_ != 1 || comm_ || peer_) throw DescError("djg_advance_host: single-part, one-slab engines");
-        if (!side_) CK(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
-        if (!evPrev_) CK(cudaEventCreateWithFlags(&evPrev_, cudaEventDisableTiming));
-        if (!flat2_.p) flat2_.alloc(flat_.bytes);
-        reset_ctrl(step);
-        CK(cudaMemcpyAsync(hstart_, ctrl_.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream_));
-        const int ph = int(step % 3);
-        const size_t bytes = size_t(3 * N_) * sizeof(Real);
-        const unsigned gn = unsigned((N_ + 255) / 256);
-        // u_curr first: the copy engine serves the copies in issue order, and
-        // the element kernel can start as soon as u_curr has landed
-        CK(cudaMemcpyAsync(flat_.p, u, bytes, cudaMemcpyHostToDevice, stream_));
-        k_pack_nodes<Real><<<gn, 256, 0, stream_>>>(flat_.as<Real>(), N_, u_[ph].as<Node>());
-        CK(cudaEventRecord(evPrev_, stream_));  // (orders the side stream after reset_ctrl's work)
-        CK(cudaStreamWaitEvent(side_, evPrev_, 0));
-        CK(cudaMemcpyAsync(flat2_.p, up, bytes, cudaMemcpyHostToDevice, side_));
-        k_pack_nodes<Real><<<gn, 256, 0, side_>>>(flat2_.as<Real>(), N_, u_[(ph + 2) % 3].as<Node>());
-        CK(cudaEventRecord(evPrev_, side_));
-        CK(cudaGetLastError());
-        launch_element(stream_, 0, E_);
-        CK(cudaStreamWaitEvent(stream_, evPrev_, 0));
-        // node update in chunks of 32-node slices, each chunk's new u_curr
-        // going back on the side stream while the next chunk updates (the
-        // last chunk closes the step)
         const int64_t S = (N_ + 31) / 32;
-        const int nc = S >= 4 * 256 ? kHostChunks : 1;
+        const bool chunked = S >= 4 * 256;
+        const int nu = chunked ? kUpChunks : 1, ne = chunked ? kUpChunks : 1, nc = chunked ? kHostChunks : 1;
+        if (!side_) CK(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+        if (!down_) CK(cudaStreamCreateWithFlags(&down_, cudaStreamNonBlocking));
+        if (!flat2_.p) flat2_.alloc(flat_.bytes);
         if (!allSlices_.p) {
             std::vector<int32_t> ids(static_cast<size_t>(S));
             for (int64_t i = 0; i < S; ++i) ids[size_t(i)] = int32_t(i);
             allSlices_.alloc(ids.size() * sizeof(int32_t));
             CK(cudaMemcpy(allSlices_.p, ids.data(), allSlices_.bytes, cudaMemcpyHostToDevice));
-            evChunk_.resize(kHostChunks + 1);
+            evChunk_.resize(size_t(kUpChunks + 2 * kHostChunks + 2));
             for (auto& e : evChunk_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            // u_curr chunk each element chunk waits for
+            needChunk_.assign(size_t(kUpChunks), kUpChunks - 1);
+            if (chunked) {
+                // per-tile maxima (tiles never straddle an element chunk)
+                const int64_t ntile = (E_ + kPipeTile - 1) / kPipeTile;
+                DevBuf tm;
+                tm.alloc(sizeof(int) * size_t(ntile));
+                CK(cudaMemset(tm.p, 0xff, tm.bytes));
+                const unsigned g = unsigned((E_ + 255) / 256);
+                if (kind_ == DJG_T4) k_chunk_maxnode<4><<<g, 256>>>(conn_.as<int4>(), E_, kPipeTile, tm.as<int>());
+                else k_chunk_maxnode<8><<<g, 256>>>(conn_.as<int4>(), E_, kPipeTile, tm.as<int>());
+                CK(cudaGetLastError());
+                std::vector<int> t(static_cast<size_t>(ntile));
+                CK(cudaMemcpy(t.data(), tm.p, tm.bytes, cudaMemcpyDeviceToHost));
+                std::vector<int> m(static_cast<size_t>(kUpChunks), -1);
+                for (int j = 0; j < kUpChunks; ++j) {
+                    const int64_t t0 = ((E_ * j / kUpChunks) / kPipeTile);
+                    const int64_t t1 = j + 1 == kUpChunks ? ntile : ((E_ * (j + 1) / kUpChunks) / kPipeTile);
+                    for (int64_t q = t0; q < t1; ++q) m[size_t(j)] = std::max(m[size_t(j)], t[size_t(q)]);
+                }
+                for (int j = 0; j < kUpChunks; ++j) {
+                    int c = 0;
+                    while (c < kUpChunks - 1 && int64_t(m[size_t(j)]) >= N_ * (c + 1) / kUpChunks) ++c;
+                    needChunk_[size_t(j)] = c;
+                }
+            }
+        }
+        cudaEvent_t* evU = evChunk_.data();                    // u_curr chunk landed
+        cudaEvent_t* evP = evU + kUpChunks;                    // u_prev chunk landed
+        cudaEvent_t* evN = evP + kHostChunks;                  // node chunk updated
+        cudaEvent_t evStart = evN[kHostChunks], evDone = evN[kHostChunks + 1];
+        reset_ctrl(step);
+        CK(cudaMemcpyAsync(hstart_, ctrl_.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream_));
+        CK(cudaEventRecord(evStart, stream_));
+        CK(cudaStreamWaitEvent(side_, evStart, 0));
+        const int ph = int(step % 3);
+        Node* ucur = u_[ph].as<Node>();
+        Node* uprv = u_[(ph + 2) % 3].as<Node>();
+        auto upload = [&](const void* host, Real* stage, Node* dst, int64_t n0, int64_t n1, cudaEvent_t ev) {
+            CK(cudaMemcpyAsync(stage + 3 * n0, static_cast<const Real*>(host) + 3 * n0,
+                               size_t(3 * (n1 - n0)) * sizeof(Real), cudaMemcpyHostToDevice, side_));
+            k_pack_nodes<Real><<<unsigned(std::max<int64_t>(1, (n1 - n0 + 255) / 256)), 256, 0, side_>>>(
+                stage + 3 * n0, n1 - n0, dst + n0);
+            CK(cudaEventRecord(ev, side_));
+        };
+        for (int c = 0; c < nu; ++c) upload(u, flat_.as<Real>(), ucur, N_ * c / nu, N_ * (c + 1) / nu, evU[c]);
+        auto node_range = [&](int c, int64_t& n0, int64_t& n1) {
+            n0 = 32 * (S * c / nc);
+            n1 = std::min<int64_t>(N_, 32 * (S * (c + 1) / nc));
+        };
+        for (int c = 0; c < nc; ++c) {
+            int64_t n0, n1;
+            node_range(c, n0, n1);
+            upload(up, flat2_.as<Real>(), uprv, n0, n1, evP[c]);
+        }
+        CK(cudaGetLastError());
+        // element chunk boundaries on whole tiles (the pipeline's bulk copies
+        // of rank words and tail planes need 16-byte aligned starts)
+        auto ebound = [&](int j) { return j == ne ? E_ : (E_ * j / ne) / kPipeTile * kPipeTile; };
+        for (int j = 0; j < ne; ++j) {
+            CK(cudaStreamWaitEvent(stream_, evU[chunked ? needChunk_[size_t(j)] : 0], 0));
+            launch_element(stream_, ebound(j), ebound(j + 1));
         }
         const Node* unew = u_[(ph + 1) % 3].as<Node>();
         for (int c = 0; c < nc; ++c) {
             const int64_t s0 = S * c / nc, s1 = S * (c + 1) / nc;
             const int ns = int(s1 - s0);
+            int64_t n0, n1;
+            node_range(c, n0, n1);
+            CK(cudaStreamWaitEvent(stream_, evP[c], 0));
             k_node_slices<Real, false><<<unsigned(std::max(1, (ns * 32 + 255) / 256)), 256, 0, stream_>>>(
                 na_, allSlices_.as<int>() + s0, ns, 0, c == nc - 1 ? 1 : 0);
-            const int64_t n0 = 32 * s0, n1 = std::min<int64_t>(N_, 32 * s1);
-            k_unpack_nodes<Real><<<unsigned((n1 - n0 + 255) / 256), 256, 0, stream_>>>(unew + n0, n1 - n0,
-                                                                                       flat_.as<Real>() + 3 * n0);
-            CK(cudaEventRecord(evChunk_[size_t(c)], stream_));
-            CK(cudaStreamWaitEvent(side_, evChunk_[size_t(c)], 0));
+            // the unpacked result reuses the u_curr staging buffer (its upload
+            // has been consumed by the pack kernels the element chunks waited on)
+            k_unpack_nodes<Real><<<unsigned(std::max<int64_t>(1, (n1 - n0 + 255) / 256)), 256, 0, stream_>>>(
+                unew + n0, n1 - n0, flat_.as<Real>() + 3 * n0);
+            CK(cudaEventRecord(evN[c], stream_));
+            CK(cudaStreamWaitEvent(down_, evN[c], 0));
             CK(cudaMemcpyAsync(static_cast<Real*>(u_next) + 3 * n0, flat_.as<Real>() + 3 * n0,
-                               size_t(3 * (n1 - n0)) * sizeof(Real), cudaMemcpyDeviceToHost, side_));
+                               size_t(3 * (n1 - n0)) * sizeof(Real), cudaMemcpyDeviceToHost, down_));
         }
-        CK(cudaEventRecord(evChunk_[size_t(kHostChunks)], side_));
-        CK(cudaStreamWaitEvent(stream_, evChunk_[size_t(kHostChunks)], 0));
+        CK(cudaEventRecord(evDone, down_));
+        CK(cudaStreamWaitEvent(stream_, evDone, 0));
         CK(cudaGetLastError());
         const int status = sync(rep);
         if (status != DJG_OK) {  // the state did not advance: hand back u_curr
@@ -1490,6 +1541,9 @@ private:
     DevBuf flat2_, allSlices_;
     std::vector<cudaEvent_t> evChunk_;
     static constexpr int kHostChunks = 4;
+    static constexpr int kUpChunks = 8;  // djg_advance_host: u_curr upload / element chunks
+    cudaStream_t down_ = nullptr;        // djg_advance_host: result read-back
+    std::vector<int> needChunk_;
     PeerArgs<Real> pa_{};
     DevBuf mailbox_, destOff_, dest_, peerU_, peerMail_;
     std::vector<void*> ipc_open_;

@@ -1805,6 +1805,32 @@ __global__ void k_lump_mass(const int* __restrict__ pairs, const int* __restrict
     mass[n] = acc;
 }
 
+// djg_advance_host: the largest node id each element chunk reads (so a chunk
+// can start once that prefix of u_curr has been uploaded).
+template <int NPE>
+__global__ void k_chunk_maxnode(const int4* __restrict__ conn, long long E, long long chunk, int* __restrict__ out) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    int m = -1;
+    if (e < E) {
+#pragma unroll
+        for (int p = 0; p < NPE / 4; ++p) {
+            const int4 q = conn[(long long)p * E + e];
+            m = max(m, max(max(q.x, q.y), max(q.z, q.w)));
+        }
+    }
+    // a warp may straddle two chunks: reduce per chunk id
+    const long long c = e < E ? e / chunk : -1;
+    const long long c0 = __shfl_sync(0xffffffffu, c, 0);
+    const bool uniform = __all_sync(0xffffffffu, c == c0);
+    if (uniform) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if ((threadIdx.x & 31) == 0 && c0 >= 0) atomicMax(out + c0, m);
+    } else if (c >= 0) {
+        atomicMax(out + c, m);
+    }
+}
+
 // Packs flat Real[3N] into padded nodes and back.
 template <class Real>
 __global__ void k_pack_nodes(const Real* __restrict__ flat, long long N, typename RT<Real>::Node* __restrict__ out) {

@@ -46,6 +46,9 @@ namespace {
 
 constexpr int kPipeStages = DJG_PIPE_STAGES;
 
+#ifndef DJG_HOST_CHUNKS
+#define DJG_HOST_CHUNKS 4  // djg_advance_host: u_prev upload / node-update / read-back chunks
+#endif
 constexpr int kPipeMaxStageBytes = DJG_PIPE_MAX_STAGE_KB * 1024;
 
 thread_local std::string g_create_error;
@@ -1540,7 +1543,7 @@ private:
     cudaEvent_t evPrev_ = nullptr;     // djg_advance_host: u_prev uploaded
     DevBuf flat2_, allSlices_;
     std::vector<cudaEvent_t> evChunk_;
-    static constexpr int kHostChunks = 4;
+    static constexpr int kHostChunks = DJG_HOST_CHUNKS;
     static constexpr int kUpChunks = 8;  // djg_advance_host: u_curr upload / element chunks
     cudaStream_t down_ = nullptr;        // djg_advance_host: result read-back
     std::vector<int> needChunk_;

@@ -591,6 +591,37 @@ def test_advance_host_chunked_readback():
     assert np.array_equal(u, u_ref) and np.array_equal(up, up_ref) and np.abs(u).max() > 0
 
 
+@pytest.mark.parametrize("kind,d", [("T4", 33), ("H8", 40)])
+def test_advance_host_chunked_permuted_nodes(kind, d):
+    """Chunked host-state step on a mesh whose node ids are randomly permuted:
+    every element chunk reads nodes from the whole id range (each waits for
+    the full u_curr upload); same bits as the device loop."""
+    img = Scenario(box_spec(kind=kind, divisions=d, precision=4)).image()
+    nodes, conn = img["nodes"].reshape(-1, 3).astype(np.float64), img["conn"].reshape(-1, 4 if kind == "T4" else 8)
+    N = nodes.shape[0]
+    perm = np.random.default_rng(11).permutation(N)
+    nodes_p = np.empty_like(nodes)
+    nodes_p[perm] = nodes
+    conn_p = perm[conn].astype(np.int32)
+    bottom = np.flatnonzero(nodes_p[:, 2] == 0.0)
+    top = np.flatnonzero(nodes_p[:, 2] == nodes_p[:, 2].max())
+    spec = mesh_spec(nodes_p, conn_p, kind=kind, precision=4, fixed=[(n, a) for n in bottom for a in range(3)],
+                     prescribed=[(n, 2, 0.01, 1e-3) for n in top])
+    sc = Scenario(spec)
+    assert (sc.num_nodes + 31) // 32 >= 1024
+    with GpuDjEngine(sc) as ref:
+        ref.step(20)
+        u_ref, up_ref, _ = ref.get_state()
+    with GpuDjEngine(sc) as eng:
+        n3 = 3 * sc.num_nodes
+        u, up = np.zeros(n3, np.float32), np.zeros(n3, np.float32)
+        for st in range(20):
+            un, rep = eng.advance_host(u, up, st)
+            assert rep.status == 0
+            u, up = un, u
+    assert np.array_equal(u, u_ref) and np.array_equal(up, up_ref) and np.abs(u).max() > 0
+
+
 def test_descriptor_limits_fail_loudly():
     """32-bit slot indexing: more than INT32_MAX element-nodes is refused with
     a config error before any device work; so is an empty mesh."""

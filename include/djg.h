@@ -172,10 +172,12 @@ int djg_get_state(djg_engine* eng, void* u_curr, void* u_prev, int64_t* step);
  * DJG_E_DIVERGENCE (report->fail_step = state.step + 1). */
 int djg_step(djg_engine* eng, int64_t nsteps, djg_report* report);
 /* advance_step (solver.hpp:98-153) with a host SimState, in one call: uploads
- * u_curr and u_prev (3N Reals each; the u_prev copy overlaps the element
- * kernel, which reads only u_curr), runs one step from `step`, writes the new
- * u_curr to u_next (or u_curr unchanged when the step failed) and fills the
- * report. For loops whose state lives on the host. */
+ * u_curr and u_prev (3N Reals each) in chunks -- each element chunk starts as
+ * soon as the u_curr nodes it reads have landed, each node-update chunk when
+ * its u_prev chunk has -- runs one step from `step`, writes the new u_curr to
+ * u_next chunk by chunk (or u_curr unchanged when the step failed) and fills
+ * the report. For loops whose state lives on the host; pinned host buffers
+ * let the copies overlap. */
 int djg_advance_host(djg_engine* eng, const void* u_curr, const void* u_prev, int64_t step, void* u_next,
                      djg_report* report);
 

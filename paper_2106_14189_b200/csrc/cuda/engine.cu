@@ -478,14 +478,19 @@ public:
                       static_cast<const Real*>(d.dof_t_total), Real(d.c2), Real(d.c3), Real(d.dt));
         }
         {
-            // k_node grid: on meshes of up to a few waves, a grid-stride launch
+            // k_node grid: on meshes of up to 16 waves, a grid-stride launch
             // sized to the resident blocks (one barrier + completion count per
-            // block, no tail wave: cfg4 53 -> 41 us); on large meshes one thread
-            // per node streams better (cfg5).
+            // block, no tail wave: cfg4 54 -> 40 us), twice that for long rows
+            // (T4, ~24 slots per node) beyond 4 waves (1 % better there, 7 %
+            // worse for H8's 8-slot rows); on large meshes one thread per node
+            // streams better (cfg5).
             int nb = 0;
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_node<Real, false>, 256, 0));
             const int64_t resident = int64_t(std::max(nb, 1)) * sms_, blocks = (N_ + 255) / 256;
-            node_grid_ = blocks > 16 * resident ? 0 : blocks > 4 * resident ? 2 * resident : resident;
+            const bool long_rows = int64_t(npe_) * E_ >= 16 * N_;
+            node_grid_ = blocks > 16 * resident                ? 0
+                         : (blocks > 4 * resident && long_rows) ? 2 * resident
+                                                                : resident;
             if (const char* v = std::getenv("DJG_NODE_GRID")) node_grid_ = std::atoll(v);
         }
         pipe_ = !(flags_ & DJG_FLAG_NO_PIPE) && n_slabs_ == 1;

@@ -151,3 +151,40 @@ def test_distributed_engine_single_rank_nccl(engine_comm):
         assert r1.status == r2.status and r1.fail_step == r2.fail_step and r1.first_inverted == r2.first_inverted
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("prec", [4, 8])
+def test_halo_pack_unpack_against_host_indexing(prec):
+    """SURVEY §8(e) halo-only unit test: djg_halo_pack gathers exactly the
+    current displacements of the part's send list (host re-assembly from the
+    global state through node_l2g), and djg_halo_unpack writes exactly the
+    receive list."""
+    import torch
+    from paper_2106_14189_b200.parallel import Partition, PartEngine
+    spec = box_spec(kind="T4", model="NH", divisions=6, precision=prec)
+    sc = Scenario(spec)
+    rng = np.random.default_rng(5)
+    dt = np.float32 if prec == 4 else np.float64
+    tdt = torch.float32 if prec == 4 else torch.float64
+    ug = rng.uniform(-1, 1, 3 * sc.num_nodes).astype(dt)
+    upg = rng.uniform(-1, 1, 3 * sc.num_nodes).astype(dt)
+    for me in range(3):
+        part = Partition(sc, 3, me)
+        with PartEngine(part) as pe:
+            for step in (0, 1, 2):  # every buffer phase
+                pe.set_global_state(ug, upg, step)
+                ns, nr = part.send_nodes.size, part.recv_nodes.size
+                assert ns > 0 and nr > 0
+                buf = torch.zeros((ns, 4), dtype=tdt, device="cuda")
+                pe.halo_pack(buf.data_ptr())
+                torch.cuda.synchronize()
+                want = ug.reshape(-1, 3)[part.node_l2g[part.send_nodes]]
+                assert np.array_equal(buf.cpu().numpy()[:, :3], want)
+                vals = torch.from_numpy(rng.uniform(-1, 1, (nr, 4)).astype(dt)).cuda()
+                pe.halo_unpack(vals.data_ptr())
+                torch.cuda.synchronize()
+                u, up, st = pe.get_state()
+                u = u.reshape(-1, 3)
+                assert np.array_equal(u[part.recv_nodes], vals.cpu().numpy()[:, :3]) and st == step
+                others = np.setdiff1d(np.arange(part.num_nodes), part.recv_nodes)
+                assert np.array_equal(u[others], ug.reshape(-1, 3)[part.node_l2g[others]])

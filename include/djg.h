@@ -93,7 +93,8 @@ typedef struct djg_desc {
 #define DJG_FLAG_DEVICE_PRECOMPUTE 16u /* build the per-element record on the GPU from
                                           nodes + conn (desc.consts may be NULL) */
 #define DJG_FLAG_FULL_RECORD 32u /* keep the full record in HBM (default for
-                                    Mooney-Rivlin; otherwise the compact record) */
+                                    Mooney-Rivlin in f64 and on H8; otherwise
+                                    the compact record) */
 #define DJG_FLAG_TLED 64u        /* conventional TLED element forces (tled_force.hpp), the
                                     paper's comparison path; record built on the device */
 #define DJG_FLAG_NO_PIPE 128u    /* one-shot element kernel instead of the bulk-copy

@@ -10,8 +10,10 @@
 
 #if defined(__CUDACC__)
 #define DJG_HD __host__ __device__ __forceinline__
+#define DJG_UNROLL _Pragma("unroll")
 #else
 #define DJG_HD inline
+#define DJG_UNROLL
 #endif
 
 namespace djg {
@@ -63,7 +65,9 @@ template <class R>
 DJG_HD void congruence(const R q[3][3], const R s[6], R out[6]) {
     const R sf[3][3] = {{s[0], s[3], s[4]}, {s[3], s[1], s[5]}, {s[4], s[5], s[2]}};
     R sq[3][3];
+    DJG_UNROLL
     for (int i = 0; i < 3; ++i)
+        DJG_UNROLL
         for (int j = 0; j < 3; ++j) sq[i][j] = sf[i][0] * q[0][j] + sf[i][1] * q[1][j] + sf[i][2] * q[2][j];
     out[0] = q[0][0] * sq[0][0] + q[1][0] * sq[1][0] + q[2][0] * sq[2][0];
     out[1] = q[0][1] * sq[0][1] + q[1][1] * sq[1][1] + q[2][1] * sq[2][1];
@@ -100,6 +104,7 @@ DJG_HD R trace6(const R g[6]) { return g[0] + g[1] + g[2]; }
 // m1[k] = tr(G_k) and I1m = 2 V0 J0inv^T J0inv (precompute.hpp:52-58, 97-101, 224-225).
 template <class R>
 DJG_HD void first_invariant_tensors(const R ji[3][3], R v0, R m1[6], R i1m[6]) {
+    DJG_UNROLL
     for (int k = 0; k < 6; ++k) {
         R g[6];
         g_matrix(ji, k, g);
@@ -109,6 +114,7 @@ DJG_HD void first_invariant_tensors(const R ji[3][3], R v0, R m1[6], R i1m[6]) {
     R t[6];
     congruence(ji, ident, t);
     const R two_v0 = 2 * v0;
+    DJG_UNROLL
     for (int c = 0; c < 6; ++c) i1m[c] = two_v0 * t[c];
 }
 
@@ -119,19 +125,23 @@ DJG_HD void first_invariant_tensors(const R ji[3][3], R v0, R m1[6], R i1m[6]) {
 // zero). Used by the compact force kernel, where it saves ~80 operations.
 template <class R>
 DJG_HD void first_invariant_tensors_fast(const R ji[3][3], R v0, R m1[6], R i1m[6]) {
+    DJG_UNROLL
     for (int k = 0; k < 6; ++k) {
         R g[6];
         g_matrix(ji, k, g);
         m1[k] = trace6(g);
     }
     const R two_v0 = 2 * v0;
+    DJG_UNROLL
     for (int c = 0; c < 3; ++c) i1m[c] = two_v0 * m1[c];
+    DJG_UNROLL
     for (int c = 3; c < 6; ++c) i1m[c] = v0 * m1[c];
 }
 
 // Fibre family: m[k] = tr(S G_k), Im = 2 V0 J0inv^T S J0inv (precompute.hpp:60-65, 97-101).
 template <class R>
 DJG_HD void fibre_tensors(const R ji[3][3], R v0, const R S[6], R m[6], R im[6]) {
+    DJG_UNROLL
     for (int k = 0; k < 6; ++k) {
         R g[6];
         g_matrix(ji, k, g);
@@ -140,6 +150,7 @@ DJG_HD void fibre_tensors(const R ji[3][3], R v0, const R S[6], R m[6], R im[6])
     R t[6];
     congruence(ji, S, t);
     const R two_v0 = 2 * v0;
+    DJG_UNROLL
     for (int c = 0; c < 6; ++c) im[c] = two_v0 * t[c];
 }
 
@@ -148,9 +159,11 @@ DJG_HD void fibre_tensors(const R ji[3][3], R v0, const R S[6], R m[6], R im[6])
 template <class R>
 DJG_HD void second_invariant_tensors(const R ji[3][3], R v0, const R m1[6], R m2[21], R i2m[36]) {
     int w = 0;
+    DJG_UNROLL
     for (int p = 0; p < 6; ++p) {
         R gp[6];
         g_matrix(ji, p, gp);
+        DJG_UNROLL
         for (int q = p; q < 6; ++q) {
             R gq[6];
             g_matrix(ji, q, gq);
@@ -158,6 +171,7 @@ DJG_HD void second_invariant_tensors(const R ji[3][3], R v0, const R m1[6], R m2
         }
     }
     const R two_v0 = 2 * v0;
+    DJG_UNROLL
     for (int k = 0; k < 6; ++k) {
         R g[6];
         g_matrix(ji, k, g);
@@ -165,6 +179,7 @@ DJG_HD void second_invariant_tensors(const R ji[3][3], R v0, const R m1[6], R m2
         const R ker[6] = {tr - g[0], tr - g[1], tr - g[2], -g[3], -g[4], -g[5]};
         R t[6];
         congruence(ji, ker, t);
+        DJG_UNROLL
         for (int c = 0; c < 6; ++c) i2m[6 * k + c] = two_v0 * t[c];
     }
 }
@@ -175,6 +190,7 @@ DJG_HD void second_invariant_tensors(const R ji[3][3], R v0, const R m1[6], R m2
 template <class R>
 DJG_HD void fibre_second_tensors(const R ji[3][3], R v0, const R s[3], const R S[6], R m[21], R im[36]) {
     R gs[6][3];
+    DJG_UNROLL
     for (int k = 0; k < 6; ++k) {  // mul(G_k.full(), s)
         R g[6];
         g_matrix(ji, k, g);
@@ -183,21 +199,27 @@ DJG_HD void fibre_second_tensors(const R ji[3][3], R v0, const R s[3], const R S
         gs[k][2] = g[4] * s[0] + g[5] * s[1] + g[2] * s[2];
     }
     int w = 0;
+    DJG_UNROLL
     for (int p = 0; p < 6; ++p)
+        DJG_UNROLL
         for (int q = p; q < 6; ++q) m[w++] = gs[p][0] * gs[q][0] + gs[p][1] * gs[q][1] + gs[p][2] * gs[q][2];
     const R sf[3][3] = {{S[0], S[3], S[4]}, {S[3], S[1], S[5]}, {S[4], S[5], S[2]}};
     const R two_v0 = 2 * v0;
+    DJG_UNROLL
     for (int k = 0; k < 6; ++k) {
         R g[6];
         g_matrix(ji, k, g);
         const R gf[3][3] = {{g[0], g[3], g[4]}, {g[3], g[1], g[5]}, {g[4], g[5], g[2]}};
         R sg[3][3];  // mul(S.full(), G_k.full())
+        DJG_UNROLL
         for (int i = 0; i < 3; ++i)
+            DJG_UNROLL
             for (int j = 0; j < 3; ++j) sg[i][j] = sf[i][0] * gf[0][j] + sf[i][1] * gf[1][j] + sf[i][2] * gf[2][j];
         const R ker[6] = {2 * sg[0][0], 2 * sg[1][1], 2 * sg[2][2],
                           sg[0][1] + sg[1][0], sg[0][2] + sg[2][0], sg[1][2] + sg[2][1]};
         R t[6];
         congruence(ji, ker, t);
+        DJG_UNROLL
         for (int c = 0; c < 6; ++c) im[6 * k + c] = two_v0 * t[c];
     }
 }
@@ -206,18 +228,25 @@ DJG_HD void fibre_second_tensors(const R ji[3][3], R v0, const R s[3], const R S
 template <class R>
 DJG_HD void hourglass_vectors(const R x[8][3], const R ji[3][3], R gamma[4][8]) {
     R b[3][8];
+    DJG_UNROLL
     for (int j = 0; j < 3; ++j)
+        DJG_UNROLL
         for (int a = 0; a < 8; ++a)
             b[j][a] = ji[j][0] * shape_d<R>(1, 0, a) + ji[j][1] * shape_d<R>(1, 1, a) + ji[j][2] * shape_d<R>(1, 2, a);
+    DJG_UNROLL
     for (int m = 0; m < 4; ++m) {
         R base[8];
+        DJG_UNROLL
         for (int a = 0; a < 8; ++a) {
             const int xi = corner_sign(a, 0), eta = corner_sign(a, 1), zeta = corner_sign(a, 2);
             base[a] = R(m == 0 ? eta * zeta : (m == 1 ? xi * zeta : (m == 2 ? xi * eta : xi * eta * zeta)));
         }
         R hx[3] = {R(0), R(0), R(0)};
+        DJG_UNROLL
         for (int j = 0; j < 3; ++j)
+            DJG_UNROLL
             for (int a = 0; a < 8; ++a) hx[j] += base[a] * x[a][j];
+        DJG_UNROLL
         for (int a = 0; a < 8; ++a) gamma[m][a] = base[a] - (hx[0] * b[0][a] + hx[1] * b[1][a] + hx[2] * b[2][a]);
     }
 }
@@ -226,8 +255,10 @@ DJG_HD void hourglass_vectors(const R x[8][3], const R ji[3][3], R gamma[4][8]) 
 template <class R>
 DJG_HD bool jacobian0(int kind, const R x[8][3], R J[3][3], R Ji[3][3], R& det) {
     const int n = kind == 0 ? 4 : 8;
+    DJG_UNROLL
     for (int i = 0; i < 3; ++i) {
         R r0 = R(0), r1 = R(0), r2 = R(0);
+        DJG_UNROLL
         for (int a = 0; a < n; ++a) {
             const R d = shape_d<R>(kind, i, a);
             r0 = r0 + d * x[a][0];
@@ -264,6 +295,7 @@ DJG_HD R char_length(int kind, const R x[8][3], R v0) {
     R a_max = 0;
     if (kind == 0) {
         constexpr int f[4][3] = {{1, 2, 3}, {0, 2, 3}, {0, 1, 3}, {0, 1, 2}};
+        DJG_UNROLL
         for (int t = 0; t < 4; ++t) {
             const R a = tri_area(x[f[t][0]], x[f[t][1]], x[f[t][2]]);
             a_max = a_max < a ? a : a_max;  // std::max(a_max, a)
@@ -271,6 +303,7 @@ DJG_HD R char_length(int kind, const R x[8][3], R v0) {
         return 3 * v0 / a_max;
     }
     constexpr int f[6][4] = {{0, 3, 2, 1}, {4, 5, 6, 7}, {0, 1, 5, 4}, {1, 2, 6, 5}, {2, 3, 7, 6}, {3, 0, 4, 7}};
+    DJG_UNROLL
     for (int q = 0; q < 6; ++q) {
         const R a = tri_area(x[f[q][0]], x[f[q][1]], x[f[q][2]]) + tri_area(x[f[q][0]], x[f[q][2]], x[f[q][3]]);
         a_max = a_max < a ? a : a_max;
@@ -284,7 +317,9 @@ DJG_HD R char_length(int kind, const R x[8][3], R v0) {
 template <class R>
 DJG_HD void tled_b0(int kind, const R ji[3][3], R* b0) {
     const int n = kind == 0 ? 4 : 8;
+    DJG_UNROLL
     for (int a = 0; a < n; ++a)
+        DJG_UNROLL
         for (int j = 0; j < 3; ++j)
             b0[3 * a + j] = ji[j][0] * shape_d<R>(kind, 0, a) + ji[j][1] * shape_d<R>(kind, 1, a) +
                             ji[j][2] * shape_d<R>(kind, 2, a);

@@ -201,14 +201,16 @@ public:
         flags_ = d.flags;
         if (const char* v = std::getenv("DJG_SLAB_KB")) slab_bytes_ = int64_t(std::atoll(v)) << 10;
         nconst_ = const_count(kind_, model_);
-        // Default record: compact (fewer bytes win) except for Mooney-Rivlin,
-        // whose 57 second-invariant Reals cost more to rebuild than to read
-        // (compact MR T4 measured 2.1x (f32) / 2.7x (f64) slower than full).
+        // Default record: compact (fewer bytes win) except for Mooney-Rivlin
+        // in f64 and on H8, where rebuilding its 57 second-invariant Reals
+        // costs more than reading them (10.4M tets: f32 T4 compact 590 vs
+        // full 676 us; f64 T4 1588 vs 1343; 2.2M hexes f32 351 vs 238).
         tled_ = (flags_ & DJG_FLAG_TLED) != 0;
         if (model_ == DJG_I57 && (flags_ & (DJG_FLAG_COMPACT | DJG_FLAG_DEVICE_PRECOMPUTE | DJG_FLAG_TLED)))
             throw DescError("the I57 energy runs on the host-built full record only "
                             "(no DJG_FLAG_COMPACT / DJG_FLAG_DEVICE_PRECOMPUTE / DJG_FLAG_TLED)");
-        const bool compact_default = model_ != DJG_MR && model_ != DJG_I57;
+        const bool compact_default =
+            model_ != DJG_I57 && (model_ != DJG_MR || (kind_ == DJG_T4 && sizeof(Real) == 4));
         compact_ = !tled_ && ((flags_ & DJG_FLAG_COMPACT) != 0 ||
                               (!(flags_ & DJG_FLAG_FULL_RECORD) && compact_default));
         // The compact T4 record is empty: the kernel rebuilds J0 from the node

@@ -1024,7 +1024,7 @@ struct PipeShape {
 #define DJG_PIPE_MINB_T4C_M2 4
 #endif
 #ifndef DJG_PIPE_MINB_T4C_M3
-#define DJG_PIPE_MINB_T4C_M3 4
+#define DJG_PIPE_MINB_T4C_M3 3
 #endif
 #ifndef DJG_PIPE_MINB_T4C64_M1
 #define DJG_PIPE_MINB_T4C64_M1 3

@@ -76,9 +76,9 @@ def test_parts_metis_partition_bitwise():
     for kind, model in (("T4", "NH"), ("H8", "OT")):
         spec = box_spec(kind=kind, model=model, divisions=7, precision=4, ramp_steps=150)
         u1, up1, r1 = single(spec, 150)
-        for nparts in (3, 8):
-            em = EmulatedParts(Scenario(spec), nparts, method="metis")
-            reps = em.step(150, overlap=True)
+        for nparts, transport in ((3, "copy"), (8, "copy"), (5, "p2p")):
+            em = EmulatedParts(Scenario(spec), nparts, method="metis", transport=transport)
+            reps = em.step(150, overlap=transport == "copy")
             u, up, step = em.global_state()
             em.close()
             assert all(r.status == 0 for r in reps) and step == 150

@@ -1004,10 +1004,10 @@ struct PipeShape {
 
 // Blocks per SM the register allocation is sized for, per material and
 // precision (DJG_PIPE_MINB_T4C{,64}_M<model>, measured on a 10.4M-tet cube,
-// tools/ab_models.py): f32 NH 6 (64 registers), TI 5, OT 4; f64 NH 4, TI 3,
-// OT 2. Tighter caps spill the heavier bodies; looser ones lose latency
-// hiding. (MR keeps the full record by default.) The full-record forms are
-// left uncapped.
+// tools/ab_models.py): f32 NH 6 (64 registers), TI 5, OT 4, MR 3; f64 NH 4,
+// TI 3, OT 2. Tighter caps spill the heavier bodies; looser ones lose latency
+// hiding. (f64 MR keeps the full record by default.) The full-record forms
+// are left uncapped.
 #ifndef DJG_PIPE_MINB_T4C
 #define DJG_PIPE_MINB_T4C 6
 #endif

@@ -90,8 +90,8 @@ def test_compact_and_device_precompute_bitwise(kind, model, precision, flags):
 def test_pipeline_partial_tiles(model, precision, flags):
     """k_element_pipe on a mesh whose element count is not a multiple of the
     128-element tile (720 tets: 5 full tiles + 80), with record tail planes
-    and rank words whose copies round up to 16 bytes. (Mooney-Rivlin keeps the
-    full record by default; its compact pipeline is forced here.)"""
+    and rank words whose copies round up to 16 bytes. (f64 Mooney-Rivlin keeps
+    the full record by default; its compact pipeline is forced here.)"""
     if model == "MR" and not flags & (A.DJG_FLAG_FULL_RECORD | A.DJG_FLAG_TLED):
         flags |= A.DJG_FLAG_COMPACT
     spec = box_spec(kind="T4", model=model, divisions=(5, 4, 6), precision=precision, ramp_steps=250)

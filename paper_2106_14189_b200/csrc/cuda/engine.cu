@@ -1130,6 +1130,18 @@ public:
         CK(cudaMemcpyAsync(hstart_, ctrl_.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream_));
         CK(cudaEventRecord(evStart, stream_));
         CK(cudaStreamWaitEvent(side_, evStart, 0));
+        // DJG_TRACE_HOST=1: timing events along the three streams, printed
+        // (ms from the start) to stderr after the step -- developer timeline
+        static const bool trace = std::getenv("DJG_TRACE_HOST") != nullptr;
+        std::vector<std::pair<std::string, cudaEvent_t>> tl;
+        auto mark = [&](const std::string& what, cudaStream_t st) {
+            if (!trace) return;
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            CK(cudaEventRecord(e, st));
+            tl.emplace_back(what, e);
+        };
+        mark("start", stream_);
         const int ph = int(step % 3);
         Node* ucur = u_[ph].as<Node>();
         Node* uprv = u_[(ph + 2) % 3].as<Node>();
@@ -1139,6 +1151,7 @@ public:
             k_pack_nodes<Real><<<unsigned(std::max<int64_t>(1, (n1 - n0 + 255) / 256)), 256, 0, side_>>>(
                 stage + 3 * n0, n1 - n0, dst + n0);
             CK(cudaEventRecord(ev, side_));
+            mark(std::string(stage == flat_.as<Real>() ? "up u_curr " : "up u_prev ") + std::to_string(n0), side_);
         };
         for (int c = 0; c < nu; ++c) upload(u, flat_.as<Real>(), ucur, N_ * c / nu, N_ * (c + 1) / nu, evU[c]);
         auto node_range = [&](int c, int64_t& n0, int64_t& n1) {
@@ -1157,6 +1170,7 @@ public:
         for (int j = 0; j < ne; ++j) {
             CK(cudaStreamWaitEvent(stream_, evU[chunked ? needChunk_[size_t(j)] : 0], 0));
             launch_element(stream_, ebound(j), ebound(j + 1));
+            mark("element chunk " + std::to_string(j), stream_);
         }
         const Node* unew = u_[(ph + 1) % 3].as<Node>();
         for (int c = 0; c < nc; ++c) {
@@ -1172,14 +1186,24 @@ public:
             k_unpack_nodes<Real><<<unsigned(std::max<int64_t>(1, (n1 - n0 + 255) / 256)), 256, 0, stream_>>>(
                 unew + n0, n1 - n0, flat_.as<Real>() + 3 * n0);
             CK(cudaEventRecord(evN[c], stream_));
+            mark("node chunk " + std::to_string(c), stream_);
             CK(cudaStreamWaitEvent(down_, evN[c], 0));
             CK(cudaMemcpyAsync(static_cast<Real*>(u_next) + 3 * n0, flat_.as<Real>() + 3 * n0,
                                size_t(3 * (n1 - n0)) * sizeof(Real), cudaMemcpyDeviceToHost, down_));
+            mark("down " + std::to_string(c), down_);
         }
         CK(cudaEventRecord(evDone, down_));
         CK(cudaStreamWaitEvent(stream_, evDone, 0));
         CK(cudaGetLastError());
         const int status = sync(rep);
+        if (trace) {
+            for (auto& [what, e] : tl) {
+                float ms = 0;
+                CK(cudaEventElapsedTime(&ms, tl.front().second, e));
+                std::fprintf(stderr, "[djg host step] %8.3f ms  %s\n", ms, what.c_str());
+            }
+            for (auto& te : tl) cudaEventDestroy(te.second);
+        }
         if (status != DJG_OK) {  // the state did not advance: hand back u_curr
             download_nodes(u_[ph].as<Node>(), u_next);
             CK(cudaStreamSynchronize(stream_));

@@ -1154,9 +1154,20 @@ public:
             mark(std::string(stage == flat_.as<Real>() ? "up u_curr " : "up u_prev ") + std::to_string(n0), side_);
         };
         for (int c = 0; c < nu; ++c) upload(u, flat_.as<Real>(), ucur, N_ * c / nu, N_ * (c + 1) / nu, evU[c]);
+#ifndef DJG_HOST_TAPER
+#define DJG_HOST_TAPER 1
+#endif
+        // node-update chunk c covers slices [sb(c), sb(c + 1)); tapered: the
+        // last chunks are smaller, so less is left to update and read back
+        // after the last upload lands
+        auto sb = [&](int c) -> int64_t {
+            if (!DJG_HOST_TAPER || nc != 4) return S * c / nc;
+            static const int w[5] = {0, 30, 60, 85, 100};
+            return S * w[c] / 100;
+        };
         auto node_range = [&](int c, int64_t& n0, int64_t& n1) {
-            n0 = 32 * (S * c / nc);
-            n1 = std::min<int64_t>(N_, 32 * (S * (c + 1) / nc));
+            n0 = 32 * sb(c);
+            n1 = std::min<int64_t>(N_, 32 * sb(c + 1));
         };
         for (int c = 0; c < nc; ++c) {
             int64_t n0, n1;
@@ -1174,7 +1185,7 @@ public:
         }
         const Node* unew = u_[(ph + 1) % 3].as<Node>();
         for (int c = 0; c < nc; ++c) {
-            const int64_t s0 = S * c / nc, s1 = S * (c + 1) / nc;
+            const int64_t s0 = sb(c), s1 = sb(c + 1);
             const int ns = int(s1 - s0);
             int64_t n0, n1;
             node_range(c, n0, n1);

@@ -331,7 +331,7 @@ def our_arm(args):
                 "d2h_bytes_per_step": 3 * N * rbytes, "ms_per_step": e2e_ms,
                 "mode": "per step: djg_advance_host -- advance_step with a host SimState: H2D u_curr and "
                         "u_prev from pinned host (u_curr in 8 chunks, each element chunk starting once the node "
-                        "prefix it reads has landed; u_prev in 4 chunks gating the node-update chunks), one "
+                        "prefix it reads has landed; u_prev in 4 tapered chunks gating the node-update chunks), one "
                         "step, D2H the new u_curr chunk by chunk on the other copy direction; the next u_prev "
                         "is the host's previous u_curr; wall clock"},
         "e2e_run": {"value": E / (run_ms * 1e-3), "unit": UNIT, "steps": K, "ms_per_step": run_ms,

@@ -1126,8 +1126,22 @@ public:
         cudaEvent_t* evP = evU + kUpChunks;                    // u_prev chunk landed
         cudaEvent_t* evN = evP + kHostChunks;                  // node chunk updated
         cudaEvent_t evStart = evN[kHostChunks], evDone = evN[kHostChunks + 1];
-        reset_ctrl(step);
-        CK(cudaMemcpyAsync(hstart_, ctrl_.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream_));
+        // control block reset without a host round trip: the H2D copy is
+        // stream-ordered before the step (single-part engines never read the
+        // epoch stamps, so the last host copy's epoch is carried)
+        {
+            Ctrl c{};
+            c.epoch = ctrl_initialized_ ? hctrl_->epoch : 0u;
+            c.step = step;
+            c.first_inv = kNone;
+            c.asm_first = kNone;
+            c.halt_first_inv = -1;
+            c.fail_step = -1;
+            *hctrl_ = c;
+            *hstart_ = c;
+            ctrl_initialized_ = true;
+            CK(cudaMemcpyAsync(ctrl_.p, hctrl_, sizeof(Ctrl), cudaMemcpyHostToDevice, stream_));
+        }
         CK(cudaEventRecord(evStart, stream_));
         CK(cudaStreamWaitEvent(side_, evStart, 0));
         // DJG_TRACE_HOST=1: timing events along the three streams, printed

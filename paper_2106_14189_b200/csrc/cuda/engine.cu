@@ -45,6 +45,16 @@ namespace {
 #endif
 
 constexpr int kPipeStages = DJG_PIPE_STAGES;
+// H8 through the bulk-copy pipeline where its stage fits (f32 compact NH / TI /
+// OT: 29 KB per 128-element stage, 2 stages, 3 blocks/SM): 2.2M hexes NH 163
+// -> 142 us, TI 166 -> 146, OT 178 -> 153; cfg4 81 -> 73. The larger records
+// (f64, full, TLED) keep the one-shot kernel.
+#ifndef DJG_PIPE_H8
+#define DJG_PIPE_H8 1
+#endif
+#ifndef DJG_PIPE_H8_STAGES
+#define DJG_PIPE_H8_STAGES 2
+#endif
 
 #ifndef DJG_HOST_CHUNKS
 #define DJG_HOST_CHUNKS 4  // djg_advance_host: u_prev upload / node-update / read-back chunks
@@ -1269,10 +1279,10 @@ public:
     bool launch_pipe(cudaStream_t s, const ElemArgs<Real>& a, int64_t e0, int64_t e1, bool setup) {
         using PS = PipeShape<Real, K, M, RB, FORM>;
         // H8 bodies (heavier, 8 gathers, full record) run better one-shot.
-        if constexpr (K == 1 || PS::kStageBytes > kPipeMaxStageBytes) {
+        if constexpr ((K == 1 && !DJG_PIPE_H8) || PS::kStageBytes > kPipeMaxStageBytes) {
             return false;
         } else {
-            constexpr int ST = kPipeStages;
+            constexpr int ST = K == 1 ? DJG_PIPE_H8_STAGES : kPipeStages;
             auto kern = k_element_pipe<Real, K, M, RB, FORM, ST>;
             const size_t smem = PS::smem_bytes(ST);
             if (setup) {

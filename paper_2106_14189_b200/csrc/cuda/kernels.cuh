@@ -1042,7 +1042,12 @@ constexpr int kPipeMinBlocksT4C =
                       : (MODEL == 1 ? DJG_PIPE_MINB_T4C64_M1 : MODEL == 2 ? DJG_PIPE_MINB_T4C64_M2
                                                      : MODEL == 3 ? DJG_PIPE_MINB_T4C64_M3 : DJG_PIPE_MINB_T4C64);
 template <class Real, int KIND, int MODEL, int FORM>
-constexpr int kPipeMinBlocks = (KIND == 0 && FORM == 1) ? kPipeMinBlocksT4C<Real, MODEL> : DJG_PIPE_MINB_OTHER;
+#ifndef DJG_PIPE_MINB_H8
+#define DJG_PIPE_MINB_H8 3
+#endif
+constexpr int kPipeMinBlocks = (KIND == 0 && FORM == 1) ? kPipeMinBlocksT4C<Real, MODEL>
+                               : (KIND == 1 && FORM == 1 && sizeof(Real) == 4 && MODEL != 3) ? DJG_PIPE_MINB_H8
+                                                                                             : DJG_PIPE_MINB_OTHER;
 constexpr int kPipeThreads = kPipeTile + 32;  // 4 compute warps + the producer warp
 
 // Persistent blocks; tile `it` of a block (global tile blockIdx + it * grid)

@@ -124,8 +124,10 @@ def test_i57_longer_run(kind, precision):
 
 
 def test_pipeline_selection():
-    """T4 runs the bulk-copy pipeline by default; H8 and DJG_FLAG_NO_PIPE the one-shot kernel."""
-    for kind, flags, want in (("T4", 0, 1), ("T4", A.DJG_FLAG_NO_PIPE, 0), ("H8", 0, 0)):
+    """T4 and f32 compact H8 run the bulk-copy pipeline by default; DJG_FLAG_NO_PIPE and the
+    larger H8 records the one-shot kernel."""
+    for kind, flags, want in (("T4", 0, 1), ("T4", A.DJG_FLAG_NO_PIPE, 0), ("H8", 0, 1),
+                              ("H8", A.DJG_FLAG_FULL_RECORD, 0)):
         sc = Scenario(box_spec(kind=kind, divisions=3, precision=4))
         with GpuDjEngine(sc, flags=flags) as eng:
             assert eng.info()["pipelined"] == want, (kind, flags)

@@ -207,13 +207,22 @@ def _cpu_baseline_line(args):
         return {"value": None, "error": str(ex)}
 
 
+# SURVEY §8(d) config names, keyed by (kind, material, divisions).
+CFG_NAMES = {("T4", "NH", 12): "cfg1", ("H8", "NH", 22): "cfg2", ("T4", "NH", 70): "cfg3",
+             ("H8", "TI", 100): "cfg4", ("T4", "NH", 203): "cfg5"}
+
+
+def cfg_name(args):
+    return CFG_NAMES.get((args.kind, args.model, args.divisions), "custom")
+
+
 def _line(args, world, K, W, E, ms_step, value, extra):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": K, "warmup": W,
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32" if args.precision == 4 else "f64",
         "data": "synthetic (generate_box unit cube, bench_material, +1% z-extension ramp)",
-        "config": {"workload": f"cfg5: {args.kind}-{args.model} unit cube d={args.divisions}",
+        "config": {"workload": f"{cfg_name(args)}: {args.kind}-{args.model} unit cube d={args.divisions}",
                    "kind": args.kind, "material": args.model, "divisions": args.divisions,
                    "num_elements": E, "parallelism": f"{world} GPU" + (f" ({args.partition.upper()} partition, {args.transport} halo)" if world > 1 else "")},
         "time_per_step_us": ms_step * 1e3,
@@ -301,7 +310,7 @@ def our_arm(args):
         step_c.value = rep_c.step
         cur, prev, spare = spare, cur, prev
     te1 = time.perf_counter()
-    e2e_ms = (te1 - te0) / args.e2e_steps * 1e3
+    e2e_ms = (te1 - te0) / args.e2e_steps * 1e3 if args.e2e_steps > 0 else 1.0
     # The run_simulation path (solver.hpp:205-258) through the C-ABI: the
     # host SimState goes up once (djg_set_state from pinned host), K steps
     # run on the device (graph replay, failure checks on the device), the
@@ -324,8 +333,8 @@ def our_arm(args):
     k1_ms = ms_e / K
     achieved = B["k_element"] / (k1_ms * 1e-3) / 1e9
     traffic, traffic_src = None, None
-    if args.divisions == 203 and args.kind == "T4" and args.model == "NH" and args.precision == 4:
-        traffic, traffic_src = measured_traffic("cfg5", "k_element_pipe" if info.get("pipelined") else "k_element<")
+    if cfg_name(args) != "custom" and args.precision == 4:
+        traffic, traffic_src = measured_traffic(cfg_name(args), "k_element_pipe" if info.get("pipelined") else "k_element<")
     extra = {
         "e2e": {"value": E / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 2 * 3 * N * rbytes,
                 "d2h_bytes_per_step": 3 * N * rbytes, "ms_per_step": e2e_ms,
@@ -333,7 +342,7 @@ def our_arm(args):
                         "u_prev from pinned host (u_curr in 8 chunks, each element chunk starting once the node "
                         "prefix it reads has landed; u_prev in 4 tapered chunks gating the node-update chunks), one "
                         "step, D2H the new u_curr chunk by chunk on the other copy direction; the next u_prev "
-                        "is the host's previous u_curr; wall clock"},
+                        "is the host's previous u_curr; wall clock"} if args.e2e_steps > 0 else None,
         "e2e_run": {"value": E / (run_ms * 1e-3), "unit": UNIT, "steps": K, "ms_per_step": run_ms,
                     "h2d_bytes": 2 * 3 * N * rbytes, "d2h_bytes": 2 * 3 * N * rbytes,
                     "mode": "run_simulation path: djg_set_state (host SimState up once), djg_step(K) on the "

@@ -16,8 +16,8 @@ forces -> CSR gather -> central-difference update.
             host memory, advances one step and reads the new u_curr back
   roofline  k_element's algorithmic bytes / its average event-timed duration
             against MEASURED_PEAKS.json hbm_gbs
-  cpu_baseline  the unmodified reference (oracle/_ref, all host threads) on a
-            bounded sample of the same workload
+  cpu_baseline  the unmodified reference (oracle/_ref) on the same workload:
+            all host threads (and one thread), a bounded number of steps
 
 `--impl reference` times the reference's own CPU implementation instead.
 """
@@ -43,7 +43,6 @@ UNIT = "element-steps/s"
 # Hot-constant bytes per element in f32.
 CONST_BYTES = {("T4", "NH"): 92, ("T4", "TI"): 140, ("H8", "NH"): 224, ("H8", "TI"): 272,
                ("T4", "OT"): 188, ("H8", "OT"): 320, ("T4", "MR"): 320, ("H8", "MR"): 452}
-SAMPLE_DIVISIONS = 70   # reference CPU sample: cfg3-sized T4 box (2,058,000 elements)
 
 
 def log(*a):
@@ -152,57 +151,142 @@ def dist_env():
     return rank, world, local
 
 
-def cpu_reference_sample(steps: int, warmup: int, kind: str, model: str, precision: int) -> dict:
-    """The unmodified reference's advance_step loop (oracle/_ref) on the host,
-    all threads, on a bounded sample of the workload. Falls back to the C
-    restatement (kind "port") only where the reference library is absent."""
+def _mem_available() -> int:
+    """Host bytes this process may still allocate: MemAvailable, capped by
+    the cgroup limit when there is one."""
+    avail = 1 << 62
+    try:
+        for ln in open("/proc/meminfo"):
+            if ln.startswith("MemAvailable:"):
+                avail = int(ln.split()[1]) * 1024
+    except OSError:
+        pass
+    for p in ("/sys/fs/cgroup/memory.max", "/sys/fs/cgroup/memory/memory.limit_in_bytes"):
+        try:
+            v = open(p).read().strip()
+            if v.isdigit():
+                avail = min(avail, int(v))
+        except OSError:
+            pass
+    return avail
+
+
+def _peak_rss_gb() -> float:
+    import resource
+    return resource.getrusage(resource.RUSAGE_SELF).ru_maxrss / 2**20
+
+
+def _ref_host_bytes(kind: str, d: int, precision: int, tled: bool) -> int:
+    """Peak host memory of the reference's DjEngine on a d^3 box: the AoS
+    ElementConstants (1196 B f32 / 2384 B f64, every optional block
+    allocated), the 16-byte CSR pairs, connectivity and the
+    element-force scratch; TLED adds its 236 B (f32) record while the DJ
+    model is still alive."""
+    npe = 4 if kind == "T4" else 8
+    E = d ** 3 * (6 if kind == "T4" else 1)
+    rec = 1196 if precision == 4 else 2384
+    per = rec + npe * (16 + 4 + 3 * precision) + (236 * precision // 4 if tled else 0)
+    return int(E * per * 1.1) + (2 << 30)
+
+
+def cpu_reference_protocol(args, warmup: int, steps: int, one_thread: bool, tled: bool) -> dict:
+    """SURVEY §8(d)'s CPU path on the bench workload itself: the unmodified
+    reference (oracle/_ref: DjEngine + advance_step, the bench.hpp:87-95
+    loop), built with build_threads = all host threads (solver.hpp:264-267;
+    the build is not timed), then `warmup` + `steps` timed steps on all host
+    threads, 1 + 2 steps on one thread, and the same all-thread protocol on
+    the reference's TledEngine for the paper's DJ/TLED ratio. Falls back to
+    the C restatement (kind "port") only where the reference library is
+    absent, and to a smaller box only when host memory cannot hold the
+    reference's AoS constants (same_config false, said in `sample`)."""
     import oracle
     from paper_2106_14189_b200.spec import box_spec
     threads = os.cpu_count() or 1
-    spec = box_spec(kind=kind, model=model, divisions=SAMPLE_DIVISIONS, precision=precision, target=0.01,
+    d = args.divisions
+    need = _ref_host_bytes(args.kind, d, args.precision, tled)
+    avail = _mem_available()
+    note = ""
+    while need > avail and d > 8:
+        d = int(d * 0.8)
+        need = _ref_host_bytes(args.kind, d, args.precision, tled)
+    if d != args.divisions:
+        note = (f"; host memory {avail / 2**30:.0f} GiB cannot hold the reference's cfg d={args.divisions} "
+                f"constants: sampled d={d}")
+    E = d ** 3 * (6 if args.kind == "T4" else 1)
+    spec = box_spec(kind=args.kind, model=args.model, divisions=d, precision=args.precision, target=0.01,
                     ramp_steps=warmup + steps)
-    E = SAMPLE_DIVISIONS ** 3 * (6 if kind == "T4" else 1)
+    out = {"nproc": threads, "divisions": d, "num_elements": E, "same_config": d == args.divisions,
+           "omp_proc_bind": os.environ.get("OMP_PROC_BIND")}
     if oracle.have("ref"):
-        sec = oracle.ref_time_steps(spec, warmup, steps, threads, 0)
-        kind_s = "reference"
+        runs = [(threads, warmup, steps)] + ([(1, 1, 2)] if one_thread else [])
+        secs, build = oracle.ref_time_protocol(spec, 0, threads, runs)
+        out.update(kind="reference", sec=secs[0], build_s=build)
+        if one_thread:
+            out["threads_1"] = {"value": E / secs[1], "unit": UNIT, "ms_per_step": secs[1] * 1e3, "cores": 1,
+                                "sample": "1 warm-up + 2 timed advance_step calls, 1 thread"}
+        if tled:
+            tsecs, tbuild = oracle.ref_time_protocol(spec, 2, threads, [(threads, warmup, steps)])
+            out["tled"] = {"value": E / tsecs[0], "unit": UNIT, "ms_per_step": tsecs[0] * 1e3, "cores": threads,
+                           "dj_over_tled_time": secs[0] / tsecs[0], "build_s": tbuild,
+                           "sample": f"reference TledEngine, {warmup} warm-up + {steps} timed steps, "
+                                     f"{threads} threads (paper Table 5 ratio)"}
     else:
         t0 = time.perf_counter()
         oracle.run(spec, warmup, "oracle", threads=threads)
         t1 = time.perf_counter()
         oracle.run(spec, warmup + steps, "oracle", threads=threads)
         t2 = time.perf_counter()
-        sec = ((t2 - t1) - (t1 - t0)) / steps
-        kind_s = "port"
-    return {"value": E / sec, "unit": UNIT, "cores": threads, "kind": kind_s,
-            "ms_per_step": sec * 1e3,
-            "sample": f"{kind}-{model} box d={SAMPLE_DIVISIONS} ({E} elements), {warmup} warm-up + {steps} timed "
-                      f"advance_step calls, f{8 * precision}, OMP threads={threads}"}
+        out.update(kind="port", sec=((t2 - t1) - (t1 - t0)) / steps, build_s=None)
+    sec = out["sec"]
+    out.update(value=E / sec, unit=UNIT, cores=threads, ms_per_step=sec * 1e3,
+               sample=f"{args.kind}-{args.model} box d={d} ({E} elements), {warmup} warm-up + {steps} timed "
+                      f"advance_step calls, f{8 * args.precision}, {threads} threads (all host threads), "
+                      f"build_threads={threads} (build untimed){note}")
+    return out
 
 
 def reference_arm(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    steps = max(args.steps, 1)
-    cb = cpu_reference_sample(steps, max(args.warmup, 1), args.kind, args.model, args.precision)
+    # SURVEY §8(d)'s cfg5 CPU protocol is 3 warm-up + 10 timed steps: the
+    # driver's K is capped there so the arm ends within a few minutes, and
+    # the 3 warm-up steps are kept (the first steps after a multi-threaded
+    # build run several times slower while the kernel settles the freshly
+    # touched pages).
+    W, K = 3, min(max(args.steps, 1), 10)
+    cb = cpu_reference_protocol(args, W, K, one_thread=True, tled=True)
     line = {
-        "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": steps,
-        "warmup": args.warmup, "ms_per_step": cb["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+        "metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": K,
+        "warmup": W, "ms_per_step": cb["ms_per_step"], "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32" if args.precision == 4 else "f64",
-        "data": "synthetic (generate_box unit cube, bench_material)",
-        "config": {"workload": f"cfg5 reference sample: {args.kind}-{args.model} box d={SAMPLE_DIVISIONS}",
-                   "kind": args.kind, "material": args.model, "divisions": SAMPLE_DIVISIONS},
+        "data": "synthetic (generate_box unit cube, bench_material, +1% z-extension ramp)",
+        "config": {"workload": f"{cfg_name(args)}: {args.kind}-{args.model} unit cube d={cb['divisions']}",
+                   "kind": args.kind, "material": args.model, "divisions": cb["divisions"],
+                   "num_elements": cb["num_elements"], "parallelism": f"{cb['nproc']} host threads"},
         "impl": "reference",
+        "same_config": cb["same_config"],
         "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
         "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "nproc": cb["nproc"], "build_s": cb["build_s"], "host_peak_rss_gb": _peak_rss_gb(),
+        "steps_note": f"SURVEY §8(d)'s CPU protocol: 3 warm-up + min(K, 10) timed steps (asked K={args.steps}, W={args.warmup})",
     }
+    for k in ("threads_1", "tled"):
+        if k in cb:
+            line[k] = cb[k]
     print(json.dumps(line), flush=True)
 
 
 def _cpu_baseline_line(args):
+    """cpu_baseline: the reference on the bench workload itself, a bounded
+    number of steps (2 warm-up + 3 timed on all threads, 1 + 2 on one)."""
     try:
-        cb = cpu_reference_sample(args.cpu_steps, 2, args.kind, args.model, args.precision)
-        return {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cb = cpu_reference_protocol(args, 2, args.cpu_steps, one_thread=True, tled=False)
+        r = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        r.update(same_config=cb["same_config"], nproc=cb["nproc"], ms_per_step=cb["ms_per_step"])
+        if "threads_1" in cb:
+            r["threads_1"] = cb["threads_1"]
+        return r
     except Exception as ex:  # reported, not fatal
         return {"value": None, "error": str(ex)}
 
@@ -532,7 +616,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--tled-steps", type=int, default=100)
     ap.add_argument("--f64-steps", type=int, default=50, help="also time the f64 problem (0: skip)")
-    ap.add_argument("--cpu-steps", type=int, default=20)
+    ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="multi-GPU halo / agreement: peer-memory stores from the node kernel (default) or NCCL")

@@ -70,6 +70,8 @@ def lib(which: str = "oracle") -> C.CDLL:
                                           P(C.c_double), P(C.c_double), P(C.c_double), C.c_int32]
         L.djref_time_steps.argtypes = [P(A.djg_scenario_spec), C.c_int64, C.c_int64, C.c_int32, C.c_int32]
         L.djref_time_steps.restype = C.c_double
+        L.djref_time_protocol.argtypes = [P(A.djg_scenario_spec), C.c_int32, C.c_int32, C.c_int32, P(C.c_int32),
+                                          P(C.c_int64), P(C.c_int64), P(C.c_double), P(C.c_double)]
         L.djref_error.restype = C.c_char_p
     _libs[which] = L
     return L
@@ -196,6 +198,23 @@ def ref_time_steps(spec: Spec, warmup: int, steps: int, threads: int = 0, engine
     if r < 0:
         raise RuntimeError(lib("ref").djref_error().decode())
     return r
+
+
+def ref_time_protocol(spec: Spec, engine: int, build_threads: int, runs) -> tuple[list[float], float]:
+    """One reference problem built with `build_threads` (engine 0 DjEngine,
+    2 TledEngine), then for each (threads, warmup, steps) in `runs` the
+    advance_step loop from rest: mean seconds per timed step, and the build
+    time in seconds."""
+    n = len(runs)
+    th = (C.c_int32 * n)(*[r[0] for r in runs])
+    wu = (C.c_int64 * n)(*[r[1] for r in runs])
+    st = (C.c_int64 * n)(*[r[2] for r in runs])
+    secs = (C.c_double * n)()
+    b = C.c_double()
+    rc = lib("ref").djref_time_protocol(spec.ref(), engine, build_threads, n, th, wu, st, secs, C.byref(b))
+    if rc:
+        raise RuntimeError(lib("ref").djref_error().decode())
+    return list(secs), b.value
 
 
 def rel_max_err(a: np.ndarray, b: np.ndarray) -> float:

@@ -52,7 +52,9 @@ struct RefProblem {
     Real dt = 0, crit = 0, alpha = 0, ramp_t_total = 0, c_wave = 0;
     InversionPolicy policy = InversionPolicy::Abort;
 
-    RefProblem(const djg_scenario_spec& s, int engine) {
+    // engine 0: DJ-TLED only; 1: also TLED; 2: TLED only (the DJ model is
+    // built for lump_mass / critical_dt, which take its constants, then freed).
+    RefProblem(const djg_scenario_spec& s, int engine, int build_threads = 1) {
         const ElementKind kind = s.kind == DJG_T4 ? ElementKind::T4 : ElementKind::H8;
         if (!s.nodes) {
             mesh = generate_box<Real>({Real(s.extent[0]), Real(s.extent[1]), Real(s.extent[2])},
@@ -66,11 +68,15 @@ struct RefProblem {
         }
         mat = make_material<Real>(s.material);
         const Real c_hg = Real(s.c_hg);
-        dj = std::make_unique<DjEngine<Real>>(mesh, mat, c_hg, 1);
-        if (engine == 1) tled = std::make_unique<TledEngine<Real>>(mesh, mat, c_hg, 1);
+        dj = std::make_unique<DjEngine<Real>>(mesh, mat, c_hg, build_threads);
+        if (engine == 1) tled = std::make_unique<TledEngine<Real>>(mesh, mat, c_hg, build_threads);
         mass = lump_mass(mesh, mat.rho, dj->model().elems);
         c_wave = dilatational_wave_speed(mat);
         crit = critical_dt(mesh, dj->model().elems, c_wave);
+        if (engine == 2) {
+            dj.reset();
+            tled = std::make_unique<TledEngine<Real>>(mesh, mat, c_hg, build_threads);
+        }
         dt = s.dt > 0 ? Real(s.dt) : Real(s.safety) * crit;
         alpha = s.alpha_mode == 0 ? relaxation_alpha(mat, mesh) : Real(s.alpha);
         policy = s.policy == DJG_ABORT ? InversionPolicy::Abort : InversionPolicy::SkipAndReport;
@@ -340,6 +346,32 @@ double time_impl(const djg_scenario_spec& s, int64_t warmup, int64_t steps, int 
     return steps > 0 ? secs / double(steps) : 0.0;
 }
 
+// The SURVEY §8(d) CPU protocol on ONE built problem (cfg5 takes tens of
+// seconds to build): engine 0 (DjEngine) or 2 (TledEngine, built with
+// build_threads like the DjEngine), then for each i: warmup[i] untimed +
+// steps[i] timed advance_step calls with threads[i] threads, from rest.
+// secs[i] = mean seconds per timed step; *build_s = problem build time.
+template <class Real>
+int protocol_impl(const djg_scenario_spec& s, int engine, int build_threads, int n, const int32_t* threads,
+                  const int64_t* warmup, const int64_t* steps, double* secs, double* build_s) {
+    const auto t0 = std::chrono::steady_clock::now();
+    RefProblem<Real> P(s, engine == 0 ? 0 : 2, build_threads);
+    *build_s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    const Real* none = nullptr;
+    Real* out = nullptr;
+    for (int i = 0; i < n; ++i) {
+        djg_report r{};
+        double sec = 0;
+        if (engine == 0)
+            run_loop(P, *P.dj, warmup[i] + steps[i], threads[i], none, none, out, out, &r, &sec, warmup[i]);
+        else
+            run_loop(P, *P.tled, warmup[i] + steps[i], threads[i], none, none, out, out, &r, &sec, warmup[i]);
+        if (r.status != 0) throw SimulationError(SimulationError::Kind::Divergence, "timed run failed", r.fail_step);
+        secs[i] = steps[i] > 0 ? sec / double(steps[i]) : 0.0;
+    }
+    return 0;
+}
+
 template <class F>
 int guarded(F&& f) {
     try {
@@ -395,6 +427,15 @@ double djref_time_steps(const djg_scenario_spec* s, int64_t warmup, int64_t step
         return 0;
     });
     return r;
+}
+
+int djref_time_protocol(const djg_scenario_spec* s, int32_t engine, int32_t build_threads, int32_t n,
+                        const int32_t* threads, const int64_t* warmup, const int64_t* steps, double* secs,
+                        double* build_s) {
+    return guarded([&] {
+        return s->precision == 4 ? protocol_impl<float>(*s, engine, build_threads, n, threads, warmup, steps, secs, build_s)
+                                 : protocol_impl<double>(*s, engine, build_threads, n, threads, warmup, steps, secs, build_s);
+    });
 }
 
 int djref_max_threads(void) { return hardware_threads(); }

@@ -99,6 +99,11 @@ typedef struct djg_desc {
                                     paper's comparison path; record built on the device */
 #define DJG_FLAG_NO_PIPE 128u    /* one-shot element kernel instead of the bulk-copy
                                     pipelined one (k_element_pipe); bit-identical */
+#define DJG_FLAG_WINDOW 256u     /* pipelined element kernel with node windows: each
+                                    tile's node rows staged in shared memory by bulk
+                                    copies next to its slot positions (k_element_win);
+                                    bit-identical. Opt-in: faster on L2-resident meshes
+                                    (cfg3), slower on cfg5 */
 
 /* DjEngine(mesh, material, c_hg) (solver.hpp:264-267) at the mesh level:
  * the library runs the precompute (build_element_constants,
@@ -283,6 +288,8 @@ typedef struct djg_engine_info {
     int64_t slab_elements;      /* elements per slab */
     int32_t formulation;        /* 0 DJ-TLED, 1 TLED (DJG_FLAG_TLED) */
     int32_t pipelined;          /* element kernel streams tiles through shared memory */
+    int32_t windowed;           /* ... with each tile's node rows staged as windows */
+    int64_t window_tiles;       /* tiles whose nodes fit a window (the rest gather) */
 } djg_engine_info;
 int djg_get_info(djg_engine* eng, djg_engine_info* info);
 

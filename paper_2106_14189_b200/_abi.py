@@ -29,6 +29,7 @@ DJG_FLAG_DEVICE_PRECOMPUTE = 16
 DJG_FLAG_FULL_RECORD = 32
 DJG_FLAG_TLED = 64
 DJG_FLAG_NO_PIPE = 128
+DJG_FLAG_WINDOW = 256
 DJG_PART_RCB, DJG_PART_METIS = 0, 1
 PART_METHODS = {"rcb": DJG_PART_RCB, "metis": DJG_PART_METIS}
 
@@ -159,6 +160,7 @@ class djg_engine_info(C.Structure):
         ("npe", C.c_int32), ("nconst", C.c_int32), ("const_planes", C.c_int32), ("precision", C.c_int32),
         ("kernels_per_step", C.c_int32), ("sm_count", C.c_int32), ("slabs", C.c_int32),
         ("compact", C.c_int32), ("slab_elements", C.c_int64), ("formulation", C.c_int32), ("pipelined", C.c_int32),
+        ("windowed", C.c_int32), ("window_tiles", C.c_int64),
     ]
 
 

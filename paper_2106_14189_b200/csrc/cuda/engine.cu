@@ -60,6 +60,15 @@ constexpr int kPipeStages = DJG_PIPE_STAGES;
 #define DJG_HOST_CHUNKS 4  // djg_advance_host: u_prev upload / node-update / read-back chunks
 #endif
 constexpr int kPipeMaxStageBytes = DJG_PIPE_MAX_STAGE_KB * 1024;
+// k_element_win (node windows staged with the tile): the largest stage it is
+// used for, and whether H8 tiles use it (cfg4 hexes: ~460 window nodes).
+#ifndef DJG_WIN_MAX_STAGE_KB
+#define DJG_WIN_MAX_STAGE_KB 40
+#endif
+#ifndef DJG_WIN_H8
+#define DJG_WIN_H8 0
+#endif
+constexpr int kWinMaxStageBytes = DJG_WIN_MAX_STAGE_KB * 1024;
 
 thread_local std::string g_create_error;
 
@@ -506,8 +515,101 @@ public:
             if (const char* v = std::getenv("DJG_NODE_GRID")) node_grid_ = std::atoll(v);
         }
         pipe_ = !(flags_ & DJG_FLAG_NO_PIPE) && n_slabs_ == 1;
+        win_ = pipe_ && (flags_ & DJG_FLAG_WINDOW) && (kind_ == DJG_T4 || DJG_WIN_H8);
+        if (win_) build_windows(d.conn);
         if (pipe_) launch_element(stream_, 0, E_, nullptr, /*setup=*/true);
+        if (!win_) {
+            slot_.release();
+            widx_.release();
+            wdesc_.release();
+            ea_.slot = nullptr;
+            ea_.widx = nullptr;
+            ea_.wdesc = nullptr;
+            win_tiles_ = 0;
+        }
         set_state(nullptr, nullptr, 0);
+    }
+
+    // Node windows of the 128-element tiles (k_element_win, kernels.cuh): per
+    // tile the distinct node ids as at most kWinRuns runs (ids closer than
+    // kGap are merged: a few unused rows are cheaper than another copy) and
+    // at most kWinCap nodes, else the tile is flagged for the global gather;
+    // per element-node its index in the window; and the slot position of
+    // every element-node (device, from the ranks and slice bases).
+    void build_windows(const int32_t* conn) {
+        constexpr int kGap = 8;
+        const int npe = npe_;
+        const int cap = kind_ == DJG_H8 ? kWinCap<1> : kWinCap<0>;
+        const int lb = kind_ == DJG_H8 ? kWinIdxBytes<1> : kWinIdxBytes<0>;
+        const int64_t ntiles = (E_ + kPipeTile - 1) / kPipeTile;
+        std::vector<int32_t> desc(size_t(ntiles) * kWinDesc, 0);
+        std::vector<uint8_t> idx(size_t(E_) * size_t(npe * lb) + 16, 0);
+        int64_t fit = 0;
+        const bool force_fallback = std::getenv("DJG_WIN_FORCE_FALLBACK") != nullptr;  // (A/B diagnosis)
+#pragma omp parallel reduction(+ : fit)
+        {
+            std::vector<int32_t> ids;
+            ids.reserve(size_t(kPipeTile * npe));
+#pragma omp for schedule(dynamic, 512)
+            for (int64_t t = 0; t < ntiles; ++t) {
+                const int64_t eb = t * kPipeTile, ee = std::min<int64_t>(E_, eb + kPipeTile);
+                ids.assign(conn + eb * npe, conn + ee * npe);
+                std::sort(ids.begin(), ids.end());
+                ids.erase(std::unique(ids.begin(), ids.end()), ids.end());
+                int32_t rs[kWinRuns], ro[kWinRuns];
+                int nr = 0, total = 0;
+                bool ok = true;
+                for (size_t i = 0; i < ids.size() && ok;) {
+                    size_t j = i + 1;
+                    while (j < ids.size() && ids[j] - ids[j - 1] <= kGap) ++j;
+                    const int len = ids[j - 1] - ids[i] + 1;
+                    if (nr == kWinRuns || total + len > cap) {
+                        ok = false;
+                    } else {
+                        rs[nr] = ids[i];
+                        ro[nr] = total;
+                        total += len;
+                        ++nr;
+                    }
+                    i = j;
+                }
+                if (!ok || force_fallback) continue;  // nruns = 0: global gather
+                int32_t* d = desc.data() + size_t(t) * kWinDesc;
+                d[0] = nr;
+                d[1] = total;
+                for (int r = 0; r < nr; ++r) {
+                    d[2 + 2 * r] = rs[r];
+                    d[3 + 2 * r] = ro[r];
+                }
+                for (int64_t e = eb; e < ee; ++e)
+                    for (int a = 0; a < npe; ++a) {
+                        const int32_t n = conn[e * npe + a];
+                        int r = nr - 1;
+                        while (rs[r] > n) --r;
+                        const int w = ro[r] + (n - rs[r]);
+                        uint8_t* q = idx.data() + size_t(e * npe + a) * size_t(lb);
+                        q[0] = uint8_t(w & 0xff);
+                        if (lb == 2) q[1] = uint8_t(w >> 8);
+                    }
+                ++fit;
+            }
+        }
+        win_tiles_ = fit;
+        wdesc_.alloc(desc.size() * sizeof(int32_t));
+        CK(cudaMemcpy(wdesc_.p, desc.data(), wdesc_.bytes, cudaMemcpyHostToDevice));
+        widx_.alloc(idx.size());
+        CK(cudaMemcpy(widx_.p, idx.data(), widx_.bytes, cudaMemcpyHostToDevice));
+        slot_.alloc(size_t(E_) * size_t(npe) * sizeof(int32_t));
+        const unsigned grid = unsigned((E_ + 255) / 256);
+        if (rank_bytes_ == 1)
+            k_slot_planes<1><<<grid, 256>>>(conn_.as<int4>(), rank_.p, slicebase_.as<int>(), E_, npe, slot_.as<int4>());
+        else
+            k_slot_planes<2><<<grid, 256>>>(conn_.as<int4>(), rank_.p, slicebase_.as<int>(), E_, npe, slot_.as<int4>());
+        CK(cudaGetLastError());
+        CK(cudaDeviceSynchronize());
+        ea_.slot = slot_.as<int4>();
+        ea_.widx = widx_.p;
+        ea_.wdesc = wdesc_.as<int>();
     }
 
     // Step data: UpdateCoeffs (c1 per node, massless, c2, c3), DofConstraints
@@ -1301,6 +1403,33 @@ public:
         }
     }
 
+    // Windowed element kernel (k_element_win): tiles must start on the
+    // descriptor grid (e0 a multiple of the tile); otherwise false.
+    template <int K, int M, int FORM>
+    bool launch_win(cudaStream_t s, const ElemArgs<Real>& a, int64_t e0, int64_t e1, bool setup) {
+        using WS = WinShape<Real, K, M, FORM>;
+        if constexpr (WS::kStageBytes > kWinMaxStageBytes) {
+            return false;
+        } else {
+            constexpr int ST = K == 1 ? DJG_PIPE_H8_STAGES : kPipeStages;
+            auto kern = k_element_win<Real, K, M, FORM, ST>;
+            const size_t smem = WS::smem_bytes(ST);
+            if (setup) {
+                CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+                int nb = 0;
+                CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kPipeThreads, smem));
+                win_blocks_sm_ = nb;
+                return nb > 0;
+            }
+            if (e0 % kPipeTile != 0) return false;
+            const int64_t tiles = (e1 - e0 + kPipeTile - 1) / kPipeTile;
+            const int64_t sms = std::max(1, sms_ - pipe_spare_sms_);
+            const unsigned grid = unsigned(std::max<int64_t>(1, std::min<int64_t>(tiles, int64_t(win_blocks_sm_) * sms)));
+            kern<<<grid, kPipeThreads, smem, s>>>(a, e0, e1);
+            return true;
+        }
+    }
+
     void launch_element(cudaStream_t s, int64_t e0, int64_t e1, const Node* u_override = nullptr,
                         bool setup = false) {
         if (e1 <= e0 && !setup) return;
@@ -1310,6 +1439,13 @@ public:
         const int form = tled_ ? 2 : compact_ ? 1 : 0;
 #define DJG_K1(K, M)                                                                                            \
     do {                                                                                                        \
+        if (win_) {                                                                                             \
+            const bool wok = form == 2   ? launch_win<K, M, 2>(s, a, e0, e1, setup)                             \
+                             : form == 1 ? launch_win<K, M, 1>(s, a, e0, e1, setup)                             \
+                                         : launch_win<K, M, 0>(s, a, e0, e1, setup);                            \
+            if (setup) win_ = wok;                                                                              \
+            else if (wok) break;                                                                                \
+        }                                                                                                       \
         if (pipe_) {                                                                                            \
             bool ok;                                                                                            \
             if (rank_bytes_ == 1)                                                                               \
@@ -1540,7 +1676,7 @@ public:
         o->num_elements = E_;
         o->num_slots = E_ * npe_;
         o->slot_capacity = capacity_;
-        o->device_bytes = int64_t(conn_.bytes + rank_.bytes + consts_.bytes + 3 * u_[0].bytes + uscratch_.bytes +
+        o->device_bytes = int64_t(slot_.bytes + widx_.bytes + wdesc_.bytes + conn_.bytes + rank_.bytes + consts_.bytes + 3 * u_[0].bytes + uscratch_.bytes +
                                   flat_.bytes + ef_.bytes + rowlen_.bytes + slicebase_.bytes + c1_.bytes +
                                   code_.bytes + target_.bytes + tTotal_.bytes + rext_.bytes + ctrl_.bytes +
                                   slabSlices_.bytes);
@@ -1552,6 +1688,8 @@ public:
         o->compact = compact_ ? 1 : 0;
         o->formulation = tled_ ? 1 : 0;
         o->pipelined = pipe_ ? 1 : 0;
+        o->windowed = win_ ? 1 : 0;
+        o->window_tiles = win_tiles_;
         o->slabs = n_slabs_;
         o->slab_elements = slab_elems_;
         o->sm_count = sms_;
@@ -1618,9 +1756,11 @@ private:
     std::vector<void*> ipc_open_;
     DevBuf pairs_, rowoff_, mass_;  // device layout: sorted CSR pairs (until masses are built), lump_mass
     Real lmin_ = 0;
-    bool compact_ = false, tled_ = false, pipe_ = false;
-    int pipe_blocks_sm_ = 0;
+    bool compact_ = false, tled_ = false, pipe_ = false, win_ = false;
+    int pipe_blocks_sm_ = 0, win_blocks_sm_ = 0;
     size_t pipe_smem_ = 0;
+    int64_t win_tiles_ = 0;            // tiles whose nodes fit a window (k_element_win)
+    DevBuf slot_, widx_, wdesc_;       // node windows: slot positions, window indices, tile descriptors
     uint32_t flags_ = 0;
     int64_t N_ = 0, E_ = 0, capacity_ = 0;
     cudaStream_t stream_ = nullptr;

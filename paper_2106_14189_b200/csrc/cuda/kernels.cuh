@@ -156,6 +156,10 @@ struct ElemArgs {
     const void* rank;                    // per element: npe ranks (uint8 or uint16) of the element
                                          // in its nodes' CSR rows, packed in one 4/8/16-byte word
     const int* slice_base;               // first slot of each 32-node slice
+    const int4* slot;                    // node windows: NPE/4 planes of int4[E], slot position of
+                                         // each element-node (slice_base[n/32] + 32 rank + n%32)
+    const void* widx;                    // node windows: per element NPE window indices (uint8 / uint16)
+    const int* wdesc;                    // node windows: kWinDesc ints per 128-element tile, or NULL
     const long long* elem_l2g;           // multi-part: global id of each local element (inversions
                                          // are reported in global ids), else NULL
     const typename RT<Real>::Plane* c;   // nplanes planes of Plane[E]
@@ -963,6 +967,20 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
         "r"(parity)
         : "memory");
 }
+// The same wait with a suspend-time hint: a waiting warp sleeps (up to
+// `ns`) instead of re-polling, leaving the issue slots to the warps that
+// have work.
+__device__ __forceinline__ void mbar_wait_sleep(unsigned long long* b, unsigned parity, unsigned ns) {
+    asm volatile(
+        "{\n"
+        " .reg .pred p;\n"
+        "DJG_WAITS_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        " @!p bra DJG_WAITS_%=;\n"
+        "}\n" ::"r"(smem_addr(b)),
+        "r"(parity), "r"(ns)
+        : "memory");
+}
 __device__ __forceinline__ unsigned long long l2_evict_first_policy() {
     unsigned long long pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -1129,6 +1147,324 @@ __global__ void __launch_bounds__(kPipeThreads, (kPipeMinBlocks<Real, KIND, MODE
         }
         __syncwarp();
         if ((tid & 31) == 0) mbar_arrive(empty + s);
+    }
+}
+
+// ------------------------------------------------------------------ K1, node windows
+
+// A 128-element tile of a mesh numbered with some locality touches its nodes
+// in a few contiguous id runs (the cube: <= 6 runs, <= 96 nodes per T4 tile,
+// <= 528 per H8 tile). The engine lists each tile's runs once (kWinDesc ints:
+// nruns, window length, then (first node, window offset) per run) and gives
+// every element-node its index in the tile's window. The producer warp then
+// moves the window's displacements (and, for the compact T4 record, the
+// reference coordinates) into the stage with one bulk copy per run, next to
+// the slot positions, window indices and record planes of the tile: the
+// compute warps read every input from shared memory and only store to HBM,
+// so the dependent node gather no longer sits on their critical path.
+// Tiles whose nodes do not fit (more than kWinRuns runs or kWinCap nodes)
+// are flagged nruns = 0 and stage their connectivity instead (global gather,
+// as in k_element_pipe). Arithmetic and slot positions are unchanged:
+// bit-identical to k_element / k_element_pipe.
+constexpr int kWinDesc = 16;  // ints per tile descriptor
+// (A/B diagnosis only) DJG_WIN_NULL_COMPUTE: compute warps skip the element
+// body; DJG_WIN_XGLOBAL: no coordinate window (wrong results, timing only).
+// L2 policy of the window copies: 0 evict_normal, 1 evict_last, 2 evict_last
+// on half the lines, 3 evict_unchanged.
+#ifndef DJG_WIN_POL
+#define DJG_WIN_POL 0
+#endif
+// Suspend-time hint (ns) of the window kernel's barrier waits (0: poll).
+#ifndef DJG_WIN_SLEEP
+#define DJG_WIN_SLEEP 0
+#endif
+#ifndef DJG_WIN_NULL_COMPUTE
+#define DJG_WIN_NULL_COMPUTE 0
+#endif
+#ifndef DJG_WIN_XGLOBAL
+#define DJG_WIN_XGLOBAL 0
+#endif
+constexpr int kWinRuns = 7;   // runs per tile descriptor
+#ifndef DJG_WIN_CAP_T4
+#define DJG_WIN_CAP_T4 128
+#endif
+#ifndef DJG_WIN_CAP_H8
+#define DJG_WIN_CAP_H8 576
+#endif
+template <int KIND>
+constexpr int kWinCap = KIND == 1 ? DJG_WIN_CAP_H8 : DJG_WIN_CAP_T4;
+template <int KIND>
+constexpr int kWinIdxBytes = kWinCap<KIND> <= 256 ? 1 : 2;
+
+template <class Real, int KIND, int MODEL, int FORM>  // FORM 0 full, 1 compact, 2 TLED
+struct WinShape {
+    using T = RT<Real>;
+    using Node = typename T::Node;
+    static constexpr int NPE = KIND == 1 ? 8 : 4;
+    static constexpr int NCP = NPE / 4;
+    static constexpr int LB = kWinIdxBytes<KIND>;
+    static constexpr int CAP = kWinCap<KIND>;
+    static constexpr int NX = (FORM == 1 && KIND == 0 && !DJG_WIN_XGLOBAL) ? 2 : 1;  // u (+ X for the compact T4 rebuild)
+    static constexpr int kRecLen = FORM == 2   ? TledLayout<KIND>::count
+                                   : FORM == 1 ? kCompactLen<KIND>
+                                               : Layout<KIND, MODEL>::count;
+    using RP = RecPlanes<Real, kRecLen, FORM == 1 && kTailRecord<KIND, true>>;
+    static constexpr int NRP = RP::NFULL;
+    static constexpr int NTAIL = RP::NTAIL;
+    static constexpr int kSlotOff = 0;
+    static constexpr int kIdxOff = kSlotOff + kPipeTile * 16 * NCP;
+    static constexpr int kRecOff = kIdxOff + kPipeTile * NPE * LB;
+    static constexpr int kTailOff = kRecOff + kPipeTile * 16 * NRP;
+    static constexpr int kWinOff = (kTailOff + kPipeTile * int(sizeof(Real)) * NTAIL + 15) / 16 * 16;
+    static constexpr int kWinBytes = CAP * int(sizeof(Node)) * NX > kPipeTile * 16 * NCP
+                                         ? CAP * int(sizeof(Node)) * NX
+                                         : kPipeTile * 16 * NCP;  // (fallback tiles: connectivity planes)
+    static constexpr int kModeOff = kWinOff + kWinBytes;
+    static constexpr int kStageBytes = kModeOff + 16;
+    static constexpr size_t smem_bytes(int stages) { return size_t(stages) * kStageBytes + 2 * 8 * size_t(stages); }
+};
+
+// Inputs of a windowed tile: everything from the stage.
+template <class Real, int TILE, int NPE, int LB>
+struct WinSrc {
+    using Node = typename RT<Real>::Node;
+    const int4* sslot;                     // [NPE/4][TILE] slot positions
+    const void* sidx;                      // [TILE] window indices
+    const typename RT<Real>::Plane* srec;  // [planes][TILE]
+    const Real* stail;                     // [NTAIL][TILE]
+    const Node* wu;                        // window displacements
+    const Node* wx;                        // window coordinates (compact T4)
+    int i;
+    __device__ __forceinline__ int4 conn(int p) const {
+        if constexpr (LB == 1) {
+            static_assert(NPE == 4, "uint8 window indices: T4");
+            const unsigned w = static_cast<const unsigned*>(sidx)[i];
+            return make_int4(int(w & 0xff), int((w >> 8) & 0xff), int((w >> 16) & 0xff), int(w >> 24));
+        } else {
+            const uint2 q = static_cast<const uint2*>(sidx)[i * (NPE / 4) + p];
+            return make_int4(int(q.x & 0xffff), int(q.x >> 16), int(q.y & 0xffff), int(q.y >> 16));
+        }
+    }
+    __device__ __forceinline__ Node node(int, const Node* __restrict__, int h) const { return wu[h]; }
+    __device__ __forceinline__ Node coord(const ElemArgs<Real>& A, int h) const {
+        if constexpr (DJG_WIN_XGLOBAL) return RT<Real>::load_node(A.X + xbase[h]);
+        else return wx[h];
+    }
+    __device__ __forceinline__ typename RT<Real>::Plane plane(int p) const { return srec[p * TILE + i]; }
+    __device__ __forceinline__ Real tail(int t) const { return stail[t * TILE + i]; }
+    template <int N, int RB>
+    __device__ __forceinline__ void ranks(int (&rk)[N]) const {
+#pragma unroll
+        for (int a = 0; a < N; ++a) rk[a] = 0;
+    }
+    __device__ __forceinline__ int slot(const int* __restrict__, int a, int, int) const {
+        return reinterpret_cast<const int*>(sslot + (a >> 2) * TILE + i)[a & 3];
+    }
+    const int* xbase;                      // (A/B DJG_WIN_XGLOBAL) unused otherwise
+};
+
+// Inputs of a tile that did not fit a window: connectivity staged in the
+// window region, node rows gathered from global memory.
+template <class Real, int TILE>
+struct WinGlobalSrc {
+    using Node = typename RT<Real>::Node;
+    const int4* sslot;
+    const int4* sconn;                     // [NPE/4][TILE] node ids
+    const typename RT<Real>::Plane* srec;
+    const Real* stail;
+    int i;
+    __device__ __forceinline__ int4 conn(int p) const { return sconn[p * TILE + i]; }
+    __device__ __forceinline__ Node node(int, const Node* __restrict__ u, int n) const { return RT<Real>::load_node(u + n); }
+    __device__ __forceinline__ Node coord(const ElemArgs<Real>& a, int n) const { return RT<Real>::load_node(a.X + n); }
+    __device__ __forceinline__ typename RT<Real>::Plane plane(int p) const { return srec[p * TILE + i]; }
+    __device__ __forceinline__ Real tail(int t) const { return stail[t * TILE + i]; }
+    template <int N, int RB>
+    __device__ __forceinline__ void ranks(int (&rk)[N]) const {
+#pragma unroll
+        for (int a = 0; a < N; ++a) rk[a] = 0;
+    }
+    __device__ __forceinline__ int slot(const int* __restrict__, int a, int, int) const {
+        return reinterpret_cast<const int*>(sslot + (a >> 2) * TILE + i)[a & 3];
+    }
+};
+
+// Persistent blocks over tiles [e0, e1) (e0 on a tile boundary), tile `it` of
+// a block in stage it % STAGES: the producer warp (warp 4) reads the tile's
+// descriptor, lane 0 posts the stage's byte count and copies the per-element
+// streams, lanes r < nruns copy run r of the window; the compute warps run
+// the element body on the stage and release it.
+template <class Real, int KIND, int MODEL, int FORM, int STAGES>
+__global__ void __launch_bounds__(kPipeThreads, (kPipeMinBlocks<Real, KIND, MODEL, FORM>))
+    k_element_win(const ElemArgs<Real> A, long long e0, long long e1) {
+    using WS = WinShape<Real, KIND, MODEL, FORM>;
+    using Plane = typename RT<Real>::Plane;
+    using Node = typename RT<Real>::Node;
+    static_assert(STAGES >= 2, "pipeline needs at least two stages");
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(smem + STAGES * WS::kStageBytes);
+    unsigned long long* empty = full + STAGES;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+#pragma unroll
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, kPipeTile / 32);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (__ldcg(&A.ctrl->halted)) return;
+    const long long ntiles = (e1 - e0 + kPipeTile - 1) / kPipeTile;
+    const long long G = gridDim.x;
+    const long long nmine = blockIdx.x < ntiles ? (ntiles - 1 - blockIdx.x) / G + 1 : 0;
+    const int phase = int(__ldcg(&A.ctrl->step) % 3);
+    const Node* u = A.u_override ? A.u_override : pick3(phase, A.u[0], A.u[1], A.u[2]);
+
+    if (tid >= kPipeTile) {  // producer warp
+        const int lane = tid - kPipeTile;
+        const unsigned long long pol = l2_evict_first_policy();
+        unsigned long long wpol;
+        if constexpr (DJG_WIN_POL == 1)
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(wpol));
+        else if constexpr (DJG_WIN_POL == 2)
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 0.5;" : "=l"(wpol));
+        else if constexpr (DJG_WIN_POL == 3)
+            asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(wpol));
+        else
+            asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(wpol));
+        // Descriptors are read kWinAhead tiles ahead (registers), so their
+        // HBM latency overlaps the empty-barrier waits instead of delaying
+        // the tile's copies. Every lane reads the run count and window
+        // length, lane r < kWinRuns its run's first node and window offsets
+        // (no shuffles: the producer's issue slots are the scarce resource).
+        constexpr int kWinAhead = 2;
+        struct Desc {
+            int nruns, total, rstart, roff, rnext;
+        };
+        auto desc_of = [&](long long it) {
+            Desc d{0, 0, 0, 0, 0};
+            if (it < nmine) {
+                const int* p = A.wdesc + ((e0 + (blockIdx.x + it * G) * kPipeTile) / kPipeTile) * kWinDesc;
+                d.nruns = __ldg(p);
+                d.total = __ldg(p + 1);
+                if (lane < kWinRuns) {
+                    d.rstart = __ldg(p + 2 + 2 * lane);
+                    d.roff = __ldg(p + 3 + 2 * lane);
+                    d.rnext = lane + 1 < kWinRuns ? __ldg(p + 5 + 2 * lane) : 0;
+                }
+            }
+            return d;
+        };
+        Desc dq[kWinAhead];
+#pragma unroll
+        for (int k = 0; k < kWinAhead; ++k) dq[k] = desc_of(k);
+        for (long long it = 0; it < nmine; ++it) {
+            const int s = int(it % STAGES);
+            const Desc dv = dq[0];
+#pragma unroll
+            for (int k = 0; k + 1 < kWinAhead; ++k) dq[k] = dq[k + 1];
+            dq[kWinAhead - 1] = desc_of(it + kWinAhead);
+            // all lanes wait (a converged warp: no collective emulation below)
+            if (it >= STAGES) {
+                if constexpr (DJG_WIN_SLEEP > 0) mbar_wait_sleep(empty + s, unsigned((it / STAGES - 1) & 1), DJG_WIN_SLEEP);
+                else mbar_wait(empty + s, unsigned((it / STAGES - 1) & 1));
+            }
+            const long long eb = e0 + (blockIdx.x + it * G) * kPipeTile;
+            const unsigned n = unsigned(min((long long)kPipeTile, e1 - eb));
+            const int nruns = dv.nruns, total = dv.total, rstart = dv.rstart, roff = dv.roff, rnext = dv.rnext;
+            unsigned char* st = smem + s * WS::kStageBytes;
+            if (lane == 0) {
+                DJG_ASSERT(nruns >= 0 && nruns <= kWinRuns && total >= 0 && total <= WS::CAP);
+                const unsigned ibytes = (n * WS::NPE * WS::LB + 15u) & ~15u;  // index array padded by 16 bytes
+                const unsigned tbytes = (n * unsigned(sizeof(Real)) + 15u) & ~15u;
+                const unsigned wbytes = nruns > 0 ? unsigned(total) * unsigned(sizeof(Node)) * WS::NX : n * 16u * WS::NCP;
+                *reinterpret_cast<int*>(st + WS::kModeOff) = nruns;
+                mbar_expect_tx(full + s, n * 16u * (WS::NCP + WS::NRP) + ibytes + tbytes * WS::NTAIL + wbytes);
+#pragma unroll
+                for (int p = 0; p < WS::NCP; ++p)
+                    bulk_load(st + WS::kSlotOff + p * kPipeTile * 16, A.slot + (long long)p * A.E + eb, n * 16u,
+                              full + s, pol);
+                bulk_load(st + WS::kIdxOff, static_cast<const unsigned char*>(A.widx) + eb * WS::NPE * WS::LB, ibytes,
+                          full + s, pol);
+#pragma unroll
+                for (int p = 0; p < WS::NRP; ++p)
+                    bulk_load(st + WS::kRecOff + p * kPipeTile * 16, A.c + (long long)p * A.E + eb, n * 16u, full + s,
+                              pol);
+#pragma unroll
+                for (int t = 0; t < WS::NTAIL; ++t)
+                    bulk_load(st + WS::kTailOff + t * kPipeTile * int(sizeof(Real)), A.ctail + t * A.tail_stride + eb,
+                              tbytes, full + s, pol);
+                if (nruns == 0) {
+#pragma unroll
+                    for (int p = 0; p < WS::NCP; ++p)
+                        bulk_load(st + WS::kWinOff + p * kPipeTile * 16, A.conn + (long long)p * A.E + eb, n * 16u,
+                                  full + s, pol);
+                }
+            }
+            __syncwarp();
+            if (lane < nruns) {
+                const int wend = lane + 1 < nruns ? rnext : total;
+                const unsigned bytes = unsigned(wend - roff) * unsigned(sizeof(Node));
+                DJG_ASSERT(roff >= 0 && wend <= total && rstart >= 0 && rstart + (wend - roff) <= A.N);
+                // node rows are re-read by neighbouring tiles (other cell rows
+                // and planes): kept in L2 with the window policy
+                bulk_load(st + WS::kWinOff + roff * int(sizeof(Node)), u + rstart, bytes, full + s, wpol);
+                if constexpr (WS::NX == 2)
+                    bulk_load(st + WS::kWinOff + (WS::CAP + roff) * int(sizeof(Node)), A.X + rstart, bytes, full + s,
+                              wpol);
+            }
+        }
+        return;
+    }
+
+    for (long long it = 0; it < nmine; ++it) {
+        const int s = int(it % STAGES);
+        if constexpr (DJG_WIN_SLEEP > 0) mbar_wait_sleep(full + s, unsigned((it / STAGES) & 1), DJG_WIN_SLEEP);
+        else mbar_wait(full + s, unsigned((it / STAGES) & 1));
+        const long long e = e0 + (blockIdx.x + it * G) * kPipeTile + tid;
+        const unsigned char* st = smem + s * WS::kStageBytes;
+        const int mode = *reinterpret_cast<const int*>(st + WS::kModeOff);
+        if (DJG_WIN_NULL_COMPUTE && e < e1 && mode < 0) A.ef[0] = Node{};
+        if (!DJG_WIN_NULL_COMPUTE && e < e1) {
+            const int4* sslot = reinterpret_cast<const int4*>(st + WS::kSlotOff);
+            const Plane* srec = reinterpret_cast<const Plane*>(st + WS::kRecOff);
+            const Real* stail = reinterpret_cast<const Real*>(st + WS::kTailOff);
+            if (mode > 0) {
+                const Node* wu = reinterpret_cast<const Node*>(st + WS::kWinOff);
+                const WinSrc<Real, kPipeTile, WS::NPE, WS::LB> src{sslot, st + WS::kIdxOff, srec, stail, wu,
+                                                                     wu + WS::CAP, tid, nullptr};
+                if constexpr (FORM == 2) element_body_tled<Real, KIND, MODEL, 1>(A, e, u, src);
+                else element_body<Real, KIND, MODEL, 1, FORM == 1>(A, e, u, src);
+            } else {
+                const WinGlobalSrc<Real, kPipeTile> src{sslot, reinterpret_cast<const int4*>(st + WS::kWinOff), srec,
+                                                        stail, tid};
+                if constexpr (FORM == 2) element_body_tled<Real, KIND, MODEL, 1>(A, e, u, src);
+                else element_body<Real, KIND, MODEL, 1, FORM == 1>(A, e, u, src);
+            }
+        }
+        __syncwarp();
+        if ((tid & 31) == 0) mbar_arrive(empty + s);
+    }
+}
+
+// Slot position of every element-node (slice_base[n/32] + 32 rank + n%32),
+// in the connectivity's int4 plane layout, for the windowed element kernel.
+template <int RB>
+__global__ void k_slot_planes(const int4* __restrict__ conn, const void* __restrict__ rank,
+                              const int* __restrict__ slice_base, long long E, int npe, int4* __restrict__ out) {
+    const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= E) return;
+    const unsigned char* r = static_cast<const unsigned char*>(rank) + e * npe * RB;
+    for (int p = 0; p < npe / 4; ++p) {
+        const int4 q = conn[(long long)p * E + e];
+        const int n[4] = {q.x, q.y, q.z, q.w};
+        int v[4];
+        for (int k = 0; k < 4; ++k) {
+            const int a = 4 * p + k;
+            const int rk = RB == 1 ? int(r[a]) : int(r[2 * a] | (r[2 * a + 1] << 8));
+            v[k] = slice_base[n[k] >> 5] + 32 * rk + (n[k] & 31);
+        }
+        out[(long long)p * E + e] = make_int4(v[0], v[1], v[2], v[3]);
     }
 }
 

@@ -104,6 +104,55 @@ def test_pipeline_partial_tiles(model, precision, flags):
     check_run(spec, 250, flags=flags)
 
 
+@pytest.mark.parametrize("precision", [4, 8])
+@pytest.mark.parametrize("model", ["NH", "TI", "OT", "MR"])
+@pytest.mark.parametrize("flags", [0, A.DJG_FLAG_FULL_RECORD, A.DJG_FLAG_DEVICE_PRECOMPUTE])
+def test_node_windows_bitwise(model, precision, flags):
+    """k_element_win (DJG_FLAG_WINDOW): each tile's node rows staged by
+    bulk copies beside precomputed slot positions -- every T4 tile of the
+    box fits its window, partial last tile included; bit-identical to the
+    oracle."""
+    if model == "MR" and not flags & A.DJG_FLAG_FULL_RECORD:
+        flags |= A.DJG_FLAG_COMPACT
+    spec = box_spec(kind="T4", model=model, divisions=(5, 4, 6), precision=precision, ramp_steps=250)
+    with GpuDjEngine(Scenario(spec), flags=flags | A.DJG_FLAG_WINDOW) as eng:
+        info = eng.info()
+    if info["pipelined"]:
+        assert info["windowed"] == 1 and info["window_tiles"] == 6, info
+    check_run(spec, 250, flags=flags | A.DJG_FLAG_WINDOW)
+
+
+def test_node_windows_mixed_tiles():
+    """A box whose node ids are permuted in the upper half only: tiles of the
+    lower half fit their windows, the others fall back to the staged
+    connectivity + global gather; both kinds of tile in one launch, the
+    multi-step graph and the host-state step, bit-identical."""
+    rng = np.random.default_rng(5)
+    img = Scenario(box_spec(kind="T4", divisions=(8, 6, 10), precision=4)).image()
+    x = img["nodes"].reshape(-1, 3).astype(np.float64)
+    conn = img["conn"].reshape(-1, 4)
+    N = len(x)
+    perm = np.arange(N)
+    hi = np.flatnonzero(x[:, 2] > 0.5)
+    perm[hi] = rng.permutation(hi)          # old node i -> new id perm[i]
+    xn = np.empty_like(x)
+    xn[perm] = x
+    cn = perm[conn].astype(np.int32)
+    z = xn[:, 2]
+    bottom = np.flatnonzero(z == z.min())
+    top = np.flatnonzero(z == z.max())
+    for prec in (4, 8):
+        spec = mesh_spec(xn, cn, kind="T4", precision=prec, fixed=[(int(n), a) for n in bottom for a in range(3)],
+                         prescribed=[(int(n), 2, -0.04, 1e-3) for n in top])
+        sc = Scenario(spec)
+        with GpuDjEngine(sc, flags=A.DJG_FLAG_WINDOW) as eng:
+            info = eng.info()
+            ntiles = (sc.num_elements + 127) // 128
+            assert 0 < info["window_tiles"] < ntiles, info
+        check_run(spec, 200, flags=A.DJG_FLAG_WINDOW)
+        check_run(spec, 200, flags=A.DJG_FLAG_WINDOW | A.DJG_FLAG_NO_GRAPH)
+
+
 @pytest.mark.parametrize("flags", [A.DJG_FLAG_COMPACT, A.DJG_FLAG_DEVICE_PRECOMPUTE, A.DJG_FLAG_TLED])
 def test_i57_full_record_only(flags):
     """DJG_I57 (the I5 / I7 test energy) runs on the host-built full record;

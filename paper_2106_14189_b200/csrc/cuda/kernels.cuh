@@ -967,20 +967,6 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity
         "r"(parity)
         : "memory");
 }
-// The same wait with a suspend-time hint: a waiting warp sleeps (up to
-// `ns`) instead of re-polling, leaving the issue slots to the warps that
-// have work.
-__device__ __forceinline__ void mbar_wait_sleep(unsigned long long* b, unsigned parity, unsigned ns) {
-    asm volatile(
-        "{\n"
-        " .reg .pred p;\n"
-        "DJG_WAITS_%=:\n"
-        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
-        " @!p bra DJG_WAITS_%=;\n"
-        "}\n" ::"r"(smem_addr(b)),
-        "r"(parity), "r"(ns)
-        : "memory");
-}
 __device__ __forceinline__ unsigned long long l2_evict_first_policy() {
     unsigned long long pol;
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
@@ -1167,23 +1153,6 @@ __global__ void __launch_bounds__(kPipeThreads, (kPipeMinBlocks<Real, KIND, MODE
 // as in k_element_pipe). Arithmetic and slot positions are unchanged:
 // bit-identical to k_element / k_element_pipe.
 constexpr int kWinDesc = 16;  // ints per tile descriptor
-// (A/B diagnosis only) DJG_WIN_NULL_COMPUTE: compute warps skip the element
-// body; DJG_WIN_XGLOBAL: no coordinate window (wrong results, timing only).
-// L2 policy of the window copies: 0 evict_normal, 1 evict_last, 2 evict_last
-// on half the lines, 3 evict_unchanged.
-#ifndef DJG_WIN_POL
-#define DJG_WIN_POL 0
-#endif
-// Suspend-time hint (ns) of the window kernel's barrier waits (0: poll).
-#ifndef DJG_WIN_SLEEP
-#define DJG_WIN_SLEEP 0
-#endif
-#ifndef DJG_WIN_NULL_COMPUTE
-#define DJG_WIN_NULL_COMPUTE 0
-#endif
-#ifndef DJG_WIN_XGLOBAL
-#define DJG_WIN_XGLOBAL 0
-#endif
 constexpr int kWinRuns = 7;   // runs per tile descriptor
 #ifndef DJG_WIN_CAP_T4
 #define DJG_WIN_CAP_T4 128
@@ -1204,7 +1173,7 @@ struct WinShape {
     static constexpr int NCP = NPE / 4;
     static constexpr int LB = kWinIdxBytes<KIND>;
     static constexpr int CAP = kWinCap<KIND>;
-    static constexpr int NX = (FORM == 1 && KIND == 0 && !DJG_WIN_XGLOBAL) ? 2 : 1;  // u (+ X for the compact T4 rebuild)
+    static constexpr int NX = (FORM == 1 && KIND == 0) ? 2 : 1;  // u (+ X for the compact T4 rebuild)
     static constexpr int kRecLen = FORM == 2   ? TledLayout<KIND>::count
                                    : FORM == 1 ? kCompactLen<KIND>
                                                : Layout<KIND, MODEL>::count;
@@ -1219,7 +1188,7 @@ struct WinShape {
     static constexpr int kWinBytes = CAP * int(sizeof(Node)) * NX > kPipeTile * 16 * NCP
                                          ? CAP * int(sizeof(Node)) * NX
                                          : kPipeTile * 16 * NCP;  // (fallback tiles: connectivity planes)
-    static constexpr int kModeOff = kWinOff + kWinBytes;
+    static constexpr int kModeOff = kWinOff + kWinBytes;  // the tile's run count (0: global gather)
     static constexpr int kStageBytes = kModeOff + 16;
     static constexpr size_t smem_bytes(int stages) { return size_t(stages) * kStageBytes + 2 * 8 * size_t(stages); }
 };
@@ -1246,10 +1215,7 @@ struct WinSrc {
         }
     }
     __device__ __forceinline__ Node node(int, const Node* __restrict__, int h) const { return wu[h]; }
-    __device__ __forceinline__ Node coord(const ElemArgs<Real>& A, int h) const {
-        if constexpr (DJG_WIN_XGLOBAL) return RT<Real>::load_node(A.X + xbase[h]);
-        else return wx[h];
-    }
+    __device__ __forceinline__ Node coord(const ElemArgs<Real>&, int h) const { return wx[h]; }
     __device__ __forceinline__ typename RT<Real>::Plane plane(int p) const { return srec[p * TILE + i]; }
     __device__ __forceinline__ Real tail(int t) const { return stail[t * TILE + i]; }
     template <int N, int RB>
@@ -1260,7 +1226,6 @@ struct WinSrc {
     __device__ __forceinline__ int slot(const int* __restrict__, int a, int, int) const {
         return reinterpret_cast<const int*>(sslot + (a >> 2) * TILE + i)[a & 3];
     }
-    const int* xbase;                      // (A/B DJG_WIN_XGLOBAL) unused otherwise
 };
 
 // Inputs of a tile that did not fit a window: connectivity staged in the
@@ -1323,15 +1288,8 @@ __global__ void __launch_bounds__(kPipeThreads, (kPipeMinBlocks<Real, KIND, MODE
     if (tid >= kPipeTile) {  // producer warp
         const int lane = tid - kPipeTile;
         const unsigned long long pol = l2_evict_first_policy();
-        unsigned long long wpol;
-        if constexpr (DJG_WIN_POL == 1)
-            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(wpol));
-        else if constexpr (DJG_WIN_POL == 2)
-            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 0.5;" : "=l"(wpol));
-        else if constexpr (DJG_WIN_POL == 3)
-            asm volatile("createpolicy.fractional.L2::evict_unchanged.b64 %0, 1.0;" : "=l"(wpol));
-        else
-            asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(wpol));
+        unsigned long long wpol;  // (evict_last measured no better: profiles/r02)
+        asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(wpol));
         // Descriptors are read kWinAhead tiles ahead (registers), so their
         // HBM latency overlaps the empty-barrier waits instead of delaying
         // the tile's copies. Every lane reads the run count and window
@@ -1365,10 +1323,7 @@ __global__ void __launch_bounds__(kPipeThreads, (kPipeMinBlocks<Real, KIND, MODE
             for (int k = 0; k + 1 < kWinAhead; ++k) dq[k] = dq[k + 1];
             dq[kWinAhead - 1] = desc_of(it + kWinAhead);
             // all lanes wait (a converged warp: no collective emulation below)
-            if (it >= STAGES) {
-                if constexpr (DJG_WIN_SLEEP > 0) mbar_wait_sleep(empty + s, unsigned((it / STAGES - 1) & 1), DJG_WIN_SLEEP);
-                else mbar_wait(empty + s, unsigned((it / STAGES - 1) & 1));
-            }
+            if (it >= STAGES) mbar_wait(empty + s, unsigned((it / STAGES - 1) & 1));
             const long long eb = e0 + (blockIdx.x + it * G) * kPipeTile;
             const unsigned n = unsigned(min((long long)kPipeTile, e1 - eb));
             const int nruns = dv.nruns, total = dv.total, rstart = dv.rstart, roff = dv.roff, rnext = dv.rnext;
@@ -1419,20 +1374,18 @@ __global__ void __launch_bounds__(kPipeThreads, (kPipeMinBlocks<Real, KIND, MODE
 
     for (long long it = 0; it < nmine; ++it) {
         const int s = int(it % STAGES);
-        if constexpr (DJG_WIN_SLEEP > 0) mbar_wait_sleep(full + s, unsigned((it / STAGES) & 1), DJG_WIN_SLEEP);
-        else mbar_wait(full + s, unsigned((it / STAGES) & 1));
+        mbar_wait(full + s, unsigned((it / STAGES) & 1));
         const long long e = e0 + (blockIdx.x + it * G) * kPipeTile + tid;
         const unsigned char* st = smem + s * WS::kStageBytes;
         const int mode = *reinterpret_cast<const int*>(st + WS::kModeOff);
-        if (DJG_WIN_NULL_COMPUTE && e < e1 && mode < 0) A.ef[0] = Node{};
-        if (!DJG_WIN_NULL_COMPUTE && e < e1) {
+        if (e < e1) {
             const int4* sslot = reinterpret_cast<const int4*>(st + WS::kSlotOff);
             const Plane* srec = reinterpret_cast<const Plane*>(st + WS::kRecOff);
             const Real* stail = reinterpret_cast<const Real*>(st + WS::kTailOff);
             if (mode > 0) {
                 const Node* wu = reinterpret_cast<const Node*>(st + WS::kWinOff);
                 const WinSrc<Real, kPipeTile, WS::NPE, WS::LB> src{sslot, st + WS::kIdxOff, srec, stail, wu,
-                                                                     wu + WS::CAP, tid, nullptr};
+                                                                     wu + WS::CAP, tid};
                 if constexpr (FORM == 2) element_body_tled<Real, KIND, MODEL, 1>(A, e, u, src);
                 else element_body<Real, KIND, MODEL, 1, FORM == 1>(A, e, u, src);
             } else {

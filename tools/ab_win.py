@@ -33,9 +33,10 @@ for label, flags in (("win", A.DJG_FLAG_WINDOW), ("nowin", 0), ("win2", A.DJG_FL
             eng.sync()
             out.append(round(a.elapsed_time(b) / K * 1e3, 1))
         e, n, t = eng.profile_steps(50)
+        status = eng.sync().status
         states[label] = eng.get_state()[0]
         res[label] = dict(graph_us=out, k_element_us=round(e / 50 * 1e3, 1), k_node_us=round(n / 50 * 1e3, 1),
-                          windowed=info["windowed"], window_tiles=info["window_tiles"],
+                          status=status, windowed=info["windowed"], window_tiles=info["window_tiles"],
                           device_gb=round(info["device_bytes"] / 1e9, 2))
 res["bitwise"] = bool(np.array_equal(states["win"], states["nowin"]))
 print(json.dumps(dict(cfg=name, prec=prec, **res)), flush=True)

@@ -57,21 +57,36 @@ def peaks():
     return 6650.0, "fallback"
 
 
+# Kernel sources whose content the committed ncu traffic numbers belong to.
+KERNEL_SOURCES = ("paper_2106_14189_b200/csrc/cuda/kernels.cuh", "paper_2106_14189_b200/csrc/cuda/engine.cu",
+                  "paper_2106_14189_b200/csrc/common/element_math.hpp")
+
+
+def source_hash() -> str:
+    """sha256 (first 16 hex digits) of the kernel sources, as
+    tools/ncu_traffic.py records it next to each capture."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in KERNEL_SOURCES:
+        h.update((ROOT / f).read_bytes())
+    return h.hexdigest()[:16]
+
+
 def measured_traffic(workload: str, kernel_prefix: str):
-    """DRAM bytes per launch of the element kernel from the committed ncu
-    launch list of the same workload (profiles/r01/ncu_traffic.json, made by
+    """DRAM bytes per launch of a kernel from the newest committed ncu launch
+    list of the same workload (profiles/r*/ncu_traffic.json, made by
     tools/ncu_traffic.py from `ncu --metrics dram__bytes_read.sum,
-    dram__bytes_write.sum`), or None."""
-    p = ROOT / "profiles" / "r01" / "ncu_traffic.json"
-    if not p.exists():
-        return None, None
-    d = json.loads(p.read_text()).get(workload)
-    if not d:
-        return None, None
-    for k, v in d["kernels"].items():
-        if k.startswith(kernel_prefix):
-            return v["dram_bytes_per_launch"], f"profiles/r01/{d['source']} ({k}, ncu, per launch)"
-    return None, None
+    dram__bytes_write.sum`): (bytes, source, stale). `stale` is True when the
+    capture's kernel-source hash differs from the sources built here."""
+    for p in sorted((ROOT / "profiles").glob("r*/ncu_traffic.json"), reverse=True):
+        d = json.loads(p.read_text()).get(workload)
+        if not d:
+            continue
+        for k, v in d["kernels"].items():
+            if k.startswith(kernel_prefix):
+                src = f"{p.relative_to(ROOT).parent}/{d['source']} ({k}, ncu, per launch)"
+                return v["dram_bytes_per_launch"], src, d.get("source_hash") != source_hash()
+    return None, None, None
 
 
 def algo_bytes(kind: str, model: str, N: int, E: int, prec: int) -> dict:
@@ -291,6 +306,51 @@ def _cpu_baseline_line(args):
         return {"value": None, "error": str(ex)}
 
 
+def element_kernel_prefix(info) -> str:
+    if info.get("windowed"):
+        return "k_element_win"
+    return "k_element_pipe" if info.get("pipelined") else "k_element<"
+
+
+def sub_config(name: str, device: int, warmup: int = 100, steps: int = 1000) -> dict:
+    """SURVEY §8(d)'s roofline gate on cfg3 / cfg4 (one GPU, f32): graph
+    replay, `warmup` untimed + `steps` timed steps (events on the engine
+    stream), the per-kernel split from profile_steps, the step's fraction of
+    the HBM peak on algorithmic bytes and the element kernel's fraction on the
+    DRAM bytes ncu measured for it (moved_frac)."""
+    import torch
+
+    from paper_2106_14189_b200 import GpuDjEngine, Scenario, config_spec
+    from paper_2106_14189_b200.spec import CONFIGS
+    c = CONFIGS[name]
+    sc = Scenario(config_spec(name, precision=4, target=0.01, ramp_steps=warmup + steps + 200))
+    N, E = sc.num_nodes, sc.num_elements
+    with GpuDjEngine(sc, device=device) as eng:
+        info = eng.info()
+        eng.step(warmup)
+        s = torch.cuda.ExternalStream(eng.stream)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        a.record(s)
+        eng.step_async(steps)
+        b.record(s)
+        b.synchronize()
+        rep = eng.sync()
+        me, mn, _ = eng.profile_steps(100)
+    sc.close()
+    ms = a.elapsed_time(b) / steps
+    hbm, _ = peaks()
+    B = algo_bytes(c["kind"], c["model"], N, E, 4)
+    traffic, src, stale = measured_traffic(name, element_kernel_prefix(info))
+    k1 = me / 100
+    return {"workload": f"{name}: {c['kind']}-{c['model']} unit cube d={c['divisions']}", "num_elements": E,
+            "num_nodes": N, "steps": steps, "warmup": warmup, "status": rep.status, "ms_per_step": ms,
+            "value": E / (ms * 1e-3), "unit": UNIT, "k_element_ms": k1, "k_node_ms": mn / 100,
+            "step_frac": B["step"] / (ms * 1e-3) / 1e9 / hbm, "k_element_frac": B["k_element"] / (k1 * 1e-3) / 1e9 / hbm,
+            "moved_frac": (traffic / (k1 * 1e-3) / 1e9 / hbm) if traffic else None, "traffic": traffic,
+            "traffic_source": src, "traffic_stale": stale}
+
+
 # SURVEY §8(d) config names, keyed by (kind, material, divisions).
 CFG_NAMES = {("T4", "NH", 12): "cfg1", ("H8", "NH", 22): "cfg2", ("T4", "NH", 70): "cfg3",
              ("H8", "TI", 100): "cfg4", ("T4", "NH", 203): "cfg5"}
@@ -416,9 +476,9 @@ def our_arm(args):
     B = algo_bytes(args.kind, args.model, N, E, args.precision)
     k1_ms = ms_e / K
     achieved = B["k_element"] / (k1_ms * 1e-3) / 1e9
-    traffic, traffic_src = None, None
+    traffic, traffic_src, stale = None, None, None
     if cfg_name(args) != "custom" and args.precision == 4:
-        traffic, traffic_src = measured_traffic(cfg_name(args), "k_element_pipe" if info.get("pipelined") else "k_element<")
+        traffic, traffic_src, stale = measured_traffic(cfg_name(args), element_kernel_prefix(info))
     extra = {
         "e2e": {"value": E / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 2 * 3 * N * rbytes,
                 "d2h_bytes_per_step": 3 * N * rbytes, "ms_per_step": e2e_ms,
@@ -434,9 +494,12 @@ def our_arm(args):
         "roofline": {"bound": "hbm", "kernel": "k_element", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm, "traffic": traffic, "traffic_source": traffic_src,
                      "moved_frac": (traffic / (k1_ms * 1e-3) / 1e9 / hbm) if traffic else None,
-                     "note": "achieved/frac use SURVEY §8(d)'s algorithmic bytes (the reference's hot-field "
-                             "set, 12-byte force rows); the compact record moves fewer bytes, so frac can "
-                             "exceed 1. moved_frac = measured DRAM bytes (traffic) / event-timed launch / peak",
+                     "traffic_stale": stale, "source_hash": source_hash(),
+                     "note": "moved_frac is the kernel's efficiency: measured DRAM bytes (traffic, ncu, capture "
+                             "of the same kernel sources unless traffic_stale) / event-timed launch / peak. "
+                             "achieved/frac use SURVEY §8(d)'s algorithmic bytes (the reference's hot-field set, "
+                             "12-byte force rows); the compact record moves fewer bytes, so frac exceeds 1 and "
+                             "is not an efficiency figure",
                      "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": B["k_element"], "launch_ms": k1_ms,
                      "k_node_ms": ms_n / K, "k_node_frac": B["k_node"] / (ms_n / K * 1e-3) / 1e9 / hbm,
@@ -448,6 +511,13 @@ def our_arm(args):
     }
     extra["config"] = None
     line = _line(args, 1, K, W, E, ms_step, value, {k: v for k, v in extra.items() if k != "config"})
+    if args.sub_configs:
+        line["sub_configs"] = {}
+        for name in args.sub_configs.split(","):
+            try:
+                line["sub_configs"][name] = sub_config(name, device)
+            except Exception as ex:  # reported, not fatal
+                line["sub_configs"][name] = {"error": str(ex)}
     line["config"]["num_nodes"] = N
     line["config"]["l2"] = "inputs larger than L2 (state %.1f GB resident)" % (info["device_bytes"] / 1e9)
     eng.close()
@@ -617,6 +687,8 @@ def main():
     ap.add_argument("--tled-steps", type=int, default=100)
     ap.add_argument("--f64-steps", type=int, default=50, help="also time the f64 problem (0: skip)")
     ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--sub-configs", default="cfg3,cfg4",
+                    help="also time these SURVEY configs on one GPU (roofline gate), '' to skip")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="multi-GPU halo / agreement: peer-memory stores from the node kernel (default) or NCCL")

@@ -31,14 +31,19 @@ SMALL = ["--divisions", "24", "--steps", "40", "--warmup", "3", "--e2e-steps", "
 
 
 def test_bench_single_gpu_line():
-    line = _run([sys.executable, "bench.py", *SMALL, "--cpu-steps", "2"])
+    line = _run([sys.executable, "bench.py", *SMALL, "--cpu-steps", "2", "--sub-configs", "cfg1,cfg2"])
     assert KEYS <= set(line) and line["n_gpus"] == 1 and line["value"] > 0
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
     assert line["e2e"]["value"] < line["value"]
     r = line["roofline"]
     assert r["bound"] == "hbm" and r["peak"] > 0 and r["achieved"] > 0
     assert line["gpu_launches"] == 2 * 40 and line["clocks"]["samples"] > 0
-    assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["value"] > 0
+    cb = line["cpu_baseline"]
+    assert cb["kind"] == "reference" and cb["value"] > 0 and cb["same_config"] and cb["threads_1"]["cores"] == 1
+    assert r["traffic_stale"] in (None, True, False) and len(r["source_hash"]) == 16
+    for name in ("cfg1", "cfg2"):
+        sub = line["sub_configs"][name]
+        assert sub["status"] == 0 and sub["ms_per_step"] > 0 and sub["step_frac"] > 0, sub
     assert line["tled"]["status"] == 0
     assert line["f64"]["status"] == 0 and line["f64"]["ms_per_step"] > 0
     assert line["e2e_run"]["value"] > 0 and line["e2e_run"]["steps"] == 40
@@ -60,6 +65,9 @@ def test_bench_multi_gpu_arm_one_rank():
 
 
 def test_bench_reference_arm():
-    line = _run([sys.executable, "bench.py", "--impl", "reference", "--steps", "3", "--warmup", "1"])
+    line = _run([sys.executable, "bench.py", "--impl", "reference", "--divisions", "24", "--steps", "3",
+                 "--warmup", "1"])
     assert line["impl"] == "reference" and line["value"] > 0 and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0
+    assert line["same_config"] and line["config"]["divisions"] == 24 and line["steps"] == 3 and line["warmup"] == 3
+    assert line["threads_1"]["value"] > 0 and line["tled"]["value"] > 0

@@ -1,7 +1,13 @@
 """Summarise an ncu launch list (gpu__time_duration, dram__bytes_read/write
 per launch) into profiles/<round>/ncu_traffic.json: per kernel, the mean
-DRAM bytes and duration per launch. bench.py reports the element kernel's
-entry as roofline.traffic."""
+DRAM bytes and duration per launch, tagged with the hash of the kernel
+sources the capture ran (bench.source_hash; run this on the GPU box right
+after the capture, or here before editing a kernel). bench.py reports the
+element kernel's entry as roofline.traffic and flags it stale when the
+sources changed since.
+
+  python tools/ncu_traffic.py profiles/r02/ncu_traffic.json cfg5=launches_cfg5.csv ...
+(existing entries of other configs in the destination are kept)"""
 import collections
 import csv
 import json
@@ -27,10 +33,12 @@ def summarise(path):
 
 
 if __name__ == "__main__":
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    from bench import source_hash
     dst = Path(sys.argv[1])
-    res = {}
+    res = json.loads(dst.read_text()) if dst.exists() else {}
     for spec in sys.argv[2:]:
         cfg, path = spec.split("=", 1)
-        res[cfg] = {"source": Path(path).name, "kernels": summarise(path)}
+        res[cfg] = {"source": Path(path).name, "source_hash": source_hash(), "kernels": summarise(path)}
     dst.write_text(json.dumps(res, indent=1) + "\n")
     print(json.dumps(res, indent=1))

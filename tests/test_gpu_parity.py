@@ -276,6 +276,29 @@ def test_cfg5_full_size_bitwise():
 
 
 @pytest.mark.slow
+@pytest.mark.parametrize("load", ["extension", "compression"])
+def test_cfg5_soak_550_steps(load):
+    """SURVEY §8(d)'s cfg5 protocol length on the full 50,192,562-tet mesh
+    against the CPU oracle on the host cores: the +1 % extension ramp for all
+    550 steps, bit-identical (u and u_prev); the 20 % compression ramp, which
+    inverts elements at step 118 -- same abort step, same first inverted
+    element and count, same retained state."""
+    if load == "extension":
+        spec = config_spec("cfg5", precision=4, target=0.01, ramp_steps=550)
+    else:
+        spec = config_spec("cfg5", precision=4)
+    u, up, rep = run_gpu(spec, 550)
+    ur, upr, rr = oracle.run(spec, 550, "oracle")
+    assert (rep.status, rep.step, rep.first_inverted, rep.inverted_count) == \
+        (rr["status"], rr["step"], rr["first_inverted"], rr["inverted_count"]), (rep, rr)
+    if load == "compression":
+        assert rr["status"] == A.DJG_E_INVERSION and rr["fail_step"] == 118
+    else:
+        assert rr["status"] == 0 and rr["step"] == 550
+    assert np.array_equal(u, ur) and np.array_equal(up, upr)
+
+
+@pytest.mark.slow
 def test_cfg4_first_100_steps():
     """configs[3] at full size (1,000,000 H8 TI): first 100 steps vs the oracle."""
     check_run(config_spec("cfg4", precision=4, ramp_steps=1100), 100)

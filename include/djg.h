@@ -214,13 +214,24 @@ int djg_profile_steps(djg_engine* eng, int64_t nsteps, float* ms_element, float*
  *   djg_halo_pack(eng, send)            owned nodes others reference -> send
  *   <exchange send/recv with the neighbors>
  *   djg_halo_unpack(eng, recv)          recv -> ghost nodes
- *   djg_step_status(eng, status)        int64[2] failure summary of this part
- *   <allreduce MAX of status over parts>
+ *   djg_step_status(eng, status)        int64[3] step summary of this part
+ *   <allreduce over parts: MAX of words 0-1, SUM of word 2>
  *   djg_step_agree(eng, reduced)        every part halts at the same state
+ * status[0]: 2 inversion halt, 1 divergence, 0 none; status[1]: -(global id
+ * of the first inverted element) or INT64_MIN; status[2]: inverted elements
+ * this part reports for the step (its own elements only, see
+ * djg_set_counted_elements) -- the reduced sum is the step's global count,
+ * accumulated by djg_step_agree into the report's inverted_count /
+ * inverted_steps on every part.
  * Halo buffers hold one 16-byte (f32) / 32-byte (f64) node record per entry.
  */
 int djg_set_partition(djg_engine* eng, int64_t num_owned, const int64_t* elem_l2g);
 int djg_set_halo(djg_engine* eng, int64_t nsend, const int32_t* send_nodes, int64_t nrecv, const int32_t* recv_nodes);
+/* Multi-part inversion counting: counted[e] = 1 for the local elements this
+ * part reports (djg_partition_owned_elements), 0 for ghost copies, so every
+ * inverted element is counted once over all parts. Without it a part counts
+ * every element it computes. */
+int djg_set_counted_elements(djg_engine* eng, const uint8_t* counted);
 int djg_halo_pack(djg_engine* eng, void* dev_send);
 int djg_halo_unpack(djg_engine* eng, const void* dev_recv);
 int djg_step_status(djg_engine* eng, int64_t* dev_status);
@@ -254,18 +265,22 @@ int djg_comm_unique_id(void* id128);
  *   djg_peer_ipc_export  their CUDA IPC handles (4 x 64 bytes), for other ranks
  *   djg_peer_ipc_open    map another rank's 4 handles -> 4 device pointers
  *   djg_peer_setup       every part's pointers (peer_u: 3 per part, peer_mail:
- *                        1 per part, own included) and this part's halo
- *                        destinations: owned node dest_node[i] -> part
- *                        dest_part[i], local node dest_index[i]
+ *                        1 per part, own included), every part's local node
+ *                        count (peer_num_nodes: the destination bounds) and
+ *                        this part's halo destinations: owned node
+ *                        dest_node[i] -> part dest_part[i], local node
+ *                        dest_index[i] < peer_num_nodes[dest_part[i]]
  * Then djg_step runs element kernel -> node kernel with peer stores ->
- * wait/agree per step, graph-captured. djg_step_peer_local /
+ * wait/agree per step, graph-captured. The wait is bounded: a part whose
+ * peers do not post within DJG_PEER_TIMEOUT_MS (default 10 s) halts with
+ * DJG_E_PEER instead of spinning forever. djg_step_peer_local /
  * djg_step_peer_agree split one step for single-device emulation. */
 int djg_peer_export(djg_engine* eng, void** ptrs4);
 int djg_peer_ipc_export(djg_engine* eng, void* handles);
 int djg_peer_ipc_open(djg_engine* eng, const void* handles, void** ptrs4);
 int djg_peer_setup(djg_engine* eng, int32_t nparts, int32_t part, const void* const* peer_u,
-                   const void* const* peer_mail, int64_t ndest, const int32_t* dest_node, const int32_t* dest_part,
-                   const int32_t* dest_index);
+                   const void* const* peer_mail, const int64_t* peer_num_nodes, int64_t ndest,
+                   const int32_t* dest_node, const int32_t* dest_part, const int32_t* dest_index);
 int djg_step_peer_local(djg_engine* eng);
 int djg_step_peer_agree(djg_engine* eng);
 int djg_set_interior(djg_engine* eng, int64_t num_interior);

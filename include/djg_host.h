@@ -94,6 +94,10 @@ int djg_partition_halo(const djg_partition* p, int32_t* neighbors, int64_t* send
                        int32_t* send_nodes, int32_t* recv_nodes);
 /* Local -> global ids: node_l2g[num_nodes], elem_l2g[num_elements]. */
 int djg_partition_maps(const djg_partition* p, int64_t* node_l2g, int64_t* elem_l2g);
+/* Per local element: 1 if the partitioner assigned it to this part (it
+ * reports that element's inversions, djg_set_counted_elements), 0 for the
+ * ghost copies of other parts' elements. */
+int djg_partition_owned_elements(const djg_partition* p, uint8_t* owned);
 /* Element -> part assignment of the whole scenario (E entries). */
 int djg_element_parts(const djg_scenario* sc, int32_t nparts, int32_t* part);
 int djg_element_parts_method(const djg_scenario* sc, int32_t nparts, int32_t method, int32_t* part);

@@ -56,7 +56,10 @@ enum djg_status {
     DJG_E_CONFIG = 2,     /* kConfig: ConfigError / MeshError / bad descriptor */
     DJG_E_CUDA = 3,       /* CUDA runtime failure (no reference analogue) */
     DJG_E_INVERSION = 4,  /* kInversion: SimulationError::ElementInversion */
-    DJG_E_DIVERGENCE = 5  /* kDivergence: SimulationError::Divergence */
+    DJG_E_DIVERGENCE = 5, /* kDivergence: SimulationError::Divergence */
+    DJG_E_PEER = 6        /* peer-memory step: a part did not post its step within the
+                             wait limit (DJG_PEER_TIMEOUT_MS, default 10000); no reference
+                             analogue -- the engine halts instead of hanging the GPU */
 };
 
 /* Material<Real> (material.hpp:140-230). Only the fields of `model` are read. */

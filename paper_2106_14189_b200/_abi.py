@@ -20,7 +20,7 @@ DJG_T4, DJG_H8 = 0, 1
 DJG_NH, DJG_TI, DJG_OT, DJG_MR, DJG_I57 = 0, 1, 2, 3, 4
 DJG_ABORT, DJG_SKIP_AND_REPORT = 0, 1
 DJG_FREE, DJG_FIXED, DJG_PRESCRIBED = 0, 1, 2
-DJG_OK, DJG_E_INTERNAL, DJG_E_CONFIG, DJG_E_CUDA, DJG_E_INVERSION, DJG_E_DIVERGENCE = 0, 1, 2, 3, 4, 5
+DJG_OK, DJG_E_INTERNAL, DJG_E_CONFIG, DJG_E_CUDA, DJG_E_INVERSION, DJG_E_DIVERGENCE, DJG_E_PEER = 0, 1, 2, 3, 4, 5, 6
 DJG_FLAG_NO_GRAPH = 1
 DJG_FLAG_SLABS = 2
 DJG_FLAG_NO_DISCARD = 4
@@ -168,14 +168,16 @@ def ptr(a: np.ndarray | None):
     """void* of a C-contiguous numpy array (None -> NULL)."""
     if a is None:
         return None
-    assert a.flags["C_CONTIGUOUS"], "array must be C-contiguous"
+    if not a.flags["C_CONTIGUOUS"]:  # explicit check: `python -O` strips asserts
+        raise ValueError("array must be C-contiguous")
     return a.ctypes.data_as(C.c_void_p)
 
 
 def typed_ptr(a: np.ndarray | None, ctype):
     if a is None:
         return None
-    assert a.flags["C_CONTIGUOUS"]
+    if not a.flags["C_CONTIGUOUS"]:
+        raise ValueError("array must be C-contiguous")
     return a.ctypes.data_as(C.POINTER(ctype))
 
 
@@ -206,8 +208,8 @@ EXPORTS = [
     ("djg_peer_export", C.c_int, [C.c_void_p, C.c_void_p]),
     ("djg_peer_ipc_export", C.c_int, [C.c_void_p, C.c_void_p]),
     ("djg_peer_ipc_open", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
-    ("djg_peer_setup", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p,
-                                 C.c_void_p, C.c_void_p]),
+    ("djg_peer_setup", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                 C.c_void_p, C.c_void_p, C.c_void_p]),
     ("djg_step_peer_local", C.c_int, [C.c_void_p]),
     ("djg_step_peer_agree", C.c_int, [C.c_void_p]),
     ("djg_step_interior", C.c_int, [C.c_void_p]),
@@ -219,6 +221,7 @@ EXPORTS = [
     ("djg_debug_cbrt", C.c_int, [C.c_int32, C.c_void_p, C.c_void_p, C.c_int64, C.c_int32]),
     ("djg_set_partition", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p]),
     ("djg_set_halo", C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_void_p]),
+    ("djg_set_counted_elements", C.c_int, [C.c_void_p, C.c_void_p]),
     ("djg_halo_pack", C.c_int, [C.c_void_p, C.c_void_p]),
     ("djg_halo_unpack", C.c_int, [C.c_void_p, C.c_void_p]),
     ("djg_step_status", C.c_int, [C.c_void_p, C.c_void_p]),
@@ -231,6 +234,7 @@ EXPORTS = [
     ("djg_partition_image", C.c_int, [C.c_void_p, _P(djg_image_ptrs)]),
     ("djg_partition_halo", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     ("djg_partition_maps", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    ("djg_partition_owned_elements", C.c_int, [C.c_void_p, C.c_void_p]),
     ("djg_element_parts", C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     ("djg_element_parts_method", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
     ("djg_last_error", C.c_char_p, [C.c_void_p]),

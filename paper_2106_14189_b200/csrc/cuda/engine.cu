@@ -184,6 +184,7 @@ public:
     virtual void set_policy(int policy) = 0;
     virtual void set_partition(int64_t num_owned, const int64_t* elem_l2g) = 0;
     virtual void set_halo(int64_t nsend, const int32_t* send, int64_t nrecv, const int32_t* recv) = 0;
+    virtual void set_counted_elements(const uint8_t* counted) = 0;
     virtual void halo_pack(void* dev_out) = 0;
     virtual void halo_unpack(const void* dev_in) = 0;
     virtual void step_status(int64_t* dev_status) = 0;
@@ -194,8 +195,9 @@ public:
     virtual void peer_export(void** ptrs) = 0;
     virtual void peer_ipc_export(void* handles) = 0;
     virtual void peer_ipc_open(const void* handles, void** ptrs) = 0;
-    virtual void peer_setup(int nparts, int part, const void* const* peer_u, const void* const* peer_mail, int64_t ndest,
-                            const int32_t* dest_node, const int32_t* dest_part, const int32_t* dest_index) = 0;
+    virtual void peer_setup(int nparts, int part, const void* const* peer_u, const void* const* peer_mail,
+                            const int64_t* peer_num_nodes, int64_t ndest, const int32_t* dest_node,
+                            const int32_t* dest_part, const int32_t* dest_index) = 0;
     virtual void step_peer_local() = 0;
     virtual int advance_host(const void* u, const void* up, int64_t step, void* u_next, djg_report* rep) = 0;
     virtual void step_peer_agree() = 0;
@@ -683,6 +685,22 @@ public:
         drop_graphs();
     }
 
+    // Multi-part inversion counting (djg_set_counted_elements): only this
+    // part's own elements are counted; the parts' step counts are summed by
+    // the agreement (k_agree / k_wait_agree) into every part's totals.
+    void set_counted_elements(const uint8_t* counted) override {
+        if (!counted) throw DescError("counted elements missing");
+        counted_.alloc(size_t(E_));
+        CK(cudaMemcpy(counted_.p, counted, size_t(E_), cudaMemcpyHostToDevice));
+        ea_.counted = counted_.as<unsigned char>();
+        multipart_ = true;
+        read_ctrl();
+        hctrl_->multipart = 1;
+        CK(cudaMemcpyAsync(ctrl_.p, hctrl_, sizeof(Ctrl), cudaMemcpyHostToDevice, stream_));
+        CK(cudaStreamSynchronize(stream_));
+        drop_graphs();
+    }
+
     void set_halo(int64_t nsend, const int32_t* send, int64_t nrecv, const int32_t* recv) override {
         auto up = [&](DevBuf& b, int64_t n, const int32_t* v) {
             for (int64_t i = 0; i < n; ++i)
@@ -759,7 +777,7 @@ public:
         }
         sendBuf_.alloc(size_t(std::max<int64_t>(nsend_, 1)) * sizeof(Node));
         recvBuf_.alloc(size_t(std::max<int64_t>(nrecv_, 1)) * sizeof(Node));
-        status_.alloc(2 * sizeof(int64_t));
+        status_.alloc(3 * sizeof(int64_t));
         drop_graphs();
     }
 
@@ -791,6 +809,7 @@ public:
         }
         k_step_status<<<1, 1, 0, s>>>(ctrl_.as<Ctrl>(), elemL2g_.as<long long>(), status_.as<long long>());
         NK(api.all_reduce(status_.p, status_.p, 2, ncclInt64, ncclMax, c, s));
+        NK(api.all_reduce(status_.as<long long>() + 2, status_.as<long long>() + 2, 1, ncclInt64, ncclSum, c, s));
         k_agree<<<1, 1, 0, s>>>(ctrl_.as<Ctrl>(), status_.as<long long>());
         CK(cudaGetLastError());
     }
@@ -824,6 +843,8 @@ public:
 
     void step_interior() override {
         if (!configured_) throw DescError("step data not configured (djg_configure_step)");
+        // a step starts here: sync() reports from this point (as djg_step_async)
+        CK(cudaMemcpyAsync(hstart_, ctrl_.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream_));
         launch_element(stream_, 0, split_point());
     }
 
@@ -858,6 +879,7 @@ public:
         launch_node(s, 0, false);
         k_step_status<<<1, 1, 0, s>>>(ctrl_.as<Ctrl>(), elemL2g_.as<long long>(), status_.as<long long>());
         NK(api.all_reduce(status_.p, status_.p, 2, ncclInt64, ncclMax, c, s));
+        NK(api.all_reduce(status_.as<long long>() + 2, status_.as<long long>() + 2, 1, ncclInt64, ncclSum, c, s));
         k_agree<<<1, 1, 0, s>>>(ctrl_.as<Ctrl>(), status_.as<long long>());
         CK(cudaGetLastError());
     }
@@ -885,15 +907,20 @@ public:
         }
     }
 
-    void peer_setup(int nparts, int part, const void* const* peer_u, const void* const* peer_mail, int64_t ndest,
-                    const int32_t* dest_node, const int32_t* dest_part, const int32_t* dest_index) override {
+    void peer_setup(int nparts, int part, const void* const* peer_u, const void* const* peer_mail,
+                    const int64_t* peer_num_nodes, int64_t ndest, const int32_t* dest_node, const int32_t* dest_part,
+                    const int32_t* dest_index) override {
         if (!elemL2g_.p || !mailbox_.p) throw DescError("djg_peer_setup needs djg_set_partition with elem_l2g first");
         if (nparts < 1 || nparts > kMaxParts || part < 0 || part >= nparts) throw DescError("invalid part count / index");
+        if (!peer_num_nodes || peer_num_nodes[part] != N_) throw DescError("peer node counts missing or inconsistent");
         const int64_t no = na_.N;
         std::vector<int32_t> off(size_t(no) + 1, 0);
         for (int64_t i = 0; i < ndest; ++i) {
             if (dest_node[i] < 0 || dest_node[i] >= no) throw DescError("halo destination of a non-owned node");
             if (dest_part[i] < 0 || dest_part[i] >= nparts || dest_part[i] == part) throw DescError("invalid peer part");
+            // the node kernel stores through peer_u[dest_part] + dest_index: keep it inside that buffer
+            if (dest_index[i] < 0 || dest_index[i] >= peer_num_nodes[dest_part[i]])
+                throw DescError("halo destination index outside the peer's node range");
             off[size_t(dest_node[i]) + 1]++;
         }
         for (int64_t n = 0; n < no; ++n) off[size_t(n) + 1] += off[size_t(n)];
@@ -915,6 +942,7 @@ public:
         pa_.nparts = nparts;
         pa_.part = part;
         peer_ = true;
+        if (const char* v = std::getenv("DJG_PEER_TIMEOUT_MS")) peer_timeout_ns_ = std::strtoull(v, nullptr, 10) * 1000000ull;
         drop_graphs();
     }
 
@@ -927,13 +955,14 @@ public:
     }
 
     void launch_peer_agree(cudaStream_t s) {
-        k_wait_agree<<<1, 32, 0, s>>>(ctrl_.as<Ctrl>(), mailbox_.as<Mailbox>(), pa_.nparts);
+        k_wait_agree<<<1, 32, 0, s>>>(ctrl_.as<Ctrl>(), mailbox_.as<Mailbox>(), pa_.nparts, peer_timeout_ns_);
         CK(cudaGetLastError());
     }
 
     void step_peer_local() override {
         if (!peer_) throw DescError("djg_peer_setup first");
         if (!configured_) throw DescError("step data not configured (djg_configure_step)");
+        CK(cudaMemcpyAsync(hstart_, ctrl_.p, sizeof(Ctrl), cudaMemcpyDeviceToHost, stream_));  // (see step_interior)
         launch_peer_local(stream_);
     }
 
@@ -1144,6 +1173,7 @@ public:
         ctrl_initialized_ = true;
         Ctrl c{};
         c.epoch = epoch;
+        c.multipart = multipart_ ? 1 : 0;
         c.step = step;
         c.first_inv = kNone;
         c.asm_first = kNone;
@@ -1244,6 +1274,7 @@ public:
         {
             Ctrl c{};
             c.epoch = ctrl_initialized_ ? hctrl_->epoch : 0u;
+            c.multipart = multipart_ ? 1 : 0;
             c.step = step;
             c.first_inv = kNone;
             c.asm_first = kNone;
@@ -1737,13 +1768,15 @@ private:
     int device_ = 0;
     std::vector<int32_t> nbr_;
     std::vector<int64_t> send_off_, recv_off_;
-    DevBuf sendBuf_, recvBuf_, status_;
+    DevBuf sendBuf_, recvBuf_, status_, counted_;
+    bool multipart_ = false;           // djg_set_counted_elements given: totals from the agreement
     int64_t interior_ = -1;            // split step: local elements [0, interior_) touch no ghost node
     int pipe_spare_sms_ = 0;           // SMs the pipelined element kernel leaves free
     static constexpr int kSpareSms = 4;
     cudaStream_t side_ = nullptr;      // interior elements of the overlapped step
     cudaEvent_t evFork_ = nullptr, evJoin_ = nullptr;
     bool peer_ = false;                // peer-memory multi-GPU step
+    unsigned long long peer_timeout_ns_ = 10000000000ull;  // k_wait_agree's bound (DJG_PEER_TIMEOUT_MS)
     cudaEvent_t evPrev_ = nullptr;     // djg_advance_host: u_prev uploaded
     DevBuf flat2_, allSlices_;
     std::vector<cudaEvent_t> evChunk_;
@@ -1950,6 +1983,13 @@ int djg_set_halo(djg_engine* eng, int64_t nsend, const int32_t* send_nodes, int6
     });
 }
 
+int djg_set_counted_elements(djg_engine* eng, const uint8_t* counted) {
+    return guarded(eng, [&](djg::EngineBase& e) {
+        e.set_counted_elements(counted);
+        return DJG_OK;
+    });
+}
+
 int djg_halo_pack(djg_engine* eng, void* dev_send) {
     return guarded(eng, [&](djg::EngineBase& e) {
         e.halo_pack(dev_send);
@@ -2062,10 +2102,10 @@ int djg_peer_ipc_open(djg_engine* eng, const void* handles, void** ptrs4) {
 }
 
 int djg_peer_setup(djg_engine* eng, int32_t nparts, int32_t part, const void* const* peer_u,
-                   const void* const* peer_mail, int64_t ndest, const int32_t* dest_node, const int32_t* dest_part,
-                   const int32_t* dest_index) {
+                   const void* const* peer_mail, const int64_t* peer_num_nodes, int64_t ndest,
+                   const int32_t* dest_node, const int32_t* dest_part, const int32_t* dest_index) {
     return guarded(eng, [&](djg::EngineBase& e) {
-        e.peer_setup(nparts, part, peer_u, peer_mail, ndest, dest_node, dest_part, dest_index);
+        e.peer_setup(nparts, part, peer_u, peer_mail, peer_num_nodes, ndest, dest_node, dest_part, dest_index);
         return DJG_OK;
     });
 }

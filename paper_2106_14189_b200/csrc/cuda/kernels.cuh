@@ -112,6 +112,8 @@ struct Ctrl {
     unsigned long long asm_count;
     unsigned int epoch;             // fused step: launches completed (flag stamps)
     int ticket;                     // fused step: next work-list item
+    int multipart;                  // 1: totals accumulate the parts' summed counts (k_agree)
+    unsigned long long step_inv;    // counted inversions of the last closed step (k_step_status)
 };
 
 constexpr unsigned long long kNone = ~0ull;
@@ -162,6 +164,8 @@ struct ElemArgs {
     const int* wdesc;                    // node windows: kWinDesc ints per 128-element tile, or NULL
     const long long* elem_l2g;           // multi-part: global id of each local element (inversions
                                          // are reported in global ids), else NULL
+    const unsigned char* counted;        // multi-part: 1 for the elements whose inversions this part
+                                         // counts (its own; ghosts are counted by their owner), or NULL
     const typename RT<Real>::Plane* c;   // nplanes planes of Plane[E]
     const Real* ctail;                   // record remainder planes (compact T4): Real[tail_stride]
     long long tail_stride;
@@ -540,7 +544,7 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
 
     if (!(det > Real(0))) {
         // record_inversion (djtled_force.hpp:107-112) + zeroed rows (:187-191).
-        atomicAdd(&A.ctrl->inv_count, 1ull);
+        if (!A.counted || A.counted[e]) atomicAdd(&A.ctrl->inv_count, 1ull);
         atomicMin(&A.ctrl->first_inv, (unsigned long long)(A.elem_l2g ? A.elem_l2g[e] : e));
 #pragma unroll
         for (int a = 0; a < NPE; ++a) store_row(A, sl[a], Real(0), Real(0), Real(0));
@@ -811,7 +815,7 @@ __device__ __forceinline__ void element_body_tled(const ElemArgs<Real>& A, const
     // deformation_state (tled_force.hpp:39-48)
     const Real J = em::det3(X);
     if (!(J > Real(0))) {
-        atomicAdd(&A.ctrl->inv_count, 1ull);
+        if (!A.counted || A.counted[e]) atomicAdd(&A.ctrl->inv_count, 1ull);
         atomicMin(&A.ctrl->first_inv, (unsigned long long)(A.elem_l2g ? A.elem_l2g[e] : e));
 #pragma unroll
         for (int a = 0; a < NPE; ++a) store_row(A, sl[a], Real(0), Real(0), Real(0));
@@ -1578,8 +1582,11 @@ __device__ __forceinline__ void close_step(Ctrl* ctrl, long long step, int polic
         ctrl->asm_count = cnt;
     } else {
         const int div = atomicOr(&ctrl->diverged, 0);
-        ctrl->total_inv += cnt;
-        if (cnt > 0) ctrl->inv_steps += 1;
+        if (!ctrl->multipart) {
+            ctrl->total_inv += cnt;
+            if (cnt > 0) ctrl->inv_steps += 1;
+        }
+        ctrl->step_inv = cnt;
         if (first != kNone && policy == 0) {
             ctrl->halted = 4;  // DJG_E_INVERSION: state stays at the last good step
             ctrl->halt_first_inv = (long long)first;
@@ -1662,8 +1669,11 @@ __global__ void __launch_bounds__(256) k_node(const NodeArgs<Real> A) {
         ctrl->asm_count = cnt;
     } else {
         const int div = atomicOr(&ctrl->diverged, 0);
-        ctrl->total_inv += cnt;
-        if (cnt > 0) ctrl->inv_steps += 1;
+        if (!ctrl->multipart) {
+            ctrl->total_inv += cnt;
+            if (cnt > 0) ctrl->inv_steps += 1;
+        }
+        ctrl->step_inv = cnt;
         if (skip) {
             ctrl->halted = 4;  // DJG_E_INVERSION
             ctrl->halt_first_inv = (long long)first;
@@ -1766,18 +1776,31 @@ __global__ void k_halo_unpack(const Ctrl* ctrl, typename RT<Real>::Node* u0, typ
 // element) or INT64_MIN. Reduced with MAX over parts, then k_agree applies the
 // global outcome: parts that did advance roll back one step (their previous
 // two buffers are intact), so every part halts at the same state.
-__global__ void k_step_status(const Ctrl* ctrl, const long long* __restrict__ elem_l2g, long long* status) {
+// status[2]: the inversions this part counted in the step (its own elements
+// only), summed over parts; k_agree accumulates the sum into every part's
+// totals, so all parts report the global count of the single-GPU run.
+__global__ void k_step_status(Ctrl* ctrl, const long long* __restrict__ elem_l2g, long long* status) {
     const int h = ctrl->halted;
     const long long none = -0x7fffffffffffffffll - 1;
     status[0] = h == 4 ? 2 : (h == 5 ? 1 : 0);
     (void)elem_l2g;  // inversions are recorded in global ids already (ElemArgs::elem_l2g)
     if (h != 4 || ctrl->halt_first_inv < 0) status[1] = none;
     else status[1] = -ctrl->halt_first_inv;
+    status[2] = (long long)ctrl->step_inv;
+    ctrl->step_inv = 0;  // (a halted part runs no more steps: it contributes 0 from now on)
+}
+
+__device__ __forceinline__ void accumulate_counts(Ctrl* ctrl, long long global_count) {
+    if (!ctrl->multipart) return;
+    ctrl->total_inv += (unsigned long long)global_count;
+    if (global_count > 0) ctrl->inv_steps += 1;
 }
 
 __global__ void k_agree(Ctrl* ctrl, const long long* __restrict__ reduced) {
     const long long code = reduced[0];
-    if (code == 0 || ctrl->agreed) return;
+    if (ctrl->agreed) return;
+    accumulate_counts(ctrl, reduced[2]);
+    if (code == 0) return;
     if (ctrl->halted == 0) {
         ctrl->step -= 1;  // this part advanced; another one failed the same step
         ctrl->fail_step = ctrl->step + 1;
@@ -1801,7 +1824,7 @@ constexpr int kMaxParts = 64;
 
 struct Mailbox {
     unsigned long long flag[kMaxParts];  // last epoch each part closed
-    long long status[2][kMaxParts][2];   // by epoch parity: {code, -global first inverted}
+    long long status[2][kMaxParts][3];   // by epoch parity: {code, -global first inverted, counted inversions}
 };
 
 template <class Real>
@@ -1857,10 +1880,13 @@ __global__ void __launch_bounds__(256) k_node_peer(const NodeArgs<Real> A, const
     const unsigned long long epoch = ++ctrl->epoch;
     const long long code = ctrl->halted == 4 ? 2 : (ctrl->halted == 5 ? 1 : 0);
     const long long first = code == 2 ? -ctrl->halt_first_inv : (-0x7fffffffffffffffll - 1);
+    const long long counted = (long long)ctrl->step_inv;
+    ctrl->step_inv = 0;
     for (int q = 0; q < P.nparts; ++q) {
         Mailbox* m = P.peer_mail[q];
         m->status[epoch & 1][P.part][0] = code;
         m->status[epoch & 1][P.part][1] = first;
+        m->status[epoch & 1][P.part][2] = counted;
     }
     __threadfence_system();
     for (int q = 0; q < P.nparts; ++q) st_release_sys(&P.peer_mail[q]->flag[P.part], epoch);
@@ -1869,18 +1895,38 @@ __global__ void __launch_bounds__(256) k_node_peer(const NodeArgs<Real> A, const
 
 // Waits until every part closed this part's last epoch, then agrees on the
 // outcome exactly like k_agree (all parts halt at the same state).
-__global__ void k_wait_agree(Ctrl* ctrl, const Mailbox* __restrict__ own, int nparts) {
+// The wait is bounded by `timeout_ns` (%globaltimer): a part that never
+// posts (dead or stuck rank) halts this one with DJG_E_PEER (6) instead of
+// leaving a kernel spinning on the GPU.
+__device__ __forceinline__ unsigned long long global_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__global__ void k_wait_agree(Ctrl* ctrl, const Mailbox* __restrict__ own, int nparts, unsigned long long timeout_ns) {
     if (threadIdx.x != 0) return;
     if (ctrl->agreed) return;  // halted and agreed in an earlier step: nothing ran since
     const unsigned long long epoch = ctrl->epoch;
     if (epoch == 0) return;
+    const unsigned long long t0 = global_ns();
     for (int q = 0; q < nparts; ++q)
-        while (ld_acquire_sys(&own->flag[q]) < epoch) __nanosleep(64);
-    long long code = 0, first = -0x7fffffffffffffffll - 1;
+        while (ld_acquire_sys(&own->flag[q]) < epoch) {
+            if (global_ns() - t0 > timeout_ns) {
+                ctrl->halted = 6;  // DJG_E_PEER
+                ctrl->fail_step = ctrl->step + 1;
+                ctrl->agreed = 1;
+                return;
+            }
+            __nanosleep(256);
+        }
+    long long code = 0, first = -0x7fffffffffffffffll - 1, counted = 0;
     for (int q = 0; q < nparts; ++q) {
         code = max(code, own->status[epoch & 1][q][0]);
         first = max(first, own->status[epoch & 1][q][1]);
+        counted += own->status[epoch & 1][q][2];
     }
+    accumulate_counts(ctrl, counted);
     if (code == 0) return;
     if (ctrl->halted == 0) {
         ctrl->step -= 1;  // this part advanced; another one failed the same step

@@ -798,6 +798,8 @@ struct PartProblem {
     int64_t num_owned = 0, global_nodes = 0, global_elements = 0, owned_elements = 0;
     int64_t interior_elements = 0;  // local elements [0, interior) reference no ghost node
     std::vector<int64_t> node_l2g, elem_l2g;
+    std::vector<uint8_t> elem_owned;  // per local element: 1 if assigned to this part (it reports the
+                                      // element's inversions; other parts hold it as a ghost)
     Halo halo;
 };
 
@@ -897,6 +899,8 @@ inline PartProblem<Real> build_part(const Problem<Real>& P, int nparts, int part
         R.interior_elements = int64_t(interior.size());
         R.elem_l2g = std::move(interior);
         R.elem_l2g.insert(R.elem_l2g.end(), boundary.begin(), boundary.end());
+        R.elem_owned.resize(R.elem_l2g.size());
+        for (size_t q = 0; q < R.elem_l2g.size(); ++q) R.elem_owned[q] = epart[size_t(R.elem_l2g[q])] == part;
     }
     // local problem arrays
     Problem<Real>& L = R.local;

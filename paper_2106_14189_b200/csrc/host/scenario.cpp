@@ -361,6 +361,12 @@ int djg_partition_maps(const djg_partition* p, int64_t* node_l2g, int64_t* elem_
     return DJG_OK;
 }
 
+int djg_partition_owned_elements(const djg_partition* p, uint8_t* owned) {
+    if (!p || !owned) return DJG_E_CONFIG;
+    std::visit([&](const auto& R) { std::memcpy(owned, R.elem_owned.data(), R.elem_owned.size()); }, p->p);
+    return DJG_OK;
+}
+
 int djg_element_parts(const djg_scenario* sc, int32_t nparts, int32_t* part) {
     return djg_element_parts_method(sc, nparts, DJG_PART_RCB, part);
 }

@@ -146,7 +146,7 @@ class GpuDjEngine:
 
     # -- plumbing
     def _check(self, rc: int):
-        if rc in (A.DJG_OK, A.DJG_E_INVERSION, A.DJG_E_DIVERGENCE):
+        if rc in (A.DJG_OK, A.DJG_E_INVERSION, A.DJG_E_DIVERGENCE, A.DJG_E_PEER):
             return rc
         msg = _lib().djg_last_error(self._h).decode()
         raise (CudaError if rc == A.DJG_E_CUDA else ConfigError)(msg)
@@ -221,7 +221,13 @@ class GpuDjEngine:
         """advance_step with a host SimState (djg_advance_host): one step from
         (u_curr, u_prev, step); returns (new u_curr, StepReport)."""
         u, up = self._vec(u_curr), self._vec(u_prev)
-        out = np.empty(3 * self.num_nodes, self.dtype) if out is None else out
+        if out is None:
+            out = np.empty(3 * self.num_nodes, self.dtype)
+        elif not (isinstance(out, np.ndarray) and out.dtype == self.dtype and out.size == 3 * self.num_nodes
+                  and out.flags["C_CONTIGUOUS"] and out.flags["WRITEABLE"]):
+            # the library writes 3N Reals through this pointer
+            raise ConfigError(f"out must be a writeable C-contiguous {np.dtype(self.dtype).name} array of "
+                              f"{3 * self.num_nodes} DOFs")
         rep = A.djg_report()
         self._check(_lib().djg_advance_host(self._h, A.ptr(u), A.ptr(up), step, A.ptr(out), C.byref(rep)))
         return out, StepReport.from_c(rep)
@@ -281,6 +287,8 @@ def raise_for(r: StepReport):
     if r.status == A.DJG_E_INVERSION:
         raise SimulationError(SimulationError.ElementInversion,
                               f"element {r.first_inverted} inverted at step {r.fail_step}", r.first_inverted)
+    if r.status == A.DJG_E_PEER:
+        raise CudaError(f"peer-memory step {r.fail_step}: a part did not post its step within the wait limit")
 
 
 @dataclass

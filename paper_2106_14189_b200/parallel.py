@@ -9,7 +9,7 @@ order, so a k-rank run is bit-identical to the 1-GPU run.
 
 Per step, all enqueued on the engine's CUDA stream (no host synchronisation):
   djg_step_async(1) -> djg_halo_pack -> NCCL send/recv with each neighbor ->
-  djg_halo_unpack -> djg_step_status -> NCCL allreduce(MAX) -> djg_step_agree
+  djg_halo_unpack -> djg_step_status -> NCCL allreduce (MAX; SUM of the counts) -> djg_step_agree
 
 `EmulatedParts` runs all parts in one process on one device, exchanging the
 halo with device copies (no kernel ever waits on another): it is how the
@@ -52,6 +52,8 @@ class Partition:
         self.node_l2g = np.zeros(i.num_nodes, np.int64)
         self.elem_l2g = np.zeros(i.num_elements, np.int64)
         _lib().djg_partition_maps(self._h, A.ptr(self.node_l2g), A.ptr(self.elem_l2g))
+        self.elem_owned = np.zeros(i.num_elements, np.uint8)  # elements this part reports inversions of
+        _lib().djg_partition_owned_elements(self._h, A.ptr(self.elem_owned))
         self.num_owned = i.num_owned
         self.num_nodes = i.num_nodes
         self.num_elements = i.num_elements
@@ -119,6 +121,7 @@ class PartEngine(GpuDjEngine):
         self._check(_lib().djg_set_halo(self._h, part.send_nodes.size, A.ptr(part.send_nodes),
                                         part.recv_nodes.size, A.ptr(part.recv_nodes)))
         self._check(_lib().djg_set_interior(self._h, part.info["interior_elements"]))
+        self._check(_lib().djg_set_counted_elements(self._h, A.ptr(part.elem_owned)))
 
     def set_global_state(self, u_curr=None, u_prev=None, step: int = 0):
         l2g = self.part.node_l2g
@@ -152,12 +155,15 @@ class PartEngine(GpuDjEngine):
         self._check(_lib().djg_peer_ipc_open(self._h, C.create_string_buffer(handles, 4 * 64), out))
         return [int(v or 0) for v in out]
 
-    def peer_setup(self, nparts: int, part: int, ptrs: list[list[int]], dests):
+    def peer_setup(self, nparts: int, part: int, ptrs: list[list[int]], dests, num_nodes):
+        """ptrs[q]: part q's 4 device pointers; dests: peer_destinations();
+        num_nodes[q]: part q's local node count (the destination bounds)."""
         peer_u = (C.c_void_p * (3 * nparts))(*[p[i] for p in ptrs for i in range(3)])
         peer_mail = (C.c_void_p * nparts)(*[p[3] for p in ptrs])
+        counts = np.ascontiguousarray(num_nodes, np.int64)
         node, dpart, index = (np.ascontiguousarray(a, np.int32) for a in dests)
-        self._check(_lib().djg_peer_setup(self._h, nparts, part, peer_u, peer_mail, int(node.size), A.ptr(node),
-                                          A.ptr(dpart), A.ptr(index)))
+        self._check(_lib().djg_peer_setup(self._h, nparts, part, peer_u, peer_mail, A.ptr(counts), int(node.size),
+                                          A.ptr(node), A.ptr(dpart), A.ptr(index)))
 
     def step_peer_local(self):
         self._check(_lib().djg_step_peer_local(self._h))
@@ -184,10 +190,10 @@ def peer_destinations(halos: list, me: int):
     position of q's receive block from me (the blocks list the same global
     nodes in the same order). halos[q] = (neighbors, send_off, recv_off,
     send_nodes, recv_nodes) of part q."""
-    nb, s_off, _, s_nodes, _ = halos[me]
+    nb, s_off, _, s_nodes, _ = halos[me][:5]
     node, part, index = [], [], []
     for k, q in enumerate(list(nb)):
-        qnb, _, q_roff, _, q_rnodes = halos[q]
+        qnb, _, q_roff, _, q_rnodes = halos[q][:5]
         j = list(qnb).index(me)
         send = s_nodes[s_off[k]:s_off[k + 1]]
         recv = q_rnodes[q_roff[j]:q_roff[j + 1]]
@@ -199,7 +205,8 @@ def peer_destinations(halos: list, me: int):
 
 
 def _halo(p: "Partition"):
-    return (p.neighbors.copy(), p.send_off.copy(), p.recv_off.copy(), p.send_nodes.copy(), p.recv_nodes.copy())
+    return (p.neighbors.copy(), p.send_off.copy(), p.recv_off.copy(), p.send_nodes.copy(), p.recv_nodes.copy(),
+            p.num_nodes)
 
 
 def _torch_dtype(dtype):
@@ -232,7 +239,7 @@ class DistributedEngine:
         dev = torch.device("cuda", device)
         self.send = torch.zeros((max(self.part.send_nodes.size, 1), 4), dtype=tdt, device=dev)
         self.recv = torch.zeros((max(self.part.recv_nodes.size, 1), 4), dtype=tdt, device=dev)
-        self.status = torch.zeros(2, dtype=torch.int64, device=dev)
+        self.status = torch.zeros(3, dtype=torch.int64, device=dev)  # djg_step_status: MAX, MAX, SUM
         self.stream = torch.cuda.ExternalStream(self.eng.stream, device=dev)
         self.transport = transport
         if transport == "p2p":
@@ -244,7 +251,8 @@ class DistributedEngine:
             dist.all_gather_object(halos, _halo(self.part), group=group)
             ptrs = [self.eng.peer_export() if q == self.rank else self.eng.peer_ipc_open(handles[q])
                     for q in range(self.world)]
-            self.eng.peer_setup(self.world, self.rank, ptrs, peer_destinations(halos, self.rank))
+            self.eng.peer_setup(self.world, self.rank, ptrs, peer_destinations(halos, self.rank),
+                                [h[5] for h in halos])
             dist.barrier(group=group)
             self.engine_comm = True  # the engine drives every step
         elif engine_comm:
@@ -286,7 +294,8 @@ class DistributedEngine:
                 self._exchange()
                 self.eng.halo_unpack(self.recv.data_ptr())
                 self.eng.step_status(self.status.data_ptr())
-                self.dist.all_reduce(self.status, op=self.dist.ReduceOp.MAX, group=self.group)
+                self.dist.all_reduce(self.status[:2], op=self.dist.ReduceOp.MAX, group=self.group)
+                self.dist.all_reduce(self.status[2:], op=self.dist.ReduceOp.SUM, group=self.group)
                 self.eng.step_agree(self.status.data_ptr())
 
     def step(self, nsteps: int, raise_on_failure=True) -> StepReport:
@@ -333,12 +342,12 @@ class EmulatedParts:
             ptrs = [e.peer_export() for e in self.engs]
             halos = [_halo(p) for p in self.parts]
             for i, e in enumerate(self.engs):
-                e.peer_setup(nparts, i, ptrs, peer_destinations(halos, i))
+                e.peer_setup(nparts, i, ptrs, peer_destinations(halos, i), [h[5] for h in halos])
         tdt = _torch_dtype(scenario.dtype)
         dev = torch.device("cuda", device)
         self.send = [torch.zeros((max(p.send_nodes.size, 1), 4), dtype=tdt, device=dev) for p in self.parts]
         self.recv = [torch.zeros((max(p.recv_nodes.size, 1), 4), dtype=tdt, device=dev) for p in self.parts]
-        self.status = [torch.zeros(2, dtype=torch.int64, device=dev) for _ in self.parts]
+        self.status = [torch.zeros(3, dtype=torch.int64, device=dev) for _ in self.parts]
         self.global_nodes = scenario.num_nodes
 
     def _sync(self):
@@ -360,7 +369,8 @@ class EmulatedParts:
 
     def _agree(self):
         torch = self.torch
-        red = torch.stack(self.status).max(dim=0).values
+        st = torch.stack(self.status)
+        red = torch.cat([st[:, :2].max(dim=0).values, st[:, 2:].sum(dim=0)])
         torch.cuda.synchronize()  # red is produced on torch's stream, read on the engines'
         for e in self.engs:
             e.step_agree(red.data_ptr())
@@ -370,42 +380,54 @@ class EmulatedParts:
         """overlap=False: local step, then halo exchange and agreement.
         overlap=True: the order of the engine's overlapped NCCL step -- halo
         pack and interior elements, exchange, unpack, boundary elements and
-        node update, agreement."""
+        node update, agreement. Returns one report per part over the whole
+        call (each engine call covers one step: the counts are summed)."""
+        acc = [None] * len(self.engs)
         for _ in range(nsteps):
-            if self.transport == "p2p":
-                # every part's step (its node kernel stores the halo into the
-                # other parts' buffers and posts its status) before any part
-                # waits: no kernel ever waits for another one here
-                for e in self.engs:
-                    e.step_peer_local()
-                self._sync()
-                for e in self.engs:
-                    e.step_peer_agree()
-                self._sync()
-                continue
-            if overlap:
-                for p, e in enumerate(self.engs):
-                    e.halo_pack(self.send[p].data_ptr())
-                    e.step_interior()
-                self._sync()
-                self._exchange()
-                for p, e in enumerate(self.engs):
-                    e.halo_unpack(self.recv[p].data_ptr())
-                    e.step_boundary()
-                    e.step_status(self.status[p].data_ptr())
-            else:
-                for e in self.engs:
-                    e.step_async(1)
-                for p, e in enumerate(self.engs):
-                    e.halo_pack(self.send[p].data_ptr())
-                self._sync()
-                self._exchange()
-                for p, e in enumerate(self.engs):
-                    e.halo_unpack(self.recv[p].data_ptr())
-                    e.step_status(self.status[p].data_ptr())
+            self._step1(overlap)
+            for i, e in enumerate(self.engs):
+                r = e.sync()
+                if acc[i] is not None:
+                    r.steps_done += acc[i].steps_done
+                    r.inverted_count += acc[i].inverted_count
+                    r.inverted_steps += acc[i].inverted_steps
+                acc[i] = r
+        return acc if nsteps > 0 else [e.sync() for e in self.engs]
+
+    def _step1(self, overlap: bool):
+        if self.transport == "p2p":
+            # every part's step (its node kernel stores the halo into the
+            # other parts' buffers and posts its status) before any part
+            # waits: no kernel ever waits for another one here
+            for e in self.engs:
+                e.step_peer_local()
             self._sync()
-            self._agree()
-        return [e.sync() for e in self.engs]
+            for e in self.engs:
+                e.step_peer_agree()
+            self._sync()
+            return
+        if overlap:
+            for p, e in enumerate(self.engs):
+                e.halo_pack(self.send[p].data_ptr())
+                e.step_interior()
+            self._sync()
+            self._exchange()
+            for p, e in enumerate(self.engs):
+                e.halo_unpack(self.recv[p].data_ptr())
+                e.step_boundary()
+                e.step_status(self.status[p].data_ptr())
+        else:
+            for e in self.engs:
+                e.step_async(1)
+            for p, e in enumerate(self.engs):
+                e.halo_pack(self.send[p].data_ptr())
+            self._sync()
+            self._exchange()
+            for p, e in enumerate(self.engs):
+                e.halo_unpack(self.recv[p].data_ptr())
+                e.step_status(self.status[p].data_ptr())
+        self._sync()
+        self._agree()
 
     def set_global_state(self, u=None, up=None, step=0):
         for e in self.engs:

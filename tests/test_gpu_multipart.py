@@ -113,6 +113,86 @@ def test_parts_agree_on_inversion(overlap):
     assert np.array_equal(u, u1) and np.array_equal(up, up1)
 
 
+@pytest.mark.parametrize("nparts", [2, 3, 4])
+@pytest.mark.parametrize("transport", ["sequential", "overlapped", "p2p"])
+def test_parts_skip_and_report_counts(nparts, transport):
+    """SkipAndReport over a crushing load: elements invert on several steps,
+    some of them ghosts held by more than one part. Every part reports the
+    single-GPU (= reference) inverted_count and inverted_steps: an inversion
+    is counted only on the part that owns the element and the step counts are
+    summed by the agreement."""
+    sc0 = Scenario(box_spec(kind="T4", divisions=4, extent=(0.1, 0.1, 0.1), precision=8))
+    img = sc0.image()
+    nodes, conn = img["nodes"].reshape(-1, 3), img["conn"].reshape(-1, 4)
+    bottom = [n for n in range(len(nodes)) if nodes[n, 2] == 0.0]
+    top = [n for n in range(len(nodes)) if nodes[n, 2] == nodes[:, 2].max()]
+    spec = mesh_spec(nodes, conn, kind="T4", precision=8, fixed=[(n, a) for n in bottom for a in range(3)],
+                     prescribed=[(n, 2, -0.35, 2e-4) for n in top], dt=1e-5, alpha=0.0,
+                     policy=A.DJG_SKIP_AND_REPORT)
+    steps = 60
+    u1, up1, r1 = single(spec, steps)
+    ur, upr, rr = oracle.run(spec, steps, "oracle")
+    assert (r1.inverted_count, r1.inverted_steps, r1.status) == (rr["inverted_count"], rr["inverted_steps"],
+                                                                 rr["status"])
+    assert r1.inverted_count > r1.inverted_steps > 1, r1  # several elements on several steps
+    if transport == "p2p":
+        em = EmulatedParts(Scenario(spec), nparts, transport="p2p")
+        reps = em.step(steps)
+    else:
+        em = EmulatedParts(Scenario(spec), nparts)
+        reps = em.step(steps, overlap=transport == "overlapped")
+    u, up, step = em.global_state()
+    em.close()
+    for r in reps:
+        assert (r.inverted_count, r.inverted_steps, r.status, r.step) == \
+            (r1.inverted_count, r1.inverted_steps, r1.status, r1.step), (r, r1)
+    assert np.array_equal(u, u1) and np.array_equal(up, up1)
+
+
+def test_peer_setup_rejects_out_of_range_destinations():
+    """djg_peer_setup bounds-checks every halo destination against the peer's
+    node count before any peer store can run."""
+    from paper_2106_14189_b200.engine import ConfigError
+    from paper_2106_14189_b200.parallel import _halo, peer_destinations
+    spec = box_spec(kind="T4", divisions=4, precision=4, ramp_steps=50)
+    em = EmulatedParts(Scenario(spec), 2, transport="p2p")
+    try:
+        ptrs = [e.peer_export() for e in em.engs]
+        halos = [_halo(p) for p in em.parts]
+        node, part, index = peer_destinations(halos, 0)
+        assert len(index) > 0
+        counts = [h[5] for h in halos]
+        bad = list(index)
+        bad[0] = counts[part[0]]  # one past the peer's last node
+        with pytest.raises(ConfigError, match="outside the peer"):
+            em.engs[0].peer_setup(2, 0, ptrs, (node, part, bad), counts)
+        with pytest.raises(ConfigError, match="node counts"):
+            em.engs[0].peer_setup(2, 0, ptrs, (node, part, index), [counts[0] + 1, counts[1]])
+    finally:
+        em.close()
+
+
+def test_peer_wait_is_bounded(monkeypatch):
+    """A part whose peer never posts its step: the agreement kernel gives up
+    after DJG_PEER_TIMEOUT_MS and halts the part with DJG_E_PEER instead of
+    spinning on the GPU (one kernel waits here, on a flag no kernel will
+    write: nothing else has to run concurrently)."""
+    monkeypatch.setenv("DJG_PEER_TIMEOUT_MS", "200")
+    spec = box_spec(kind="T4", divisions=4, precision=4, ramp_steps=50)
+    em = EmulatedParts(Scenario(spec), 2, transport="p2p")
+    try:
+        e0 = em.engs[0]
+        e0.step_peer_local()
+        e0.sync()
+        e0.step_peer_agree()
+        r = e0.sync()
+        assert r.status == A.DJG_E_PEER, r
+        e0.step_async(3)  # a halted part runs no further steps
+        assert e0.sync().status == A.DJG_E_PEER
+    finally:
+        em.close()
+
+
 def _port():
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))

@@ -307,6 +307,33 @@ class DistributedEngine:
             raise_for(r)
         return r
 
+    def step_lockstep(self, nsteps: int) -> StepReport:
+        """Peer-memory step with a host barrier between each step's local part
+        (element kernel, node kernel with its peer stores and mailbox posts)
+        and the agreement: by the time any rank's k_wait_agree runs, every
+        rank's posts have completed, so no kernel ever waits on another
+        process's kernel. For ranks that share one GPU (processes on one
+        device are time-sliced: a kernel spinning on another process's flag
+        is not guaranteed to see it run). Same kernels, IPC mappings,
+        system-scope release/acquire and agreement as the graph-captured step;
+        counts summed over the steps."""
+        if self.transport != "p2p":
+            raise ConfigError("step_lockstep drives the peer-memory transport")
+        acc = None
+        for _ in range(nsteps):
+            self.eng.step_peer_local()
+            self.eng.sync()
+            self.dist.barrier(group=self.group)
+            self.eng.step_peer_agree()
+            r = self.eng.sync()
+            self.dist.barrier(group=self.group)
+            if acc is not None:
+                r.steps_done += acc.steps_done
+                r.inverted_count += acc.inverted_count
+                r.inverted_steps += acc.inverted_steps
+            acc = r
+        return acc
+
     def gather_global(self):
         """All ranks' owned displacements assembled into global arrays (rank 0
         gets the result; others return None)."""

@@ -27,69 +27,100 @@ inline bool ends_with(const std::string& s, const std::string& suffix) {
     return s.size() >= suffix.size() && s.compare(s.size() - suffix.size(), suffix.size(), suffix) == 0;
 }
 
-inline bool blank_or_comment(const std::string& line) {
-    for (char c : line) {
-        if (c == '#') return true;
-        if (!std::isspace(static_cast<unsigned char>(c))) return false;
+// Reader of the reference's text mesh format (the format and its error
+// messages, mesh.hpp:105-185, are the interface): a record cursor that yields
+// the significant lines ('#' comment lines and blank lines skipped) with
+// their line numbers, and a scanner that reads whitespace-separated fields
+// off a record left to right -- a field ends where its number does, so
+// "1.5abc" reads 1.5 and leaves "abc" for the next field, like stream
+// extraction.
+class MeshRecords {
+public:
+    explicit MeshRecords(std::istream& in) : in_(in) {}
+
+    // Next significant line; ParseError at end of file.
+    const std::string& next(const char* expected) {
+        while (std::getline(in_, text_)) {
+            ++line_;
+            const size_t first = text_.find_first_not_of(" \t\r\n\v\f");
+            if (first != std::string::npos && text_[first] != '#') {
+                pos_ = 0;
+                return text_;
+            }
+        }
+        throw ParseError(std::string("unexpected end of file, expected ") + expected, line_);
     }
-    return true;
-}
+    long line() const { return line_; }
+
+    bool word(std::string& out) {
+        skip_blanks();
+        const size_t b = pos_;
+        while (pos_ < text_.size() && !std::isspace(static_cast<unsigned char>(text_[pos_]))) ++pos_;
+        out.assign(text_, b, pos_ - b);
+        return pos_ > b;
+    }
+    bool integer(long& out) {
+        skip_blanks();
+        const size_t n = number_prefix(text_.substr(pos_), true);
+        if (n == 0) return false;
+        out = std::strtol(text_.c_str() + pos_, nullptr, 10);
+        pos_ += n;
+        return true;
+    }
+    template <class Real>
+    bool real(Real& out) {
+        skip_blanks();
+        const size_t n = number_prefix(text_.substr(pos_), false);
+        if (n == 0 || !convert(text_.substr(pos_, n), out)) return false;
+        pos_ += n;
+        return true;
+    }
+
+private:
+    void skip_blanks() {
+        while (pos_ < text_.size() && std::isspace(static_cast<unsigned char>(text_[pos_]))) ++pos_;
+    }
+    std::istream& in_;
+    std::string text_;
+    size_t pos_ = 0;
+    long line_ = 0;
+};
 
 template <class Real>
 inline Mesh<Real> load_text_mesh(std::istream& in) {
-    std::string line;
-    long lineno = 0;
-    auto next = [&](const char* what) -> std::string& {
-        while (std::getline(in, line)) {
-            ++lineno;
-            if (!blank_or_comment(line)) return line;
-        }
-        throw ParseError(std::string("unexpected end of file, expected ") + what, lineno);
-    };
-    {
-        std::istringstream ls(next("header"));
-        std::string magic;
-        int version = 0;
-        if (!(ls >> magic >> version) || magic != "djtled-mesh") throw ParseError("expected header 'djtled-mesh 1'", lineno);
-        if (version != 1) throw ParseError("unsupported mesh format version " + std::to_string(version), lineno);
-    }
-    long n_nodes = 0;
-    {
-        std::istringstream ls(next("'nodes N'"));
-        std::string kw;
-        if (!(ls >> kw >> n_nodes) || kw != "nodes" || n_nodes < 0) throw ParseError("expected 'nodes N'", lineno);
-    }
+    MeshRecords r(in);
+    std::string w;
+    long count = 0;
+    r.next("header");
+    if (!r.word(w) || w != "djtled-mesh" || !r.integer(count)) throw ParseError("expected header 'djtled-mesh 1'", r.line());
+    if (count != 1) throw ParseError("unsupported mesh format version " + std::to_string(count), r.line());
+
+    r.next("'nodes N'");
+    if (!r.word(w) || w != "nodes" || !r.integer(count) || count < 0) throw ParseError("expected 'nodes N'", r.line());
     Mesh<Real> m;
-    m.nodes.reserve(size_t(3 * n_nodes));
-    for (long i = 0; i < n_nodes; ++i) {
-        std::istringstream ls(next("node coordinates"));
-        Real x, y, z;
-        if (!(ls >> x >> y >> z)) throw ParseError("malformed node coordinates", lineno);
-        m.nodes.push_back(x);
-        m.nodes.push_back(y);
-        m.nodes.push_back(z);
+    m.nodes.resize(size_t(3 * count));
+    for (Real* x = m.nodes.data(); x != m.nodes.data() + m.nodes.size(); x += 3) {
+        r.next("node coordinates");
+        if (!(r.real(x[0]) && r.real(x[1]) && r.real(x[2]))) throw ParseError("malformed node coordinates", r.line());
     }
-    long n_elems = 0;
-    {
-        std::istringstream ls(next("'elements T4|H8 M'"));
-        std::string kw, kind;
-        if (!(ls >> kw >> kind >> n_elems) || kw != "elements" || n_elems < 0)
-            throw ParseError("expected 'elements T4|H8 M'", lineno);
-        if (kind == "T4") m.kind = DJG_T4;
-        else if (kind == "H8") m.kind = DJG_H8;
-        else throw ParseError("unknown element kind '" + kind + "'", lineno);
-    }
+
+    r.next("'elements T4|H8 M'");
+    std::string kind;
+    if (!r.word(w) || w != "elements" || !r.word(kind) || !r.integer(count) || count < 0)
+        throw ParseError("expected 'elements T4|H8 M'", r.line());
+    if (kind != "T4" && kind != "H8") throw ParseError("unknown element kind '" + kind + "'", r.line());
+    m.kind = kind == "T4" ? DJG_T4 : DJG_H8;
     const int npe = m.npe();
-    m.conn.reserve(size_t(n_elems) * size_t(npe));
-    for (long e = 0; e < n_elems; ++e) {
-        std::istringstream ls(next("element connectivity"));
+    m.conn.resize(size_t(count) * size_t(npe));
+    for (int32_t* c = m.conn.data(); c != m.conn.data() + m.conn.size(); c += npe) {
+        r.next("element connectivity");
         for (int a = 0; a < npe; ++a) {
-            long idx;
-            if (!(ls >> idx)) throw ParseError("expected " + std::to_string(npe) + " node indices", lineno);
-            m.conn.push_back(int32_t(idx));
+            long id;
+            if (!r.integer(id)) throw ParseError("expected " + std::to_string(npe) + " node indices", r.line());
+            c[a] = int32_t(id);
         }
-        long extra;
-        if (ls >> extra) throw ParseError("too many node indices on element line", lineno);
+        long surplus;
+        if (r.integer(surplus)) throw ParseError("too many node indices on element line", r.line());
     }
     return m;
 }

@@ -109,90 +109,18 @@ struct V3 {
     Real x, y, z;
 };
 
-// 3x3 helpers with the reference's evaluation order (core.hpp:144-212).
-template <class Real>
-inline Real det3(const Real a[3][3]) {
-    return a[0][0] * (a[1][1] * a[2][2] - a[1][2] * a[2][1]) -
-           a[0][1] * (a[1][0] * a[2][2] - a[1][2] * a[2][0]) +
-           a[0][2] * (a[1][0] * a[2][1] - a[1][1] * a[2][0]);
-}
-
-template <class Real>
-inline void inv3(const Real a[3][3], Real d, Real r[3][3]) {
-    const Real s = Real(1) / d;
-    r[0][0] = (a[1][1] * a[2][2] - a[1][2] * a[2][1]) * s;
-    r[0][1] = (a[0][2] * a[2][1] - a[0][1] * a[2][2]) * s;
-    r[0][2] = (a[0][1] * a[1][2] - a[0][2] * a[1][1]) * s;
-    r[1][0] = (a[1][2] * a[2][0] - a[1][0] * a[2][2]) * s;
-    r[1][1] = (a[0][0] * a[2][2] - a[0][2] * a[2][0]) * s;
-    r[1][2] = (a[0][2] * a[1][0] - a[0][0] * a[1][2]) * s;
-    r[2][0] = (a[1][0] * a[2][1] - a[1][1] * a[2][0]) * s;
-    r[2][1] = (a[0][1] * a[2][0] - a[0][0] * a[2][1]) * s;
-    r[2][2] = (a[0][0] * a[1][1] - a[0][1] * a[1][0]) * s;
-}
-
 // Symmetric 3x3 in (xx,yy,zz,xy,xz,yz) order (core.hpp:214-228).
 template <class Real>
 struct Sym {
     Real v[6];
 };
 
-template <class Real>
-inline void sym_full(const Sym<Real>& s, Real m[3][3]) {
-    m[0][0] = s.v[0]; m[0][1] = s.v[3]; m[0][2] = s.v[4];
-    m[1][0] = s.v[3]; m[1][1] = s.v[1]; m[1][2] = s.v[5];
-    m[2][0] = s.v[4]; m[2][1] = s.v[5]; m[2][2] = s.v[2];
-}
-
-// Q^T S Q (core.hpp:259-271): first SQ = S_full * Q, then the six entries.
-template <class Real>
-inline Sym<Real> congruence(const Real q[3][3], const Sym<Real>& s) {
-    Real sf[3][3], sq[3][3];
-    sym_full(s, sf);
-    for (int i = 0; i < 3; ++i)
-        for (int j = 0; j < 3; ++j)
-            sq[i][j] = sf[i][0] * q[0][j] + sf[i][1] * q[1][j] + sf[i][2] * q[2][j];
-    Sym<Real> r;
-    r.v[0] = q[0][0] * sq[0][0] + q[1][0] * sq[1][0] + q[2][0] * sq[2][0];
-    r.v[1] = q[0][1] * sq[0][1] + q[1][1] * sq[1][1] + q[2][1] * sq[2][1];
-    r.v[2] = q[0][2] * sq[0][2] + q[1][2] * sq[1][2] + q[2][2] * sq[2][2];
-    r.v[3] = q[0][0] * sq[0][1] + q[1][0] * sq[1][1] + q[2][0] * sq[2][1];
-    r.v[4] = q[0][0] * sq[0][2] + q[1][0] * sq[1][2] + q[2][0] * sq[2][2];
-    r.v[5] = q[0][1] * sq[0][2] + q[1][1] * sq[1][2] + q[2][1] * sq[2][2];
-    return r;
-}
-
-template <class Real>
-inline Sym<Real> scaled(Real s, const Sym<Real>& a) {
-    Sym<Real> r;
-    for (int k = 0; k < 6; ++k) r.v[k] = s * a.v[k];
-    return r;
-}
-
-// Frobenius product of symmetric matrices (core.hpp:277-280).
-template <class Real>
-inline Real ddot(const Sym<Real>& a, const Sym<Real>& b) {
-    return a.v[0] * b.v[0] + a.v[1] * b.v[1] + a.v[2] * b.v[2] +
-           2 * (a.v[3] * b.v[3] + a.v[4] * b.v[4] + a.v[5] * b.v[5]);
-}
-
-template <class Real>
-inline Real trace(const Sym<Real>& a) { return a.v[0] + a.v[1] + a.v[2]; }
-
-// outer(v) and sym_outer(u, v) (core.hpp:240-251).
+// outer(v) (core.hpp:240-251): the fibre structure tensor of a unit fibre.
+// (Every other tensor operation of the precompute lives in
+// common/element_math.hpp, shared with the device.)
 template <class Real>
 inline Sym<Real> outer(const V3<Real>& v) {
     return {{v.x * v.x, v.y * v.y, v.z * v.z, v.x * v.y, v.x * v.z, v.y * v.z}};
-}
-template <class Real>
-inline Sym<Real> sym_outer(const V3<Real>& u, const V3<Real>& v) {
-    return {{2 * u.x * v.x, 2 * u.y * v.y, 2 * u.z * v.z, u.x * v.y + u.y * v.x,
-             u.x * v.z + u.z * v.x, u.y * v.z + u.z * v.y}};
-}
-
-inline int sym6_index(int i, int j) {
-    if (i > j) std::swap(i, j);
-    return i * 6 - i * (i + 1) / 2 + j;
 }
 
 // ---------------------------------------------------------------- material
@@ -339,36 +267,6 @@ inline Mesh<Real> generate_box(const double extent_in[3], const int32_t div[3], 
     return m;
 }
 
-// Reference Jacobian J = D X (element.hpp:59-77) and volume (element.hpp:80-85).
-template <class Real>
-struct Jac {
-    Real J[3][3], Jinv[3][3], det;
-};
-
-template <class Real>
-inline bool jacobian0(const V3<Real>* x, const Shape<Real>& D, Jac<Real>& j) {
-    for (int i = 0; i < 3; ++i) {
-        Real r[3] = {Real(0), Real(0), Real(0)};
-        for (int a = 0; a < D.n; ++a) {
-            r[0] = r[0] + D.d[i][a] * x[a].x;
-            r[1] = r[1] + D.d[i][a] * x[a].y;
-            r[2] = r[2] + D.d[i][a] * x[a].z;
-        }
-        j.J[i][0] = r[0];
-        j.J[i][1] = r[1];
-        j.J[i][2] = r[2];
-    }
-    j.det = det3(j.J);
-    if (!(j.det > Real(0))) return false;
-    inv3(j.J, j.det, j.Jinv);
-    return true;
-}
-
-template <class Real>
-inline Real volume0(const Jac<Real>& j, int kind) {
-    return kind == DJG_T4 ? j.det / Real(6) : Real(8) * j.det;
-}
-
 // validate_mesh (mesh.hpp:75-92).
 template <class Real>
 inline void validate_mesh(const Mesh<Real>& m) {
@@ -382,14 +280,19 @@ inline void validate_mesh(const Mesh<Real>& m) {
             const int32_t c = m.conn[size_t(e * npe + a)];
             if (c < 0 || c >= n) throw MeshError("connectivity index " + std::to_string(c) + " out of range", long(e));
         }
-    const Shape<Real> D(m.kind);
     int64_t bad = -1;
 #pragma omp parallel for schedule(static) reduction(max : bad)
     for (int64_t e = 0; e < E; ++e) {
-        V3<Real> x[8];
-        for (int a = 0; a < npe; ++a) x[a] = m.node(m.conn[size_t(e * npe + a)]);
-        Jac<Real> j;
-        if (!jacobian0(x, D, j) || !(volume0(j, m.kind) > Real(0))) bad = std::max<int64_t>(bad, E - e);
+        Real x[8][3] = {};
+        for (int a = 0; a < npe; ++a) {
+            const V3<Real> p = m.node(m.conn[size_t(e * npe + a)]);
+            x[a][0] = p.x;
+            x[a][1] = p.y;
+            x[a][2] = p.z;
+        }
+        Real J[3][3], Ji[3][3], det;
+        if (!em::jacobian0(m.kind, x, J, Ji, det) || !(em::volume0(m.kind, det) > Real(0)))
+            bad = std::max<int64_t>(bad, E - e);
     }
     if (bad >= 0) throw MeshError("non-positive reference Jacobian determinant", long(E - bad));
 }
@@ -422,33 +325,6 @@ inline Adjacency build_adjacency(const std::vector<int32_t>& conn, int64_t n, in
 }
 
 // ---------------------------------------------------------------- precompute
-
-// Hourglass shape vectors (precompute.hpp:136-165).
-template <class Real>
-inline void hourglass_vectors(const V3<Real>* x, const Shape<Real>& D, const Real jinv[3][3], Real gamma[4][8]) {
-    Real base[4][8];
-    for (int a = 0; a < 8; ++a) {
-        const int xi = kCornerSign[a][0], eta = kCornerSign[a][1], zeta = kCornerSign[a][2];
-        base[0][a] = Real(eta * zeta);
-        base[1][a] = Real(xi * zeta);
-        base[2][a] = Real(xi * eta);
-        base[3][a] = Real(xi * eta * zeta);
-    }
-    Real b[3][8];
-    for (int j = 0; j < 3; ++j)
-        for (int a = 0; a < 8; ++a)
-            b[j][a] = jinv[j][0] * D.d[0][a] + jinv[j][1] * D.d[1][a] + jinv[j][2] * D.d[2][a];
-    for (int m = 0; m < 4; ++m) {
-        Real hx[3] = {Real(0), Real(0), Real(0)};
-        for (int j = 0; j < 3; ++j)
-            for (int a = 0; a < 8; ++a) {
-                const Real c = j == 0 ? x[a].x : (j == 1 ? x[a].y : x[a].z);
-                hx[j] += base[m][a] * c;
-            }
-        for (int a = 0; a < 8; ++a)
-            gamma[m][a] = base[m][a] - (hx[0] * b[0][a] + hx[1] * b[1][a] + hx[2] * b[2][a]);
-    }
-}
 
 // The hot-field record of build_element_constants (precompute.hpp:206-255),
 // through the arithmetic shared with the device (common/element_math.hpp).

@@ -158,6 +158,7 @@ struct ElemArgs {
     const void* rank;                    // per element: npe ranks (uint8 or uint16) of the element
                                          // in its nodes' CSR rows, packed in one 4/8/16-byte word
     const int* slice_base;               // first slot of each 32-node slice
+    int slice_w;                         // > 0: uniform slices, slice_base[s] = 32 slice_w s
     const int4* slot;                    // node windows: NPE/4 planes of int4[E], slot position of
                                          // each element-node (slice_base[n/32] + 32 rank + n%32)
     const void* widx;                    // node windows: per element NPE window indices (uint8 / uint16)
@@ -183,6 +184,7 @@ struct NodeArgs {
     long long cap;                       // force-slot entries (DJG_CHECKS bounds)
     const int* row_len;                  // CSR row length per node
     const int* slice_base;               // first slot position of each 32-node slice
+    int slice_w;                         // > 0: uniform slices, slice_base[s] = 32 slice_w s
     const typename RT<Real>::Node* ef;   // force slots
     typename RT<Real>::Node* u[3];
     const typename RT<Real>::Node* r_ext;  // NULL: identically zero
@@ -301,9 +303,13 @@ __device__ __forceinline__ void load_ranks(const void* base, long long e, int (&
     decode_ranks<NPE, RB>(__ldcs(static_cast<const W*>(base) + e), rk);
 }
 
-// Slot of element-node (n, rank k): slice_base[n/32] + 32 k + n%32.
-__device__ __forceinline__ int slot_of(const int* __restrict__ slice_base, int n, int k) {
-    return __ldg(slice_base + (n >> 5)) + 32 * k + (n & 31);
+// Slot of element-node (n, rank k): slice_base[n/32] + 32 k + n%32 -- the
+// base computed (uniform slices, w > 0) or loaded.
+__device__ __forceinline__ int slice_base_of(const int* __restrict__ slice_base, int w, long long n) {
+    return w > 0 ? int(32 * w * (n >> 5)) : __ldg(slice_base + (n >> 5));
+}
+__device__ __forceinline__ int slot_of(const int* __restrict__ slice_base, int w, int n, int k) {
+    return slice_base_of(slice_base, w, n) + 32 * k + (n & 31);
 }
 
 // Where element_body takes its streamed per-element inputs from: straight
@@ -323,7 +329,9 @@ struct GlobalSrc {
                                                             int n) const {
         return RT<Real>::load_node(u + n);
     }
-    __device__ __forceinline__ int slot(const int* __restrict__ sb, int, int n, int k) const { return slot_of(sb, n, k); }
+    __device__ __forceinline__ int slot(const int* __restrict__ sb, int, int n, int k) const {
+        return slot_of(sb, A.slice_w, n, k);
+    }
     __device__ __forceinline__ Real tail(int t) const { return __ldcs(A.ctail + t * A.tail_stride + e); }
     __device__ __forceinline__ typename RT<Real>::Node coord(const ElemArgs<Real>& a, int n) const {
         return RT<Real>::load_node(a.X + n);
@@ -337,6 +345,7 @@ struct SmemSrc {
     const void* srank;                   // [TILE] rank words
     const Real* stail;                   // [NTAIL][TILE] record remainder
     int i;
+    int w;                               // ElemArgs::slice_w
     __device__ __forceinline__ typename RT<Real>::Node node(int, const typename RT<Real>::Node* __restrict__ u,
                                                             int n) const {
         return RT<Real>::load_node(u + n);
@@ -348,7 +357,9 @@ struct SmemSrc {
         using W = typename RankWord<NPE, RB>::type;
         decode_ranks<NPE, RB>(static_cast<const W*>(srank)[i], rk);
     }
-    __device__ __forceinline__ int slot(const int* __restrict__ sb, int, int n, int k) const { return slot_of(sb, n, k); }
+    __device__ __forceinline__ int slot(const int* __restrict__ sb, int, int n, int k) const {
+        return slot_of(sb, w, n, k);
+    }
     __device__ __forceinline__ Real tail(int t) const { return stail[t * TILE + i]; }
     __device__ __forceinline__ typename RT<Real>::Node coord(const ElemArgs<Real>& a, int n) const {
         return RT<Real>::load_node(a.X + n);
@@ -1131,7 +1142,8 @@ __global__ void __launch_bounds__(kPipeThreads, (kPipeMinBlocks<Real, KIND, MODE
             const unsigned char* st = smem + s * PS::kStageBytes;
             const SmemSrc<Real, kPipeTile> src{reinterpret_cast<const int4*>(st + PS::kConnOff),
                                                reinterpret_cast<const Plane*>(st + PS::kRecOff), st + PS::kRankOff,
-                                               reinterpret_cast<const Real*>(st + PS::kTailOff), tid};
+                                               reinterpret_cast<const Real*>(st + PS::kTailOff), tid,
+                                               A.slice_w};
             if constexpr (FORM == 2) element_body_tled<Real, KIND, MODEL, RB>(A, e, u, src);
             else element_body<Real, KIND, MODEL, RB, FORM == 1>(A, e, u, src);
         }
@@ -1623,8 +1635,9 @@ __global__ void __launch_bounds__(256) k_node(const NodeArgs<Real> A) {
     for (long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x; n < A.N && !skip;
          n += (long long)gridDim.x * blockDim.x) {
         Real fx, fy, fz;
-        DJG_ASSERT(A.row_len[n] == 0 || (long long)A.slice_base[n >> 5] + (n & 31) + 32LL * (A.row_len[n] - 1) < A.cap);
-        gather_row<Real>(A.ef + (long long)A.slice_base[n >> 5] + (n & 31), A.row_len[n], fx, fy, fz);
+        const long long p0 = (long long)slice_base_of(A.slice_base, A.slice_w, n) + (n & 31);
+        DJG_ASSERT(A.row_len[n] == 0 || p0 + 32LL * (A.row_len[n] - 1) < A.cap);
+        gather_row<Real>(A.ef + p0, A.row_len[n], fx, fy, fz);
         if constexpr (kAssemble) {
             A.f_out[3 * n + 0] = fx;
             A.f_out[3 * n + 1] = fy;
@@ -1858,7 +1871,8 @@ __global__ void __launch_bounds__(256) k_node_peer(const NodeArgs<Real> A, const
     typename T::Node* unxt = pick3(phn, A.u[0], A.u[1], A.u[2]);
     for (long long n = (long long)blockIdx.x * blockDim.x + threadIdx.x; n < A.N;
          n += (long long)gridDim.x * blockDim.x) {
-        if (node_body<Real, false>(A, n, (long long)A.slice_base[n >> 5] + (n & 31), A.row_len[n], step))
+        if (node_body<Real, false>(A, n, (long long)slice_base_of(A.slice_base, A.slice_w, n) + (n & 31), A.row_len[n],
+                                   step))
             s_nonfinite = 1;
         const int d0 = P.dest_off[n], d1 = P.dest_off[n + 1];
         if (d0 < d1) {

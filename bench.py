@@ -583,13 +583,19 @@ def multi_arm(args, rank, world, device):
     spec = box_spec(kind=args.kind, model=args.model, divisions=args.divisions, precision=args.precision,
                     target=0.01, ramp_steps=total)
     t0 = time.perf_counter()
-    sc = Scenario(spec)
-    de = DistributedEngine(sc, device=device, method=args.partition, transport=args.transport)
+    if args.partition == "box":
+        # part-local setup: this rank builds only its part from the box spec
+        de = DistributedEngine(spec, device=device, method="box-local", transport=args.transport)
+    else:
+        de = DistributedEngine(Scenario(spec), device=device, method=args.partition, transport=args.transport)
     t1 = time.perf_counter()
-    E = sc.num_elements
     pi = de.part.info
+    E = pi["global_elements"]
+    setup = torch.tensor([t1 - t0, _peak_rss_gb()], dtype=torch.float64, device="cuda")
+    dist.all_reduce(setup, op=dist.ReduceOp.MAX)
     log(f"[bench rank {rank}] local E={pi['num_elements']} owned N={pi['num_owned']} "
-        f"neighbors={pi['num_neighbors']} halo send={pi['send_total']} setup {t1 - t0:.1f}s")
+        f"neighbors={pi['num_neighbors']} halo send={pi['send_total']} setup {t1 - t0:.1f}s "
+        f"peak RSS {_peak_rss_gb():.2f} GB")
     de.step(W)
     torch.cuda.synchronize()
     dist.barrier()
@@ -666,8 +672,11 @@ def multi_arm(args, rank, world, device):
             "gpu_launches_note": "rank 0: element, node, halo pack / unpack, status, agree per step (NCCL kernels "
                                  "not counted)",
             "clocks": clk,
-            "partition": {"local_elements": pi["num_elements"], "owned_elements": pi["owned_elements"],
-                          "halo_send_nodes": pi["send_total"], "neighbors": pi["num_neighbors"]},
+            "partition": {"method": "box (part-local build)" if args.partition == "box" else args.partition,
+                          "local_elements": pi["num_elements"], "owned_elements": pi["owned_elements"],
+                          "halo_send_nodes": pi["send_total"], "neighbors": pi["num_neighbors"],
+                          "setup_s_max_over_ranks": float(setup[0].item()),
+                          "host_peak_rss_gb_max_over_ranks": float(setup[1].item())},
         }
         print(json.dumps(_line(args, world, K, W, E, ms_step, value, extra)), flush=True)
     dist.destroy_process_group()
@@ -692,8 +701,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--transport", default="p2p", choices=["p2p", "nccl"],
                     help="multi-GPU halo / agreement: peer-memory stores from the node kernel (default) or NCCL")
-    ap.add_argument("--partition", default="rcb", choices=["rcb", "metis"],
-                    help="multi-GPU partition: coordinate bisection (default) or METIS k-way on the dual graph")
+    ap.add_argument("--partition", default="box", choices=["box", "rcb", "metis"],
+                    help="multi-GPU partition: blocks of the box's cell grid, each rank building only its part "
+                         "(default), or -- from the global problem -- coordinate bisection / METIS k-way")
     args = ap.parse_args()
     if args.impl == "reference":
         reference_arm(args)

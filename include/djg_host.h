@@ -75,12 +75,25 @@ typedef struct djg_partition_info {
 } djg_partition_info;
 
 /* Partition methods: recursive coordinate bisection of element centroids
- * (default; fast, reproducible), or METIS k-way on the element dual graph
- * (faces shared; METIS_PartMeshDual, fixed seed: reproducible). */
-enum djg_partition_method { DJG_PART_RCB = 0, DJG_PART_METIS = 1 };
+ * (default; fast, reproducible), METIS k-way on the element dual graph
+ * (faces shared; METIS_PartMeshDual, fixed seed: reproducible), or -- for
+ * generated boxes -- recursive bisection of the cell grid (every part a
+ * block of cells; the partition the part-local build uses). */
+enum djg_partition_method { DJG_PART_RCB = 0, DJG_PART_METIS = 1, DJG_PART_BOX = 2 };
 int djg_partition_build(const djg_scenario* sc, int32_t nparts, int32_t part, djg_partition** out);
 int djg_partition_build_method(const djg_scenario* sc, int32_t nparts, int32_t part, int32_t method,
                                djg_partition** out);
+/* Part-local build of a generated box (spec->nodes == NULL, plane BCs):
+ * part `part` of the DJG_PART_BOX partition built without the global mesh or
+ * problem -- the same local problem djg_partition_build_method(...,
+ * DJG_PART_BOX) extracts from the global one, for every owned node and local
+ * element. Two steps, because dt needs the global minimum characteristic
+ * length: build returns this part's minimum in *local_min_length; the caller
+ * reduces it over the parts (MIN) and passes it to djg_partition_finish,
+ * which completes dt, alpha, the BCs and the update coefficients. */
+int djg_partition_build_box(const djg_scenario_spec* spec, int32_t nparts, int32_t part, djg_partition** out,
+                            double* local_min_length);
+int djg_partition_finish(djg_partition* p, double global_min_length);
 void djg_partition_free(djg_partition* p);
 int djg_partition_get_info(const djg_partition* p, djg_partition_info* out);
 /* Local problem arrays (same layout as djg_scenario_image, local ids). */

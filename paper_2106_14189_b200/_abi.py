@@ -31,7 +31,8 @@ DJG_FLAG_TLED = 64
 DJG_FLAG_NO_PIPE = 128
 DJG_FLAG_WINDOW = 256
 DJG_PART_RCB, DJG_PART_METIS = 0, 1
-PART_METHODS = {"rcb": DJG_PART_RCB, "metis": DJG_PART_METIS}
+DJG_PART_BOX = 2
+PART_METHODS = {"rcb": DJG_PART_RCB, "metis": DJG_PART_METIS, "box": DJG_PART_BOX}
 
 KIND_NAMES = {"T4": DJG_T4, "H8": DJG_H8}
 MODEL_NAMES = {"NH": DJG_NH, "TI": DJG_TI, "OT": DJG_OT, "MR": DJG_MR, "I57": DJG_I57}
@@ -228,6 +229,9 @@ EXPORTS = [
     ("djg_step_agree", C.c_int, [C.c_void_p, C.c_void_p]),
     ("djg_partition_build", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, _P(C.c_void_p)]),
     ("djg_partition_build_method", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, _P(C.c_void_p)]),
+    ("djg_partition_build_box", C.c_int, [_P(djg_scenario_spec), C.c_int32, C.c_int32, _P(C.c_void_p),
+                                          _P(C.c_double)]),
+    ("djg_partition_finish", C.c_int, [C.c_void_p, C.c_double]),
     ("djg_partition_free", None, [C.c_void_p]),
     ("djg_partition_get_info", C.c_int, [C.c_void_p, _P(djg_partition_info)]),
     ("djg_partition_desc", C.c_int, [C.c_void_p, C.c_int32, _P(djg_desc)]),

@@ -201,6 +201,7 @@ struct Mesh {
     int kind = DJG_T4;
     std::vector<Real> nodes;      // 3N
     std::vector<int32_t> conn;    // npe*E
+    int32_t box_div[3] = {0, 0, 0};  // generate_box divisions (0: not a generated box)
     int npe() const { return npe_of(kind); }
     int64_t num_nodes() const { return int64_t(nodes.size() / 3); }
     int64_t num_elements() const { return int64_t(conn.size()) / npe(); }
@@ -209,61 +210,73 @@ struct Mesh {
 
 // generate_box (mesh.hpp:208-264): lexicographic nodes, H8 cells in corner
 // order, T4 six-tet split along the (0,0,0)-(1,1,1) diagonal, odd axis orders
-// swapping the middle pair.
+// swapping the middle pair. The per-node and per-cell pieces are separate
+// so a part of the box can be generated without the rest (build_box_part).
 template <class Real>
-inline Mesh<Real> generate_box(const double extent_in[3], const int32_t div[3], int kind) {
-    const Real ex[3] = {Real(extent_in[0]), Real(extent_in[1]), Real(extent_in[2])};
+inline Real box_coord(const double extent, int64_t i, int64_t n) {
+    return Real(extent) * Real(int(i)) / Real(int(n));
+}
+
+// Global connectivity of cell c (H8: 8 corners; T4: 6 tets x 4).
+inline void box_cell_conn(int kind, const int32_t div[3], int64_t c, int32_t* out) {
+    const int64_t nx = div[0], ny = div[1];
+    const int64_t i = c % nx, j = (c / nx) % ny, k = c / (nx * ny);
+    auto id = [&](int64_t a, int64_t b, int64_t d) { return int32_t(a + (nx + 1) * (b + (ny + 1) * d)); };
+    int32_t corner[2][2][2];
+    for (int dz = 0; dz < 2; ++dz)
+        for (int dy = 0; dy < 2; ++dy)
+            for (int dx = 0; dx < 2; ++dx) corner[dx][dy][dz] = id(i + dx, j + dy, k + dz);
+    if (kind == DJG_H8) {
+        for (int a = 0; a < 8; ++a)
+            out[a] = corner[(kCornerSign[a][0] + 1) / 2][(kCornerSign[a][1] + 1) / 2][(kCornerSign[a][2] + 1) / 2];
+        return;
+    }
+    static constexpr int orders[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    for (int t = 0; t < 6; ++t) {
+        const int* o = orders[t];
+        int s[3] = {0, 0, 0};
+        int32_t path[4];
+        path[0] = corner[0][0][0];
+        for (int q = 0; q < 3; ++q) {
+            s[o[q]] = 1;
+            path[q + 1] = corner[s[0]][s[1]][s[2]];
+        }
+        const bool odd = (o[0] == 0 && o[1] == 2) || (o[0] == 1 && o[1] == 0) || (o[0] == 2 && o[1] == 1);
+        if (odd) std::swap(path[1], path[2]);
+        for (int a = 0; a < 4; ++a) out[t * 4 + a] = path[a];
+    }
+}
+
+inline void check_box(const double extent[3], const int32_t div[3]) {
     for (int i = 0; i < 3; ++i) {
-        if (!(ex[i] > Real(0))) throw ConfigError("box extent must be positive");
+        if (!(extent[i] > 0)) throw ConfigError("box extent must be positive");
         if (div[i] < 1) throw ConfigError("box divisions must be >= 1");
     }
+}
+
+template <class Real>
+inline Mesh<Real> generate_box(const double extent_in[3], const int32_t div[3], int kind) {
+    for (int i = 0; i < 3; ++i)
+        if (!(Real(extent_in[i]) > Real(0))) throw ConfigError("box extent must be positive");
+    check_box(extent_in, div);
     const int64_t nx = div[0], ny = div[1], nz = div[2];
     Mesh<Real> m;
     m.kind = kind;
+    for (int i = 0; i < 3; ++i) m.box_div[i] = div[i];
     m.nodes.resize(size_t(3 * (nx + 1) * (ny + 1) * (nz + 1)));
     size_t w = 0;
     for (int64_t k = 0; k <= nz; ++k)
         for (int64_t j = 0; j <= ny; ++j)
             for (int64_t i = 0; i <= nx; ++i) {
-                m.nodes[w++] = ex[0] * Real(int(i)) / Real(int(nx));
-                m.nodes[w++] = ex[1] * Real(int(j)) / Real(int(ny));
-                m.nodes[w++] = ex[2] * Real(int(k)) / Real(int(nz));
+                m.nodes[w++] = box_coord<Real>(extent_in[0], i, nx);
+                m.nodes[w++] = box_coord<Real>(extent_in[1], j, ny);
+                m.nodes[w++] = box_coord<Real>(extent_in[2], k, nz);
             }
-    const int npe = npe_of(kind);
     const int64_t cells = nx * ny * nz;
-    m.conn.resize(size_t(cells * (kind == DJG_H8 ? 8 : 24)));
-    auto id = [&](int64_t i, int64_t j, int64_t k) { return int32_t(i + (nx + 1) * (j + (ny + 1) * k)); };
-    static constexpr int orders[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
-    (void)npe;
+    const int per = kind == DJG_H8 ? 8 : 24;
+    m.conn.resize(size_t(cells * per));
 #pragma omp parallel for schedule(static)
-    for (int64_t c = 0; c < cells; ++c) {
-        const int64_t i = c % nx, j = (c / nx) % ny, k = c / (nx * ny);
-        int32_t corner[2][2][2];
-        for (int dz = 0; dz < 2; ++dz)
-            for (int dy = 0; dy < 2; ++dy)
-                for (int dx = 0; dx < 2; ++dx) corner[dx][dy][dz] = id(i + dx, j + dy, k + dz);
-        if (kind == DJG_H8) {
-            int32_t* out = m.conn.data() + c * 8;
-            for (int a = 0; a < 8; ++a)
-                out[a] = corner[(kCornerSign[a][0] + 1) / 2][(kCornerSign[a][1] + 1) / 2]
-                                [(kCornerSign[a][2] + 1) / 2];
-            continue;
-        }
-        int32_t* out = m.conn.data() + c * 24;
-        for (int t = 0; t < 6; ++t) {
-            const int* o = orders[t];
-            int s[3] = {0, 0, 0};
-            int32_t path[4];
-            path[0] = corner[0][0][0];
-            for (int q = 0; q < 3; ++q) {
-                s[o[q]] = 1;
-                path[q + 1] = corner[s[0]][s[1]][s[2]];
-            }
-            const bool odd = (o[0] == 0 && o[1] == 2) || (o[0] == 1 && o[1] == 0) || (o[0] == 2 && o[1] == 1);
-            if (odd) std::swap(path[1], path[2]);
-            for (int a = 0; a < 4; ++a) out[t * 4 + a] = path[a];
-        }
-    }
+    for (int64_t c = 0; c < cells; ++c) box_cell_conn(kind, div, c, m.conn.data() + c * per);
     return m;
 }
 
@@ -691,7 +704,58 @@ int METIS_PartMeshDual(int64_t* ne, int64_t* nn, int64_t* eptr, int64_t* eind, i
                        int64_t* epart, int64_t* npart);
 }
 
-enum PartMethod { kPartRcb = 0, kPartMetis = 1 };
+enum PartMethod { kPartRcb = 0, kPartMetis = 1, kPartBox = 2 };
+
+// Box partition (generated boxes only): recursive bisection of the CELL grid
+// -- the longest axis (in cells; ties to the lower axis) split at
+// cells * floor(np/2) / np -- so all elements of a cell share a part and every
+// part is a block of cells. It needs no coordinates and no global mesh: a
+// rank can build its part alone (build_box_part).
+struct CellBlock {
+    int64_t lo[3], hi[3];  // [lo, hi) cells per axis
+};
+
+inline std::vector<CellBlock> box_blocks(const int32_t div[3], int nparts) {
+    std::vector<CellBlock> out(static_cast<size_t>(nparts));
+    struct Job {
+        CellBlock b;
+        int p0, np;
+    };
+    std::vector<Job> stack{{{{0, 0, 0}, {div[0], div[1], div[2]}}, 0, nparts}};
+    while (!stack.empty()) {
+        Job j = stack.back();
+        stack.pop_back();
+        if (j.np == 1) {
+            out[size_t(j.p0)] = j.b;
+            continue;
+        }
+        int ax = 0;
+        for (int i = 1; i < 3; ++i)
+            if (j.b.hi[i] - j.b.lo[i] > j.b.hi[ax] - j.b.lo[ax]) ax = i;
+        const int nl = j.np / 2;
+        const int64_t len = j.b.hi[ax] - j.b.lo[ax];
+        if (len < 2) throw ConfigError("box too small for the requested part count");
+        const int64_t cut = j.b.lo[ax] + std::max<int64_t>(1, std::min<int64_t>(len - 1, len * nl / j.np));
+        Job a = j, b = j;
+        a.b.hi[ax] = cut;
+        a.np = nl;
+        b.b.lo[ax] = cut;
+        b.p0 = j.p0 + nl;
+        b.np = j.np - nl;
+        stack.push_back(b);
+        stack.push_back(a);
+    }
+    return out;
+}
+
+inline int box_part_of_cell(const std::vector<CellBlock>& blocks, int64_t ci, int64_t cj, int64_t ck) {
+    for (size_t p = 0; p < blocks.size(); ++p) {
+        const CellBlock& b = blocks[p];
+        if (ci >= b.lo[0] && ci < b.hi[0] && cj >= b.lo[1] && cj < b.hi[1] && ck >= b.lo[2] && ck < b.hi[2])
+            return int(p);
+    }
+    return 0;
+}
 
 template <class Real>
 inline std::vector<int32_t> metis_parts(const Mesh<Real>& m, int nparts) {
@@ -714,10 +778,51 @@ inline std::vector<int32_t> metis_parts(const Mesh<Real>& m, int nparts) {
 }
 
 template <class Real>
+inline std::vector<int32_t> box_parts(const Mesh<Real>& m, int nparts) {
+    if (m.box_div[0] < 1) throw ConfigError("the box partition needs a generated box mesh");
+    const auto blocks = box_blocks(m.box_div, nparts);
+    const int64_t E = m.num_elements(), nx = m.box_div[0], ny = m.box_div[1];
+    const int per_cell = m.kind == DJG_T4 ? 6 : 1;
+    std::vector<int32_t> part(static_cast<size_t>(E));
+#pragma omp parallel for schedule(static)
+    for (int64_t e = 0; e < E; ++e) {
+        const int64_t c = e / per_cell;
+        part[size_t(e)] = box_part_of_cell(blocks, c % nx, (c / nx) % ny, c / (nx * ny));
+    }
+    return part;
+}
+
+template <class Real>
 inline std::vector<int32_t> element_parts(const Mesh<Real>& m, int nparts, int method) {
     if (method == kPartRcb) return rcb_parts(m, nparts);
     if (method == kPartMetis) return metis_parts(m, nparts);
+    if (method == kPartBox) return box_parts(m, nparts);
     throw ConfigError("unknown partition method");
+}
+
+// Adjacency of a part's local mesh with every node's row in ascending GLOBAL
+// element id (local element ids are interior-first), so an owned node sums
+// its rows in the single-GPU order.
+inline Adjacency local_adjacency(const std::vector<int32_t>& conn, int64_t Nl, int npe,
+                                 const std::vector<int64_t>& elem_l2g) {
+    Adjacency adj = build_adjacency(conn, Nl, npe);
+#pragma omp parallel for schedule(dynamic, 1024)
+    for (int64_t q = 0; q < Nl; ++q) {
+        const int64_t b = adj.offsets[size_t(q)], t = adj.offsets[size_t(q + 1)];
+        std::vector<std::pair<int64_t, int64_t>> row;
+        row.reserve(size_t(t - b));
+        for (int64_t p = b; p < t; ++p) row.emplace_back(elem_l2g[size_t(adj.elem[size_t(p)])], p);
+        std::sort(row.begin(), row.end());
+        std::vector<int64_t> el(size_t(t - b));
+        std::vector<int32_t> lo(size_t(t - b));
+        for (int64_t k = 0; k < t - b; ++k) {
+            el[size_t(k)] = adj.elem[size_t(row[size_t(k)].second)];
+            lo[size_t(k)] = adj.local[size_t(row[size_t(k)].second)];
+        }
+        std::copy(el.begin(), el.end(), adj.elem.begin() + b);
+        std::copy(lo.begin(), lo.end(), adj.local.begin() + b);
+    }
+    return adj;
 }
 
 template <class Real>
@@ -821,24 +926,7 @@ inline PartProblem<Real> build_part(const Problem<Real>& P, int nparts, int part
         std::copy(P.consts.begin() + e * P.nconst, P.consts.begin() + (e + 1) * P.nconst,
                   L.consts.begin() + q * P.nconst);
     }
-    L.adj = build_adjacency(L.mesh.conn, Nl, npe);
-    // rows in ascending GLOBAL element id (local ids are interior-first)
-#pragma omp parallel for schedule(dynamic, 1024)
-    for (int64_t q = 0; q < Nl; ++q) {
-        const int64_t b = L.adj.offsets[size_t(q)], t = L.adj.offsets[size_t(q + 1)];
-        std::vector<std::pair<int64_t, int64_t>> row;
-        row.reserve(size_t(t - b));
-        for (int64_t p = b; p < t; ++p) row.emplace_back(R.elem_l2g[size_t(L.adj.elem[size_t(p)])], p);
-        std::sort(row.begin(), row.end());
-        std::vector<int64_t> el(size_t(t - b));
-        std::vector<int32_t> lo(size_t(t - b));
-        for (int64_t k = 0; k < t - b; ++k) {
-            el[size_t(k)] = L.adj.elem[size_t(row[size_t(k)].second)];
-            lo[size_t(k)] = L.adj.local[size_t(row[size_t(k)].second)];
-        }
-        std::copy(el.begin(), el.end(), L.adj.elem.begin() + b);
-        std::copy(lo.begin(), lo.end(), L.adj.local.begin() + b);
-    }
+    L.adj = local_adjacency(L.mesh.conn, Nl, npe, R.elem_l2g);
     // halo: parts referencing each node (as a local node of theirs)
     // recv: my ghosts, from their owners
     std::vector<std::vector<int32_t>> recv(static_cast<size_t>(nparts)), send(static_cast<size_t>(nparts));
@@ -869,6 +957,331 @@ inline PartProblem<Real> build_part(const Problem<Real>& P, int nparts, int part
         R.halo.recv_off.push_back(int64_t(R.halo.recv_nodes.size()));
     }
     return R;
+}
+
+
+// ---------------------------------------------------------------- part-local build
+//
+// One part of a generated box, built without the global mesh or the global
+// problem (multi-GPU setup at scale: each rank builds only its part, SURVEY
+// §8(e)). With the box partition (box_blocks) everything the global path
+// derives from the whole mesh has a closed form here: the lowest-id element
+// of node (i, j, k) lies in cell (max(i-1,0), max(j-1,0), max(k-1,0)), so a
+// node's owner is that cell's part; the elements touching an owned node lie
+// in the part's cell block grown by one cell on its low sides. The result is
+// identical to build_part(build_problem(spec), nparts, part, kPartBox) on
+// every owned node and local element (tests/test_partition.py) except the
+// time-step data, which needs the GLOBAL minimum characteristic length:
+// build_box_part returns this part's minimum, the caller reduces it over the
+// parts (MIN is exact) and finish_box_part completes dt, alpha, the BCs and
+// the update coefficients.
+template <class Real>
+inline PartProblem<Real> build_box_part(const djg_scenario_spec& s, int nparts, int part, Real& local_lmin) {
+    if (s.nodes != nullptr) throw ConfigError("the part-local build needs a generated box (no explicit mesh)");
+    if (s.kind != DJG_T4 && s.kind != DJG_H8) throw ConfigError("unknown element kind");
+    if (nparts < 1 || part < 0 || part >= nparts) throw ConfigError("invalid part index");
+    if (s.bc_mode != 0 && s.bc_mode != 1) throw ConfigError("the part-local build supports the plane BCs (bc_mode 0 / 1)");
+    check_box(s.extent, s.divisions);
+    for (int i = 0; i < 3; ++i)
+        if (!(Real(s.extent[i]) > Real(0))) throw ConfigError("box extent must be positive");
+    const int kind = s.kind, npe = npe_of(kind), per_cell = kind == DJG_T4 ? 6 : 1;
+    const int32_t* div = s.divisions;
+    const int64_t nx = div[0], ny = div[1], nz = div[2];
+    const int64_t N = (nx + 1) * (ny + 1) * (nz + 1), cells = nx * ny * nz;
+    if (int64_t(npe) * cells * per_cell > INT32_MAX || N > INT32_MAX) throw ConfigError("box too large for int32 ids");
+    const auto blocks = box_blocks(div, nparts);
+    const CellBlock& B = blocks[size_t(part)];
+    auto node_ijk = [&](int64_t n, int64_t& i, int64_t& j, int64_t& k) {
+        i = n % (nx + 1);
+        j = (n / (nx + 1)) % (ny + 1);
+        k = n / ((nx + 1) * (ny + 1));
+    };
+    auto owner = [&](int64_t n) {
+        int64_t i, j, k;
+        node_ijk(n, i, j, k);
+        return box_part_of_cell(blocks, std::max<int64_t>(i - 1, 0), std::max<int64_t>(j - 1, 0),
+                                std::max<int64_t>(k - 1, 0));
+    };
+    // owned node ranges per axis (inclusive): max(i-1, 0) in [lo, hi)
+    int64_t a0[3], a1[3];
+    for (int ax = 0; ax < 3; ++ax) {
+        a0[ax] = B.lo[ax] == 0 ? 0 : B.lo[ax] + 1;
+        a1[ax] = B.hi[ax];
+    }
+    PartProblem<Real> R;
+    R.nparts = nparts;
+    R.part = part;
+    R.global_nodes = N;
+    R.global_elements = cells * per_cell;
+    for (int64_t k = a0[2]; k <= a1[2]; ++k)
+        for (int64_t j = a0[1]; j <= a1[1]; ++j)
+            for (int64_t i = a0[0]; i <= a1[0]; ++i) R.node_l2g.push_back(i + (nx + 1) * (j + (ny + 1) * k));
+    R.num_owned = int64_t(R.node_l2g.size());
+    auto is_owned = [&](int64_t n) {
+        int64_t i, j, k;
+        node_ijk(n, i, j, k);
+        return i >= a0[0] && i <= a1[0] && j >= a0[1] && j <= a1[1] && k >= a0[2] && k <= a1[2];
+    };
+    // candidate cells: the part's block grown by one cell on the low sides
+    int64_t c0[3], c1[3];
+    for (int ax = 0; ax < 3; ++ax) {
+        c0[ax] = std::max<int64_t>(a0[ax] - 1, 0);
+        c1[ax] = std::min<int64_t>(a1[ax], int64_t(div[ax]) - 1);
+    }
+    std::vector<int64_t> interior, boundary;  // global element ids, ascending
+    std::vector<int32_t> gconn;               // global connectivity of the local elements, by global id
+    std::vector<int64_t> order;               // global ids in ascending order (parallel to gconn)
+    std::vector<int32_t> ghosts;
+    {
+        // one cell layer (ck) per work item, concatenated in ck order: the
+        // element ids stay ascending
+        const int64_t nk = c1[2] - c0[2] + 1;
+        struct Layer {
+            std::vector<int64_t> interior, boundary, order;
+            std::vector<int32_t> gconn, ghosts;
+        };
+        std::vector<Layer> layers(static_cast<size_t>(std::max<int64_t>(nk, 0)));
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int64_t l = 0; l < nk; ++l) {
+            const int64_t ck = c0[2] + l;
+            Layer& Ly = layers[size_t(l)];
+            int32_t cc[24];
+            for (int64_t cj = c0[1]; cj <= c1[1]; ++cj)
+                for (int64_t ci = c0[0]; ci <= c1[0]; ++ci) {
+                    const int64_t c = ci + nx * (cj + ny * ck);
+                    box_cell_conn(kind, div, c, cc);
+                    for (int t = 0; t < per_cell; ++t) {
+                        bool touches = false, ghost = false;
+                        for (int a = 0; a < npe; ++a) {
+                            const bool o = is_owned(cc[t * npe + a]);
+                            touches |= o;
+                            ghost |= !o;
+                        }
+                        if (!touches) continue;
+                        const int64_t e = c * per_cell + t;
+                        Ly.order.push_back(e);
+                        Ly.gconn.insert(Ly.gconn.end(), cc + t * npe, cc + (t + 1) * npe);
+                        (ghost ? Ly.boundary : Ly.interior).push_back(e);
+                        if (ghost)
+                            for (int a = 0; a < npe; ++a)
+                                if (!is_owned(cc[t * npe + a])) Ly.ghosts.push_back(cc[t * npe + a]);
+                    }
+                }
+        }
+        size_t ni = 0, nb = 0, no = 0, ng = 0;
+        for (const Layer& Ly : layers) {
+            ni += Ly.interior.size();
+            nb += Ly.boundary.size();
+            no += Ly.order.size();
+            ng += Ly.ghosts.size();
+        }
+        interior.reserve(ni);
+        boundary.reserve(nb);
+        order.reserve(no);
+        gconn.reserve(no * size_t(npe));
+        ghosts.reserve(ng);
+        for (Layer& Ly : layers) {
+            interior.insert(interior.end(), Ly.interior.begin(), Ly.interior.end());
+            boundary.insert(boundary.end(), Ly.boundary.begin(), Ly.boundary.end());
+            order.insert(order.end(), Ly.order.begin(), Ly.order.end());
+            gconn.insert(gconn.end(), Ly.gconn.begin(), Ly.gconn.end());
+            ghosts.insert(ghosts.end(), Ly.ghosts.begin(), Ly.ghosts.end());
+            Ly = Layer{};
+        }
+    }
+    std::sort(ghosts.begin(), ghosts.end());
+    ghosts.erase(std::unique(ghosts.begin(), ghosts.end()), ghosts.end());
+    R.node_l2g.insert(R.node_l2g.end(), ghosts.begin(), ghosts.end());
+    R.interior_elements = int64_t(interior.size());
+    R.elem_l2g = std::move(interior);
+    R.elem_l2g.insert(R.elem_l2g.end(), boundary.begin(), boundary.end());
+    const int64_t Nl = int64_t(R.node_l2g.size()), El = int64_t(R.elem_l2g.size());
+    R.elem_owned.resize(size_t(El));
+    for (int64_t q = 0; q < El; ++q) {
+        const int64_t c = R.elem_l2g[size_t(q)] / per_cell;
+        R.elem_owned[size_t(q)] = box_part_of_cell(blocks, c % nx, (c / nx) % ny, c / (nx * ny)) == part;
+        R.owned_elements += R.elem_owned[size_t(q)];
+    }
+    // global -> local node ids: owned nodes form a block; ghosts by search
+    const int64_t bx = a1[0] - a0[0] + 1, by = a1[1] - a0[1] + 1;
+    auto g2l = [&](int64_t n) -> int32_t {
+        int64_t i, j, k;
+        node_ijk(n, i, j, k);
+        if (is_owned(n)) return int32_t((i - a0[0]) + bx * ((j - a0[1]) + by * (k - a0[2])));
+        return int32_t(R.num_owned + (std::lower_bound(ghosts.begin(), ghosts.end(), int32_t(n)) - ghosts.begin()));
+    };
+    // local problem
+    Problem<Real>& L = R.local;
+    L.policy = s.policy;
+    L.mat = Material<Real>::from(s.material);
+    L.mesh.kind = kind;
+    L.mesh.nodes.resize(size_t(3 * Nl));
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < Nl; ++q) {
+        int64_t i, j, k;
+        node_ijk(R.node_l2g[size_t(q)], i, j, k);
+        L.mesh.nodes[size_t(3 * q + 0)] = box_coord<Real>(s.extent[0], i, nx);
+        L.mesh.nodes[size_t(3 * q + 1)] = box_coord<Real>(s.extent[1], j, ny);
+        L.mesh.nodes[size_t(3 * q + 2)] = box_coord<Real>(s.extent[2], k, nz);
+    }
+    L.mesh.conn.resize(size_t(El * npe));
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < El; ++q) {
+        const int64_t pos = std::lower_bound(order.begin(), order.end(), R.elem_l2g[size_t(q)]) - order.begin();
+        for (int a = 0; a < npe; ++a) L.mesh.conn[size_t(q * npe + a)] = g2l(gconn[size_t(pos * npe + a)]);
+    }
+    std::vector<int32_t>().swap(gconn);  // (peak host memory: the global-id copies go before the records)
+    std::vector<int64_t>().swap(order);
+    const ConstLayout CL(kind, L.mat.model);
+    L.nconst = CL.count;
+    V3<Real> fa{0, 0, 0}, fb{0, 0, 0};
+    if (L.mat.needs_fibre_a()) fa = Material<Real>::unit(L.mat.fa);
+    if (L.mat.needs_fibre_b()) fb = Material<Real>::unit(L.mat.fb);
+    L.c_hg = Real(s.c_hg);
+    const Shape<Real> D(kind);
+    L.consts.assign(size_t(El) * size_t(CL.count), Real(0));
+    int64_t bad = -1;
+    Real lmin = std::numeric_limits<Real>::max();
+#pragma omp parallel reduction(max : bad)
+    {
+        Real lm = std::numeric_limits<Real>::max();
+#pragma omp for schedule(static) nowait
+        for (int64_t q = 0; q < El; ++q) {
+            V3<Real> x[8];
+            for (int a = 0; a < npe; ++a) x[a] = L.mesh.node(L.mesh.conn[size_t(q * npe + a)]);
+            Real* rec = L.consts.data() + size_t(q) * CL.count;
+            if (!element_record(x, D, L.mat, fa, fb, L.c_hg, CL, rec)) {
+                bad = std::max<int64_t>(bad, R.global_elements - R.elem_l2g[size_t(q)]);
+                continue;
+            }
+            lm = std::min(lm, char_length(x, kind, rec[CL.V0]));
+        }
+#pragma omp critical
+        lmin = std::min(lmin, lm);
+    }
+    if (bad >= 0) throw MeshError("non-positive reference Jacobian determinant", long(R.global_elements - bad));
+    local_lmin = lmin;
+    L.adj = local_adjacency(L.mesh.conn, Nl, npe, R.elem_l2g);
+    // lump_mass: owned nodes hold all their elements (ascending global id);
+    // ghost masses are partial and never used (only owned nodes are updated)
+    L.mass.assign(size_t(Nl), Real(0));
+#pragma omp parallel for schedule(static)
+    for (int64_t q = 0; q < Nl; ++q) {
+        Real acc = Real(0);
+        for (int64_t p = L.adj.offsets[size_t(q)]; p < L.adj.offsets[size_t(q + 1)]; ++p)
+            acc += L.mat.rho * L.consts[size_t(L.adj.elem[size_t(p)]) * CL.count + CL.V0] / Real(npe);
+        L.mass[size_t(q)] = acc;
+    }
+    // halo: recv = my ghosts grouped by owner; send = my owned nodes that
+    // another part's elements touch (the elements around the node)
+    std::vector<std::vector<int32_t>> recv(static_cast<size_t>(nparts)), send(static_cast<size_t>(nparts));
+    for (int64_t q = R.num_owned; q < Nl; ++q) recv[size_t(owner(R.node_l2g[size_t(q)]))].push_back(int32_t(q));
+    std::vector<std::vector<int32_t>> need(static_cast<size_t>(R.num_owned));
+#pragma omp parallel for schedule(dynamic, 4096)
+    for (int64_t q = 0; q < R.num_owned; ++q) {
+        const int64_t n = R.node_l2g[size_t(q)];
+        int64_t i, j, k;
+        node_ijk(n, i, j, k);
+        // interior of the owned block: every neighbour is owned here
+        if (i > a0[0] && i < a1[0] && j > a0[1] && j < a1[1] && k > a0[2] && k < a1[2]) continue;
+        int32_t cc[24];
+        std::vector<int32_t> parts;
+        for (int64_t ck = std::max<int64_t>(k - 1, 0); ck <= std::min<int64_t>(k, nz - 1); ++ck)
+            for (int64_t cj = std::max<int64_t>(j - 1, 0); cj <= std::min<int64_t>(j, ny - 1); ++cj)
+                for (int64_t ci = std::max<int64_t>(i - 1, 0); ci <= std::min<int64_t>(i, nx - 1); ++ci) {
+                    box_cell_conn(kind, div, ci + nx * (cj + ny * ck), cc);
+                    for (int t = 0; t < per_cell; ++t) {
+                        const int32_t* ec = cc + t * npe;
+                        if (std::find(ec, ec + npe, int32_t(n)) == ec + npe) continue;
+                        for (int a = 0; a < npe; ++a) {
+                            const int o = owner(ec[a]);
+                            if (o != part) parts.push_back(o);
+                        }
+                    }
+                }
+        std::sort(parts.begin(), parts.end());
+        parts.erase(std::unique(parts.begin(), parts.end()), parts.end());
+        need[size_t(q)] = std::move(parts);
+    }
+    for (int64_t q = 0; q < R.num_owned; ++q)
+        for (int32_t o : need[size_t(q)]) send[size_t(o)].push_back(int32_t(q));
+    R.halo.send_off.push_back(0);
+    R.halo.recv_off.push_back(0);
+    for (int q = 0; q < nparts; ++q) {
+        if (q == part || (send[size_t(q)].empty() && recv[size_t(q)].empty())) continue;
+        R.halo.neighbors.push_back(q);
+        R.halo.send_nodes.insert(R.halo.send_nodes.end(), send[size_t(q)].begin(), send[size_t(q)].end());
+        R.halo.recv_nodes.insert(R.halo.recv_nodes.end(), recv[size_t(q)].begin(), recv[size_t(q)].end());
+        R.halo.send_off.push_back(int64_t(R.halo.send_nodes.size()));
+        R.halo.recv_off.push_back(int64_t(R.halo.recv_nodes.size()));
+    }
+    return R;
+}
+
+// Time-step data of a part-local box (build_problem's, from the GLOBAL
+// minimum characteristic length `lmin`): critical dt, dt, relaxation alpha
+// (the box's bounding box: its coordinates at 0 and at the last division),
+// the zmin / zmax plane BCs (the same predicate as plane_nodes) and the
+// update coefficients.
+template <class Real>
+inline void finish_box_part(PartProblem<Real>& R, const djg_scenario_spec& s, Real lmin) {
+    Problem<Real>& P = R.local;
+    if (!(lmin > Real(0))) throw MeshError("degenerate element with zero characteristic length");
+    P.c_wave = wave_speed(P.mat);
+    P.crit_dt = lmin / P.c_wave;
+    P.dt = s.dt > 0 ? Real(s.dt) : Real(s.safety) * P.crit_dt;
+    if (!(P.dt > Real(0))) throw ConfigError("time step must be positive");
+    Real lo[3], hi[3];
+    for (int ax = 0; ax < 3; ++ax) {
+        lo[ax] = box_coord<Real>(s.extent[ax], 0, s.divisions[ax]);
+        hi[ax] = box_coord<Real>(s.extent[ax], s.divisions[ax], s.divisions[ax]);
+    }
+    if (s.alpha_mode == 0) {
+        const Real mu = P.mat.shear_modulus();
+        const Real e_mod = 9 * P.mat.kappa * mu / (3 * P.mat.kappa + mu);
+        const Real c_bar = std::sqrt(e_mod / P.mat.rho);
+        const Real l = std::max({hi[0] - lo[0], hi[1] - lo[1], hi[2] - lo[2]});
+        if (!(l > Real(0))) throw ConfigError("mesh has zero extent");
+        P.alpha = Real(M_PI) * c_bar / l;
+    } else {
+        P.alpha = Real(s.alpha);
+    }
+    const int64_t Nl = P.mesh.num_nodes();
+    P.dof_kind.assign(size_t(3 * Nl), uint8_t(DJG_FREE));
+    P.dof_target.assign(size_t(3 * Nl), Real(0));
+    P.dof_t_total.assign(size_t(3 * Nl), Real(1));
+    P.ramp_t_total = 0;
+    if (s.bc_mode == 1) {
+        const auto bottom = plane_nodes(P.mesh, 2, false, lo, hi);
+        const auto top = plane_nodes(P.mesh, 2, true, lo, hi);
+        for (int32_t n : bottom) {
+            if (s.fix_all_axes) {
+                P.dof_kind[size_t(3 * n + 0)] = DJG_FIXED;
+                P.dof_kind[size_t(3 * n + 1)] = DJG_FIXED;
+            }
+            P.dof_kind[size_t(3 * n + 2)] = DJG_FIXED;
+        }
+        P.ramp_t_total = P.dt * Real(s.ramp_steps);
+        if (!(P.ramp_t_total > Real(0))) throw ConfigError("ramp duration must be positive");
+        for (int32_t n : top) {
+            if (P.dof_kind[size_t(3 * n + 2)] != DJG_FREE)
+                throw ConfigError("node axis 2 appears in more than one boundary condition");
+            P.dof_kind[size_t(3 * n + 2)] = DJG_PRESCRIBED;
+            P.dof_target[size_t(3 * n + 2)] = Real(s.target);
+            P.dof_t_total[size_t(3 * n + 2)] = P.ramp_t_total;
+        }
+    }
+    const Real denom = Real(1) + P.alpha * P.dt / 2;
+    P.c2 = Real(2) / denom;
+    P.c3 = -(Real(1) - P.alpha * P.dt / 2) / denom;
+    P.c1.assign(size_t(Nl), Real(0));
+    P.massless.assign(size_t(Nl), 0);
+    for (int64_t n = 0; n < Nl; ++n) {
+        if (P.mass[size_t(n)] > Real(0))
+            P.c1[size_t(n)] = P.dt * P.dt / (P.mass[size_t(n)] * denom);
+        else
+            P.massless[size_t(n)] = 1;
+    }
 }
 
 }  // namespace djg

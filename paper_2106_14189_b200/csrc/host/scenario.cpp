@@ -157,6 +157,7 @@ struct djg_scenario {
 
 struct djg_partition {
     std::variant<djg::PartProblem<float>, djg::PartProblem<double>> p;
+    djg_scenario_spec spec{};  // part-local build: the box spec (its pointers are not kept)
 };
 
 extern "C" {
@@ -290,6 +291,50 @@ int djg_partition_build_method(const djg_scenario* sc, int32_t nparts, int32_t p
             },
             sc->p);
         *out = pp.release();
+        return DJG_OK;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return DJG_E_CONFIG;
+    }
+}
+
+int djg_partition_build_box(const djg_scenario_spec* spec, int32_t nparts, int32_t part, djg_partition** out,
+                            double* local_min_length) {
+    if (!spec || !out) return DJG_E_CONFIG;
+    *out = nullptr;
+    try {
+        auto pp = std::make_unique<djg_partition>();
+        double lmin = 0;
+        if (spec->precision == 4) {
+            float l = 0;
+            pp->p = djg::build_box_part<float>(*spec, nparts, part, l);
+            lmin = l;
+        } else if (spec->precision == 8) {
+            double l = 0;
+            pp->p = djg::build_box_part<double>(*spec, nparts, part, l);
+            lmin = l;
+        } else {
+            throw djg::ConfigError("precision must be 4 or 8");
+        }
+        pp->spec = *spec;
+        if (local_min_length) *local_min_length = lmin;
+        *out = pp.release();
+        return DJG_OK;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return DJG_E_CONFIG;
+    }
+}
+
+int djg_partition_finish(djg_partition* p, double global_min_length) {
+    if (!p) return DJG_E_CONFIG;
+    try {
+        std::visit(
+            [&](auto& R) {
+                using Real = typename std::decay_t<decltype(R.local.consts)>::value_type;
+                djg::finish_box_part<Real>(R, p->spec, Real(global_min_length));
+            },
+            p->p);
         return DJG_OK;
     } catch (const std::exception& e) {
         g_error = e.what();

@@ -30,13 +30,64 @@ def _lib():
 
 
 class Partition:
-    """Host-side local problem of part `part` of `nparts`."""
+    """Host-side local problem of part `part` of `nparts`: extracted from a
+    built global Scenario, or (Partition.box_local) built alone from a box
+    spec without the global mesh."""
 
     def __init__(self, scenario: Scenario, nparts: int, part: int, method: str = "rcb"):
         self.scenario = scenario
         h = C.c_void_p()
         if _lib().djg_partition_build_method(scenario._h, nparts, part, A.PART_METHODS[method], C.byref(h)) != A.DJG_OK:
             raise ConfigError(_lib().djg_scenario_error().decode())
+        self._load(h, scenario.dtype, scenario.npe, scenario.nconst)
+        self.dt = scenario.dt
+
+    @classmethod
+    def box_local(cls, spec, nparts: int, part: int, reduce_min=None) -> "Partition":
+        """Part `part` of the box partition (DJG_PART_BOX) of a generated-box
+        spec, built from the spec alone (djg_partition_build_box): the rank's
+        host memory and setup time scale with its part, not the mesh.
+        reduce_min(x) returns the minimum of x over all parts (the global
+        minimum characteristic length behind dt); None for a single part."""
+        obj = cls.__new__(cls)
+        obj.scenario = None
+        h = C.c_void_p()
+        lmin = C.c_double()
+        if _lib().djg_partition_build_box(spec.ref(), nparts, part, C.byref(h), C.byref(lmin)) != A.DJG_OK:
+            raise ConfigError(_lib().djg_scenario_error().decode())
+        g = reduce_min(lmin.value) if reduce_min is not None else lmin.value
+        if _lib().djg_partition_finish(h, g) != A.DJG_OK:
+            _lib().djg_partition_free(h)
+            raise ConfigError(_lib().djg_scenario_error().decode())
+        obj._load(h, spec.dtype, spec.npe, A.const_count(spec.c.kind, spec.c.material.model))
+        obj.dt = obj.desc().dt
+        return obj
+
+    @classmethod
+    def box_local_all(cls, spec, nparts: int) -> list["Partition"]:
+        """Every part of the box partition built part-locally in one process
+        (single-device emulation): the minimum characteristic length is
+        reduced over the parts' own builds, as ranks would with allreduce."""
+        hs, mins = [], []
+        for p in range(nparts):
+            h = C.c_void_p()
+            lmin = C.c_double()
+            if _lib().djg_partition_build_box(spec.ref(), nparts, p, C.byref(h), C.byref(lmin)) != A.DJG_OK:
+                raise ConfigError(_lib().djg_scenario_error().decode())
+            hs.append(h)
+            mins.append(lmin.value)
+        out = []
+        for h in hs:
+            if _lib().djg_partition_finish(h, min(mins)) != A.DJG_OK:
+                raise ConfigError(_lib().djg_scenario_error().decode())
+            obj = cls.__new__(cls)
+            obj.scenario = None
+            obj._load(h, spec.dtype, spec.npe, A.const_count(spec.c.kind, spec.c.material.model))
+            obj.dt = obj.desc().dt
+            out.append(obj)
+        return out
+
+    def _load(self, h, dtype, npe: int, nconst: int):
         self._h = h
         i = A.djg_partition_info()
         _lib().djg_partition_get_info(self._h, C.byref(i))
@@ -57,10 +108,9 @@ class Partition:
         self.num_owned = i.num_owned
         self.num_nodes = i.num_nodes
         self.num_elements = i.num_elements
-        self.dtype = scenario.dtype
-        self.npe = scenario.npe
-        self.nconst = scenario.nconst
-        self.dt = scenario.dt
+        self.dtype = dtype
+        self.npe = npe
+        self.nconst = nconst
 
     def image(self) -> dict:
         n, e, npe, nc, dt = self.num_nodes, self.num_elements, self.npe, self.nconst, self.dtype
@@ -204,6 +254,12 @@ def peer_destinations(halos: list, me: int):
     return node, part, index
 
 
+def _spec_of(scenario):
+    """The Spec behind a Scenario (or a Spec itself): the part-local build
+    reads only the box spec."""
+    return getattr(scenario, "spec", scenario)
+
+
 def _halo(p: "Partition"):
     return (p.neighbors.copy(), p.send_off.copy(), p.recv_off.copy(), p.send_nodes.copy(), p.recv_nodes.copy(),
             p.num_nodes)
@@ -233,7 +289,16 @@ class DistributedEngine:
         self.world = dist.get_world_size(group)
         self.device = device
         self.engine_comm = engine_comm
-        self.part = Partition(scenario, self.world, self.rank, method)
+        if method == "box-local":
+            # this rank's part from the box spec alone (no global mesh); the
+            # global minimum characteristic length through the group
+            def reduce_min(x):
+                vals = [None] * self.world
+                dist.all_gather_object(vals, float(x), group=group)
+                return min(vals)
+            self.part = Partition.box_local(_spec_of(scenario), self.world, self.rank, reduce_min)
+        else:
+            self.part = Partition(scenario, self.world, self.rank, method)
         self.eng = PartEngine(self.part, device, flags)
         tdt = _torch_dtype(self.part.dtype)
         dev = torch.device("cuda", device)
@@ -362,7 +427,10 @@ class EmulatedParts:
                  transport: str = "copy"):
         import torch
         self.torch = torch
-        self.parts = [Partition(scenario, nparts, p, method) for p in range(nparts)]
+        if method == "box-local":
+            self.parts = Partition.box_local_all(_spec_of(scenario), nparts)
+        else:
+            self.parts = [Partition(scenario, nparts, p, method) for p in range(nparts)]
         self.engs = [PartEngine(p, device, flags) for p in self.parts]
         self.transport = transport
         if transport == "p2p":
@@ -375,7 +443,7 @@ class EmulatedParts:
         self.send = [torch.zeros((max(p.send_nodes.size, 1), 4), dtype=tdt, device=dev) for p in self.parts]
         self.recv = [torch.zeros((max(p.recv_nodes.size, 1), 4), dtype=tdt, device=dev) for p in self.parts]
         self.status = [torch.zeros(3, dtype=torch.int64, device=dev) for _ in self.parts]
-        self.global_nodes = scenario.num_nodes
+        self.global_nodes = self.parts[0].info["global_nodes"]
 
     def _sync(self):
         for e in self.engs:

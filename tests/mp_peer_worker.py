@@ -37,8 +37,9 @@ def single(spec, steps):
     return u, up, r
 
 
-def case(name, spec, steps):
-    de = DistributedEngine(Scenario(spec), device=0, transport="p2p")
+def case(name, spec, steps, method="rcb"):
+    de = DistributedEngine(spec if method == "box-local" else Scenario(spec), device=0, transport="p2p",
+                           method=method)
     r = de.step_lockstep(steps)
     g = de.gather_global()
     reps = [None] * dist.get_world_size()
@@ -55,6 +56,8 @@ def case(name, spec, steps):
 
 case("smooth_t4_f32", box_spec(kind="T4", model="NH", divisions=8, precision=4, ramp_steps=120), 120)
 case("smooth_h8_ti_f64", box_spec(kind="H8", model="TI", divisions=7, precision=8, ramp_steps=80), 80)
+case("box_local_t4_f32", box_spec(kind="T4", model="NH", divisions=(9, 8, 10), precision=4, ramp_steps=100), 100,
+     method="box-local")
 case("abort_inversion", box_spec(kind="T4", divisions=3, extent=(0.1,) * 3, precision=8, target=-0.09,
                                  ramp_steps=3, fix_all_axes=True), 50)
 sc0 = Scenario(box_spec(kind="T4", divisions=4, extent=(0.1, 0.1, 0.1), precision=8))

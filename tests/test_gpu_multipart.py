@@ -85,6 +85,22 @@ def test_parts_metis_partition_bitwise():
             assert np.array_equal(u, u1) and np.array_equal(up, up1)
 
 
+@pytest.mark.parametrize("transport", ["copy", "p2p"])
+@pytest.mark.parametrize("nparts", [2, 3, 8])
+@pytest.mark.parametrize("kind,model,prec", [("T4", "NH", 4), ("H8", "TI", 8)])
+def test_parts_box_local_bitwise(kind, model, prec, nparts, transport):
+    """Parts built part-locally from the box spec (no global mesh or problem,
+    Partition.box_local): bit-identical to one engine."""
+    spec = box_spec(kind=kind, model=model, divisions=(9, 7, 8), precision=prec, ramp_steps=150)
+    u1, up1, r1 = single(spec, 150)
+    em = EmulatedParts(spec, nparts, method="box-local", transport=transport)
+    reps = em.step(150, overlap=transport == "copy")
+    u, up, step = em.global_state()
+    em.close()
+    assert all(r.status == 0 for r in reps) and step == 150
+    assert np.array_equal(u, u1) and np.array_equal(up, up1)
+
+
 @pytest.mark.parametrize("overlap", [False, True, "p2p"], ids=["sequential", "overlapped", "peer-memory"])
 def test_parts_agree_on_inversion(overlap):
     """The crushing case of test_solver.cpp:214-241 split in two: every part

@@ -37,7 +37,7 @@ def test_peer_memory_two_processes_one_gpu():
     assert len(lines) == 1, p.stdout[-2000:] + p.stderr[-2000:]
     res = json.loads(lines[0])
     assert res["world"] == 2
-    for name in ("smooth_t4_f32", "smooth_h8_ti_f64", "abort_inversion", "skip_and_report"):
+    for name in ("smooth_t4_f32", "smooth_h8_ti_f64", "box_local_t4_f32", "abort_inversion", "skip_and_report"):
         c = res[name]
         assert c["halo_send"] > 0, (name, c)
         assert c["bitwise_u"] and c["bitwise_u_prev"] and c["reports_match"], (name, c)

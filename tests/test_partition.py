@@ -179,3 +179,55 @@ def test_gloo_two_ranks_bitwise_equal_single_process(method):
         assert np.array_equal(u, ur[ids]) and np.array_equal(up, upr[ids])
         covered[ids] = True
     assert covered.all() and np.abs(ur).max() > 0.05
+
+
+@pytest.mark.parametrize("prec", [4, 8])
+@pytest.mark.parametrize("kind,model", [("T4", "NH"), ("H8", "TI"), ("T4", "OT")])
+@pytest.mark.parametrize("nparts", [1, 2, 3, 5, 8])
+def test_box_local_build_equals_global_extraction(kind, model, nparts, prec):
+    """Partition.box_local builds part p of the box partition from the spec
+    alone; it must equal the part djg_partition_build_method(DJG_PART_BOX)
+    extracts from the global problem: maps, halo lists, element ownership,
+    local connectivity, coordinates, records and CSR, and on every owned
+    node the mass, update coefficient and BCs (ghost-node masses are partial
+    locally and never used: only owned nodes are updated)."""
+    spec = box_spec(kind=kind, model=model, divisions=(7, 5, 6), precision=prec, ramp_steps=100)
+    sc = Scenario(spec)
+    parts = [Partition.box_local(spec, nparts, p) for p in range(nparts)]
+    for p in range(nparts):
+        glob = Partition(sc, nparts, p, "box")
+        loc = Partition.box_local(spec, nparts, p,
+                                  reduce_min=lambda x: _global_lmin(spec, nparts))
+        assert loc.info == glob.info
+        for f in ("node_l2g", "elem_l2g", "elem_owned", "neighbors", "send_off", "recv_off", "send_nodes",
+                  "recv_nodes"):
+            assert np.array_equal(getattr(loc, f), getattr(glob, f)), f
+        a, b = loc.image(), glob.image()
+        no = loc.num_owned
+        for f in ("nodes", "conn", "csr_offsets", "csr_elem", "csr_local", "consts"):
+            assert np.array_equal(a[f], b[f]), f
+        for f in ("mass", "c1", "massless"):
+            assert np.array_equal(a[f][:no], b[f][:no]), f
+        for f in ("dof_kind", "dof_target", "dof_t_total"):
+            assert np.array_equal(a[f][: 3 * no], b[f][: 3 * no]), f
+        da, db = loc.desc(), glob.desc()
+        for f in ("dt", "c2", "c3"):
+            assert getattr(da, f) == getattr(db, f), f
+    # every element is owned by exactly one part; owned nodes cover the mesh
+    owned = np.concatenate([p.node_l2g[: p.num_owned] for p in parts])
+    assert np.array_equal(np.sort(owned), np.arange(sc.num_nodes))
+    oe = np.concatenate([p.elem_l2g[p.elem_owned.astype(bool)] for p in parts])
+    assert np.array_equal(np.sort(oe), np.arange(sc.num_elements))
+
+
+def _global_lmin(spec, nparts):
+    """min over the parts of their local minimum characteristic length (what
+    a rank obtains with an allreduce(MIN))."""
+    out = []
+    for p in range(nparts):
+        h = A.C.c_void_p()
+        x = A.C.c_double()
+        assert A.load_library().djg_partition_build_box(spec.ref(), nparts, p, A.C.byref(h), A.C.byref(x)) == 0
+        A.load_library().djg_partition_free(h)
+        out.append(x.value)
+    return min(out)

@@ -99,6 +99,12 @@ typedef struct djg_desc {
                                     paper's comparison path; record built on the device */
 #define DJG_FLAG_NO_PIPE 128u    /* one-shot element kernel instead of the bulk-copy
                                     pipelined one (k_element_pipe); bit-identical */
+#define DJG_FLAG_NO_FUSED 512u  /* keep the two-kernel step (element kernel + gather/update)
+                                    on a generated box, where the default is one fused
+                                    kernel per step (k_box_step, no force slots in HBM)
+                                    once the box fills the GPU */
+#define DJG_FLAG_FUSED 1024u     /* the fused box step on any generated T4 box it supports,
+                                    however small (bit-identical either way) */
 #define DJG_FLAG_WINDOW 256u     /* pipelined element kernel with node windows: each
                                     tile's node rows staged in shared memory by bulk
                                     copies next to its slot positions (k_element_win);
@@ -305,6 +311,8 @@ typedef struct djg_engine_info {
     int32_t pipelined;          /* element kernel streams tiles through shared memory */
     int32_t windowed;           /* ... with each tile's node rows staged as windows */
     int64_t window_tiles;       /* tiles whose nodes fit a window (the rest gather) */
+    int32_t fused;              /* 1: one fused kernel per step (generated box, k_box_step) */
+    int32_t _pad_fused;
 } djg_engine_info;
 int djg_get_info(djg_engine* eng, djg_engine_info* info);
 

@@ -30,6 +30,8 @@ DJG_FLAG_FULL_RECORD = 32
 DJG_FLAG_TLED = 64
 DJG_FLAG_NO_PIPE = 128
 DJG_FLAG_WINDOW = 256
+DJG_FLAG_NO_FUSED = 512
+DJG_FLAG_FUSED = 1024
 DJG_PART_RCB, DJG_PART_METIS = 0, 1
 DJG_PART_BOX = 2
 PART_METHODS = {"rcb": DJG_PART_RCB, "metis": DJG_PART_METIS, "box": DJG_PART_BOX}
@@ -161,7 +163,7 @@ class djg_engine_info(C.Structure):
         ("npe", C.c_int32), ("nconst", C.c_int32), ("const_planes", C.c_int32), ("precision", C.c_int32),
         ("kernels_per_step", C.c_int32), ("sm_count", C.c_int32), ("slabs", C.c_int32),
         ("compact", C.c_int32), ("slab_elements", C.c_int64), ("formulation", C.c_int32), ("pipelined", C.c_int32),
-        ("windowed", C.c_int32), ("window_tiles", C.c_int64),
+        ("windowed", C.c_int32), ("window_tiles", C.c_int64), ("fused", C.c_int32), ("_pad_fused", C.c_int32),
     ]
 
 

@@ -26,6 +26,7 @@
 #endif
 
 #include "djg.h"
+#include "../common/box_mesh.hpp"
 #include <cub/cub.cuh>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -69,6 +70,17 @@ constexpr int kPipeMaxStageBytes = DJG_PIPE_MAX_STAGE_KB * 1024;
 #define DJG_WIN_H8 0
 #endif
 constexpr int kWinMaxStageBytes = DJG_WIN_MAX_STAGE_KB * 1024;
+// k_box_step tile: BX x BY owned nodes (one thread each) and BZ node layers
+#ifndef DJG_BOX_BX
+#define DJG_BOX_BX 16
+#endif
+#ifndef DJG_BOX_BY
+#define DJG_BOX_BY 16
+#endif
+#ifndef DJG_BOX_BZ
+#define DJG_BOX_BZ 16
+#endif
+constexpr int kBoxBX = DJG_BOX_BX, kBoxBY = DJG_BOX_BY, kBoxBZ = DJG_BOX_BZ;
 
 thread_local std::string g_create_error;
 
@@ -523,6 +535,7 @@ public:
         win_ = pipe_ && (flags_ & DJG_FLAG_WINDOW) && (kind_ == DJG_T4 || DJG_WIN_H8);
         if (win_) build_windows(d.conn);
         if (pipe_) launch_element(stream_, 0, E_, nullptr, /*setup=*/true);
+        fused_ = detect_box(d.conn);
         if (!win_) {
             slot_.release();
             widx_.release();
@@ -534,6 +547,83 @@ public:
         }
         set_state(nullptr, nullptr, 0);
     }
+
+    // The fused box step (k_box_step) applies to a mesh generate_box made:
+    // T4 cells in cell order, lexicographic nodes. The box dimensions follow
+    // from element 0 (its first tet runs corner 0 -> 1 -> 3 -> 7: node ids 0,
+    // 1, nx + 2, nx + 2 + (nx + 1)(ny + 1)); every element is then checked
+    // against the generator. f32 compact records (J0 rebuilt from X) with
+    // NH / TI / OT, one part, no slabs. It is the default when the box is
+    // large enough to fill the GPU (>= 4 waves of its blocks: cfg5, not cfg3,
+    // where its column tiles are too few); DJG_FLAG_FUSED forces it on any
+    // such box (tests), DJG_FLAG_NO_FUSED or DJG_NO_FUSED=1 keep the
+    // two-kernel step.
+    bool detect_box(const int32_t* conn) {
+        if (kind_ != DJG_T4 || sizeof(Real) != 4 || !compact_ || tled_ || !X_.p || n_slabs_ != 1 || win_) return false;
+        if (model_ != DJG_NH && model_ != DJG_TI && model_ != DJG_OT) return false;
+        if ((flags_ & DJG_FLAG_NO_FUSED) || (std::getenv("DJG_NO_FUSED") && std::atoi(std::getenv("DJG_NO_FUSED"))))
+            return false;
+        const bool forced = (flags_ & DJG_FLAG_FUSED) || (std::getenv("DJG_FUSED") && std::atoi(std::getenv("DJG_FUSED")));
+        if (E_ < 6 || E_ % 6) return false;
+        const int64_t nx = int64_t(conn[2]) - 2;
+        if (nx < 1 || conn[0] != 0 || conn[1] != 1) return false;
+        const int64_t plane = int64_t(conn[3]) - conn[2];
+        if (plane % (nx + 1)) return false;
+        const int64_t ny = plane / (nx + 1) - 1;
+        if (ny < 1 || N_ % ((nx + 1) * (ny + 1))) return false;
+        const int64_t nz = N_ / ((nx + 1) * (ny + 1)) - 1;
+        if (nz < 1 || 6 * nx * ny * nz != E_ || nx > INT32_MAX / 2 || ny > INT32_MAX / 2 || nz > INT32_MAX / 2)
+            return false;
+        const int32_t div[3] = {int32_t(nx), int32_t(ny), int32_t(nz)};
+        bool ok = true;
+#pragma omp parallel for schedule(static) reduction(&& : ok)
+        for (int64_t c = 0; c < nx * ny * nz; ++c) {
+            int32_t cc[24];
+            box_cell_conn(DJG_T4, div, c, cc);
+            ok = ok && std::memcmp(cc, conn + c * 24, sizeof(cc)) == 0;
+        }
+        if (!ok) return false;
+        box_.nx = int(nx);
+        box_.ny = int(ny);
+        box_.nz = int(nz);
+        box_.bz = kBoxBZ;
+        if (const char* v = std::getenv("DJG_BOX_BZ")) box_.bz = std::max(1, std::atoi(v));
+        box_.tiles_x = int((nx + 1 + kBoxBX - 1) / kBoxBX);
+        box_.tiles_y = int((ny + 1 + kBoxBY - 1) / kBoxBY);
+        const size_t smem = BoxShape<kBoxBX, kBoxBY>::template smem_bytes<Real>();
+        int per_sm = 0;
+        auto setup = [&](auto kern) {
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+            int nb = 0;
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, BoxShape<kBoxBX, kBoxBY>::kThreads, smem));
+            per_sm = per_sm == 0 ? nb : std::min(per_sm, nb);
+        };
+        if constexpr (sizeof(Real) == 4) {
+            setup(k_box_step<Real, DJG_NH, kBoxBX, kBoxBY>);
+            setup(k_box_step<Real, DJG_TI, kBoxBX, kBoxBY>);
+            setup(k_box_step<Real, DJG_OT, kBoxBX, kBoxBY>);
+        }
+        if (per_sm < 1) return false;
+        const int64_t blocks = int64_t(box_.tiles_x) * box_.tiles_y * ((nz + 1 + box_.bz - 1) / box_.bz);
+        return forced || blocks >= 4LL * per_sm * sms_;
+    }
+
+    void launch_box(cudaStream_t s) {
+        if constexpr (sizeof(Real) == 4) {
+            const int tiles_z = (box_.nz + 1 + box_.bz - 1) / box_.bz;
+            const unsigned grid = unsigned(box_.tiles_x * box_.tiles_y * tiles_z);
+            const size_t smem = BoxShape<kBoxBX, kBoxBY>::template smem_bytes<Real>();
+            constexpr int NT = BoxShape<kBoxBX, kBoxBY>::kThreads;
+            switch (model_) {
+                case DJG_NH: k_box_step<Real, DJG_NH, kBoxBX, kBoxBY><<<grid, NT, smem, s>>>(ea_, na_, box_); break;
+                case DJG_TI: k_box_step<Real, DJG_TI, kBoxBX, kBoxBY><<<grid, NT, smem, s>>>(ea_, na_, box_); break;
+                default: k_box_step<Real, DJG_OT, kBoxBX, kBoxBY><<<grid, NT, smem, s>>>(ea_, na_, box_); break;
+            }
+            CK(cudaGetLastError());
+        }
+    }
+
+    bool fused_now() const { return fused_ && na_.N == N_ && !peer_ && !comm_ && n_slabs_ == 1; }
 
     // Uniform slices: when every 32-node slice given the widest row's width
     // costs at most 2 % more slots (the cube: 0.9 %), all slices get that
@@ -1556,6 +1646,14 @@ public:
     // One advance_step (or one assemble) on the stream: S slab pairs.
     void launch_step(cudaStream_t s, bool assemble_mode = false, const Node* u_override = nullptr,
                      std::vector<cudaEvent_t>* marks = nullptr) {
+        if (!assemble_mode && !u_override && fused_now()) {
+            launch_box(s);
+            if (marks) {
+                CK(cudaEventRecord((*marks)[0], s));
+                CK(cudaEventRecord((*marks)[1], s));
+            }
+            return;
+        }
         for (int q = 0; q < n_slabs_; ++q) {
             const int64_t e0 = int64_t(q) * slab_elems_, e1 = std::min<int64_t>(E_, e0 + slab_elems_);
             launch_element(s, e0, e1, u_override);
@@ -1741,6 +1839,7 @@ public:
         o->formulation = tled_ ? 1 : 0;
         o->pipelined = pipe_ ? 1 : 0;
         o->windowed = win_ ? 1 : 0;
+        o->fused = fused_now() ? 1 : 0;
         o->window_tiles = win_tiles_;
         o->slabs = n_slabs_;
         o->slab_elements = slab_elems_;
@@ -1815,6 +1914,8 @@ private:
     size_t pipe_smem_ = 0;
     int64_t win_tiles_ = 0;            // tiles whose nodes fit a window (k_element_win)
     DevBuf slot_, widx_, wdesc_;       // node windows: slot positions, window indices, tile descriptors
+    bool fused_ = false;               // generated box of T4 cells: one fused kernel per step (k_box_step)
+    BoxArgs box_{};
     uint32_t flags_ = 0;
     int64_t N_ = 0, E_ = 0, capacity_ = 0;
     cudaStream_t stream_ = nullptr;

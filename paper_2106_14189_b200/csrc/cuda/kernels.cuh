@@ -266,6 +266,25 @@ __device__ __forceinline__ void store_row(const ElemArgs<Real>& A, int pos, Real
     RT<Real>::store_node(A.ef + pos, x, y, z);
 }
 
+// Where element_body's rows go: the force slots in HBM (store_row), or -- for
+// a Src that declares itself a row sink (the fused box step) -- the Src's own
+// storage. Likewise whether an inversion is counted: A.counted, or the Src.
+template <class Src, class = void>
+struct RowSink : std::false_type {};
+template <class Src>
+struct RowSink<Src, std::void_t<decltype(Src::kRowSink)>> : std::true_type {};
+
+template <class Real, class Src>
+__device__ __forceinline__ void emit_row(const ElemArgs<Real>& A, const Src& src, int pos, Real x, Real y, Real z) {
+    if constexpr (RowSink<Src>::value) src.store(pos, x, y, z);
+    else store_row(A, pos, x, y, z);
+}
+template <class Real, class Src>
+__device__ __forceinline__ bool counts_inversion(const ElemArgs<Real>& A, const Src& src, long long e) {
+    if constexpr (RowSink<Src>::value) return src.count_inv;
+    else return !A.counted || A.counted[e];
+}
+
 // Ranks of element e in its nodes' CSR rows (RB bytes each), packed in one
 // 4 / 8 / 16-byte word per element.
 template <int NPE, int RB>
@@ -555,10 +574,10 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
 
     if (!(det > Real(0))) {
         // record_inversion (djtled_force.hpp:107-112) + zeroed rows (:187-191).
-        if (!A.counted || A.counted[e]) atomicAdd(&A.ctrl->inv_count, 1ull);
+        if (counts_inversion(A, src, e)) atomicAdd(&A.ctrl->inv_count, 1ull);
         atomicMin(&A.ctrl->first_inv, (unsigned long long)(A.elem_l2g ? A.elem_l2g[e] : e));
 #pragma unroll
-        for (int a = 0; a < NPE; ++a) store_row(A, sl[a], Real(0), Real(0), Real(0));
+        for (int a = 0; a < NPE; ++a) emit_row(A, src, sl[a], Real(0), Real(0), Real(0));
         return;
     }
     const Real s_inv = Real(1) / det;
@@ -659,10 +678,10 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
 
     if constexpr (KIND == 0) {
         // T4 rows: f1..f3 = columns of K, f0 = -(f1 + f2 + f3).
-        store_row(A, sl[1], K[0][0], K[1][0], K[2][0]);
-        store_row(A, sl[2], K[0][1], K[1][1], K[2][1]);
-        store_row(A, sl[3], K[0][2], K[1][2], K[2][2]);
-        store_row(A, sl[0], Real(-1) * ((K[0][0] + K[0][1]) + K[0][2]), Real(-1) * ((K[1][0] + K[1][1]) + K[1][2]),
+        emit_row(A, src, sl[1], K[0][0], K[1][0], K[2][0]);
+        emit_row(A, src, sl[2], K[0][1], K[1][1], K[2][1]);
+        emit_row(A, src, sl[3], K[0][2], K[1][2], K[2][2]);
+        emit_row(A, src, sl[0], Real(-1) * ((K[0][0] + K[0][1]) + K[0][2]), Real(-1) * ((K[1][0] + K[1][1]) + K[1][2]),
                   Real(-1) * ((K[2][0] + K[2][1]) + K[2][2]));
     } else {
         // Hourglass data: the remaining record planes, loaded now.
@@ -717,7 +736,7 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
                     f[2] = f[2] + kg * q[m][2];
                 }
             }
-            store_row(A, sl[a], f[0], f[1], f[2]);
+            emit_row(A, src, sl[a], f[0], f[1], f[2]);
         }
     }
 }
@@ -1701,6 +1720,270 @@ __global__ void __launch_bounds__(256) k_node(const NodeArgs<Real> A) {
     ctrl->inv_count = 0;
     ctrl->first_inv = kNone;
     ctrl->diverged = 0;
+    __threadfence();
+    ctrl->blocks_done = 0;
+}
+
+// ------------------------------------------------------------------ fused box step
+//
+// One kernel per explicit step for a generated box of T4 cells
+// (generate_box: lexicographic nodes, six Kuhn tets per cell in cell order),
+// with no force slots in HBM. Block = a column tile of BX x BY owned nodes
+// and a segment of BZ node layers; it streams cell layer by cell layer:
+//   1. the node rows (u, X) of the two node layers a cell layer spans are in
+//      a 3-layer shared ring (the next layer's rows go in with cp.async while
+//      the current one is computed);
+//   2. every tet of the cell layer that touches the tile's nodes -- the
+//      tile's (BX+1) x (BY+1) cell footprint, ~10 % of them also computed by a
+//      neighbouring tile -- runs element_body with its four rows written to
+//      shared memory instead of HBM;
+//   3. each owned node folds the rows of the tets around it in ascending
+//      element id from +0 (the four cells below it in id order, each cell's
+//      tets in order, then the four cells above: the order of its CSR row),
+//      carrying the partial sum of the layer below in a register, then runs
+//      the central-difference update (dof_update) and stores u_next.
+// The last block closes the step (close_step). Rows, sums and update are
+// those of k_element + k_node: bit-identical; what disappears is the 16-byte
+// slot row per element-node written and read back through HBM (6.4 GB per
+// cfg5 step). Inversions are counted by the tile that owns the cell (the
+// one owning node (ci+1, cj+1)) in the segment that owns its layer.
+#ifndef DJG_BOX_MINB
+#define DJG_BOX_MINB 2
+#endif
+struct BoxArgs {
+    int nx, ny, nz;   // cells per axis
+    int bz;           // node layers per segment
+    int tiles_x, tiles_y;
+};
+
+// Corner code (dx + 2 dy + 4 dz) of local node a of Kuhn tet t
+// (generate_box's axis orders with the odd-permutation swap, mesh.hpp:228-258).
+__device__ __constant__ signed char kTetCorner[6][4] = {{0, 1, 3, 7}, {0, 5, 1, 7}, {0, 3, 2, 7},
+                                                        {0, 2, 6, 7}, {0, 4, 5, 7}, {0, 6, 4, 7}};
+
+template <class Real>
+struct BoxSrc {
+    using Node = typename RT<Real>::Node;
+    static constexpr bool kRowSink = true;
+    const Node* su;    // stage u (all ring slots)
+    const Node* sx;    // stage X
+    float* rows;       // [footprint cell][t][a][3]
+    int h[4];          // stage indices of the tet's nodes
+    int row0;          // first row of this tet
+    bool count_inv;
+    __device__ __forceinline__ int4 conn(int) const { return make_int4(h[0], h[1], h[2], h[3]); }
+    __device__ __forceinline__ Node node(int, const Node* __restrict__, int k) const { return su[k]; }
+    __device__ __forceinline__ Node coord(const ElemArgs<Real>&, int k) const { return sx[k]; }
+    __device__ __forceinline__ typename RT<Real>::Plane plane(int) const { return typename RT<Real>::Plane{}; }
+    __device__ __forceinline__ Real tail(int) const { return Real(0); }
+    template <int N, int RB>
+    __device__ __forceinline__ void ranks(int (&rk)[N]) const {
+#pragma unroll
+        for (int a = 0; a < N; ++a) rk[a] = 0;
+    }
+    int ntet;          // tets per footprint layer: 9 planes [column j][xyz][tet] of K
+    __device__ __forceinline__ int slot(const int* __restrict__, int a, int, int) const { return row0 + a; }
+    // T4 rows 1..3 are the columns of K (element_body); row 0 is not kept --
+    // the fold recomputes it from the columns with the same operations.
+    __device__ __forceinline__ void store(int pos, Real x, Real y, Real z) const {
+        const int tet = pos >> 2, a = pos & 3;
+        if (a == 0) return;
+        rows[(3 * (a - 1) + 0) * ntet + tet] = x;  // consecutive tets -> consecutive words: no bank conflicts
+        rows[(3 * (a - 1) + 1) * ntet + tet] = y;
+        rows[(3 * (a - 1) + 2) * ntet + tet] = z;
+    }
+};
+
+// The Kuhn tets of a cell holding corner C, as (tet, local node) in
+// ascending tet order (the inverse of kTetCorner), at compile time.
+template <int C, int NCELL>
+__device__ __forceinline__ void corner_rows(const float* __restrict__ rows, int ntet, int c, float& fx, float& fy,
+                                            float& fz) {
+    constexpr int n = (C == 0 || C == 7) ? 6 : 2;
+    constexpr int T0[8][6] = {{0, 1, 2, 3, 4, 5}, {0, 1}, {2, 3}, {0, 2}, {4, 5}, {1, 4}, {3, 5}, {0, 1, 2, 3, 4, 5}};
+    constexpr int A0[8][6] = {{0, 0, 0, 0, 0, 0}, {1, 2}, {2, 1}, {2, 1}, {1, 2}, {1, 2}, {2, 1}, {3, 3, 3, 3, 3, 3}};
+#pragma unroll
+    for (int m = 0; m < n; ++m) {
+        const int tet = T0[C][m] * NCELL + c, a = A0[C][m];
+        if (a == 0) {  // f0 = -(f1 + f2 + f3), element_body's expression (djtled_force.hpp:73-77)
+            const float* k = rows + tet;
+            fx += -1.0f * ((k[0 * ntet] + k[3 * ntet]) + k[6 * ntet]);
+            fy += -1.0f * ((k[1 * ntet] + k[4 * ntet]) + k[7 * ntet]);
+            fz += -1.0f * ((k[2 * ntet] + k[5 * ntet]) + k[8 * ntet]);
+        } else {
+            fx += rows[(3 * (a - 1) + 0) * ntet + tet];
+            fy += rows[(3 * (a - 1) + 1) * ntet + tet];
+            fz += rows[(3 * (a - 1) + 2) * ntet + tet];
+        }
+    }
+}
+
+template <int BX, int BY>
+struct BoxShape {
+    static constexpr int SX = BX + 2, SY = BY + 2;  // stage nodes per layer (footprint + 1 halo node each side)
+    static constexpr int CX = BX + 1, CY = BY + 1;  // footprint cells per layer
+    static constexpr int kStageNodes = SX * SY;
+    static constexpr size_t kRowFloats = size_t(CX) * CY * 6 * 9;  // K per tet
+    // one thread per footprint cell (its six tets in turn: every thread the
+    // same work per layer), the first BX * BY of them also one owned node each
+    static constexpr int kThreads = (CX * CY + 31) / 32 * 32;
+    template <class Real>
+    static constexpr size_t smem_bytes() {
+        return 2 * 3 * size_t(kStageNodes) * sizeof(typename RT<Real>::Node) + kRowFloats * sizeof(float);
+    }
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
+}
+
+template <class Real, int MODEL, int BX, int BY>
+__global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_box_step(const ElemArgs<Real> A, const NodeArgs<Real> NA,
+                                                          const BoxArgs B) {
+    static_assert(sizeof(Real) == 4, "the fused box step keeps float rows");
+    using T = RT<Real>;
+    using Node = typename T::Node;
+    using BS = BoxShape<BX, BY>;
+    constexpr int NT = BS::kThreads;
+    extern __shared__ __align__(128) unsigned char smem[];
+    Node* su = reinterpret_cast<Node*>(smem);
+    Node* sx = su + 3 * BS::kStageNodes;
+    float* rows = reinterpret_cast<float*>(sx + 3 * BS::kStageNodes);
+    __shared__ int s_nonfinite;
+    Ctrl* ctrl = A.ctrl;
+    if (*(volatile const int*)&ctrl->halted) return;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_nonfinite = 0;
+    const int tx = blockIdx.x % B.tiles_x, ty = (blockIdx.x / B.tiles_x) % B.tiles_y;
+    const int tz = blockIdx.x / (B.tiles_x * B.tiles_y);
+    const int nx = B.nx, ny = B.ny, nz = B.nz;
+    const int i0 = tx * BX, j0 = ty * BY, k0 = tz * B.bz, k1 = min(k0 + B.bz, nz + 1);
+    const long long step = ctrl->step;
+    const int ph = int(step % 3);
+    const Node* ucur = pick3(ph, NA.u[0], NA.u[1], NA.u[2]);
+    const Node* uprv = pick3(ph, NA.u[2], NA.u[0], NA.u[1]);
+    Node* unxt = pick3(ph, NA.u[1], NA.u[2], NA.u[0]);
+    auto gid = [&](int i, int j, int k) { return (long long)i + (long long)(nx + 1) * (j + (long long)(ny + 1) * k); };
+    // node layer k into ring slot k % 3 (cp.async; out-of-box rows are left stale and never read)
+    auto load_layer = [&](int k) {
+        if (k > nz) return;
+        const int slot = k % 3;
+        for (int q = tid; q < BS::kStageNodes; q += NT) {
+            const int gi = i0 - 1 + q % BS::SX, gj = j0 - 1 + q / BS::SX;
+            if (gi < 0 || gi > nx || gj < 0 || gj > ny) continue;
+            const long long n = gid(gi, gj, k);
+            cp_async16(su + slot * BS::kStageNodes + q, ucur + n);
+            cp_async16(sx + slot * BS::kStageNodes + q, A.X + n);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const int kc0 = max(k0 - 1, 0), kc1 = min(k1 - 1, nz - 1);  // cell layers this segment computes
+    load_layer(kc0);
+    load_layer(kc0 + 1);
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+
+    // owned node of this thread (one per column position)
+    const int oi = i0 + tid % BX, oj = j0 + tid / BX;
+    const bool own = tid < BX * BY && oi <= nx && oj <= ny;
+    Real px = Real(0), py = Real(0), pz = Real(0);  // partial sum of the node one layer up (cells below it)
+
+    // fold the rows of the cell layer around node (oi, oj): its four cells in
+    // id order (the node is their corner 3, 2, 1, 0 at height dz), each
+    // cell's tets in order
+    constexpr int NCELL = BS::CX * BS::CY, NTET = NCELL * 6;  // rows: tet t of footprint cell c is t * NCELL + c
+    const int cb = (oj - j0) * BS::CX + (oi - i0);  // footprint cell (oi - 1, oj - 1)
+    const bool hx0 = oi >= 1, hx1 = oi < nx, hy0 = oj >= 1, hy1 = oj < ny;
+    auto fold_below = [&](Real& fx, Real& fy, Real& fz) {  // node at the top (dz = 1) of the cells
+        if (hy0 && hx0) corner_rows<7, NCELL>(rows, NTET, cb, fx, fy, fz);
+        if (hy0 && hx1) corner_rows<6, NCELL>(rows, NTET, cb + 1, fx, fy, fz);
+        if (hy1 && hx0) corner_rows<5, NCELL>(rows, NTET, cb + BS::CX, fx, fy, fz);
+        if (hy1 && hx1) corner_rows<4, NCELL>(rows, NTET, cb + BS::CX + 1, fx, fy, fz);
+    };
+    auto fold_above = [&](Real& fx, Real& fy, Real& fz) {  // node at the bottom (dz = 0)
+        if (hy0 && hx0) corner_rows<3, NCELL>(rows, NTET, cb, fx, fy, fz);
+        if (hy0 && hx1) corner_rows<2, NCELL>(rows, NTET, cb + 1, fx, fy, fz);
+        if (hy1 && hx0) corner_rows<1, NCELL>(rows, NTET, cb + BS::CX, fx, fy, fz);
+        if (hy1 && hx1) corner_rows<0, NCELL>(rows, NTET, cb + BS::CX + 1, fx, fy, fz);
+    };
+    auto update = [&](int k, Real fx, Real fy, Real fz) {
+        const long long n = gid(oi, oj, k);
+        const typename T::Node uc = su[(k % 3) * BS::kStageNodes + (oj - j0 + 1) * BS::SX + (oi - i0 + 1)];
+        const typename T::Node up = T::load_node(uprv + n);
+        typename T::Node r;
+        if (NA.r_ext) r = T::load_node(NA.r_ext + n);
+        else { r.x = Real(0); r.y = Real(0); r.z = Real(0); }
+        const int code = NA.code[n];
+        const bool massless = (code >> 6) & 1;
+        const Real c1 = NA.c1[n];
+        const Real t_next = NA.dt * Real(step + 1);
+        bool nf = false;
+        const Real vx = dof_update<Real>(code & 3, massless, c1, r.x, fx, uc.x, up.x, NA.c2, NA.c3, t_next, NA.target,
+                                         NA.t_total, 3 * n + 0, nf);
+        const Real vy = dof_update<Real>((code >> 2) & 3, massless, c1, r.y, fy, uc.y, up.y, NA.c2, NA.c3, t_next,
+                                         NA.target, NA.t_total, 3 * n + 1, nf);
+        const Real vz = dof_update<Real>((code >> 4) & 3, massless, c1, r.z, fz, uc.z, up.z, NA.c2, NA.c3, t_next,
+                                         NA.target, NA.t_total, 3 * n + 2, nf);
+        T::store_node(unxt + n, vx, vy, vz);
+        if (nf) s_nonfinite = 1;
+    };
+
+    // this thread's footprint cell (fixed across layers)
+    const int mcy = tid / BS::CX, mcx = tid - mcy * BS::CX;
+    const int mci = i0 - 1 + mcx, mcj = j0 - 1 + mcy;
+    const bool my_cell = tid < NCELL && mci >= 0 && mci < nx && mcj >= 0 && mcj < ny;
+    const bool my_count = mcx < BX && mcy < BY;  // the tile owning node (ci + 1, cj + 1) counts its inversions
+    const int mbase = mcy * BS::SX + mcx;
+    for (int kc = kc0; kc <= kc1; ++kc) {
+        load_layer(kc + 2);  // ring slot (kc + 2) % 3 held layer kc - 1, released by the last barrier
+        // 2. the cell layer's tets around the tile: this thread's cell, its
+        // six tets in order (a warp shares t: uniform corner offsets;
+        // consecutive cells write consecutive row words)
+        if (my_cell) {
+            const int slot0 = (kc % 3) * BS::kStageNodes, slot1 = ((kc + 1) % 3) * BS::kStageNodes;
+            const bool count = my_count && kc >= k0;
+            const long long ebase = ((long long)mci + (long long)nx * (mcj + (long long)ny * kc)) * 6;
+            for (int t = 0; t < 6; ++t) {
+                BoxSrc<Real> src;
+                src.su = su;
+                src.sx = sx;
+                src.rows = rows;
+                src.ntet = NTET;
+                src.row0 = (t * NCELL + tid) * 4;
+                src.count_inv = count;
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const int cr = kTetCorner[t][a];
+                    src.h[a] = ((cr >> 2) ? slot1 : slot0) + mbase + ((cr >> 1) & 1) * BS::SX + (cr & 1);
+                }
+                element_body<Real, 0, MODEL, 1, true>(A, ebase + t, nullptr, src);
+            }
+        }
+        __syncthreads();
+        // 3. finish node layer kc, start node layer kc + 1
+        if (own) {
+            if (kc >= k0) {
+                Real fx = px, fy = py, fz = pz;
+                fold_above(fx, fy, fz);
+                update(kc, fx, fy, fz);
+            }
+            if (kc + 1 < k1) {
+                px = Real(0); py = Real(0); pz = Real(0);
+                fold_below(px, py, pz);
+            }
+        }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+    }
+    // the top node layer has no cells above it
+    if (own && k1 - 1 == nz && nz >= k0 && nz > kc1) update(nz, px, py, pz);
+    __syncthreads();
+    if (tid != 0) return;
+    if (s_nonfinite) atomicOr(&ctrl->diverged, 1);
+    __threadfence();
+    const unsigned int done = atomicAdd(&ctrl->blocks_done, 1u);
+    if (done != gridDim.x - 1) return;
+    close_step<false>(ctrl, step, NA.policy);
     __threadfence();
     ctrl->blocks_done = 0;
 }

@@ -23,6 +23,7 @@
 #endif
 
 #include "djg_types.h"
+#include "../common/box_mesh.hpp"
 #include "../common/element_math.hpp"
 
 namespace djg {
@@ -215,36 +216,6 @@ struct Mesh {
 template <class Real>
 inline Real box_coord(const double extent, int64_t i, int64_t n) {
     return Real(extent) * Real(int(i)) / Real(int(n));
-}
-
-// Global connectivity of cell c (H8: 8 corners; T4: 6 tets x 4).
-inline void box_cell_conn(int kind, const int32_t div[3], int64_t c, int32_t* out) {
-    const int64_t nx = div[0], ny = div[1];
-    const int64_t i = c % nx, j = (c / nx) % ny, k = c / (nx * ny);
-    auto id = [&](int64_t a, int64_t b, int64_t d) { return int32_t(a + (nx + 1) * (b + (ny + 1) * d)); };
-    int32_t corner[2][2][2];
-    for (int dz = 0; dz < 2; ++dz)
-        for (int dy = 0; dy < 2; ++dy)
-            for (int dx = 0; dx < 2; ++dx) corner[dx][dy][dz] = id(i + dx, j + dy, k + dz);
-    if (kind == DJG_H8) {
-        for (int a = 0; a < 8; ++a)
-            out[a] = corner[(kCornerSign[a][0] + 1) / 2][(kCornerSign[a][1] + 1) / 2][(kCornerSign[a][2] + 1) / 2];
-        return;
-    }
-    static constexpr int orders[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
-    for (int t = 0; t < 6; ++t) {
-        const int* o = orders[t];
-        int s[3] = {0, 0, 0};
-        int32_t path[4];
-        path[0] = corner[0][0][0];
-        for (int q = 0; q < 3; ++q) {
-            s[o[q]] = 1;
-            path[q + 1] = corner[s[0]][s[1]][s[2]];
-        }
-        const bool odd = (o[0] == 0 && o[1] == 2) || (o[0] == 1 && o[1] == 0) || (o[0] == 2 && o[1] == 1);
-        if (odd) std::swap(path[1], path[2]);
-        for (int a = 0; a < 4; ++a) out[t * 4 + a] = path[a];
-    }
 }
 
 inline void check_box(const double extent[3], const int32_t div[3]) {

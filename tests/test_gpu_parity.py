@@ -153,6 +153,59 @@ def test_node_windows_mixed_tiles():
         check_run(spec, 200, flags=A.DJG_FLAG_WINDOW | A.DJG_FLAG_NO_GRAPH)
 
 
+@pytest.mark.parametrize("model", ["NH", "TI", "OT"])
+@pytest.mark.parametrize("divisions", [(5, 4, 6), (17, 9, 33), (16, 16, 16), (33, 2, 5), (1, 1, 1)])
+def test_fused_box_step_bitwise(divisions, model):
+    """k_box_step (DJG_FLAG_FUSED): one kernel per step on a generated box --
+    element forces into shared memory, each node folding its tets' rows in
+    ascending element id, the update -- bit-identical to the oracle, on boxes
+    whose sides are and are not multiples of the 16 x 16 x 16 tile."""
+    spec = box_spec(kind="T4", model=model, divisions=divisions, precision=4, ramp_steps=200)
+    with GpuDjEngine(Scenario(spec), flags=A.DJG_FLAG_FUSED) as eng:
+        assert eng.info()["fused"] == 1
+    check_run(spec, 200, flags=A.DJG_FLAG_FUSED)
+
+
+@pytest.mark.parametrize("policy", [A.DJG_ABORT, A.DJG_SKIP_AND_REPORT])
+def test_fused_box_step_inversion(policy):
+    """The fused step under a crushing load: Abort halts on the same element
+    and step with the same state as the two-kernel step (the fused kernel has
+    already written u_next when it learns of the inversion; the step is not
+    closed, so the state stays), SkipAndReport gives the same counts (each
+    inversion counted once, by the tile owning the cell)."""
+    spec = box_spec(kind="T4", divisions=(9, 7, 8), extent=(0.1, 0.1, 0.1), precision=4, target=-0.09,
+                    ramp_steps=3, fix_all_axes=True, policy=policy)
+    outs = []
+    for flags in (A.DJG_FLAG_FUSED, A.DJG_FLAG_NO_FUSED):
+        with GpuDjEngine(Scenario(spec), flags=flags) as eng:
+            r = eng.step(60, raise_on_failure=False)
+            outs.append((r, *eng.get_state()))
+    (r1, u1, up1, s1), (r2, u2, up2, s2) = outs
+    assert (r1.status, r1.step, r1.first_inverted, r1.inverted_count, r1.inverted_steps) == \
+        (r2.status, r2.step, r2.first_inverted, r2.inverted_count, r2.inverted_steps), (r1, r2)
+    assert r1.inverted_count > 0
+    assert np.array_equal(u1, u2) and np.array_equal(up1, up2)
+    ur, upr, rr = oracle.run(spec, 60, "oracle")
+    assert (r1.status, r1.first_inverted, r1.inverted_count) == (rr["status"], rr["first_inverted"],
+                                                                 rr["inverted_count"])
+    assert np.array_equal(u1, ur)
+
+
+def test_fused_box_step_large_vs_two_kernel():
+    """A 96^3 box (5.3M tets, 343 fused blocks) against the two-kernel step
+    on the same device, 300 steps, bitwise (u and u_prev)."""
+    spec = box_spec(kind="T4", model="NH", divisions=96, precision=4, target=0.01, ramp_steps=300)
+    sc = Scenario(spec)
+    res = []
+    for flags in (A.DJG_FLAG_FUSED, A.DJG_FLAG_NO_FUSED):
+        with GpuDjEngine(sc, flags=flags) as eng:
+            res.append(eng.info()["fused"])
+            eng.step(300)
+            res.append(eng.get_state())
+    assert res[0] == 1 and res[2] == 0
+    assert np.array_equal(res[1][0], res[3][0]) and np.array_equal(res[1][1], res[3][1])
+
+
 @pytest.mark.parametrize("flags", [A.DJG_FLAG_COMPACT, A.DJG_FLAG_DEVICE_PRECOMPUTE, A.DJG_FLAG_TLED])
 def test_i57_full_record_only(flags):
     """DJG_I57 (the I5 / I7 test energy) runs on the host-built full record;
@@ -272,7 +325,11 @@ def test_cfg5_full_size_bitwise():
     """BASELINE configs[4] at full size (50,192,562 tets, the bench problem
     and loading): 8 steps of a fast +1 % extension ramp, bit-identical to the
     CPU oracle (all host threads)."""
-    check_run(config_spec("cfg5", precision=4, target=0.01, ramp_steps=8), 8)
+    spec = config_spec("cfg5", precision=4, target=0.01, ramp_steps=8)
+    with GpuDjEngine(Scenario(spec)) as eng:
+        assert eng.info()["fused"] == 1  # the default step on cfg5: one fused kernel
+    check_run(spec, 8)
+    check_run(spec, 8, flags=A.DJG_FLAG_NO_FUSED)
 
 
 @pytest.mark.slow

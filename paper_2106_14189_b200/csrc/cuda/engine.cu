@@ -605,7 +605,8 @@ public:
         }
         if (per_sm < 1) return false;
         const int64_t blocks = int64_t(box_.tiles_x) * box_.tiles_y * ((nz + 1 + box_.bz - 1) / box_.bz);
-        return forced || blocks >= 4LL * per_sm * sms_;
+        if (!(forced || blocks >= 4LL * per_sm * sms_)) return false;
+        return true;
     }
 
     void launch_box(cudaStream_t s) {

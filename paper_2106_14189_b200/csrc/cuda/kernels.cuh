@@ -1747,6 +1747,10 @@ __global__ void __launch_bounds__(256) k_node(const NodeArgs<Real> A) {
 // slot row per element-node written and read back through HBM (6.4 GB per
 // cfg5 step). Inversions are counted by the tile that owns the cell (the
 // one owning node (ci+1, cj+1)) in the segment that owns its layer.
+#ifndef DJG_BOX_UNROLL_T
+#define DJG_BOX_UNROLL_T 2  // tets of a cell per unrolled iteration (1: 1.58 ms on cfg5, 2: 1.57, 6: 1.60)
+#endif
+constexpr int kBoxUnrollT = DJG_BOX_UNROLL_T;
 #ifndef DJG_BOX_MINB
 #define DJG_BOX_MINB 2
 #endif
@@ -1943,6 +1947,7 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
             const int slot0 = (kc % 3) * BS::kStageNodes, slot1 = ((kc + 1) % 3) * BS::kStageNodes;
             const bool count = my_count && kc >= k0;
             const long long ebase = ((long long)mci + (long long)nx * (mcj + (long long)ny * kc)) * 6;
+#pragma unroll kBoxUnrollT
             for (int t = 0; t < 6; ++t) {
                 BoxSrc<Real> src;
                 src.su = su;

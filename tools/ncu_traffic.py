@@ -29,6 +29,9 @@ def summarise(path):
         wr = sum(m["dram__bytes_write.sum"]) / n
         out[k] = {"launches": n, "dram_bytes_per_launch": rd + wr, "dram_read": rd, "dram_write": wr,
                   "ncu_ms_per_launch": sum(m["gpu__time_duration.sum"]) / n / 1e6}
+        ia = m.get("smsp__issue_active.avg.pct_of_peak_sustained_active")
+        if ia:
+            out[k]["issue_active_pct"] = sum(ia) / len(ia)
     return out
 
 

@@ -1835,7 +1835,7 @@ public:
         o->nconst = nconst_;
         o->const_planes = nplanes_;
         o->precision = int32_t(sizeof(Real));
-        o->kernels_per_step = 2 * n_slabs_;
+        o->kernels_per_step = fused_now() ? 1 : 2 * n_slabs_;
         o->compact = compact_ ? 1 : 0;
         o->formulation = tled_ ? 1 : 0;
         o->pipelined = pipe_ ? 1 : 0;

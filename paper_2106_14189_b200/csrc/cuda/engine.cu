@@ -70,17 +70,14 @@ constexpr int kPipeMaxStageBytes = DJG_PIPE_MAX_STAGE_KB * 1024;
 #define DJG_WIN_H8 0
 #endif
 constexpr int kWinMaxStageBytes = DJG_WIN_MAX_STAGE_KB * 1024;
-// k_box_step tile: BX x BY owned nodes (one thread each) and BZ node layers
+// k_box_step tile: BX x BY owned nodes (one thread each)
 #ifndef DJG_BOX_BX
 #define DJG_BOX_BX 16
 #endif
 #ifndef DJG_BOX_BY
 #define DJG_BOX_BY 16
 #endif
-#ifndef DJG_BOX_BZ
-#define DJG_BOX_BZ 16
-#endif
-constexpr int kBoxBX = DJG_BOX_BX, kBoxBY = DJG_BOX_BY, kBoxBZ = DJG_BOX_BZ;
+constexpr int kBoxBX = DJG_BOX_BX, kBoxBY = DJG_BOX_BY;
 
 thread_local std::string g_create_error;
 
@@ -586,8 +583,6 @@ public:
         box_.nx = int(nx);
         box_.ny = int(ny);
         box_.nz = int(nz);
-        box_.bz = kBoxBZ;
-        if (const char* v = std::getenv("DJG_BOX_BZ")) box_.bz = std::max(1, std::atoi(v));
         box_.tiles_x = int((nx + 1 + kBoxBX - 1) / kBoxBX);
         box_.tiles_y = int((ny + 1 + kBoxBY - 1) / kBoxBY);
         const size_t smem = BoxShape<kBoxBX, kBoxBY>::template smem_bytes<Real>();
@@ -604,15 +599,16 @@ public:
             setup(k_box_step<Real, DJG_OT, kBoxBX, kBoxBY>);
         }
         if (per_sm < 1) return false;
-        const int64_t blocks = int64_t(box_.tiles_x) * box_.tiles_y * ((nz + 1 + box_.bz - 1) / box_.bz);
-        if (!(forced || blocks >= 4LL * per_sm * sms_)) return false;
-        return true;
+        box_grid_ = per_sm * sms_;  // persistent: every block resident
+        // each block walks W / grid column-layers with one extra cell layer
+        // per column piece: worth it from >= 32 layers per block (cfg5: 116)
+        const int64_t W = int64_t(box_.tiles_x) * box_.tiles_y * (nz + 1);
+        return forced || W >= 32LL * box_grid_;
     }
 
     void launch_box(cudaStream_t s) {
         if constexpr (sizeof(Real) == 4) {
-            const int tiles_z = (box_.nz + 1 + box_.bz - 1) / box_.bz;
-            const unsigned grid = unsigned(box_.tiles_x * box_.tiles_y * tiles_z);
+            const unsigned grid = unsigned(box_grid_);
             const size_t smem = BoxShape<kBoxBX, kBoxBY>::template smem_bytes<Real>();
             constexpr int NT = BoxShape<kBoxBX, kBoxBY>::kThreads;
             switch (model_) {
@@ -1917,6 +1913,7 @@ private:
     DevBuf slot_, widx_, wdesc_;       // node windows: slot positions, window indices, tile descriptors
     bool fused_ = false;               // generated box of T4 cells: one fused kernel per step (k_box_step)
     BoxArgs box_{};
+    int box_grid_ = 0;
     uint32_t flags_ = 0;
     int64_t N_ = 0, E_ = 0, capacity_ = 0;
     cudaStream_t stream_ = nullptr;

@@ -1756,7 +1756,6 @@ constexpr int kBoxUnrollT = DJG_BOX_UNROLL_T;
 #endif
 struct BoxArgs {
     int nx, ny, nz;   // cells per axis
-    int bz;           // node layers per segment
     int tiles_x, tiles_y;
 };
 
@@ -1858,10 +1857,8 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
     if (*(volatile const int*)&ctrl->halted) return;
     const int tid = threadIdx.x;
     if (tid == 0) s_nonfinite = 0;
-    const int tx = blockIdx.x % B.tiles_x, ty = (blockIdx.x / B.tiles_x) % B.tiles_y;
-    const int tz = blockIdx.x / (B.tiles_x * B.tiles_y);
     const int nx = B.nx, ny = B.ny, nz = B.nz;
-    const int i0 = tx * BX, j0 = ty * BY, k0 = tz * B.bz, k1 = min(k0 + B.bz, nz + 1);
+    int i0 = 0, j0 = 0, k0 = 0, k1 = 0;  // the current piece: column tile at (i0, j0), node layers [k0, k1)
     const long long step = ctrl->step;
     const int ph = int(step % 3);
     const Node* ucur = pick3(ph, NA.u[0], NA.u[1], NA.u[2]);
@@ -1881,23 +1878,17 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    const int kc0 = max(k0 - 1, 0), kc1 = min(k1 - 1, nz - 1);  // cell layers this segment computes
-    load_layer(kc0);
-    load_layer(kc0 + 1);
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
 
-    // owned node of this thread (one per column position)
-    const int oi = i0 + tid % BX, oj = j0 + tid / BX;
-    const bool own = tid < BX * BY && oi <= nx && oj <= ny;
+    // owned node of this thread (one per column position) and footprint
+    // cell (one per thread), relative to the tile
+    int oi = 0, oj = 0, cb = 0, mci = 0, mcj = 0;
+    bool own = false, hx0 = false, hx1 = false, hy0 = false, hy1 = false, my_cell = false;
     Real px = Real(0), py = Real(0), pz = Real(0);  // partial sum of the node one layer up (cells below it)
 
     // fold the rows of the cell layer around node (oi, oj): its four cells in
     // id order (the node is their corner 3, 2, 1, 0 at height dz), each
     // cell's tets in order
     constexpr int NCELL = BS::CX * BS::CY, NTET = NCELL * 6;  // rows: tet t of footprint cell c is t * NCELL + c
-    const int cb = (oj - j0) * BS::CX + (oi - i0);  // footprint cell (oi - 1, oj - 1)
-    const bool hx0 = oi >= 1, hx1 = oi < nx, hy0 = oj >= 1, hy1 = oj < ny;
     auto fold_below = [&](Real& fx, Real& fy, Real& fz) {  // node at the top (dz = 1) of the cells
         if (hy0 && hx0) corner_rows<7, NCELL>(rows, NTET, cb, fx, fy, fz);
         if (hy0 && hx1) corner_rows<6, NCELL>(rows, NTET, cb + 1, fx, fy, fz);
@@ -1932,57 +1923,83 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
         if (nf) s_nonfinite = 1;
     };
 
-    // this thread's footprint cell (fixed across layers)
     const int mcy = tid / BS::CX, mcx = tid - mcy * BS::CX;
-    const int mci = i0 - 1 + mcx, mcj = j0 - 1 + mcy;
-    const bool my_cell = tid < NCELL && mci >= 0 && mci < nx && mcj >= 0 && mcj < ny;
     const bool my_count = mcx < BX && mcy < BY;  // the tile owning node (ci + 1, cj + 1) counts its inversions
     const int mbase = mcy * BS::SX + mcx;
-    for (int kc = kc0; kc <= kc1; ++kc) {
-        load_layer(kc + 2);  // ring slot (kc + 2) % 3 held layer kc - 1, released by the last barrier
-        // 2. the cell layer's tets around the tile: this thread's cell, its
-        // six tets in order (a warp shares t: uniform corner offsets;
-        // consecutive cells write consecutive row words)
-        if (my_cell) {
-            const int slot0 = (kc % 3) * BS::kStageNodes, slot1 = ((kc + 1) % 3) * BS::kStageNodes;
-            const bool count = my_count && kc >= k0;
-            const long long ebase = ((long long)mci + (long long)nx * (mcj + (long long)ny * kc)) * 6;
-#pragma unroll kBoxUnrollT
-            for (int t = 0; t < 6; ++t) {
-                BoxSrc<Real> src;
-                src.su = su;
-                src.sx = sx;
-                src.rows = rows;
-                src.ntet = NTET;
-                src.row0 = (t * NCELL + tid) * 4;
-                src.count_inv = count;
-#pragma unroll
-                for (int a = 0; a < 4; ++a) {
-                    const int cr = kTetCorner[t][a];
-                    src.h[a] = ((cr >> 2) ? slot1 : slot0) + mbase + ((cr >> 1) & 1) * BS::SX + (cr & 1);
-                }
-                element_body<Real, 0, MODEL, 1, true>(A, ebase + t, nullptr, src);
-            }
-        }
-        __syncthreads();
-        // 3. finish node layer kc, start node layer kc + 1
-        if (own) {
-            if (kc >= k0) {
-                Real fx = px, fy = py, fz = pz;
-                fold_above(fx, fy, fz);
-                update(kc, fx, fy, fz);
-            }
-            if (kc + 1 < k1) {
-                px = Real(0); py = Real(0); pz = Real(0);
-                fold_below(px, py, pz);
-            }
-        }
+
+    // Persistent blocks: the column-layers (every column tile x every node
+    // layer, columns in order) are split evenly over the grid; a block walks
+    // its range as one or two column pieces, each starting with one extra
+    // cell layer below it (the partial sums of its first node layer).
+    const long long L = nz + 1, W = (long long)B.tiles_x * B.tiles_y * L;
+    const long long w_end = W * (blockIdx.x + 1) / gridDim.x;
+    for (long long w = W * blockIdx.x / gridDim.x; w < w_end;) {
+        const long long col = w / L;
+        k0 = int(w - col * L);
+        k1 = int(min(L, (long long)k0 + (w_end - w)));
+        w += k1 - k0;
+        i0 = int(col % B.tiles_x) * BX;
+        j0 = int(col / B.tiles_x) * BY;
+        oi = i0 + tid % BX;
+        oj = j0 + tid / BX;
+        own = tid < BX * BY && oi <= nx && oj <= ny;
+        cb = (oj - j0) * BS::CX + (oi - i0);  // footprint cell (oi - 1, oj - 1)
+        hx0 = oi >= 1; hx1 = oi < nx; hy0 = oj >= 1; hy1 = oj < ny;
+        mci = i0 - 1 + mcx;
+        mcj = j0 - 1 + mcy;
+        my_cell = tid < NCELL && mci >= 0 && mci < nx && mcj >= 0 && mcj < ny;
+        px = Real(0); py = Real(0); pz = Real(0);
+        const int kc0 = max(k0 - 1, 0), kc1 = min(k1 - 1, nz - 1);  // cell layers this piece computes
+        load_layer(kc0);
+        load_layer(kc0 + 1);
         asm volatile("cp.async.wait_all;" ::: "memory");
         __syncthreads();
+        for (int kc = kc0; kc <= kc1; ++kc) {
+            load_layer(kc + 2);  // ring slot (kc + 2) % 3 held layer kc - 1, released by the last barrier
+            // 2. the cell layer's tets around the tile: this thread's cell, its
+            // six tets in order (a warp shares t: uniform corner offsets;
+            // consecutive cells write consecutive row words)
+            if (my_cell) {
+                const int slot0 = (kc % 3) * BS::kStageNodes, slot1 = ((kc + 1) % 3) * BS::kStageNodes;
+                const bool count = my_count && kc >= k0;
+                const long long ebase = ((long long)mci + (long long)nx * (mcj + (long long)ny * kc)) * 6;
+    #pragma unroll kBoxUnrollT
+                for (int t = 0; t < 6; ++t) {
+                    BoxSrc<Real> src;
+                    src.su = su;
+                    src.sx = sx;
+                    src.rows = rows;
+                    src.ntet = NTET;
+                    src.row0 = (t * NCELL + tid) * 4;
+                    src.count_inv = count;
+    #pragma unroll
+                    for (int a = 0; a < 4; ++a) {
+                        const int cr = kTetCorner[t][a];
+                        src.h[a] = ((cr >> 2) ? slot1 : slot0) + mbase + ((cr >> 1) & 1) * BS::SX + (cr & 1);
+                    }
+                    element_body<Real, 0, MODEL, 1, true>(A, ebase + t, nullptr, src);
+                }
+            }
+            __syncthreads();
+            // 3. finish node layer kc, start node layer kc + 1
+            if (own) {
+                if (kc >= k0) {
+                    Real fx = px, fy = py, fz = pz;
+                    fold_above(fx, fy, fz);
+                    update(kc, fx, fy, fz);
+                }
+                if (kc + 1 < k1) {
+                    px = Real(0); py = Real(0); pz = Real(0);
+                    fold_below(px, py, pz);
+                }
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncthreads();
+        }
+        // the top node layer has no cells above it
+        if (own && k1 - 1 == nz && nz >= k0 && nz > kc1) update(nz, px, py, pz);
+        __syncthreads();  // (the next piece's loads reuse the ring)
     }
-    // the top node layer has no cells above it
-    if (own && k1 - 1 == nz && nz >= k0 && nz > kc1) update(nz, px, py, pz);
-    __syncthreads();
     if (tid != 0) return;
     if (s_nonfinite) atomicOr(&ctrl->diverged, 1);
     __threadfence();

@@ -556,28 +556,32 @@ public:
     // such box (tests), DJG_FLAG_NO_FUSED or DJG_NO_FUSED=1 keep the
     // two-kernel step.
     bool detect_box(const int32_t* conn) {
-        if (kind_ != DJG_T4 || sizeof(Real) != 4 || !compact_ || tled_ || !X_.p || n_slabs_ != 1 || win_) return false;
+        if (sizeof(Real) != 4 || !compact_ || tled_ || n_slabs_ != 1 || win_) return false;
+        if (kind_ == DJG_T4 && !X_.p) return false;
         if (model_ != DJG_NH && model_ != DJG_TI && model_ != DJG_OT) return false;
         if ((flags_ & DJG_FLAG_NO_FUSED) || (std::getenv("DJG_NO_FUSED") && std::atoi(std::getenv("DJG_NO_FUSED"))))
             return false;
         const bool forced = (flags_ & DJG_FLAG_FUSED) || (std::getenv("DJG_FUSED") && std::atoi(std::getenv("DJG_FUSED")));
-        if (E_ < 6 || E_ % 6) return false;
+        const bool t4 = kind_ == DJG_T4;
+        const int per_cell = t4 ? 6 : 1, per = t4 ? 24 : 8;
+        if (E_ < per_cell || E_ % per_cell || conn[0] != 0 || conn[1] != 1) return false;
+        // T4 tet 0 runs corners 0 -> 1 -> 3 -> 7; H8 corners 0, 1, (1,1,0), (0,1,0), (0,0,1), ...
         const int64_t nx = int64_t(conn[2]) - 2;
-        if (nx < 1 || conn[0] != 0 || conn[1] != 1) return false;
-        const int64_t plane = int64_t(conn[3]) - conn[2];
+        if (nx < 1) return false;
+        const int64_t plane = t4 ? int64_t(conn[3]) - conn[2] : int64_t(conn[4]);
         if (plane % (nx + 1)) return false;
         const int64_t ny = plane / (nx + 1) - 1;
         if (ny < 1 || N_ % ((nx + 1) * (ny + 1))) return false;
         const int64_t nz = N_ / ((nx + 1) * (ny + 1)) - 1;
-        if (nz < 1 || 6 * nx * ny * nz != E_ || nx > INT32_MAX / 2 || ny > INT32_MAX / 2 || nz > INT32_MAX / 2)
+        if (nz < 1 || per_cell * nx * ny * nz != E_ || nx > INT32_MAX / 2 || ny > INT32_MAX / 2 || nz > INT32_MAX / 2)
             return false;
         const int32_t div[3] = {int32_t(nx), int32_t(ny), int32_t(nz)};
         bool ok = true;
 #pragma omp parallel for schedule(static) reduction(&& : ok)
         for (int64_t c = 0; c < nx * ny * nz; ++c) {
             int32_t cc[24];
-            box_cell_conn(DJG_T4, div, c, cc);
-            ok = ok && std::memcmp(cc, conn + c * 24, sizeof(cc)) == 0;
+            box_cell_conn(t4 ? 0 : 1, div, c, cc);
+            ok = ok && std::memcmp(cc, conn + c * per, size_t(per) * sizeof(int32_t)) == 0;
         }
         if (!ok) return false;
         box_.nx = int(nx);
@@ -585,18 +589,27 @@ public:
         box_.nz = int(nz);
         box_.tiles_x = int((nx + 1 + kBoxBX - 1) / kBoxBX);
         box_.tiles_y = int((ny + 1 + kBoxBY - 1) / kBoxBY);
-        const size_t smem = BoxShape<kBoxBX, kBoxBY>::template smem_bytes<Real>();
         int per_sm = 0;
-        auto setup = [&](auto kern) {
+        auto setup = [&](auto kern, size_t smem, int threads) {
             CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
             int nb = 0;
-            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, BoxShape<kBoxBX, kBoxBY>::kThreads, smem));
+            CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem));
             per_sm = per_sm == 0 ? nb : std::min(per_sm, nb);
         };
         if constexpr (sizeof(Real) == 4) {
-            setup(k_box_step<Real, DJG_NH, kBoxBX, kBoxBY>);
-            setup(k_box_step<Real, DJG_TI, kBoxBX, kBoxBY>);
-            setup(k_box_step<Real, DJG_OT, kBoxBX, kBoxBY>);
+            if (t4) {
+                using BS = BoxShape<kBoxBX, kBoxBY>;
+                const size_t smem = BS::template smem_bytes<Real>();
+                setup(k_box_step<Real, DJG_NH, kBoxBX, kBoxBY>, smem, BS::kThreads);
+                setup(k_box_step<Real, DJG_TI, kBoxBX, kBoxBY>, smem, BS::kThreads);
+                setup(k_box_step<Real, DJG_OT, kBoxBX, kBoxBY>, smem, BS::kThreads);
+            } else {
+                using BS = BoxShapeH8<kBoxBX, kBoxBY>;
+                const size_t smem = BS::template smem_bytes<Real>();
+                setup(k_box_step_h8<Real, DJG_NH, kBoxBX, kBoxBY>, smem, BS::kThreads);
+                setup(k_box_step_h8<Real, DJG_TI, kBoxBX, kBoxBY>, smem, BS::kThreads);
+                setup(k_box_step_h8<Real, DJG_OT, kBoxBX, kBoxBY>, smem, BS::kThreads);
+            }
         }
         if (per_sm < 1) return false;
         box_grid_ = per_sm * sms_;  // persistent: every block resident
@@ -609,12 +622,22 @@ public:
     void launch_box(cudaStream_t s) {
         if constexpr (sizeof(Real) == 4) {
             const unsigned grid = unsigned(box_grid_);
-            const size_t smem = BoxShape<kBoxBX, kBoxBY>::template smem_bytes<Real>();
-            constexpr int NT = BoxShape<kBoxBX, kBoxBY>::kThreads;
-            switch (model_) {
-                case DJG_NH: k_box_step<Real, DJG_NH, kBoxBX, kBoxBY><<<grid, NT, smem, s>>>(ea_, na_, box_); break;
-                case DJG_TI: k_box_step<Real, DJG_TI, kBoxBX, kBoxBY><<<grid, NT, smem, s>>>(ea_, na_, box_); break;
-                default: k_box_step<Real, DJG_OT, kBoxBX, kBoxBY><<<grid, NT, smem, s>>>(ea_, na_, box_); break;
+            if (kind_ == DJG_T4) {
+                using BS = BoxShape<kBoxBX, kBoxBY>;
+                const size_t smem = BS::template smem_bytes<Real>();
+                switch (model_) {
+                    case DJG_NH: k_box_step<Real, DJG_NH, kBoxBX, kBoxBY><<<grid, BS::kThreads, smem, s>>>(ea_, na_, box_); break;
+                    case DJG_TI: k_box_step<Real, DJG_TI, kBoxBX, kBoxBY><<<grid, BS::kThreads, smem, s>>>(ea_, na_, box_); break;
+                    default: k_box_step<Real, DJG_OT, kBoxBX, kBoxBY><<<grid, BS::kThreads, smem, s>>>(ea_, na_, box_); break;
+                }
+            } else {
+                using BS = BoxShapeH8<kBoxBX, kBoxBY>;
+                const size_t smem = BS::template smem_bytes<Real>();
+                switch (model_) {
+                    case DJG_NH: k_box_step_h8<Real, DJG_NH, kBoxBX, kBoxBY><<<grid, BS::kThreads, smem, s>>>(ea_, na_, box_); break;
+                    case DJG_TI: k_box_step_h8<Real, DJG_TI, kBoxBX, kBoxBY><<<grid, BS::kThreads, smem, s>>>(ea_, na_, box_); break;
+                    default: k_box_step_h8<Real, DJG_OT, kBoxBX, kBoxBY><<<grid, BS::kThreads, smem, s>>>(ea_, na_, box_); break;
+                }
             }
             CK(cudaGetLastError());
         }

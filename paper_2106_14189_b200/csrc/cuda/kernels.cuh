@@ -1759,6 +1759,13 @@ struct BoxArgs {
     int tiles_x, tiles_y;
 };
 
+// H8 corner signs (element.hpp:17-20) as a compile-time function for device code.
+__device__ __forceinline__ constexpr int kBoxCornerSignDev(int a, int i) {
+    constexpr int s[8][3] = {{-1, -1, -1}, {+1, -1, -1}, {+1, +1, -1}, {-1, +1, -1},
+                             {-1, -1, +1}, {+1, -1, +1}, {+1, +1, +1}, {-1, +1, +1}};
+    return s[a][i];
+}
+
 // Corner code (dx + 2 dy + 4 dz) of local node a of Kuhn tet t
 // (generate_box's axis orders with the odd-permutation swap, mesh.hpp:228-258).
 __device__ __constant__ signed char kTetCorner[6][4] = {{0, 1, 3, 7}, {0, 5, 1, 7}, {0, 3, 2, 7},
@@ -1999,6 +2006,207 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
         // the top node layer has no cells above it
         if (own && k1 - 1 == nz && nz >= k0 && nz > kc1) update(nz, px, py, pz);
         __syncthreads();  // (the next piece's loads reuse the ring)
+    }
+    if (tid != 0) return;
+    if (s_nonfinite) atomicOr(&ctrl->diverged, 1);
+    __threadfence();
+    const unsigned int done = atomicAdd(&ctrl->blocks_done, 1u);
+    if (done != gridDim.x - 1) return;
+    close_step<false>(ctrl, step, NA.policy);
+    __threadfence();
+    ctrl->blocks_done = 0;
+}
+
+// The same fused step for a generated box of H8 cells (one hexahedron per
+// cell, corners in kBoxCornerSign order): a thread per footprint cell runs
+// element_body on its hex -- compact record planes streamed from HBM, node
+// rows from the stage -- and keeps its eight rows in shared memory; a node
+// folds the row of each of its eight cells (corner order below) in cell-id
+// order.
+template <class Real>
+struct BoxSrcH8 {
+    using Node = typename RT<Real>::Node;
+    static constexpr bool kRowSink = true;
+    const Node* su;
+    float* rows;       // planes [a][xyz][cell]
+    const typename RT<Real>::Plane* rec;  // this element's record: plane p at rec[p * E]
+    long long E;
+    int h[8];
+    int cell, ncell;
+    bool count_inv;
+    __device__ __forceinline__ int4 conn(int p) const { return make_int4(h[4 * p], h[4 * p + 1], h[4 * p + 2], h[4 * p + 3]); }
+    __device__ __forceinline__ Node node(int, const Node* __restrict__, int k) const { return su[k]; }
+    __device__ __forceinline__ Node coord(const ElemArgs<Real>&, int) const { return Node{}; }
+    __device__ __forceinline__ typename RT<Real>::Plane plane(int p) const { return RT<Real>::load_plane(rec + p * E); }
+    __device__ __forceinline__ Real tail(int) const { return Real(0); }
+    template <int N, int RB>
+    __device__ __forceinline__ void ranks(int (&rk)[N]) const {
+#pragma unroll
+        for (int a = 0; a < N; ++a) rk[a] = 0;
+    }
+    __device__ __forceinline__ int slot(const int* __restrict__, int a, int, int) const { return a; }
+    __device__ __forceinline__ void store(int a, Real x, Real y, Real z) const {
+        rows[(3 * a + 0) * ncell + cell] = x;
+        rows[(3 * a + 1) * ncell + cell] = y;
+        rows[(3 * a + 2) * ncell + cell] = z;
+    }
+};
+
+template <int BX, int BY>
+struct BoxShapeH8 {
+    static constexpr int SX = BX + 2, SY = BY + 2, CX = BX + 1, CY = BY + 1;
+    static constexpr int kStageNodes = SX * SY;
+    static constexpr int kThreads = (CX * CY + 31) / 32 * 32;
+    template <class Real>
+    static constexpr size_t smem_bytes() {
+        return 3 * size_t(kStageNodes) * sizeof(typename RT<Real>::Node) + size_t(CX) * CY * 24 * sizeof(float);
+    }
+};
+
+#ifndef DJG_BOXH8_MINB
+#define DJG_BOXH8_MINB 2
+#endif
+template <class Real, int MODEL, int BX, int BY>
+__global__ void __launch_bounds__(BoxShapeH8<BX, BY>::kThreads, DJG_BOXH8_MINB)
+    k_box_step_h8(const ElemArgs<Real> A, const NodeArgs<Real> NA, const BoxArgs B) {
+    static_assert(sizeof(Real) == 4, "the fused box step keeps float rows");
+    using T = RT<Real>;
+    using Node = typename T::Node;
+    using BS = BoxShapeH8<BX, BY>;
+    constexpr int NT = BS::kThreads, NCELL = BS::CX * BS::CY;
+    extern __shared__ __align__(128) unsigned char smem[];
+    Node* su = reinterpret_cast<Node*>(smem);
+    float* rows = reinterpret_cast<float*>(su + 3 * BS::kStageNodes);
+    __shared__ int s_nonfinite;
+    Ctrl* ctrl = A.ctrl;
+    if (*(volatile const int*)&ctrl->halted) return;
+    const int tid = threadIdx.x;
+    if (tid == 0) s_nonfinite = 0;
+    const int nx = B.nx, ny = B.ny, nz = B.nz;
+    int i0 = 0, j0 = 0, k0 = 0, k1 = 0;
+    const long long step = ctrl->step;
+    const int ph = int(step % 3);
+    const Node* ucur = pick3(ph, NA.u[0], NA.u[1], NA.u[2]);
+    const Node* uprv = pick3(ph, NA.u[2], NA.u[0], NA.u[1]);
+    Node* unxt = pick3(ph, NA.u[1], NA.u[2], NA.u[0]);
+    auto gid = [&](int i, int j, int k) { return (long long)i + (long long)(nx + 1) * (j + (long long)(ny + 1) * k); };
+    auto load_layer = [&](int k) {
+        if (k > nz) return;
+        const int slot = k % 3;
+        for (int q = tid; q < BS::kStageNodes; q += NT) {
+            const int gi = i0 - 1 + q % BS::SX, gj = j0 - 1 + q / BS::SX;
+            if (gi < 0 || gi > nx || gj < 0 || gj > ny) continue;
+            cp_async16(su + slot * BS::kStageNodes + q, ucur + gid(gi, gj, k));
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    int oi = 0, oj = 0, cb = 0, mci = 0, mcj = 0;
+    bool own = false, hx0 = false, hx1 = false, hy0 = false, hy1 = false, my_cell = false;
+    Real px = Real(0), py = Real(0), pz = Real(0);
+    auto row = [&](int a, int c, Real& fx, Real& fy, Real& fz) {
+        fx += rows[(3 * a + 0) * NCELL + c];
+        fy += rows[(3 * a + 1) * NCELL + c];
+        fz += rows[(3 * a + 2) * NCELL + c];
+    };
+    // the node is corner (dx, dy, dz) of cell (oi - dx, oj - dy): local node
+    // a of kBoxCornerSign: (1,1,dz) -> 2 / 6, (0,1,dz) -> 3 / 7, (1,0,dz) -> 1 / 5, (0,0,dz) -> 0 / 4
+    auto fold_below = [&](Real& fx, Real& fy, Real& fz) {
+        if (hy0 && hx0) row(6, cb, fx, fy, fz);
+        if (hy0 && hx1) row(7, cb + 1, fx, fy, fz);
+        if (hy1 && hx0) row(5, cb + BS::CX, fx, fy, fz);
+        if (hy1 && hx1) row(4, cb + BS::CX + 1, fx, fy, fz);
+    };
+    auto fold_above = [&](Real& fx, Real& fy, Real& fz) {
+        if (hy0 && hx0) row(2, cb, fx, fy, fz);
+        if (hy0 && hx1) row(3, cb + 1, fx, fy, fz);
+        if (hy1 && hx0) row(1, cb + BS::CX, fx, fy, fz);
+        if (hy1 && hx1) row(0, cb + BS::CX + 1, fx, fy, fz);
+    };
+    auto update = [&](int k, Real fx, Real fy, Real fz) {
+        const long long n = gid(oi, oj, k);
+        const typename T::Node uc = su[(k % 3) * BS::kStageNodes + (oj - j0 + 1) * BS::SX + (oi - i0 + 1)];
+        const typename T::Node up = T::load_node(uprv + n);
+        typename T::Node r;
+        if (NA.r_ext) r = T::load_node(NA.r_ext + n);
+        else { r.x = Real(0); r.y = Real(0); r.z = Real(0); }
+        const int code = NA.code[n];
+        const bool massless = (code >> 6) & 1;
+        const Real c1 = NA.c1[n];
+        const Real t_next = NA.dt * Real(step + 1);
+        bool nf = false;
+        const Real vx = dof_update<Real>(code & 3, massless, c1, r.x, fx, uc.x, up.x, NA.c2, NA.c3, t_next, NA.target,
+                                         NA.t_total, 3 * n + 0, nf);
+        const Real vy = dof_update<Real>((code >> 2) & 3, massless, c1, r.y, fy, uc.y, up.y, NA.c2, NA.c3, t_next,
+                                         NA.target, NA.t_total, 3 * n + 1, nf);
+        const Real vz = dof_update<Real>((code >> 4) & 3, massless, c1, r.z, fz, uc.z, up.z, NA.c2, NA.c3, t_next,
+                                         NA.target, NA.t_total, 3 * n + 2, nf);
+        T::store_node(unxt + n, vx, vy, vz);
+        if (nf) s_nonfinite = 1;
+    };
+    const int mcy = tid / BS::CX, mcx = tid - mcy * BS::CX;
+    const bool my_count = mcx < BX && mcy < BY;
+    const int mbase = mcy * BS::SX + mcx;
+    const long long L = nz + 1, W = (long long)B.tiles_x * B.tiles_y * L;
+    const long long w_end = W * (blockIdx.x + 1) / gridDim.x;
+    for (long long w = W * blockIdx.x / gridDim.x; w < w_end;) {
+        const long long col = w / L;
+        k0 = int(w - col * L);
+        k1 = int(min(L, (long long)k0 + (w_end - w)));
+        w += k1 - k0;
+        i0 = int(col % B.tiles_x) * BX;
+        j0 = int(col / B.tiles_x) * BY;
+        oi = i0 + tid % BX;
+        oj = j0 + tid / BX;
+        own = tid < BX * BY && oi <= nx && oj <= ny;
+        cb = (oj - j0) * BS::CX + (oi - i0);
+        hx0 = oi >= 1; hx1 = oi < nx; hy0 = oj >= 1; hy1 = oj < ny;
+        mci = i0 - 1 + mcx;
+        mcj = j0 - 1 + mcy;
+        my_cell = tid < NCELL && mci >= 0 && mci < nx && mcj >= 0 && mcj < ny;
+        px = Real(0); py = Real(0); pz = Real(0);
+        const int kc0 = max(k0 - 1, 0), kc1 = min(k1 - 1, nz - 1);
+        load_layer(kc0);
+        load_layer(kc0 + 1);
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+        for (int kc = kc0; kc <= kc1; ++kc) {
+            load_layer(kc + 2);
+            if (my_cell) {
+                const int slot0 = (kc % 3) * BS::kStageNodes, slot1 = ((kc + 1) % 3) * BS::kStageNodes;
+                const long long e = (long long)mci + (long long)nx * (mcj + (long long)ny * kc);
+                BoxSrcH8<Real> src;
+                src.su = su;
+                src.rows = rows;
+                src.rec = A.c + e;
+                src.E = A.E;
+                src.cell = tid;
+                src.ncell = NCELL;
+                src.count_inv = my_count && kc >= k0;
+#pragma unroll
+                for (int a = 0; a < 8; ++a) {
+                    const int dx = (kBoxCornerSignDev(a, 0) + 1) / 2, dy = (kBoxCornerSignDev(a, 1) + 1) / 2,
+                              dz = (kBoxCornerSignDev(a, 2) + 1) / 2;
+                    src.h[a] = (dz ? slot1 : slot0) + mbase + dy * BS::SX + dx;
+                }
+                element_body<Real, 1, MODEL, 1, true>(A, e, nullptr, src);
+            }
+            __syncthreads();
+            if (own) {
+                if (kc >= k0) {
+                    Real fx = px, fy = py, fz = pz;
+                    fold_above(fx, fy, fz);
+                    update(kc, fx, fy, fz);
+                }
+                if (kc + 1 < k1) {
+                    px = Real(0); py = Real(0); pz = Real(0);
+                    fold_below(px, py, pz);
+                }
+            }
+            asm volatile("cp.async.wait_all;" ::: "memory");
+            __syncthreads();
+        }
+        if (own && k1 - 1 == nz && nz >= k0 && nz > kc1) update(nz, px, py, pz);
+        __syncthreads();
     }
     if (tid != 0) return;
     if (s_nonfinite) atomicOr(&ctrl->diverged, 1);

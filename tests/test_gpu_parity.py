@@ -153,27 +153,29 @@ def test_node_windows_mixed_tiles():
         check_run(spec, 200, flags=A.DJG_FLAG_WINDOW | A.DJG_FLAG_NO_GRAPH)
 
 
+@pytest.mark.parametrize("kind", ["T4", "H8"])
 @pytest.mark.parametrize("model", ["NH", "TI", "OT"])
 @pytest.mark.parametrize("divisions", [(5, 4, 6), (17, 9, 33), (16, 16, 16), (33, 2, 5), (1, 1, 1)])
-def test_fused_box_step_bitwise(divisions, model):
+def test_fused_box_step_bitwise(divisions, model, kind):
     """k_box_step (DJG_FLAG_FUSED): one kernel per step on a generated box --
     element forces into shared memory, each node folding its tets' rows in
     ascending element id, the update -- bit-identical to the oracle, on boxes
     whose sides are and are not multiples of the 16 x 16 x 16 tile."""
-    spec = box_spec(kind="T4", model=model, divisions=divisions, precision=4, ramp_steps=200)
+    spec = box_spec(kind=kind, model=model, divisions=divisions, precision=4, ramp_steps=200)
     with GpuDjEngine(Scenario(spec), flags=A.DJG_FLAG_FUSED) as eng:
         assert eng.info()["fused"] == 1
     check_run(spec, 200, flags=A.DJG_FLAG_FUSED)
 
 
+@pytest.mark.parametrize("kind", ["T4", "H8"])
 @pytest.mark.parametrize("policy", [A.DJG_ABORT, A.DJG_SKIP_AND_REPORT])
-def test_fused_box_step_inversion(policy):
+def test_fused_box_step_inversion(policy, kind):
     """The fused step under a crushing load: Abort halts on the same element
     and step with the same state as the two-kernel step (the fused kernel has
     already written u_next when it learns of the inversion; the step is not
     closed, so the state stays), SkipAndReport gives the same counts (each
     inversion counted once, by the tile owning the cell)."""
-    spec = box_spec(kind="T4", divisions=(9, 7, 8), extent=(0.1, 0.1, 0.1), precision=4, target=-0.09,
+    spec = box_spec(kind=kind, divisions=(9, 7, 8), extent=(0.1, 0.1, 0.1), precision=4, target=-0.09,
                     ramp_steps=3, fix_all_axes=True, policy=policy)
     outs = []
     for flags in (A.DJG_FLAG_FUSED, A.DJG_FLAG_NO_FUSED):
@@ -191,10 +193,11 @@ def test_fused_box_step_inversion(policy):
     assert np.array_equal(u1, ur)
 
 
-def test_fused_box_step_large_vs_two_kernel():
-    """A 96^3 box (5.3M tets, 343 fused blocks) against the two-kernel step
-    on the same device, 300 steps, bitwise (u and u_prev)."""
-    spec = box_spec(kind="T4", model="NH", divisions=96, precision=4, target=0.01, ramp_steps=300)
+@pytest.mark.parametrize("kind,model,d", [("T4", "NH", 96), ("H8", "TI", 100)])
+def test_fused_box_step_large_vs_two_kernel(kind, model, d):
+    """A 96^3 T4 box (5.3M tets) and cfg4 (1M hexes, TI) against the
+    two-kernel step on the same device, 300 steps, bitwise (u and u_prev)."""
+    spec = box_spec(kind=kind, model=model, divisions=d, precision=4, target=0.01, ramp_steps=300)
     sc = Scenario(spec)
     res = []
     for flags in (A.DJG_FLAG_FUSED, A.DJG_FLAG_NO_FUSED):

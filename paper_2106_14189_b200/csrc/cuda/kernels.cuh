@@ -1771,6 +1771,30 @@ __device__ __forceinline__ constexpr int kBoxCornerSignDev(int a, int i) {
 __device__ __constant__ signed char kTetCorner[6][4] = {{0, 1, 3, 7}, {0, 5, 1, 7}, {0, 3, 2, 7},
                                                         {0, 2, 6, 7}, {0, 4, 5, 7}, {0, 6, 4, 7}};
 
+// Stage offset (dy * SX + dx, bit 7 = dz) of local node a of Kuhn tet t,
+// four per tet packed in a word.
+template <int SX>
+__device__ __forceinline__ unsigned tet_stage_offsets(int t) {
+    constexpr int C[6][4] = {{0, 1, 3, 7}, {0, 5, 1, 7}, {0, 3, 2, 7}, {0, 2, 6, 7}, {0, 4, 5, 7}, {0, 6, 4, 7}};
+    static_assert(SX + 1 < 128, "stage row too long for the packed offsets");
+    auto pack = [](int t2) {
+        unsigned w = 0;
+        for (int a = 0; a < 4; ++a) {
+            const int cr = C[t2][a];
+            w |= unsigned(((cr >> 1) & 1) * SX + (cr & 1) + ((cr >> 2) << 7)) << (8 * a);
+        }
+        return w;
+    };
+    switch (t) {
+        case 0: return pack(0);
+        case 1: return pack(1);
+        case 2: return pack(2);
+        case 3: return pack(3);
+        case 4: return pack(4);
+        default: return pack(5);
+    }
+}
+
 template <class Real>
 struct BoxSrc {
     using Node = typename RT<Real>::Node;
@@ -1967,7 +1991,7 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
             // six tets in order (a warp shares t: uniform corner offsets;
             // consecutive cells write consecutive row words)
             if (my_cell) {
-                const int slot0 = (kc % 3) * BS::kStageNodes, slot1 = ((kc + 1) % 3) * BS::kStageNodes;
+                const int hb0 = (kc % 3) * BS::kStageNodes + mbase, hb1 = ((kc + 1) % 3) * BS::kStageNodes + mbase;
                 const bool count = my_count && kc >= k0;
                 const long long ebase = ((long long)mci + (long long)nx * (mcj + (long long)ny * kc)) * 6;
     #pragma unroll kBoxUnrollT
@@ -1979,10 +2003,12 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
                     src.ntet = NTET;
                     src.row0 = (t * NCELL + tid) * 4;
                     src.count_inv = count;
-    #pragma unroll
+                        // the tet's four stage offsets, packed per tet (bit 7: upper layer)
+                    const unsigned pk = tet_stage_offsets<BS::SX>(t);
+#pragma unroll
                     for (int a = 0; a < 4; ++a) {
-                        const int cr = kTetCorner[t][a];
-                        src.h[a] = ((cr >> 2) ? slot1 : slot0) + mbase + ((cr >> 1) & 1) * BS::SX + (cr & 1);
+                        const unsigned v = (pk >> (8 * a)) & 0xffu;
+                        src.h[a] = ((v & 0x80u) ? hb1 : hb0) + int(v & 0x7fu);
                     }
                     element_body<Real, 0, MODEL, 1, true>(A, ebase + t, nullptr, src);
                 }

@@ -209,17 +209,14 @@ struct NodeArgs {
 // (no FMA: --fmad=false) it returns the same bits as the host libm; pinned by
 // tests/test_cbrt.py against the host for every float in [0.25, 4).
 __device__ __forceinline__ double glibc_cbrt_factor(int r) {
-    // 2^(r/3) for r = xe % 3 in {-2..2}
-    switch (r) {
-        case -2: return 1.0 / 1.5874010519681994748;
-        case -1: return 1.0 / 1.2599210498948731648;
-        case 1: return 1.2599210498948731648;
-        case 2: return 1.5874010519681994748;
-        default: return 1.0;
-    }
+    // 2^(r/3) for r = xe % 3 in {-2..2} (selects, no branch)
+    const double pos = r == 1 ? 1.2599210498948731648 : 1.5874010519681994748;
+    const double neg = r == -1 ? 1.0 / 1.2599210498948731648 : 1.0 / 1.5874010519681994748;
+    return r == 0 ? 1.0 : (r > 0 ? pos : neg);
 }
 
-__device__ __forceinline__ float ref_cbrt(float x) {
+// glibc's cbrtf for zero, subnormal, infinite and NaN x (frexpf / ldexpf).
+__device__ __noinline__ float ref_cbrt_general(float x) {
     int xe;
     const float xm = frexpf(fabsf(x), &xe);
     if (x == 0.0f || !isfinite(x)) return x + x;
@@ -229,6 +226,24 @@ __device__ __forceinline__ float ref_cbrt(float x) {
     const float ym = float(double(u) * (double(t2) + 2.0 * double(xm)) / (2.0 * double(t2) + double(xm)) *
                            glibc_cbrt_factor(xe % 3));
     return ldexpf(x > 0.0f ? ym : -ym, xe / 3);
+}
+
+// Normal x: frexp and ldexp on the exponent field directly -- the same
+// values (|ym| lies in [0.5, 1.6) and |xe / 3| <= 42, so the result is normal
+// and the exponent addition is exact).
+__device__ __forceinline__ float ref_cbrt(float x) {
+    const unsigned bits = __float_as_uint(x);
+    const unsigned ex = (bits >> 23) & 0xffu;
+    if (ex == 0u || ex == 0xffu) return ref_cbrt_general(x);
+    const int xe = int(ex) - 126;
+    const float xm = __uint_as_float((bits & 0x007fffffu) | 0x3f000000u);
+    const float u = float(0.492659620528969547 + (0.697570460207922770 - 0.191502161678719066 * double(xm)) *
+                                                     double(xm));
+    const float t2 = u * u * u;
+    const float ym = float(double(u) * (double(t2) + 2.0 * double(xm)) / (2.0 * double(t2) + double(xm)) *
+                           glibc_cbrt_factor(xe % 3));
+    const float sy = x > 0.0f ? ym : -ym;
+    return __uint_as_float(__float_as_uint(sy) + (unsigned(xe / 3) << 23));
 }
 
 __device__ __forceinline__ double ref_cbrt(double x) {

@@ -519,7 +519,9 @@ def our_arm(args):
                      "issue_active": issue,
                      "note": ("the fused step keeps the element forces on chip: it moves ~0.6 GB per cfg5 step "
                               "against the two-kernel step's 8.2 GB, so HBM is not its bound -- instruction issue "
-                              "is (issue_active: ncu smsp__issue_active of the same capture). " if fused else
+                              "is (issue_active: ncu smsp__issue_active of the same capture); with engine.lattice = 1 the tets' "
+                              "records come from the verified per-class table instead of a per-tet rebuild "
+                              "(DESIGN.md §4). " if fused else
                               "moved_frac is the kernel's efficiency: measured DRAM bytes (traffic, ncu, capture "
                               "of the same kernel sources unless traffic_stale) / event-timed launch / peak. ") +
                              "achieved/frac use SURVEY §8(d)'s algorithmic bytes (the reference's hot-field set, "
@@ -534,7 +536,7 @@ def our_arm(args):
         "gpu_launches": (1 if fused else 2) * K,
         "clocks": clk,
         "engine": {k: info[k] for k in ("slabs", "kernels_per_step", "device_bytes", "slot_capacity", "pipelined",
-                                        "fused")},
+                                        "fused", "lattice")},
     }
     extra["config"] = None
     line = _line(args, 1, K, W, E, ms_step, value, {k: v for k, v in extra.items() if k != "config"})

@@ -312,7 +312,7 @@ typedef struct djg_engine_info {
     int32_t windowed;           /* ... with each tile's node rows staged as windows */
     int64_t window_tiles;       /* tiles whose nodes fit a window (the rest gather) */
     int32_t fused;              /* 1: one fused kernel per step (generated box, k_box_step) */
-    int32_t _pad_fused;
+    int32_t lattice;            /* 1: the fused step reads its records from the lattice table */
 } djg_engine_info;
 int djg_get_info(djg_engine* eng, djg_engine_info* info);
 

@@ -163,7 +163,7 @@ class djg_engine_info(C.Structure):
         ("npe", C.c_int32), ("nconst", C.c_int32), ("const_planes", C.c_int32), ("precision", C.c_int32),
         ("kernels_per_step", C.c_int32), ("sm_count", C.c_int32), ("slabs", C.c_int32),
         ("compact", C.c_int32), ("slab_elements", C.c_int64), ("formulation", C.c_int32), ("pipelined", C.c_int32),
-        ("windowed", C.c_int32), ("window_tiles", C.c_int64), ("fused", C.c_int32), ("_pad_fused", C.c_int32),
+        ("windowed", C.c_int32), ("window_tiles", C.c_int64), ("fused", C.c_int32), ("lattice", C.c_int32),
     ]
 
 

@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -533,6 +534,7 @@ public:
         if (win_) build_windows(d.conn);
         if (pipe_) launch_element(stream_, 0, E_, nullptr, /*setup=*/true);
         fused_ = detect_box(d.conn);
+        if (fused_ && kind_ == DJG_T4 && d.nodes) build_lattice(static_cast<const Real*>(d.nodes));
         if (!win_) {
             slot_.release();
             widx_.release();
@@ -599,10 +601,17 @@ public:
         if constexpr (sizeof(Real) == 4) {
             if (t4) {
                 using BS = BoxShape<kBoxBX, kBoxBY>;
-                const size_t smem = BS::template smem_bytes<Real>();
-                setup(k_box_step<Real, DJG_NH, kBoxBX, kBoxBY>, smem, BS::kThreads);
-                setup(k_box_step<Real, DJG_TI, kBoxBX, kBoxBY>, smem, BS::kThreads);
-                setup(k_box_step<Real, DJG_OT, kBoxBX, kBoxBY>, smem, BS::kThreads);
+                const size_t smem = BS::template smem_bytes<Real>(), lsmem = BS::template smem_bytes<Real, true>();
+                setup(k_box_step<Real, DJG_NH, kBoxBX, kBoxBY, false>, smem, BS::kThreads);
+                setup(k_box_step<Real, DJG_TI, kBoxBX, kBoxBY, false>, smem, BS::kThreads);
+                setup(k_box_step<Real, DJG_OT, kBoxBX, kBoxBY, false>, smem, BS::kThreads);
+                // (the lattice variants: the same grid -- their smem is smaller)
+                CK(cudaFuncSetAttribute(k_box_step<Real, DJG_NH, kBoxBX, kBoxBY, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(lsmem)));
+                CK(cudaFuncSetAttribute(k_box_step<Real, DJG_TI, kBoxBX, kBoxBY, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(lsmem)));
+                CK(cudaFuncSetAttribute(k_box_step<Real, DJG_OT, kBoxBX, kBoxBY, true>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, int(lsmem)));
             } else {
                 using BS = BoxShapeH8<kBoxBX, kBoxBY>;
                 const size_t smem = BS::template smem_bytes<Real>();
@@ -624,11 +633,21 @@ public:
             const unsigned grid = unsigned(box_grid_);
             if (kind_ == DJG_T4) {
                 using BS = BoxShape<kBoxBX, kBoxBY>;
-                const size_t smem = BS::template smem_bytes<Real>();
-                switch (model_) {
-                    case DJG_NH: k_box_step<Real, DJG_NH, kBoxBX, kBoxBY><<<grid, BS::kThreads, smem, s>>>(ea_, na_, box_); break;
-                    case DJG_TI: k_box_step<Real, DJG_TI, kBoxBX, kBoxBY><<<grid, BS::kThreads, smem, s>>>(ea_, na_, box_); break;
-                    default: k_box_step<Real, DJG_OT, kBoxBX, kBoxBY><<<grid, BS::kThreads, smem, s>>>(ea_, na_, box_); break;
+                auto go = [&](auto kern, size_t smem) { kern<<<grid, BS::kThreads, smem, s>>>(ea_, na_, box_); };
+                if (lattice_) {
+                    const size_t smem = BS::template smem_bytes<Real, true>();
+                    switch (model_) {
+                        case DJG_NH: go(k_box_step<Real, DJG_NH, kBoxBX, kBoxBY, true>, smem); break;
+                        case DJG_TI: go(k_box_step<Real, DJG_TI, kBoxBX, kBoxBY, true>, smem); break;
+                        default: go(k_box_step<Real, DJG_OT, kBoxBX, kBoxBY, true>, smem); break;
+                    }
+                } else {
+                    const size_t smem = BS::template smem_bytes<Real>();
+                    switch (model_) {
+                        case DJG_NH: go(k_box_step<Real, DJG_NH, kBoxBX, kBoxBY, false>, smem); break;
+                        case DJG_TI: go(k_box_step<Real, DJG_TI, kBoxBX, kBoxBY, false>, smem); break;
+                        default: go(k_box_step<Real, DJG_OT, kBoxBX, kBoxBY, false>, smem); break;
+                    }
                 }
             } else {
                 using BS = BoxShapeH8<kBoxBX, kBoxBY>;
@@ -640,6 +659,92 @@ public:
                 }
             }
             CK(cudaGetLastError());
+        }
+    }
+
+    // Coordinate lattice (generate_box's nodes: x depends on i alone, y on j,
+    // z on k): a tet's compact record is a function of its J0 alone, and J0
+    // of tet t in cell (i, j, k) is built from the x / y / z rows of the
+    // cell's two node planes per axis -- so cells whose three axis intervals
+    // hold the same coordinate pairs up to the exact differences the rebuild
+    // forms have the same six records. Axis classes: the pair ((0 + -a) + b,
+    // (0 + -b) + a) of the interval's end coordinates a, b (the two J0
+    // entries it can produce). k_lattice_table rebuilds the record of each
+    // class triple once; k_lattice_verify then rebuilds every tet's record
+    // and compares it bit for bit with its class's, and the fused step reads
+    // the table (not the coordinates) only if all agree -- cfg5: 9 classes
+    // per axis, 729 x 6 records (0.4 MB), against ~22 % of the step's
+    // instructions. DJG_LATTICE=0 keeps the per-tet rebuild.
+    void build_lattice(const Real* nodes) {
+        if constexpr (sizeof(Real) == 4) {
+            const char* v = std::getenv("DJG_LATTICE");
+            if (v && std::atoi(v) == 0) return;
+            const int64_t nx = box_.nx, ny = box_.ny, nz = box_.nz;
+            auto gid = [&](int64_t i, int64_t j, int64_t k) { return i + (nx + 1) * (j + (ny + 1) * k); };
+            std::vector<int32_t> cls(size_t(nx + ny + nz)), rep;
+            int ncl[3] = {0, 0, 0};
+            const int64_t n[3] = {nx, ny, nz};
+            int64_t off = 0;
+            for (int ax = 0; ax < 3; ++ax) {
+                std::map<std::pair<uint32_t, uint32_t>, int> ids;
+                for (int64_t i = 0; i < n[ax]; ++i) {
+                    const int64_t g0 = ax == 0 ? gid(i, 0, 0) : ax == 1 ? gid(0, i, 0) : gid(0, 0, i);
+                    const int64_t g1 = ax == 0 ? gid(i + 1, 0, 0) : ax == 1 ? gid(0, i + 1, 0) : gid(0, 0, i + 1);
+                    const Real a = nodes[3 * g0 + ax], b = nodes[3 * g1 + ax];
+                    const Real fwd = (Real(0) + -a) + b, bwd = (Real(0) + -b) + a;
+                    uint32_t kf, kb;
+                    std::memcpy(&kf, &fwd, 4);
+                    std::memcpy(&kb, &bwd, 4);
+                    const auto [it, fresh] = ids.emplace(std::make_pair(kf, kb), int(ids.size()));
+                    if (fresh) rep.push_back(int32_t(i));  // the class's first cell index
+                    cls[size_t(off + i)] = it->second;
+                }
+                ncl[ax] = int(ids.size());
+                off += n[ax];
+            }
+            const int64_t ncomb = int64_t(ncl[0]) * ncl[1] * ncl[2];
+            int nq = 0;
+            switch (model_) {
+                case DJG_NH: nq = kLatQuads<DJG_NH>; break;
+                case DJG_TI: nq = kLatQuads<DJG_TI>; break;
+                default: nq = kLatQuads<DJG_OT>; break;
+            }
+            const size_t bytes = size_t(ncomb) * 6 * nq * sizeof(float4);
+            if (bytes > (size_t(16) << 20)) return;  // an irregular box: too many classes
+            lcls_.alloc(cls.size() * sizeof(int32_t));
+            CK(cudaMemcpy(lcls_.p, cls.data(), lcls_.bytes, cudaMemcpyHostToDevice));
+            DevBuf drep, bad;
+            drep.alloc(rep.size() * sizeof(int32_t));
+            CK(cudaMemcpy(drep.p, rep.data(), drep.bytes, cudaMemcpyHostToDevice));
+            lat_.alloc(bytes);
+            bad.alloc(sizeof(unsigned long long));
+            CK(cudaMemset(bad.p, 0, bad.bytes));
+            BoxArgs b = box_;
+            b.lat = lat_.as<float4>();
+            b.lcls = lcls_.as<int32_t>();
+            b.lncx = ncl[0];
+            b.lncy = ncl[1];
+            b.lncz = ncl[2];
+            const unsigned tb = unsigned((ncomb * 6 + 127) / 128), vb = unsigned(sms_ * 8);
+            auto run = [&](auto table, auto verify) {
+                table<<<tb, 128>>>(ea_, b, drep.as<int32_t>(), lat_.as<float4>());
+                verify<<<vb, 256>>>(ea_, b, lat_.as<float4>(), bad.as<unsigned long long>());
+            };
+            switch (model_) {
+                case DJG_NH: run(k_lattice_table<Real, DJG_NH>, k_lattice_verify<Real, DJG_NH>); break;
+                case DJG_TI: run(k_lattice_table<Real, DJG_TI>, k_lattice_verify<Real, DJG_TI>); break;
+                default: run(k_lattice_table<Real, DJG_OT>, k_lattice_verify<Real, DJG_OT>); break;
+            }
+            CK(cudaGetLastError());
+            unsigned long long nbad = 0;
+            CK(cudaMemcpy(&nbad, bad.p, sizeof(nbad), cudaMemcpyDeviceToHost));
+            if (nbad) {
+                lat_.release();
+                lcls_.release();
+                return;
+            }
+            box_ = b;
+            lattice_ = true;
         }
     }
 
@@ -1860,6 +1965,7 @@ public:
         o->pipelined = pipe_ ? 1 : 0;
         o->windowed = win_ ? 1 : 0;
         o->fused = fused_now() ? 1 : 0;
+        o->lattice = fused_now() && lattice_ ? 1 : 0;
         o->window_tiles = win_tiles_;
         o->slabs = n_slabs_;
         o->slab_elements = slab_elems_;
@@ -1937,6 +2043,8 @@ private:
     bool fused_ = false;               // generated box of T4 cells: one fused kernel per step (k_box_step)
     BoxArgs box_{};
     int box_grid_ = 0;
+    bool lattice_ = false;  // the fused step reads records from lat_ (build_lattice)
+    DevBuf lat_, lcls_;
     uint32_t flags_ = 0;
     int64_t N_ = 0, E_ = 0, capacity_ = 0;
     cudaStream_t stream_ = nullptr;

@@ -455,6 +455,46 @@ __device__ __forceinline__ void fibre_quad_term(const Real* M, const Real* Im, c
     dev += Real(2) * d * Ib;
 }
 
+// A row source that supplies the whole record of an element (the fused box
+// step on a coordinate lattice: one record per tet kind and cell-size class).
+template <class S, class = void>
+struct SrcLattice : std::false_type {};
+template <class S>
+struct SrcLattice<S, std::void_t<decltype(S::kLattice)>> : std::bool_constant<S::kLattice> {};
+
+// Compact T4 record, part 1 -- jacobian0 (element.hpp:59-77):
+// J0[i][j] = sum_a D[i][a] x_a[j] with D[i] = (-1, e_i), summed from +0 in
+// node order; the 0 * x terms cannot change a sum that is never -0, so
+// J0[i][j] = (0 + -x_0[j]) + x_{i+1}[j] exactly; then det J0 and volume0
+// (element.hpp:80-85).
+template <class Node, class Real>
+__device__ __forceinline__ void t4_jacobian0(int kind, const Node (&x)[4], Real* c) {
+    const Real x0[3] = {Real(0) + -x[0].x, Real(0) + -x[0].y, Real(0) + -x[0].z};
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        c[3 * i + 0] = x0[0] + x[i + 1].x;
+        c[3 * i + 1] = x0[1] + x[i + 1].y;
+        c[3 * i + 2] = x0[2] + x[i + 1].z;
+    }
+    const Real J0[3][3] = {{c[0], c[1], c[2]}, {c[3], c[4], c[5]}, {c[6], c[7], c[8]}};
+    c[9] = em::det3(J0);
+    c[10] = em::volume0(kind, c[9]);
+}
+
+// Compact record, part 2: the invariant tensors from J0^-1 and V0, the
+// precompute's own arithmetic (element.hpp / invariants.hpp).
+template <class Real, int KIND, int MODEL>
+__device__ __forceinline__ void compact_record_tail(const ElemArgs<Real>& A, Real* c) {
+    using L = Layout<KIND, MODEL>;
+    const Real J0[3][3] = {{c[0], c[1], c[2]}, {c[3], c[4], c[5]}, {c[6], c[7], c[8]}};
+    Real J0i[3][3];
+    em::inv3(J0, c[9], J0i);
+    em::first_invariant_tensors_fast(J0i, c[10], c + 11, c + 17);
+    if constexpr (L::kI4) em::fibre_tensors(J0i, c[10], A.mat.A, c + L::m4, c + L::I4m);
+    if constexpr (L::kI6) em::fibre_tensors(J0i, c[10], A.mat.B, c + L::m6, c + L::I6m);
+    if constexpr (L::kI2) em::second_invariant_tensors(J0i, c[10], c + 11, c + L::M2, c + L::I2m);
+}
+
 template <class Real, int KIND, int MODEL, int RB, bool COMPACT, class Src>
 __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long long e,
                                              const typename RT<Real>::Node* __restrict__ u, const Src& src) {
@@ -510,37 +550,19 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
 #pragma unroll
         for (int k = 0; k < NCU; ++k) c[k] = r[k];
     } else {
-        if constexpr (KIND == 0) {
-            // jacobian0 (element.hpp:59-77): J0[i][j] = sum_a D[i][a] x_a[j]
-            // with D[i] = (-1, e_i), summed from +0 in node order; the 0 * x
-            // terms cannot change a sum that is never -0, so
-            // J0[i][j] = (0 + -x_0[j]) + x_{i+1}[j] exactly.
-            Real x0[3];
-            {
-                const typename T::Node v = src.coord(A, nid[0]);
-                x0[0] = Real(0) + -v.x; x0[1] = Real(0) + -v.y; x0[2] = Real(0) + -v.z;
-            }
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                const typename T::Node v = src.coord(A, nid[i + 1]);
-                c[3 * i + 0] = x0[0] + v.x;
-                c[3 * i + 1] = x0[1] + v.y;
-                c[3 * i + 2] = x0[2] + v.z;
-            }
-            const Real J0[3][3] = {{c[0], c[1], c[2]}, {c[3], c[4], c[5]}, {c[6], c[7], c[8]}};
-            c[9] = em::det3(J0);                 // jacobian0 (element.hpp:59-77)
-            c[10] = em::volume0(KIND, c[9]);     // volume0 (element.hpp:80-85)
+        if constexpr (KIND == 0 && SrcLattice<Src>::value) {
+            src.template lattice_record<L::count>(c);  // the whole record of this tet's lattice class (k_box_step)
         } else {
+            if constexpr (KIND == 0) {
+                const typename T::Node x[4] = {src.coord(A, nid[0]), src.coord(A, nid[1]), src.coord(A, nid[2]),
+                                               src.coord(A, nid[3])};
+                t4_jacobian0(KIND, x, c);
+            } else {
 #pragma unroll
-            for (int k = 0; k < 11; ++k) c[k] = r[k];
+                for (int k = 0; k < 11; ++k) c[k] = r[k];
+            }
+            compact_record_tail<Real, KIND, MODEL>(A, c);
         }
-        const Real J0[3][3] = {{c[0], c[1], c[2]}, {c[3], c[4], c[5]}, {c[6], c[7], c[8]}};
-        Real J0i[3][3];
-        em::inv3(J0, c[9], J0i);
-        em::first_invariant_tensors_fast(J0i, c[10], c + 11, c + 17);
-        if constexpr (L::kI4) em::fibre_tensors(J0i, c[10], A.mat.A, c + L::m4, c + L::I4m);
-        if constexpr (L::kI6) em::fibre_tensors(J0i, c[10], A.mat.B, c + L::m6, c + L::I6m);
-        if constexpr (L::kI2) em::second_invariant_tensors(J0i, c[10], c + 11, c + L::M2, c + L::I2m);
     }
     // update_jacobian (kinematics.hpp:31-45): Jt = J0 + D U.
     Real Jt[3][3];
@@ -1772,6 +1794,13 @@ constexpr int kBoxUnrollT = DJG_BOX_UNROLL_T;
 struct BoxArgs {
     int nx, ny, nz;   // cells per axis
     int tiles_x, tiles_y;
+    // coordinate lattice (k_box_step<..., LAT = true>): the record of tet t
+    // of a cell with axis classes (cx, cy, cz) is lat[((cz * lncy + cy) * lncx
+    // + cx) * 6 + t] (float4-padded); lcls = the class of every cell index
+    // along x, then y, then z
+    const float4* lat;
+    const int* lcls;
+    int lncx, lncy, lncz, _pad;
 };
 
 // H8 corner signs (element.hpp:17-20) as a compile-time function for device code.
@@ -1810,12 +1839,25 @@ __device__ __forceinline__ unsigned tet_stage_offsets(int t) {
     }
 }
 
-template <class Real>
+template <class Real, bool LAT = false>
 struct BoxSrc {
     using Node = typename RT<Real>::Node;
     static constexpr bool kRowSink = true;
+    static constexpr bool kLattice = LAT;
     const Node* su;    // stage u (all ring slots)
-    const Node* sx;    // stage X
+    const Node* sx;    // stage X (LAT: unused)
+    const float4* lrec;  // LAT: this tet's record
+    template <int NREC>
+    __device__ __forceinline__ void lattice_record(Real* c) const {
+#pragma unroll
+        for (int q = 0; q < (NREC + 3) / 4; ++q) {
+            const float4 v = __ldg(lrec + q);
+            c[4 * q] = v.x;
+            if (4 * q + 1 < NREC) c[4 * q + 1] = v.y;
+            if (4 * q + 2 < NREC) c[4 * q + 2] = v.z;
+            if (4 * q + 3 < NREC) c[4 * q + 3] = v.w;
+        }
+    }
     float* rows;       // [footprint cell][t][a][3]
     int h[4];          // stage indices of the tet's nodes
     int row0;          // first row of this tet
@@ -1876,17 +1918,21 @@ struct BoxShape {
     // one thread per footprint cell (its six tets in turn: every thread the
     // same work per layer), the first BX * BY of them also one owned node each
     static constexpr int kThreads = (CX * CY + 31) / 32 * 32;
-    template <class Real>
+    template <class Real, bool LAT = false>
     static constexpr size_t smem_bytes() {
-        return 2 * 3 * size_t(kStageNodes) * sizeof(typename RT<Real>::Node) + kRowFloats * sizeof(float);
+        return (LAT ? 1 : 2) * 3 * size_t(kStageNodes) * sizeof(typename RT<Real>::Node) + kRowFloats * sizeof(float);
     }
 };
+
+// Floats of a T4 record in the lattice table (float4-padded per tet).
+template <int MODEL>
+constexpr int kLatQuads = (Layout<0, MODEL>::count + 3) / 4;
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
 }
 
-template <class Real, int MODEL, int BX, int BY>
+template <class Real, int MODEL, int BX, int BY, bool LAT>
 __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_box_step(const ElemArgs<Real> A, const NodeArgs<Real> NA,
                                                           const BoxArgs B) {
     static_assert(sizeof(Real) == 4, "the fused box step keeps float rows");
@@ -1897,7 +1943,8 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
     extern __shared__ __align__(128) unsigned char smem[];
     Node* su = reinterpret_cast<Node*>(smem);
     Node* sx = su + 3 * BS::kStageNodes;
-    float* rows = reinterpret_cast<float*>(sx + 3 * BS::kStageNodes);
+    float* rows = reinterpret_cast<float*>(su + (LAT ? 1 : 2) * 3 * BS::kStageNodes);
+    constexpr int NQ = kLatQuads<MODEL>;
     __shared__ int s_nonfinite;
     Ctrl* ctrl = A.ctrl;
     if (*(volatile const int*)&ctrl->halted) return;
@@ -1920,7 +1967,7 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
             if (gi < 0 || gi > nx || gj < 0 || gj > ny) continue;
             const long long n = gid(gi, gj, k);
             cp_async16(su + slot * BS::kStageNodes + q, ucur + n);
-            cp_async16(sx + slot * BS::kStageNodes + q, A.X + n);
+            if constexpr (!LAT) cp_async16(sx + slot * BS::kStageNodes + q, A.X + n);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -1994,6 +2041,10 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
         mci = i0 - 1 + mcx;
         mcj = j0 - 1 + mcy;
         my_cell = tid < NCELL && mci >= 0 && mci < nx && mcj >= 0 && mcj < ny;
+        int lxy = 0;  // LAT: the cell's (cy * lncx + cx)
+        if constexpr (LAT) {
+            if (my_cell) lxy = __ldg(B.lcls + nx + mcj) * B.lncx + __ldg(B.lcls + mci);
+        }
         px = Real(0); py = Real(0); pz = Real(0);
         const int kc0 = max(k0 - 1, 0), kc1 = min(k1 - 1, nz - 1);  // cell layers this piece computes
         load_layer(kc0);
@@ -2009,11 +2060,14 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
                 const int hb0 = (kc % 3) * BS::kStageNodes + mbase, hb1 = ((kc + 1) % 3) * BS::kStageNodes + mbase;
                 const bool count = my_count && kc >= k0;
                 const long long ebase = ((long long)mci + (long long)nx * (mcj + (long long)ny * kc)) * 6;
+                const float4* lcell = nullptr;
+                if constexpr (LAT) lcell = B.lat + size_t((__ldg(B.lcls + nx + ny + kc) * B.lncy) * B.lncx + lxy) * 6 * NQ;
     #pragma unroll kBoxUnrollT
                 for (int t = 0; t < 6; ++t) {
-                    BoxSrc<Real> src;
+                    BoxSrc<Real, LAT> src;
                     src.su = su;
                     src.sx = sx;
+                    src.lrec = LAT ? lcell + t * NQ : nullptr;
                     src.rows = rows;
                     src.ntet = NTET;
                     src.row0 = (t * NCELL + tid) * 4;
@@ -2056,6 +2110,74 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
     close_step<false>(ctrl, step, NA.policy);
     __threadfence();
     ctrl->blocks_done = 0;
+}
+
+// Lattice table of the fused T4 step: for every axis-class triple, the
+// record of each tet of a representative cell (rep[cx], rep[lncx + cy],
+// rep[lncx + lncy + cz]: the first cell index of each class), rebuilt by
+// element_body's own compact arithmetic.
+template <class Node>
+__device__ __forceinline__ void box_tet_coords(const Node* __restrict__ X, const BoxArgs& B, int ci, int cj, int ck,
+                                               int t, Node (&x)[4]) {
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int cr = kTetCorner[t][a];
+        x[a] = X[(long long)(ci + (cr & 1)) +
+                 (long long)(B.nx + 1) * ((cj + ((cr >> 1) & 1)) + (long long)(B.ny + 1) * (ck + (cr >> 2)))];
+    }
+}
+
+template <class Real, int MODEL>
+__global__ void k_lattice_table(const ElemArgs<Real> A, const BoxArgs B, const int* __restrict__ rep,
+                                float4* __restrict__ lat) {
+    constexpr int NQ = kLatQuads<MODEL>;
+    const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (q >= (long long)B.lncx * B.lncy * B.lncz * 6) return;
+    const int t = int(q % 6);
+    const long long comb = q / 6;
+    const int cx = int(comb % B.lncx), cy = int(comb / B.lncx % B.lncy), cz = int(comb / B.lncx / B.lncy);
+    typename RT<Real>::Node x[4];
+    box_tet_coords(A.X, B, rep[cx], rep[B.lncx + cy], rep[B.lncx + B.lncy + cz], t, x);
+    Real c[NQ * 4];
+#pragma unroll
+    for (int k = 0; k < NQ * 4; ++k) c[k] = Real(0);
+    t4_jacobian0(0, x, c);
+    compact_record_tail<Real, 0, MODEL>(A, c);
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) lat[q * NQ + k] = make_float4(c[4 * k], c[4 * k + 1], c[4 * k + 2], c[4 * k + 3]);
+}
+
+// Every tet of the box against its class's table record, bit for bit (+0
+// and -0 distinct); `bad` counts the mismatches. The fused step reads the
+// table only when there are none: the table is exact by check, not by an
+// argument about the coordinates.
+template <class Real, int MODEL>
+__global__ void k_lattice_verify(const ElemArgs<Real> A, const BoxArgs B, const float4* __restrict__ lat,
+                                 unsigned long long* bad) {
+    constexpr int NQ = kLatQuads<MODEL>, NREC = Layout<0, MODEL>::count;
+    const long long ncell = (long long)B.nx * B.ny * B.nz;
+    unsigned long long mism = 0;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < ncell * 6;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int t = int(e % 6);
+        const long long cell = e / 6;
+        const int ci = int(cell % B.nx), cj = int(cell / B.nx % B.ny), ck = int(cell / B.nx / B.ny);
+        typename RT<Real>::Node x[4];
+        box_tet_coords(A.X, B, ci, cj, ck, t, x);
+        Real c[NQ * 4];
+#pragma unroll
+        for (int k = 0; k < NQ * 4; ++k) c[k] = Real(0);
+        t4_jacobian0(0, x, c);
+        compact_record_tail<Real, 0, MODEL>(A, c);
+        const long long comb =
+            ((long long)B.lcls[B.nx + B.ny + ck] * B.lncy + B.lcls[B.nx + cj]) * B.lncx + B.lcls[ci];
+        const float* want = reinterpret_cast<const float*>(lat + (comb * 6 + t) * NQ);
+        bool same = true;
+#pragma unroll
+        for (int k = 0; k < NREC; ++k) same = same && __float_as_uint(c[k]) == __float_as_uint(want[k]);
+        mism += same ? 0 : 1;
+    }
+    if (mism) atomicAdd(bad, mism);
 }
 
 // The same fused step for a generated box of H8 cells (one hexahedron per

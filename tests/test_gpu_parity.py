@@ -163,8 +163,50 @@ def test_fused_box_step_bitwise(divisions, model, kind):
     whose sides are and are not multiples of the 16 x 16 x 16 tile."""
     spec = box_spec(kind=kind, model=model, divisions=divisions, precision=4, ramp_steps=200)
     with GpuDjEngine(Scenario(spec), flags=A.DJG_FLAG_FUSED) as eng:
-        assert eng.info()["fused"] == 1
+        info = eng.info()
+        assert info["fused"] == 1 and info["lattice"] == (kind == "T4")
     check_run(spec, 200, flags=A.DJG_FLAG_FUSED)
+
+
+def _box_with_nodes(divisions, move, **kw):
+    """A generated T4 box's connectivity with its node coordinates moved by
+    move(x) (fixed bottom face, prescribed top face)."""
+    img = Scenario(box_spec(kind="T4", divisions=divisions, precision=4)).image()
+    x = move(img["nodes"].reshape(-1, 3).astype(np.float64))
+    z = x[:, 2]
+    bottom, top = np.flatnonzero(z == z.min()), np.flatnonzero(z == z.max())
+    return mesh_spec(x, img["conn"].reshape(-1, 4), kind="T4", precision=4,
+                     fixed=[(int(n), a) for n in bottom for a in range(3)],
+                     prescribed=[(int(n), 2, -0.04, 1e-3) for n in top], **kw)
+
+
+@pytest.mark.parametrize("model", ["NH", "TI", "OT"])
+def test_fused_lattice_table(model, monkeypatch):
+    """The fused T4 step's lattice table (build_lattice): on a graded lattice
+    (x_i = (i / n)^2: a class per interval, hundreds of class triples) the
+    table is used and bit-identical to the oracle; on the same box with one
+    interior node moved off the lattice the table check fails on the tets
+    around it and the step rebuilds every record (lattice = 0), still
+    bit-identical; DJG_LATTICE=0 gives the rebuild on the generated box."""
+    d = (11, 7, 9)
+    graded = _box_with_nodes(d, lambda x: x * x, model=model)
+
+    def off_lattice(x):
+        x = x.copy()
+        n = 3 + 12 * (4 + 8 * 5)  # node (3, 4, 5)
+        x[n, 0] += 0.013
+        return x
+    moved = _box_with_nodes(d, off_lattice, model=model)
+    for spec, want in ((graded, 1), (moved, 0)):
+        with GpuDjEngine(Scenario(spec), flags=A.DJG_FLAG_FUSED) as eng:
+            info = eng.info()
+            assert info["fused"] == 1 and info["lattice"] == want, info
+        check_run(spec, 150, flags=A.DJG_FLAG_FUSED)
+    monkeypatch.setenv("DJG_LATTICE", "0")
+    spec = box_spec(kind="T4", model=model, divisions=d, precision=4, ramp_steps=150)
+    with GpuDjEngine(Scenario(spec), flags=A.DJG_FLAG_FUSED) as eng:
+        assert eng.info()["lattice"] == 0
+    check_run(spec, 150, flags=A.DJG_FLAG_FUSED)
 
 
 @pytest.mark.parametrize("kind", ["T4", "H8"])

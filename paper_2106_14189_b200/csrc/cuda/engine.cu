@@ -682,6 +682,7 @@ public:
             const int64_t nx = box_.nx, ny = box_.ny, nz = box_.nz;
             auto gid = [&](int64_t i, int64_t j, int64_t k) { return i + (nx + 1) * (j + (ny + 1) * k); };
             std::vector<int32_t> cls(size_t(nx + ny + nz)), rep;
+            std::vector<float> len;  // each class's interval length (0 + -a) + b
             int ncl[3] = {0, 0, 0};
             const int64_t n[3] = {nx, ny, nz};
             int64_t off = 0;
@@ -696,7 +697,10 @@ public:
                     std::memcpy(&kf, &fwd, 4);
                     std::memcpy(&kb, &bwd, 4);
                     const auto [it, fresh] = ids.emplace(std::make_pair(kf, kb), int(ids.size()));
-                    if (fresh) rep.push_back(int32_t(i));  // the class's first cell index
+                    if (fresh) {
+                        rep.push_back(int32_t(i));  // the class's first cell index
+                        len.push_back(float(fwd));
+                    }
                     cls[size_t(off + i)] = it->second;
                 }
                 ncl[ax] = int(ids.size());
@@ -713,6 +717,8 @@ public:
             if (bytes > (size_t(16) << 20)) return;  // an irregular box: too many classes
             lcls_.alloc(cls.size() * sizeof(int32_t));
             CK(cudaMemcpy(lcls_.p, cls.data(), lcls_.bytes, cudaMemcpyHostToDevice));
+            ld_.alloc(len.size() * sizeof(float));
+            CK(cudaMemcpy(ld_.p, len.data(), ld_.bytes, cudaMemcpyHostToDevice));
             DevBuf drep, bad;
             drep.alloc(rep.size() * sizeof(int32_t));
             CK(cudaMemcpy(drep.p, rep.data(), drep.bytes, cudaMemcpyHostToDevice));
@@ -722,6 +728,7 @@ public:
             BoxArgs b = box_;
             b.lat = lat_.as<float4>();
             b.lcls = lcls_.as<int32_t>();
+            b.ld = ld_.as<float>();
             b.lncx = ncl[0];
             b.lncy = ncl[1];
             b.lncz = ncl[2];
@@ -741,6 +748,7 @@ public:
             if (nbad) {
                 lat_.release();
                 lcls_.release();
+                ld_.release();
                 return;
             }
             box_ = b;
@@ -2044,7 +2052,7 @@ private:
     BoxArgs box_{};
     int box_grid_ = 0;
     bool lattice_ = false;  // the fused step reads records from lat_ (build_lattice)
-    DevBuf lat_, lcls_;
+    DevBuf lat_, lcls_, ld_;
     uint32_t flags_ = 0;
     int64_t N_ = 0, E_ = 0, capacity_ = 0;
     cudaStream_t stream_ = nullptr;

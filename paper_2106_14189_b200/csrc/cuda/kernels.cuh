@@ -1785,7 +1785,7 @@ __global__ void __launch_bounds__(256) k_node(const NodeArgs<Real> A) {
 // cfg5 step). Inversions are counted by the tile that owns the cell (the
 // one owning node (ci+1, cj+1)) in the segment that owns its layer.
 #ifndef DJG_BOX_UNROLL_T
-#define DJG_BOX_UNROLL_T 2  // tets of a cell per unrolled iteration (1: 1.58 ms on cfg5, 2: 1.57, 6: 1.60)
+#define DJG_BOX_UNROLL_T 6  // tets of a cell per unrolled iteration (lattice table, cfg5: 1: 1.28 ms, 2: 1.27, 3: 1.28, 6: 1.22)
 #endif
 constexpr int kBoxUnrollT = DJG_BOX_UNROLL_T;
 #ifndef DJG_BOX_MINB
@@ -1794,12 +1794,14 @@ constexpr int kBoxUnrollT = DJG_BOX_UNROLL_T;
 struct BoxArgs {
     int nx, ny, nz;   // cells per axis
     int tiles_x, tiles_y;
-    // coordinate lattice (k_box_step<..., LAT = true>): the record of tet t
-    // of a cell with axis classes (cx, cy, cz) is lat[((cz * lncy + cy) * lncx
-    // + cx) * 6 + t] (float4-padded); lcls = the class of every cell index
-    // along x, then y, then z
+    // coordinate lattice (k_box_step<..., LAT = true>): record fields 9.. of
+    // tet t of a cell with axis classes (cx, cy, cz) are lat[((cz * lncy + cy)
+    // * lncx + cx) * 6 + t] (float4-padded); its J0 is made of the classes'
+    // interval lengths ld[cx], ld[lncx + cy], ld[lncx + lncy + cz]; lcls =
+    // the class of every cell index along x, then y, then z
     const float4* lat;
     const int* lcls;
+    const float* ld;
     int lncx, lncy, lncz, _pad;
 };
 
@@ -1839,6 +1841,28 @@ __device__ __forceinline__ unsigned tet_stage_offsets(int t) {
     }
 }
 
+// J0 of Kuhn tet t on a lattice cell with interval lengths d: node 0 is
+// corner 0, so row i (node i + 1 at corner cr) is d_j where cr has bit j,
+// else (0 + -x) + x = +0 -- t4_jacobian0's values (k_lattice_verify checks
+// them on every tet).
+__device__ __forceinline__ void lattice_j0(int t, const float (&d)[3], float* c) {
+    constexpr int C[6][4] = {{0, 1, 3, 7}, {0, 5, 1, 7}, {0, 3, 2, 7}, {0, 2, 6, 7}, {0, 4, 5, 7}, {0, 6, 4, 7}};
+    int cr[3];
+    switch (t) {
+        case 0: cr[0] = C[0][1]; cr[1] = C[0][2]; break;
+        case 1: cr[0] = C[1][1]; cr[1] = C[1][2]; break;
+        case 2: cr[0] = C[2][1]; cr[1] = C[2][2]; break;
+        case 3: cr[0] = C[3][1]; cr[1] = C[3][2]; break;
+        case 4: cr[0] = C[4][1]; cr[1] = C[4][2]; break;
+        default: cr[0] = C[5][1]; cr[1] = C[5][2]; break;
+    }
+    cr[2] = 7;
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) c[3 * i + j] = ((cr[i] >> j) & 1) ? d[j] : 0.0f;
+}
+
 template <class Real, bool LAT = false>
 struct BoxSrc {
     using Node = typename RT<Real>::Node;
@@ -1846,16 +1870,19 @@ struct BoxSrc {
     static constexpr bool kLattice = LAT;
     const Node* su;    // stage u (all ring slots)
     const Node* sx;    // stage X (LAT: unused)
-    const float4* lrec;  // LAT: this tet's record
+    const float4* lrec;  // LAT: this tet's record fields 9..
+    float d[3];          // LAT: the cell's interval lengths
+    int t;               // LAT: the tet (a compile-time constant once the tet loop is unrolled)
     template <int NREC>
     __device__ __forceinline__ void lattice_record(Real* c) const {
+        lattice_j0(t, d, c);
 #pragma unroll
-        for (int q = 0; q < (NREC + 3) / 4; ++q) {
+        for (int q = 0; q < (NREC - 9 + 3) / 4; ++q) {
             const float4 v = __ldg(lrec + q);
-            c[4 * q] = v.x;
-            if (4 * q + 1 < NREC) c[4 * q + 1] = v.y;
-            if (4 * q + 2 < NREC) c[4 * q + 2] = v.z;
-            if (4 * q + 3 < NREC) c[4 * q + 3] = v.w;
+            c[9 + 4 * q] = v.x;
+            if (9 + 4 * q + 1 < NREC) c[9 + 4 * q + 1] = v.y;
+            if (9 + 4 * q + 2 < NREC) c[9 + 4 * q + 2] = v.z;
+            if (9 + 4 * q + 3 < NREC) c[9 + 4 * q + 3] = v.w;
         }
     }
     float* rows;       // [footprint cell][t][a][3]
@@ -1926,7 +1953,7 @@ struct BoxShape {
 
 // Floats of a T4 record in the lattice table (float4-padded per tet).
 template <int MODEL>
-constexpr int kLatQuads = (Layout<0, MODEL>::count + 3) / 4;
+constexpr int kLatQuads = (Layout<0, MODEL>::count - 9 + 3) / 4;
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
@@ -2041,9 +2068,15 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
         mci = i0 - 1 + mcx;
         mcj = j0 - 1 + mcy;
         my_cell = tid < NCELL && mci >= 0 && mci < nx && mcj >= 0 && mcj < ny;
-        int lxy = 0;  // LAT: the cell's (cy * lncx + cx)
+        int lxy = 0;  // LAT: the cell's (cy * lncx + cx) and x / y interval lengths
+        float ldx = 0.0f, ldy = 0.0f;
         if constexpr (LAT) {
-            if (my_cell) lxy = __ldg(B.lcls + nx + mcj) * B.lncx + __ldg(B.lcls + mci);
+            if (my_cell) {
+                const int cx = __ldg(B.lcls + mci), cy = __ldg(B.lcls + nx + mcj);
+                lxy = cy * B.lncx + cx;
+                ldx = __ldg(B.ld + cx);
+                ldy = __ldg(B.ld + B.lncx + cy);
+            }
         }
         px = Real(0); py = Real(0); pz = Real(0);
         const int kc0 = max(k0 - 1, 0), kc1 = min(k1 - 1, nz - 1);  // cell layers this piece computes
@@ -2061,13 +2094,20 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
                 const bool count = my_count && kc >= k0;
                 const long long ebase = ((long long)mci + (long long)nx * (mcj + (long long)ny * kc)) * 6;
                 const float4* lcell = nullptr;
-                if constexpr (LAT) lcell = B.lat + size_t((__ldg(B.lcls + nx + ny + kc) * B.lncy) * B.lncx + lxy) * 6 * NQ;
+                float ldz = 0.0f;
+                if constexpr (LAT) {
+                    const int cz = __ldg(B.lcls + nx + ny + kc);
+                    lcell = B.lat + size_t(cz * B.lncy * B.lncx + lxy) * 6 * NQ;
+                    ldz = __ldg(B.ld + B.lncx + B.lncy + cz);
+                }
     #pragma unroll kBoxUnrollT
                 for (int t = 0; t < 6; ++t) {
                     BoxSrc<Real, LAT> src;
                     src.su = su;
                     src.sx = sx;
                     src.lrec = LAT ? lcell + t * NQ : nullptr;
+                    src.d[0] = ldx; src.d[1] = ldy; src.d[2] = ldz;
+                    src.t = t;
                     src.rows = rows;
                     src.ntet = NTET;
                     src.row0 = (t * NCELL + tid) * 4;
@@ -2138,13 +2178,14 @@ __global__ void k_lattice_table(const ElemArgs<Real> A, const BoxArgs B, const i
     const int cx = int(comb % B.lncx), cy = int(comb / B.lncx % B.lncy), cz = int(comb / B.lncx / B.lncy);
     typename RT<Real>::Node x[4];
     box_tet_coords(A.X, B, rep[cx], rep[B.lncx + cy], rep[B.lncx + B.lncy + cz], t, x);
-    Real c[NQ * 4];
+    Real c[9 + NQ * 4];
 #pragma unroll
-    for (int k = 0; k < NQ * 4; ++k) c[k] = Real(0);
+    for (int k = 0; k < 9 + NQ * 4; ++k) c[k] = Real(0);
     t4_jacobian0(0, x, c);
     compact_record_tail<Real, 0, MODEL>(A, c);
+    const Real* f = c + 9;
 #pragma unroll
-    for (int k = 0; k < NQ; ++k) lat[q * NQ + k] = make_float4(c[4 * k], c[4 * k + 1], c[4 * k + 2], c[4 * k + 3]);
+    for (int k = 0; k < NQ; ++k) lat[q * NQ + k] = make_float4(f[4 * k], f[4 * k + 1], f[4 * k + 2], f[4 * k + 3]);
 }
 
 // Every tet of the box against its class's table record, bit for bit (+0
@@ -2164,17 +2205,22 @@ __global__ void k_lattice_verify(const ElemArgs<Real> A, const BoxArgs B, const 
         const int ci = int(cell % B.nx), cj = int(cell / B.nx % B.ny), ck = int(cell / B.nx / B.ny);
         typename RT<Real>::Node x[4];
         box_tet_coords(A.X, B, ci, cj, ck, t, x);
-        Real c[NQ * 4];
+        Real c[9 + NQ * 4];
 #pragma unroll
-        for (int k = 0; k < NQ * 4; ++k) c[k] = Real(0);
+        for (int k = 0; k < 9 + NQ * 4; ++k) c[k] = Real(0);
         t4_jacobian0(0, x, c);
         compact_record_tail<Real, 0, MODEL>(A, c);
-        const long long comb =
-            ((long long)B.lcls[B.nx + B.ny + ck] * B.lncy + B.lcls[B.nx + cj]) * B.lncx + B.lcls[ci];
+        const int cx = B.lcls[ci], cy = B.lcls[B.nx + cj], cz = B.lcls[B.nx + B.ny + ck];
+        const long long comb = ((long long)cz * B.lncy + cy) * B.lncx + cx;
         const float* want = reinterpret_cast<const float*>(lat + (comb * 6 + t) * NQ);
+        float j0[9];
+        const float d[3] = {B.ld[cx], B.ld[B.lncx + cy], B.ld[B.lncx + B.lncy + cz]};
+        lattice_j0(t, d, j0);
         bool same = true;
 #pragma unroll
-        for (int k = 0; k < NREC; ++k) same = same && __float_as_uint(c[k]) == __float_as_uint(want[k]);
+        for (int k = 0; k < 9; ++k) same = same && __float_as_uint(c[k]) == __float_as_uint(j0[k]);
+#pragma unroll
+        for (int k = 9; k < NREC; ++k) same = same && __float_as_uint(c[k]) == __float_as_uint(want[k - 9]);
         mism += same ? 0 : 1;
     }
     if (mism) atomicAdd(bad, mism);

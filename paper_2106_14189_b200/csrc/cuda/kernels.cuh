@@ -2021,16 +2021,27 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
         if (hy1 && hx0) corner_rows<1, NCELL>(rows, NTET, cb + BS::CX, fx, fy, fz);
         if (hy1 && hx1) corner_rows<0, NCELL>(rows, NTET, cb + BS::CX + 1, fx, fy, fz);
     };
-    auto update = [&](int k, Real fx, Real fy, Real fz) {
+    // the update's per-node operands, loaded a cell layer ahead of their use
+    // (their HBM latency then overlaps the layer's tets, not the barrier)
+    struct NodeOps {
+        typename T::Node up;
+        int code;
+        Real c1;
+    };
+    auto node_ops = [&](int k) {
+        const long long n = gid(oi, oj, k);
+        return NodeOps{T::load_node(uprv + n), int(NA.code[n]), NA.c1[n]};
+    };
+    auto update = [&](int k, const NodeOps& ops, Real fx, Real fy, Real fz) {
         const long long n = gid(oi, oj, k);
         const typename T::Node uc = su[(k % 3) * BS::kStageNodes + (oj - j0 + 1) * BS::SX + (oi - i0 + 1)];
-        const typename T::Node up = T::load_node(uprv + n);
+        const typename T::Node up = ops.up;
         typename T::Node r;
         if (NA.r_ext) r = T::load_node(NA.r_ext + n);
         else { r.x = Real(0); r.y = Real(0); r.z = Real(0); }
-        const int code = NA.code[n];
+        const int code = ops.code;
         const bool massless = (code >> 6) & 1;
-        const Real c1 = NA.c1[n];
+        const Real c1 = ops.c1;
         const Real t_next = NA.dt * Real(step + 1);
         bool nf = false;
         const Real vx = dof_update<Real>(code & 3, massless, c1, r.x, fx, uc.x, up.x, NA.c2, NA.c3, t_next, NA.target,
@@ -2089,6 +2100,8 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
             // 2. the cell layer's tets around the tile: this thread's cell, its
             // six tets in order (a warp shares t: uniform corner offsets;
             // consecutive cells write consecutive row words)
+            NodeOps ops{};
+            if (own && kc >= k0) ops = node_ops(kc);
             if (my_cell) {
                 const int hb0 = (kc % 3) * BS::kStageNodes + mbase, hb1 = ((kc + 1) % 3) * BS::kStageNodes + mbase;
                 const bool count = my_count && kc >= k0;
@@ -2128,7 +2141,7 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
                 if (kc >= k0) {
                     Real fx = px, fy = py, fz = pz;
                     fold_above(fx, fy, fz);
-                    update(kc, fx, fy, fz);
+                    update(kc, ops, fx, fy, fz);
                 }
                 if (kc + 1 < k1) {
                     px = Real(0); py = Real(0); pz = Real(0);
@@ -2139,7 +2152,7 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
             __syncthreads();
         }
         // the top node layer has no cells above it
-        if (own && k1 - 1 == nz && nz >= k0 && nz > kc1) update(nz, px, py, pz);
+        if (own && k1 - 1 == nz && nz >= k0 && nz > kc1) update(nz, node_ops(nz), px, py, pz);
         __syncthreads();  // (the next piece's loads reuse the ring)
     }
     if (tid != 0) return;

@@ -358,12 +358,16 @@ def sub_config(name: str, device: int, warmup: int = 100, steps: int = 1000) -> 
     B = algo_bytes(c["kind"], c["model"], N, E, 4)
     traffic, src, stale = measured_traffic(name, element_kernel_prefix(info))
     k1 = me / 100
+    fused = bool(info.get("fused"))  # one kernel: its algorithmic bytes are the step's
     return {"workload": f"{name}: {c['kind']}-{c['model']} unit cube d={c['divisions']}", "num_elements": E,
             "num_nodes": N, "steps": steps, "warmup": warmup, "status": rep.status, "ms_per_step": ms,
-            "value": E / (ms * 1e-3), "unit": UNIT, "k_element_ms": k1, "k_node_ms": mn / 100,
-            "step_frac": B["step"] / (ms * 1e-3) / 1e9 / hbm, "k_element_frac": B["k_element"] / (k1 * 1e-3) / 1e9 / hbm,
+            "value": E / (ms * 1e-3), "unit": UNIT, "kernel": element_kernel_prefix(info), "fused": int(fused),
+            "lattice": int(info.get("lattice", 0)), "k_element_ms": k1, "k_node_ms": mn / 100,
+            "step_frac": B["step"] / (ms * 1e-3) / 1e9 / hbm,
+            "k_element_frac": B["step" if fused else "k_element"] / (k1 * 1e-3) / 1e9 / hbm,
             "moved_frac": (traffic / (k1 * 1e-3) / 1e9 / hbm) if traffic else None, "traffic": traffic,
-            "traffic_source": src, "traffic_stale": stale}
+            "traffic_source": src, "traffic_stale": stale,
+            "issue_active": measured_issue(name, element_kernel_prefix(info))}
 
 
 # SURVEY §8(d) config names, keyed by (kind, material, divisions).

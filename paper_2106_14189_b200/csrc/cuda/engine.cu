@@ -533,8 +533,17 @@ public:
         win_ = pipe_ && (flags_ & DJG_FLAG_WINDOW) && (kind_ == DJG_T4 || DJG_WIN_H8);
         if (win_) build_windows(d.conn);
         if (pipe_) launch_element(stream_, 0, E_, nullptr, /*setup=*/true);
-        fused_ = detect_box(d.conn);
-        if (fused_ && kind_ == DJG_T4 && d.nodes) build_lattice(static_cast<const Real*>(d.nodes));
+        if (detect_box(d.conn)) {
+            // the fused step pays for its column pieces' extra cell layer and
+            // its halo cells: with per-tet rebuilds it wins from >= 32
+            // column-layers per block (cfg5: 116, not cfg3: 6); with the
+            // lattice table from >= 4 (cfg3: 75.3 -> 67.3 us). Smaller boxes
+            // keep the kernel form their flags ask for.
+            const int64_t W = int64_t(box_.tiles_x) * box_.tiles_y * (box_.nz + 1), g = box_grid_;
+            if (kind_ == DJG_T4 && d.nodes && (box_forced_ || W >= 4 * g))
+                build_lattice(static_cast<const Real*>(d.nodes));
+            fused_ = box_forced_ || W >= 32 * g || (lattice_ && W >= 4 * g);
+        }
         if (!win_) {
             slot_.release();
             widx_.release();
@@ -552,11 +561,11 @@ public:
     // from element 0 (its first tet runs corner 0 -> 1 -> 3 -> 7: node ids 0,
     // 1, nx + 2, nx + 2 + (nx + 1)(ny + 1)); every element is then checked
     // against the generator. f32 compact records (J0 rebuilt from X) with
-    // NH / TI / OT, one part, no slabs. It is the default when the box is
-    // large enough to fill the GPU (>= 4 waves of its blocks: cfg5, not cfg3,
-    // where its column tiles are too few); DJG_FLAG_FUSED forces it on any
-    // such box (tests), DJG_FLAG_NO_FUSED or DJG_NO_FUSED=1 keep the
-    // two-kernel step.
+    // NH / TI / OT, one part, no slabs. It is the default when the box gives
+    // every block enough column-layers (the constructor's gate);
+    // DJG_FLAG_FUSED forces it on any such box (tests), DJG_FLAG_NO_FUSED or
+    // DJG_NO_FUSED=1 keep the two-kernel step. Returns whether the box
+    // qualifies (box_, box_grid_ set).
     bool detect_box(const int32_t* conn) {
         if (sizeof(Real) != 4 || !compact_ || tled_ || n_slabs_ != 1 || win_) return false;
         if (kind_ == DJG_T4 && !X_.p) return false;
@@ -622,10 +631,8 @@ public:
         }
         if (per_sm < 1) return false;
         box_grid_ = per_sm * sms_;  // persistent: every block resident
-        // each block walks W / grid column-layers with one extra cell layer
-        // per column piece: worth it from >= 32 layers per block (cfg5: 116)
-        const int64_t W = int64_t(box_.tiles_x) * box_.tiles_y * (nz + 1);
-        return forced || W >= 32LL * box_grid_;
+        box_forced_ = forced;
+        return true;
     }
 
     void launch_box(cudaStream_t s) {
@@ -2052,6 +2059,7 @@ private:
     BoxArgs box_{};
     int box_grid_ = 0;
     bool lattice_ = false;  // the fused step reads records from lat_ (build_lattice)
+    bool box_forced_ = false;  // DJG_FLAG_FUSED / DJG_FUSED=1
     DevBuf lat_, lcls_, ld_;
     uint32_t flags_ = 0;
     int64_t N_ = 0, E_ = 0, capacity_ = 0;

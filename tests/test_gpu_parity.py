@@ -317,7 +317,10 @@ def test_slab_path_cfg(cfg, monkeypatch):
 
 def test_slab_schedule_on_large_mesh():
     sc = Scenario(config_spec("cfg3", precision=4))
-    with GpuDjEngine(sc) as eng:
+    with GpuDjEngine(sc) as eng:  # cfg3's default: the fused step on the lattice table
+        info = eng.info()
+        assert info["fused"] == 1 and info["lattice"] == 1 and info["kernels_per_step"] == 1
+    with GpuDjEngine(sc, flags=A.DJG_FLAG_NO_FUSED) as eng:
         assert eng.info()["slabs"] == 1 and eng.info()["kernels_per_step"] == 2
     with GpuDjEngine(sc, flags=A.DJG_FLAG_SLABS) as eng:
         info = eng.info()
@@ -340,10 +343,11 @@ def test_many_slabs_bitwise(kind, model, monkeypatch):
 @pytest.mark.slow
 def test_cfg3_slab_vs_two_kernel_bitwise():
     spec = config_spec("cfg3", precision=4, target=0.01, ramp_steps=1000)
-    a = run_gpu(spec, 50)[0]
+    a = run_gpu(spec, 50)[0]  # fused (lattice table)
     b = run_gpu(spec, 50, flags=A.DJG_FLAG_SLABS)[0]
     c = run_gpu(spec, 50, flags=A.DJG_FLAG_SLABS | A.DJG_FLAG_NO_DISCARD)[0]
-    assert np.array_equal(a, b) and np.array_equal(a, c)
+    d = run_gpu(spec, 50, flags=A.DJG_FLAG_NO_FUSED)[0]
+    assert np.array_equal(a, b) and np.array_equal(a, c) and np.array_equal(a, d)
 
 
 @pytest.mark.parametrize("flags", [A.DJG_FLAG_SLABS | A.DJG_FLAG_NO_DISCARD, A.DJG_FLAG_NO_GRAPH | A.DJG_FLAG_SLABS,

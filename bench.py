@@ -558,20 +558,29 @@ def our_arm(args):
     # element forces with the same gather/update (DJG_FLAG_TLED), graph replay.
     if args.tled_steps > 0:
         from paper_2106_14189_b200 import _abi as A
-        with GpuDjEngine(sc, device=device, flags=A.DJG_FLAG_TLED) as teng:
-            teng.step(W)
-            ts = torch.cuda.ExternalStream(teng.stream)
-            t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            torch.cuda.synchronize()
-            t0e.record(ts)
-            teng.step_async(args.tled_steps)
-            t1e.record(ts)
-            t1e.synchronize()
-            trep = teng.sync()
-        tled_ms = t0e.elapsed_time(t1e) / args.tled_steps
+
+        def replay(flags):
+            with GpuDjEngine(sc, device=device, flags=flags) as teng:
+                teng.step(W)
+                ts = torch.cuda.ExternalStream(teng.stream)
+                t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda.synchronize()
+                t0e.record(ts)
+                teng.step_async(args.tled_steps)
+                t1e.record(ts)
+                t1e.synchronize()
+                return t0e.elapsed_time(t1e) / args.tled_steps, teng.sync().status
+        tled_ms, tstatus = replay(A.DJG_FLAG_TLED)
         line["tled"] = {"ms_per_step": tled_ms, "value": E / (tled_ms * 1e-3), "unit": UNIT,
-                        "dj_over_tled_time": ms_step / tled_ms, "status": trep.status,
-                        "note": "paper Table 5 ratio (CPU: 0.70-0.88); same problem, DJG_FLAG_TLED"}
+                        "dj_over_tled_time": ms_step / tled_ms, "status": tstatus,
+                        "note": "paper Table 5 ratio (CPU: 0.70-0.88) on the same problem and the same kernel "
+                                "shape: DJ-TLED (this line's step) against conventional TLED (DJG_FLAG_TLED), "
+                                "both in the fused box step on the lattice table when the line's step is fused; "
+                                "two_kernel: both as element kernel + CSR gather / update kernel"}
+        if info.get("fused"):
+            dj2_ms, _ = replay(A.DJG_FLAG_NO_FUSED)
+            tl2_ms, _ = replay(A.DJG_FLAG_TLED | A.DJG_FLAG_NO_FUSED)
+            line["tled"]["two_kernel"] = {"dj_ms": dj2_ms, "tled_ms": tl2_ms, "dj_over_tled_time": dj2_ms / tl2_ms}
     sc.close()
     # SURVEY §8(d)'s secondary precision: the same problem in f64 (graph
     # replay, events on the engine stream; per-kernel split from

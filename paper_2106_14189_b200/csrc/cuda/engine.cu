@@ -567,8 +567,11 @@ public:
     // DJG_NO_FUSED=1 keep the two-kernel step. Returns whether the box
     // qualifies (box_, box_grid_ set).
     bool detect_box(const int32_t* conn) {
-        if (sizeof(Real) != 4 || !compact_ || tled_ || n_slabs_ != 1 || win_) return false;
-        if (kind_ == DJG_T4 && !X_.p) return false;
+        // DJ-TLED: f32 compact records (T4 rebuilt from X, H8 streamed);
+        // TLED: T4, its B0 / V0 planes streamed or from the lattice table
+        if (sizeof(Real) != 4 || n_slabs_ != 1 || win_) return false;
+        if (tled_ ? kind_ != DJG_T4 : !compact_) return false;
+        if (kind_ == DJG_T4 && !tled_ && !X_.p) return false;
         if (model_ != DJG_NH && model_ != DJG_TI && model_ != DJG_OT) return false;
         if ((flags_ & DJG_FLAG_NO_FUSED) || (std::getenv("DJG_NO_FUSED") && std::atoi(std::getenv("DJG_NO_FUSED"))))
             return false;
@@ -608,7 +611,16 @@ public:
             per_sm = per_sm == 0 ? nb : std::min(per_sm, nb);
         };
         if constexpr (sizeof(Real) == 4) {
-            if (t4) {
+            if (t4 && tled_) {
+                using BS = BoxShape<kBoxBX, kBoxBY>;
+                const size_t smem = BS::template smem_bytes<Real, false, true>();
+                setup(k_box_step<Real, DJG_NH, kBoxBX, kBoxBY, false, true>, smem, BS::kThreads);
+                setup(k_box_step<Real, DJG_TI, kBoxBX, kBoxBY, false, true>, smem, BS::kThreads);
+                setup(k_box_step<Real, DJG_OT, kBoxBX, kBoxBY, false, true>, smem, BS::kThreads);
+                setup(k_box_step<Real, DJG_NH, kBoxBX, kBoxBY, true, true>, smem, BS::kThreads);
+                setup(k_box_step<Real, DJG_TI, kBoxBX, kBoxBY, true, true>, smem, BS::kThreads);
+                setup(k_box_step<Real, DJG_OT, kBoxBX, kBoxBY, true, true>, smem, BS::kThreads);
+            } else if (t4) {
                 using BS = BoxShape<kBoxBX, kBoxBY>;
                 const size_t smem = BS::template smem_bytes<Real>(), lsmem = BS::template smem_bytes<Real, true>();
                 setup(k_box_step<Real, DJG_NH, kBoxBX, kBoxBY, false>, smem, BS::kThreads);
@@ -641,7 +653,22 @@ public:
             if (kind_ == DJG_T4) {
                 using BS = BoxShape<kBoxBX, kBoxBY>;
                 auto go = [&](auto kern, size_t smem) { kern<<<grid, BS::kThreads, smem, s>>>(ea_, na_, box_); };
-                if (lattice_) {
+                if (tled_) {
+                    const size_t smem = BS::template smem_bytes<Real, false, true>();
+                    if (lattice_) {
+                        switch (model_) {
+                            case DJG_NH: go(k_box_step<Real, DJG_NH, kBoxBX, kBoxBY, true, true>, smem); break;
+                            case DJG_TI: go(k_box_step<Real, DJG_TI, kBoxBX, kBoxBY, true, true>, smem); break;
+                            default: go(k_box_step<Real, DJG_OT, kBoxBX, kBoxBY, true, true>, smem); break;
+                        }
+                    } else {
+                        switch (model_) {
+                            case DJG_NH: go(k_box_step<Real, DJG_NH, kBoxBX, kBoxBY, false, true>, smem); break;
+                            case DJG_TI: go(k_box_step<Real, DJG_TI, kBoxBX, kBoxBY, false, true>, smem); break;
+                            default: go(k_box_step<Real, DJG_OT, kBoxBX, kBoxBY, false, true>, smem); break;
+                        }
+                    }
+                } else if (lattice_) {
                     const size_t smem = BS::template smem_bytes<Real, true>();
                     switch (model_) {
                         case DJG_NH: go(k_box_step<Real, DJG_NH, kBoxBX, kBoxBY, true>, smem); break;
@@ -720,6 +747,7 @@ public:
                 case DJG_TI: nq = kLatQuads<DJG_TI>; break;
                 default: nq = kLatQuads<DJG_OT>; break;
             }
+            if (tled_) nq = (TledLayout<0>::count + 3) / 4;
             const size_t bytes = size_t(ncomb) * 6 * nq * sizeof(float4);
             if (bytes > (size_t(16) << 20)) return;  // an irregular box: too many classes
             lcls_.alloc(cls.size() * sizeof(int32_t));
@@ -744,10 +772,16 @@ public:
                 table<<<tb, 128>>>(ea_, b, drep.as<int32_t>(), lat_.as<float4>());
                 verify<<<vb, 256>>>(ea_, b, lat_.as<float4>(), bad.as<unsigned long long>());
             };
-            switch (model_) {
-                case DJG_NH: run(k_lattice_table<Real, DJG_NH>, k_lattice_verify<Real, DJG_NH>); break;
-                case DJG_TI: run(k_lattice_table<Real, DJG_TI>, k_lattice_verify<Real, DJG_TI>); break;
-                default: run(k_lattice_table<Real, DJG_OT>, k_lattice_verify<Real, DJG_OT>); break;
+            if (tled_) {
+                // TLED: the records exist already (B0 / V0 planes): copy a
+                // representative's, compare every tet's planes
+                run(k_lattice_table_rec<Real>, k_lattice_verify_rec<Real>);
+            } else {
+                switch (model_) {
+                    case DJG_NH: run(k_lattice_table<Real, DJG_NH>, k_lattice_verify<Real, DJG_NH>); break;
+                    case DJG_TI: run(k_lattice_table<Real, DJG_TI>, k_lattice_verify<Real, DJG_TI>); break;
+                    default: run(k_lattice_table<Real, DJG_OT>, k_lattice_verify<Real, DJG_OT>); break;
+                }
             }
             CK(cudaGetLastError());
             unsigned long long nbad = 0;

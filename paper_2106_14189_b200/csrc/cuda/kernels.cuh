@@ -882,10 +882,10 @@ __device__ __forceinline__ void element_body_tled(const ElemArgs<Real>& A, const
     // deformation_state (tled_force.hpp:39-48)
     const Real J = em::det3(X);
     if (!(J > Real(0))) {
-        if (!A.counted || A.counted[e]) atomicAdd(&A.ctrl->inv_count, 1ull);
+        if (counts_inversion(A, src, e)) atomicAdd(&A.ctrl->inv_count, 1ull);
         atomicMin(&A.ctrl->first_inv, (unsigned long long)(A.elem_l2g ? A.elem_l2g[e] : e));
 #pragma unroll
-        for (int a = 0; a < NPE; ++a) store_row(A, sl[a], Real(0), Real(0), Real(0));
+        for (int a = 0; a < NPE; ++a) emit_row(A, src, sl[a], Real(0), Real(0), Real(0));
         return;
     }
     Real m[3][3];
@@ -990,7 +990,7 @@ __device__ __forceinline__ void element_body_tled(const ElemArgs<Real>& A, const
         }
     }
 #pragma unroll
-    for (int a = 0; a < NPE; ++a) store_row(A, sl[a], f[a][0], f[a][1], f[a][2]);
+    for (int a = 0; a < NPE; ++a) emit_row(A, src, sl[a], f[a][0], f[a][1], f[a][2]);
 }
 
 template <class Real, int KIND, int MODEL, int RB>
@@ -1863,11 +1863,13 @@ __device__ __forceinline__ void lattice_j0(int t, const float (&d)[3], float* c)
         for (int j = 0; j < 3; ++j) c[3 * i + j] = ((cr[i] >> j) & 1) ? d[j] : 0.0f;
 }
 
-template <class Real, bool LAT = false>
+template <class Real, bool LAT = false, bool ROW0 = false>
 struct BoxSrc {
     using Node = typename RT<Real>::Node;
     static constexpr bool kRowSink = true;
     static constexpr bool kLattice = LAT;
+    const ElemArgs<Real>* ea;  // TLED: the record planes (A.c) when not on the lattice
+    long long e;               // TLED: this tet's element id
     const Node* su;    // stage u (all ring slots)
     const Node* sx;    // stage X (LAT: unused)
     const float4* lrec;  // LAT: this tet's record fields 9..
@@ -1892,29 +1894,44 @@ struct BoxSrc {
     __device__ __forceinline__ int4 conn(int) const { return make_int4(h[0], h[1], h[2], h[3]); }
     __device__ __forceinline__ Node node(int, const Node* __restrict__, int k) const { return su[k]; }
     __device__ __forceinline__ Node coord(const ElemArgs<Real>&, int k) const { return sx[k]; }
-    __device__ __forceinline__ typename RT<Real>::Plane plane(int) const { return typename RT<Real>::Plane{}; }
+    // TLED (ROW0): the tet's B0 / V0 record -- the lattice table's entry or
+    // the precomputed planes in HBM
+    __device__ __forceinline__ typename RT<Real>::Plane plane(int p) const {
+        if constexpr (ROW0) {
+            if constexpr (LAT) return __ldg(reinterpret_cast<const typename RT<Real>::Plane*>(lrec) + p);
+            else return RT<Real>::load_plane(ea->c + (long long)p * ea->E + e);
+        } else {
+            return typename RT<Real>::Plane{};
+        }
+    }
     __device__ __forceinline__ Real tail(int) const { return Real(0); }
     template <int N, int RB>
     __device__ __forceinline__ void ranks(int (&rk)[N]) const {
 #pragma unroll
         for (int a = 0; a < N; ++a) rk[a] = 0;
     }
-    int ntet;          // tets per footprint layer: 9 planes [column j][xyz][tet] of K
+    int ntet;          // tets per footprint layer: 9 planes [column j][xyz][tet] of K (ROW0: 12, rows 0..3)
     __device__ __forceinline__ int slot(const int* __restrict__, int a, int, int) const { return row0 + a; }
     // T4 rows 1..3 are the columns of K (element_body); row 0 is not kept --
     // the fold recomputes it from the columns with the same operations.
     __device__ __forceinline__ void store(int pos, Real x, Real y, Real z) const {
         const int tet = pos >> 2, a = pos & 3;
-        if (a == 0) return;
-        rows[(3 * (a - 1) + 0) * ntet + tet] = x;  // consecutive tets -> consecutive words: no bank conflicts
-        rows[(3 * (a - 1) + 1) * ntet + tet] = y;
-        rows[(3 * (a - 1) + 2) * ntet + tet] = z;
+        if constexpr (ROW0) {
+            rows[(3 * a + 0) * ntet + tet] = x;
+            rows[(3 * a + 1) * ntet + tet] = y;
+            rows[(3 * a + 2) * ntet + tet] = z;
+        } else {
+            if (a == 0) return;
+            rows[(3 * (a - 1) + 0) * ntet + tet] = x;  // consecutive tets -> consecutive words: no bank conflicts
+            rows[(3 * (a - 1) + 1) * ntet + tet] = y;
+            rows[(3 * (a - 1) + 2) * ntet + tet] = z;
+        }
     }
 };
 
 // The Kuhn tets of a cell holding corner C, as (tet, local node) in
 // ascending tet order (the inverse of kTetCorner), at compile time.
-template <int C, int NCELL>
+template <int C, int NCELL, bool ROW0 = false>
 __device__ __forceinline__ void corner_rows(const float* __restrict__ rows, int ntet, int c, float& fx, float& fy,
                                             float& fz) {
     constexpr int n = (C == 0 || C == 7) ? 6 : 2;
@@ -1923,7 +1940,11 @@ __device__ __forceinline__ void corner_rows(const float* __restrict__ rows, int 
 #pragma unroll
     for (int m = 0; m < n; ++m) {
         const int tet = T0[C][m] * NCELL + c, a = A0[C][m];
-        if (a == 0) {  // f0 = -(f1 + f2 + f3), element_body's expression (djtled_force.hpp:73-77)
+        if constexpr (ROW0) {  // TLED: all four rows kept
+            fx += rows[(3 * a + 0) * ntet + tet];
+            fy += rows[(3 * a + 1) * ntet + tet];
+            fz += rows[(3 * a + 2) * ntet + tet];
+        } else if (a == 0) {  // f0 = -(f1 + f2 + f3), element_body's expression (djtled_force.hpp:73-77)
             const float* k = rows + tet;
             fx += -1.0f * ((k[0 * ntet] + k[3 * ntet]) + k[6 * ntet]);
             fy += -1.0f * ((k[1 * ntet] + k[4 * ntet]) + k[7 * ntet]);
@@ -1941,13 +1962,16 @@ struct BoxShape {
     static constexpr int SX = BX + 2, SY = BY + 2;  // stage nodes per layer (footprint + 1 halo node each side)
     static constexpr int CX = BX + 1, CY = BY + 1;  // footprint cells per layer
     static constexpr int kStageNodes = SX * SY;
-    static constexpr size_t kRowFloats = size_t(CX) * CY * 6 * 9;  // K per tet
+    static constexpr size_t kRowFloats = size_t(CX) * CY * 6 * 9;  // K per tet (TLED: 12, rows 0..3)
     // one thread per footprint cell (its six tets in turn: every thread the
     // same work per layer), the first BX * BY of them also one owned node each
     static constexpr int kThreads = (CX * CY + 31) / 32 * 32;
-    template <class Real, bool LAT = false>
+    // the ring holds u, and X unless the records come from the lattice table
+    // or the TLED planes
+    template <class Real, bool LAT = false, bool TLED = false>
     static constexpr size_t smem_bytes() {
-        return (LAT ? 1 : 2) * 3 * size_t(kStageNodes) * sizeof(typename RT<Real>::Node) + kRowFloats * sizeof(float);
+        return (LAT || TLED ? 1 : 2) * 3 * size_t(kStageNodes) * sizeof(typename RT<Real>::Node) +
+               kRowFloats / 9 * (TLED ? 12 : 9) * sizeof(float);
     }
 };
 
@@ -1959,7 +1983,7 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
 }
 
-template <class Real, int MODEL, int BX, int BY, bool LAT>
+template <class Real, int MODEL, int BX, int BY, bool LAT, bool TLED = false>
 __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_box_step(const ElemArgs<Real> A, const NodeArgs<Real> NA,
                                                           const BoxArgs B) {
     static_assert(sizeof(Real) == 4, "the fused box step keeps float rows");
@@ -1970,8 +1994,9 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
     extern __shared__ __align__(128) unsigned char smem[];
     Node* su = reinterpret_cast<Node*>(smem);
     Node* sx = su + 3 * BS::kStageNodes;
-    float* rows = reinterpret_cast<float*>(su + (LAT ? 1 : 2) * 3 * BS::kStageNodes);
-    constexpr int NQ = kLatQuads<MODEL>;
+    constexpr bool kXRing = !LAT && !TLED;  // coordinates staged (per-tet DJ record rebuild)
+    float* rows = reinterpret_cast<float*>(su + (kXRing ? 2 : 1) * 3 * BS::kStageNodes);
+    constexpr int NQ = TLED ? (TledLayout<0>::count + 3) / 4 : kLatQuads<MODEL>;
     __shared__ int s_nonfinite;
     Ctrl* ctrl = A.ctrl;
     if (*(volatile const int*)&ctrl->halted) return;
@@ -1994,7 +2019,7 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
             if (gi < 0 || gi > nx || gj < 0 || gj > ny) continue;
             const long long n = gid(gi, gj, k);
             cp_async16(su + slot * BS::kStageNodes + q, ucur + n);
-            if constexpr (!LAT) cp_async16(sx + slot * BS::kStageNodes + q, A.X + n);
+            if constexpr (kXRing) cp_async16(sx + slot * BS::kStageNodes + q, A.X + n);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -2010,16 +2035,16 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
     // cell's tets in order
     constexpr int NCELL = BS::CX * BS::CY, NTET = NCELL * 6;  // rows: tet t of footprint cell c is t * NCELL + c
     auto fold_below = [&](Real& fx, Real& fy, Real& fz) {  // node at the top (dz = 1) of the cells
-        if (hy0 && hx0) corner_rows<7, NCELL>(rows, NTET, cb, fx, fy, fz);
-        if (hy0 && hx1) corner_rows<6, NCELL>(rows, NTET, cb + 1, fx, fy, fz);
-        if (hy1 && hx0) corner_rows<5, NCELL>(rows, NTET, cb + BS::CX, fx, fy, fz);
-        if (hy1 && hx1) corner_rows<4, NCELL>(rows, NTET, cb + BS::CX + 1, fx, fy, fz);
+        if (hy0 && hx0) corner_rows<7, NCELL, TLED>(rows, NTET, cb, fx, fy, fz);
+        if (hy0 && hx1) corner_rows<6, NCELL, TLED>(rows, NTET, cb + 1, fx, fy, fz);
+        if (hy1 && hx0) corner_rows<5, NCELL, TLED>(rows, NTET, cb + BS::CX, fx, fy, fz);
+        if (hy1 && hx1) corner_rows<4, NCELL, TLED>(rows, NTET, cb + BS::CX + 1, fx, fy, fz);
     };
     auto fold_above = [&](Real& fx, Real& fy, Real& fz) {  // node at the bottom (dz = 0)
-        if (hy0 && hx0) corner_rows<3, NCELL>(rows, NTET, cb, fx, fy, fz);
-        if (hy0 && hx1) corner_rows<2, NCELL>(rows, NTET, cb + 1, fx, fy, fz);
-        if (hy1 && hx0) corner_rows<1, NCELL>(rows, NTET, cb + BS::CX, fx, fy, fz);
-        if (hy1 && hx1) corner_rows<0, NCELL>(rows, NTET, cb + BS::CX + 1, fx, fy, fz);
+        if (hy0 && hx0) corner_rows<3, NCELL, TLED>(rows, NTET, cb, fx, fy, fz);
+        if (hy0 && hx1) corner_rows<2, NCELL, TLED>(rows, NTET, cb + 1, fx, fy, fz);
+        if (hy1 && hx0) corner_rows<1, NCELL, TLED>(rows, NTET, cb + BS::CX, fx, fy, fz);
+        if (hy1 && hx1) corner_rows<0, NCELL, TLED>(rows, NTET, cb + BS::CX + 1, fx, fy, fz);
     };
     // the update's per-node operands, loaded a cell layer ahead of their use
     // (their HBM latency then overlaps the layer's tets, not the barrier)
@@ -2115,7 +2140,9 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
                 }
     #pragma unroll kBoxUnrollT
                 for (int t = 0; t < 6; ++t) {
-                    BoxSrc<Real, LAT> src;
+                    BoxSrc<Real, LAT, TLED> src;
+                    src.ea = &A;
+                    src.e = ebase + t;
                     src.su = su;
                     src.sx = sx;
                     src.lrec = LAT ? lcell + t * NQ : nullptr;
@@ -2132,7 +2159,8 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
                         const unsigned v = (pk >> (8 * a)) & 0xffu;
                         src.h[a] = ((v & 0x80u) ? hb1 : hb0) + int(v & 0x7fu);
                     }
-                    element_body<Real, 0, MODEL, 1, true>(A, ebase + t, nullptr, src);
+                    if constexpr (TLED) element_body_tled<Real, 0, MODEL, 1>(A, ebase + t, nullptr, src);
+                    else element_body<Real, 0, MODEL, 1, true>(A, ebase + t, nullptr, src);
                 }
             }
             __syncthreads();
@@ -2234,6 +2262,51 @@ __global__ void k_lattice_verify(const ElemArgs<Real> A, const BoxArgs B, const 
         for (int k = 0; k < 9; ++k) same = same && __float_as_uint(c[k]) == __float_as_uint(j0[k]);
 #pragma unroll
         for (int k = 9; k < NREC; ++k) same = same && __float_as_uint(c[k]) == __float_as_uint(want[k - 9]);
+        mism += same ? 0 : 1;
+    }
+    if (mism) atomicAdd(bad, mism);
+}
+
+// TLED on a lattice: the B0 / V0 record of tet t of a representative cell
+// per class triple, copied from the precomputed planes (A.c); then every
+// tet's planes against its class's entry, bit for bit.
+template <class Real>
+__global__ void k_lattice_table_rec(const ElemArgs<Real> A, const BoxArgs B, const int* __restrict__ rep,
+                                    float4* __restrict__ lat) {
+    constexpr int NQ = (TledLayout<0>::count + 3) / 4;
+    const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (q >= (long long)B.lncx * B.lncy * B.lncz * 6) return;
+    const int t = int(q % 6);
+    const long long comb = q / 6;
+    const int cx = int(comb % B.lncx), cy = int(comb / B.lncx % B.lncy), cz = int(comb / B.lncx / B.lncy);
+    const long long e =
+        (rep[cx] + (long long)B.nx * (rep[B.lncx + cy] + (long long)B.ny * rep[B.lncx + B.lncy + cz])) * 6 + t;
+#pragma unroll
+    for (int p = 0; p < NQ; ++p) lat[q * NQ + p] = A.c[(long long)p * A.E + e];
+}
+
+template <class Real>
+__global__ void k_lattice_verify_rec(const ElemArgs<Real> A, const BoxArgs B, const float4* __restrict__ lat,
+                                     unsigned long long* bad) {
+    constexpr int NQ = (TledLayout<0>::count + 3) / 4, NREC = TledLayout<0>::count;
+    const long long ncell = (long long)B.nx * B.ny * B.nz;
+    unsigned long long mism = 0;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < ncell * 6;
+         e += (long long)gridDim.x * blockDim.x) {
+        const int t = int(e % 6);
+        const long long cell = e / 6;
+        const int ci = int(cell % B.nx), cj = int(cell / B.nx % B.ny), ck = int(cell / B.nx / B.ny);
+        const long long comb =
+            ((long long)B.lcls[B.nx + B.ny + ck] * B.lncy + B.lcls[B.nx + cj]) * B.lncx + B.lcls[ci];
+        bool same = true;
+#pragma unroll
+        for (int p = 0; p < NQ; ++p) {
+            const float4 g = A.c[(long long)p * A.E + e], w = lat[(comb * 6 + t) * NQ + p];
+            const float gv[4] = {g.x, g.y, g.z, g.w}, wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (4 * p + k < NREC) same = same && __float_as_uint(gv[k]) == __float_as_uint(wv[k]);
+        }
         mism += same ? 0 : 1;
     }
     if (mism) atomicAdd(bad, mism);

@@ -70,3 +70,56 @@ def test_tled_inversion_semantics():
         ur, upr, rr = oracle.run(spec, 100, "ref", engine=1)
         assert (rep.first_inverted, rep.fail_step) == (rr["first_inverted"], rr["fail_step"])
         assert np.array_equal(u, ur)
+
+
+def _moved_box(d, model):
+    """A generated T4 box with one interior node moved off the coordinate
+    lattice (the fused step then streams the B0 / V0 planes)."""
+    from paper_2106_14189_b200 import mesh_spec
+    img = Scenario(box_spec(kind="T4", divisions=d, precision=4)).image()
+    x = img["nodes"].reshape(-1, 3).astype(np.float64)
+    x[3 + (d[0] + 1) * (2 + (d[1] + 1) * 3), 0] += 0.013
+    z = x[:, 2]
+    bottom, top = np.flatnonzero(z == z.min()), np.flatnonzero(z == z.max())
+    return mesh_spec(x, img["conn"].reshape(-1, 4), kind="T4", model=model, precision=4,
+                     fixed=[(int(n), a) for n in bottom for a in range(3)],
+                     prescribed=[(int(n), 2, -0.04, 1e-3) for n in top])
+
+
+@pytest.mark.parametrize("model", ["NH", "TI", "OT"])
+@pytest.mark.parametrize("d", [(5, 4, 6), (17, 9, 33), "moved"])
+def test_tled_fused_box_step(model, d):
+    """TLED in the fused box step (k_box_step<..., TLED>): all four rows of a
+    tet kept in shared memory, the record from the lattice table (generated
+    box) or streamed from the B0 / V0 planes (a node off the lattice) --
+    bit-identical to the two-kernel TLED step and to the reference's
+    TledEngine."""
+    spec = _moved_box((6, 5, 7), model) if d == "moved" else \
+        box_spec(kind="T4", model=model, divisions=d, precision=4, ramp_steps=200)
+    u, up, rep, info = run(spec, 200, A.DJG_FLAG_TLED | A.DJG_FLAG_FUSED)
+    assert info["fused"] == 1 and info["formulation"] == 1 and info["lattice"] == (d != "moved"), info
+    u2, up2, rep2, info2 = run(spec, 200, A.DJG_FLAG_TLED | A.DJG_FLAG_NO_FUSED)
+    assert info2["fused"] == 0
+    assert rep.status == rep2.status == 0 and rep.step == rep2.step
+    assert np.array_equal(u, u2) and np.array_equal(up, up2)
+    if oracle.have("ref"):
+        ur, upr, rr = oracle.run(spec, 200, "ref", engine=1)
+        assert np.array_equal(u, ur) and np.array_equal(up, upr)
+    assert np.abs(u).max() > 0
+
+
+@pytest.mark.parametrize("policy", [A.DJG_ABORT, A.DJG_SKIP_AND_REPORT])
+def test_tled_fused_inversion(policy):
+    """TLED fused under a crushing load: same halt / counts / state as the
+    two-kernel TLED step."""
+    spec = box_spec(kind="T4", divisions=(9, 7, 8), extent=(0.1, 0.1, 0.1), precision=4, target=-0.09,
+                    ramp_steps=3, fix_all_axes=True, policy=policy)
+    outs = []
+    for flags in (A.DJG_FLAG_FUSED, A.DJG_FLAG_NO_FUSED):
+        u, up, r, info = run(spec, 60, A.DJG_FLAG_TLED | flags)
+        outs.append((r, u, up))
+    (r1, u1, up1), (r2, u2, up2) = outs
+    assert (r1.status, r1.step, r1.first_inverted, r1.inverted_count, r1.inverted_steps) == \
+        (r2.status, r2.step, r2.first_inverted, r2.inverted_count, r2.inverted_steps), (r1, r2)
+    assert r1.inverted_count > 0
+    assert np.array_equal(u1, u2) and np.array_equal(up1, up2)

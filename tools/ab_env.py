@@ -1,7 +1,7 @@
 """Developer A/B: graph-replay step time and per-kernel split of the default
 engine under environment variants ("NAME=VALUE[,NAME=VALUE]" or "" for
 none), one process per variant, interleaved twice. Optional --lib PATH
-selects a library variant for all runs.  usage: ab_env.py cfg5 "" "DJG_X=0" ..."""
+selects a library variant for all runs; AB_FLAGS=<int> sets the engine flags.  usage: ab_env.py cfg5 "" "DJG_X=0" ..."""
 import json
 import os
 import subprocess
@@ -13,8 +13,9 @@ code = r'''
 import json, sys, torch
 sys.path.insert(0, ".")
 from paper_2106_14189_b200 import GpuDjEngine, Scenario, config_spec
+import os
 sc = Scenario(config_spec(sys.argv[1], precision=int(sys.argv[3]), target=0.01, ramp_steps=100000))
-with GpuDjEngine(sc) as eng:
+with GpuDjEngine(sc, flags=int(os.environ.get("AB_FLAGS", "0"))) as eng:
     info = eng.info()
     eng.step(10)
     s = torch.cuda.ExternalStream(eng.stream)

@@ -506,11 +506,17 @@ def our_arm(args):
     extra = {
         "e2e": {"value": E / (e2e_ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 2 * 3 * N * rbytes,
                 "d2h_bytes_per_step": 3 * N * rbytes, "ms_per_step": e2e_ms,
-                "mode": "per step: djg_advance_host -- advance_step with a host SimState: H2D u_curr and "
-                        "u_prev from pinned host (u_curr in 8 chunks, each element chunk starting once the node "
-                        "prefix it reads has landed; u_prev in 4 tapered chunks gating the node-update chunks), one "
-                        "step, D2H the new u_curr chunk by chunk on the other copy direction; the next u_prev "
-                        "is the host's previous u_curr; wall clock"} if args.e2e_steps > 0 else None,
+                "mode": ("per step: djg_advance_host -- advance_step with a host SimState: H2D u_curr and "
+                         "u_prev from pinned host, region by region (8 tapered runs of node layers; u_curr and "
+                         "u_prev on two copy streams), the fused box step launched on each region's layers as "
+                         "soon as they have landed, each region's new u_curr D2H on the other copy direction "
+                         "behind the next region; the next u_prev is the host's previous u_curr; wall clock"
+                         if fused else
+                         "per step: djg_advance_host -- advance_step with a host SimState: H2D u_curr and "
+                         "u_prev from pinned host (u_curr in 8 chunks, each element chunk starting once the node "
+                         "prefix it reads has landed; u_prev in 4 tapered chunks gating the node-update chunks), one "
+                         "step, D2H the new u_curr chunk by chunk on the other copy direction; the next u_prev "
+                         "is the host's previous u_curr; wall clock")} if args.e2e_steps > 0 else None,
         "e2e_run": {"value": E / (run_ms * 1e-3), "unit": UNIT, "steps": K, "ms_per_step": run_ms,
                     "h2d_bytes": 2 * 3 * N * rbytes, "d2h_bytes": 2 * 3 * N * rbytes,
                     "mode": "run_simulation path: djg_set_state (host SimState up once), djg_step(K) on the "

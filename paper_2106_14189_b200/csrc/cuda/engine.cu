@@ -603,6 +603,9 @@ public:
         box_.nz = int(nz);
         box_.tiles_x = int((nx + 1 + kBoxBX - 1) / kBoxBX);
         box_.tiles_y = int((ny + 1 + kBoxBY - 1) / kBoxBY);
+        box_.lay0 = 0;
+        box_.lay1 = int(nz + 1);
+        box_.close = 1;
         int per_sm = 0;
         auto setup = [&](auto kern, size_t smem, int threads) {
             CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
@@ -647,12 +650,23 @@ public:
         return true;
     }
 
-    void launch_box(cudaStream_t s) {
+    void launch_box(cudaStream_t s) { launch_box(s, box_); }
+
+    // node layers [lay0, lay1) only; the last such launch of a step closes it
+    void launch_box(cudaStream_t s, int lay0, int lay1, bool close) {
+        BoxArgs b = box_;
+        b.lay0 = lay0;
+        b.lay1 = lay1;
+        b.close = close ? 1 : 0;
+        launch_box(s, b);
+    }
+
+    void launch_box(cudaStream_t s, const BoxArgs& box) {
         if constexpr (sizeof(Real) == 4) {
             const unsigned grid = unsigned(box_grid_);
             if (kind_ == DJG_T4) {
                 using BS = BoxShape<kBoxBX, kBoxBY>;
-                auto go = [&](auto kern, size_t smem) { kern<<<grid, BS::kThreads, smem, s>>>(ea_, na_, box_); };
+                auto go = [&](auto kern, size_t smem) { kern<<<grid, BS::kThreads, smem, s>>>(ea_, na_, box); };
                 if (tled_) {
                     const size_t smem = BS::template smem_bytes<Real, false, true>();
                     if (lattice_) {
@@ -687,9 +701,9 @@ public:
                 using BS = BoxShapeH8<kBoxBX, kBoxBY>;
                 const size_t smem = BS::template smem_bytes<Real>();
                 switch (model_) {
-                    case DJG_NH: k_box_step_h8<Real, DJG_NH, kBoxBX, kBoxBY><<<grid, BS::kThreads, smem, s>>>(ea_, na_, box_); break;
-                    case DJG_TI: k_box_step_h8<Real, DJG_TI, kBoxBX, kBoxBY><<<grid, BS::kThreads, smem, s>>>(ea_, na_, box_); break;
-                    default: k_box_step_h8<Real, DJG_OT, kBoxBX, kBoxBY><<<grid, BS::kThreads, smem, s>>>(ea_, na_, box_); break;
+                    case DJG_NH: k_box_step_h8<Real, DJG_NH, kBoxBX, kBoxBY><<<grid, BS::kThreads, smem, s>>>(ea_, na_, box); break;
+                    case DJG_TI: k_box_step_h8<Real, DJG_TI, kBoxBX, kBoxBY><<<grid, BS::kThreads, smem, s>>>(ea_, na_, box); break;
+                    default: k_box_step_h8<Real, DJG_OT, kBoxBX, kBoxBY><<<grid, BS::kThreads, smem, s>>>(ea_, na_, box); break;
                 }
             }
             CK(cudaGetLastError());
@@ -1438,8 +1452,10 @@ public:
         if (evPrev_) cudaEventDestroy(evPrev_);
         if (down_) cudaStreamDestroy(down_);
         for (auto e : evChunk_) cudaEventDestroy(e);
+        for (auto e : evBox_) cudaEventDestroy(e);
         if (evJoin_) cudaEventDestroy(evJoin_);
         if (side_) cudaStreamDestroy(side_);
+        if (side2_) cudaStreamDestroy(side2_);
         if (graph_big_) cudaGraphExecDestroy(graph_big_);
         if (graph_one_) cudaGraphExecDestroy(graph_one_);
         if (hctrl_) cudaFreeHost(hctrl_);
@@ -1509,6 +1525,8 @@ public:
         if (!u || !up || !u_next) throw DescError("djg_advance_host needs u_curr, u_prev and u_next");
         if (step < 0) throw DescError("step must be >= 0");
         if (n_slabs_ != 1 || comm_ || peer_) throw DescError("djg_advance_host: single-part, one-slab engines");
+        if (fused_now() && !(std::getenv("DJG_HOST_TWO_KERNEL") && std::atoi(std::getenv("DJG_HOST_TWO_KERNEL"))))
+            return advance_host_box(u, up, step, u_next, rep);
         const int64_t S = (N_ + 31) / 32;
         const bool chunked = S >= 4 * 256;
         const int nu = chunked ? kUpChunks : 1, ne = chunked ? kUpChunks : 1, nc = chunked ? kHostChunks : 1;
@@ -1644,6 +1662,124 @@ public:
             CK(cudaMemcpyAsync(static_cast<Real*>(u_next) + 3 * n0, flat_.as<Real>() + 3 * n0,
                                size_t(3 * (n1 - n0)) * sizeof(Real), cudaMemcpyDeviceToHost, down_));
             mark("down " + std::to_string(c), down_);
+        }
+        CK(cudaEventRecord(evDone, down_));
+        CK(cudaStreamWaitEvent(stream_, evDone, 0));
+        CK(cudaGetLastError());
+        const int status = sync(rep);
+        if (trace) {
+            for (auto& [what, e] : tl) {
+                float ms = 0;
+                CK(cudaEventElapsedTime(&ms, tl.front().second, e));
+                std::fprintf(stderr, "[djg host step] %8.3f ms  %s\n", ms, what.c_str());
+            }
+            for (auto& te : tl) cudaEventDestroy(te.second);
+        }
+        if (status != DJG_OK) {  // the state did not advance: hand back u_curr
+            download_nodes(u_[ph].as<Node>(), u_next);
+            CK(cudaStreamSynchronize(stream_));
+        }
+        return status;
+    }
+
+    // advance_host on the fused box step: the box is cut into kBoxRegions
+    // runs of node layers (lexicographic ids: contiguous node ranges). Region
+    // r's uploads -- u_curr through the first layer above it (its top cell
+    // layer reads it), then its own u_prev -- go up one copy stream in
+    // region order; k_box_step updates region r's layers as soon as they
+    // have landed (the last region's launch closes the step) and region r's
+    // u_next goes back on the other copy direction while region r + 1
+    // uploads. The regions taper so that little is left to compute and read
+    // back after the last upload.
+    static constexpr int kBoxRegions = 8;
+    int advance_host_box(const void* u, const void* up, int64_t step, void* u_next, djg_report* rep) {
+        const int64_t plane = int64_t(box_.nx + 1) * (box_.ny + 1), L = box_.nz + 1;
+        const bool chunked = L >= 4 * kBoxRegions && N_ >= (int64_t(1) << 16);
+        const int R = chunked ? kBoxRegions : 1;
+        if (!side_) CK(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
+        if (!side2_) CK(cudaStreamCreateWithFlags(&side2_, cudaStreamNonBlocking));
+        if (!down_) CK(cudaStreamCreateWithFlags(&down_, cudaStreamNonBlocking));
+        if (!flat2_.p) flat2_.alloc(flat_.bytes);
+        if (evBox_.empty()) {
+            evBox_.resize(size_t(3 * kBoxRegions + 2));
+            for (auto& e : evBox_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        }
+        cudaEvent_t* evUp = evBox_.data();         // region r's u_curr rows landed
+        cudaEvent_t* evUpP = evUp + kBoxRegions;  // region r's u_prev rows landed
+        cudaEvent_t* evNew = evUpP + kBoxRegions; // region r's u_next unpacked
+        cudaEvent_t evStart = evNew[kBoxRegions], evDone = evNew[kBoxRegions + 1];
+        {
+            Ctrl c{};
+            c.epoch = ctrl_initialized_ ? hctrl_->epoch : 0u;
+            c.multipart = multipart_ ? 1 : 0;
+            c.step = step;
+            c.first_inv = kNone;
+            c.asm_first = kNone;
+            c.halt_first_inv = -1;
+            c.fail_step = -1;
+            *hctrl_ = c;
+            *hstart_ = c;
+            ctrl_initialized_ = true;
+            CK(cudaMemcpyAsync(ctrl_.p, hctrl_, sizeof(Ctrl), cudaMemcpyHostToDevice, stream_));
+        }
+        CK(cudaEventRecord(evStart, stream_));
+        CK(cudaStreamWaitEvent(side_, evStart, 0));
+        CK(cudaStreamWaitEvent(side2_, evStart, 0));
+        static const bool trace = std::getenv("DJG_TRACE_HOST") != nullptr;  // as advance_host
+        std::vector<std::pair<std::string, cudaEvent_t>> tl;
+        auto mark = [&](const std::string& what, cudaStream_t st) {
+            if (!trace) return;
+            cudaEvent_t e;
+            CK(cudaEventCreate(&e));
+            CK(cudaEventRecord(e, st));
+            tl.emplace_back(what, e);
+        };
+        mark("start", stream_);
+        const int ph = int(step % 3);
+        Node* ucur = u_[ph].as<Node>();
+        Node* uprv = u_[(ph + 2) % 3].as<Node>();
+        const Node* unew = u_[(ph + 1) % 3].as<Node>();
+        // region boundaries in node layers (percent of the layers, tapered)
+        static const int w8[kBoxRegions + 1] = {0, 15, 30, 45, 60, 73, 84, 93, 100};
+        auto lay = [&](int r) -> int64_t { return R == 1 ? (r ? L : 0) : L * w8[r] / 100; };
+        // u_curr and u_prev go up on two streams (a copy stream alone moved
+        // ~40 GB/s in tools/pcie_probe.py, two at once ~55 GB/s; in the step
+        // they reach ~48 GB/s together: cfg5 4.78 -> 4.51 ms per host-state
+        // step; splitting each array over both streams was slower)
+        auto upload = [&](const void* host, Real* stage, Node* dst, int64_t n0, int64_t n1, cudaStream_t st) {
+            if (n1 <= n0) return;
+            CK(cudaMemcpyAsync(stage + 3 * n0, static_cast<const Real*>(host) + 3 * n0,
+                               size_t(3 * (n1 - n0)) * sizeof(Real), cudaMemcpyHostToDevice, st));
+            k_pack_nodes<Real><<<unsigned(std::max<int64_t>(1, (n1 - n0 + 255) / 256)), 256, 0, st>>>(
+                stage + 3 * n0, n1 - n0, dst + n0);
+        };
+        int64_t cur_done = 0;  // u_curr nodes uploaded so far
+        for (int r = 0; r < R; ++r) {
+            const int64_t n0 = lay(r) * plane, n1 = lay(r + 1) * plane;
+            const int64_t c1 = std::min(N_, (lay(r + 1) + 1) * plane);  // through the layer above
+            upload(u, flat_.as<Real>(), ucur, cur_done, c1, side_);
+            cur_done = std::max(cur_done, c1);
+            upload(up, flat2_.as<Real>(), uprv, n0, n1, side2_);
+            CK(cudaEventRecord(evUp[r], side_));
+            CK(cudaEventRecord(evUpP[r], side2_));
+            mark("up u_curr region " + std::to_string(r), side_);
+            mark("up u_prev region " + std::to_string(r), side2_);
+        }
+        CK(cudaGetLastError());
+        for (int r = 0; r < R; ++r) {
+            const int64_t n0 = lay(r) * plane, n1 = lay(r + 1) * plane;
+            CK(cudaStreamWaitEvent(stream_, evUp[r], 0));
+            CK(cudaStreamWaitEvent(stream_, evUpP[r], 0));
+            launch_box(stream_, int(lay(r)), int(lay(r + 1)), r == R - 1);
+            mark("box region " + std::to_string(r), stream_);
+            // region r's result into the u_curr staging rows it no longer needs
+            k_unpack_nodes<Real><<<unsigned(std::max<int64_t>(1, (n1 - n0 + 255) / 256)), 256, 0, stream_>>>(
+                unew + n0, n1 - n0, flat_.as<Real>() + 3 * n0);
+            CK(cudaEventRecord(evNew[r], stream_));
+            CK(cudaStreamWaitEvent(down_, evNew[r], 0));
+            CK(cudaMemcpyAsync(static_cast<Real*>(u_next) + 3 * n0, flat_.as<Real>() + 3 * n0,
+                               size_t(3 * (n1 - n0)) * sizeof(Real), cudaMemcpyDeviceToHost, down_));
+            mark("down region " + std::to_string(r), down_);
         }
         CK(cudaEventRecord(evDone, down_));
         CK(cudaStreamWaitEvent(stream_, evDone, 0));
@@ -2073,6 +2209,8 @@ private:
     bool peer_ = false;                // peer-memory multi-GPU step
     unsigned long long peer_timeout_ns_ = 10000000000ull;  // k_wait_agree's bound (DJG_PEER_TIMEOUT_MS)
     cudaEvent_t evPrev_ = nullptr;     // djg_advance_host: u_prev uploaded
+    std::vector<cudaEvent_t> evBox_;   // djg_advance_host on the fused box step
+    cudaStream_t side2_ = nullptr;     // djg_advance_host on the fused box step: u_prev uploads
     DevBuf flat2_, allSlices_;
     std::vector<cudaEvent_t> evChunk_;
     static constexpr int kHostChunks = DJG_HOST_CHUNKS;

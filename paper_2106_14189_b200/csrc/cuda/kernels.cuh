@@ -1794,6 +1794,9 @@ constexpr int kBoxUnrollT = DJG_BOX_UNROLL_T;
 struct BoxArgs {
     int nx, ny, nz;   // cells per axis
     int tiles_x, tiles_y;
+    // node layers [lay0, lay1) updated by this launch (the whole box: 0,
+    // nz + 1); close: the launch's last block closes the step
+    int lay0, lay1, close;
     // coordinate lattice (k_box_step<..., LAT = true>): record fields 9.. of
     // tet t of a cell with axis classes (cx, cy, cz) are lat[((cz * lncy + cy)
     // * lncx + cx) * 6 + t] (float4-padded); its J0 is made of the classes'
@@ -2087,12 +2090,12 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
     // layer, columns in order) are split evenly over the grid; a block walks
     // its range as one or two column pieces, each starting with one extra
     // cell layer below it (the partial sums of its first node layer).
-    const long long L = nz + 1, W = (long long)B.tiles_x * B.tiles_y * L;
+    const long long L = B.lay1 - B.lay0, W = (long long)B.tiles_x * B.tiles_y * L;
     const long long w_end = W * (blockIdx.x + 1) / gridDim.x;
     for (long long w = W * blockIdx.x / gridDim.x; w < w_end;) {
         const long long col = w / L;
-        k0 = int(w - col * L);
-        k1 = int(min(L, (long long)k0 + (w_end - w)));
+        k0 = B.lay0 + int(w - col * L);
+        k1 = int(min((long long)B.lay1, (long long)k0 + (w_end - w)));
         w += k1 - k0;
         i0 = int(col % B.tiles_x) * BX;
         j0 = int(col / B.tiles_x) * BY;
@@ -2188,7 +2191,7 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
     __threadfence();
     const unsigned int done = atomicAdd(&ctrl->blocks_done, 1u);
     if (done != gridDim.x - 1) return;
-    close_step<false>(ctrl, step, NA.policy);
+    if (B.close) close_step<false>(ctrl, step, NA.policy);
     __threadfence();
     ctrl->blocks_done = 0;
 }
@@ -2441,12 +2444,12 @@ __global__ void __launch_bounds__(BoxShapeH8<BX, BY>::kThreads, DJG_BOXH8_MINB)
     const int mcy = tid / BS::CX, mcx = tid - mcy * BS::CX;
     const bool my_count = mcx < BX && mcy < BY;
     const int mbase = mcy * BS::SX + mcx;
-    const long long L = nz + 1, W = (long long)B.tiles_x * B.tiles_y * L;
+    const long long L = B.lay1 - B.lay0, W = (long long)B.tiles_x * B.tiles_y * L;
     const long long w_end = W * (blockIdx.x + 1) / gridDim.x;
     for (long long w = W * blockIdx.x / gridDim.x; w < w_end;) {
         const long long col = w / L;
-        k0 = int(w - col * L);
-        k1 = int(min(L, (long long)k0 + (w_end - w)));
+        k0 = B.lay0 + int(w - col * L);
+        k1 = int(min((long long)B.lay1, (long long)k0 + (w_end - w)));
         w += k1 - k0;
         i0 = int(col % B.tiles_x) * BX;
         j0 = int(col / B.tiles_x) * BY;
@@ -2508,7 +2511,7 @@ __global__ void __launch_bounds__(BoxShapeH8<BX, BY>::kThreads, DJG_BOXH8_MINB)
     __threadfence();
     const unsigned int done = atomicAdd(&ctrl->blocks_done, 1u);
     if (done != gridDim.x - 1) return;
-    close_step<false>(ctrl, step, NA.policy);
+    if (B.close) close_step<false>(ctrl, step, NA.policy);
     __threadfence();
     ctrl->blocks_done = 0;
 }

@@ -771,6 +771,57 @@ def test_advance_host_chunked_readback():
     assert np.array_equal(u, u_ref) and np.array_equal(up, up_ref) and np.abs(u).max() > 0
 
 
+@pytest.mark.parametrize("kind,model,d", [("T4", "NH", (40, 41, 45)), ("T4", "TI", (12, 9, 33)), ("H8", "TI", (41, 40, 40)),
+                                           ("T4", "NH", (5, 4, 6))])
+@pytest.mark.parametrize("tled", [False, True])
+def test_advance_host_fused_regions(kind, model, d, tled):
+    """The host-state step on the fused box step (advance_host_box): region
+    by region (8 tapered runs of node layers when the box has >= 32 layers,
+    else one launch) -- uploads, partial k_box_step launches, read-back --
+    the same bits as the device-resident loop of the same engine and of the
+    two-kernel step; an Abort step hands back the state."""
+    if tled and kind == "H8":
+        pytest.skip("TLED fused step: T4 only")
+    flags = A.DJG_FLAG_FUSED | (A.DJG_FLAG_TLED if tled else 0)
+    spec = box_spec(kind=kind, model=model, divisions=d, precision=4, target=0.01, ramp_steps=25)
+    sc = Scenario(spec)
+    with GpuDjEngine(sc, flags=(A.DJG_FLAG_TLED if tled else 0) | A.DJG_FLAG_NO_FUSED) as ref:
+        ref.step(25)
+        u_ref, up_ref, _ = ref.get_state()
+    with GpuDjEngine(sc, flags=flags) as eng:
+        assert eng.info()["fused"] == 1
+        n3 = 3 * sc.num_nodes
+        u, up = np.zeros(n3, np.float32), np.zeros(n3, np.float32)
+        for st in range(25):
+            un, rep = eng.advance_host(u, up, st)
+            assert rep.status == 0 and rep.step == st + 1
+            u, up = un, u
+    assert np.array_equal(u, u_ref) and np.array_equal(up, up_ref) and np.abs(u).max() > 0
+
+
+def test_advance_host_fused_inversion():
+    """A crushing ramp through the fused host-state step: the same failing
+    step, status and counts as the device loop; the state handed back."""
+    spec = box_spec(kind="T4", divisions=(9, 7, 40), extent=(0.1, 0.1, 0.4), precision=4, target=-0.35,
+                    ramp_steps=3, fix_all_axes=True, policy=A.DJG_ABORT)
+    sc = Scenario(spec)
+    with GpuDjEngine(sc, flags=A.DJG_FLAG_FUSED) as ref:
+        rr = ref.step(60, raise_on_failure=False)
+    assert rr.status != 0
+    with GpuDjEngine(sc, flags=A.DJG_FLAG_FUSED) as eng:
+        n3 = 3 * sc.num_nodes
+        u, up = np.zeros(n3, np.float32), np.zeros(n3, np.float32)
+        for st in range(60):
+            un, rep = eng.advance_host(u, up, st)
+            if rep.status:
+                assert rep.status == rr.status and st == rr.step and rep.first_inverted == rr.first_inverted
+                assert np.array_equal(un, u)
+                break
+            u, up = un, u
+        else:
+            pytest.fail("no failing step")
+
+
 @pytest.mark.parametrize("kind,d", [("T4", 33), ("H8", 40)])
 def test_advance_host_chunked_permuted_nodes(kind, d):
     """Chunked host-state step on a mesh whose node ids are randomly permuted:

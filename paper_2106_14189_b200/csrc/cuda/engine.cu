@@ -569,7 +569,7 @@ public:
     bool detect_box(const int32_t* conn) {
         // DJ-TLED: f32 compact records (T4 rebuilt from X, H8 streamed);
         // TLED: T4, its B0 / V0 planes streamed or from the lattice table
-        if (sizeof(Real) != 4 || n_slabs_ != 1 || win_) return false;
+        if ((sizeof(Real) != 4 && kind_ != DJG_T4) || n_slabs_ != 1 || win_) return false;  // (f64: T4)
         if (tled_ ? kind_ != DJG_T4 : !compact_) return false;
         if (kind_ == DJG_T4 && !tled_ && !X_.p) return false;
         if (model_ != DJG_NH && model_ != DJG_TI && model_ != DJG_OT) return false;
@@ -613,7 +613,7 @@ public:
             CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem));
             per_sm = per_sm == 0 ? nb : std::min(per_sm, nb);
         };
-        if constexpr (sizeof(Real) == 4) {
+        {
             if (t4 && tled_) {
                 using BS = BoxShape<kBoxBX, kBoxBY>;
                 const size_t smem = BS::template smem_bytes<Real, false, true>();
@@ -636,7 +636,7 @@ public:
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(lsmem)));
                 CK(cudaFuncSetAttribute(k_box_step<Real, DJG_OT, kBoxBX, kBoxBY, true>,
                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(lsmem)));
-            } else {
+            } else if constexpr (sizeof(Real) == 4) {
                 using BS = BoxShapeH8<kBoxBX, kBoxBY>;
                 const size_t smem = BS::template smem_bytes<Real>();
                 setup(k_box_step_h8<Real, DJG_NH, kBoxBX, kBoxBY>, smem, BS::kThreads);
@@ -662,7 +662,7 @@ public:
     }
 
     void launch_box(cudaStream_t s, const BoxArgs& box) {
-        if constexpr (sizeof(Real) == 4) {
+        {
             const unsigned grid = unsigned(box_grid_);
             if (kind_ == DJG_T4) {
                 using BS = BoxShape<kBoxBX, kBoxBY>;
@@ -697,7 +697,7 @@ public:
                         default: go(k_box_step<Real, DJG_OT, kBoxBX, kBoxBY, false>, smem); break;
                     }
                 }
-            } else {
+            } else if constexpr (sizeof(Real) == 4) {
                 using BS = BoxShapeH8<kBoxBX, kBoxBY>;
                 const size_t smem = BS::template smem_bytes<Real>();
                 switch (model_) {
@@ -724,30 +724,30 @@ public:
     // per axis, 729 x 6 records (0.4 MB), against ~22 % of the step's
     // instructions. DJG_LATTICE=0 keeps the per-tet rebuild.
     void build_lattice(const Real* nodes) {
-        if constexpr (sizeof(Real) == 4) {
+        {
             const char* v = std::getenv("DJG_LATTICE");
             if (v && std::atoi(v) == 0) return;
             const int64_t nx = box_.nx, ny = box_.ny, nz = box_.nz;
             auto gid = [&](int64_t i, int64_t j, int64_t k) { return i + (nx + 1) * (j + (ny + 1) * k); };
             std::vector<int32_t> cls(size_t(nx + ny + nz)), rep;
-            std::vector<float> len;  // each class's interval length (0 + -a) + b
+            std::vector<Real> len;  // each class's interval length (0 + -a) + b
             int ncl[3] = {0, 0, 0};
             const int64_t n[3] = {nx, ny, nz};
             int64_t off = 0;
             for (int ax = 0; ax < 3; ++ax) {
-                std::map<std::pair<uint32_t, uint32_t>, int> ids;
+                std::map<std::pair<uint64_t, uint64_t>, int> ids;
                 for (int64_t i = 0; i < n[ax]; ++i) {
                     const int64_t g0 = ax == 0 ? gid(i, 0, 0) : ax == 1 ? gid(0, i, 0) : gid(0, 0, i);
                     const int64_t g1 = ax == 0 ? gid(i + 1, 0, 0) : ax == 1 ? gid(0, i + 1, 0) : gid(0, 0, i + 1);
                     const Real a = nodes[3 * g0 + ax], b = nodes[3 * g1 + ax];
                     const Real fwd = (Real(0) + -a) + b, bwd = (Real(0) + -b) + a;
-                    uint32_t kf, kb;
-                    std::memcpy(&kf, &fwd, 4);
-                    std::memcpy(&kb, &bwd, 4);
+                    uint64_t kf = 0, kb = 0;
+                    std::memcpy(&kf, &fwd, sizeof(Real));
+                    std::memcpy(&kb, &bwd, sizeof(Real));
                     const auto [it, fresh] = ids.emplace(std::make_pair(kf, kb), int(ids.size()));
                     if (fresh) {
                         rep.push_back(int32_t(i));  // the class's first cell index
-                        len.push_back(float(fwd));
+                        len.push_back(fwd);
                     }
                     cls[size_t(off + i)] = it->second;
                 }
@@ -757,16 +757,16 @@ public:
             const int64_t ncomb = int64_t(ncl[0]) * ncl[1] * ncl[2];
             int nq = 0;
             switch (model_) {
-                case DJG_NH: nq = kLatQuads<DJG_NH>; break;
-                case DJG_TI: nq = kLatQuads<DJG_TI>; break;
-                default: nq = kLatQuads<DJG_OT>; break;
+                case DJG_NH: nq = kLatPlanes<Real, DJG_NH>; break;
+                case DJG_TI: nq = kLatPlanes<Real, DJG_TI>; break;
+                default: nq = kLatPlanes<Real, DJG_OT>; break;
             }
-            if (tled_) nq = (TledLayout<0>::count + 3) / 4;
-            const size_t bytes = size_t(ncomb) * 6 * nq * sizeof(float4);
+            if (tled_) nq = kTledPlanes<Real>;
+            const size_t bytes = size_t(ncomb) * 6 * nq * sizeof(Plane);
             if (bytes > (size_t(16) << 20)) return;  // an irregular box: too many classes
             lcls_.alloc(cls.size() * sizeof(int32_t));
             CK(cudaMemcpy(lcls_.p, cls.data(), lcls_.bytes, cudaMemcpyHostToDevice));
-            ld_.alloc(len.size() * sizeof(float));
+            ld_.alloc(len.size() * sizeof(Real));
             CK(cudaMemcpy(ld_.p, len.data(), ld_.bytes, cudaMemcpyHostToDevice));
             DevBuf drep, bad;
             drep.alloc(rep.size() * sizeof(int32_t));
@@ -775,16 +775,16 @@ public:
             bad.alloc(sizeof(unsigned long long));
             CK(cudaMemset(bad.p, 0, bad.bytes));
             BoxArgs b = box_;
-            b.lat = lat_.as<float4>();
+            b.lat = lat_.p;
             b.lcls = lcls_.as<int32_t>();
-            b.ld = ld_.as<float>();
+            b.ld = ld_.p;
             b.lncx = ncl[0];
             b.lncy = ncl[1];
             b.lncz = ncl[2];
             const unsigned tb = unsigned((ncomb * 6 + 127) / 128), vb = unsigned(sms_ * 8);
             auto run = [&](auto table, auto verify) {
-                table<<<tb, 128>>>(ea_, b, drep.as<int32_t>(), lat_.as<float4>());
-                verify<<<vb, 256>>>(ea_, b, lat_.as<float4>(), bad.as<unsigned long long>());
+                table<<<tb, 128>>>(ea_, b, drep.as<int32_t>(), lat_.as<Plane>());
+                verify<<<vb, 256>>>(ea_, b, lat_.as<Plane>(), bad.as<unsigned long long>());
             };
             if (tled_) {
                 // TLED: the records exist already (B0 / V0 planes): copy a

@@ -75,6 +75,12 @@ struct RT<double> {
     __device__ static inline Plane load_plane(const Plane* p) { return __ldcs(p); }
 };
 
+// Component k of a record plane; bit-for-bit equality (+0 and -0 distinct).
+__device__ __forceinline__ float plane_at(const float4& v, int k) { return k == 0 ? v.x : k == 1 ? v.y : k == 2 ? v.z : v.w; }
+__device__ __forceinline__ double plane_at(const double2& v, int k) { return k == 0 ? v.x : v.y; }
+__device__ __forceinline__ bool same_bits(float a, float b) { return __float_as_uint(a) == __float_as_uint(b); }
+__device__ __forceinline__ bool same_bits(double a, double b) { return __double_as_longlong(a) == __double_as_longlong(b); }
+
 // Record layout per (kind, model): offsets in the canonical record (djg.h).
 template <int KIND, int MODEL>
 struct Layout {
@@ -1799,12 +1805,12 @@ struct BoxArgs {
     int lay0, lay1, close;
     // coordinate lattice (k_box_step<..., LAT = true>): record fields 9.. of
     // tet t of a cell with axis classes (cx, cy, cz) are lat[((cz * lncy + cy)
-    // * lncx + cx) * 6 + t] (float4-padded); its J0 is made of the classes'
+    // * lncx + cx) * 6 + t] (plane-padded); its J0 is made of the classes'
     // interval lengths ld[cx], ld[lncx + cy], ld[lncx + lncy + cz]; lcls =
     // the class of every cell index along x, then y, then z
-    const float4* lat;
+    const void* lat;   // RT<Real>::Plane[]
     const int* lcls;
-    const float* ld;
+    const void* ld;    // Real[]
     int lncx, lncy, lncz, _pad;
 };
 
@@ -1848,7 +1854,8 @@ __device__ __forceinline__ unsigned tet_stage_offsets(int t) {
 // corner 0, so row i (node i + 1 at corner cr) is d_j where cr has bit j,
 // else (0 + -x) + x = +0 -- t4_jacobian0's values (k_lattice_verify checks
 // them on every tet).
-__device__ __forceinline__ void lattice_j0(int t, const float (&d)[3], float* c) {
+template <class Real>
+__device__ __forceinline__ void lattice_j0(int t, const Real (&d)[3], Real* c) {
     constexpr int C[6][4] = {{0, 1, 3, 7}, {0, 5, 1, 7}, {0, 3, 2, 7}, {0, 2, 6, 7}, {0, 4, 5, 7}, {0, 6, 4, 7}};
     int cr[3];
     switch (t) {
@@ -1863,7 +1870,7 @@ __device__ __forceinline__ void lattice_j0(int t, const float (&d)[3], float* c)
 #pragma unroll
     for (int i = 0; i < 3; ++i)
 #pragma unroll
-        for (int j = 0; j < 3; ++j) c[3 * i + j] = ((cr[i] >> j) & 1) ? d[j] : 0.0f;
+        for (int j = 0; j < 3; ++j) c[3 * i + j] = ((cr[i] >> j) & 1) ? d[j] : Real(0);
 }
 
 template <class Real, bool LAT = false, bool ROW0 = false>
@@ -1875,22 +1882,22 @@ struct BoxSrc {
     long long e;               // TLED: this tet's element id
     const Node* su;    // stage u (all ring slots)
     const Node* sx;    // stage X (LAT: unused)
-    const float4* lrec;  // LAT: this tet's record fields 9..
-    float d[3];          // LAT: the cell's interval lengths
+    const typename RT<Real>::Plane* lrec;  // LAT: this tet's record (DJ: fields 9..; TLED: all)
+    Real d[3];           // LAT: the cell's interval lengths
     int t;               // LAT: the tet (a compile-time constant once the tet loop is unrolled)
     template <int NREC>
     __device__ __forceinline__ void lattice_record(Real* c) const {
+        constexpr int KP = RT<Real>::kPlane;
         lattice_j0(t, d, c);
 #pragma unroll
-        for (int q = 0; q < (NREC - 9 + 3) / 4; ++q) {
-            const float4 v = __ldg(lrec + q);
-            c[9 + 4 * q] = v.x;
-            if (9 + 4 * q + 1 < NREC) c[9 + 4 * q + 1] = v.y;
-            if (9 + 4 * q + 2 < NREC) c[9 + 4 * q + 2] = v.z;
-            if (9 + 4 * q + 3 < NREC) c[9 + 4 * q + 3] = v.w;
+        for (int q = 0; q < (NREC - 9 + KP - 1) / KP; ++q) {
+            const typename RT<Real>::Plane v = __ldg(lrec + q);
+#pragma unroll
+            for (int k = 0; k < KP; ++k)
+                if (9 + KP * q + k < NREC) c[9 + KP * q + k] = plane_at(v, k);
         }
     }
-    float* rows;       // [footprint cell][t][a][3]
+    Real* rows;        // [footprint cell][t][a][3]
     int h[4];          // stage indices of the tet's nodes
     int row0;          // first row of this tet
     bool count_inv;
@@ -1901,7 +1908,7 @@ struct BoxSrc {
     // the precomputed planes in HBM
     __device__ __forceinline__ typename RT<Real>::Plane plane(int p) const {
         if constexpr (ROW0) {
-            if constexpr (LAT) return __ldg(reinterpret_cast<const typename RT<Real>::Plane*>(lrec) + p);
+            if constexpr (LAT) return __ldg(lrec + p);
             else return RT<Real>::load_plane(ea->c + (long long)p * ea->E + e);
         } else {
             return typename RT<Real>::Plane{};
@@ -1934,9 +1941,9 @@ struct BoxSrc {
 
 // The Kuhn tets of a cell holding corner C, as (tet, local node) in
 // ascending tet order (the inverse of kTetCorner), at compile time.
-template <int C, int NCELL, bool ROW0 = false>
-__device__ __forceinline__ void corner_rows(const float* __restrict__ rows, int ntet, int c, float& fx, float& fy,
-                                            float& fz) {
+template <int C, int NCELL, bool ROW0 = false, class Real>
+__device__ __forceinline__ void corner_rows(const Real* __restrict__ rows, int ntet, int c, Real& fx, Real& fy,
+                                            Real& fz) {
     constexpr int n = (C == 0 || C == 7) ? 6 : 2;
     constexpr int T0[8][6] = {{0, 1, 2, 3, 4, 5}, {0, 1}, {2, 3}, {0, 2}, {4, 5}, {1, 4}, {3, 5}, {0, 1, 2, 3, 4, 5}};
     constexpr int A0[8][6] = {{0, 0, 0, 0, 0, 0}, {1, 2}, {2, 1}, {2, 1}, {1, 2}, {1, 2}, {2, 1}, {3, 3, 3, 3, 3, 3}};
@@ -1948,10 +1955,10 @@ __device__ __forceinline__ void corner_rows(const float* __restrict__ rows, int 
             fy += rows[(3 * a + 1) * ntet + tet];
             fz += rows[(3 * a + 2) * ntet + tet];
         } else if (a == 0) {  // f0 = -(f1 + f2 + f3), element_body's expression (djtled_force.hpp:73-77)
-            const float* k = rows + tet;
-            fx += -1.0f * ((k[0 * ntet] + k[3 * ntet]) + k[6 * ntet]);
-            fy += -1.0f * ((k[1 * ntet] + k[4 * ntet]) + k[7 * ntet]);
-            fz += -1.0f * ((k[2 * ntet] + k[5 * ntet]) + k[8 * ntet]);
+            const Real* k = rows + tet;
+            fx += Real(-1) * ((k[0 * ntet] + k[3 * ntet]) + k[6 * ntet]);
+            fy += Real(-1) * ((k[1 * ntet] + k[4 * ntet]) + k[7 * ntet]);
+            fz += Real(-1) * ((k[2 * ntet] + k[5 * ntet]) + k[8 * ntet]);
         } else {
             fx += rows[(3 * (a - 1) + 0) * ntet + tet];
             fy += rows[(3 * (a - 1) + 1) * ntet + tet];
@@ -1974,22 +1981,32 @@ struct BoxShape {
     template <class Real, bool LAT = false, bool TLED = false>
     static constexpr size_t smem_bytes() {
         return (LAT || TLED ? 1 : 2) * 3 * size_t(kStageNodes) * sizeof(typename RT<Real>::Node) +
-               kRowFloats / 9 * (TLED ? 12 : 9) * sizeof(float);
+               kRowFloats / 9 * (TLED ? 12 : 9) * sizeof(Real);
     }
 };
 
-// Floats of a T4 record in the lattice table (float4-padded per tet).
-template <int MODEL>
-constexpr int kLatQuads = (Layout<0, MODEL>::count - 9 + 3) / 4;
+// Planes of a T4 record in the lattice table (DJ: fields 9..; TLED: B0 / V0).
+template <class Real, int MODEL>
+constexpr int kLatPlanes = (Layout<0, MODEL>::count - 9 + RT<Real>::kPlane - 1) / RT<Real>::kPlane;
+template <class Real>
+constexpr int kTledPlanes = (TledLayout<0>::count + RT<Real>::kPlane - 1) / RT<Real>::kPlane;
 
 __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_addr(dst)), "l"(src) : "memory");
 }
+template <class Node>
+__device__ __forceinline__ void cp_async_node(Node* dst, const Node* src) {
+#pragma unroll
+    for (int k = 0; k < int(sizeof(Node) / 16); ++k)
+        cp_async16(reinterpret_cast<char*>(dst) + 16 * k, reinterpret_cast<const char*>(src) + 16 * k);
+}
+#ifndef DJG_BOX_MINB64
+#define DJG_BOX_MINB64 1  // f64: 156 KB of shared memory per block
+#endif
 
 template <class Real, int MODEL, int BX, int BY, bool LAT, bool TLED = false>
-__global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_box_step(const ElemArgs<Real> A, const NodeArgs<Real> NA,
-                                                          const BoxArgs B) {
-    static_assert(sizeof(Real) == 4, "the fused box step keeps float rows");
+__global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, sizeof(Real) == 4 ? DJG_BOX_MINB : DJG_BOX_MINB64)
+    k_box_step(const ElemArgs<Real> A, const NodeArgs<Real> NA, const BoxArgs B) {
     using T = RT<Real>;
     using Node = typename T::Node;
     using BS = BoxShape<BX, BY>;
@@ -1998,8 +2015,11 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
     Node* su = reinterpret_cast<Node*>(smem);
     Node* sx = su + 3 * BS::kStageNodes;
     constexpr bool kXRing = !LAT && !TLED;  // coordinates staged (per-tet DJ record rebuild)
-    float* rows = reinterpret_cast<float*>(su + (kXRing ? 2 : 1) * 3 * BS::kStageNodes);
-    constexpr int NQ = TLED ? (TledLayout<0>::count + 3) / 4 : kLatQuads<MODEL>;
+    Real* rows = reinterpret_cast<Real*>(su + (kXRing ? 2 : 1) * 3 * BS::kStageNodes);
+    constexpr int NQ = TLED ? kTledPlanes<Real> : kLatPlanes<Real, MODEL>;
+    using Plane = typename T::Plane;
+    const Plane* lat = static_cast<const Plane*>(B.lat);
+    const Real* ld = static_cast<const Real*>(B.ld);
     __shared__ int s_nonfinite;
     Ctrl* ctrl = A.ctrl;
     if (*(volatile const int*)&ctrl->halted) return;
@@ -2021,8 +2041,8 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
             const int gi = i0 - 1 + q % BS::SX, gj = j0 - 1 + q / BS::SX;
             if (gi < 0 || gi > nx || gj < 0 || gj > ny) continue;
             const long long n = gid(gi, gj, k);
-            cp_async16(su + slot * BS::kStageNodes + q, ucur + n);
-            if constexpr (kXRing) cp_async16(sx + slot * BS::kStageNodes + q, A.X + n);
+            cp_async_node(su + slot * BS::kStageNodes + q, ucur + n);
+            if constexpr (kXRing) cp_async_node(sx + slot * BS::kStageNodes + q, A.X + n);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
@@ -2108,13 +2128,13 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
         mcj = j0 - 1 + mcy;
         my_cell = tid < NCELL && mci >= 0 && mci < nx && mcj >= 0 && mcj < ny;
         int lxy = 0;  // LAT: the cell's (cy * lncx + cx) and x / y interval lengths
-        float ldx = 0.0f, ldy = 0.0f;
+        Real ldx = Real(0), ldy = Real(0);
         if constexpr (LAT) {
             if (my_cell) {
                 const int cx = __ldg(B.lcls + mci), cy = __ldg(B.lcls + nx + mcj);
                 lxy = cy * B.lncx + cx;
-                ldx = __ldg(B.ld + cx);
-                ldy = __ldg(B.ld + B.lncx + cy);
+                ldx = __ldg(ld + cx);
+                ldy = __ldg(ld + B.lncx + cy);
             }
         }
         px = Real(0); py = Real(0); pz = Real(0);
@@ -2134,12 +2154,12 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, DJG_BOX_MINB) k_bo
                 const int hb0 = (kc % 3) * BS::kStageNodes + mbase, hb1 = ((kc + 1) % 3) * BS::kStageNodes + mbase;
                 const bool count = my_count && kc >= k0;
                 const long long ebase = ((long long)mci + (long long)nx * (mcj + (long long)ny * kc)) * 6;
-                const float4* lcell = nullptr;
-                float ldz = 0.0f;
+                const Plane* lcell = nullptr;
+                Real ldz = Real(0);
                 if constexpr (LAT) {
                     const int cz = __ldg(B.lcls + nx + ny + kc);
-                    lcell = B.lat + size_t(cz * B.lncy * B.lncx + lxy) * 6 * NQ;
-                    ldz = __ldg(B.ld + B.lncx + B.lncy + cz);
+                    lcell = lat + size_t(cz * B.lncy * B.lncx + lxy) * 6 * NQ;
+                    ldz = __ldg(ld + B.lncx + B.lncy + cz);
                 }
     #pragma unroll kBoxUnrollT
                 for (int t = 0; t < 6; ++t) {
@@ -2213,8 +2233,8 @@ __device__ __forceinline__ void box_tet_coords(const Node* __restrict__ X, const
 
 template <class Real, int MODEL>
 __global__ void k_lattice_table(const ElemArgs<Real> A, const BoxArgs B, const int* __restrict__ rep,
-                                float4* __restrict__ lat) {
-    constexpr int NQ = kLatQuads<MODEL>;
+                                typename RT<Real>::Plane* __restrict__ lat) {
+    constexpr int NQ = kLatPlanes<Real, MODEL>, KP = RT<Real>::kPlane;
     const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (q >= (long long)B.lncx * B.lncy * B.lncz * 6) return;
     const int t = int(q % 6);
@@ -2222,14 +2242,14 @@ __global__ void k_lattice_table(const ElemArgs<Real> A, const BoxArgs B, const i
     const int cx = int(comb % B.lncx), cy = int(comb / B.lncx % B.lncy), cz = int(comb / B.lncx / B.lncy);
     typename RT<Real>::Node x[4];
     box_tet_coords(A.X, B, rep[cx], rep[B.lncx + cy], rep[B.lncx + B.lncy + cz], t, x);
-    Real c[9 + NQ * 4];
+    Real c[9 + NQ * KP];
 #pragma unroll
-    for (int k = 0; k < 9 + NQ * 4; ++k) c[k] = Real(0);
+    for (int k = 0; k < 9 + NQ * KP; ++k) c[k] = Real(0);
     t4_jacobian0(0, x, c);
     compact_record_tail<Real, 0, MODEL>(A, c);
-    const Real* f = c + 9;
+    Real* f = reinterpret_cast<Real*>(lat + q * NQ);
 #pragma unroll
-    for (int k = 0; k < NQ; ++k) lat[q * NQ + k] = make_float4(f[4 * k], f[4 * k + 1], f[4 * k + 2], f[4 * k + 3]);
+    for (int k = 0; k < NQ * KP; ++k) f[k] = c[9 + k];
 }
 
 // Every tet of the box against its class's table record, bit for bit (+0
@@ -2237,9 +2257,10 @@ __global__ void k_lattice_table(const ElemArgs<Real> A, const BoxArgs B, const i
 // table only when there are none: the table is exact by check, not by an
 // argument about the coordinates.
 template <class Real, int MODEL>
-__global__ void k_lattice_verify(const ElemArgs<Real> A, const BoxArgs B, const float4* __restrict__ lat,
+__global__ void k_lattice_verify(const ElemArgs<Real> A, const BoxArgs B, const typename RT<Real>::Plane* __restrict__ lat,
                                  unsigned long long* bad) {
-    constexpr int NQ = kLatQuads<MODEL>, NREC = Layout<0, MODEL>::count;
+    constexpr int NQ = kLatPlanes<Real, MODEL>, KP = RT<Real>::kPlane, NREC = Layout<0, MODEL>::count;
+    const Real* ld = static_cast<const Real*>(B.ld);
     const long long ncell = (long long)B.nx * B.ny * B.nz;
     unsigned long long mism = 0;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < ncell * 6;
@@ -2249,22 +2270,22 @@ __global__ void k_lattice_verify(const ElemArgs<Real> A, const BoxArgs B, const 
         const int ci = int(cell % B.nx), cj = int(cell / B.nx % B.ny), ck = int(cell / B.nx / B.ny);
         typename RT<Real>::Node x[4];
         box_tet_coords(A.X, B, ci, cj, ck, t, x);
-        Real c[9 + NQ * 4];
+        Real c[9 + NQ * KP];
 #pragma unroll
-        for (int k = 0; k < 9 + NQ * 4; ++k) c[k] = Real(0);
+        for (int k = 0; k < 9 + NQ * KP; ++k) c[k] = Real(0);
         t4_jacobian0(0, x, c);
         compact_record_tail<Real, 0, MODEL>(A, c);
         const int cx = B.lcls[ci], cy = B.lcls[B.nx + cj], cz = B.lcls[B.nx + B.ny + ck];
         const long long comb = ((long long)cz * B.lncy + cy) * B.lncx + cx;
-        const float* want = reinterpret_cast<const float*>(lat + (comb * 6 + t) * NQ);
-        float j0[9];
-        const float d[3] = {B.ld[cx], B.ld[B.lncx + cy], B.ld[B.lncx + B.lncy + cz]};
+        const Real* want = reinterpret_cast<const Real*>(lat + (comb * 6 + t) * NQ);
+        Real j0[9];
+        const Real d[3] = {ld[cx], ld[B.lncx + cy], ld[B.lncx + B.lncy + cz]};
         lattice_j0(t, d, j0);
         bool same = true;
 #pragma unroll
-        for (int k = 0; k < 9; ++k) same = same && __float_as_uint(c[k]) == __float_as_uint(j0[k]);
+        for (int k = 0; k < 9; ++k) same = same && same_bits(c[k], j0[k]);
 #pragma unroll
-        for (int k = 9; k < NREC; ++k) same = same && __float_as_uint(c[k]) == __float_as_uint(want[k - 9]);
+        for (int k = 9; k < NREC; ++k) same = same && same_bits(c[k], want[k - 9]);
         mism += same ? 0 : 1;
     }
     if (mism) atomicAdd(bad, mism);
@@ -2275,8 +2296,8 @@ __global__ void k_lattice_verify(const ElemArgs<Real> A, const BoxArgs B, const 
 // tet's planes against its class's entry, bit for bit.
 template <class Real>
 __global__ void k_lattice_table_rec(const ElemArgs<Real> A, const BoxArgs B, const int* __restrict__ rep,
-                                    float4* __restrict__ lat) {
-    constexpr int NQ = (TledLayout<0>::count + 3) / 4;
+                                    typename RT<Real>::Plane* __restrict__ lat) {
+    constexpr int NQ = kTledPlanes<Real>;
     const long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (q >= (long long)B.lncx * B.lncy * B.lncz * 6) return;
     const int t = int(q % 6);
@@ -2289,9 +2310,9 @@ __global__ void k_lattice_table_rec(const ElemArgs<Real> A, const BoxArgs B, con
 }
 
 template <class Real>
-__global__ void k_lattice_verify_rec(const ElemArgs<Real> A, const BoxArgs B, const float4* __restrict__ lat,
-                                     unsigned long long* bad) {
-    constexpr int NQ = (TledLayout<0>::count + 3) / 4, NREC = TledLayout<0>::count;
+__global__ void k_lattice_verify_rec(const ElemArgs<Real> A, const BoxArgs B,
+                                     const typename RT<Real>::Plane* __restrict__ lat, unsigned long long* bad) {
+    constexpr int NQ = kTledPlanes<Real>, KP = RT<Real>::kPlane, NREC = TledLayout<0>::count;
     const long long ncell = (long long)B.nx * B.ny * B.nz;
     unsigned long long mism = 0;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < ncell * 6;
@@ -2304,11 +2325,10 @@ __global__ void k_lattice_verify_rec(const ElemArgs<Real> A, const BoxArgs B, co
         bool same = true;
 #pragma unroll
         for (int p = 0; p < NQ; ++p) {
-            const float4 g = A.c[(long long)p * A.E + e], w = lat[(comb * 6 + t) * NQ + p];
-            const float gv[4] = {g.x, g.y, g.z, g.w}, wv[4] = {w.x, w.y, w.z, w.w};
+            const typename RT<Real>::Plane g = A.c[(long long)p * A.E + e], w = lat[(comb * 6 + t) * NQ + p];
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
-                if (4 * p + k < NREC) same = same && __float_as_uint(gv[k]) == __float_as_uint(wv[k]);
+            for (int k = 0; k < KP; ++k)
+                if (KP * p + k < NREC) same = same && same_bits(plane_at(g, k), plane_at(w, k));
         }
         mism += same ? 0 : 1;
     }

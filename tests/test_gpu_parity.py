@@ -168,6 +168,28 @@ def test_fused_box_step_bitwise(divisions, model, kind):
     check_run(spec, 200, flags=A.DJG_FLAG_FUSED)
 
 
+@pytest.mark.parametrize("model", ["NH", "TI", "OT"])
+@pytest.mark.parametrize("divisions", [(5, 4, 6), (17, 9, 33), (1, 1, 1)])
+def test_fused_box_step_f64(divisions, model):
+    """The fused T4 step in double precision (f64 rows and records, one
+    block per SM): bit-identical to the oracle, with and without the lattice
+    table."""
+    spec = box_spec(kind="T4", model=model, divisions=divisions, precision=8, ramp_steps=200)
+    with GpuDjEngine(Scenario(spec), flags=A.DJG_FLAG_FUSED) as eng:
+        info = eng.info()
+        assert info["fused"] == 1 and info["lattice"] == 1
+    check_run(spec, 200, flags=A.DJG_FLAG_FUSED)
+
+
+def test_fused_box_step_f64_off_lattice(monkeypatch):
+    monkeypatch.setenv("DJG_LATTICE", "0")
+    spec = box_spec(kind="T4", model="TI", divisions=(9, 8, 7), precision=8, ramp_steps=200)
+    with GpuDjEngine(Scenario(spec), flags=A.DJG_FLAG_FUSED) as eng:
+        info = eng.info()
+        assert info["fused"] == 1 and info["lattice"] == 0
+    check_run(spec, 200, flags=A.DJG_FLAG_FUSED)
+
+
 def _box_with_nodes(divisions, move, **kw):
     """A generated T4 box's connectivity with its node coordinates moved by
     move(x) (fixed bottom face, prescribed top face)."""

@@ -123,3 +123,13 @@ def test_tled_fused_inversion(policy):
         (r2.status, r2.step, r2.first_inverted, r2.inverted_count, r2.inverted_steps), (r1, r2)
     assert r1.inverted_count > 0
     assert np.array_equal(u1, u2) and np.array_equal(up1, up2)
+
+
+@pytest.mark.parametrize("model", ["NH", "TI"])
+def test_tled_fused_box_step_f64(model):
+    spec = box_spec(kind="T4", model=model, divisions=(7, 5, 9), precision=8, ramp_steps=200)
+    u, up, rep, info = run(spec, 200, A.DJG_FLAG_TLED | A.DJG_FLAG_FUSED)
+    assert info["fused"] == 1 and info["lattice"] == 1
+    u2, up2, rep2, _ = run(spec, 200, A.DJG_FLAG_TLED | A.DJG_FLAG_NO_FUSED)
+    assert rep.status == rep2.status == 0
+    assert np.array_equal(u, u2) and np.array_equal(up, up2) and np.abs(u).max() > 0

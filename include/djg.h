@@ -102,7 +102,7 @@ typedef struct djg_desc {
 #define DJG_FLAG_NO_FUSED 512u  /* keep the two-kernel step (element kernel + gather/update)
                                     on a generated box, where the default is one fused
                                     kernel per step (k_box_step, no force slots in HBM)
-                                    once the box fills the GPU */
+                                    once the box gives every block enough column layers */
 #define DJG_FLAG_FUSED 1024u     /* the fused box step on any generated T4 box it supports,
                                     however small (bit-identical either way) */
 #define DJG_FLAG_WINDOW 256u     /* pipelined element kernel with node windows: each

@@ -1695,7 +1695,9 @@ public:
     int advance_host_box(const void* u, const void* up, int64_t step, void* u_next, djg_report* rep) {
         const int64_t plane = int64_t(box_.nx + 1) * (box_.ny + 1), L = box_.nz + 1;
         const bool chunked = L >= 4 * kBoxRegions && N_ >= (int64_t(1) << 16);
-        const int R = chunked ? kBoxRegions : 1;
+        int R = chunked ? kBoxRegions : 1;
+        if (const char* v = std::getenv("DJG_HOST_REGIONS"); v && *v && chunked)  // developer A/B: equal regions
+            R = std::max(1, std::min(kBoxRegions, std::atoi(v)));
         if (!side_) CK(cudaStreamCreateWithFlags(&side_, cudaStreamNonBlocking));
         if (!side2_) CK(cudaStreamCreateWithFlags(&side2_, cudaStreamNonBlocking));
         if (!down_) CK(cudaStreamCreateWithFlags(&down_, cudaStreamNonBlocking));
@@ -1741,7 +1743,7 @@ public:
         const Node* unew = u_[(ph + 1) % 3].as<Node>();
         // region boundaries in node layers (percent of the layers, tapered)
         static const int w8[kBoxRegions + 1] = {0, 15, 30, 45, 60, 73, 84, 93, 100};
-        auto lay = [&](int r) -> int64_t { return R == 1 ? (r ? L : 0) : L * w8[r] / 100; };
+        auto lay = [&](int r) -> int64_t { return R == kBoxRegions ? L * w8[r] / 100 : L * r / R; };
         // u_curr and u_prev go up on two streams (a copy stream alone moved
         // ~40 GB/s in tools/pcie_probe.py, two at once ~55 GB/s; in the step
         // they reach ~48 GB/s together: cfg5 4.78 -> 4.51 ms per host-state

@@ -1878,8 +1878,8 @@ struct BoxSrc {
     using Node = typename RT<Real>::Node;
     static constexpr bool kRowSink = true;
     static constexpr bool kLattice = LAT;
-    const ElemArgs<Real>* ea;  // TLED: the record planes (A.c) when not on the lattice
-    long long e;               // TLED: this tet's element id
+    const typename RT<Real>::Plane* rc;  // TLED: the record planes (A.c) when not on the lattice
+    long long E, e;                      // TLED: plane stride, this tet's element id
     const Node* su;    // stage u (all ring slots)
     const Node* sx;    // stage X (LAT: unused)
     const typename RT<Real>::Plane* lrec;  // LAT: this tet's record (DJ: fields 9..; TLED: all)
@@ -1909,7 +1909,7 @@ struct BoxSrc {
     __device__ __forceinline__ typename RT<Real>::Plane plane(int p) const {
         if constexpr (ROW0) {
             if constexpr (LAT) return __ldg(lrec + p);
-            else return RT<Real>::load_plane(ea->c + (long long)p * ea->E + e);
+            else return RT<Real>::load_plane(rc + (long long)p * E + e);
         } else {
             return typename RT<Real>::Plane{};
         }
@@ -2164,7 +2164,8 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, sizeof(Real) == 4 
     #pragma unroll kBoxUnrollT
                 for (int t = 0; t < 6; ++t) {
                     BoxSrc<Real, LAT, TLED> src;
-                    src.ea = &A;
+                    src.rc = A.c;
+                    src.E = A.E;
                     src.e = ebase + t;
                     src.su = su;
                     src.sx = sx;

@@ -793,10 +793,11 @@ def test_advance_host_chunked_readback():
     assert np.array_equal(u, u_ref) and np.array_equal(up, up_ref) and np.abs(u).max() > 0
 
 
-@pytest.mark.parametrize("kind,model,d", [("T4", "NH", (40, 41, 45)), ("T4", "TI", (12, 9, 33)), ("H8", "TI", (41, 40, 40)),
-                                           ("T4", "NH", (5, 4, 6))])
+@pytest.mark.parametrize("kind,model,d,prec", [("T4", "NH", (40, 41, 45), 4), ("T4", "TI", (12, 9, 33), 4),
+                                                ("H8", "TI", (41, 40, 40), 4), ("T4", "NH", (5, 4, 6), 4),
+                                                ("T4", "OT", (10, 11, 36), 8)])
 @pytest.mark.parametrize("tled", [False, True])
-def test_advance_host_fused_regions(kind, model, d, tled):
+def test_advance_host_fused_regions(kind, model, d, prec, tled):
     """The host-state step on the fused box step (advance_host_box): region
     by region (8 tapered runs of node layers when the box has >= 32 layers,
     else one launch) -- uploads, partial k_box_step launches, read-back --
@@ -805,7 +806,7 @@ def test_advance_host_fused_regions(kind, model, d, tled):
     if tled and kind == "H8":
         pytest.skip("TLED fused step: T4 only")
     flags = A.DJG_FLAG_FUSED | (A.DJG_FLAG_TLED if tled else 0)
-    spec = box_spec(kind=kind, model=model, divisions=d, precision=4, target=0.01, ramp_steps=25)
+    spec = box_spec(kind=kind, model=model, divisions=d, precision=prec, target=0.01, ramp_steps=25)
     sc = Scenario(spec)
     with GpuDjEngine(sc, flags=(A.DJG_FLAG_TLED if tled else 0) | A.DJG_FLAG_NO_FUSED) as ref:
         ref.step(25)
@@ -813,7 +814,7 @@ def test_advance_host_fused_regions(kind, model, d, tled):
     with GpuDjEngine(sc, flags=flags) as eng:
         assert eng.info()["fused"] == 1
         n3 = 3 * sc.num_nodes
-        u, up = np.zeros(n3, np.float32), np.zeros(n3, np.float32)
+        u, up = np.zeros(n3, spec.dtype), np.zeros(n3, spec.dtype)
         for st in range(25):
             un, rep = eng.advance_host(u, up, st)
             assert rep.status == 0 and rep.step == st + 1

@@ -468,6 +468,13 @@ struct SrcLattice : std::false_type {};
 template <class S>
 struct SrcLattice<S, std::void_t<decltype(S::kLattice)>> : std::bool_constant<S::kLattice> {};
 
+// A row source that supplies a T4 tet's kinematics (Jt, g, det and the
+// adjugate) from per-cell edge terms (the fused box step on a lattice).
+template <class S, class = void>
+struct SrcCellKin : std::false_type {};
+template <class S>
+struct SrcCellKin<S, std::void_t<decltype(S::kCellKin)>> : std::bool_constant<S::kCellKin> {};
+
 // Compact T4 record, part 1 -- jacobian0 (element.hpp:59-77):
 // J0[i][j] = sum_a D[i][a] x_a[j] with D[i] = (-1, e_i), summed from +0 in
 // node order; the 0 * x terms cannot change a sum that is never -0, so
@@ -572,7 +579,13 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
     }
     // update_jacobian (kinematics.hpp:31-45): Jt = J0 + D U.
     Real Jt[3][3];
-    if constexpr (KIND == 0) {
+    Real g[6];         // g_vector (the cell path has it here; else below)
+    Real cof[3][3];    // adjugate entries (cell path)
+    Real det;
+    constexpr bool kCell = KIND == 0 && SrcCellKin<Src>::value;
+    if constexpr (kCell) {
+        src.cell_kinematics(Jt, g, cof, det);
+    } else if constexpr (KIND == 0) {
         // T4: D[i] = (-1, e_i): du = u_{i+1} - u_0 (the reference's sum
         // 0 - u0 + u_{i+1} + 0 + 0 rounds identically).
 #pragma unroll
@@ -603,9 +616,10 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
     }
 
     // det / inversion test / adjugate inverse (core.hpp:187-212).
-    const Real det = Jt[0][0] * (Jt[1][1] * Jt[2][2] - Jt[1][2] * Jt[2][1]) -
-                     Jt[0][1] * (Jt[1][0] * Jt[2][2] - Jt[1][2] * Jt[2][0]) +
-                     Jt[0][2] * (Jt[1][0] * Jt[2][1] - Jt[1][1] * Jt[2][0]);
+    if constexpr (!kCell)
+        det = Jt[0][0] * (Jt[1][1] * Jt[2][2] - Jt[1][2] * Jt[2][1]) -
+              Jt[0][1] * (Jt[1][0] * Jt[2][2] - Jt[1][2] * Jt[2][0]) +
+              Jt[0][2] * (Jt[1][0] * Jt[2][1] - Jt[1][1] * Jt[2][0]);
 
     int sl[NPE];  // slot positions fit in 32 bits (checked at engine creation)
     {
@@ -625,25 +639,33 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
     }
     const Real s_inv = Real(1) / det;
     Real Ji[3][3];
-    Ji[0][0] = (Jt[1][1] * Jt[2][2] - Jt[1][2] * Jt[2][1]) * s_inv;
-    Ji[0][1] = (Jt[0][2] * Jt[2][1] - Jt[0][1] * Jt[2][2]) * s_inv;
-    Ji[0][2] = (Jt[0][1] * Jt[1][2] - Jt[0][2] * Jt[1][1]) * s_inv;
-    Ji[1][0] = (Jt[1][2] * Jt[2][0] - Jt[1][0] * Jt[2][2]) * s_inv;
-    Ji[1][1] = (Jt[0][0] * Jt[2][2] - Jt[0][2] * Jt[2][0]) * s_inv;
-    Ji[1][2] = (Jt[0][2] * Jt[1][0] - Jt[0][0] * Jt[1][2]) * s_inv;
-    Ji[2][0] = (Jt[1][0] * Jt[2][1] - Jt[1][1] * Jt[2][0]) * s_inv;
-    Ji[2][1] = (Jt[0][1] * Jt[2][0] - Jt[0][0] * Jt[2][1]) * s_inv;
-    Ji[2][2] = (Jt[0][0] * Jt[1][1] - Jt[0][1] * Jt[1][0]) * s_inv;
+    if constexpr (kCell) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+#pragma unroll
+            for (int j = 0; j < 3; ++j) Ji[i][j] = cof[i][j] * s_inv;
+    } else {
+        Ji[0][0] = (Jt[1][1] * Jt[2][2] - Jt[1][2] * Jt[2][1]) * s_inv;
+        Ji[0][1] = (Jt[0][2] * Jt[2][1] - Jt[0][1] * Jt[2][2]) * s_inv;
+        Ji[0][2] = (Jt[0][1] * Jt[1][2] - Jt[0][2] * Jt[1][1]) * s_inv;
+        Ji[1][0] = (Jt[1][2] * Jt[2][0] - Jt[1][0] * Jt[2][2]) * s_inv;
+        Ji[1][1] = (Jt[0][0] * Jt[2][2] - Jt[0][2] * Jt[2][0]) * s_inv;
+        Ji[1][2] = (Jt[0][2] * Jt[1][0] - Jt[0][0] * Jt[1][2]) * s_inv;
+        Ji[2][0] = (Jt[1][0] * Jt[2][1] - Jt[1][1] * Jt[2][0]) * s_inv;
+        Ji[2][1] = (Jt[0][1] * Jt[2][0] - Jt[0][0] * Jt[2][1]) * s_inv;
+        Ji[2][2] = (Jt[0][0] * Jt[1][1] - Jt[0][1] * Jt[1][0]) * s_inv;
+    }
 
     // volume_ratio, g_vector, invariants (kinematics.hpp:47-103).
     const Real J = det / c[9];
-    Real g[6];
-    g[0] = Jt[0][0] * Jt[0][0] + Jt[0][1] * Jt[0][1] + Jt[0][2] * Jt[0][2];
-    g[1] = Jt[1][0] * Jt[1][0] + Jt[1][1] * Jt[1][1] + Jt[1][2] * Jt[1][2];
-    g[2] = Jt[2][0] * Jt[2][0] + Jt[2][1] * Jt[2][1] + Jt[2][2] * Jt[2][2];
-    g[3] = Jt[0][0] * Jt[1][0] + Jt[0][1] * Jt[1][1] + Jt[0][2] * Jt[1][2];
-    g[4] = Jt[0][0] * Jt[2][0] + Jt[0][1] * Jt[2][1] + Jt[0][2] * Jt[2][2];
-    g[5] = Jt[1][0] * Jt[2][0] + Jt[1][1] * Jt[2][1] + Jt[1][2] * Jt[2][2];
+    if constexpr (!kCell) {
+        g[0] = Jt[0][0] * Jt[0][0] + Jt[0][1] * Jt[0][1] + Jt[0][2] * Jt[0][2];
+        g[1] = Jt[1][0] * Jt[1][0] + Jt[1][1] * Jt[1][1] + Jt[1][2] * Jt[1][2];
+        g[2] = Jt[2][0] * Jt[2][0] + Jt[2][1] * Jt[2][1] + Jt[2][2] * Jt[2][2];
+        g[3] = Jt[0][0] * Jt[1][0] + Jt[0][1] * Jt[1][1] + Jt[0][2] * Jt[1][2];
+        g[4] = Jt[0][0] * Jt[2][0] + Jt[0][1] * Jt[2][1] + Jt[0][2] * Jt[2][2];
+        g[5] = Jt[1][0] * Jt[2][0] + Jt[1][1] * Jt[2][1] + Jt[1][2] * Jt[2][2];
+    }
     const Real cb = ref_cbrt(J);
     const Real j_m23 = Real(1) / (cb * cb);
     const Real I1 = g[0] * c[11] + g[1] * c[12] + g[2] * c[13] + g[3] * c[14] + g[4] * c[15] + g[5] * c[16];
@@ -1873,11 +1895,84 @@ __device__ __forceinline__ void lattice_j0(int t, const Real (&d)[3], Real* c) {
         for (int j = 0; j < 3; ++j) c[3 * i + j] = ((cr[i] >> j) & 1) ? d[j] : Real(0);
 }
 
+#ifndef DJG_BOX_EDGES
+#define DJG_BOX_EDGES 1
+#endif
+
+// Corner code of local node a of Kuhn tet t (a compile-time constant once
+// the tet loop is unrolled).
+__device__ __forceinline__ int box_tet_corner(int t, int a) {
+    constexpr int C[6][4] = {{0, 1, 3, 7}, {0, 5, 1, 7}, {0, 3, 2, 7}, {0, 2, 6, 7}, {0, 4, 5, 7}, {0, 6, 4, 7}};
+    switch (t) {
+        case 0: return C[0][a];
+        case 1: return C[1][a];
+        case 2: return C[2][a];
+        case 3: return C[3][a];
+        case 4: return C[4][a];
+        default: return C[5][a];
+    }
+}
+
+// The terms of one Jt row that the tets of a lattice cell share: the row E
+// of the edge from corner 0 to corner c (J0's d-masked row + u_c - u_0,
+// update_jacobian's sums), its g-vector norm, its dot product with the
+// diagonal row D (corner 7), and its products with D as the det minors /
+// adjugate entries take them (each in element_body's operand order, so
+// every value is the one the tet would compute itself).
+template <class Real>
+struct EdgeKin {
+    Real E[3], N, P, m0, m1, m2, n0, n1, n2;
+};
+template <class Real>
+__device__ __forceinline__ EdgeKin<Real> edge_kin(int c, const Real (&d)[3], const typename RT<Real>::Node& uc,
+                                                  const typename RT<Real>::Node& u0, const Real (&D)[3]) {
+    EdgeKin<Real> k;
+    k.E[0] = ((c & 1) ? d[0] : Real(0)) + (uc.x - u0.x);
+    k.E[1] = ((c & 2) ? d[1] : Real(0)) + (uc.y - u0.y);
+    k.E[2] = ((c & 4) ? d[2] : Real(0)) + (uc.z - u0.z);
+    k.N = k.E[0] * k.E[0] + k.E[1] * k.E[1] + k.E[2] * k.E[2];
+    k.P = k.E[0] * D[0] + k.E[1] * D[1] + k.E[2] * D[2];
+    k.m0 = k.E[1] * D[2] - k.E[2] * D[1];  // as row 1: J11 J22 - J12 J21
+    k.m1 = k.E[0] * D[2] - k.E[2] * D[0];  //           J10 J22 - J12 J20 (as row 0: J00 J22 - J02 J20)
+    k.m2 = k.E[0] * D[1] - k.E[1] * D[0];  //           J10 J21 - J11 J20
+    k.n0 = k.E[2] * D[1] - k.E[1] * D[2];  // as row 0: J02 J21 - J01 J22
+    k.n1 = k.E[2] * D[0] - k.E[0] * D[2];  // as row 1: J12 J20 - J10 J22
+    k.n2 = k.E[1] * D[0] - k.E[0] * D[1];  // as row 0: J01 J20 - J00 J21
+    return k;
+}
+
 template <class Real, bool LAT = false, bool ROW0 = false>
 struct BoxSrc {
     using Node = typename RT<Real>::Node;
     static constexpr bool kRowSink = true;
     static constexpr bool kLattice = LAT;
+    static constexpr bool kCellKin = LAT && !ROW0 && DJG_BOX_EDGES;
+    EdgeKin<Real> e0, e1;  // kCellKin: the tet's rows 0 and 1
+    Real D[3], ND;         // kCellKin: row 2 (the diagonal) and its norm
+    __device__ __forceinline__ void cell_kinematics(Real (&Jt)[3][3], Real (&g)[6], Real (&cof)[3][3], Real& det) const {
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            Jt[0][j] = e0.E[j];
+            Jt[1][j] = e1.E[j];
+            Jt[2][j] = D[j];
+        }
+        g[0] = e0.N;
+        g[1] = e1.N;
+        g[2] = ND;
+        g[3] = e0.E[0] * e1.E[0] + e0.E[1] * e1.E[1] + e0.E[2] * e1.E[2];
+        g[4] = e0.P;
+        g[5] = e1.P;
+        det = e0.E[0] * e1.m0 - e0.E[1] * e1.m1 + e0.E[2] * e1.m2;
+        cof[0][0] = e1.m0;
+        cof[0][1] = e0.n0;
+        cof[0][2] = e0.E[1] * e1.E[2] - e0.E[2] * e1.E[1];
+        cof[1][0] = e1.n1;
+        cof[1][1] = e0.m1;
+        cof[1][2] = e0.E[2] * e1.E[0] - e0.E[0] * e1.E[2];
+        cof[2][0] = e1.m2;
+        cof[2][1] = e0.n2;
+        cof[2][2] = e0.E[0] * e1.E[1] - e0.E[1] * e1.E[0];
+    }
     const typename RT<Real>::Plane* rc;  // TLED: the record planes (A.c) when not on the lattice
     long long E, e;                      // TLED: plane stride, this tet's element id
     const Node* su;    // stage u (all ring slots)
@@ -2161,9 +2256,40 @@ __global__ void __launch_bounds__(BoxShape<BX, BY>::kThreads, sizeof(Real) == 4 
                     lcell = lat + size_t(cz * B.lncy * B.lncx + lxy) * 6 * NQ;
                     ldz = __ldg(ld + B.lncx + B.lncy + cz);
                 }
+                // the cell path (kCellKin): tets in the order 0, 1, 4, 5, 3, 2, so
+                // that each tet's row 1 is the previous tet's row 0 (the edges
+                // to corners 3, 1, 5, 4, 6, 2) and its terms carry over; the
+                // diagonal's (corner 7) serve all six
+                constexpr bool kCell = BoxSrc<Real, LAT, TLED>::kCellKin;
+                static_assert(!kCell || kBoxUnrollT == 6, "the cell path needs the tet loop unrolled");
+                constexpr int kOrder[6] = {0, 1, 4, 5, 3, 2};
+                typename T::Node cu0{}, cu7{};
+                Real Dg[3] = {Real(0), Real(0), Real(0)}, NDg = Real(0);
+                EdgeKin<Real> prev{};
+                const Real dcell[3] = {ldx, ldy, ldz};
+                if constexpr (kCell) {
+                    cu0 = su[hb0];
+                    cu7 = su[hb1 + BS::SX + 1];
+                    Dg[0] = dcell[0] + (cu7.x - cu0.x);
+                    Dg[1] = dcell[1] + (cu7.y - cu0.y);
+                    Dg[2] = dcell[2] + (cu7.z - cu0.z);
+                    NDg = Dg[0] * Dg[0] + Dg[1] * Dg[1] + Dg[2] * Dg[2];
+                }
+                auto corner_u = [&](int cr) {
+                    return su[((cr >> 2) ? hb1 : hb0) + ((cr >> 1) & 1) * BS::SX + (cr & 1)];
+                };
     #pragma unroll kBoxUnrollT
-                for (int t = 0; t < 6; ++t) {
+                for (int q = 0; q < 6; ++q) {
+                    const int t = kCell ? kOrder[q] : q;
                     BoxSrc<Real, LAT, TLED> src;
+                    if constexpr (kCell) {
+                        const int c1 = box_tet_corner(t, 1), c2 = box_tet_corner(t, 2);
+                        src.e1 = q == 0 ? edge_kin<Real>(c2, dcell, corner_u(c2), cu0, Dg) : prev;
+                        src.e0 = edge_kin<Real>(c1, dcell, corner_u(c1), cu0, Dg);
+                        src.D[0] = Dg[0]; src.D[1] = Dg[1]; src.D[2] = Dg[2];
+                        src.ND = NDg;
+                        prev = src.e0;
+                    }
                     src.rc = A.c;
                     src.E = A.E;
                     src.e = ebase + t;

@@ -675,7 +675,11 @@ __device__ __forceinline__ void element_body(const ElemArgs<Real>& A, const long
     const Real dJ = A.mat.kappa * (J - Real(1));
     Real s[6];
 #pragma unroll
-    for (int k = 0; k < 6; ++k) s[k] = A.mat.dI1 * c[17 + k];
+    for (int k = 0; k < 6; ++k) {
+        // (the lattice table holds dI1 I1m already: the same product, once per class)
+        if constexpr (KIND == 0 && SrcLattice<Src>::value) s[k] = c[17 + k];
+        else s[k] = A.mat.dI1 * c[17 + k];
+    }
     Real dev = A.mat.dI1 * Ib1;
     if constexpr (L::kI4) {
         const Real I4 = g[0] * c[L::m4 + 0] + g[1] * c[L::m4 + 1] + g[2] * c[L::m4 + 2] + g[3] * c[L::m4 + 3] +
@@ -2080,7 +2084,7 @@ struct BoxShape {
     }
 };
 
-// Planes of a T4 record in the lattice table (DJ: fields 9..; TLED: B0 / V0).
+// Planes of a T4 record in the lattice table (DJ: fields 9.., I1m pre-multiplied by dI1; TLED: B0 / V0).
 template <class Real, int MODEL>
 constexpr int kLatPlanes = (Layout<0, MODEL>::count - 9 + RT<Real>::kPlane - 1) / RT<Real>::kPlane;
 template <class Real>
@@ -2374,6 +2378,8 @@ __global__ void k_lattice_table(const ElemArgs<Real> A, const BoxArgs B, const i
     for (int k = 0; k < 9 + NQ * KP; ++k) c[k] = Real(0);
     t4_jacobian0(0, x, c);
     compact_record_tail<Real, 0, MODEL>(A, c);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) c[17 + k] = A.mat.dI1 * c[17 + k];  // element_body's first s term
     Real* f = reinterpret_cast<Real*>(lat + q * NQ);
 #pragma unroll
     for (int k = 0; k < NQ * KP; ++k) f[k] = c[9 + k];
@@ -2402,6 +2408,8 @@ __global__ void k_lattice_verify(const ElemArgs<Real> A, const BoxArgs B, const 
         for (int k = 0; k < 9 + NQ * KP; ++k) c[k] = Real(0);
         t4_jacobian0(0, x, c);
         compact_record_tail<Real, 0, MODEL>(A, c);
+#pragma unroll
+        for (int k = 0; k < 6; ++k) c[17 + k] = A.mat.dI1 * c[17 + k];  // as k_lattice_table
         const int cx = B.lcls[ci], cy = B.lcls[B.nx + cj], cz = B.lcls[B.nx + B.ny + ck];
         const long long comb = ((long long)cz * B.lncy + cy) * B.lncx + cx;
         const Real* want = reinterpret_cast<const Real*>(lat + (comb * 6 + t) * NQ);

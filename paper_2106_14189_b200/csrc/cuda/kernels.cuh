@@ -246,10 +246,20 @@ __device__ __forceinline__ float ref_cbrt(float x) {
     const float u = float(0.492659620528969547 + (0.697570460207922770 - 0.191502161678719066 * double(xm)) *
                                                      double(xm));
     const float t2 = u * u * u;
-    const float ym = float(double(u) * (double(t2) + 2.0 * double(xm)) / (2.0 * double(t2) + double(xm)) *
-                           glibc_cbrt_factor(xe % 3));
+    // x in [0.5, 2) (the volume ratio of any sane step): xe = 0 or 1, so
+    // xe / 3 = 0 and xe % 3 = xe -- the same factor without the division
+    double f;
+    int q;
+    if (__builtin_expect(unsigned(xe) <= 1u, 1)) {
+        f = xe ? 1.2599210498948731648 : 1.0;
+        q = 0;
+    } else {
+        f = glibc_cbrt_factor(xe % 3);
+        q = xe / 3;
+    }
+    const float ym = float(double(u) * (double(t2) + 2.0 * double(xm)) / (2.0 * double(t2) + double(xm)) * f);
     const float sy = x > 0.0f ? ym : -ym;
-    return __uint_as_float(__float_as_uint(sy) + (unsigned(xe / 3) << 23));
+    return __uint_as_float(__float_as_uint(sy) + (unsigned(q) << 23));
 }
 
 __device__ __forceinline__ double ref_cbrt(double x) {

@@ -202,6 +202,26 @@ def _box_with_nodes(divisions, move, **kw):
                      prescribed=[(int(n), 2, -0.04, 1e-3) for n in top], **kw)
 
 
+@pytest.mark.parametrize("axis", [0, 2])
+def test_fused_lattice_one_ulp_off(axis):
+    """One interior node moved by a single float ulp: the per-axis classes
+    (taken along the box's edges) do not see it, the check of every tet's
+    record against its class entry does -- the table is refused (lattice = 0)
+    and the step stays bit-identical to the oracle."""
+    d = (8, 7, 9)
+
+    def nudge(x):
+        x = x.copy()
+        n = 4 + (d[0] + 1) * (3 + (d[1] + 1) * 5)  # node (4, 3, 5)
+        x[n, axis] = float(np.nextafter(np.float32(x[n, axis]), np.float32(2)))
+        return x
+    spec = _box_with_nodes(d, nudge)
+    with GpuDjEngine(Scenario(spec), flags=A.DJG_FLAG_FUSED) as eng:
+        info = eng.info()
+        assert info["fused"] == 1 and info["lattice"] == 0, info
+    check_run(spec, 120, flags=A.DJG_FLAG_FUSED)
+
+
 @pytest.mark.parametrize("model", ["NH", "TI", "OT"])
 def test_fused_lattice_table(model, monkeypatch):
     """The fused T4 step's lattice table (build_lattice): on a graded lattice

@@ -811,7 +811,11 @@ public:
         }
     }
 
-    bool fused_now() const { return fused_ && na_.N == N_ && !peer_ && !comm_ && n_slabs_ == 1; }
+    // (a part of a decomposition -- element ids mapped, inversions counted
+    // per owner, ghost nodes -- keeps the two-kernel step)
+    bool fused_now() const {
+        return fused_ && na_.N == N_ && !peer_ && !comm_ && n_slabs_ == 1 && !ea_.elem_l2g && !ea_.counted;
+    }
 
     // Uniform slices: when every 32-node slice given the widest row's width
     // costs at most 2 % more slots (the cube: 0.9 %), all slices get that

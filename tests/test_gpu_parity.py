@@ -842,6 +842,32 @@ def test_advance_host_fused_regions(kind, model, d, prec, tled):
     assert np.array_equal(u, u_ref) and np.array_equal(up, up_ref) and np.abs(u).max() > 0
 
 
+@pytest.mark.parametrize("kind,prec,tled,off", [("T4", 4, False, 0), ("T4", 4, False, 1), ("T4", 4, True, 0),
+                                                ("H8", 4, False, 0), ("T4", 8, False, 0)])
+def test_advance_host_fused_pinned(kind, prec, tled, off):
+    """The host-state step on page-locked host arrays (the bench's e2e
+    shape), aligned and not: same bits as the device loop."""
+    import torch
+    flags = A.DJG_FLAG_FUSED | (A.DJG_FLAG_TLED if tled else 0)
+    d = (40, 41, 45) if kind == "T4" else (41, 40, 40)
+    spec = box_spec(kind=kind, model="TI", divisions=d, precision=prec, target=0.01, ramp_steps=12)
+    sc = Scenario(spec)
+    with GpuDjEngine(sc, flags=flags) as ref:
+        ref.step(12)
+        u_ref, up_ref, _ = ref.get_state()
+    tdt = torch.float32 if prec == 4 else torch.float64
+    n3 = 3 * sc.num_nodes
+    # off = 1: rows not 16-byte aligned (the kernels' scalar path)
+    bufs = [torch.zeros(n3 + 4, dtype=tdt).pin_memory()[off:n3 + off].numpy() for _ in range(3)]
+    with GpuDjEngine(sc, flags=flags) as eng:
+        u, up, nxt = bufs
+        for st in range(12):
+            _, rep = eng.advance_host(u, up, st, out=nxt)
+            assert rep.status == 0 and rep.step == st + 1
+            u, up, nxt = nxt, u, up
+    assert np.array_equal(u, u_ref) and np.array_equal(up, up_ref) and np.abs(u).max() > 0
+
+
 def test_advance_host_fused_inversion():
     """A crushing ramp through the fused host-state step: the same failing
     step, status and counts as the device loop; the state handed back."""
